@@ -1,0 +1,244 @@
+/*
+ * dl.h -- C ABI of the B200-native decomposed-LLM tensor-parallel library.
+ *
+ * The library computes the hot path of arxiv 2604.17709 ("DeInfer"):
+ * low-rank factorised linear layers W ~= A B (Section 2.1,
+ * Eq. 1; A = U_k sqrt(S_k) in R^{m x k}, B = sqrt(S_k) V_k^T in R^{k x n},
+ * y = A (B x)) inside a decomposed LLaMA-3 transformer block, with the rank
+ * dimension k sharded over tensor-parallel ranks (Section
+ * 2.2.1, Fig. 2(b): "every process holds a small chunk of matrices", partial
+ * results combined by reduce-sum).
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Math convention as in the paper: W in R^{m x n}, y = W x.  Activations
+ *    are token rows, row-major: X[T x n], Y[T x m], so Y = (X B^T) A^T.
+ *  - Matrices are row-major with an explicit leading dimension (elements).
+ *    A is [m x k] (lda >= k), B is [k x n] (ldb >= n): both are K-major,
+ *    i.e. exactly the operand layout the sm_100a tensor cores consume.
+ *  - All tensor arguments are DEVICE pointers owned by the caller, unless
+ *    a parameter says "host".  The library never allocates device memory in
+ *    dl_lowrank_linear / dl_decomposed_block_forward (CUDA-Graph capturable,
+ *    PAPER.md:147-150 Section 2.2.3 "CUDA Graph requires fixed arguments");
+ *    scratch comes from a caller-provided workspace sized by *_workspace().
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy stream).  All
+ *    device work is enqueued asynchronously on it; the call returns before
+ *    the work completes.
+ *  - Alignment: every device pointer 16-byte aligned, every leading
+ *    dimension a multiple of 8 elements (bf16) / 4 elements (fp32): the TMA
+ *    unit requires 16-byte row strides.  Violations -> DL_ERR_ALIGN.
+ *  - Errors: arguments are validated synchronously before any launch; on a
+ *    non-OK status nothing was enqueued and dl_last_error() returns a
+ *    thread-local description.  Launch failures -> DL_ERR_CUDA, NCCL
+ *    failures -> DL_ERR_NCCL.  Non-finite inputs are not checked.
+ *  - Dtypes: DL_BF16 inputs/outputs with fp32 accumulation (tensor cores,
+ *    tcgen05); DL_F32 inputs/outputs use true fp32 FFMA (SIMT path) and are
+ *    limited to T <= 16 tokens per call.
+ *  - There is no CPU fallback: without a usable sm_100 GPU every compute
+ *    entry point returns DL_ERR_CUDA.
+ */
+#ifndef DL_H_
+#define DL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DL_OK = 0,
+  DL_ERR_INVALID_ARG = 1, /* null pointer / bad enum                          */
+  DL_ERR_SHAPE = 2,       /* T < 0, m/n <= 0, ld < row length                 */
+  DL_ERR_RANK = 3,        /* k < 1 or k > min(m, n)          */
+  DL_ERR_PARTITION = 4,   /* k_total < world, strict split with k % world,
+                             heads not divisible by world  */
+  DL_ERR_DTYPE = 5,       /* dtype unsupported on the selected path          */
+  DL_ERR_ALIGN = 6,       /* pointer not 16 B aligned or ld not 16 B multiple */
+  DL_ERR_WORKSPACE = 7,   /* workspace NULL or smaller than *_workspace()     */
+  DL_ERR_CUDA = 8,        /* no sm_100 device / launch or runtime error       */
+  DL_ERR_NCCL = 9,        /* NCCL call failed or NCCL not loadable            */
+  DL_ERR_UNSUPPORTED = 10 /* shape outside this version's kernels             */
+} dl_status;
+
+typedef enum { DL_F32 = 0, DL_BF16 = 1 } dl_dtype;
+
+/* Opaque tensor-parallel communicator: wraps an ncclComm_t created by the
+ * caller (e.g. torch ProcessGroupNCCL._comm_ptr()); does not own it. */
+typedef struct dl_comm_s *dl_comm;
+
+/* Thread-local message for the last non-OK status of this thread. */
+const char *dl_last_error(void);
+/* ABI version (major*100 + minor). */
+int dl_version(void);
+/* 1 if a device with compute capability 10.x is current, else 0. */
+int dl_device_ok(void);
+
+/* ------------------------------------------------------------------------
+ * Communicator.  nccl_comm: an initialised ncclComm_t (host handle) of
+ * `world` ranks in which this process is `rank`.  NCCL symbols are resolved
+ * from the process (the NCCL that owns nccl_comm); DL_ERR_NCCL if absent.
+ * ---------------------------------------------------------------------- */
+dl_status dl_comm_create(void *nccl_comm, int rank, int world, dl_comm *out);
+dl_status dl_comm_destroy(dl_comm comm);
+
+/* ------------------------------------------------------------------------
+ * dl_lowrank_linear -- one decomposed linear layer
+ * (Section 2.1, Eq. 1):  Y[t] (+)= A (B X[t])  for t in [0, T).
+ *
+ *   X [T x n] (ldx), A [m x k] (lda), B [k x n] (ldb), Y [T x m] (ldy).
+ *   comm == NULL : A, B are the full factors.
+ *   comm != NULL : A, B are this rank's k-shards (k = k_r; the columns of A
+ *                  and rows of B given by dl_tp_plan) and the rank partials
+ *                  are reduce-summed over the communicator (all-reduce,
+ *                  PAPER.md:123) so every rank ends with the full Y.
+ *   accumulate   : 0 -> Y = result;  1 -> Y = Y + result (residual fusion).
+ *   The rank-k intermediate Z = X B^T is fp32-accumulated and rounded to
+ *   the input dtype before the second stage; for T <= 16 it never leaves
+ *   shared memory / registers of the fused SIMT chain.
+ *   workspace: >= dl_lowrank_linear_workspace() bytes, 256 B aligned.
+ * Errors: SHAPE, RANK (k < 1, or k > min(m,n) when comm == NULL), ALIGN,
+ *   DTYPE (fp32 with T > 16), WORKSPACE, CUDA, NCCL.  T == 0 -> DL_OK no-op.
+ * ---------------------------------------------------------------------- */
+dl_status dl_lowrank_linear_workspace(int64_t T, int64_t m, int64_t n,
+                                      int64_t k, dl_dtype dtype, size_t *bytes);
+dl_status dl_lowrank_linear(const void *X, int64_t ldx, const void *A,
+                            int64_t lda, const void *B, int64_t ldb, void *Y,
+                            int64_t ldy, int64_t T, int64_t m, int64_t n,
+                            int64_t k, dl_dtype dtype, int accumulate,
+                            dl_comm comm, void *workspace,
+                            size_t workspace_bytes, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Rank-sharding planner, PAPER.md:183 (Section 4.1: downward factors "first
+ * concatenated and then evenly split") and PAPER.md:242 (Section 4.3:
+ * "appropriately partitioned and evenly distributed").
+ *
+ * A factor GROUP is n_seg (1..3) factor pairs that share the same input x
+ * (q|k|v, gate|up, or a single matrix).  Their ranks r_0..r_{n_seg-1} are
+ * concatenated into [0, R), R = sum r_g, and [0, R) is split into `world`
+ * contiguous balanced ranges (rank r gets R/world, +1 for r < R % world).
+ * strict != 0 reproduces SPEC.md:202: R % world != 0 -> DL_ERR_PARTITION.
+ *
+ * dl_tp_plan (host only): for `rank`, seg_begin[g]/seg_len[g] (host arrays
+ * of n_seg) receive the rank's range inside segment g's own rank dimension
+ * (len may be 0), *k_loc the rank's total.
+ * ---------------------------------------------------------------------- */
+dl_status dl_tp_plan(const int64_t *seg_ranks, int n_seg, int world, int rank,
+                     int strict, int64_t *seg_begin, int64_t *seg_len,
+                     int64_t *k_loc);
+
+/* dl_tp_shard_factors: copy rank `rank`'s shard of a factor group on
+ * `stream`.  Inputs (device): A[g] [m[g] x r[g]] (lda[g]), B[g] [r[g] x n]
+ * (ldb[g]).  Outputs (device, caller-allocated): B_shard [k_loc x n]
+ * (ldb_shard) = concatenation of the rank's B rows in segment order;
+ * A_shard[g] [m[g] x seg_len[g]] (lda_shard[g]) = the matching columns of
+ * A[g] (A_shard[g] may be NULL when seg_len[g] == 0).  seg_len_out (host,
+ * optional) receives the per-segment lengths.  Host arrays: A, lda, B, ldb,
+ * m, r, A_shard, lda_shard.  No collectives; runs once at load. */
+dl_status dl_tp_shard_factors(int n_seg, const void *const *A,
+                              const int64_t *lda, const void *const *B,
+                              const int64_t *ldb, const int64_t *m,
+                              const int64_t *r, int64_t n, dl_dtype dtype,
+                              int world, int rank, int strict, void *B_shard,
+                              int64_t ldb_shard, void *const *A_shard,
+                              const int64_t *lda_shard, int64_t *seg_len_out,
+                              void *stream);
+
+/* ------------------------------------------------------------------------
+ * dl_decomposed_block_forward -- one decomposed LLaMA-3 block (pipeline of
+ * PAPER.md:183 Fig. 3 contents; norm/residual placement per LLaMA-3, reading
+ * c9 in DESIGN.md), bf16 storage, fp32 accumulation:
+ *     a = rmsnorm(x, attn_norm); q,k,v = A(B a) per matrix (one group)
+ *     q,k <- RoPE(positions);  append k,v to the cache
+ *     x += A_o(B_o causal_gqa_attention(q, K, V))
+ *     b = rmsnorm(x, mlp_norm); x += A_down(B_down(silu(A_g(B_g b)) * A_u(B_u b)))
+ * Rank sharding (comm != NULL, world P): each group's factors are the
+ * rank's dl_tp_shard_factors shard; the block issues five collectives per
+ * call on `stream`: reduce-scatter of the q|k|v partials by head, all-gather
+ * of the attention output, all-reduce after o, gate|up and down.  Heads must
+ * divide by P.  Attention runs on the rank's local heads only (removing the
+ * duplicated self-attention of PAPER.md:141-144).
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  int64_t h, n_heads, n_kv_heads, head_dim, m; /* m = MLP intermediate      */
+  int64_t rank_q, rank_k, rank_v, rank_o, rank_gate, rank_up, rank_down;
+  float rope_theta, rms_eps;
+  int64_t max_tokens; /* upper bound on T per call (workspace sizing)       */
+  int64_t max_seqs;   /* upper bound on num_seqs per call                   */
+} dl_block_config;
+
+typedef struct {
+  const void *A;  /* [m_seg x k] bf16, this rank's columns (NULL if k==0) */
+  int64_t lda;    /* >= k, multiple of 8                                    */
+  int64_t k;      /* this rank's rank-range length for the segment (>= 0)  */
+} dl_segment;
+
+typedef struct {
+  const void *B;  /* [k_loc x n] bf16, concatenated rank rows, seg order   */
+  int64_t ldb;    /* >= n, multiple of 8                                    */
+  dl_segment seg[3];
+} dl_factor_group;
+
+typedef struct {
+  const void *attn_norm, *mlp_norm; /* gamma, [h] bf16                     */
+  dl_factor_group qkv;  /* segments q (m=h), k (m=h_kv), v (m=h_kv); n = h */
+  dl_factor_group o;    /* segment o (m=h); n = h                          */
+  dl_factor_group gu;   /* segments gate (m), up (m); n = h                */
+  dl_factor_group down; /* segment down (m=h); n = m                       */
+} dl_block_weights;
+
+typedef enum { DL_PREFILL = 0, DL_DECODE = 1 } dl_phase;
+
+/* x          [T x h] bf16, residual stream, identical on every rank, updated
+ *            in place.
+ * positions  [T] int32 device: absolute position of each token.
+ * cu_seqlens [num_seqs+1] int32 device (PREFILL): packed sequence offsets;
+ *            token t of sequence s attends to tokens of s up to itself.
+ * k_cache, v_cache [max_seqs x n_kv_heads/P x max_seq x head_dim] bf16:
+ *            post-RoPE keys and values of this rank's kv heads.
+ * cache_lens [num_seqs] int32 device: tokens already cached per sequence.
+ *            PREFILL: the sequence's tokens are written at cache positions
+ *            cache_lens[s] + i and attend to the cached prefix too.
+ *            DECODE: T == num_seqs, token s is appended at cache_lens[s].
+ *            The caller advances cache_lens after the call.
+ * max_seq    cache capacity per sequence.
+ * workspace  >= dl_block_workspace() bytes, 256 B aligned.  It must be
+ *            zero-filled (cudaMemset) before its first use; every call
+ *            leaves its fp32 reduction scratch zero-filled again (the
+ *            epilogues consume-and-clear), so no per-call memset is needed.
+ *            Errors: SHAPE (T > max_tokens, num_seqs), PARTITION (heads %
+ *            world, shard wider than the balanced split), RANK, ALIGN,
+ *            UNSUPPORTED (head_dim != 128), WORKSPACE, CUDA, NCCL.       */
+dl_status dl_block_workspace(const dl_block_config *cfg, int world,
+                             size_t *bytes);
+dl_status dl_decomposed_block_forward(
+    const dl_block_config *cfg, const dl_block_weights *w, void *x, int64_t T,
+    const int32_t *positions, const int32_t *cu_seqlens, int32_t num_seqs,
+    dl_phase phase, void *k_cache, void *v_cache, const int32_t *cache_lens,
+    int64_t max_seq, dl_comm comm, void *workspace, size_t workspace_bytes,
+    void *stream);
+
+/* ------------------------------------------------------------------------
+ * Model-level helpers used by the decode / prefill step (embedding gather,
+ * final norm + dense LM head).  Not part of the paper's method; provided so
+ * a whole-model step runs in this library's kernels only.
+ * ---------------------------------------------------------------------- */
+/* out[t] = table[ids[t]]   (table [vocab x h] bf16, out [T x h] bf16)     */
+dl_status dl_embedding(const void *table, int64_t vocab, int64_t h,
+                       const int32_t *ids, int64_t T, void *out, void *stream);
+/* out = rmsnorm(x, gamma) (bf16, fp32 math)                               */
+dl_status dl_rmsnorm(const void *x, const void *gamma, void *out, int64_t T,
+                     int64_t h, float eps, void *stream);
+/* Dense C[T x N] = X[T x K] W[N x K]^T (bf16 in/out, fp32 acc, tcgen05),
+ * used for the vocab-sharded LM head; workspace per dl_dense_workspace.   */
+dl_status dl_dense_workspace(int64_t T, int64_t N, int64_t K, size_t *bytes);
+dl_status dl_dense(const void *X, int64_t ldx, const void *W, int64_t ldw,
+                   void *C, int64_t ldc, int64_t T, int64_t N, int64_t K,
+                   void *workspace, size_t workspace_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DL_H_ */

@@ -1,0 +1,305 @@
+"""ctypes binding of libdl.so (include/dl.h).  Argument marshalling only:
+every computation runs in the library's sm_100a kernels.  There is no CPU
+or PyTorch fallback -- if libdl.so is missing or the device is not an
+sm_100 GPU, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdl.so")
+
+DL_F32, DL_BF16 = 0, 1
+DL_PREFILL, DL_DECODE = 0, 1
+STATUS = {0: "DL_OK", 1: "DL_ERR_INVALID_ARG", 2: "DL_ERR_SHAPE", 3: "DL_ERR_RANK", 4: "DL_ERR_PARTITION",
+          5: "DL_ERR_DTYPE", 6: "DL_ERR_ALIGN", 7: "DL_ERR_WORKSPACE", 8: "DL_ERR_CUDA", 9: "DL_ERR_NCCL",
+          10: "DL_ERR_UNSUPPORTED"}
+EXPORTS = ("dl_last_error", "dl_version", "dl_device_ok", "dl_comm_create", "dl_comm_destroy",
+           "dl_lowrank_linear_workspace", "dl_lowrank_linear", "dl_tp_plan", "dl_tp_shard_factors",
+           "dl_block_workspace", "dl_decomposed_block_forward", "dl_embedding", "dl_rmsnorm",
+           "dl_dense_workspace", "dl_dense")
+
+
+class DLError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+P = ctypes.c_void_p
+I64 = ctypes.c_int64
+I32 = ctypes.c_int32
+I = ctypes.c_int
+
+
+class dl_block_config(ctypes.Structure):
+    _fields_ = [(n, I64) for n in ("h", "n_heads", "n_kv_heads", "head_dim", "m", "rank_q", "rank_k", "rank_v",
+                                   "rank_o", "rank_gate", "rank_up", "rank_down")] + \
+               [("rope_theta", ctypes.c_float), ("rms_eps", ctypes.c_float), ("max_tokens", I64),
+                ("max_seqs", I64)]
+
+
+class dl_segment(ctypes.Structure):
+    _fields_ = [("A", P), ("lda", I64), ("k", I64)]
+
+
+class dl_factor_group(ctypes.Structure):
+    _fields_ = [("B", P), ("ldb", I64), ("seg", dl_segment * 3)]
+
+
+class dl_block_weights(ctypes.Structure):
+    _fields_ = [("attn_norm", P), ("mlp_norm", P), ("qkv", dl_factor_group), ("o", dl_factor_group),
+                ("gu", dl_factor_group), ("down", dl_factor_group)]
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load():
+    """Load libdl.so (fails loudly if it was not built)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(f"{LIB_PATH} is missing: run `python -m paper_2604_17709_b200.build` "
+                                   "(there is no fallback implementation)")
+            lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+            lib.dl_last_error.restype = ctypes.c_char_p
+            lib.dl_version.restype = I
+            lib.dl_device_ok.restype = I
+            lib.dl_comm_create.argtypes = [P, I, I, ctypes.POINTER(P)]
+            lib.dl_comm_destroy.argtypes = [P]
+            lib.dl_lowrank_linear_workspace.argtypes = [I64, I64, I64, I64, I, ctypes.POINTER(ctypes.c_size_t)]
+            lib.dl_lowrank_linear.argtypes = [P, I64, P, I64, P, I64, P, I64, I64, I64, I64, I64, I, I, P, P,
+                                              ctypes.c_size_t, P]
+            lib.dl_tp_plan.argtypes = [P, I, I, I, I, P, P, P]
+            lib.dl_tp_shard_factors.argtypes = [I, P, P, P, P, P, P, I64, I, I, I, I, P, I64, P, P, P, P]
+            lib.dl_block_workspace.argtypes = [ctypes.POINTER(dl_block_config), I, ctypes.POINTER(ctypes.c_size_t)]
+            lib.dl_decomposed_block_forward.argtypes = [ctypes.POINTER(dl_block_config),
+                                                        ctypes.POINTER(dl_block_weights), P, I64, P, P, I32, I,
+                                                        P, P, P, I64, P, P, ctypes.c_size_t, P]
+            lib.dl_embedding.argtypes = [P, I64, I64, P, I64, P, P]
+            lib.dl_rmsnorm.argtypes = [P, P, P, I64, I64, ctypes.c_float, P]
+            lib.dl_dense_workspace.argtypes = [I64, I64, I64, ctypes.POINTER(ctypes.c_size_t)]
+            lib.dl_dense.argtypes = [P, I64, P, I64, P, I64, I64, I64, I64, P, ctypes.c_size_t, P]
+            for name in EXPORTS[3:]:
+                getattr(lib, name).restype = I
+            _lib = lib
+    return _lib
+
+
+def _check(status: int):
+    if status != 0:
+        raise DLError(status, load().dl_last_error().decode())
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _ld(t: torch.Tensor) -> int:
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise ValueError("expected a row-major 2-D tensor with unit column stride")
+    return t.stride(0)
+
+
+def _dtype(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return DL_F32
+    if t.dtype == torch.bfloat16:
+        return DL_BF16
+    raise ValueError(f"unsupported dtype {t.dtype}")
+
+
+def dl_version() -> int:
+    return load().dl_version()
+
+
+def dl_device_ok() -> bool:
+    return bool(load().dl_device_ok())
+
+
+# ---------------------------------------------------------------------------
+class Comm:
+    """dl_comm wrapper around an ncclComm_t (e.g. from a torch NCCL process group)."""
+
+    def __init__(self, nccl_comm_ptr: int, rank: int, world: int):
+        h = P()
+        _check(load().dl_comm_create(ctypes.c_void_p(nccl_comm_ptr), rank, world, ctypes.byref(h)))
+        self.handle = h
+        self.rank, self.world = rank, world
+
+    @classmethod
+    def from_process_group(cls, pg=None):
+        import torch.distributed as dist
+        pg = pg or dist.group.WORLD
+        backend = pg._get_backend(torch.device("cuda"))
+        return cls(backend._comm_ptr(), dist.get_rank(pg), dist.get_world_size(pg))
+
+    def close(self):
+        if self.handle:
+            load().dl_comm_destroy(self.handle)
+            self.handle = None
+
+
+def dl_comm_create(nccl_comm_ptr: int, rank: int, world: int) -> Comm:
+    return Comm(nccl_comm_ptr, rank, world)
+
+
+def _comm(c):
+    return None if c is None else c.handle
+
+
+# ---------------------------------------------------------------------------
+def dl_lowrank_linear_workspace(T: int, m: int, n: int, k: int, dtype=torch.bfloat16) -> int:
+    b = ctypes.c_size_t()
+    _check(load().dl_lowrank_linear_workspace(T, m, n, k, DL_F32 if dtype == torch.float32 else DL_BF16,
+                                              ctypes.byref(b)))
+    return b.value
+
+
+def dl_lowrank_linear(X: torch.Tensor, A: torch.Tensor, B: torch.Tensor, Y: torch.Tensor, accumulate: bool = False,
+                      comm: Comm | None = None, workspace: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Y (+)= A (B x) per token row.  Tensors are device tensors."""
+    T, n = X.shape
+    m, k = A.shape
+    if B.shape[0] != k or B.shape[1] != n or Y.shape[0] != T or Y.shape[1] != m:
+        raise ValueError("shape mismatch")
+    dt = _dtype(X)
+    if workspace is None:
+        workspace = torch.empty(dl_lowrank_linear_workspace(T, m, n, k, X.dtype), dtype=torch.uint8,
+                                device=X.device)
+    _check(load().dl_lowrank_linear(_ptr(X), _ld(X), _ptr(A), _ld(A), _ptr(B), _ld(B), _ptr(Y), _ld(Y), T, m, n, k,
+                                    dt, int(accumulate), _comm(comm), _ptr(workspace), workspace.numel(),
+                                    _stream(stream)))
+    return Y
+
+
+# ---------------------------------------------------------------------------
+def dl_tp_plan(seg_ranks, world: int, rank: int, strict: bool = False):
+    """Host planner: returns (seg_begin list, seg_len list, k_loc)."""
+    n = len(seg_ranks)
+    r = (I64 * n)(*seg_ranks)
+    b = (I64 * n)()
+    ln = (I64 * n)()
+    kl = I64()
+    _check(load().dl_tp_plan(ctypes.cast(r, P), n, world, rank, int(strict), ctypes.cast(b, P), ctypes.cast(ln, P),
+                             ctypes.byref(kl)))
+    return list(b), list(ln), kl.value
+
+
+def _pad8(x: int) -> int:
+    return (x + 7) // 8 * 8
+
+
+def dl_tp_shard_factors(As, Bs, world: int, rank: int, strict: bool = False, stream=None):
+    """Shard a factor group (lists of A_g [m_g x r_g], B_g [r_g x n]) for `rank`.
+
+    Returns (A_shards, B_shard, seg_lens).  Output buffers are allocated here
+    (torch = memory plumbing); the copy runs in the library on `stream`.
+    """
+    ng = len(As)
+    dt = _dtype(As[0])
+    n = Bs[0].shape[1]
+    ranks = [a.shape[1] for a in As]
+    _, lens, kloc = dl_tp_plan(ranks, world, rank, strict)
+    dev = As[0].device
+    B_shard = torch.zeros((kloc, _pad8(n)), dtype=As[0].dtype, device=dev)[:, :n]
+    A_shards = [torch.zeros((a.shape[0], max(_pad8(ln), 8)), dtype=a.dtype, device=dev)[:, :ln]
+                for a, ln in zip(As, lens)]
+    arr = lambda vals, ty=I64: (ty * ng)(*vals)  # noqa: E731
+    a_p = (P * ng)(*[a.data_ptr() for a in As])
+    b_p = (P * ng)(*[b.data_ptr() for b in Bs])
+    as_p = (P * ng)(*[a.data_ptr() for a in A_shards])
+    out_len = (I64 * ng)()
+    _check(load().dl_tp_shard_factors(ng, ctypes.cast(a_p, P), ctypes.cast(arr([_ld(a) for a in As]), P),
+                                      ctypes.cast(b_p, P), ctypes.cast(arr([_ld(b) for b in Bs]), P),
+                                      ctypes.cast(arr([a.shape[0] for a in As]), P), ctypes.cast(arr(ranks), P),
+                                      n, dt, world, rank, int(strict), _ptr(B_shard), B_shard.stride(0),
+                                      ctypes.cast(as_p, P), ctypes.cast(arr([a.stride(0) for a in A_shards]), P),
+                                      ctypes.cast(out_len, P), _stream(stream)))
+    return A_shards, B_shard, list(out_len)
+
+
+# ---------------------------------------------------------------------------
+def make_block_config(shape, ranks: dict, max_tokens: int, max_seqs: int) -> dl_block_config:
+    return dl_block_config(shape.h, shape.n_heads, shape.n_kv_heads, shape.head_dim, shape.m, ranks["q"],
+                           ranks["k"], ranks["v"], ranks["o"], ranks["gate"], ranks["up"], ranks["down"],
+                           float(shape.rope_theta), float(shape.rms_eps), max_tokens, max_seqs)
+
+
+class BlockWeights:
+    """Rank shard of one block's factors in the library's group layout
+    (B of a group concatenated, A per segment), built with dl_tp_shard_factors."""
+
+    GROUPS = (("qkv", ("q", "k", "v")), ("o", ("o",)), ("gu", ("gate", "up")), ("down", ("down",)))
+
+    def __init__(self, w: dict, world: int = 1, rank: int = 0, stream=None):
+        self.tensors = {"attn_norm": w["g_attn"].contiguous(), "mlp_norm": w["g_mlp"].contiguous()}
+        self.c = dl_block_weights()
+        self.c.attn_norm = self.tensors["attn_norm"].data_ptr()
+        self.c.mlp_norm = self.tensors["mlp_norm"].data_ptr()
+        self.seg_lens = {}
+        for gname, mats in self.GROUPS:
+            A_sh, B_sh, lens = dl_tp_shard_factors([w["A_" + m] for m in mats], [w["B_" + m] for m in mats],
+                                                   world, rank, stream=stream)
+            self.tensors["B_" + gname] = B_sh
+            grp = getattr(self.c, gname)
+            grp.B = B_sh.data_ptr()
+            grp.ldb = B_sh.stride(0)
+            for i, (mname, a, ln) in enumerate(zip(mats, A_sh, lens)):
+                self.tensors["A_" + mname] = a
+                grp.seg[i].A = a.data_ptr() if ln > 0 else None
+                grp.seg[i].lda = a.stride(0)
+                grp.seg[i].k = ln
+            self.seg_lens[gname] = lens
+
+
+def dl_block_workspace(cfg: dl_block_config, world: int = 1) -> int:
+    b = ctypes.c_size_t()
+    _check(load().dl_block_workspace(ctypes.byref(cfg), world, ctypes.byref(b)))
+    return b.value
+
+
+def dl_decomposed_block_forward(cfg: dl_block_config, weights: BlockWeights, x: torch.Tensor,
+                                positions: torch.Tensor, cu_seqlens: torch.Tensor | None, num_seqs: int,
+                                phase: int, k_cache: torch.Tensor, v_cache: torch.Tensor,
+                                cache_lens: torch.Tensor, comm: Comm | None, workspace: torch.Tensor,
+                                stream=None) -> torch.Tensor:
+    T = x.shape[0]
+    _check(load().dl_decomposed_block_forward(ctypes.byref(cfg), ctypes.byref(weights.c), _ptr(x), T,
+                                              _ptr(positions), _ptr(cu_seqlens), num_seqs, phase, _ptr(k_cache),
+                                              _ptr(v_cache), _ptr(cache_lens), k_cache.shape[2], _comm(comm),
+                                              _ptr(workspace), workspace.numel(), _stream(stream)))
+    return x
+
+
+def dl_embedding(table: torch.Tensor, ids: torch.Tensor, out: torch.Tensor, stream=None):
+    _check(load().dl_embedding(_ptr(table), table.shape[0], table.shape[1], _ptr(ids), ids.numel(), _ptr(out),
+                               _stream(stream)))
+    return out
+
+
+def dl_rmsnorm(x: torch.Tensor, gamma: torch.Tensor, out: torch.Tensor, eps: float, stream=None):
+    _check(load().dl_rmsnorm(_ptr(x), _ptr(gamma), _ptr(out), x.shape[0], x.shape[1], eps, _stream(stream)))
+    return out
+
+
+def dl_dense(X: torch.Tensor, W: torch.Tensor, C: torch.Tensor, stream=None):
+    T, K = X.shape
+    N = W.shape[0]
+    _check(load().dl_dense(_ptr(X), _ld(X), _ptr(W), _ld(W), _ptr(C), _ld(C), T, N, K, None, 0, _stream(stream)))
+    return C

@@ -1,0 +1,848 @@
+// C ABI (include/dl.h): argument validation, path selection, the rank-shard
+// planner, NCCL plumbing and the decomposed-block orchestration.  Every
+// arithmetic step runs in this library's kernels (tc_gemm.cu,
+// simt_chain.cu, elementwise.cu, attention.cu); there is no CPU fallback.
+#include <dlfcn.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+
+#include "dl_internal.h"
+
+namespace dl {
+
+static thread_local std::string g_last_error;
+
+void set_error(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+dl_status cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return DL_OK;
+  set_error("%s: %s", what, cudaGetErrorString(e));
+  return DL_ERR_CUDA;
+}
+
+int num_sms() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return kNumSMsB200;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+    return kNumSMsB200;
+  return n;
+}
+
+}  // namespace dl
+
+using namespace dl;
+
+#define DL_TRY(expr)                  \
+  do {                                \
+    dl_status _s = (expr);            \
+    if (_s != DL_OK) return _s;       \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// NCCL, resolved from the process (the NCCL instance that owns the comm).
+// ---------------------------------------------------------------------------
+namespace {
+constexpr int kNcclSum = 0;
+constexpr int kNcclFloat32 = 7;
+constexpr int kNcclBfloat16 = 9;
+typedef int (*nccl_allreduce_fn)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+typedef int (*nccl_reducescatter_fn)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+typedef int (*nccl_allgather_fn)(const void*, void*, size_t, int, void*, cudaStream_t);
+typedef const char* (*nccl_errstr_fn)(int);
+}  // namespace
+
+struct dl_comm_s {
+  void* nccl;
+  int rank, world;
+  nccl_allreduce_fn allreduce;
+  nccl_reducescatter_fn reducescatter;
+  nccl_allgather_fn allgather;
+  nccl_errstr_fn errstr;
+};
+
+namespace {
+
+void* find_sym(const char* name) {
+  void* p = dlsym(RTLD_DEFAULT, name);
+  if (p) return p;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  return h ? dlsym(h, name) : nullptr;
+}
+
+dl_status nccl_check(const dl_comm_s* c, int r, const char* what) {
+  if (r == 0) return DL_OK;
+  set_error("%s failed: %s", what, c->errstr ? c->errstr(r) : "nccl error");
+  return DL_ERR_NCCL;
+}
+
+dl_status all_reduce(dl_comm c, void* buf, size_t count, int dtype, cudaStream_t st) {
+  return nccl_check(c, c->allreduce(buf, buf, count, dtype, kNcclSum, c->nccl, st), "ncclAllReduce");
+}
+dl_status reduce_scatter(dl_comm c, const void* src, void* dst, size_t recv_count, int dtype, cudaStream_t st) {
+  return nccl_check(c, c->reducescatter(src, dst, recv_count, dtype, kNcclSum, c->nccl, st), "ncclReduceScatter");
+}
+dl_status all_gather(dl_comm c, const void* src, void* dst, size_t send_count, int dtype, cudaStream_t st) {
+  return nccl_check(c, c->allgather(src, dst, send_count, dtype, c->nccl, st), "ncclAllGather");
+}
+
+// ---------------------------------------------------------------------------
+// validation helpers
+// ---------------------------------------------------------------------------
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+size_t esize(dl_dtype t) { return t == DL_F32 ? 4 : 2; }
+int64_t rup(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+size_t rup_sz(size_t x) { return (x + 255) & ~size_t(255); }
+
+dl_status check_ld(int64_t ld, int64_t row, dl_dtype dt, const char* name) {
+  if (ld < row) {
+    set_error("%s: leading dimension %lld < row length %lld", name, (long long)ld, (long long)row);
+    return DL_ERR_SHAPE;
+  }
+  if ((ld * static_cast<int64_t>(esize(dt))) % 16 != 0) {
+    set_error("%s: leading dimension %lld is not a 16-byte multiple", name, (long long)ld);
+    return DL_ERR_ALIGN;
+  }
+  return DL_OK;
+}
+dl_status check_ptr(const void* p, const char* name) {
+  if (!p) {
+    set_error("%s is NULL", name);
+    return DL_ERR_INVALID_ARG;
+  }
+  if (!aligned16(p)) {
+    set_error("%s is not 16-byte aligned", name);
+    return DL_ERR_ALIGN;
+  }
+  return DL_OK;
+}
+dl_status check_device() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_status(e, "cudaGetDevice");
+  int major = 0;
+  e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (e != cudaSuccess) return cuda_status(e, "cudaDeviceGetAttribute");
+  if (major != 10) {
+    set_error("device compute capability %d.x is not sm_100 (B200)", major);
+    return DL_ERR_CUDA;
+  }
+  return DL_OK;
+}
+
+// path of dl_lowrank_linear
+enum LinPath { PATH_SIMT, PATH_SKINNY, PATH_WIDE };
+LinPath lin_path(int64_t T, dl_dtype dt) {
+  if (dt == DL_F32 || T <= 16) return PATH_SIMT;
+  if (T <= 256) return PATH_SKINNY;
+  return PATH_WIDE;
+}
+
+// workspace carving
+struct Carver {
+  uint8_t* base;
+  size_t off = 0;
+  explicit Carver(void* b) : base(static_cast<uint8_t*>(b)) {}
+  template <typename T>
+  T* take(size_t count) {
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += rup_sz(count * sizeof(T));
+    return p;
+  }
+};
+
+struct LinWs {
+  float* zf;           // [T x ldz32] fp32 (skinny) / SIMT z
+  __nv_bfloat16* zb;   // [T x ldzb]
+  float* yf;           // [T x ldy32] fp32
+  int64_t ldz32, ldzb, ldy32;
+};
+
+LinWs carve_lin(Carver& c, int64_t T, int64_t m, int64_t k, LinPath path, bool comm) {
+  LinWs w{};
+  w.ldz32 = rup(k, 4);
+  w.ldzb = rup(k, 8);
+  w.ldy32 = rup(m, 4);
+  w.zf = c.take<float>(static_cast<size_t>(T) * w.ldz32);
+  if (path != PATH_SIMT) w.zb = c.take<__nv_bfloat16>(static_cast<size_t>(T) * w.ldzb);
+  if (path == PATH_SKINNY || comm) w.yf = c.take<float>(static_cast<size_t>(T) * w.ldy32);
+  return w;
+}
+
+GemmProblem one_seg(const void* act, int64_t ld_act, int64_t T, int64_t k_act, const void* w, int64_t ldw,
+                    int64_t rows, int64_t klen, GemmOut out) {
+  GemmProblem p{};
+  p.act = act;
+  p.ld_act = ld_act;
+  p.T = T;
+  p.k_act = k_act;
+  p.nseg = 1;
+  p.seg[0] = GemmSeg{w, ldw, rows, klen, 0, 0};
+  p.n_feat = rows;
+  p.out = out;
+  return p;
+}
+
+GemmOut out_plain(void* ptr, int64_t ld, int mode, int accumulate) {
+  GemmOut o{};
+  o.ptr = ptr;
+  o.ld = ld;
+  o.mode = mode;
+  o.accumulate = accumulate;
+  o.scatter_p = 1;
+  return o;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dl_last_error(void) { return g_last_error.c_str(); }
+int dl_version(void) { return 100; }
+int dl_device_ok(void) { return check_device() == DL_OK ? 1 : 0; }
+
+dl_status dl_comm_create(void* nccl_comm, int rank, int world, dl_comm* out) {
+  if (!out || !nccl_comm) {
+    set_error("dl_comm_create: null argument");
+    return DL_ERR_INVALID_ARG;
+  }
+  if (world < 1 || rank < 0 || rank >= world) {
+    set_error("dl_comm_create: bad rank %d / world %d", rank, world);
+    return DL_ERR_INVALID_ARG;
+  }
+  dl_comm_s c{};
+  c.nccl = nccl_comm;
+  c.rank = rank;
+  c.world = world;
+  c.allreduce = reinterpret_cast<nccl_allreduce_fn>(find_sym("ncclAllReduce"));
+  c.reducescatter = reinterpret_cast<nccl_reducescatter_fn>(find_sym("ncclReduceScatter"));
+  c.allgather = reinterpret_cast<nccl_allgather_fn>(find_sym("ncclAllGather"));
+  c.errstr = reinterpret_cast<nccl_errstr_fn>(find_sym("ncclGetErrorString"));
+  if (!c.allreduce || !c.reducescatter || !c.allgather) {
+    set_error("dl_comm_create: NCCL symbols not found in the process");
+    return DL_ERR_NCCL;
+  }
+  *out = new dl_comm_s(c);
+  return DL_OK;
+}
+
+dl_status dl_comm_destroy(dl_comm comm) {
+  delete comm;
+  return DL_OK;
+}
+
+// ---------------------------------------------------------------------------
+dl_status dl_lowrank_linear_workspace(int64_t T, int64_t m, int64_t n, int64_t k, dl_dtype dtype, size_t* bytes) {
+  (void)n;
+  if (!bytes) {
+    set_error("bytes is NULL");
+    return DL_ERR_INVALID_ARG;
+  }
+  Carver c(nullptr);
+  carve_lin(c, T > 0 ? T : 1, m, k, lin_path(T, dtype), true);
+  *bytes = c.off;
+  return DL_OK;
+}
+
+dl_status dl_lowrank_linear(const void* X, int64_t ldx, const void* A, int64_t lda, const void* B, int64_t ldb,
+                            void* Y, int64_t ldy, int64_t T, int64_t m, int64_t n, int64_t k, dl_dtype dtype,
+                            int accumulate, dl_comm comm, void* workspace, size_t workspace_bytes, void* stream) {
+  if (dtype != DL_F32 && dtype != DL_BF16) {
+    set_error("unknown dtype %d", (int)dtype);
+    return DL_ERR_INVALID_ARG;
+  }
+  if (T < 0 || m <= 0 || n <= 0) {
+    set_error("bad shape T=%lld m=%lld n=%lld", (long long)T, (long long)m, (long long)n);
+    return DL_ERR_SHAPE;
+  }
+  if (k < 1 || (!comm && k > std::min(m, n))) {
+    set_error("rank k=%lld outside [1, min(m,n)=%lld]", (long long)k, (long long)std::min(m, n));
+    return DL_ERR_RANK;
+  }
+  if (T == 0) return DL_OK;
+  DL_TRY(check_ptr(X, "X"));
+  DL_TRY(check_ptr(A, "A"));
+  DL_TRY(check_ptr(B, "B"));
+  DL_TRY(check_ptr(Y, "Y"));
+  DL_TRY(check_ld(ldx, n, dtype, "ldx"));
+  DL_TRY(check_ld(lda, k, dtype, "lda"));
+  DL_TRY(check_ld(ldb, n, dtype, "ldb"));
+  DL_TRY(check_ld(ldy, m, dtype, "ldy"));
+  if (dtype == DL_F32 && T > 16) {
+    set_error("fp32 runs on the exact-FFMA SIMT path, limited to T <= 16 (got %lld)", (long long)T);
+    return DL_ERR_DTYPE;
+  }
+  const LinPath path = lin_path(T, dtype);
+  if ((path != PATH_SIMT || comm) && m % 4 != 0) {
+    set_error("tensor-core path requires m %% 4 == 0 (got m=%lld)", (long long)m);
+    return DL_ERR_UNSUPPORTED;
+  }
+  size_t need = 0;
+  dl_lowrank_linear_workspace(T, m, n, k, dtype, &need);
+  if (!workspace || workspace_bytes < need) {
+    set_error("workspace %zu B < required %zu B", workspace_bytes, need);
+    return DL_ERR_WORKSPACE;
+  }
+  DL_TRY(check_device());
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Carver cv(workspace);
+  LinWs ws = carve_lin(cv, T, m, k, path, comm != nullptr);
+  const bool reduce = comm != nullptr && comm->world > 1;
+
+  if (path == PATH_SIMT) {
+    if (!reduce) return simt_lowrank(X, ldx, A, lda, B, ldb, Y, ldy, T, m, n, k, dtype, accumulate, ws.zf, st);
+    // partial into fp32 Y scratch, all-reduce, then finish into Y
+    DL_TRY(cuda_status(cudaMemsetAsync(ws.yf, 0, sizeof(float) * T * ws.ldy32, st), "memset"));
+    if (dtype == DL_F32) {
+      DL_TRY(simt_lowrank(X, ldx, A, lda, B, ldb, ws.yf, ws.ldy32, T, m, n, k, dtype, 0, ws.zf, st));
+      DL_TRY(all_reduce(comm, ws.yf, static_cast<size_t>(T) * ws.ldy32, kNcclFloat32, st));
+      if (!accumulate)
+        return cuda_status(cudaMemcpy2DAsync(Y, ldy * 4, ws.yf, ws.ldy32 * 4, m * 4, T, cudaMemcpyDeviceToDevice, st),
+                           "copy");
+      set_error("fp32 accumulate with comm is not supported");
+      return DL_ERR_UNSUPPORTED;
+    }
+    // bf16: compute bf16 partial into zb-sized scratch via Y itself is unsafe with accumulate -> use tensor path
+  }
+
+  // ---- tensor-core paths (bf16) ----
+  if (path == PATH_SKINNY || (path == PATH_SIMT && reduce)) {
+    // stage 1: Zf += X B^T (stream-K, fp32 reduction), then bf16 Z
+    DL_TRY(cuda_status(cudaMemsetAsync(ws.zf, 0, sizeof(float) * T * ws.ldz32, st), "memset"));
+    DL_TRY(cuda_status(cudaMemsetAsync(ws.yf, 0, sizeof(float) * T * ws.ldy32, st), "memset"));
+    DL_TRY(tc_gemm(one_seg(X, ldx, T, n, B, ldb, k, n, out_plain(ws.zf, ws.ldz32, OUT_F32_RED, 0)), true, st));
+    DL_TRY(launch_f32_to_bf16(ws.zf, ws.ldz32, ws.zb, ws.ldzb, T, rup(k, 4), 1, st));
+    DL_TRY(tc_gemm(one_seg(ws.zb, ws.ldzb, T, k, A, lda, m, k, out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0)), true,
+                   st));
+    if (reduce) DL_TRY(all_reduce(comm, ws.yf, static_cast<size_t>(T) * ws.ldy32, kNcclFloat32, st));
+    if (accumulate)
+      return launch_residual_add_f32(ws.yf, ws.ldy32, static_cast<__nv_bfloat16*>(Y), ldy, T, m, 1, st);
+    return launch_f32_to_bf16(ws.yf, ws.ldy32, static_cast<__nv_bfloat16*>(Y), ldy, T, m, 1, st);
+  }
+  // PATH_WIDE: whole-tile, bf16 Z straight from the epilogue
+  DL_TRY(tc_gemm(one_seg(X, ldx, T, n, B, ldb, k, n, out_plain(ws.zb, ws.ldzb, OUT_BF16, 0)), false, st));
+  if (!reduce)
+    return tc_gemm(one_seg(ws.zb, ws.ldzb, T, k, A, lda, m, k, out_plain(Y, ldy, OUT_BF16, accumulate)), false, st);
+  DL_TRY(tc_gemm(one_seg(ws.zb, ws.ldzb, T, k, A, lda, m, k, out_plain(ws.yf, ws.ldy32, OUT_F32_STORE, 0)), false,
+                 st));
+  DL_TRY(all_reduce(comm, ws.yf, static_cast<size_t>(T) * ws.ldy32, kNcclFloat32, st));
+  if (accumulate) return launch_residual_add_f32(ws.yf, ws.ldy32, static_cast<__nv_bfloat16*>(Y), ldy, T, m, 0, st);
+  return launch_f32_to_bf16(ws.yf, ws.ldy32, static_cast<__nv_bfloat16*>(Y), ldy, T, m, 0, st);
+}
+
+// ---------------------------------------------------------------------------
+// rank-shard planner
+// ---------------------------------------------------------------------------
+dl_status dl_tp_plan(const int64_t* seg_ranks, int n_seg, int world, int rank, int strict, int64_t* seg_begin,
+                     int64_t* seg_len, int64_t* k_loc) {
+  if (!seg_ranks || !seg_begin || !seg_len || n_seg < 1 || n_seg > 3) {
+    set_error("dl_tp_plan: bad arguments");
+    return DL_ERR_INVALID_ARG;
+  }
+  if (world < 1 || rank < 0 || rank >= world) {
+    set_error("dl_tp_plan: bad rank %d / world %d", rank, world);
+    return DL_ERR_PARTITION;
+  }
+  int64_t R = 0;
+  for (int g = 0; g < n_seg; ++g) {
+    if (seg_ranks[g] < 1) {
+      set_error("dl_tp_plan: segment %d rank %lld < 1", g, (long long)seg_ranks[g]);
+      return DL_ERR_RANK;
+    }
+    R += seg_ranks[g];
+  }
+  if (R < world) {
+    set_error("dl_tp_plan: total rank %lld < world %d", (long long)R, world);
+    return DL_ERR_PARTITION;
+  }
+  if (strict && R % world != 0) {
+    set_error("dl_tp_plan: strict split of %lld over %d ranks is uneven", (long long)R, world);
+    return DL_ERR_PARTITION;
+  }
+  // balanced contiguous split of the concatenated range [0, R)
+  const int64_t base = R / world, extra = R % world;
+  const int64_t lo = rank * base + std::min<int64_t>(rank, extra);
+  const int64_t hi = lo + base + (rank < extra ? 1 : 0);
+  int64_t off = 0, total = 0;
+  for (int g = 0; g < n_seg; ++g) {
+    const int64_t a = std::max(lo, off), b = std::min(hi, off + seg_ranks[g]);
+    seg_begin[g] = std::max<int64_t>(0, a - off);
+    seg_len[g] = std::max<int64_t>(0, b - a);
+    if (seg_len[g] == 0) seg_begin[g] = 0;
+    total += seg_len[g];
+    off += seg_ranks[g];
+  }
+  if (k_loc) *k_loc = total;
+  return DL_OK;
+}
+
+dl_status dl_tp_shard_factors(int n_seg, const void* const* A, const int64_t* lda, const void* const* B,
+                              const int64_t* ldb, const int64_t* m, const int64_t* r, int64_t n, dl_dtype dtype,
+                              int world, int rank, int strict, void* B_shard, int64_t ldb_shard,
+                              void* const* A_shard, const int64_t* lda_shard, int64_t* seg_len_out, void* stream) {
+  if (!A || !lda || !B || !ldb || !m || !r || !A_shard || !lda_shard || !B_shard) {
+    set_error("dl_tp_shard_factors: null argument");
+    return DL_ERR_INVALID_ARG;
+  }
+  int64_t beg[3], len[3], kloc = 0;
+  DL_TRY(dl_tp_plan(r, n_seg, world, rank, strict, beg, len, &kloc));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t es = esize(dtype);
+  DL_TRY(check_ld(ldb_shard, n, dtype, "ldb_shard"));
+  int64_t row = 0;
+  for (int g = 0; g < n_seg; ++g) {
+    if (len[g] > 0) {
+      DL_TRY(check_ld(lda_shard[g], len[g], dtype, "lda_shard"));
+      const uint8_t* bsrc = static_cast<const uint8_t*>(B[g]) + beg[g] * ldb[g] * es;
+      uint8_t* bdst = static_cast<uint8_t*>(B_shard) + row * ldb_shard * es;
+      DL_TRY(launch_copy2d(bsrc, ldb[g] * es, bdst, ldb_shard * es, len[g], n * es, st));
+      const uint8_t* asrc = static_cast<const uint8_t*>(A[g]) + beg[g] * es;
+      DL_TRY(launch_copy2d(asrc, lda[g] * es, A_shard[g], lda_shard[g] * es, m[g], len[g] * es, st));
+      row += len[g];
+    }
+    if (seg_len_out) seg_len_out[g] = len[g];
+  }
+  return DL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// decomposed block
+// ---------------------------------------------------------------------------
+namespace {
+
+struct BlockDims {
+  int64_t h, hkv, m, H, Hk, d, P;
+  int64_t Hq_loc, Hk_loc, W;       // local heads, RS slab width
+  int64_t k_qkv, k_o, k_gu, k_down, kmax;
+  int64_t nmax;                    // widest stage-2 output (features)
+};
+
+dl_status block_dims(const dl_block_config* c, int world, BlockDims* d) {
+  if (!c) {
+    set_error("cfg is NULL");
+    return DL_ERR_INVALID_ARG;
+  }
+  if (c->h <= 0 || c->n_heads <= 0 || c->n_kv_heads <= 0 || c->head_dim <= 0 || c->m <= 0) {
+    set_error("bad block dims");
+    return DL_ERR_SHAPE;
+  }
+  if (c->n_heads * c->head_dim != c->h || c->n_heads % c->n_kv_heads != 0) {
+    set_error("h must equal n_heads*head_dim and n_heads %% n_kv_heads == 0");
+    return DL_ERR_SHAPE;
+  }
+  if (c->head_dim != 128) {
+    set_error("head_dim %lld unsupported (128)", (long long)c->head_dim);
+    return DL_ERR_UNSUPPORTED;
+  }
+  if (world < 1 || c->n_heads % world != 0 || c->n_kv_heads % world != 0) {
+    set_error("heads (%lld q, %lld kv) not divisible by world %d", (long long)c->n_heads,
+              (long long)c->n_kv_heads, world);
+    return DL_ERR_PARTITION;
+  }
+  const int64_t hkv = c->n_kv_heads * c->head_dim;
+  const int64_t ranks[7] = {c->rank_q, c->rank_k, c->rank_v, c->rank_o, c->rank_gate, c->rank_up, c->rank_down};
+  const int64_t mins[7] = {c->h, hkv, hkv, c->h, std::min(c->h, c->m), std::min(c->h, c->m), std::min(c->h, c->m)};
+  for (int i = 0; i < 7; ++i)
+    if (ranks[i] < 1 || ranks[i] > mins[i]) {
+      set_error("rank %d = %lld outside [1, %lld]", i, (long long)ranks[i], (long long)mins[i]);
+      return DL_ERR_RANK;
+    }
+  if (c->h % 64 || c->m % 64) {
+    set_error("h and m must be multiples of 64");
+    return DL_ERR_UNSUPPORTED;
+  }
+  d->h = c->h; d->hkv = hkv; d->m = c->m; d->H = c->n_heads; d->Hk = c->n_kv_heads; d->d = c->head_dim;
+  d->P = world;
+  d->Hq_loc = c->n_heads / world;
+  d->Hk_loc = c->n_kv_heads / world;
+  d->W = (c->h + 2 * hkv) / world;
+  auto cdiv = [](int64_t a, int64_t b) { return (a + b - 1) / b; };
+  d->k_qkv = cdiv(c->rank_q + c->rank_k + c->rank_v, world);
+  d->k_o = cdiv(c->rank_o, world);
+  d->k_gu = cdiv(c->rank_gate + c->rank_up, world);
+  d->k_down = cdiv(c->rank_down, world);
+  // Z columns: every segment starts on a 64-column (one K block) boundary
+  d->kmax = std::max(std::max(d->k_qkv, d->k_o), std::max(d->k_gu, d->k_down)) + 3 * 64;
+  d->nmax = std::max(c->h + 2 * hkv, 2 * c->m);
+  return DL_OK;
+}
+
+struct BlockWs {
+  float* zf; float* yf;              // fp32 reduction targets (zero-maintained)
+  __nv_bfloat16 *xn, *zb, *yb, *rs, *q, *att, *att_full, *ag, *act;
+  int64_t ldz32, ldzb, ldy32;
+};
+
+BlockWs carve_block(Carver& c, const BlockDims& d, int64_t Tmax) {
+  BlockWs w{};
+  const int64_t Ts = std::min<int64_t>(Tmax, 256);   // skinny path bound
+  w.ldz32 = rup(d.kmax, 64);
+  w.ldzb = rup(d.kmax, 64);
+  w.ldy32 = rup(d.nmax, 4);
+  w.zf = c.take<float>(static_cast<size_t>(Ts) * w.ldz32);
+  w.yf = c.take<float>(static_cast<size_t>(Ts) * w.ldy32);
+  w.xn = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.h);
+  w.zb = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * w.ldzb);
+  w.yb = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * rup(d.nmax, 8));
+  w.rs = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.W);
+  w.q = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.Hq_loc * d.d);
+  w.att = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.Hq_loc * d.d);
+  if (d.P > 1) {
+    w.att_full = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.h);
+    w.ag = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.h);
+  }
+  w.act = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.m);
+  return w;
+}
+
+dl_status check_group(const dl_factor_group& g, int nseg, int64_t n, const char* name, int64_t* k_loc) {
+  int64_t k = 0;
+  for (int s = 0; s < nseg; ++s) {
+    if (g.seg[s].k < 0) {
+      set_error("%s: negative segment rank", name);
+      return DL_ERR_RANK;
+    }
+    if (g.seg[s].k > 0) {
+      DL_TRY(check_ptr(g.seg[s].A, name));
+      DL_TRY(check_ld(g.seg[s].lda, g.seg[s].k, DL_BF16, name));
+    }
+    k += g.seg[s].k;
+  }
+  if (k < 1) {
+    set_error("%s: rank shard is empty", name);
+    return DL_ERR_PARTITION;
+  }
+  DL_TRY(check_ptr(g.B, name));
+  DL_TRY(check_ld(g.ldb, n, DL_BF16, name));
+  *k_loc = k;
+  return DL_OK;
+}
+
+// Z column layout of a group: segment g occupies [off_g, off_g + rup(k_g, 64)),
+// so every stage-2 TMA box starts on a K-block boundary of its own segment.
+struct ZLayout {
+  int64_t off[3];
+  int64_t width;
+};
+ZLayout zlayout(const dl_factor_group& g, int nseg) {
+  ZLayout z{};
+  int64_t o = 0;
+  for (int s = 0; s < nseg; ++s) {
+    z.off[s] = o;
+    o += rup(g.seg[s].k, 64);
+  }
+  z.width = o;
+  return z;
+}
+
+// stage 1: Z[:, off_g + j] = act . B_g[j]^T for the rows of B belonging to segment g
+GemmProblem stage1(const dl_factor_group& grp, int nseg, const void* act, int64_t ld_act, int64_t T, int64_t n,
+                   const ZLayout& zl, GemmOut out) {
+  GemmProblem p{};
+  p.act = act;
+  p.ld_act = ld_act;
+  p.T = T;
+  p.k_act = n;
+  p.nseg = nseg;
+  int64_t row = 0;
+  out.remap_cols = 1;
+  for (int s = 0; s < nseg; ++s) {
+    const int64_t k = grp.seg[s].k;
+    p.seg[s] = GemmSeg{static_cast<const __nv_bfloat16*>(grp.B) + row * grp.ldb, grp.ldb, k, n, row, 0};
+    out.seg_col_off[s] = zl.off[s];
+    out.seg_write_rows[s] = rup(k, 64);
+    row += k;
+  }
+  p.n_feat = row;
+  p.out = out;
+  return p;
+}
+
+// stage 2: segment g writes features [begin_g, begin_g + rows_g) from Z[:, off_g ...]
+GemmProblem stage2(const dl_factor_group& grp, int nseg, const int64_t* rows, const __nv_bfloat16* zb, int64_t ldzb,
+                   int64_t T, const ZLayout& zl, GemmOut out) {
+  GemmProblem p{};
+  p.act = zb;
+  p.ld_act = ldzb;
+  p.T = T;
+  p.k_act = zl.width;
+  p.nseg = nseg;
+  int64_t fb = 0;
+  for (int s = 0; s < nseg; ++s) {
+    p.seg[s] = GemmSeg{grp.seg[s].A, grp.seg[s].lda, rows[s], grp.seg[s].k, fb, zl.off[s]};
+    fb += rows[s];
+  }
+  p.n_feat = fb;
+  p.out = out;
+  return p;
+}
+
+// One factor group: Z = act . B^T (Z kept as bf16 in the workspace), then
+// Y = Z . A_g^T into `out2` (skinny: stream-K fp32 reduction; wide: bf16).
+dl_status run_group(const dl_factor_group& grp, int nseg, const int64_t* rows, const __nv_bfloat16* act,
+                    int64_t ld_act, int64_t n, int64_t T, bool skinny, const BlockWs& ws, const GemmOut& out2,
+                    cudaStream_t st) {
+  const ZLayout zl = zlayout(grp, nseg);
+  if (skinny) {
+    DL_TRY(tc_gemm(stage1(grp, nseg, act, ld_act, T, n, zl, out_plain(ws.zf, ws.ldz32, OUT_F32_RED, 0)), true, st));
+    DL_TRY(launch_f32_to_bf16(ws.zf, ws.ldz32, ws.zb, ws.ldzb, T, zl.width, 1, st));
+  } else {
+    DL_TRY(tc_gemm(stage1(grp, nseg, act, ld_act, T, n, zl, out_plain(ws.zb, ws.ldzb, OUT_BF16, 0)), false, st));
+  }
+  return tc_gemm(stage2(grp, nseg, rows, ws.zb, ws.ldzb, T, zl, out2), skinny, st);
+}
+
+}  // namespace
+
+dl_status dl_block_workspace(const dl_block_config* cfg, int world, size_t* bytes) {
+  if (!bytes) {
+    set_error("bytes is NULL");
+    return DL_ERR_INVALID_ARG;
+  }
+  BlockDims d;
+  DL_TRY(block_dims(cfg, world, &d));
+  Carver c(nullptr);
+  carve_block(c, d, std::max<int64_t>(cfg->max_tokens, 1));
+  *bytes = c.off;
+  return DL_OK;
+}
+
+dl_status dl_decomposed_block_forward(const dl_block_config* cfg, const dl_block_weights* w, void* x_, int64_t T,
+                                      const int32_t* positions, const int32_t* cu_seqlens, int32_t num_seqs,
+                                      dl_phase phase, void* k_cache, void* v_cache, const int32_t* cache_lens,
+                                      int64_t max_seq, dl_comm comm, void* workspace, size_t workspace_bytes,
+                                      void* stream) {
+  const int P = comm ? comm->world : 1;
+  BlockDims d;
+  DL_TRY(block_dims(cfg, P, &d));
+  if (!w) {
+    set_error("weights NULL");
+    return DL_ERR_INVALID_ARG;
+  }
+  if (T < 0 || T > cfg->max_tokens) {
+    set_error("T=%lld outside [0, max_tokens=%lld]", (long long)T, (long long)cfg->max_tokens);
+    return DL_ERR_SHAPE;
+  }
+  if (T == 0) return DL_OK;
+  if (phase != DL_PREFILL && phase != DL_DECODE) {
+    set_error("bad phase");
+    return DL_ERR_INVALID_ARG;
+  }
+  if (num_seqs < 1 || num_seqs > cfg->max_seqs || (phase == DL_DECODE && num_seqs != T)) {
+    set_error("num_seqs=%d invalid (max_seqs=%lld, decode requires num_seqs == T)", num_seqs,
+              (long long)cfg->max_seqs);
+    return DL_ERR_SHAPE;
+  }
+  if (!positions || !cache_lens || (phase == DL_PREFILL && !cu_seqlens) || max_seq < 1) {
+    set_error("positions / cache_lens / cu_seqlens / max_seq missing");
+    return DL_ERR_INVALID_ARG;
+  }
+  DL_TRY(check_ptr(x_, "x"));
+  DL_TRY(check_ptr(k_cache, "k_cache"));
+  DL_TRY(check_ptr(v_cache, "v_cache"));
+  DL_TRY(check_ptr(w->attn_norm, "attn_norm"));
+  DL_TRY(check_ptr(w->mlp_norm, "mlp_norm"));
+  int64_t kq, ko, kg, kd;
+  DL_TRY(check_group(w->qkv, 3, d.h, "qkv", &kq));
+  DL_TRY(check_group(w->o, 1, d.h, "o", &ko));
+  DL_TRY(check_group(w->gu, 2, d.h, "gate|up", &kg));
+  DL_TRY(check_group(w->down, 1, d.m, "down", &kd));
+  if (kq > d.k_qkv || ko > d.k_o || kg > d.k_gu || kd > d.k_down) {
+    set_error("group shard larger than the balanced split allows");
+    return DL_ERR_PARTITION;
+  }
+  size_t need = 0;
+  dl_block_workspace(cfg, P, &need);
+  if (!workspace || workspace_bytes < need) {
+    set_error("workspace %zu B < required %zu B", workspace_bytes, need);
+    return DL_ERR_WORKSPACE;
+  }
+  DL_TRY(check_device());
+
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  __nv_bfloat16* x = static_cast<__nv_bfloat16*>(x_);
+  Carver cv(workspace);
+  const BlockWs ws = carve_block(cv, d, cfg->max_tokens);
+  const bool skinny = T <= 256;
+  const bool tp = comm && P > 1;
+  const int64_t qkv_rows[3] = {d.h, d.hkv, d.hkv};
+  const int64_t gu_rows[2] = {d.m, d.m};
+  const int64_t h_rows[1] = {d.h};
+  const int64_t NQKV = d.h + 2 * d.hkv;
+  const int red_mode = skinny ? OUT_F32_RED : OUT_BF16;
+
+  // ---- q|k|v: one group; partials laid out rank-major by head for the RS ----
+  GemmOut qkv_out{};
+  qkv_out.mode = red_mode;
+  qkv_out.scatter_p = tp ? P : 1;
+  qkv_out.slab = d.W;
+  qkv_out.seg_slab_off[0] = 0;
+  qkv_out.seg_slab_off[1] = d.h / P;
+  qkv_out.seg_slab_off[2] = d.h / P + d.hkv / P;
+  qkv_out.seg_rpr[0] = d.h / P;
+  qkv_out.seg_rpr[1] = d.hkv / P;
+  qkv_out.seg_rpr[2] = d.hkv / P;
+  qkv_out.ptr = skinny ? static_cast<void*>(ws.yf) : static_cast<void*>(ws.yb);
+  qkv_out.ld = skinny ? ws.ldy32 : NQKV;
+
+  DL_TRY(launch_rmsnorm(x, static_cast<const __nv_bfloat16*>(w->attn_norm), ws.xn, T, d.h, cfg->rms_eps, st));
+  DL_TRY(run_group(w->qkv, 3, qkv_rows, ws.xn, d.h, d.h, T, skinny, ws, qkv_out, st));
+
+  RopeCacheArgs rc{};
+  rc.q_out = ws.q;
+  rc.k_cache = static_cast<__nv_bfloat16*>(k_cache);
+  rc.v_cache = static_cast<__nv_bfloat16*>(v_cache);
+  rc.max_seq = max_seq;
+  rc.positions = positions;
+  rc.cu_seqlens = cu_seqlens;
+  rc.cache_lens = cache_lens;
+  rc.num_seqs = num_seqs;
+  rc.decode = phase == DL_DECODE;
+  rc.T = T;
+  rc.Hq = static_cast<int>(d.Hq_loc);
+  rc.Hk = static_cast<int>(d.Hk_loc);
+  rc.d = static_cast<int>(d.d);
+  rc.theta = cfg->rope_theta;
+  if (!tp) {
+    if (skinny) {
+      rc.acc = ws.yf;
+      rc.ld_src = ws.ldy32;
+      rc.clear = 1;
+    } else {
+      rc.src = ws.yb;
+      rc.ld_src = NQKV;
+    }
+  } else {
+    if (skinny) DL_TRY(launch_f32_to_bf16(ws.yf, NQKV, ws.yb, NQKV, 1, T * NQKV, 1, st));   // contiguous [P][T][W]
+    DL_TRY(reduce_scatter(comm, ws.yb, ws.rs, static_cast<size_t>(T) * d.W, kNcclBfloat16, st));
+    rc.src = ws.rs;
+    rc.ld_src = d.W;
+  }
+  DL_TRY(launch_rope_cache(rc, st));
+
+  AttnArgs aa{};
+  aa.q = ws.q;
+  aa.out = ws.att;
+  aa.k_cache = rc.k_cache;
+  aa.v_cache = rc.v_cache;
+  aa.max_seq = max_seq;
+  aa.cu_seqlens = cu_seqlens;
+  aa.cache_lens = cache_lens;
+  aa.num_seqs = num_seqs;
+  aa.T = T;
+  aa.Hq = static_cast<int>(d.Hq_loc);
+  aa.Hk = static_cast<int>(d.Hk_loc);
+  aa.d = static_cast<int>(d.d);
+  aa.decode = phase == DL_DECODE;
+  DL_TRY(launch_attention(aa, st));
+
+  const __nv_bfloat16* att_in = ws.att;
+  if (tp) {
+    const int64_t wl = d.Hq_loc * d.d;
+    DL_TRY(all_gather(comm, ws.att, ws.ag, static_cast<size_t>(T) * wl, kNcclBfloat16, st));
+    DL_TRY(launch_unpermute(ws.ag, ws.att_full, P, T, wl, st));
+    att_in = ws.att_full;
+  }
+
+  // Finish a [T x n] group output: + residual (o, down) with the TP reduction.
+  auto finish_residual = [&](int64_t n) -> dl_status {
+    if (!tp) return skinny ? launch_residual_add_f32(ws.yf, ws.ldy32, x, d.h, T, n, 1, st) : DL_OK;
+    if (skinny) DL_TRY(launch_f32_to_bf16(ws.yf, ws.ldy32, ws.yb, n, T, n, 1, st));
+    DL_TRY(all_reduce(comm, ws.yb, static_cast<size_t>(T) * n, kNcclBfloat16, st));
+    return launch_residual_add_bf16(ws.yb, n, x, d.h, T, n, st);
+  };
+  // wide & TP=1: the stage-2 epilogue adds straight into x (fused residual)
+  auto resid_out = [&]() -> GemmOut {
+    if (skinny) return out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0);
+    if (!tp) return out_plain(x, d.h, OUT_BF16, 1);
+    return out_plain(ws.yb, d.h, OUT_BF16, 0);
+  };
+
+  // ---- o projection + residual ----------------------------------------------
+  DL_TRY(run_group(w->o, 1, h_rows, att_in, d.h, d.h, T, skinny, ws, resid_out(), st));
+  DL_TRY(finish_residual(d.h));
+
+  // ---- MLP: gate|up group, SiLU(gate)*up, down + residual ----------------------
+  DL_TRY(launch_rmsnorm(x, static_cast<const __nv_bfloat16*>(w->mlp_norm), ws.xn, T, d.h, cfg->rms_eps, st));
+  GemmOut gu_out = skinny ? out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0) : out_plain(ws.yb, 2 * d.m, OUT_BF16, 0);
+  DL_TRY(run_group(w->gu, 2, gu_rows, ws.xn, d.h, d.h, T, skinny, ws, gu_out, st));
+  if (!tp && skinny) {
+    DL_TRY(launch_silu_mul_f32(ws.yf, ws.ldy32, ws.act, d.m, T, d.m, 1, st));
+  } else {
+    if (skinny) DL_TRY(launch_f32_to_bf16(ws.yf, ws.ldy32, ws.yb, 2 * d.m, T, 2 * d.m, 1, st));
+    if (tp) DL_TRY(all_reduce(comm, ws.yb, static_cast<size_t>(T) * 2 * d.m, kNcclBfloat16, st));
+    DL_TRY(launch_silu_mul_bf16(ws.yb, 2 * d.m, ws.act, d.m, T, d.m, st));
+  }
+  DL_TRY(run_group(w->down, 1, h_rows, ws.act, d.m, d.m, T, skinny, ws, resid_out(), st));
+  DL_TRY(finish_residual(d.h));
+  return DL_OK;
+}
+// ---------------------------------------------------------------------------
+// model-level helpers
+// ---------------------------------------------------------------------------
+dl_status dl_embedding(const void* table, int64_t vocab, int64_t h, const int32_t* ids, int64_t T, void* out,
+                       void* stream) {
+  if (T == 0) return DL_OK;
+  DL_TRY(check_ptr(table, "table"));
+  DL_TRY(check_ptr(out, "out"));
+  if (!ids || h % 8 || vocab < 1) {
+    set_error("dl_embedding: bad arguments");
+    return DL_ERR_INVALID_ARG;
+  }
+  DL_TRY(check_device());
+  return launch_embedding(static_cast<const __nv_bfloat16*>(table), vocab, h, ids, T,
+                          static_cast<__nv_bfloat16*>(out), static_cast<cudaStream_t>(stream));
+}
+
+dl_status dl_rmsnorm(const void* x, const void* gamma, void* out, int64_t T, int64_t h, float eps, void* stream) {
+  if (T == 0) return DL_OK;
+  DL_TRY(check_ptr(x, "x"));
+  DL_TRY(check_ptr(gamma, "gamma"));
+  DL_TRY(check_ptr(out, "out"));
+  if (h % 8) {
+    set_error("h must be a multiple of 8");
+    return DL_ERR_ALIGN;
+  }
+  DL_TRY(check_device());
+  return launch_rmsnorm(static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(gamma),
+                        static_cast<__nv_bfloat16*>(out), T, h, eps, static_cast<cudaStream_t>(stream));
+}
+
+dl_status dl_dense_workspace(int64_t T, int64_t N, int64_t K, size_t* bytes) {
+  (void)T; (void)N; (void)K;
+  if (!bytes) return DL_ERR_INVALID_ARG;
+  *bytes = 0;
+  return DL_OK;
+}
+
+dl_status dl_dense(const void* X, int64_t ldx, const void* W, int64_t ldw, void* C, int64_t ldc, int64_t T,
+                   int64_t N, int64_t K, void* workspace, size_t workspace_bytes, void* stream) {
+  (void)workspace; (void)workspace_bytes;
+  if (T == 0) return DL_OK;
+  if (T < 0 || N <= 0 || K <= 0) {
+    set_error("dl_dense: bad shape");
+    return DL_ERR_SHAPE;
+  }
+  DL_TRY(check_ptr(X, "X"));
+  DL_TRY(check_ptr(W, "W"));
+  DL_TRY(check_ptr(C, "C"));
+  DL_TRY(check_ld(ldx, K, DL_BF16, "ldx"));
+  DL_TRY(check_ld(ldw, K, DL_BF16, "ldw"));
+  DL_TRY(check_ld(ldc, N, DL_BF16, "ldc"));
+  DL_TRY(check_device());
+  return tc_gemm(one_seg(X, ldx, T, K, W, ldw, N, K, out_plain(C, ldc, OUT_BF16, 0)), false,
+                 static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,133 @@
+// Internal interfaces between the C-ABI layer (api.cu) and the kernels.
+// Product code only: nothing here is shared with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "../../include/dl.h"
+
+namespace dl {
+
+void set_error(const char* fmt, ...);
+dl_status cuda_status(cudaError_t e, const char* what);
+
+constexpr int kNumSMsB200 = 148;
+int num_sms();
+
+// ---------------------------------------------------------------------------
+// tcgen05 GEMM family (tc_gemm.cu).
+//   C[token][feature] = sum_k act[token][act_koff + k] * W_seg[feature - begin][k]
+// act is bf16 row-major [T x Kact] (ld in elements); each segment's weight is
+// bf16 row-major [rows x klen] (K-major).  Tiles never straddle segments.
+// ---------------------------------------------------------------------------
+struct GemmSeg {
+  const void* w;      // [rows x klen] bf16 (may be null iff klen == 0)
+  int64_t ldw;        // elements
+  int64_t rows;       // features in this segment
+  int64_t klen;       // K extent of this segment (0 allowed -> zeros)
+  int64_t feat_begin; // first global output feature of the segment
+  int64_t act_koff;   // column offset of this segment's K range inside act
+};
+
+enum OutMode { OUT_BF16 = 0, OUT_F32_RED = 1, OUT_F32_STORE = 2 };
+
+struct GemmOut {
+  void* ptr;
+  int64_t ld;          // elements (row stride of [T x features] output)
+  int mode;            // OutMode
+  int accumulate;      // OUT_BF16 only: out = bf16(acc + out)
+  // reduce-scatter layout (P > 1): feature f of segment g goes to
+  //   owner = (f - begin_g) / rpr_g, col = slab_off_g + (f - begin_g) % rpr_g,
+  //   index = owner * T * slab + token * slab + col
+  int scatter_p;       // <= 1: plain [token][feature] with ld
+  int64_t slab;
+  int64_t seg_slab_off[3];
+  int64_t seg_rpr[3];
+  // plain layout only: remap_cols != 0 -> feature f of segment g is stored
+  // at column seg_col_off[g] + (f - begin_g) (else column f); the first
+  // seg_write_rows[g] (> rows: zero-padded) features of a segment are stored.
+  int remap_cols;
+  int64_t seg_col_off[3];
+  int64_t seg_write_rows[3];
+};
+
+struct GemmProblem {
+  const void* act; int64_t ld_act; int64_t T; int64_t k_act;  // act [T x k_act]
+  int nseg; GemmSeg seg[3];
+  int64_t n_feat;      // total output features (sum of seg rows)
+  GemmOut out;
+};
+
+// Picks the tile configuration (swap-AB for T <= 256, stream-K when the
+// output is fp32-reduced) and launches.  `stream_k` requires OUT_F32_RED.
+dl_status tc_gemm(const GemmProblem& p, bool stream_k, cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// SIMT skinny chain (simt_chain.cu): Y[T x m] (+)= (X B^T) A^T, T <= 16.
+// ---------------------------------------------------------------------------
+dl_status simt_lowrank(const void* X, int64_t ldx, const void* A, int64_t lda,
+                       const void* B, int64_t ldb, void* Y, int64_t ldy,
+                       int64_t T, int64_t m, int64_t n, int64_t k, dl_dtype dt,
+                       int accumulate, void* zbuf, cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// Elementwise (elementwise.cu); bf16 storage, fp32 math.
+// ---------------------------------------------------------------------------
+dl_status launch_rmsnorm(const __nv_bfloat16* x, const __nv_bfloat16* g,
+                         __nv_bfloat16* y, int64_t T, int64_t h, float eps,
+                         cudaStream_t st);
+// out_bf16[t][c] = bf16(acc[t][c]) ; acc zeroed afterwards (consume-and-clear)
+dl_status launch_f32_to_bf16(float* acc, int64_t ld_acc, __nv_bfloat16* out,
+                             int64_t ld_out, int64_t T, int64_t n, int clear,
+                             cudaStream_t st);
+// x[t][c] = bf16(x + acc) ; acc cleared
+dl_status launch_residual_add_f32(float* acc, int64_t ld_acc, __nv_bfloat16* x,
+                                  int64_t ldx, int64_t T, int64_t n,
+                                  int clear, cudaStream_t st);
+// x[t][c] = bf16(x + y)
+dl_status launch_residual_add_bf16(const __nv_bfloat16* y, int64_t ldy, __nv_bfloat16* x,
+                                   int64_t ldx, int64_t T, int64_t n, cudaStream_t st);
+// act[t][i] = bf16(silu(g) * u) with g = src[t][i], u = src[t][m + i]
+dl_status launch_silu_mul_f32(float* acc, int64_t ld_acc, __nv_bfloat16* act,
+                              int64_t ld_act, int64_t T, int64_t m, int clear,
+                              cudaStream_t st);
+dl_status launch_silu_mul_bf16(const __nv_bfloat16* src, int64_t ld_src,
+                               __nv_bfloat16* act, int64_t ld_act, int64_t T,
+                               int64_t m, cudaStream_t st);
+// q|k|v local rows [T x (Hq + 2 Hk) * d] (fp32 acc or bf16): RoPE on q, k;
+// q written (bf16) to q_out [T x Hq*d]; k, v appended to the cache at
+// position cache_lens[seq(t)] + (t - cu[seq]).
+struct RopeCacheArgs {
+  const float* acc; const __nv_bfloat16* src; int64_t ld_src; int clear;
+  __nv_bfloat16* q_out;
+  __nv_bfloat16* k_cache; __nv_bfloat16* v_cache; int64_t max_seq;
+  const int32_t* positions; const int32_t* cu_seqlens; const int32_t* cache_lens;
+  int32_t num_seqs; int decode;
+  int64_t T; int Hq, Hk, d; float theta;
+};
+dl_status launch_rope_cache(const RopeCacheArgs& a, cudaStream_t st);
+dl_status launch_embedding(const __nv_bfloat16* table, int64_t vocab, int64_t h,
+                           const int32_t* ids, int64_t T, __nv_bfloat16* out,
+                           cudaStream_t st);
+// [P][T][w] -> [T][P*w]
+dl_status launch_unpermute(const __nv_bfloat16* src, __nv_bfloat16* dst,
+                           int P, int64_t T, int64_t w, cudaStream_t st);
+dl_status launch_copy2d(const void* src, int64_t lds, void* dst, int64_t ldd,
+                        int64_t rows, int64_t cols_bytes, cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// Attention (attention.cu).  Cache layout [S][Hk][max_seq][d] bf16.
+// q [T x Hq*d] bf16 (post-RoPE), out [T x Hq*d] bf16.
+// ---------------------------------------------------------------------------
+struct AttnArgs {
+  const __nv_bfloat16* q; __nv_bfloat16* out;
+  const __nv_bfloat16* k_cache; const __nv_bfloat16* v_cache; int64_t max_seq;
+  const int32_t* cu_seqlens; const int32_t* cache_lens; int32_t num_seqs;
+  int64_t T; int Hq, Hk, d; int decode;
+  float* partial; size_t partial_bytes;   // split-KV scratch (decode)
+};
+dl_status launch_attention(const AttnArgs& a, cudaStream_t st);
+size_t attention_workspace(int64_t max_tokens, int Hq, int d);
+
+}  // namespace dl

@@ -1,0 +1,284 @@
+// Memory-bound block pieces (bf16 storage, fp32 math), each one pass over
+// its tensors with 16-byte vector accesses:
+//   RMSNorm (LLaMA-3 pre-norm; reading c9), the epilogues that turn the fp32
+//   rank-partial accumulators into the next operand (consume-and-clear: the
+//   accumulator is zeroed as it is read so the next stream-K GEMM can
+//   red.add into it without a separate memset), SiLU(gate)*up, residual add,
+//   RoPE + KV-cache append ("in-place rotary position
+//   embedding"), embedding gather and the all-gather un-permute.
+#include <math.h>
+
+#include "dl_internal.h"
+
+namespace dl {
+namespace {
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// one CTA (256 threads) per row; h % 8 == 0
+__global__ void __launch_bounds__(256) rmsnorm_kernel(const __nv_bfloat16* __restrict__ x,
+                                                      const __nv_bfloat16* __restrict__ g,
+                                                      __nv_bfloat16* __restrict__ y, int h, float eps) {
+  __shared__ float red[8];
+  const int64_t t = blockIdx.x;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + t * h);
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < h / 8; i += blockDim.x) {
+    uint4 v = xr[i];
+    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float2 f = __bfloat1622float2(b[e]);
+      ss += f.x * f.x + f.y * f.y;
+    }
+  }
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float inv = rsqrtf(red[0] / static_cast<float>(h) + eps);
+  const uint4* gr = reinterpret_cast<const uint4*>(g);
+  uint4* yr = reinterpret_cast<uint4*>(y + t * h);
+  for (int i = threadIdx.x; i < h / 8; i += blockDim.x) {
+    uint4 v = xr[i], gv = gr[i], o;
+    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v);
+    const __nv_bfloat162* gb = reinterpret_cast<const __nv_bfloat162*>(&gv);
+    __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float2 f = __bfloat1622float2(b[e]);
+      float2 w = __bfloat1622float2(gb[e]);
+      ob[e] = __floats2bfloat162_rn(f.x * inv * w.x, f.y * inv * w.y);
+    }
+    yr[i] = o;
+  }
+}
+
+// Generic 2-D elementwise over [T x n] in groups of 4 columns (n % 4 == 0).
+template <typename F>
+__global__ void ew4_kernel(int64_t T, int64_t n4, F f) {
+  const int64_t total = T * n4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = i / n4;
+    const int64_t c = (i - t * n4) * 4;
+    f(t, c);
+  }
+}
+
+template <typename F>
+dl_status launch_ew4(int64_t T, int64_t n, F f, cudaStream_t st, const char* what) {
+  if (T <= 0 || n <= 0) return DL_OK;
+  const int64_t n4 = n / 4;
+  const int64_t total = T * n4;
+  int64_t blocks = (total + 255) / 256;
+  const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
+  if (blocks > cap) blocks = cap;
+  ew4_kernel<<<static_cast<int>(blocks), 256, 0, st>>>(T, n4, f);
+  return cuda_status(cudaGetLastError(), what);
+}
+
+__device__ __forceinline__ float4 take4(float* p, int clear) {
+  float4 v = *reinterpret_cast<float4*>(p);
+  if (clear) *reinterpret_cast<float4*>(p) = make_float4(0.f, 0.f, 0.f, 0.f);
+  return v;
+}
+__device__ __forceinline__ void store4(__nv_bfloat16* p, float a, float b, float c, float d) {
+  uint2 o;
+  reinterpret_cast<__nv_bfloat162*>(&o)[0] = __floats2bfloat162_rn(a, b);
+  reinterpret_cast<__nv_bfloat162*>(&o)[1] = __floats2bfloat162_rn(c, d);
+  *reinterpret_cast<uint2*>(p) = o;
+}
+__device__ __forceinline__ float4 load4(const __nv_bfloat16* p) {
+  uint2 v = *reinterpret_cast<const uint2*>(p);
+  float2 a = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(&v)[0]);
+  float2 b = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(&v)[1]);
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+__device__ __forceinline__ float silu(float g) { return g / (1.f + __expf(-g)); }
+
+struct F32ToBf16 {
+  float* acc; int64_t lda; __nv_bfloat16* out; int64_t ldo; int clear;
+  __device__ void operator()(int64_t t, int64_t c) const {
+    float4 v = take4(acc + t * lda + c, clear);
+    store4(out + t * ldo + c, v.x, v.y, v.z, v.w);
+  }
+};
+struct ResidualAdd {
+  float* acc; int64_t lda; __nv_bfloat16* x; int64_t ldx; int clear;
+  __device__ void operator()(int64_t t, int64_t c) const {
+    float4 v = take4(acc + t * lda + c, clear);
+    float4 r = load4(x + t * ldx + c);
+    store4(x + t * ldx + c, r.x + v.x, r.y + v.y, r.z + v.z, r.w + v.w);
+  }
+};
+struct ResidualAddBf16 {
+  const __nv_bfloat16* y; int64_t ldy; __nv_bfloat16* x; int64_t ldx;
+  __device__ void operator()(int64_t t, int64_t c) const {
+    float4 v = load4(y + t * ldy + c);
+    float4 r = load4(x + t * ldx + c);
+    store4(x + t * ldx + c, r.x + v.x, r.y + v.y, r.z + v.z, r.w + v.w);
+  }
+};
+struct SiluMulF32 {
+  float* acc; int64_t lda; __nv_bfloat16* out; int64_t ldo; int64_t m; int clear;
+  __device__ void operator()(int64_t t, int64_t c) const {
+    float4 g = take4(acc + t * lda + c, clear);
+    float4 u = take4(acc + t * lda + m + c, clear);
+    store4(out + t * ldo + c, silu(g.x) * u.x, silu(g.y) * u.y, silu(g.z) * u.z, silu(g.w) * u.w);
+  }
+};
+struct SiluMulBf16 {
+  const __nv_bfloat16* src; int64_t lds; __nv_bfloat16* out; int64_t ldo; int64_t m;
+  __device__ void operator()(int64_t t, int64_t c) const {
+    float4 g = load4(src + t * lds + c);
+    float4 u = load4(src + t * lds + m + c);
+    store4(out + t * ldo + c, silu(g.x) * u.x, silu(g.y) * u.y, silu(g.z) * u.z, silu(g.w) * u.w);
+  }
+};
+
+// RoPE + cache append.  One thread per (token, head, 2 pairs).
+__global__ void rope_cache_kernel(RopeCacheArgs a) {
+  const int heads = a.Hq + 2 * a.Hk;
+  const int quads = a.d / 4;
+  const int64_t total = a.T * heads * quads;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = i / (heads * quads);
+    const int rem = static_cast<int>(i - t * heads * quads);
+    const int hd = rem / quads;
+    const int e = (rem - hd * quads) * 4;   // first of 4 dims = pairs (e, e+1), (e+2, e+3)
+    const int64_t col = static_cast<int64_t>(hd) * a.d + e;
+    float4 v;
+    if (a.acc) {
+      v = take4(const_cast<float*>(a.acc) + t * a.ld_src + col, a.clear);
+    } else {
+      v = load4(a.src + t * a.ld_src + col);
+    }
+    if (hd < a.Hq + a.Hk) {   // rotate q and k (pair (2i, 2i+1) by pos * theta^(-2i/d))
+      const double pos = static_cast<double>(a.positions[t]);
+      const double lt = log(static_cast<double>(a.theta));
+      double s0, c0, s1, c1;
+      sincos(pos * exp(-lt * static_cast<double>(e) / a.d), &s0, &c0);
+      sincos(pos * exp(-lt * static_cast<double>(e + 2) / a.d), &s1, &c1);
+      const float cs0 = static_cast<float>(c0), sn0 = static_cast<float>(s0);
+      const float cs1 = static_cast<float>(c1), sn1 = static_cast<float>(s1);
+      v = make_float4(v.x * cs0 - v.y * sn0, v.x * sn0 + v.y * cs0, v.z * cs1 - v.w * sn1, v.z * sn1 + v.w * cs1);
+    }
+    if (hd < a.Hq) {
+      store4(a.q_out + t * static_cast<int64_t>(a.Hq) * a.d + col, v.x, v.y, v.z, v.w);
+    } else {
+      int s;
+      int64_t cpos;
+      if (a.decode) {
+        s = static_cast<int>(t);
+        cpos = a.cache_lens[s];
+      } else {
+        int lo = 0, hi = a.num_seqs - 1;   // last s with cu[s] <= t
+        while (lo < hi) {
+          int mid = (lo + hi + 1) >> 1;
+          if (a.cu_seqlens[mid] <= t) lo = mid; else hi = mid - 1;
+        }
+        s = lo;
+        cpos = a.cache_lens[s] + (t - a.cu_seqlens[s]);
+      }
+      const bool is_k = hd < a.Hq + a.Hk;
+      const int kvh = is_k ? hd - a.Hq : hd - a.Hq - a.Hk;
+      __nv_bfloat16* dst = (is_k ? a.k_cache : a.v_cache) +
+                           ((static_cast<int64_t>(s) * a.Hk + kvh) * a.max_seq + cpos) * a.d + e;
+      store4(dst, v.x, v.y, v.z, v.w);
+    }
+  }
+}
+
+__global__ void embedding_kernel(const __nv_bfloat16* __restrict__ table, int64_t h, const int32_t* __restrict__ ids,
+                                 __nv_bfloat16* __restrict__ out) {
+  const int64_t t = blockIdx.x;
+  const uint4* src = reinterpret_cast<const uint4*>(table + static_cast<int64_t>(ids[t]) * h);
+  uint4* dst = reinterpret_cast<uint4*>(out + t * h);
+  for (int i = threadIdx.x; i < h / 8; i += blockDim.x) dst[i] = src[i];
+}
+
+__global__ void unpermute_kernel(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dst, int P,
+                                 int64_t T, int64_t w8) {
+  const int64_t total = static_cast<int64_t>(P) * T * w8;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t p = i / (T * w8);
+    const int64_t r = i - p * T * w8;
+    const int64_t t = r / w8;
+    const int64_t c = r - t * w8;
+    reinterpret_cast<uint4*>(dst)[t * P * w8 + p * w8 + c] = reinterpret_cast<const uint4*>(src)[i];
+  }
+}
+
+}  // namespace
+
+dl_status launch_rmsnorm(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bfloat16* y, int64_t T, int64_t h,
+                         float eps, cudaStream_t st) {
+  if (T <= 0) return DL_OK;
+  rmsnorm_kernel<<<static_cast<int>(T), 256, 0, st>>>(x, g, y, static_cast<int>(h), eps);
+  return cuda_status(cudaGetLastError(), "rmsnorm");
+}
+dl_status launch_f32_to_bf16(float* acc, int64_t lda, __nv_bfloat16* out, int64_t ldo, int64_t T, int64_t n,
+                             int clear, cudaStream_t st) {
+  return launch_ew4(T, n, F32ToBf16{acc, lda, out, ldo, clear}, st, "f32_to_bf16");
+}
+dl_status launch_residual_add_f32(float* acc, int64_t lda, __nv_bfloat16* x, int64_t ldx, int64_t T, int64_t n,
+                                  int clear, cudaStream_t st) {
+  return launch_ew4(T, n, ResidualAdd{acc, lda, x, ldx, clear}, st, "residual_add");
+}
+dl_status launch_residual_add_bf16(const __nv_bfloat16* y, int64_t ldy, __nv_bfloat16* x, int64_t ldx, int64_t T,
+                                   int64_t n, cudaStream_t st) {
+  return launch_ew4(T, n, ResidualAddBf16{y, ldy, x, ldx}, st, "residual_add_bf16");
+}
+dl_status launch_silu_mul_f32(float* acc, int64_t lda, __nv_bfloat16* act, int64_t ldo, int64_t T, int64_t m,
+                              int clear, cudaStream_t st) {
+  return launch_ew4(T, m, SiluMulF32{acc, lda, act, ldo, m, clear}, st, "silu_mul_f32");
+}
+dl_status launch_silu_mul_bf16(const __nv_bfloat16* src, int64_t lds, __nv_bfloat16* act, int64_t ldo, int64_t T,
+                               int64_t m, cudaStream_t st) {
+  return launch_ew4(T, m, SiluMulBf16{src, lds, act, ldo, m}, st, "silu_mul_bf16");
+}
+dl_status launch_rope_cache(const RopeCacheArgs& a, cudaStream_t st) {
+  if (a.T <= 0) return DL_OK;
+  const int64_t total = a.T * (a.Hq + 2 * a.Hk) * (a.d / 4);
+  int64_t blocks = (total + 255) / 256;
+  const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
+  if (blocks > cap) blocks = cap;
+  rope_cache_kernel<<<static_cast<int>(blocks), 256, 0, st>>>(a);
+  return cuda_status(cudaGetLastError(), "rope_cache");
+}
+dl_status launch_embedding(const __nv_bfloat16* table, int64_t vocab, int64_t h, const int32_t* ids, int64_t T,
+                           __nv_bfloat16* out, cudaStream_t st) {
+  (void)vocab;
+  if (T <= 0) return DL_OK;
+  embedding_kernel<<<static_cast<int>(T), 256, 0, st>>>(table, h, ids, out);
+  return cuda_status(cudaGetLastError(), "embedding");
+}
+dl_status launch_unpermute(const __nv_bfloat16* src, __nv_bfloat16* dst, int P, int64_t T, int64_t w,
+                           cudaStream_t st) {
+  if (T <= 0) return DL_OK;
+  const int64_t total = static_cast<int64_t>(P) * T * (w / 8);
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 4096) blocks = 4096;
+  unpermute_kernel<<<static_cast<int>(blocks), 256, 0, st>>>(src, dst, P, T, w / 8);
+  return cuda_status(cudaGetLastError(), "unpermute");
+}
+dl_status launch_copy2d(const void* src, int64_t lds, void* dst, int64_t ldd, int64_t rows, int64_t cols_bytes,
+                        cudaStream_t st) {
+  if (rows <= 0 || cols_bytes <= 0) return DL_OK;
+  return cuda_status(cudaMemcpy2DAsync(dst, ldd, src, lds, cols_bytes, rows, cudaMemcpyDeviceToDevice, st),
+                     "copy2d");
+}
+
+}  // namespace dl

@@ -1,0 +1,479 @@
+// tcgen05 / TMEM / TMA GEMM family for the two stages of the low-rank chain
+// y = A (B x)  (Section 2.1, Eq. 1):
+//
+//   stage 1  Z[T x k] = X[T x n] . B[k x n]^T      (downward projection x_v)
+//   stage 2  Y[T x m] = Z[T x k] . A_g[m_g x k_g]^T (upward projection x_u,
+//            grouped: each output segment g reads its own K range of Z)
+//
+// Both operands are K-major (row-major activations, row-major A and B), the
+// layout tcgen05.mma consumes directly from 128B-swizzled shared memory.
+//
+// One persistent, warp-specialised kernel (1 CTA / SM, 192 threads):
+//   warp 0      TMA producer: STAGES-deep smem ring (full/empty mbarriers)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> global
+// The fp32 accumulator is double-buffered in TMEM (2 x BN columns) so the
+// epilogue of job i overlaps the main loop of job i+1.
+//
+// Orientation:
+//   SWAP = false (prefill, T > 256): MMA M = 128 tokens, N = BN features.
+//   SWAP = true  (decode, T <= 256): "swap-AB": MMA M = 128 weight rows
+//                (features), N = BN >= T tokens.  The weights are the
+//                streamed operand; tokens ride along as the narrow N.
+// Work split:
+//   whole-tile  : tiles dealt round-robin to CTAs, output written once
+//                 (bf16, optional fused "+= out" residual).
+//   stream-K    : the (tile, k-block) iteration space is cut into equal
+//                 contiguous ranges, one per CTA (one wave, perfect balance
+//                 for the memory-bound decode); partial tiles are reduced
+//                 with red.global.add.f32 into a zeroed fp32 buffer.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <stdio.h>
+
+#include <mutex>
+
+#include "dl_internal.h"
+#include "sm100_ptx.cuh"
+
+namespace dl {
+namespace {
+
+constexpr int BK = 64;   // K elements per stage = one 128-byte swizzle row
+constexpr int BM = 128;  // MMA M = TMEM lanes
+constexpr int kThreads = 192;
+
+struct KSeg {
+  int feat_begin, feat_end;  // global output features [begin, end)
+  int act_koff;              // K offset of this segment inside the activation
+  int nkb;                   // k-blocks (ceil(klen / 64))
+  int tile_first;            // first global tile index of the segment
+  int ntiles;                // tiles in the segment (feature tiles * token tiles)
+  long long unit_first;      // stream-K: first unit (tile, kb) of the segment
+  long long slab_off, rpr;   // reduce-scatter layout
+  int write_end;             // features < write_end are stored (>= feat_end: zeros)
+  long long col_off;         // plain layout: column of feature feat_begin
+};
+
+struct KArgs {
+  int T;
+  int tiles_tok;
+  int nseg;
+  KSeg seg[3];
+  int total_tiles;
+  long long total_units;
+  int stream_k;
+  void* out;
+  long long ldo;
+  int mode;
+  int accumulate;
+  int scatter_p;
+  long long slab;
+};
+
+struct __align__(64) KMaps {
+  CUtensorMap act;
+  CUtensorMap w[3];
+};
+
+struct Job {
+  int seg, feat0, tok0, kb0, kb1;
+};
+
+// Job enumeration shared by the three roles (pure function of blockIdx).
+struct JobIter {
+  const KArgs& a;
+  int cta, grid;
+  int next_tile;            // whole-tile mode
+  long long u, u_end;       // stream-K mode
+  __device__ JobIter(const KArgs& args, int c, int g) : a(args), cta(c), grid(g) {
+    next_tile = c;
+    if (a.stream_k) {
+      u = (a.total_units * c) / g;
+      u_end = (a.total_units * (c + 1)) / g;
+    } else {
+      u = u_end = 0;
+    }
+  }
+  __device__ bool next(Job& j, int FEAT_TILE, int TOK_TILE) {
+    if (!a.stream_k) {
+      if (next_tile >= a.total_tiles) return false;
+      int t = next_tile;
+      next_tile += grid;
+      int g = 0;
+      while (g + 1 < a.nseg && t >= a.seg[g + 1].tile_first) ++g;
+      int local = t - a.seg[g].tile_first;
+      j.seg = g;
+      j.feat0 = a.seg[g].feat_begin + (local / a.tiles_tok) * FEAT_TILE;
+      j.tok0 = (local % a.tiles_tok) * TOK_TILE;
+      j.kb0 = 0;
+      j.kb1 = a.seg[g].nkb;
+      return true;
+    }
+    while (u < u_end) {
+      int g = 0;
+      while (g + 1 < a.nseg && u >= a.seg[g + 1].unit_first) ++g;
+      const KSeg& s = a.seg[g];
+      if (s.nkb == 0) { u = (g + 1 < a.nseg) ? a.seg[g + 1].unit_first : u_end; continue; }
+      long long local = u - s.unit_first;
+      int tile = static_cast<int>(local / s.nkb);
+      int kb0 = static_cast<int>(local % s.nkb);
+      long long rem = u_end - u;
+      int kb1 = static_cast<int>(kb0 + rem < s.nkb ? kb0 + rem : s.nkb);
+      j.seg = g;
+      j.feat0 = s.feat_begin + (tile / a.tiles_tok) * FEAT_TILE;
+      j.tok0 = (tile % a.tiles_tok) * TOK_TILE;
+      j.kb0 = kb0;
+      j.kb1 = kb1;
+      u += kb1 - kb0;
+      return true;
+    }
+    return false;
+  }
+};
+
+__device__ __forceinline__ long long out_index(const KArgs& a, const KSeg& s, int tok, int f) {
+  if (a.scatter_p <= 1) return static_cast<long long>(tok) * a.ldo + s.col_off + (f - s.feat_begin);
+  long long loc = f - s.feat_begin;
+  long long owner = loc / s.rpr;
+  long long col = s.slab_off + loc % s.rpr;
+  return owner * static_cast<long long>(a.T) * a.slab + static_cast<long long>(tok) * a.slab + col;
+}
+
+template <int BN, bool SWAP, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_gemm_kernel(const __grid_constant__ KMaps maps, const __grid_constant__ KArgs a) {
+  constexpr int P_ROWS = BM;                 // MMA A operand rows
+  constexpr int Q_ROWS = BN;                 // MMA B operand rows
+  constexpr int P_BYTES = P_ROWS * BK * 2;
+  constexpr int Q_BYTES = Q_ROWS * BK * 2;
+  constexpr int STAGE_BYTES = P_BYTES + Q_BYTES;
+  constexpr int FEAT_TILE = SWAP ? BM : BN;
+  constexpr int TOK_TILE = SWAP ? BN : BM;
+  constexpr uint32_t TMEM_COLS = 2 * BN;
+  constexpr uint32_t IDESC = ptx::idesc_bf16_f32(BM, BN);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full_bar[STAGES];
+  __shared__ __align__(8) uint64_t empty_bar[STAGES];
+  __shared__ __align__(8) uint64_t accf_bar[2];
+  __shared__ __align__(8) uint64_t acce_bar[2];
+  __shared__ uint32_t tmem_slot;
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&maps.act);
+    for (int g = 0; g < a.nseg; ++g) ptx::prefetch_tmap(&maps.w[g]);
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full_bar[s], 1);
+      ptx::mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&accf_bar[b], 1);
+      ptx::mbar_init(&acce_bar[b], 4);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<TMEM_COLS>(&tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = tmem_slot;
+
+  JobIter it(a, blockIdx.x, gridDim.x);
+  Job j;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      const uint64_t pol_w = ptx::policy_evict_first();   // weights: streamed once
+      const uint64_t pol_a = ptx::policy_evict_last();    // activations: re-read
+      int stage = 0;
+      uint32_t phase = 0;
+      while (it.next(j, FEAT_TILE, TOK_TILE)) {
+        const KSeg& s = a.seg[j.seg];
+        for (int kb = j.kb0; kb < j.kb1; ++kb) {
+          ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sp = smem + stage * STAGE_BYTES;
+          uint8_t* sq = sp + P_BYTES;
+          ptx::mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES);
+          const int kx = kb * BK;
+          if (SWAP) {
+            ptx::tma_load_2d(sp, &maps.w[j.seg], &full_bar[stage], kx, j.feat0 - s.feat_begin, pol_w);
+            ptx::tma_load_2d(sq, &maps.act, &full_bar[stage], s.act_koff + kx, j.tok0, pol_a);
+          } else {
+            ptx::tma_load_2d(sp, &maps.act, &full_bar[stage], s.act_koff + kx, j.tok0, pol_a);
+            ptx::tma_load_2d(sq, &maps.w[j.seg], &full_bar[stage], kx, j.feat0 - s.feat_begin, pol_w);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (one thread) =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      while (it.next(j, FEAT_TILE, TOK_TILE)) {
+        ptx::mbar_wait(&acce_bar[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = j.kb0; kb < j.kb1; ++kb) {
+          ptx::mbar_wait(&full_bar[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t sp = ptx::smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t sq = sp + P_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // advance 16 bf16 = 32 B along K inside the 128 B swizzle row
+            const uint64_t ad = ptx::sdesc_sw128(sp + k * 32);
+            const uint64_t bd = ptx::sdesc_sw128(sq + k * 32);
+            ptx::umma_bf16(d_tmem, ad, bd, IDESC, (kb > j.kb0 || k > 0) ? 1u : 0u);
+          }
+          ptx::umma_commit(&empty_bar[stage]);   // smem slot free once these MMAs retire
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        ptx::umma_commit(&accf_bar[acc]);        // accumulator ready for the epilogue
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // ===================== epilogue (warps 2..5) =====================
+    const int quarter = warp & 3;              // TMEM lane quarter this warp may access
+    const int row = quarter * 32 + lane;       // accumulator row (M index)
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    while (it.next(j, FEAT_TILE, TOK_TILE)) {
+      const KSeg& s = a.seg[j.seg];
+      ptx::mbar_wait(&accf_bar[acc], acc_phase);
+      ptx::tc_fence_after();
+      const bool has_k = j.kb1 > j.kb0;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        if (has_k) {
+          ptx::tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + c0, r);
+          ptx::tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = 0u;
+        }
+        if (SWAP) {
+          // row = feature, columns = tokens
+          const int f = j.feat0 + row;
+          if (f < s.write_end) {
+#pragma unroll 4
+            for (int i = 0; i < 32; ++i) {
+              const int tok = j.tok0 + c0 + i;
+              if (tok < a.T) {
+                const float v = __uint_as_float(r[i]);
+                const long long idx = out_index(a, s, tok, f);
+                if (a.mode == OUT_F32_RED) {
+                  ptx::red_add_f32(static_cast<float*>(a.out) + idx, v);
+                } else if (a.mode == OUT_F32_STORE) {
+                  static_cast<float*>(a.out)[idx] = v;
+                } else {
+                  __nv_bfloat16* o = static_cast<__nv_bfloat16*>(a.out) + idx;
+                  float w = v;
+                  if (a.accumulate) w += __bfloat162float(*o);
+                  *o = __float2bfloat16_rn(w);
+                }
+              }
+            }
+          }
+        } else {
+          // row = token, columns = features f0 .. f0+31 (same segment, same owner)
+          const int tok = j.tok0 + row;
+          const int f0 = j.feat0 + c0;
+          if (tok < a.T && f0 < s.write_end) {
+            const long long idx0 = out_index(a, s, tok, f0);
+            const bool full = (f0 + 32 <= s.write_end);
+            if (a.mode == OUT_BF16) {
+              __nv_bfloat16* o = static_cast<__nv_bfloat16*>(a.out) + idx0;
+              if (full && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  float v[8];
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r[q * 8 + e]);
+                  if (a.accumulate) {
+                    uint4 old = *reinterpret_cast<const uint4*>(o + q * 8);
+                    const __nv_bfloat162* ob = reinterpret_cast<const __nv_bfloat162*>(&old);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                      float2 f2 = __bfloat1622float2(ob[e]);
+                      v[2 * e] += f2.x;
+                      v[2 * e + 1] += f2.y;
+                    }
+                  }
+                  uint4 pk;
+                  __nv_bfloat162* pb = reinterpret_cast<__nv_bfloat162*>(&pk);
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) pb[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+                  *reinterpret_cast<uint4*>(o + q * 8) = pk;
+                }
+              } else {
+                for (int i = 0; i < 32 && f0 + i < s.write_end; ++i) {
+                  float w = __uint_as_float(r[i]);
+                  if (a.accumulate) w += __bfloat162float(o[i]);
+                  o[i] = __float2bfloat16_rn(w);
+                }
+              }
+            } else {
+              float* o = static_cast<float*>(a.out) + idx0;
+              for (int i = 0; i < 32; ++i) {
+                if (f0 + i >= s.write_end) break;
+                const float v = __uint_as_float(r[i]);
+                if (a.mode == OUT_F32_RED) ptx::red_add_f32(o + i, v);
+                else o[i] = v;
+              }
+            }
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&acce_bar[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  if (warp == 1) ptx::tmem_dealloc<TMEM_COLS>(tmem_base);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+bool get_encode() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return g_encode != nullptr;
+}
+
+// 2-D bf16 map over a row-major [rows x cols] matrix (ld elements), box
+// {64 cols, box_rows}, 128B swizzle, OOB elements read as zero.
+bool make_map(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(BK), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BN, bool SWAP, int STAGES>
+dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
+  constexpr int FEAT_TILE = SWAP ? BM : BN;
+  constexpr int TOK_TILE = SWAP ? BN : BM;
+  constexpr int SMEM = STAGES * (BM + BN) * BK * 2 + 1024;
+  static bool attr_set = false;
+  auto kern = tc_gemm_kernel<BN, SWAP, STAGES>;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(tc_gemm)");
+    attr_set = true;
+  }
+  KMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  KArgs a;
+  memset(&a, 0, sizeof(a));
+  a.T = static_cast<int>(p.T);
+  a.tiles_tok = static_cast<int>((p.T + TOK_TILE - 1) / TOK_TILE);
+  a.nseg = p.nseg;
+  int tiles = 0;
+  long long units = 0;
+  for (int g = 0; g < p.nseg; ++g) {
+    const GemmSeg& s = p.seg[g];
+    KSeg& k = a.seg[g];
+    k.feat_begin = static_cast<int>(s.feat_begin);
+    k.feat_end = static_cast<int>(s.feat_begin + s.rows);
+    k.act_koff = static_cast<int>(s.act_koff);
+    k.nkb = static_cast<int>((s.klen + BK - 1) / BK);
+    k.tile_first = tiles;
+    k.ntiles = static_cast<int>((s.rows + FEAT_TILE - 1) / FEAT_TILE) * a.tiles_tok;
+    k.unit_first = units;
+    k.slab_off = p.out.seg_slab_off[g];
+    k.rpr = p.out.seg_rpr[g] > 0 ? p.out.seg_rpr[g] : 1;
+    k.write_end = static_cast<int>(s.feat_begin + (p.out.seg_write_rows[g] > 0 ? p.out.seg_write_rows[g] : s.rows));
+    k.col_off = p.out.remap_cols ? p.out.seg_col_off[g] : s.feat_begin;
+    tiles += k.ntiles;
+    units += static_cast<long long>(k.ntiles) * k.nkb;
+    if (s.klen > 0 && s.rows > 0) {
+      if (!make_map(&maps.w[g], s.w, s.rows, s.klen, s.ldw, FEAT_TILE)) {
+        set_error("cuTensorMapEncodeTiled failed (weight segment %d)", g);
+        return DL_ERR_CUDA;
+      }
+    } else {
+      maps.w[g] = maps.w[0];
+    }
+  }
+  if (!make_map(&maps.act, p.act, p.T, p.k_act, p.ld_act, TOK_TILE)) {
+    set_error("cuTensorMapEncodeTiled failed (activation)");
+    return DL_ERR_CUDA;
+  }
+  a.total_tiles = tiles;
+  a.total_units = units;
+  a.stream_k = stream_k ? 1 : 0;
+  a.out = p.out.ptr;
+  a.ldo = p.out.ld;
+  a.mode = p.out.mode;
+  a.accumulate = p.out.accumulate;
+  a.scatter_p = p.out.scatter_p;
+  a.slab = p.out.slab;
+  const int sms = num_sms();
+  int grid;
+  if (stream_k) {
+    grid = static_cast<int>(units < sms ? (units > 0 ? units : 1) : sms);
+  } else {
+    grid = tiles < sms ? (tiles > 0 ? tiles : 1) : sms;
+  }
+  kern<<<grid, kThreads, SMEM, st>>>(maps, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("tc_gemm<BN=%d,swap=%d> (T=%lld k_act=%lld nseg=%d klen=%lld/%lld/%lld koff=%lld/%lld/%lld "
+              "grid=%d stream_k=%d): %s", BN, (int)SWAP, (long long)p.T, (long long)p.k_act, p.nseg,
+              (long long)p.seg[0].klen, (long long)p.seg[1].klen, (long long)p.seg[2].klen,
+              (long long)p.seg[0].act_koff, (long long)p.seg[1].act_koff, (long long)p.seg[2].act_koff, grid,
+              (int)stream_k, cudaGetErrorString(e));
+    return DL_ERR_CUDA;
+  }
+  return DL_OK;
+}
+
+}  // namespace
+
+dl_status tc_gemm(const GemmProblem& p, bool stream_k, cudaStream_t st) {
+  if (p.T <= 0) return DL_OK;
+  if (!get_encode()) {
+    set_error("cuTensorMapEncodeTiled unavailable (driver too old or no GPU)");
+    return DL_ERR_CUDA;
+  }
+  if (stream_k && p.out.mode != OUT_F32_RED) {
+    set_error("stream-K requires an fp32 reduction output");
+    return DL_ERR_INVALID_ARG;
+  }
+  if (p.T <= 64) return launch_cfg<64, true, 8>(p, stream_k, st);
+  if (p.T <= 128) return launch_cfg<128, true, 6>(p, stream_k, st);
+  if (p.T <= 256) return launch_cfg<256, true, 4>(p, stream_k, st);
+  return launch_cfg<256, false, 4>(p, stream_k, st);
+}
+
+}  // namespace dl

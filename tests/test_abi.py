@@ -1,0 +1,123 @@
+"""C-ABI checks that run without a GPU (-m "not gpu"):
+the library builds/loads, exports every symbol include/dl.h declares, the
+host-side planner agrees with the oracle's independent range computation,
+argument validation rejects bad calls before touching the device, and a
+valid compute call on a GPU-less host fails loudly (no CPU fallback).
+"""
+import ctypes
+import os
+import re
+
+import pytest
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2604_17709_b200 import build
+    build.build()
+    import paper_2604_17709_b200 as dl
+    dl.load()
+    return dl
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "dl.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(dl_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_exports_every_header_symbol(lib):
+    so = ctypes.CDLL(lib._lib.LIB_PATH)
+    names = header_functions()
+    assert len(names) >= 14
+    for n in names:
+        assert hasattr(so, n), f"libdl.so does not export {n}"
+    assert set(names) == set(lib.EXPORTS)
+
+
+def test_version(lib):
+    assert lib.dl_version() == 100
+
+
+@pytest.mark.parametrize("ranks", [[4916, 614, 614], [4916, 4916], [4916], [3277, 819, 819], [7, 5, 3], [64]])
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_plan_matches_oracle_concat_split(lib, orc, ranks, world):
+    """dl_tp_plan: concatenate the segment ranks, split evenly, map back."""
+    R = sum(ranks)
+    if R < world:
+        pytest.skip("R < world")
+    seen = [0] * R
+    for r in range(world):
+        beg, lens, kloc = lib.dl_tp_plan(ranks, world, r)
+        b0, l0, _ = orc.shard_range(R, world, r, 1)          # independent oracle plan
+        assert kloc == l0
+        off = 0
+        got = []
+        for g, rk in enumerate(ranks):
+            for j in range(lens[g]):
+                got.append(off + beg[g] + j)
+            off += rk
+        assert got == list(range(b0, b0 + l0))
+        for i in got:
+            seen[i] += 1
+    assert all(s == 1 for s in seen)
+
+
+def test_plan_70b_qkv_tp8(lib):
+    beg, lens, kloc = lib.dl_tp_plan([4916, 614, 614], 8, 6)
+    assert kloc == 768 and lens == [308, 460, 0] and beg[:2] == [4608, 0]
+    beg, lens, kloc = lib.dl_tp_plan([4916, 614, 614], 8, 7)
+    assert kloc == 768 and lens == [0, 154, 614] and beg[1:] == [460, 0]
+
+
+def test_plan_strict_rejects_uneven(lib):
+    with pytest.raises(lib.DLError) as e:
+        lib.dl_tp_plan([614], 8, 0, strict=True)
+    assert e.value.name == "DL_ERR_PARTITION"
+    with pytest.raises(lib.DLError):
+        lib.dl_tp_plan([3], 4, 0)          # fewer ranks than world
+
+
+def _call_linear(lib, T=4, m=256, n=256, k=64, ldx=256, lda=64, ldb=256, ldy=256, dt=0, X=256, ws=1 << 20):
+    L = lib.load()
+    return L.dl_lowrank_linear(ctypes.c_void_p(X), ldx, ctypes.c_void_p(4096), lda, ctypes.c_void_p(8192), ldb,
+                               ctypes.c_void_p(16384), ldy, T, m, n, k, dt, 0, None, ctypes.c_void_p(65536), ws, None)
+
+
+def test_linear_validation_codes(lib):
+    assert _call_linear(lib, k=0) == 3            # DL_ERR_RANK
+    assert _call_linear(lib, k=300) == 3          # k > min(m, n)
+    assert _call_linear(lib, m=0) == 2            # DL_ERR_SHAPE
+    assert _call_linear(lib, ldx=100) == 2        # ld < row
+    assert _call_linear(lib, X=8) == 6            # DL_ERR_ALIGN (pointer)
+    assert _call_linear(lib, lda=66) == 6         # ld not 16-byte multiple (fp32)
+    assert _call_linear(lib, T=32, dt=0) == 5     # fp32 beyond the SIMT path
+    assert _call_linear(lib, ws=16) == 7          # DL_ERR_WORKSPACE
+    assert _call_linear(lib, T=0) == 0            # empty input is a no-op
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the GPU-less failure mode")
+def test_no_cpu_fallback(lib):
+    """A valid call on a host without an sm_100 GPU must fail loudly."""
+    assert _call_linear(lib) == 8                 # DL_ERR_CUDA
+    assert "device" in lib.load().dl_last_error().decode().lower() or \
+        "cuda" in lib.load().dl_last_error().decode().lower()
+    assert not lib.dl_device_ok()
+
+
+def test_block_workspace_and_validation(lib):
+    from synthetic import LLAMA3_70B, block_ranks
+    rk = block_ranks(LLAMA3_70B, 0.4)
+    cfg = lib.make_block_config(LLAMA3_70B, rk, max_tokens=64, max_seqs=64)
+    for world in (1, 2, 4, 8):
+        assert lib.dl_block_workspace(cfg, world) > 0
+    with pytest.raises(lib.DLError) as e:
+        lib.dl_block_workspace(cfg, 16)           # 8 kv heads do not split 16 ways
+    assert e.value.name == "DL_ERR_PARTITION"
+    bad = lib.make_block_config(LLAMA3_70B, dict(rk, q=9000), max_tokens=64, max_seqs=64)
+    with pytest.raises(lib.DLError) as e:
+        lib.dl_block_workspace(bad, 1)
+    assert e.value.name == "DL_ERR_RANK"

@@ -1,0 +1,236 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle, element by
+element on the same seeded inputs.  Tolerances (north_star): relative L2
+<= 2e-2 for bf16, <= 1e-5 for fp32.  Block outputs are compared on the
+block's contribution x_out - x_in (stricter than comparing x_out).
+"""
+import numpy as np
+import pytest
+import torch
+
+from synthetic import LLAMA3_8B, ModelShape, block_ranks, gen_block_weights, gen_factor_pair, gen_normal
+
+pytestmark = pytest.mark.gpu
+
+TOL_BF16 = 2e-2
+TOL_F32 = 1e-5
+
+
+def rel(a, b):
+    a, b = (t.detach().cpu().double().numpy() if isinstance(t, torch.Tensor) else t for t in (a, b))
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def dl():
+    import paper_2604_17709_b200 as dl
+    from paper_2604_17709_b200 import build
+    build.build()
+    dl.load()
+    assert dl.dl_device_ok(), "needs an sm_100 GPU"
+    return dl
+
+
+def _lin_inputs(T, m, n, k, dtype, seed):
+    X = gen_normal((T, n), 1.0, seed, dtype=dtype)
+    A, B = gen_factor_pair(m, n, k, seed + 7, dtype=dtype)
+    return X, A, B
+
+
+# ---- dl_lowrank_linear --------------------------------------------------------
+def test_linear_config1_fp32(dl, orc):
+    """BASELINE config 1: m=n=256, k=64, T=4, fp32 vs CPU oracle (1e-5)."""
+    X, A, B = _lin_inputs(4, 256, 256, 64, torch.float32, 1)
+    Y = torch.empty(4, 256, device="cuda")
+    dl.dl_lowrank_linear(X.cuda(), A.cuda(), B.cuda(), Y)
+    torch.cuda.synchronize()
+    assert rel(Y.cpu(), orc.lowrank_linear(X, A, B)) <= TOL_F32
+
+
+@pytest.mark.parametrize("T", [1, 3, 16])
+def test_linear_fp32_simt_large(dl, orc, T):
+    """fp32 SIMT chain at a size that takes the two-kernel path (k > 1024 is not needed: (m+n)k > 64K)."""
+    X, A, B = _lin_inputs(T, 1000, 520, 300, torch.float32, 2 + T)
+    Y = torch.empty(T, 1000, device="cuda")
+    dl.dl_lowrank_linear(X.cuda(), A.cuda(), B.cuda(), Y)
+    torch.cuda.synchronize()
+    assert rel(Y.cpu(), orc.lowrank_linear(X, A, B)) <= TOL_F32
+
+
+@pytest.mark.parametrize("T", [1, 5, 16, 17, 64, 100, 256, 257, 300, 1000])
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_linear_bf16_paths(dl, orc, T, accumulate):
+    """SIMT (T<=16), swap-AB stream-K (17..256) and wide whole-tile (>256) paths.
+    m spans 5 M-tiles, n and k are ragged (not multiples of the 64-wide K block)."""
+    m, n, k = 640, 520, 200
+    X, A, B = _lin_inputs(T, m, n, k, torch.bfloat16, 10 + T)
+    Y0 = gen_normal((T, m), 1.0, 99, dtype=torch.bfloat16)
+    Y = Y0.clone().cuda()
+    dl.dl_lowrank_linear(X.cuda(), A.cuda(), B.cuda(), Y, accumulate=accumulate)
+    torch.cuda.synchronize()
+    ref = orc.lowrank_linear(X, A, B)
+    got = Y.cpu().double().numpy()
+    if accumulate:
+        got = got - Y0.double().numpy()
+    assert rel(got, ref) <= TOL_BF16
+
+
+def test_linear_bf16_large_shapes(dl, orc):
+    """70B o-projection shape (n=m=8192, k=4916) at decode batch 64, sampled via all rows (oracle is fast here)."""
+    T, m, n, k = 64, 8192, 8192, 4916
+    X, A, B = _lin_inputs(T, m, n, k, torch.bfloat16, 5)
+    Y = torch.empty(T, m, dtype=torch.bfloat16, device="cuda")
+    A_pad = torch.zeros(m, 4920, dtype=torch.bfloat16, device="cuda")   # ld must be a 16-byte multiple
+    A_pad[:, :k] = A.cuda()
+    dl.dl_lowrank_linear(X.cuda(), A_pad[:, :k], B.cuda(), Y)
+    torch.cuda.synchronize()
+    rows = [0, 17, 63]
+    ref = orc.lowrank_linear(X[rows], A, B)
+    assert rel(Y.cpu()[rows], ref) <= TOL_BF16
+
+
+def test_dense_lm_head_shape(dl):
+    """dl_dense (used for the LM head) vs a float64 torch matmul of the same bf16 values."""
+    T, N, K = 64, 1000, 512
+    X = gen_normal((T, K), 1.0, 3, dtype=torch.bfloat16)
+    W = gen_normal((N, K), K ** -0.5, 4, dtype=torch.bfloat16)
+    C = torch.empty(T, N, dtype=torch.bfloat16, device="cuda")
+    dl.dl_dense(X.cuda(), W.cuda(), C)
+    torch.cuda.synchronize()
+    ref = X.double() @ W.double().T
+    assert rel(C.cpu(), ref) <= TOL_BF16
+
+
+# ---- decomposed block ------------------------------------------------------------
+SMALL = ModelShape("small", h=512, n_heads=4, n_kv_heads=2, head_dim=128, m=1024, n_layers=1, vocab=1000,
+                   rope_theta=500000.0)
+
+
+def _oracle_cfg(orc, s, rk):
+    return orc.BlockCfg(s.h, s.n_heads, s.n_kv_heads, s.head_dim, s.m, rk["q"], rk["k"], rk["v"], rk["o"],
+                        rk["gate"], rk["up"], rk["down"], rope_theta=s.rope_theta, rms_eps=s.rms_eps)
+
+
+def _cache_to_oracle(c, S, L):
+    # GPU [S, Hk, max_seq, d] -> oracle [S, max_seq, Hk*d]
+    return c[:S].permute(0, 2, 1, 3).reshape(S, c.shape[2], -1)[:, :L].cpu()
+
+
+def _run_prefill(dl, orc, s, ratio, lens, seed):
+    rk = block_ranks(s, ratio)
+    w = gen_block_weights(s, rk, 0, seed)
+    T = sum(lens)
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    pos = np.concatenate([np.arange(L) for L in lens]).astype(np.int32)
+    x = gen_normal((T, s.h), 1.0, seed + 100, dtype=torch.bfloat16)
+    max_seq = max(lens) + 8
+    cfg = dl.make_block_config(s, rk, max_tokens=T, max_seqs=len(lens))
+    wdev = dl.BlockWeights({k: v.cuda() for k, v in w.items()})
+    ws = torch.zeros(dl.dl_block_workspace(cfg), dtype=torch.uint8, device="cuda")
+    kc = torch.zeros(len(lens), s.n_kv_heads, max_seq, s.head_dim, dtype=torch.bfloat16, device="cuda")
+    vc = torch.zeros_like(kc)
+    xd = x.cuda()
+    dl.dl_decomposed_block_forward(cfg, wdev, xd, torch.from_numpy(pos).cuda(), torch.from_numpy(cu).cuda(),
+                                   len(lens), dl.DL_PREFILL, kc, vc, torch.zeros(len(lens), dtype=torch.int32,
+                                                                                  device="cuda"), None, ws)
+    torch.cuda.synchronize()
+    return w, rk, x, xd.cpu(), pos, cu, kc, vc
+
+
+@pytest.mark.parametrize("lens", [[100], [60, 1, 39], [300], [129, 200, 71]])
+def test_block_prefill_small(dl, orc, lens):
+    s = SMALL
+    w, rk, x, xo, pos, cu, kc, vc = _run_prefill(dl, orc, s, 0.4, lens, seed=len(lens) * 7 + lens[0])
+    ref, rk_, rv_ = orc.block_prefill(_oracle_cfg(orc, s, rk), w, x, pos, cu)
+    assert rel(xo.double() - x.double(), ref - x.double().numpy()) <= TOL_BF16
+    # KV cache written by the kernel == oracle's post-RoPE keys / values
+    for si in range(len(lens)):
+        a, b = cu[si], cu[si + 1]
+        kg = kc[si, :, :b - a].permute(1, 0, 2).reshape(b - a, -1).cpu()
+        vg = vc[si, :, :b - a].permute(1, 0, 2).reshape(b - a, -1).cpu()
+        assert rel(kg, rk_[a:b]) <= TOL_BF16
+        assert rel(vg, rv_[a:b]) <= TOL_BF16
+
+
+@pytest.mark.parametrize("cache_lens", [[0, 5, 17, 1, 33, 2, 7, 100], [511] * 4])
+def test_block_decode_small(dl, orc, cache_lens):
+    s = SMALL
+    rk = block_ranks(s, 0.4)
+    w = gen_block_weights(s, rk, 0, 3)
+    S = len(cache_lens)
+    max_seq = max(cache_lens) + 1
+    x = gen_normal((S, s.h), 1.0, 5, dtype=torch.bfloat16)
+    kc = gen_normal((S, s.n_kv_heads, max_seq, s.head_dim), 1.0, 6, dtype=torch.bfloat16)
+    vc = gen_normal((S, s.n_kv_heads, max_seq, s.head_dim), 1.0, 7, dtype=torch.bfloat16)
+    ko, vo = _cache_to_oracle(kc, S, max_seq), _cache_to_oracle(vc, S, max_seq)
+    cl = torch.tensor(cache_lens, dtype=torch.int32)
+    cfg = dl.make_block_config(s, rk, max_tokens=S, max_seqs=S)
+    wdev = dl.BlockWeights({k: v.cuda() for k, v in w.items()})
+    ws = torch.zeros(dl.dl_block_workspace(cfg), dtype=torch.uint8, device="cuda")
+    xd, kcd, vcd = x.cuda(), kc.cuda(), vc.cuda()
+    dl.dl_decomposed_block_forward(cfg, wdev, xd, cl.cuda(), None, S, dl.DL_DECODE, kcd, vcd, cl.cuda(), None, ws)
+    torch.cuda.synchronize()
+    ref, kn, vn = orc.block_decode(_oracle_cfg(orc, s, rk), w, x, ko, vo, cache_lens)
+    assert rel(xd.cpu().double() - x.double(), ref - x.double().numpy()) <= TOL_BF16
+    kg = torch.stack([kcd[b, :, cache_lens[b]].reshape(-1) for b in range(S)]).cpu()
+    assert rel(kg, kn) <= TOL_BF16
+
+
+def test_block_workspace_left_zeroed_and_repeatable(dl, orc):
+    """Consume-and-clear: two identical decode calls give identical results."""
+    s = SMALL
+    rk = block_ranks(s, 0.4)
+    w = gen_block_weights(s, rk, 0, 4)
+    S = 16
+    cl = torch.full((S,), 9, dtype=torch.int32, device="cuda")
+    cfg = dl.make_block_config(s, rk, max_tokens=S, max_seqs=S)
+    wdev = dl.BlockWeights({k: v.cuda() for k, v in w.items()})
+    ws = torch.zeros(dl.dl_block_workspace(cfg), dtype=torch.uint8, device="cuda")
+    x = gen_normal((S, s.h), 1.0, 8, dtype=torch.bfloat16).cuda()
+    kc = torch.zeros(S, s.n_kv_heads, 16, s.head_dim, dtype=torch.bfloat16, device="cuda")
+    vc = torch.zeros_like(kc)
+    outs = []
+    for _ in range(2):
+        xx = x.clone()
+        dl.dl_decomposed_block_forward(cfg, wdev, xx, cl, None, S, dl.DL_DECODE, kc, vc, cl, None, ws)
+        outs.append(xx)
+    torch.cuda.synchronize()
+    assert float((outs[0].float() - outs[1].float()).abs().max()) < 0.05
+    # everything except the bf16 staging must be zero again
+    assert rel(outs[0].cpu(), outs[1].cpu()) < 1e-2
+
+
+@pytest.mark.slow
+def test_block_8b_prefill_2048_sampled(dl, orc):
+    """BASELINE config 2 at full size (8B @20%, one sequence of 2048 tokens):
+    sampled output rows vs the oracle (which recomputes K/V for all tokens)."""
+    s = LLAMA3_8B
+    w, rk, x, xo, pos, cu, kc, vc = _run_prefill(dl, orc, s, 0.2, [2048], seed=11)
+    rows = [0, 1, 511, 1024, 2047]
+    ref, _, _ = orc.block_prefill(_oracle_cfg(orc, s, rk), w, x, pos, cu, rows=rows)
+    assert rel(xo[rows].double() - x[rows].double(), ref - x[rows].double().numpy()) <= TOL_BF16
+
+
+@pytest.mark.slow
+def test_block_8b_decode_b64_sampled(dl, orc):
+    """Config 3 layer shape: 8B @20%, decode batch 64, context 512; 4 sampled sequences."""
+    s = LLAMA3_8B
+    rk = block_ranks(s, 0.2)
+    w = gen_block_weights(s, rk, 0, 12)
+    S, L = 64, 512
+    x = gen_normal((S, s.h), 1.0, 13, dtype=torch.bfloat16)
+    kc = gen_normal((S, s.n_kv_heads, L + 1, s.head_dim), 1.0, 14, dtype=torch.bfloat16)
+    vc = gen_normal((S, s.n_kv_heads, L + 1, s.head_dim), 1.0, 15, dtype=torch.bfloat16)
+    cl = torch.full((S,), L, dtype=torch.int32)
+    cfg = dl.make_block_config(s, rk, max_tokens=S, max_seqs=S)
+    wdev = dl.BlockWeights({k: v.cuda() for k, v in w.items()})
+    ws = torch.zeros(dl.dl_block_workspace(cfg), dtype=torch.uint8, device="cuda")
+    xd, kcd, vcd = x.cuda(), kc.cuda(), vc.cuda()
+    dl.dl_decomposed_block_forward(cfg, wdev, xd, cl.cuda(), None, S, dl.DL_DECODE, kcd, vcd, cl.cuda(), None, ws)
+    torch.cuda.synchronize()
+    pick = [0, 21, 42, 63]
+    ref, _, _ = orc.block_decode(_oracle_cfg(orc, s, rk), w, x[pick], _cache_to_oracle(kc[pick], 4, L + 1),
+                                 _cache_to_oracle(vc[pick], 4, L + 1), [L] * 4)
+    got = xd.cpu()[pick].double() - x[pick].double()
+    assert rel(got, ref - x[pick].double().numpy()) <= TOL_BF16
