@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""Benchmark: decomposed LLaMA-3-70B (random init, 40% compression) tokens/s on
+N B200s (tensor parallel over the rank dimension), decode and prefill.
+
+    python bench.py [--gpus N --steps K --warmup W]            # our arm
+    python bench.py --impl reference ...                       # fp64 CPU oracle arm
+    torchrun --nproc-per-node N bench.py --gpus N ...          # TP = N
+
+A "step" is one full-model decode step: embedding -> 80 decomposed blocks
+(every row of SURVEY.md section 8(a): RMSNorm, stage-1/stage-2 low-rank
+chains, TP reductions, RoPE + cache append, causal GQA attention, SiLU*up,
+residual) -> final RMSNorm -> LM head, for a batch of 64 sequences at
+context 512, captured in one CUDA Graph.  `value` is decode tokens/s of the
+whole job; the prefill line (one 2048-token sequence) rides in "prefill".
+Weights (~115 GB at TP=1) and caches are larger than L2, so every step
+streams from HBM (no L2 flush needed; stated in config).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decomposed LLaMA-3-70B tokens/s (decode, prefill) at 1/2/4/8 B200; % roofline"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--model", default="70b", choices=["70b", "8b"])
+    p.add_argument("--ratio", type=float, default=0.4)
+    p.add_argument("--batch", type=int, default=64)
+    p.add_argument("--ctx", type=int, default=512)
+    p.add_argument("--prefill-tokens", type=int, default=2048)
+    p.add_argument("--prefill-steps", type=int, default=3)
+    p.add_argument("--layers", type=int, default=0, help="debug only: fewer layers (invalid for reporting)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-sample-seqs", type=int, default=64)
+    return p.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return pk["hbm_gbs"], pk["bf16_tflops"], pk.get("bf16_tflops_sustained", pk["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = f"/tmp/dl_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+            rows = [[c.strip() for c in r] for r in rows if len(r) >= 8]
+            if not rows:
+                return out
+            sm = [float(r[0]) for r in rows]
+            out["sm_mhz"] = statistics.median(sm)
+            out["sm_max_mhz"] = float(rows[0][1])
+            out["samples"] = len(rows)
+            out["power_w_max"] = max(float(r[2]) for r in rows if r[2] not in ("[N/A]", ""))
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for i, n in enumerate(names):
+                if any(r[4 + i].lower() == "active" for r in rows):
+                    out["reasons"].append(n)
+        except Exception as e:  # noqa: BLE001
+            out["error"] = str(e)
+        return out
+
+
+# ---------------------------------------------------------------------------
+def cpu_baseline(shape, ranks, ctx: int, sample_seqs: int, layer0_w=None, min_s: float = 10.0):
+    """The fp64 oracle, as it stands, on one decomposed layer for `sample_seqs`
+    decode tokens (context ctx), scaled to full-model tokens/s (÷ n_layers)."""
+    import numpy as np
+    import torch
+
+    import oracle
+    from synthetic import gen_block_weights, gen_normal
+    oracle.build()
+    if layer0_w is None:
+        layer0_w = gen_block_weights(shape, ranks, 3, 0, device="cpu")
+    w = {k: v.detach().to("cpu") for k, v in layer0_w.items()}
+    cfg = oracle.BlockCfg(shape.h, shape.n_heads, shape.n_kv_heads, shape.head_dim, shape.m, ranks["q"],
+                          ranks["k"], ranks["v"], ranks["o"], ranks["gate"], ranks["up"], ranks["down"],
+                          rope_theta=shape.rope_theta, rms_eps=shape.rms_eps)
+    S = sample_seqs
+    x = gen_normal((S, shape.h), 1.0, 41)
+    kc = gen_normal((S, ctx + 1, shape.h_kv), 1.0, 42, dtype=torch.bfloat16)
+    vc = gen_normal((S, ctx + 1, shape.h_kv), 1.0, 43, dtype=torch.bfloat16)
+    w64 = {k: v.double().numpy() for k, v in w.items()}
+    t0 = time.perf_counter()
+    reps = 0
+    while True:      # repeat the one-layer sample until >= min_s of CPU work
+        oracle.block_decode(cfg, w64, x, kc, vc, np.full(S, ctx, dtype=np.int32))
+        reps += 1
+        dt = time.perf_counter() - t0
+        if dt >= min_s:
+            break
+    return {"value": S * reps / (dt * shape.n_layers), "unit": "tokens/s", "cores": oracle.num_threads(),
+            "kind": "oracle",
+            "sample": f"{reps} x (1 of {shape.n_layers} decomposed layers, {S} decode tokens at context {ctx}), "
+                      f"fp64; {dt:.2f} s, scaled x{shape.n_layers} layers"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from synthetic import LLAMA3_70B, LLAMA3_8B, block_ranks
+    shape = LLAMA3_70B if args.model == "70b" else LLAMA3_8B
+    ranks = block_ranks(shape, args.ratio)
+    from synthetic import gen_block_weights
+    w = gen_block_weights(shape, ranks, 3, 0, device="cpu")
+    S = max(1, min(args.cpu_sample_seqs, args.batch))
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_baseline(shape, ranks, args.ctx, S, w, min_s=2.0)
+        if i >= args.warmup:
+            vals.append(r["value"])
+    v = statistics.mean(vals)
+    step_ms = args.batch / v * 1e3
+    line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded random-init factors)",
+            "impl": "reference",
+            "config": {"workload": f"llama3-{args.model} @{int(args.ratio * 100)}% decode B={args.batch} "
+                                   f"ctx={args.ctx}", "global_batch": args.batch, "seq_len": args.ctx,
+                       "parallelism": "cpu"},
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": r["cores"], "kind": "oracle",
+                             "sample": r["sample"]},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_17709_b200 as dl
+    from paper_2604_17709_b200.model import DecomposedLlama
+    from synthetic import LLAMA3_70B, LLAMA3_8B, block_ranks, gen_block_weights, gen_normal
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    comm = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        comm = dl.Comm.from_process_group()
+    dl.load()
+    if not dl.dl_device_ok():
+        raise SystemExit("libdl.so: no sm_100 device")
+    shape = LLAMA3_70B if args.model == "70b" else LLAMA3_8B
+    ranks = block_ranks(shape, args.ratio)
+    n_layers = args.layers or shape.n_layers
+    cfg_id = 3 if args.model == "70b" else 2
+
+    t_init = time.time()
+    keep0 = {}
+
+    def layer_iter():
+        for li in range(n_layers):
+            w = gen_block_weights(shape, ranks, cfg_id, li, device=dev)
+            if li == 0 and rank == 0 and world == 1:
+                keep0["w"] = {k: v.to("cpu") for k, v in w.items()}
+            yield w
+
+    vloc = shape.vocab // world
+    embed = gen_normal((shape.vocab, shape.h), 1.0, 7001, device=dev, dtype=torch.bfloat16)
+    lm_full_rows = gen_normal((shape.vocab, shape.h), shape.h ** -0.5, 7002, device=dev, dtype=torch.bfloat16)
+    lm_head = lm_full_rows[rank * vloc:(rank + 1) * vloc].clone()
+    del lm_full_rows
+    final_norm = torch.ones(shape.h, dtype=torch.bfloat16, device=dev)
+    model = DecomposedLlama(shape, ranks, layer_iter(), embed, final_norm, lm_head, batch=args.batch,
+                            max_seq=args.ctx + 1, prefill_tokens=args.prefill_tokens, comm=comm, device=dev)
+    # context: ctx tokens already cached per sequence (random K/V), fixed for every step
+    model.cache.normal_()
+    model.cache_lens.fill_(args.ctx)
+    g = torch.Generator(device=dev)
+    g.manual_seed(7003)
+    model.ids.copy_(torch.randint(0, shape.vocab, (args.batch,), generator=g, device=dev, dtype=torch.int32))
+    if args.prefill_tokens:
+        model.pre_ids.copy_(torch.randint(0, shape.vocab, (args.prefill_tokens,), generator=g, device=dev,
+                                          dtype=torch.int32))
+    torch.cuda.synchronize()
+    init_s = time.time() - t_init
+    print(f"[bench] init {init_s:.1f}s, {torch.cuda.memory_allocated(dev) / 1e9:.1f} GB allocated", file=sys.stderr,
+          flush=True)
+
+    stream = torch.cuda.Stream(device=dev)
+    hbm_gbs, bf16_burst, bf16_sust, peak_src = load_peaks()
+
+    def capture(fn, n_gemm_cap):
+        with torch.cuda.stream(stream):
+            fn()                                   # eager warm-up (sets kernel attributes)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        c0 = dl.dl_launch_count()
+        dl.dl_profile_begin(n_gemm_cap)
+        with torch.cuda.graph(graph, stream=stream):
+            fn()
+        dl.dl_profile_end()
+        launches = dl.dl_launch_count() - c0
+        return graph, launches
+
+    def timed(graph, steps, warmup):
+        with torch.cuda.stream(stream):
+            for _ in range(warmup):
+                graph.replay()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clk, torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(steps):
+                graph.replay()
+            e1.record(stream)
+            torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            dist.barrier()
+        return ms, clk.summary()
+
+    def gemm_roofline(kind, bound):
+        recs = [r for r in dl.dl_profile_records() if r[3] == kind]
+        if not recs:
+            return None
+        ms = sum(r[0] for r in recs)
+        if bound == "hbm":
+            ach = sum(r[1] for r in recs) / (ms * 1e-3) / 1e9
+            peak = hbm_gbs
+            unit = "GB/s"
+        else:
+            ach = sum(r[2] for r in recs) / (ms * 1e-3) / 1e12
+            peak = bf16_sust
+            unit = "TFLOP/s"
+        return {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak, "traffic": None,
+                "kernel": "tc_gemm (tcgen05 low-rank stage-1/stage-2 GEMMs, all launches of one step)",
+                "launches_per_step": len(recs), "kernel_ms_per_step": ms,
+                "peak_source": f"{peak_src} ({'hbm_gbs' if bound == 'hbm' else 'bf16_tflops_sustained'})"}
+
+    # ---- decode -------------------------------------------------------------
+    n_cap = 8 * n_layers + 8
+    dgraph, dlaunch = capture(model.decode_step, n_cap)
+    dms, dclk = timed(dgraph, args.steps, args.warmup)
+    step_ms = dms / args.steps
+    dec_tps = args.batch / (step_ms * 1e-3)
+    roof = gemm_roofline(1, "hbm")
+    # algorithmic bytes per decode step per GPU: factors + LM head + KV reads
+    pl = (2 * shape.h * ranks["q"] + (shape.h + shape.h_kv) * (ranks["k"] + ranks["v"]) + 2 * shape.h * ranks["o"]
+          + (shape.h + shape.m) * (ranks["gate"] + ranks["up"] + ranks["down"]))
+    step_bytes = (2 * (n_layers * pl + shape.vocab * shape.h) + args.batch * args.ctx * n_layers * 2 * shape.h_kv * 2) \
+        / world
+    step_gbs = step_bytes / (step_ms * 1e-3) / 1e9
+
+    # ---- e2e: H2D ids from pinned host, graph, D2H logits into pinned host -----
+    ids_h = model.ids.to("cpu").pin_memory()
+    out_dev = model.logits_local if world == 1 else model.logits
+    out_h = torch.empty(out_dev.shape, dtype=out_dev.dtype, pin_memory=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(args.steps):
+            model.ids.copy_(ids_h, non_blocking=True)
+            dgraph.replay()
+            out_h.copy_(out_dev, non_blocking=True)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    # ---- prefill ------------------------------------------------------------
+    prefill = None
+    if args.prefill_tokens:
+        pgraph, plaunch = capture(model.prefill_step, n_cap)
+        psteps = max(1, args.prefill_steps)
+        pms, pclk = timed(pgraph, psteps, min(args.warmup, 3))
+        p_step_ms = pms / psteps
+        proof = gemm_roofline(0, "tensor")
+        T = args.prefill_tokens
+        pf = (2 * T * n_layers * pl + n_layers * 4 * (T * (T + 1) / 2) * shape.h) / world
+        prefill = {"value": T / (p_step_ms * 1e-3), "unit": "tokens/s", "ms_per_step": p_step_ms,
+                   "tokens_per_step": T, "steps": psteps, "algorithmic_tflop_per_gpu": pf / 1e12,
+                   "achieved_tflops": pf / (p_step_ms * 1e-3) / 1e12,
+                   "frac_of_bf16_sustained": pf / (p_step_ms * 1e-3) / 1e12 / bf16_sust,
+                   "roofline": proof, "gpu_launches": plaunch * psteps, "clocks": pclk}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(shape, ranks, args.ctx, min(args.cpu_sample_seqs, args.batch), keep0.get("w"))
+        except Exception as e:  # noqa: BLE001
+            cpu = {"error": str(e)}
+
+    if rank == 0:
+        if roof is not None:
+            roof["step_algorithmic_gbs"] = step_gbs
+            roof["step_frac_of_hbm"] = step_gbs / hbm_gbs
+        line = {"metric": METRIC, "value": dec_tps, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded random-init factors, random KV)",
+                "config": {"workload": f"llama3-{args.model} @{int(round(args.ratio * 100))}% decode "
+                                       f"B={args.batch} ctx={args.ctx} (+ prefill {args.prefill_tokens})",
+                           "global_batch": args.batch, "seq_len": args.ctx, "parallelism": f"tp{world}",
+                           "layers": n_layers, "ranks": ranks,
+                           "l2": "inputs larger than L2 (weights+KV stream from HBM every step)",
+                           "cuda_graph": True},
+                "roofline": roof, "cpu_baseline": cpu,
+                "e2e": {"value": args.batch / (e2e_ms * 1e-3), "unit": "tokens/s",
+                        "h2d_bytes_per_step": ids_h.numel() * ids_h.element_size(),
+                        "d2h_bytes_per_step": out_h.numel() * out_h.element_size()},
+                "gpu_launches": dlaunch * args.steps, "clocks": dclk, "prefill": prefill,
+                "step_algorithmic_gb_per_gpu": step_bytes / 1e9, "init_s": init_s}
+        if args.layers:
+            line["invalid"] = f"debug run with {n_layers} layers"
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -238,6 +238,25 @@ dl_status dl_dense(const void *X, int64_t ldx, const void *W, int64_t ldw,
                    void *C, int64_t ldc, int64_t T, int64_t N, int64_t K,
                    void *workspace, size_t workspace_bytes, void *stream);
 
+/* ------------------------------------------------------------------------
+ * Instrumentation (used by bench.py; host-side state, not thread-safe
+ * across concurrent captures).
+ * dl_launch_count: kernels this library enqueued since load (a CUDA-Graph
+ *   capture counts each captured launch once).
+ * dl_profile_begin(capacity): from now on record a CUDA event pair around
+ *   each tcgen05 GEMM launch (first `capacity` launches; inside a stream
+ *   capture as external event-record nodes, so graph replays re-record).
+ * dl_profile_get(i): elapsed ms of record i plus its algorithmic bytes and
+ *   flops (weights + activations + outputs, each counted once) and kind
+ *   (1 = swap-AB decode path, 0 = wide prefill path).
+ * ---------------------------------------------------------------------- */
+long long dl_launch_count(void);
+dl_status dl_profile_begin(int capacity);
+dl_status dl_profile_end(void);
+int dl_profile_count(void);
+dl_status dl_profile_get(int i, float *ms, double *bytes, double *flops,
+                         int *kind);
+
 #ifdef __cplusplus
 }
 #endif

@@ -22,7 +22,8 @@ STATUS = {0: "DL_OK", 1: "DL_ERR_INVALID_ARG", 2: "DL_ERR_SHAPE", 3: "DL_ERR_RAN
 EXPORTS = ("dl_last_error", "dl_version", "dl_device_ok", "dl_comm_create", "dl_comm_destroy",
            "dl_lowrank_linear_workspace", "dl_lowrank_linear", "dl_tp_plan", "dl_tp_shard_factors",
            "dl_block_workspace", "dl_decomposed_block_forward", "dl_embedding", "dl_rmsnorm",
-           "dl_dense_workspace", "dl_dense")
+           "dl_dense_workspace", "dl_dense", "dl_launch_count", "dl_profile_begin", "dl_profile_end",
+           "dl_profile_count", "dl_profile_get")
 
 
 class DLError(RuntimeError):
@@ -89,8 +90,11 @@ def load():
             lib.dl_rmsnorm.argtypes = [P, P, P, I64, I64, ctypes.c_float, P]
             lib.dl_dense_workspace.argtypes = [I64, I64, I64, ctypes.POINTER(ctypes.c_size_t)]
             lib.dl_dense.argtypes = [P, I64, P, I64, P, I64, I64, I64, I64, P, ctypes.c_size_t, P]
+            lib.dl_profile_begin.argtypes = [I]
+            lib.dl_profile_get.argtypes = [I, P, P, P, P]
             for name in EXPORTS[3:]:
                 getattr(lib, name).restype = I
+            lib.dl_launch_count.restype = ctypes.c_longlong
             _lib = lib
     return _lib
 
@@ -303,3 +307,27 @@ def dl_dense(X: torch.Tensor, W: torch.Tensor, C: torch.Tensor, stream=None):
     N = W.shape[0]
     _check(load().dl_dense(_ptr(X), _ld(X), _ptr(W), _ld(W), _ptr(C), _ld(C), T, N, K, None, 0, _stream(stream)))
     return C
+
+
+def dl_launch_count() -> int:
+    """Kernels this library has enqueued since load (captured launches count once)."""
+    return int(load().dl_launch_count())
+
+
+def dl_profile_begin(capacity: int):
+    _check(load().dl_profile_begin(capacity))
+
+
+def dl_profile_end():
+    _check(load().dl_profile_end())
+
+
+def dl_profile_records():
+    """[(ms, bytes, flops, kind)] for the instrumented tcgen05 GEMM launches."""
+    L = load()
+    out = []
+    for i in range(L.dl_profile_count()):
+        ms, b, f, k = ctypes.c_float(), ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
+        _check(L.dl_profile_get(i, ctypes.byref(ms), ctypes.byref(b), ctypes.byref(f), ctypes.byref(k)))
+        out.append((ms.value, b.value, f.value, k.value))
+    return out

@@ -481,6 +481,8 @@ dl_status block_dims(const dl_block_config* c, int world, BlockDims* d) {
 struct BlockWs {
   float* zf; float* yf;              // fp32 reduction targets (zero-maintained)
   __nv_bfloat16 *xn, *zb, *yb, *rs, *q, *att, *att_full, *ag, *act;
+  float* apart;                      // split-KV attention partials (decode)
+  size_t apart_bytes;
   int64_t ldz32, ldzb, ldy32;
 };
 
@@ -503,6 +505,8 @@ BlockWs carve_block(Carver& c, const BlockDims& d, int64_t Tmax) {
     w.ag = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.h);
   }
   w.act = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.m);
+  w.apart_bytes = attention_workspace(Ts, static_cast<int>(d.Hq_loc), static_cast<int>(d.d));
+  w.apart = c.take<float>(w.apart_bytes / sizeof(float));
   return w;
 }
 
@@ -745,6 +749,8 @@ dl_status dl_decomposed_block_forward(const dl_block_config* cfg, const dl_block
   aa.Hk = static_cast<int>(d.Hk_loc);
   aa.d = static_cast<int>(d.d);
   aa.decode = phase == DL_DECODE;
+  aa.partial = ws.apart;
+  aa.partial_bytes = ws.apart_bytes;
   DL_TRY(launch_attention(aa, st));
 
   const __nv_bfloat16* att_in = ws.att;

@@ -3,13 +3,20 @@
 // reading kv head floor(g * Hk / Hq), on the rank's LOCAL
 // heads only -- the duplicated self-attention of PAPER.md:141-144 is gone.
 //
-// Cache layout [seq][kv_head][max_seq][d] (bf16): one (seq, kv head) is a
-// contiguous run of keys, so the key loop streams coalesced 256 B rows.
+// Cache layout [seq][kv_head][max_seq][d=128] (bf16): one (seq, kv head) is a
+// contiguous run of 256-byte key rows, staged into shared memory with
+// cp.async (16-byte chunks, XOR-swizzled so ldmatrix is bank-conflict free).
+// Both kernels use bf16 mma.sync.m16n8k16 tensor-core MMAs with fp32
+// accumulation and an online (running max, exp2) softmax.
 //
-// attn_warp_kernel: one warp per (query token, query head); lane owns 4 of
-// the d = 128 dims; keys are consumed 4 at a time (4 independent shuffle
-// reductions in flight) with an online (running-max) softmax in fp32.
-// Used for decode and (as the round-1 path) for prefill.
+// prefill: FlashAttention-2 layout.  CTA = 64 queries x 1 head; warp w owns
+//   query rows [16w, 16w+16); K/V tiles of 64 keys double-buffered; only the
+//   key tiles at or below the diagonal are visited.
+// decode:  one CTA per (sequence, kv head, key split).  The G = Hq/Hk query
+//   heads sharing the kv head are the MMA rows (G <= 16), so every K/V byte
+//   is read from HBM once for the whole group; the 4 warps split each 64-key
+//   tile 4 ways and are merged (log-sum-exp) through shared memory; key
+//   splits (for small batch x heads) are merged by a second tiny kernel.
 #include <math.h>
 
 #include "dl_internal.h"
@@ -17,109 +24,457 @@
 namespace dl {
 namespace {
 
-constexpr int kWarpsPerCta = 4;
+constexpr int D = 128;           // head dim
+constexpr int KT = 64;           // keys per tile
+constexpr int QT = 64;           // queries per prefill CTA
+constexpr int ROW_BYTES = D * 2; // 256
+constexpr int TILE_BYTES = KT * ROW_BYTES;   // 16 KB
+constexpr int kMaxSplits = 16;
 
-__device__ __forceinline__ float4 ld_bf16x4(const __nv_bfloat16* p) {
-  uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
-  float2 a = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(&v)[0]);
-  float2 b = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(&v)[1]);
-  return make_float4(a.x, a.y, b.x, b.y);
+__device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ uint32_t ptx_smem(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t swz(int row, int chunk) {   // byte offset in a [rows][128] bf16 tile
+  return static_cast<uint32_t>(row * ROW_BYTES + ((chunk ^ (row & 7)) << 4));
 }
 
-__global__ void __launch_bounds__(kWarpsPerCta * 32) attn_warp_kernel(AttnArgs a) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t t = blockIdx.x;
-  const int h = blockIdx.y * kWarpsPerCta + warp;
-  if (h >= a.Hq) return;
-  int s;
-  int64_t qpos;   // cache position of this query (keys 0..qpos are visible)
-  if (a.decode) {
-    s = static_cast<int>(t);
-    qpos = a.cache_lens[s];
-  } else {
-    int lo = 0, hi = a.num_seqs - 1;
-    while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (a.cu_seqlens[mid] <= t) lo = mid; else hi = mid - 1;
-    }
-    s = lo;
-    qpos = a.cache_lens[s] + (t - a.cu_seqlens[s]);
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g, bool valid) {
+  const int n = valid ? 16 : 0;   // src-size 0 -> zero fill
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ void ldsm_x4(uint32_t saddr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(saddr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t saddr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(saddr));
+}
+// C[16x8] += A[16x16] B[16x8], bf16 in, fp32 acc
+__device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// cooperative load of `rows` rows (row r from src + r*ld elements) into a swizzled tile;
+// rows >= nvalid are zero-filled.  nthr threads.
+__device__ __forceinline__ void load_tile(uint32_t sbase, const __nv_bfloat16* src, int64_t ld, int rows, int nvalid,
+                                          int tid, int nthr) {
+  for (int i = tid; i < rows * 16; i += nthr) {
+    const int r = i >> 4, c = i & 15;
+    const bool v = r < nvalid;
+    cp_async16(sbase + swz(r, c), v ? src + r * ld + c * 8 : src, v);
   }
+}
+
+// =============================== prefill ===================================
+__global__ void __launch_bounds__(128) attn_prefill_kernel(AttnArgs a) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  const int s = blockIdx.z, h = blockIdx.y;
+  const int n_new = a.cu_seqlens[s + 1] - a.cu_seqlens[s];
+  const int q0 = blockIdx.x * QT;
+  if (q0 >= n_new) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int64_t base_pos = a.cache_lens[s];
   const int kvh = static_cast<int>((static_cast<int64_t>(h) * a.Hk) / a.Hq);
-  const int d = a.d;   // 128
-  const float scale = rsqrtf(static_cast<float>(d)) * 1.4426950408889634f;   // log2(e)/sqrt(d)
-  float4 q = ld_bf16x4(a.q + t * static_cast<int64_t>(a.Hq) * d + static_cast<int64_t>(h) * d + lane * 4);
-  q.x *= scale; q.y *= scale; q.z *= scale; q.w *= scale;
-  const int64_t base = (static_cast<int64_t>(s) * a.Hk + kvh) * a.max_seq * d + lane * 4;
-  const __nv_bfloat16* K = a.k_cache + base;
-  const __nv_bfloat16* V = a.v_cache + base;
-  float m = -INFINITY, l = 0.f;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  const int64_t nk = qpos + 1;
-  int64_t u = 0;
-  for (; u + 4 <= nk; u += 4) {
-    float sc[4];
-    float4 vv[4];
+  const int64_t tok0 = a.cu_seqlens[s] + q0;
+  const int64_t ldq = static_cast<int64_t>(a.Hq) * D;
+  const __nv_bfloat16* Qg = a.q + tok0 * ldq + static_cast<int64_t>(h) * D;
+  const int64_t kvoff = (static_cast<int64_t>(s) * a.Hk + kvh) * a.max_seq * D;
+  const __nv_bfloat16* Kg = a.k_cache + kvoff;
+  const __nv_bfloat16* Vg = a.v_cache + kvoff;
+  const int nq = min(QT, n_new - q0);
+  const int64_t n_keys = base_pos + q0 + nq;          // keys 0 .. last query position
+  const int n_kt = static_cast<int>((n_keys + KT - 1) / KT);
+
+  const uint32_t sQ = ptx_smem(sm);
+  const uint32_t sK0 = sQ + QT * ROW_BYTES;
+  const uint32_t sV0 = sK0 + 2 * TILE_BYTES;
+
+  load_tile(sQ, Qg, ldq, QT, nq, tid, 128);
+  load_tile(sK0, Kg, D, KT, static_cast<int>(min64(KT, n_keys)), tid, 128);
+  load_tile(sV0, Vg, D, KT, static_cast<int>(min64(KT, n_keys)), tid, 128);
+  cp_commit();
+
+  uint32_t qf[8][4];
+  float acc[16][4];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  const float scale = rsqrtf(static_cast<float>(D)) * 1.4426950408889634f;
+  const int64_t qpos0 = base_pos + q0 + warp * 16 + g;   // row g
+  const int64_t qpos1 = qpos0 + 8;                        // row g + 8
+
+  for (int kt = 0; kt < n_kt; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < n_kt) {
+      const int64_t k1 = static_cast<int64_t>(kt + 1) * KT;
+      const int nv = static_cast<int>(min64(KT, n_keys - k1));
+      load_tile(sK0 + (buf ^ 1) * TILE_BYTES, Kg + k1 * D, D, KT, nv, tid, 128);
+      load_tile(sV0 + (buf ^ 1) * TILE_BYTES, Vg + k1 * D, D, KT, nv, tid, 128);
+    }
+    cp_commit();
+    cp_wait<1>();
+    __syncthreads();
+    if (kt == 0) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const int row = warp * 16 + (lane & 15);
+        const int chunk = kk * 2 + (lane >> 4);
+        ldsm_x4(sQ + swz(row, chunk), qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3]);
+      }
+    }
+    const uint32_t sK = sK0 + buf * TILE_BYTES, sV = sV0 + buf * TILE_BYTES;
+    // ---- S = Q K^T (16 x 64 per warp) ----
+    float sc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sc[i][0] = sc[i][1] = sc[i][2] = sc[i][3] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+#pragma unroll
+      for (int np = 0; np < 4; ++np) {
+        const int key = np * 16 + (lane >> 4) * 8 + (lane & 7);
+        const int chunk = kk * 2 + ((lane >> 3) & 1);
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(sK + swz(key, chunk), b0, b1, b2, b3);
+        mma16816(sc[2 * np], qf[kk], b0, b1);
+        mma16816(sc[2 * np + 1], qf[kk], b2, b3);
+      }
+    }
+    // ---- scale, causal mask, online softmax ----
+    const int64_t kbase = static_cast<int64_t>(kt) * KT;
+    const bool need_mask = kbase + KT - 1 > base_pos + q0 + warp * 16 || kbase + KT > n_keys;
+    float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float v = sc[nt][e] * scale;
+        if (need_mask) {
+          const int64_t kp = kbase + nt * 8 + 2 * t4 + (e & 1);
+          const int64_t qp = (e < 2) ? qpos0 : qpos1;
+          if (kp > qp || kp >= n_keys) v = -INFINITY;
+        }
+        sc[nt][e] = v;
+      }
+      mx0 = fmaxf(mx0, fmaxf(sc[nt][0], sc[nt][1]));
+      mx1 = fmaxf(mx1, fmaxf(sc[nt][2], sc[nt][3]));
+    }
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+    // rows whose every key so far is masked keep m = -inf: use 0 as the exp base
+    const float b0 = mn0 == -INFINITY ? 0.f : mn0, b1 = mn1 == -INFINITY ? 0.f : mn1;
+    const float c0 = exp2f(m0 - b0), c1 = exp2f(m1 - b1);
+    m0 = mn0;
+    m1 = mn1;
+    l0 *= c0;
+    l1 *= c1;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      acc[i][0] *= c0; acc[i][1] *= c0;
+      acc[i][2] *= c1; acc[i][3] *= c1;
+    }
+    uint32_t pf[4][4];
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      const float p0 = exp2f(sc[nt][0] - b0), p1 = exp2f(sc[nt][1] - b0);
+      const float p2 = exp2f(sc[nt][2] - b1), p3 = exp2f(sc[nt][3] - b1);
+      l0 += p0 + p1;
+      l1 += p2 + p3;
+      const int j = nt >> 1;
+      if ((nt & 1) == 0) {
+        pf[j][0] = pack_bf16(p0, p1);
+        pf[j][1] = pack_bf16(p2, p3);
+      } else {
+        pf[j][2] = pack_bf16(p0, p1);
+        pf[j][3] = pack_bf16(p2, p3);
+      }
+    }
+    // ---- O += P V ----
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      float4 k = ld_bf16x4(K + (u + j) * d);
-      vv[j] = ld_bf16x4(V + (u + j) * d);
-      sc[j] = q.x * k.x + q.y * k.y + q.z * k.z + q.w * k.w;
+#pragma unroll
+      for (int dp = 0; dp < 8; ++dp) {
+        const int key = j * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        const int chunk = dp * 2 + (lane >> 4);
+        uint32_t v0, v1, v2, v3;
+        ldsm_x4_t(sV + swz(key, chunk), v0, v1, v2, v3);
+        mma16816(acc[2 * dp], pf[j], v0, v1);
+        mma16816(acc[2 * dp + 1], pf[j], v2, v3);
+      }
+    }
+    __syncthreads();
+  }
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  const float i0 = 1.f / l0, i1 = 1.f / l1;
+  const int r0 = warp * 16 + g, r1 = r0 + 8;
+  __nv_bfloat16* O = a.out + tok0 * ldq + static_cast<int64_t>(h) * D;
+#pragma unroll
+  for (int nt = 0; nt < 16; ++nt) {
+    const int col = nt * 8 + 2 * t4;
+    if (r0 < nq) *reinterpret_cast<uint32_t*>(O + r0 * ldq + col) = pack_bf16(acc[nt][0] * i0, acc[nt][1] * i0);
+    if (r1 < nq) *reinterpret_cast<uint32_t*>(O + r1 * ldq + col) = pack_bf16(acc[nt][2] * i1, acc[nt][3] * i1);
+  }
+}
+
+// ================================ decode ===================================
+// partial layout (splits > 1): [token][head][split] -> {m, l, acc[128]}
+constexpr int PART = D + 2;
+
+__global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, int splits) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  const int s = blockIdx.z, kvh = blockIdx.y, sp = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int G = a.Hq / a.Hk;
+  const int64_t n_keys = static_cast<int64_t>(a.cache_lens[s]) + 1;
+  int64_t chunk_keys = (n_keys + splits - 1) / splits;
+  chunk_keys = (chunk_keys + KT - 1) / KT * KT;
+  const int64_t k_begin = sp * chunk_keys;
+  const int64_t k_end = min64(n_keys, k_begin + chunk_keys);
+  const int64_t ldq = static_cast<int64_t>(a.Hq) * D;
+  const __nv_bfloat16* Qg = a.q + static_cast<int64_t>(s) * ldq + static_cast<int64_t>(kvh) * G * D;
+  const int64_t kvoff = (static_cast<int64_t>(s) * a.Hk + kvh) * a.max_seq * D;
+  const __nv_bfloat16* Kg = a.k_cache + kvoff;
+  const __nv_bfloat16* Vg = a.v_cache + kvoff;
+
+  const uint32_t sQ = ptx_smem(sm);
+  const uint32_t sK0 = sQ + 16 * ROW_BYTES;
+  const uint32_t sV0 = sK0 + 2 * TILE_BYTES;
+  float* red = reinterpret_cast<float*>(sm + 16 * ROW_BYTES + 4 * TILE_BYTES);   // [4 warps][16][128]
+  float* redm = red + 4 * 16 * D;                                                 // [4][16] m, then [4][16] l
+
+  const int n_kt = k_end > k_begin ? static_cast<int>((k_end - k_begin + KT - 1) / KT) : 0;
+  load_tile(sQ, Qg, D, 16, G, tid, 128);   // head r of the group at Qg + r*D
+  if (n_kt > 0) {
+    const int nv = static_cast<int>(min64(KT, k_end - k_begin));
+    load_tile(sK0, Kg + k_begin * D, D, KT, nv, tid, 128);
+    load_tile(sV0, Vg + k_begin * D, D, KT, nv, tid, 128);
+  }
+  cp_commit();
+
+  float acc[16][4];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  const float scale = rsqrtf(static_cast<float>(D)) * 1.4426950408889634f;
+  uint32_t qf[8][4];
+
+  for (int kt = 0; kt < n_kt; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < n_kt) {
+      const int64_t k1 = k_begin + static_cast<int64_t>(kt + 1) * KT;
+      const int nv = static_cast<int>(min64(KT, k_end - k1));
+      load_tile(sK0 + (buf ^ 1) * TILE_BYTES, Kg + k1 * D, D, KT, nv, tid, 128);
+      load_tile(sV0 + (buf ^ 1) * TILE_BYTES, Vg + k1 * D, D, KT, nv, tid, 128);
+    }
+    cp_commit();
+    cp_wait<1>();
+    __syncthreads();
+    if (kt == 0) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        ldsm_x4(sQ + swz(lane & 15, kk * 2 + (lane >> 4)), qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3]);
+    }
+    const uint32_t sK = sK0 + buf * TILE_BYTES, sV = sV0 + buf * TILE_BYTES;
+    // this warp's 16 keys of the tile: rows [16w, 16w+16)
+    float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const int key = warp * 16 + (lane >> 4) * 8 + (lane & 7);
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4(sK + swz(key, kk * 2 + ((lane >> 3) & 1)), b0, b1, b2, b3);
+      mma16816(sc[0], qf[kk], b0, b1);
+      mma16816(sc[1], qf[kk], b2, b3);
+    }
+    const int64_t kbase = k_begin + static_cast<int64_t>(kt) * KT + warp * 16;
+    float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float v = sc[nt][e] * scale;
+        if (kbase + nt * 8 + 2 * t4 + (e & 1) >= k_end) v = -INFINITY;
+        sc[nt][e] = v;
+        if (e < 2) mx0 = fmaxf(mx0, v); else mx1 = fmaxf(mx1, v);
+      }
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+    const float b0 = mn0 == -INFINITY ? 0.f : mn0, b1 = mn1 == -INFINITY ? 0.f : mn1;
+    const float c0 = exp2f(m0 - b0), c1 = exp2f(m1 - b1);
+    m0 = mn0;
+    m1 = mn1;
+    l0 *= c0;
+    l1 *= c1;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      acc[i][0] *= c0; acc[i][1] *= c0;
+      acc[i][2] *= c1; acc[i][3] *= c1;
+    }
+    uint32_t pf[4];
+    {
+      const float p0 = exp2f(sc[0][0] - b0), p1 = exp2f(sc[0][1] - b0);
+      const float p2 = exp2f(sc[0][2] - b1), p3 = exp2f(sc[0][3] - b1);
+      const float p4 = exp2f(sc[1][0] - b0), p5 = exp2f(sc[1][1] - b0);
+      const float p6 = exp2f(sc[1][2] - b1), p7 = exp2f(sc[1][3] - b1);
+      l0 += p0 + p1 + p4 + p5;
+      l1 += p2 + p3 + p6 + p7;
+      pf[0] = pack_bf16(p0, p1);
+      pf[1] = pack_bf16(p2, p3);
+      pf[2] = pack_bf16(p4, p5);
+      pf[3] = pack_bf16(p6, p7);
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) sc[j] += __shfl_xor_sync(0xffffffffu, sc[j], o);
-    const float mx = fmaxf(fmaxf(sc[0], sc[1]), fmaxf(sc[2], sc[3]));
-    const float mn = fmaxf(m, mx);
-    const float corr = exp2f(m - mn);
-    l *= corr;
-    acc.x *= corr; acc.y *= corr; acc.z *= corr; acc.w *= corr;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float p = exp2f(sc[j] - mn);
-      l += p;
-      acc.x += p * vv[j].x; acc.y += p * vv[j].y; acc.z += p * vv[j].z; acc.w += p * vv[j].w;
+    for (int dp = 0; dp < 8; ++dp) {
+      const int key = warp * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+      uint32_t v0, v1, v2, v3;
+      ldsm_x4_t(sV + swz(key, dp * 2 + (lane >> 4)), v0, v1, v2, v3);
+      mma16816(acc[2 * dp], pf, v0, v1);
+      mma16816(acc[2 * dp + 1], pf, v2, v3);
     }
-    m = mn;
+    __syncthreads();
   }
-  for (; u < nk; ++u) {
-    float4 k = ld_bf16x4(K + u * d);
-    float4 v = ld_bf16x4(V + u * d);
-    float sc = q.x * k.x + q.y * k.y + q.z * k.z + q.w * k.w;
+  cp_wait<0>();
+  // ---- merge the 4 warps (log-sum-exp) ----
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  if (t4 == 0) {
+    redm[warp * 16 + g] = m0;
+    redm[warp * 16 + g + 8] = m1;
+    redm[64 + warp * 16 + g] = l0;
+    redm[64 + warp * 16 + g + 8] = l1;
+  }
+  __syncthreads();
+  float M0 = -INFINITY, M1 = -INFINITY;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
-    const float mn = fmaxf(m, sc);
-    const float corr = exp2f(m - mn);
-    const float p = exp2f(sc - mn);
-    l = l * corr + p;
-    acc.x = acc.x * corr + p * v.x; acc.y = acc.y * corr + p * v.y;
-    acc.z = acc.z * corr + p * v.z; acc.w = acc.w * corr + p * v.w;
-    m = mn;
+  for (int w = 0; w < 4; ++w) {
+    M0 = fmaxf(M0, redm[w * 16 + g]);
+    M1 = fmaxf(M1, redm[w * 16 + g + 8]);
   }
-  const float inv = 1.f / l;
-  uint2 o;
-  reinterpret_cast<__nv_bfloat162*>(&o)[0] = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
-  reinterpret_cast<__nv_bfloat162*>(&o)[1] = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
-  *reinterpret_cast<uint2*>(a.out + t * static_cast<int64_t>(a.Hq) * d + static_cast<int64_t>(h) * d + lane * 4) = o;
+  const float B0 = M0 == -INFINITY ? 0.f : M0, B1 = M1 == -INFINITY ? 0.f : M1;
+  const float f0 = exp2f(m0 - B0), f1 = exp2f(m1 - B1);
+  float* myred = red + warp * 16 * D;
+#pragma unroll
+  for (int nt = 0; nt < 16; ++nt) {
+    const int col = nt * 8 + 2 * t4;
+    myred[g * D + col] = acc[nt][0] * f0;
+    myred[g * D + col + 1] = acc[nt][1] * f0;
+    myred[(g + 8) * D + col] = acc[nt][2] * f1;
+    myred[(g + 8) * D + col + 1] = acc[nt][3] * f1;
+  }
+  __syncthreads();
+  // 128 threads: thread = column d, loop over the G valid rows
+  for (int r = 0; r < G; ++r) {
+    float Mr = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) Mr = fmaxf(Mr, redm[w * 16 + r]);
+    const float Br = Mr == -INFINITY ? 0.f : Mr;
+    float L = 0.f, o = 0.f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      L += redm[64 + w * 16 + r] * exp2f(redm[w * 16 + r] - Br);
+      o += red[(w * 16 + r) * D + tid];
+    }
+    const int h = kvh * G + r;
+    if (splits == 1) {
+      a.out[static_cast<int64_t>(s) * ldq + static_cast<int64_t>(h) * D + tid] = __float2bfloat16_rn(o / L);
+    } else {
+      float* pp = a.partial + ((static_cast<int64_t>(s) * a.Hq + h) * splits + sp) * PART;
+      pp[2 + tid] = o;
+      if (tid == 0) {
+        pp[0] = Mr;
+        pp[1] = L;
+      }
+    }
+  }
+}
+
+// merge key splits: one CTA (128 threads = d) per (token, head)
+__global__ void __launch_bounds__(128) attn_combine_kernel(AttnArgs a, int splits) {
+  const int64_t s = blockIdx.y;
+  const int h = blockIdx.x, d = threadIdx.x;
+  const float* pp = a.partial + (s * a.Hq + h) * splits * PART;
+  float M = -INFINITY;
+  for (int i = 0; i < splits; ++i) M = fmaxf(M, pp[i * PART]);
+  const float B = M == -INFINITY ? 0.f : M;
+  float L = 0.f, o = 0.f;
+  for (int i = 0; i < splits; ++i) {
+    const float f = exp2f(pp[i * PART] - B);
+    L += pp[i * PART + 1] * f;
+    o += pp[i * PART + 2 + d] * f;
+  }
+  a.out[s * a.Hq * D + static_cast<int64_t>(h) * D + d] = __float2bfloat16_rn(o / L);
 }
 
 }  // namespace
 
 size_t attention_workspace(int64_t max_tokens, int Hq, int d) {
-  (void)max_tokens; (void)Hq; (void)d;
-  return 0;
+  (void)d;
+  return static_cast<size_t>(max_tokens) * Hq * kMaxSplits * PART * sizeof(float);
 }
 
 dl_status launch_attention(const AttnArgs& a, cudaStream_t st) {
   if (a.T <= 0) return DL_OK;
-  if (a.d != 128) {
-    set_error("attention: head_dim %d unsupported (128 only)", a.d);
+  if (a.d != D || a.Hq % a.Hk != 0 || a.Hq / a.Hk > 16) {
+    set_error("attention: head_dim %d / group %d unsupported (d = 128, Hq/Hk <= 16)", a.d, a.Hq / a.Hk);
     return DL_ERR_UNSUPPORTED;
   }
-  dim3 grid(static_cast<unsigned>(a.T), static_cast<unsigned>((a.Hq + kWarpsPerCta - 1) / kWarpsPerCta));
-  attn_warp_kernel<<<grid, kWarpsPerCta * 32, 0, st>>>(a);
-  return cuda_status(cudaGetLastError(), "attention");
+  if (!a.decode) {
+    constexpr int SMEM = QT * ROW_BYTES + 4 * TILE_BYTES;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(attn_prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+      attr = true;
+    }
+    // grid.x covers the longest sequence: bounded by T
+    const int qtiles = static_cast<int>((a.T + QT - 1) / QT);
+    dim3 grid(qtiles, a.Hq, a.num_seqs);
+    attn_prefill_kernel<<<grid, 128, SMEM, st>>>(a);
+    return launched("attention prefill");
+  }
+  constexpr int SMEM = 16 * ROW_BYTES + 4 * TILE_BYTES + (4 * 16 * D + 128) * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    attr = true;
+  }
+  // enough CTAs to cover the SMs twice; each split keeps >= 2 key tiles
+  const int64_t base = static_cast<int64_t>(a.num_seqs) * a.Hk;
+  int splits = 1;
+  while (splits < kMaxSplits && base * splits < 2 * num_sms()) splits *= 2;
+  if (a.partial == nullptr || a.partial_bytes < attention_workspace(a.T, a.Hq, a.d)) splits = 1;
+  dim3 grid(splits, a.Hk, a.num_seqs);
+  attn_decode_kernel<<<grid, 128, SMEM, st>>>(a, splits);
+  dl_status s = launched("attention decode");
+  if (s != DL_OK || splits == 1) return s;
+  attn_combine_kernel<<<dim3(a.Hq, a.num_seqs), 128, 0, st>>>(a, splits);
+  return launched("attention combine");
 }
 
 }  // namespace dl

@@ -15,6 +15,11 @@ dl_status cuda_status(cudaError_t e, const char* what);
 constexpr int kNumSMsB200 = 148;
 int num_sms();
 
+// profile.cu: count a kernel launch and check it; event pair around a GEMM.
+dl_status launched(const char* what);
+int prof_begin(cudaStream_t st);
+void prof_end(int idx, cudaStream_t st, double bytes, double flops, int kind);
+
 // ---------------------------------------------------------------------------
 // tcgen05 GEMM family (tc_gemm.cu).
 //   C[token][feature] = sum_k act[token][act_koff + k] * W_seg[feature - begin][k]

@@ -84,7 +84,7 @@ dl_status launch_ew4(int64_t T, int64_t n, F f, cudaStream_t st, const char* wha
   const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
   if (blocks > cap) blocks = cap;
   ew4_kernel<<<static_cast<int>(blocks), 256, 0, st>>>(T, n4, f);
-  return cuda_status(cudaGetLastError(), what);
+  return launched(what);
 }
 
 __device__ __forceinline__ float4 take4(float* p, int clear) {
@@ -227,7 +227,7 @@ dl_status launch_rmsnorm(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bf
                          float eps, cudaStream_t st) {
   if (T <= 0) return DL_OK;
   rmsnorm_kernel<<<static_cast<int>(T), 256, 0, st>>>(x, g, y, static_cast<int>(h), eps);
-  return cuda_status(cudaGetLastError(), "rmsnorm");
+  return launched("rmsnorm");
 }
 dl_status launch_f32_to_bf16(float* acc, int64_t lda, __nv_bfloat16* out, int64_t ldo, int64_t T, int64_t n,
                              int clear, cudaStream_t st) {
@@ -256,14 +256,14 @@ dl_status launch_rope_cache(const RopeCacheArgs& a, cudaStream_t st) {
   const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
   if (blocks > cap) blocks = cap;
   rope_cache_kernel<<<static_cast<int>(blocks), 256, 0, st>>>(a);
-  return cuda_status(cudaGetLastError(), "rope_cache");
+  return launched("rope_cache");
 }
 dl_status launch_embedding(const __nv_bfloat16* table, int64_t vocab, int64_t h, const int32_t* ids, int64_t T,
                            __nv_bfloat16* out, cudaStream_t st) {
   (void)vocab;
   if (T <= 0) return DL_OK;
   embedding_kernel<<<static_cast<int>(T), 256, 0, st>>>(table, h, ids, out);
-  return cuda_status(cudaGetLastError(), "embedding");
+  return launched("embedding");
 }
 dl_status launch_unpermute(const __nv_bfloat16* src, __nv_bfloat16* dst, int P, int64_t T, int64_t w,
                            cudaStream_t st) {
@@ -272,7 +272,7 @@ dl_status launch_unpermute(const __nv_bfloat16* src, __nv_bfloat16* dst, int P, 
   int64_t blocks = (total + 255) / 256;
   if (blocks > 4096) blocks = 4096;
   unpermute_kernel<<<static_cast<int>(blocks), 256, 0, st>>>(src, dst, P, T, w / 8);
-  return cuda_status(cudaGetLastError(), "unpermute");
+  return launched("unpermute");
 }
 dl_status launch_copy2d(const void* src, int64_t lds, void* dst, int64_t ldd, int64_t rows, int64_t cols_bytes,
                         cudaStream_t st) {

@@ -167,17 +167,17 @@ dl_status run(const void* X, int64_t ldx, const void* A, int64_t lda, const void
     size_t smem = sizeof(float) * static_cast<size_t>(T) * kp;
     chain_small_kernel<E, TT><<<1, kWarps * 32, smem, st>>>(x, ldx, a, lda, b, ldb, y, ldy, (int)T, (int)m,
                                                              (int)n, (int)k, accumulate);
-    return cuda_status(cudaGetLastError(), "simt chain_small");
+    return launched("simt chain_small");
   }
   float* z = static_cast<float*>(zbuf);
   const int64_t ldz = (k + 3) & ~3;
   gemv_kernel<E, E, float, TT><<<static_cast<int>((k + rows_per_cta - 1) / rows_per_cta), kWarps * 32, 0, st>>>(
       b, ldb, (int)k, (int)n, x, ldx, (int)T, z, ldz, 0);
-  dl_status s = cuda_status(cudaGetLastError(), "simt stage1");
+  dl_status s = launched("simt stage1");
   if (s != DL_OK) return s;
   gemv_kernel<E, float, E, TT><<<static_cast<int>((m + rows_per_cta - 1) / rows_per_cta), kWarps * 32, 0, st>>>(
       a, lda, (int)m, (int)k, z, ldz, (int)T, y, ldy, accumulate);
-  return cuda_status(cudaGetLastError(), "simt stage2");
+  return launched("simt stage2");
 }
 
 template <typename E>

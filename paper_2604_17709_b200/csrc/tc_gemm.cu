@@ -445,7 +445,19 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   } else {
     grid = tiles < sms ? (tiles > 0 ? tiles : 1) : sms;
   }
+  // algorithmic work of this launch: every weight element once, the
+  // activation K-range of each segment once, every output element once
+  double flops = 0, bytes = 0;
+  for (int g = 0; g < p.nseg; ++g) {
+    const double rk = static_cast<double>(p.seg[g].rows) * p.seg[g].klen;
+    flops += 2.0 * p.T * rk;
+    bytes += 2.0 * rk + 2.0 * p.T * p.seg[g].klen;
+  }
+  bytes += static_cast<double>(p.T) * p.n_feat * (p.out.mode == OUT_BF16 ? (p.out.accumulate ? 4 : 2) : 4);
+  const int prof = prof_begin(st);
   kern<<<grid, kThreads, SMEM, st>>>(maps, a);
+  prof_end(prof, st, bytes, flops, SWAP ? 1 : 0);
+  launched("tc_gemm");
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error("tc_gemm<BN=%d,swap=%d> (T=%lld k_act=%lld nseg=%d klen=%lld/%lld/%lld koff=%lld/%lld/%lld "

@@ -1,0 +1,95 @@
+"""Whole-model decode / prefill steps of a rank-sharded decomposed LLaMA-3,
+driving only this library's C ABI (embedding gather, decomposed blocks,
+final RMSNorm, dense LM head).  PyTorch supplies device memory, streams,
+CUDA-Graph capture and (for the vocab-sharded logits) the all-gather.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib as L
+
+
+class DecomposedLlama:
+    """Rank `comm.rank` of a TP=`comm.world` decomposed LLaMA-3 (world 1 if comm is None).
+
+    layer_weights: iterable of per-layer dicts {A_<m>, B_<m>, g_attn, g_mlp}
+    (full, unsharded factors on this device; sharded here and then dropped).
+    embed [V x h], final_norm [h], lm_head_local [V/P x h] (this rank's vocab rows).
+    """
+
+    def __init__(self, shape, ranks: dict, layer_weights, embed: torch.Tensor, final_norm: torch.Tensor,
+                 lm_head_local: torch.Tensor, batch: int, max_seq: int, prefill_tokens: int = 0,
+                 comm: L.Comm | None = None, device="cuda"):
+        self.shape, self.ranks, self.comm = shape, ranks, comm
+        self.world = comm.world if comm else 1
+        self.rank = comm.rank if comm else 0
+        self.device = torch.device(device)
+        self.batch, self.max_seq = batch, max_seq
+        self.layers = []
+        for w in layer_weights:
+            self.layers.append(L.BlockWeights(w, self.world, self.rank))
+            del w
+        self.embed, self.final_norm, self.lm_head = embed, final_norm, lm_head_local
+        s = shape
+        hk_loc = s.n_kv_heads // self.world
+        nl = len(self.layers)
+        bf = torch.bfloat16
+        self.cache = torch.zeros((nl, 2, batch, hk_loc, max_seq, s.head_dim), dtype=bf, device=self.device)
+        self.dec_cfg = L.make_block_config(s, ranks, max_tokens=batch, max_seqs=batch)
+        self.dec_ws = torch.zeros(L.dl_block_workspace(self.dec_cfg, self.world), dtype=torch.uint8,
+                                  device=self.device)
+        # decode-step static buffers
+        self.ids = torch.zeros(batch, dtype=torch.int32, device=self.device)
+        self.cache_lens = torch.zeros(batch, dtype=torch.int32, device=self.device)
+        self.x = torch.zeros(batch, s.h, dtype=bf, device=self.device)
+        self.xn = torch.zeros(batch, s.h, dtype=bf, device=self.device)
+        vloc = lm_head_local.shape[0]
+        self.logits_local = torch.zeros(batch, vloc, dtype=bf, device=self.device)
+        self.logits = torch.zeros(self.world, batch, vloc, dtype=bf, device=self.device)
+        self.prefill_tokens = prefill_tokens
+        if prefill_tokens:
+            self.pre_cfg = L.make_block_config(s, ranks, max_tokens=prefill_tokens, max_seqs=1)
+            self.pre_ws = torch.zeros(L.dl_block_workspace(self.pre_cfg, self.world), dtype=torch.uint8,
+                                      device=self.device)
+            self.pre_cache = torch.zeros((nl, 2, 1, hk_loc, prefill_tokens, s.head_dim), dtype=bf,
+                                         device=self.device)
+            self.pre_ids = torch.zeros(prefill_tokens, dtype=torch.int32, device=self.device)
+            self.pre_pos = torch.arange(prefill_tokens, dtype=torch.int32, device=self.device)
+            self.pre_cu = torch.tensor([0, prefill_tokens], dtype=torch.int32, device=self.device)
+            self.pre_lens = torch.zeros(1, dtype=torch.int32, device=self.device)
+            self.pre_last = torch.tensor([prefill_tokens - 1], dtype=torch.int32, device=self.device)
+            self.pre_x = torch.zeros(prefill_tokens, s.h, dtype=bf, device=self.device)
+            self.pre_xl = torch.zeros(1, s.h, dtype=bf, device=self.device)
+            self.pre_xn = torch.zeros(1, s.h, dtype=bf, device=self.device)
+            self.pre_logits = torch.zeros(1, vloc, dtype=bf, device=self.device)
+
+    # one decode token for each of the `batch` sequences, at position cache_lens[b]
+    def decode_step(self):
+        s = self.shape
+        L.dl_embedding(self.embed, self.ids, self.x)
+        for i, lw in enumerate(self.layers):
+            L.dl_decomposed_block_forward(self.dec_cfg, lw, self.x, self.cache_lens, None, self.batch, L.DL_DECODE,
+                                          self.cache[i, 0], self.cache[i, 1], self.cache_lens, self.comm,
+                                          self.dec_ws)
+        L.dl_rmsnorm(self.x, self.final_norm, self.xn, s.rms_eps)
+        L.dl_dense(self.xn, self.lm_head, self.logits_local)
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.all_gather_into_tensor(self.logits, self.logits_local)
+        return self.logits_local if self.world == 1 else self.logits
+
+    # one sequence of prefill_tokens tokens; logits of its last token
+    def prefill_step(self):
+        s = self.shape
+        T = self.prefill_tokens
+        L.dl_embedding(self.embed, self.pre_ids, self.pre_x)
+        for i, lw in enumerate(self.layers):
+            L.dl_decomposed_block_forward(self.pre_cfg, lw, self.pre_x, self.pre_pos, self.pre_cu, 1, L.DL_PREFILL,
+                                          self.pre_cache[i, 0], self.pre_cache[i, 1], self.pre_lens, self.comm,
+                                          self.pre_ws)
+        L.dl_embedding(self.pre_x, self.pre_last, self.pre_xl)        # row gather of the last token
+        L.dl_rmsnorm(self.pre_xl, self.final_norm, self.pre_xn, s.rms_eps)
+        L.dl_dense(self.pre_xn, self.lm_head, self.pre_logits)
+        del T
+        return self.pre_logits
