@@ -239,18 +239,33 @@ def main():
     stream = torch.cuda.Stream(device=dev)
     hbm_gbs, bf16_burst, bf16_sust, peak_src = load_peaks()
 
-    def capture(fn, n_gemm_cap):
+    def capture(fn, n_gemm_cap=0):
+        """CUDA-Graph capture of one step.  n_gemm_cap > 0: the library records a CUDA
+        event pair around each tcgen05 GEMM (event nodes inside the graph); that graph is
+        only replayed for the per-kernel roofline, the timed graph has no event nodes
+        (they would break the programmatic-dependent-launch overlap between kernels)."""
         with torch.cuda.stream(stream):
             fn()                                   # eager warm-up (sets kernel attributes)
         torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
         c0 = dl.dl_launch_count()
-        dl.dl_profile_begin(n_gemm_cap)
+        if n_gemm_cap:
+            dl.dl_profile_begin(n_gemm_cap)
         with torch.cuda.graph(graph, stream=stream):
             fn()
-        dl.dl_profile_end()
+        if n_gemm_cap:
+            dl.dl_profile_end()
         launches = dl.dl_launch_count() - c0
         return graph, launches
+
+    def kernel_timing(fn, n_gemm_cap, replays=2):
+        """Replay the instrumented graph; per-launch GEMM event times of the last replay."""
+        g, _ = capture(fn, n_gemm_cap)
+        with torch.cuda.stream(stream):
+            for _ in range(replays):
+                g.replay()
+        torch.cuda.synchronize()
+        return g
 
     def timed(graph, steps, warmup):
         with torch.cuda.stream(stream):
@@ -294,11 +309,13 @@ def main():
 
     # ---- decode -------------------------------------------------------------
     n_cap = 8 * n_layers + 8
-    dgraph, dlaunch = capture(model.decode_step, n_cap)
+    dgraph, dlaunch = capture(model.decode_step)
     dms, dclk = timed(dgraph, args.steps, args.warmup)
     step_ms = dms / args.steps
     dec_tps = args.batch / (step_ms * 1e-3)
+    ig = kernel_timing(model.decode_step, n_cap)
     roof = gemm_roofline(1, "hbm")
+    del ig
     # algorithmic bytes per decode step per GPU: factors + LM head + KV reads
     pl = (2 * shape.h * ranks["q"] + (shape.h + shape.h_kv) * (ranks["k"] + ranks["v"]) + 2 * shape.h * ranks["o"]
           + (shape.h + shape.m) * (ranks["gate"] + ranks["up"] + ranks["down"]))
@@ -329,11 +346,13 @@ def main():
     # ---- prefill ------------------------------------------------------------
     prefill = None
     if args.prefill_tokens:
-        pgraph, plaunch = capture(model.prefill_step, n_cap)
+        pgraph, plaunch = capture(model.prefill_step)
         psteps = max(1, args.prefill_steps)
         pms, pclk = timed(pgraph, psteps, min(args.warmup, 3))
         p_step_ms = pms / psteps
+        ig = kernel_timing(model.prefill_step, n_cap, replays=1)
         proof = gemm_roofline(0, "tensor")
+        del ig
         T = args.prefill_tokens
         pf = (2 * T * n_layers * pl + n_layers * 4 * (T * (T + 1) / 2) * shape.h) / world
         prefill = {"value": T / (p_step_ms * 1e-3), "unit": "tokens/s", "ms_per_step": p_step_ms,

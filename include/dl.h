@@ -256,6 +256,11 @@ dl_status dl_profile_end(void);
 int dl_profile_count(void);
 dl_status dl_profile_get(int i, float *ms, double *bytes, double *flops,
                          int *kind);
+/* Debug timeline of the tcgen05 GEMM CTAs (device_buf: >= 8 u64 per CTA of
+ * the next launches, or NULL to disable): globaltimer ns at entry, setup
+ * done, first TMA issued, first stage landed, last MMA issued, epilogue
+ * done, exit; slot 7 = SM id. */
+dl_status dl_debug_gemm_trace(void *device_buf);
 
 #ifdef __cplusplus
 }

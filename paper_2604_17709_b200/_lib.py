@@ -23,7 +23,7 @@ EXPORTS = ("dl_last_error", "dl_version", "dl_device_ok", "dl_comm_create", "dl_
            "dl_lowrank_linear_workspace", "dl_lowrank_linear", "dl_tp_plan", "dl_tp_shard_factors",
            "dl_block_workspace", "dl_decomposed_block_forward", "dl_embedding", "dl_rmsnorm",
            "dl_dense_workspace", "dl_dense", "dl_launch_count", "dl_profile_begin", "dl_profile_end",
-           "dl_profile_count", "dl_profile_get")
+           "dl_profile_count", "dl_profile_get", "dl_debug_gemm_trace")
 
 
 class DLError(RuntimeError):
@@ -92,6 +92,7 @@ def load():
             lib.dl_dense.argtypes = [P, I64, P, I64, P, I64, I64, I64, I64, P, ctypes.c_size_t, P]
             lib.dl_profile_begin.argtypes = [I]
             lib.dl_profile_get.argtypes = [I, P, P, P, P]
+            lib.dl_debug_gemm_trace.argtypes = [P]
             for name in EXPORTS[3:]:
                 getattr(lib, name).restype = I
             lib.dl_launch_count.restype = ctypes.c_longlong
@@ -331,3 +332,8 @@ def dl_profile_records():
         _check(L.dl_profile_get(i, ctypes.byref(ms), ctypes.byref(b), ctypes.byref(f), ctypes.byref(k)))
         out.append((ms.value, b.value, f.value, k.value))
     return out
+
+
+def dl_debug_gemm_trace(buf: torch.Tensor | None):
+    """Enable (int64 device tensor, >= 8 per CTA) or disable (None) the GEMM CTA timeline."""
+    _check(load().dl_debug_gemm_trace(_ptr(buf)))

@@ -84,6 +84,8 @@ __device__ __forceinline__ void load_tile(uint32_t sbase, const __nv_bfloat16* s
 // =============================== prefill ===================================
 __global__ void __launch_bounds__(128) attn_prefill_kernel(AttnArgs a) {
   extern __shared__ __align__(1024) uint8_t sm[];
+  pdl_wait();
+  pdl_trigger();
   const int s = blockIdx.z, h = blockIdx.y;
   const int n_new = a.cu_seqlens[s + 1] - a.cu_seqlens[s];
   const int q0 = blockIdx.x * QT;
@@ -244,6 +246,8 @@ constexpr int PART = D + 2;
 
 __global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, int splits) {
   extern __shared__ __align__(1024) uint8_t sm[];
+  pdl_wait();
+  pdl_trigger();
   const int s = blockIdx.z, kvh = blockIdx.y, sp = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t4 = lane & 3;
@@ -417,6 +421,8 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, int splits
 
 // merge key splits: one CTA (128 threads = d) per (token, head)
 __global__ void __launch_bounds__(128) attn_combine_kernel(AttnArgs a, int splits) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t s = blockIdx.y;
   const int h = blockIdx.x, d = threadIdx.x;
   const float* pp = a.partial + (s * a.Hq + h) * splits * PART;
@@ -455,8 +461,7 @@ dl_status launch_attention(const AttnArgs& a, cudaStream_t st) {
     // grid.x covers the longest sequence: bounded by T
     const int qtiles = static_cast<int>((a.T + QT - 1) / QT);
     dim3 grid(qtiles, a.Hq, a.num_seqs);
-    attn_prefill_kernel<<<grid, 128, SMEM, st>>>(a);
-    return launched("attention prefill");
+    return launch_pdl(attn_prefill_kernel, grid, dim3(128), SMEM, st, "attention prefill", a);
   }
   constexpr int SMEM = 16 * ROW_BYTES + 4 * TILE_BYTES + (4 * 16 * D + 128) * 4;
   static bool attr = false;
@@ -470,11 +475,9 @@ dl_status launch_attention(const AttnArgs& a, cudaStream_t st) {
   while (splits < kMaxSplits && base * splits < 2 * num_sms()) splits *= 2;
   if (a.partial == nullptr || a.partial_bytes < attention_workspace(a.T, a.Hq, a.d)) splits = 1;
   dim3 grid(splits, a.Hk, a.num_seqs);
-  attn_decode_kernel<<<grid, 128, SMEM, st>>>(a, splits);
-  dl_status s = launched("attention decode");
+  dl_status s = launch_pdl(attn_decode_kernel, grid, dim3(128), SMEM, st, "attention decode", a, splits);
   if (s != DL_OK || splits == 1) return s;
-  attn_combine_kernel<<<dim3(a.Hq, a.num_seqs), 128, 0, st>>>(a, splits);
-  return launched("attention combine");
+  return launch_pdl(attn_combine_kernel, dim3(a.Hq, a.num_seqs), dim3(128), 0, st, "attention combine", a, splits);
 }
 
 }  // namespace dl

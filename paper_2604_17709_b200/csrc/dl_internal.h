@@ -20,6 +20,32 @@ dl_status launched(const char* what);
 int prof_begin(cudaStream_t st);
 void prof_end(int idx, cudaStream_t st, double bytes, double flops, int kind);
 
+// Programmatic dependent launch (PDL).  Every kernel of this library is
+// launched with programmatic stream serialization: it may start while its
+// predecessor drains, runs pdl_trigger() early so its own successor can do
+// the same, and calls pdl_wait() before touching anything a predecessor
+// produced (the GEMMs stream their static weights before that point).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+dl_status launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                     const char* what, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+  if (e != cudaSuccess) return cuda_status(e, what);
+  return launched(what);
+}
+
 // ---------------------------------------------------------------------------
 // tcgen05 GEMM family (tc_gemm.cu).
 //   C[token][feature] = sum_k act[token][act_koff + k] * W_seg[feature - begin][k]
@@ -67,6 +93,10 @@ struct GemmProblem {
 // Picks the tile configuration (swap-AB for T <= 256, stream-K when the
 // output is fp32-reduced) and launches.  `stream_k` requires OUT_F32_RED.
 dl_status tc_gemm(const GemmProblem& p, bool stream_k, cudaStream_t st);
+// debug timeline: when buf != NULL every GEMM CTA writes 8 u64 at buf[cta*8]
+// (globaltimer ns at entry, setup done, first TMA, first stage landed, last
+// MMA issued, epilogue done, exit; and its SM id)
+dl_status set_gemm_trace(void* buf);
 
 // ---------------------------------------------------------------------------
 // SIMT skinny chain (simt_chain.cu): Y[T x m] (+)= (X B^T) A^T, T <= 16.

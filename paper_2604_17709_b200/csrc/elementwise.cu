@@ -1,11 +1,13 @@
 // Memory-bound block pieces (bf16 storage, fp32 math), each one pass over
-// its tensors with 16-byte vector accesses:
+// its tensors with 8/16-byte vector accesses and 2-D grids (row = token,
+// x = column group) so no per-element 64-bit index division:
 //   RMSNorm (LLaMA-3 pre-norm; reading c9), the epilogues that turn the fp32
 //   rank-partial accumulators into the next operand (consume-and-clear: the
 //   accumulator is zeroed as it is read so the next stream-K GEMM can
 //   red.add into it without a separate memset), SiLU(gate)*up, residual add,
 //   RoPE + KV-cache append ("in-place rotary position
 //   embedding"), embedding gather and the all-gather un-permute.
+// All kernels are PDL-aware (see dl_internal.h).
 #include <math.h>
 
 #include "dl_internal.h"
@@ -23,6 +25,8 @@ __device__ __forceinline__ float warp_sum(float v) {
 __global__ void __launch_bounds__(256) rmsnorm_kernel(const __nv_bfloat16* __restrict__ x,
                                                       const __nv_bfloat16* __restrict__ g,
                                                       __nv_bfloat16* __restrict__ y, int h, float eps) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[8];
   const int64_t t = blockIdx.x;
   const uint4* xr = reinterpret_cast<const uint4*>(x + t * h);
@@ -63,28 +67,21 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const __nv_bfloat16* __res
   }
 }
 
-// Generic 2-D elementwise over [T x n] in groups of 4 columns (n % 4 == 0).
+// 2-D elementwise over [T x n] in groups of 4 columns: grid (ceil(n/4/256), T).
 template <typename F>
-__global__ void ew4_kernel(int64_t T, int64_t n4, F f) {
-  const int64_t total = T * n4;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t t = i / n4;
-    const int64_t c = (i - t * n4) * 4;
-    f(t, c);
-  }
+__global__ void __launch_bounds__(256) ew4_kernel(int n4, F f) {
+  pdl_wait();
+  pdl_trigger();
+  const int c4 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c4 < n4) f(static_cast<int64_t>(blockIdx.y), c4 * 4);
 }
 
 template <typename F>
 dl_status launch_ew4(int64_t T, int64_t n, F f, cudaStream_t st, const char* what) {
   if (T <= 0 || n <= 0) return DL_OK;
-  const int64_t n4 = n / 4;
-  const int64_t total = T * n4;
-  int64_t blocks = (total + 255) / 256;
-  const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
-  if (blocks > cap) blocks = cap;
-  ew4_kernel<<<static_cast<int>(blocks), 256, 0, st>>>(T, n4, f);
-  return launched(what);
+  const int n4 = static_cast<int>(n / 4);
+  dim3 grid((n4 + 255) / 256, static_cast<unsigned>(T));
+  return launch_pdl(ew4_kernel<F>, grid, dim3(256), 0, st, what, n4, f);
 }
 
 __device__ __forceinline__ float4 take4(float* p, int clear) {
@@ -108,14 +105,14 @@ __device__ __forceinline__ float silu(float g) { return g / (1.f + __expf(-g)); 
 
 struct F32ToBf16 {
   float* acc; int64_t lda; __nv_bfloat16* out; int64_t ldo; int clear;
-  __device__ void operator()(int64_t t, int64_t c) const {
+  __device__ void operator()(int64_t t, int c) const {
     float4 v = take4(acc + t * lda + c, clear);
     store4(out + t * ldo + c, v.x, v.y, v.z, v.w);
   }
 };
 struct ResidualAdd {
   float* acc; int64_t lda; __nv_bfloat16* x; int64_t ldx; int clear;
-  __device__ void operator()(int64_t t, int64_t c) const {
+  __device__ void operator()(int64_t t, int c) const {
     float4 v = take4(acc + t * lda + c, clear);
     float4 r = load4(x + t * ldx + c);
     store4(x + t * ldx + c, r.x + v.x, r.y + v.y, r.z + v.z, r.w + v.w);
@@ -123,7 +120,7 @@ struct ResidualAdd {
 };
 struct ResidualAddBf16 {
   const __nv_bfloat16* y; int64_t ldy; __nv_bfloat16* x; int64_t ldx;
-  __device__ void operator()(int64_t t, int64_t c) const {
+  __device__ void operator()(int64_t t, int c) const {
     float4 v = load4(y + t * ldy + c);
     float4 r = load4(x + t * ldx + c);
     store4(x + t * ldx + c, r.x + v.x, r.y + v.y, r.z + v.z, r.w + v.w);
@@ -131,7 +128,7 @@ struct ResidualAddBf16 {
 };
 struct SiluMulF32 {
   float* acc; int64_t lda; __nv_bfloat16* out; int64_t ldo; int64_t m; int clear;
-  __device__ void operator()(int64_t t, int64_t c) const {
+  __device__ void operator()(int64_t t, int c) const {
     float4 g = take4(acc + t * lda + c, clear);
     float4 u = take4(acc + t * lda + m + c, clear);
     store4(out + t * ldo + c, silu(g.x) * u.x, silu(g.y) * u.y, silu(g.z) * u.z, silu(g.w) * u.w);
@@ -139,86 +136,88 @@ struct SiluMulF32 {
 };
 struct SiluMulBf16 {
   const __nv_bfloat16* src; int64_t lds; __nv_bfloat16* out; int64_t ldo; int64_t m;
-  __device__ void operator()(int64_t t, int64_t c) const {
+  __device__ void operator()(int64_t t, int c) const {
     float4 g = load4(src + t * lds + c);
     float4 u = load4(src + t * lds + m + c);
     store4(out + t * ldo + c, silu(g.x) * u.x, silu(g.y) * u.y, silu(g.z) * u.z, silu(g.w) * u.w);
   }
 };
 
-// RoPE + cache append.  One thread per (token, head, 2 pairs).
-__global__ void rope_cache_kernel(RopeCacheArgs a) {
+// RoPE + cache append.  grid (ceil(heads*d/4 / 128), T); one thread per 4 dims
+// = two rotation pairs (2i, 2i+1) by pos * theta^(-2i/d).
+__global__ void __launch_bounds__(128) rope_cache_kernel(RopeCacheArgs a) {
+  pdl_wait();
+  pdl_trigger();
   const int heads = a.Hq + 2 * a.Hk;
   const int quads = a.d / 4;
-  const int64_t total = a.T * heads * quads;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t t = i / (heads * quads);
-    const int rem = static_cast<int>(i - t * heads * quads);
-    const int hd = rem / quads;
-    const int e = (rem - hd * quads) * 4;   // first of 4 dims = pairs (e, e+1), (e+2, e+3)
-    const int64_t col = static_cast<int64_t>(hd) * a.d + e;
-    float4 v;
-    if (a.acc) {
-      v = take4(const_cast<float*>(a.acc) + t * a.ld_src + col, a.clear);
-    } else {
-      v = load4(a.src + t * a.ld_src + col);
-    }
-    if (hd < a.Hq + a.Hk) {   // rotate q and k (pair (2i, 2i+1) by pos * theta^(-2i/d))
-      const double pos = static_cast<double>(a.positions[t]);
-      const double lt = log(static_cast<double>(a.theta));
-      double s0, c0, s1, c1;
-      sincos(pos * exp(-lt * static_cast<double>(e) / a.d), &s0, &c0);
-      sincos(pos * exp(-lt * static_cast<double>(e + 2) / a.d), &s1, &c1);
-      const float cs0 = static_cast<float>(c0), sn0 = static_cast<float>(s0);
-      const float cs1 = static_cast<float>(c1), sn1 = static_cast<float>(s1);
-      v = make_float4(v.x * cs0 - v.y * sn0, v.x * sn0 + v.y * cs0, v.z * cs1 - v.w * sn1, v.z * sn1 + v.w * cs1);
-    }
-    if (hd < a.Hq) {
-      store4(a.q_out + t * static_cast<int64_t>(a.Hq) * a.d + col, v.x, v.y, v.z, v.w);
-    } else {
-      int s;
-      int64_t cpos;
-      if (a.decode) {
-        s = static_cast<int>(t);
-        cpos = a.cache_lens[s];
-      } else {
-        int lo = 0, hi = a.num_seqs - 1;   // last s with cu[s] <= t
-        while (lo < hi) {
-          int mid = (lo + hi + 1) >> 1;
-          if (a.cu_seqlens[mid] <= t) lo = mid; else hi = mid - 1;
-        }
-        s = lo;
-        cpos = a.cache_lens[s] + (t - a.cu_seqlens[s]);
-      }
-      const bool is_k = hd < a.Hq + a.Hk;
-      const int kvh = is_k ? hd - a.Hq : hd - a.Hq - a.Hk;
-      __nv_bfloat16* dst = (is_k ? a.k_cache : a.v_cache) +
-                           ((static_cast<int64_t>(s) * a.Hk + kvh) * a.max_seq + cpos) * a.d + e;
-      store4(dst, v.x, v.y, v.z, v.w);
-    }
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= heads * quads) return;
+  const int64_t t = blockIdx.y;
+  const int hd = i / quads;
+  const int e = (i - hd * quads) * 4;
+  const int64_t col = static_cast<int64_t>(hd) * a.d + e;
+  float4 v;
+  if (a.acc) {
+    v = take4(const_cast<float*>(a.acc) + t * a.ld_src + col, a.clear);
+  } else {
+    v = load4(a.src + t * a.ld_src + col);
   }
+  if (hd < a.Hq + a.Hk) {
+    const double pos = static_cast<double>(a.positions[t]);
+    const double lt = log(static_cast<double>(a.theta));
+    double s0, c0, s1, c1;
+    sincos(pos * exp(-lt * static_cast<double>(e) / a.d), &s0, &c0);
+    sincos(pos * exp(-lt * static_cast<double>(e + 2) / a.d), &s1, &c1);
+    const float cs0 = static_cast<float>(c0), sn0 = static_cast<float>(s0);
+    const float cs1 = static_cast<float>(c1), sn1 = static_cast<float>(s1);
+    v = make_float4(v.x * cs0 - v.y * sn0, v.x * sn0 + v.y * cs0, v.z * cs1 - v.w * sn1, v.z * sn1 + v.w * cs1);
+  }
+  if (hd < a.Hq) {
+    store4(a.q_out + t * static_cast<int64_t>(a.Hq) * a.d + col, v.x, v.y, v.z, v.w);
+    return;
+  }
+  int s;
+  int64_t cpos;
+  if (a.decode) {
+    s = static_cast<int>(t);
+    cpos = a.cache_lens[s];
+  } else {
+    int lo = 0, hi = a.num_seqs - 1;   // last s with cu[s] <= t
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (a.cu_seqlens[mid] <= t) lo = mid; else hi = mid - 1;
+    }
+    s = lo;
+    cpos = a.cache_lens[s] + (t - a.cu_seqlens[s]);
+  }
+  const bool is_k = hd < a.Hq + a.Hk;
+  const int kvh = is_k ? hd - a.Hq : hd - a.Hq - a.Hk;
+  __nv_bfloat16* dst = (is_k ? a.k_cache : a.v_cache) +
+                       ((static_cast<int64_t>(s) * a.Hk + kvh) * a.max_seq + cpos) * a.d + e;
+  store4(dst, v.x, v.y, v.z, v.w);
 }
 
-__global__ void embedding_kernel(const __nv_bfloat16* __restrict__ table, int64_t h, const int32_t* __restrict__ ids,
-                                 __nv_bfloat16* __restrict__ out) {
+__global__ void __launch_bounds__(256) embedding_kernel(const __nv_bfloat16* __restrict__ table, int64_t h,
+                                                        const int32_t* __restrict__ ids,
+                                                        __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t t = blockIdx.x;
   const uint4* src = reinterpret_cast<const uint4*>(table + static_cast<int64_t>(ids[t]) * h);
   uint4* dst = reinterpret_cast<uint4*>(out + t * h);
   for (int i = threadIdx.x; i < h / 8; i += blockDim.x) dst[i] = src[i];
 }
 
-__global__ void unpermute_kernel(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dst, int P,
-                                 int64_t T, int64_t w8) {
-  const int64_t total = static_cast<int64_t>(P) * T * w8;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t p = i / (T * w8);
-    const int64_t r = i - p * T * w8;
-    const int64_t t = r / w8;
-    const int64_t c = r - t * w8;
-    reinterpret_cast<uint4*>(dst)[t * P * w8 + p * w8 + c] = reinterpret_cast<const uint4*>(src)[i];
-  }
+// [P][T][w] -> [T][P*w]; grid (ceil(w/8 / 128), T, P)
+__global__ void __launch_bounds__(128) unpermute_kernel(const __nv_bfloat16* __restrict__ src,
+                                                        __nv_bfloat16* __restrict__ dst, int P, int64_t T,
+                                                        int w8) {
+  pdl_wait();
+  pdl_trigger();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= w8) return;
+  const int64_t t = blockIdx.y, p = blockIdx.z;
+  reinterpret_cast<uint4*>(dst)[(t * P + p) * w8 + c] = reinterpret_cast<const uint4*>(src)[(p * T + t) * w8 + c];
 }
 
 }  // namespace
@@ -226,8 +225,8 @@ __global__ void unpermute_kernel(const __nv_bfloat16* __restrict__ src, __nv_bfl
 dl_status launch_rmsnorm(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bfloat16* y, int64_t T, int64_t h,
                          float eps, cudaStream_t st) {
   if (T <= 0) return DL_OK;
-  rmsnorm_kernel<<<static_cast<int>(T), 256, 0, st>>>(x, g, y, static_cast<int>(h), eps);
-  return launched("rmsnorm");
+  return launch_pdl(rmsnorm_kernel, dim3(static_cast<unsigned>(T)), dim3(256), 0, st, "rmsnorm", x, g, y,
+                    static_cast<int>(h), eps);
 }
 dl_status launch_f32_to_bf16(float* acc, int64_t lda, __nv_bfloat16* out, int64_t ldo, int64_t T, int64_t n,
                              int clear, cudaStream_t st) {
@@ -251,28 +250,23 @@ dl_status launch_silu_mul_bf16(const __nv_bfloat16* src, int64_t lds, __nv_bfloa
 }
 dl_status launch_rope_cache(const RopeCacheArgs& a, cudaStream_t st) {
   if (a.T <= 0) return DL_OK;
-  const int64_t total = a.T * (a.Hq + 2 * a.Hk) * (a.d / 4);
-  int64_t blocks = (total + 255) / 256;
-  const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
-  if (blocks > cap) blocks = cap;
-  rope_cache_kernel<<<static_cast<int>(blocks), 256, 0, st>>>(a);
-  return launched("rope_cache");
+  const int per_tok = (a.Hq + 2 * a.Hk) * (a.d / 4);
+  dim3 grid((per_tok + 127) / 128, static_cast<unsigned>(a.T));
+  return launch_pdl(rope_cache_kernel, grid, dim3(128), 0, st, "rope_cache", a);
 }
 dl_status launch_embedding(const __nv_bfloat16* table, int64_t vocab, int64_t h, const int32_t* ids, int64_t T,
                            __nv_bfloat16* out, cudaStream_t st) {
   (void)vocab;
   if (T <= 0) return DL_OK;
-  embedding_kernel<<<static_cast<int>(T), 256, 0, st>>>(table, h, ids, out);
-  return launched("embedding");
+  return launch_pdl(embedding_kernel, dim3(static_cast<unsigned>(T)), dim3(256), 0, st, "embedding", table, h, ids,
+                    out);
 }
 dl_status launch_unpermute(const __nv_bfloat16* src, __nv_bfloat16* dst, int P, int64_t T, int64_t w,
                            cudaStream_t st) {
   if (T <= 0) return DL_OK;
-  const int64_t total = static_cast<int64_t>(P) * T * (w / 8);
-  int64_t blocks = (total + 255) / 256;
-  if (blocks > 4096) blocks = 4096;
-  unpermute_kernel<<<static_cast<int>(blocks), 256, 0, st>>>(src, dst, P, T, w / 8);
-  return launched("unpermute");
+  const int w8 = static_cast<int>(w / 8);
+  dim3 grid((w8 + 127) / 128, static_cast<unsigned>(T), static_cast<unsigned>(P));
+  return launch_pdl(unpermute_kernel, grid, dim3(128), 0, st, "unpermute", src, dst, P, T, w8);
 }
 dl_status launch_copy2d(const void* src, int64_t lds, void* dst, int64_t ldd, int64_t rows, int64_t cols_bytes,
                         cudaStream_t st) {

@@ -131,6 +131,8 @@ template <typename E, typename I, typename O, int TT>
 __global__ void __launch_bounds__(kWarps * 32)
     gemv_kernel(const E* __restrict__ W, int64_t ldw, int R, int C, const I* __restrict__ in, int64_t ldi,
                 int T, O* __restrict__ out, int64_t ldo, int accumulate) {
+  pdl_wait();
+  pdl_trigger();
   const int warp = threadIdx.x >> 5;
   const int row0 = (blockIdx.x * kWarps + warp) * kRows;
   if (row0 >= R) return;
@@ -144,6 +146,8 @@ __global__ void __launch_bounds__(kWarps * 32)
                        const E* __restrict__ B, int64_t ldb, E* __restrict__ Y, int64_t ldy, int T,
                        int m, int n, int k, int accumulate) {
   extern __shared__ float zs[];   // [T x k_pad]
+  pdl_wait();
+  pdl_trigger();
   const int kp = (k + 3) & ~3;
   const int warp = threadIdx.x >> 5;
   for (int row0 = warp * kRows; row0 < k; row0 += kWarps * kRows)
@@ -165,19 +169,16 @@ dl_status run(const void* X, int64_t ldx, const void* A, int64_t lda, const void
   if (k <= 1024 && (m + n) * k <= (1 << 16)) {
     const int kp = static_cast<int>((k + 3) & ~3);
     size_t smem = sizeof(float) * static_cast<size_t>(T) * kp;
-    chain_small_kernel<E, TT><<<1, kWarps * 32, smem, st>>>(x, ldx, a, lda, b, ldb, y, ldy, (int)T, (int)m,
-                                                             (int)n, (int)k, accumulate);
-    return launched("simt chain_small");
+    return launch_pdl(chain_small_kernel<E, TT>, dim3(1), dim3(kWarps * 32), smem, st, "simt chain_small", x, ldx, a,
+                      lda, b, ldb, y, ldy, (int)T, (int)m, (int)n, (int)k, accumulate);
   }
   float* z = static_cast<float*>(zbuf);
   const int64_t ldz = (k + 3) & ~3;
-  gemv_kernel<E, E, float, TT><<<static_cast<int>((k + rows_per_cta - 1) / rows_per_cta), kWarps * 32, 0, st>>>(
-      b, ldb, (int)k, (int)n, x, ldx, (int)T, z, ldz, 0);
-  dl_status s = launched("simt stage1");
+  dl_status s = launch_pdl(gemv_kernel<E, E, float, TT>, dim3(static_cast<int>((k + rows_per_cta - 1) / rows_per_cta)),
+                           dim3(kWarps * 32), 0, st, "simt stage1", b, ldb, (int)k, (int)n, x, ldx, (int)T, z, ldz, 0);
   if (s != DL_OK) return s;
-  gemv_kernel<E, float, E, TT><<<static_cast<int>((m + rows_per_cta - 1) / rows_per_cta), kWarps * 32, 0, st>>>(
-      a, lda, (int)m, (int)k, z, ldz, (int)T, y, ldy, accumulate);
-  return launched("simt stage2");
+  return launch_pdl(gemv_kernel<E, float, E, TT>, dim3(static_cast<int>((m + rows_per_cta - 1) / rows_per_cta)),
+                    dim3(kWarps * 32), 0, st, "simt stage2", a, lda, (int)m, (int)k, z, ldz, (int)T, y, ldy, accumulate);
 }
 
 template <typename E>

@@ -30,6 +30,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <mutex>
 
@@ -41,7 +42,7 @@ namespace {
 
 constexpr int BK = 64;   // K elements per stage = one 128-byte swizzle row
 constexpr int BM = 128;  // MMA M = TMEM lanes
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;   // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
 
 struct KSeg {
   int feat_begin, feat_end;  // global output features [begin, end)
@@ -75,6 +76,18 @@ struct __align__(64) KMaps {
   CUtensorMap act;
   CUtensorMap w[3];
 };
+
+__device__ unsigned long long* g_trace = nullptr;
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned s;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(s));
+  return s;
+}
 
 struct Job {
   int seg, feat0, tok0, kb0, kb1;
@@ -163,6 +176,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  unsigned long long* tr = g_trace ? g_trace + blockIdx.x * 8 : nullptr;   // debug timeline
+  if (tr && threadIdx.x == 0) { tr[0] = gtime(); tr[7] = smid(); }
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&maps.act);
@@ -173,7 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&accf_bar[b], 1);
-      ptx::mbar_init(&acce_bar[b], 4);
+      ptx::mbar_init(&acce_bar[b], 8);
     }
     ptx::fence_barrier_init();
   }
@@ -182,7 +197,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = tmem_slot;
+  if (tr && threadIdx.x == 0) tr[1] = gtime();
 
+  pdl_trigger();   // let the next kernel launch and prefetch its own weights early
   JobIter it(a, blockIdx.x, gridDim.x);
   Job j;
 
@@ -193,24 +210,43 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_a = ptx::policy_evict_last();    // activations: re-read
       int stage = 0;
       uint32_t phase = 0;
+      // PDL: the static weight tiles of the first STAGES units are requested
+      // before griddepcontrol.wait (they do not depend on the predecessor);
+      // their activation halves follow once the predecessor has completed.
+      int u = 0;
+      bool waited = false;
+      if (tr) tr[2] = gtime();
+      int pend_c0[STAGES], pend_c1[STAGES];
+      auto flush_pending = [&]() {
+        pdl_wait();
+        waited = true;
+        for (int i = 0; i < u && i < STAGES; ++i) {
+          uint8_t* dst = smem + i * STAGE_BYTES + (SWAP ? P_BYTES : 0);
+          ptx::tma_load_2d(dst, &maps.act, &full_bar[i], pend_c0[i], pend_c1[i], pol_a);
+        }
+      };
       while (it.next(j, FEAT_TILE, TOK_TILE)) {
         const KSeg& s = a.seg[j.seg];
-        for (int kb = j.kb0; kb < j.kb1; ++kb) {
+        for (int kb = j.kb0; kb < j.kb1; ++kb, ++u) {
+          if (u >= STAGES && !waited) flush_pending();
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sp = smem + stage * STAGE_BYTES;
           uint8_t* sq = sp + P_BYTES;
           ptx::mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES);
           const int kx = kb * BK;
-          if (SWAP) {
-            ptx::tma_load_2d(sp, &maps.w[j.seg], &full_bar[stage], kx, j.feat0 - s.feat_begin, pol_w);
-            ptx::tma_load_2d(sq, &maps.act, &full_bar[stage], s.act_koff + kx, j.tok0, pol_a);
+          uint8_t* sw = SWAP ? sp : sq;
+          uint8_t* sa = SWAP ? sq : sp;
+          ptx::tma_load_2d(sw, &maps.w[j.seg], &full_bar[stage], kx, j.feat0 - s.feat_begin, pol_w);
+          if (waited) {
+            ptx::tma_load_2d(sa, &maps.act, &full_bar[stage], s.act_koff + kx, j.tok0, pol_a);
           } else {
-            ptx::tma_load_2d(sp, &maps.act, &full_bar[stage], s.act_koff + kx, j.tok0, pol_a);
-            ptx::tma_load_2d(sq, &maps.w[j.seg], &full_bar[stage], kx, j.feat0 - s.feat_begin, pol_w);
+            pend_c0[u] = s.act_koff + kx;
+            pend_c1[u] = j.tok0;
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
+      if (!waited) flush_pending();
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (one thread) =====================
@@ -225,6 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = j.kb0; kb < j.kb1; ++kb) {
           ptx::mbar_wait(&full_bar[stage], phase);
+          if (tr && tr[3] == 0) tr[3] = gtime();
           ptx::tc_fence_after();
           const uint32_t sp = ptx::smem_u32(smem + stage * STAGE_BYTES);
           const uint32_t sq = sp + P_BYTES;
@@ -241,20 +278,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::umma_commit(&accf_bar[acc]);        // accumulator ready for the epilogue
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
+      if (tr) tr[4] = gtime();
     }
   } else {
-    // ===================== epilogue (warps 2..5) =====================
+    // ===================== epilogue (warps 2..9) =====================
+    // 8 warps = 2 per SM sub-partition so the per-element store latency of
+    // one warp hides behind the other; warp e handles TMEM lane quarter
+    // (warp & 3) and column half (e / 4) of the accumulator.
+    pdl_wait();                                // outputs may alias a predecessor's buffers
     const int quarter = warp & 3;              // TMEM lane quarter this warp may access
+    const int half = (warp - 2) >> 2;
     const int row = quarter * 32 + lane;       // accumulator row (M index)
+    constexpr int HALF_COLS = BN / 2;
     int acc = 0;
     uint32_t acc_phase = 0;
     while (it.next(j, FEAT_TILE, TOK_TILE)) {
       const KSeg& s = a.seg[j.seg];
       ptx::mbar_wait(&accf_bar[acc], acc_phase);
+      if (tr && warp == 2 && lane == 0) tr[5] = gtime();   // accumulator of this job ready
       ptx::tc_fence_after();
       const bool has_k = j.kb1 > j.kb0;
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
+      for (int c0 = half * HALF_COLS; c0 < (half + 1) * HALF_COLS; c0 += 32) {
         uint32_t r[32];
         if (has_k) {
           ptx::tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + c0, r);
@@ -264,25 +309,36 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int i = 0; i < 32; ++i) r[i] = 0u;
         }
         if (SWAP) {
-          // row = feature, columns = tokens
+          // row = feature, the 32 columns = consecutive tokens (stride tstride)
           const int f = j.feat0 + row;
-          if (f < s.write_end) {
-#pragma unroll 4
-            for (int i = 0; i < 32; ++i) {
-              const int tok = j.tok0 + c0 + i;
-              if (tok < a.T) {
-                const float v = __uint_as_float(r[i]);
-                const long long idx = out_index(a, s, tok, f);
-                if (a.mode == OUT_F32_RED) {
-                  ptx::red_add_f32(static_cast<float*>(a.out) + idx, v);
-                } else if (a.mode == OUT_F32_STORE) {
-                  static_cast<float*>(a.out)[idx] = v;
-                } else {
-                  __nv_bfloat16* o = static_cast<__nv_bfloat16*>(a.out) + idx;
-                  float w = v;
-                  if (a.accumulate) w += __bfloat162float(*o);
-                  *o = __float2bfloat16_rn(w);
-                }
+          const int tok0 = j.tok0 + c0;
+          const int ntok = a.T - tok0;
+          if (f < s.write_end && ntok > 0) {
+            const long long tstride = a.scatter_p <= 1 ? a.ldo : a.slab;
+            const long long base = out_index(a, s, tok0, f);
+            if (a.mode == OUT_F32_RED) {
+              float* p = static_cast<float*>(a.out) + base;
+#pragma unroll
+              for (int i = 0; i < 32; ++i, p += tstride)
+                if (i < ntok) ptx::red_add_f32(p, __uint_as_float(r[i]));
+            } else if (a.mode == OUT_F32_STORE) {
+              float* p = static_cast<float*>(a.out) + base;
+#pragma unroll
+              for (int i = 0; i < 32; ++i, p += tstride)
+                if (i < ntok) *p = __uint_as_float(r[i]);
+            } else {
+              __nv_bfloat16* p = static_cast<__nv_bfloat16*>(a.out) + base;
+              const bool accum = a.accumulate != 0;
+#pragma unroll
+              for (int i0 = 0; i0 < 32; i0 += 8) {
+                float old[8];
+                __nv_bfloat16* q = p;
+#pragma unroll
+                for (int i = 0; i < 8; ++i, q += tstride)
+                  old[i] = (accum && i0 + i < ntok) ? __bfloat162float(*q) : 0.f;
+#pragma unroll
+                for (int i = 0; i < 8; ++i, p += tstride)
+                  if (i0 + i < ntok) *p = __float2bfloat16_rn(__uint_as_float(r[i0 + i]) + old[i]);
               }
             }
           }
@@ -318,19 +374,32 @@ __global__ void __launch_bounds__(kThreads, 1)
                   *reinterpret_cast<uint4*>(o + q * 8) = pk;
                 }
               } else {
-                for (int i = 0; i < 32 && f0 + i < s.write_end; ++i) {
-                  float w = __uint_as_float(r[i]);
-                  if (a.accumulate) w += __bfloat162float(o[i]);
-                  o[i] = __float2bfloat16_rn(w);
+                const int nf = s.write_end - f0;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                  if (i < nf) {
+                    float w = __uint_as_float(r[i]);
+                    if (a.accumulate) w += __bfloat162float(o[i]);
+                    o[i] = __float2bfloat16_rn(w);
+                  }
                 }
               }
             } else {
               float* o = static_cast<float*>(a.out) + idx0;
-              for (int i = 0; i < 32; ++i) {
-                if (f0 + i >= s.write_end) break;
-                const float v = __uint_as_float(r[i]);
-                if (a.mode == OUT_F32_RED) ptx::red_add_f32(o + i, v);
-                else o[i] = v;
+              const int nf = s.write_end - f0;
+              if (a.mode == OUT_F32_RED) {
+#pragma unroll
+                for (int i = 0; i < 32; i += 4)
+                  if (i + 4 <= nf) ptx::red_add_v4_f32(o + i, __uint_as_float(r[i]), __uint_as_float(r[i + 1]),
+                                                       __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+                  else
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                      if (i + e < nf) ptx::red_add_f32(o + i + e, __uint_as_float(r[i + e]));
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (i < nf) o[i] = __uint_as_float(r[i]);
               }
             }
           }
@@ -341,12 +410,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) ptx::mbar_arrive(&acce_bar[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (tr && warp == 2 && lane == 0) tr[6] = gtime();   // epilogue done
   }
 
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   if (warp == 1) ptx::tmem_dealloc<TMEM_COLS>(tmem_base);
+
 }
 
 // ---------------------------------------------------------------------------
@@ -455,10 +526,20 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   }
   bytes += static_cast<double>(p.T) * p.n_feat * (p.out.mode == OUT_BF16 ? (p.out.accumulate ? 4 : 2) : 4);
   const int prof = prof_begin(st);
-  kern<<<grid, kThreads, SMEM, st>>>(maps, a);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, maps, a);
   prof_end(prof, st, bytes, flops, SWAP ? 1 : 0);
   launched("tc_gemm");
-  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error("tc_gemm<BN=%d,swap=%d> (T=%lld k_act=%lld nseg=%d klen=%lld/%lld/%lld koff=%lld/%lld/%lld "
               "grid=%d stream_k=%d): %s", BN, (int)SWAP, (long long)p.T, (long long)p.k_act, p.nseg,
@@ -472,6 +553,11 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
 
 }  // namespace
 
+dl_status set_gemm_trace(void* buf) {
+  unsigned long long* p = static_cast<unsigned long long*>(buf);
+  return cuda_status(cudaMemcpyToSymbol(g_trace, &p, sizeof(p)), "set trace");
+}
+
 dl_status tc_gemm(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   if (p.T <= 0) return DL_OK;
   if (!get_encode()) {
@@ -482,7 +568,9 @@ dl_status tc_gemm(const GemmProblem& p, bool stream_k, cudaStream_t st) {
     set_error("stream-K requires an fp32 reduction output");
     return DL_ERR_INVALID_ARG;
   }
-  if (p.T <= 64) return launch_cfg<64, true, 8>(p, stream_k, st);
+  static const int dec_stages = getenv("DL_DECODE_STAGES") ? atoi(getenv("DL_DECODE_STAGES")) : 9;
+  if (p.T <= 64) return dec_stages == 4 ? launch_cfg<64, true, 4>(p, stream_k, st)
+                                        : launch_cfg<64, true, 9>(p, stream_k, st);
   if (p.T <= 128) return launch_cfg<128, true, 6>(p, stream_k, st);
   if (p.T <= 256) return launch_cfg<256, true, 4>(p, stream_k, st);
   return launch_cfg<256, false, 4>(p, stream_k, st);
