@@ -84,8 +84,8 @@ __device__ __forceinline__ void load_tile(uint32_t sbase, const __nv_bfloat16* s
 // =============================== prefill ===================================
 __global__ void __launch_bounds__(128) attn_prefill_kernel(AttnArgs a) {
   extern __shared__ __align__(1024) uint8_t sm[];
+  pdl_trigger();   // successor may launch now; it waits for us before reading
   pdl_wait();
-  pdl_trigger();
   const int s = blockIdx.z, h = blockIdx.y;
   const int n_new = a.cu_seqlens[s + 1] - a.cu_seqlens[s];
   const int q0 = blockIdx.x * QT;
@@ -246,8 +246,8 @@ constexpr int PART = D + 2;
 
 __global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, int splits) {
   extern __shared__ __align__(1024) uint8_t sm[];
+  pdl_trigger();   // successor may launch now; it waits for us before reading
   pdl_wait();
-  pdl_trigger();
   const int s = blockIdx.z, kvh = blockIdx.y, sp = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t4 = lane & 3;
@@ -421,8 +421,8 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, int splits
 
 // merge key splits: one CTA (128 threads = d) per (token, head)
 __global__ void __launch_bounds__(128) attn_combine_kernel(AttnArgs a, int splits) {
+  pdl_trigger();   // successor may launch now; it waits for us before reading
   pdl_wait();
-  pdl_trigger();
   const int64_t s = blockIdx.y;
   const int h = blockIdx.x, d = threadIdx.x;
   const float* pp = a.partial + (s * a.Hq + h) * splits * PART;

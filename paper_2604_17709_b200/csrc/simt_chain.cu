@@ -131,8 +131,8 @@ template <typename E, typename I, typename O, int TT>
 __global__ void __launch_bounds__(kWarps * 32)
     gemv_kernel(const E* __restrict__ W, int64_t ldw, int R, int C, const I* __restrict__ in, int64_t ldi,
                 int T, O* __restrict__ out, int64_t ldo, int accumulate) {
+  pdl_trigger();   // successor may launch now; it waits for us before reading
   pdl_wait();
-  pdl_trigger();
   const int warp = threadIdx.x >> 5;
   const int row0 = (blockIdx.x * kWarps + warp) * kRows;
   if (row0 >= R) return;
@@ -146,8 +146,8 @@ __global__ void __launch_bounds__(kWarps * 32)
                        const E* __restrict__ B, int64_t ldb, E* __restrict__ Y, int64_t ldy, int T,
                        int m, int n, int k, int accumulate) {
   extern __shared__ float zs[];   // [T x k_pad]
+  pdl_trigger();   // successor may launch now; it waits for us before reading
   pdl_wait();
-  pdl_trigger();
   const int kp = (k + 3) & ~3;
   const int warp = threadIdx.x >> 5;
   for (int row0 = warp * kRows; row0 < k; row0 += kWarps * kRows)
