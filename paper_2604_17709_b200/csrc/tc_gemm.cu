@@ -420,6 +420,202 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }
 
+
+// ---------------------------------------------------------------------------
+// CTA-pair prefill kernel (cta_group::2): a cluster of 2 CTAs computes a
+// 256-token x 256-feature tile with M=256, N=256 MMAs issued by the leader.
+// Each CTA stages only its own 128 token rows and 128 weight rows per
+// k-block (32 KB / stage), halving per-SM shared-memory operand traffic
+// relative to the 1-CTA 128x256 tile.  Whole tiles, bf16 (+ fused residual)
+// epilogue; every CTA drains its own TMEM half (its 128 token rows).
+// ---------------------------------------------------------------------------
+template <int STAGES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    tc_gemm_pair_kernel(const __grid_constant__ KMaps maps, const __grid_constant__ KArgs a) {
+  constexpr int HALF = 128;                       // rows per CTA of both operands
+  constexpr int TILE = 256;                       // cluster tile (tokens and features)
+  constexpr int A_BYTES = HALF * BK * 2;
+  constexpr int STAGE_BYTES = 2 * A_BYTES;        // own A half + own B half
+  constexpr uint32_t TMEM_COLS = 2 * TILE;        // double-buffered 256-column accumulator
+  constexpr uint32_t IDESC = ptx::idesc_bf16_f32(256, TILE);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full_bar[STAGES];
+  __shared__ __align__(8) uint64_t empty_bar[STAGES];
+  __shared__ __align__(8) uint64_t accf_bar[2];
+  __shared__ __align__(8) uint64_t acce_bar[2];
+  __shared__ uint32_t tmem_slot;
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&maps.act);
+    for (int g = 0; g < a.nseg; ++g) ptx::prefetch_tmap(&maps.w[g]);
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full_bar[s], 1);
+      ptx::mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&accf_bar[b], 1);
+      ptx::mbar_init(&acce_bar[b], 16);           // 8 epilogue warps x 2 CTAs
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) ptx::tmem_alloc_pair<TMEM_COLS>(&tmem_slot);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = tmem_slot;
+
+  pdl_trigger();
+  JobIter it(a, blockIdx.x / 2, gridDim.x / 2);
+  Job j;
+
+  if (warp == 0) {
+    // ===================== TMA producer (both CTAs) =====================
+    if (lane == 0) {
+      const uint64_t pol_w = ptx::policy_evict_first();
+      const uint64_t pol_a = ptx::policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      int u = 0;
+      bool waited = false;
+      int pend_c0[STAGES], pend_c1[STAGES];
+      auto flush_pending = [&]() {
+        pdl_wait();
+        waited = true;
+        for (int i = 0; i < u && i < STAGES; ++i)
+          ptx::tma_load_2d_pair(smem + i * STAGE_BYTES, &maps.act, &full_bar[i], pend_c0[i], pend_c1[i], pol_a);
+      };
+      while (it.next(j, TILE, TILE)) {
+        const KSeg& s = a.seg[j.seg];
+        for (int kb = j.kb0; kb < j.kb1; ++kb, ++u) {
+          if (u >= STAGES && !waited) flush_pending();
+          ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          uint8_t* sw = sa + A_BYTES;
+          if (leader) ptx::mbar_arrive_expect_tx(&full_bar[stage], 2 * STAGE_BYTES);
+          const int kx = kb * BK;
+          ptx::tma_load_2d_pair(sw, &maps.w[j.seg], &full_bar[stage], kx,
+                                j.feat0 - s.feat_begin + static_cast<int>(rank) * HALF, pol_w);
+          if (waited) {
+            ptx::tma_load_2d_pair(sa, &maps.act, &full_bar[stage], s.act_koff + kx,
+                                  j.tok0 + static_cast<int>(rank) * HALF, pol_a);
+          } else {
+            pend_c0[u] = s.act_koff + kx;
+            pend_c1[u] = j.tok0 + static_cast<int>(rank) * HALF;
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+      if (!waited) flush_pending();
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (leader CTA, one thread) =====================
+    if (leader && lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      while (it.next(j, TILE, TILE)) {
+        ptx::mbar_wait(&acce_bar[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * TILE;
+        for (int kb = j.kb0; kb < j.kb1; ++kb) {
+          ptx::mbar_wait(&full_bar[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t sa = ptx::smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t sw = sa + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            ptx::umma_bf16_pair(d_tmem, ptx::sdesc_sw128(sa + k * 32), ptx::sdesc_sw128(sw + k * 32), IDESC,
+                                (kb > j.kb0 || k > 0) ? 1u : 0u);
+          ptx::umma_commit_pair(&empty_bar[stage], 0x3);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        ptx::umma_commit_pair(&accf_bar[acc], 0x3);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // ===================== epilogue (warps 2..9, both CTAs) =====================
+    pdl_wait();
+    const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int row = quarter * 32 + lane;          // this CTA's token row within its half
+    const uint32_t acce0 = ptx::mapa(ptx::smem_u32(&acce_bar[0]), 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    while (it.next(j, TILE, TILE)) {
+      const KSeg& s = a.seg[j.seg];
+      ptx::mbar_wait(&accf_bar[acc], acc_phase);
+      ptx::tc_fence_after();
+      const bool has_k = j.kb1 > j.kb0;
+      const int tok = j.tok0 + static_cast<int>(rank) * HALF + row;
+#pragma unroll 1
+      for (int c0 = half * 128; c0 < (half + 1) * 128; c0 += 32) {
+        uint32_t r[32];
+        if (has_k) {
+          ptx::tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * TILE + c0, r);
+          ptx::tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = 0u;
+        }
+        const int f0 = j.feat0 + c0;
+        if (tok < a.T && f0 < s.write_end) {
+          __nv_bfloat16* o = static_cast<__nv_bfloat16*>(a.out) + out_index(a, s, tok, f0);
+          if (f0 + 32 <= s.write_end && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              float v[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r[q * 8 + e]);
+              if (a.accumulate) {
+                uint4 old = *reinterpret_cast<const uint4*>(o + q * 8);
+                const __nv_bfloat162* ob = reinterpret_cast<const __nv_bfloat162*>(&old);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  float2 f2 = __bfloat1622float2(ob[e]);
+                  v[2 * e] += f2.x;
+                  v[2 * e + 1] += f2.y;
+                }
+              }
+              uint4 pk;
+              __nv_bfloat162* pb = reinterpret_cast<__nv_bfloat162*>(&pk);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) pb[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+              *reinterpret_cast<uint4*>(o + q * 8) = pk;
+            }
+          } else {
+            const int nf = s.write_end - f0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (i < nf) {
+                float w = __uint_as_float(r[i]);
+                if (a.accumulate) w += __bfloat162float(o[i]);
+                o[i] = __float2bfloat16_rn(w);
+              }
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_cluster(acce0 + acc * 8);   // leader's acce_bar[acc]
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  if (warp == 1) ptx::tmem_dealloc_pair<TMEM_COLS>(tmem_base);
+}
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -450,13 +646,17 @@ bool make_map(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64
   return r == CUDA_SUCCESS;
 }
 
-template <int BN, bool SWAP, int STAGES>
+template <int BN, bool SWAP, int STAGES, bool PAIR = false>
 dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
-  constexpr int FEAT_TILE = SWAP ? BM : BN;
-  constexpr int TOK_TILE = SWAP ? BN : BM;
-  constexpr int SMEM = STAGES * (BM + BN) * BK * 2 + 1024;
+  // PAIR: cta_group::2 kernel, cluster tile 256 tokens x 256 features, each CTA
+  // loads 128-row boxes of both operands.
+  constexpr int FEAT_TILE = PAIR ? 256 : (SWAP ? BM : BN);
+  constexpr int TOK_TILE = PAIR ? 256 : (SWAP ? BN : BM);
+  constexpr int BOX_W = PAIR ? 128 : FEAT_TILE;
+  constexpr int BOX_A = PAIR ? 128 : TOK_TILE;
+  constexpr int SMEM = PAIR ? STAGES * 2 * 128 * BK * 2 + 1024 : STAGES * (BM + BN) * BK * 2 + 1024;
   static bool attr_set = false;
-  auto kern = tc_gemm_kernel<BN, SWAP, STAGES>;
+  void (*kern)(KMaps, KArgs) = PAIR ? tc_gemm_pair_kernel<STAGES> : tc_gemm_kernel<BN, SWAP, STAGES>;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(tc_gemm)");
@@ -488,7 +688,7 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
     tiles += k.ntiles;
     units += static_cast<long long>(k.ntiles) * k.nkb;
     if (s.klen > 0 && s.rows > 0) {
-      if (!make_map(&maps.w[g], s.w, s.rows, s.klen, s.ldw, FEAT_TILE)) {
+      if (!make_map(&maps.w[g], s.w, s.rows, s.klen, s.ldw, BOX_W)) {
         set_error("cuTensorMapEncodeTiled failed (weight segment %d)", g);
         return DL_ERR_CUDA;
       }
@@ -496,7 +696,7 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
       maps.w[g] = maps.w[0];
     }
   }
-  if (!make_map(&maps.act, p.act, p.T, p.k_act, p.ld_act, TOK_TILE)) {
+  if (!make_map(&maps.act, p.act, p.T, p.k_act, p.ld_act, BOX_A)) {
     set_error("cuTensorMapEncodeTiled failed (activation)");
     return DL_ERR_CUDA;
   }
@@ -513,6 +713,9 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   int grid;
   if (stream_k) {
     grid = static_cast<int>(units < sms ? (units > 0 ? units : 1) : sms);
+  } else if (PAIR) {
+    const int clusters = sms / 2;
+    grid = 2 * (tiles < clusters ? (tiles > 0 ? tiles : 1) : clusters);
   } else {
     grid = tiles < sms ? (tiles > 0 ? tiles : 1) : sms;
   }
@@ -573,6 +776,8 @@ dl_status tc_gemm(const GemmProblem& p, bool stream_k, cudaStream_t st) {
                                         : launch_cfg<64, true, 9>(p, stream_k, st);
   if (p.T <= 128) return launch_cfg<128, true, 6>(p, stream_k, st);
   if (p.T <= 256) return launch_cfg<256, true, 4>(p, stream_k, st);
+  static const bool pair = !getenv("DL_PREFILL_PAIR") || atoi(getenv("DL_PREFILL_PAIR")) != 0;
+  if (pair && !stream_k && p.out.mode == OUT_BF16) return launch_cfg<256, false, 6, true>(p, stream_k, st);
   return launch_cfg<256, false, 4>(p, stream_k, st);
 }
 
