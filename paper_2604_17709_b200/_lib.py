@@ -303,10 +303,11 @@ def dl_rmsnorm(x: torch.Tensor, gamma: torch.Tensor, out: torch.Tensor, eps: flo
     return out
 
 
-def dl_dense(X: torch.Tensor, W: torch.Tensor, C: torch.Tensor, stream=None):
+def dl_dense(X: torch.Tensor, W: torch.Tensor, C: torch.Tensor, stream=None, workspace: torch.Tensor | None = None):
     T, K = X.shape
     N = W.shape[0]
-    _check(load().dl_dense(_ptr(X), _ld(X), _ptr(W), _ld(W), _ptr(C), _ld(C), T, N, K, None, 0, _stream(stream)))
+    _check(load().dl_dense(_ptr(X), _ld(X), _ptr(W), _ld(W), _ptr(C), _ld(C), T, N, K, _ptr(workspace),
+                           0 if workspace is None else workspace.numel(), _stream(stream)))
     return C
 
 

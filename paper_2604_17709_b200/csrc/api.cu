@@ -3,11 +3,13 @@
 // arithmetic step runs in this library's kernels (tc_gemm.cu,
 // simt_chain.cu, elementwise.cu, attention.cu); there is no CPU fallback.
 #include <dlfcn.h>
+#include <stdlib.h>
 #include <stdarg.h>
 #include <stdio.h>
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <string>
 
 #include "dl_internal.h"
@@ -200,7 +202,7 @@ GemmOut out_plain(void* ptr, int64_t ld, int mode, int accumulate) {
   o.ld = ld;
   o.mode = mode;
   o.accumulate = accumulate;
-  o.scatter_p = 1;
+  o.scatter_p = 0;
   return o;
 }
 
@@ -478,11 +480,20 @@ dl_status block_dims(const dl_block_config* c, int world, BlockDims* d) {
   return DL_OK;
 }
 
+// Stream-K launches rotate over kSchedSlots counter pairs: a launch can only
+// overlap (PDL) with its immediate neighbours, so 4 slots never collide.
+constexpr int kSchedSlots = 4;
+unsigned int* next_sched(unsigned int* base) {
+  static std::atomic<unsigned> slot{0};
+  return base + 2 * (slot.fetch_add(1) % kSchedSlots);
+}
+
 struct BlockWs {
   float* zf; float* yf;              // fp32 reduction targets (zero-maintained)
   __nv_bfloat16 *xn, *zb, *yb, *rs, *q, *att, *att_full, *ag, *act;
   float* apart;                      // split-KV attention partials (decode)
   size_t apart_bytes;
+  unsigned int* sched;               // kSchedSlots x 2 stream-K work counters
   int64_t ldz32, ldzb, ldy32;
 };
 
@@ -500,13 +511,13 @@ BlockWs carve_block(Carver& c, const BlockDims& d, int64_t Tmax) {
   w.rs = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.W);
   w.q = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.Hq_loc * d.d);
   w.att = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.Hq_loc * d.d);
-  if (d.P > 1) {
-    w.att_full = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.h);
-    w.ag = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.h);
-  }
+  // all-gather buffers (TP path; also present at P = 1 so the TP path can be tested)
+  w.att_full = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.h);
+  w.ag = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.h);
   w.act = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.m);
   w.apart_bytes = attention_workspace(Ts, static_cast<int>(d.Hq_loc), static_cast<int>(d.d));
   w.apart = c.take<float>(w.apart_bytes / sizeof(float));
+  w.sched = c.take<unsigned int>(2 * kSchedSlots);
   return w;
 }
 
@@ -599,12 +610,16 @@ dl_status run_group(const dl_factor_group& grp, int nseg, const int64_t* rows, c
                     cudaStream_t st) {
   const ZLayout zl = zlayout(grp, nseg);
   if (skinny) {
-    DL_TRY(tc_gemm(stage1(grp, nseg, act, ld_act, T, n, zl, out_plain(ws.zf, ws.ldz32, OUT_F32_RED, 0)), true, st));
+    GemmProblem p1 = stage1(grp, nseg, act, ld_act, T, n, zl, out_plain(ws.zf, ws.ldz32, OUT_F32_RED, 0));
+    p1.sched = next_sched(ws.sched);
+    DL_TRY(tc_gemm(p1, true, st));
     DL_TRY(launch_f32_to_bf16(ws.zf, ws.ldz32, ws.zb, ws.ldzb, T, zl.width, 1, st));
   } else {
     DL_TRY(tc_gemm(stage1(grp, nseg, act, ld_act, T, n, zl, out_plain(ws.zb, ws.ldzb, OUT_BF16, 0)), false, st));
   }
-  return tc_gemm(stage2(grp, nseg, rows, ws.zb, ws.ldzb, T, zl, out2), skinny, st);
+  GemmProblem p2 = stage2(grp, nseg, rows, ws.zb, ws.ldzb, T, zl, out2);
+  if (skinny) p2.sched = next_sched(ws.sched);
+  return tc_gemm(p2, skinny, st);
 }
 
 }  // namespace
@@ -679,7 +694,11 @@ dl_status dl_decomposed_block_forward(const dl_block_config* cfg, const dl_block
   Carver cv(workspace);
   const BlockWs ws = carve_block(cv, d, cfg->max_tokens);
   const bool skinny = T <= 256;
-  const bool tp = comm && P > 1;
+  // DL_FORCE_TP_PATH=1 (tests only): take the tensor-parallel branch (bf16
+  // partials, NCCL RS/AG/AR, un-permute) even with a 1-rank communicator, so the
+  // TP code path is exercised on a single GPU.
+  static const bool force_tp = getenv("DL_FORCE_TP_PATH") && atoi(getenv("DL_FORCE_TP_PATH")) != 0;
+  const bool tp = comm && (P > 1 || force_tp);
   const int64_t qkv_rows[3] = {d.h, d.hkv, d.hkv};
   const int64_t gu_rows[2] = {d.m, d.m};
   const int64_t h_rows[1] = {d.h};
@@ -689,7 +708,7 @@ dl_status dl_decomposed_block_forward(const dl_block_config* cfg, const dl_block
   // ---- q|k|v: one group; partials laid out rank-major by head for the RS ----
   GemmOut qkv_out{};
   qkv_out.mode = red_mode;
-  qkv_out.scatter_p = tp ? P : 1;
+  qkv_out.scatter_p = tp ? P : 0;   // TP: rank-major [P][T][W] slabs, also at P = 1
   qkv_out.slab = d.W;
   qkv_out.seg_slab_off[0] = 0;
   qkv_out.seg_slab_off[1] = d.h / P;
@@ -847,6 +866,18 @@ dl_status dl_dense(const void* X, int64_t ldx, const void* W, int64_t ldw, void*
   DL_TRY(check_ld(ldw, K, DL_BF16, "ldw"));
   DL_TRY(check_ld(ldc, N, DL_BF16, "ldc"));
   DL_TRY(check_device());
+  // debug A/B switch (DL_DENSE_SK=1): stream-K with an fp32 reduction into the
+  // (zeroed, T*N*4 + 256 bytes) workspace, then conversion -- the decode path's
+  // scheme applied to a dense GEMM.
+  static const bool sk = getenv("DL_DENSE_SK") && atoi(getenv("DL_DENSE_SK")) != 0;
+  if (sk && workspace && workspace_bytes >= static_cast<size_t>(T) * N * 4 + 256 && T <= 256 && N % 4 == 0) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    float* acc = static_cast<float*>(workspace);
+    GemmProblem p = one_seg(X, ldx, T, K, W, ldw, N, K, out_plain(acc, N, OUT_F32_RED, 0));
+    p.sched = reinterpret_cast<unsigned int*>(static_cast<uint8_t*>(workspace) + static_cast<size_t>(T) * N * 4);
+    DL_TRY(tc_gemm(p, true, st));
+    return launch_f32_to_bf16(acc, N, static_cast<__nv_bfloat16*>(C), ldc, T, N, 1, st);
+  }
   return tc_gemm(one_seg(X, ldx, T, K, W, ldw, N, K, out_plain(C, ldc, OUT_BF16, 0)), false,
                  static_cast<cudaStream_t>(stream));
 }

@@ -71,7 +71,7 @@ struct GemmOut {
   // reduce-scatter layout (P > 1): feature f of segment g goes to
   //   owner = (f - begin_g) / rpr_g, col = slab_off_g + (f - begin_g) % rpr_g,
   //   index = owner * T * slab + token * slab + col
-  int scatter_p;       // <= 1: plain [token][feature] with ld
+  int scatter_p;       // 0: plain [token][feature] with ld; >= 1: [P][T][slab]
   int64_t slab;
   int64_t seg_slab_off[3];
   int64_t seg_rpr[3];
@@ -88,6 +88,10 @@ struct GemmProblem {
   int nseg; GemmSeg seg[3];
   int64_t n_feat;      // total output features (sum of seg rows)
   GemmOut out;
+  // stream-K only: 2 zero-initialised uint32 counters (work, done) in device
+  // memory enabling the hybrid static + dynamic split; null -> static split.
+  // Launches that may overlap (PDL) must use different counter pairs.
+  unsigned int* sched;
 };
 
 // Picks the tile configuration (swap-AB for T <= 256, stream-K when the

@@ -43,6 +43,8 @@ namespace {
 constexpr int BK = 64;   // K elements per stage = one 128-byte swizzle row
 constexpr int BM = 128;  // MMA M = TMEM lanes
 constexpr int kThreads = 320;   // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
+constexpr int kJobRing = 8;     // producer -> MMA / epilogue job queue depth
+constexpr int kL2Prefetch = 24; // decode: weight tiles pulled into L2 while waiting (PDL)
 
 struct KSeg {
   int feat_begin, feat_end;  // global output features [begin, end)
@@ -70,6 +72,14 @@ struct KArgs {
   int accumulate;
   int scatter_p;
   long long slab;
+  int trace_slot;            // debug timeline slot of this launch (-1: none)
+  // hybrid stream-K: CTA c first takes units [c*static_units, (c+1)*static_units),
+  // then grabs `chunk`-unit pieces of [dyn_begin, total_units) from sched[0];
+  // sched[1] counts finished CTAs (the last one resets both).  sched == null:
+  // purely static stream-K.
+  unsigned int* sched;
+  long long static_units, dyn_begin;
+  int chunk;
 };
 
 struct __align__(64) KMaps {
@@ -78,6 +88,8 @@ struct __align__(64) KMaps {
 };
 
 __device__ unsigned long long* g_trace = nullptr;
+bool g_trace_host_on = false;   // host: assign a slot to every launch while tracing
+int g_trace_next = 0;
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -107,6 +119,10 @@ struct JobIter {
     } else {
       u = u_end = 0;
     }
+  }
+  __device__ void set_range(long long b, long long e) {
+    u = b;
+    u_end = e;
   }
   __device__ bool next(Job& j, int FEAT_TILE, int TOK_TILE) {
     if (!a.stream_k) {
@@ -146,7 +162,7 @@ struct JobIter {
 };
 
 __device__ __forceinline__ long long out_index(const KArgs& a, const KSeg& s, int tok, int f) {
-  if (a.scatter_p <= 1) return static_cast<long long>(tok) * a.ldo + s.col_off + (f - s.feat_begin);
+  if (a.scatter_p <= 0) return static_cast<long long>(tok) * a.ldo + s.col_off + (f - s.feat_begin);
   long long loc = f - s.feat_begin;
   long long owner = loc / s.rpr;
   long long col = s.slab_off + loc % s.rpr;
@@ -172,11 +188,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t empty_bar[STAGES];
   __shared__ __align__(8) uint64_t accf_bar[2];
   __shared__ __align__(8) uint64_t acce_bar[2];
+  __shared__ __align__(8) uint64_t jfull_bar[kJobRing];
+  __shared__ __align__(8) uint64_t jempty_bar[kJobRing];
+  __shared__ Job jobs[kJobRing];
   __shared__ uint32_t tmem_slot;
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  unsigned long long* tr = g_trace ? g_trace + blockIdx.x * 8 : nullptr;   // debug timeline
+  unsigned long long* tr = (g_trace && a.trace_slot >= 0) ? g_trace + (static_cast<long long>(a.trace_slot) * 148 + blockIdx.x) * 8 : nullptr;   // debug timeline
   if (tr && threadIdx.x == 0) { tr[0] = gtime(); tr[7] = smid(); }
 
   if (warp == 0 && lane == 0) {
@@ -189,6 +208,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&accf_bar[b], 1);
       ptx::mbar_init(&acce_bar[b], 8);
+    }
+    for (int b = 0; b < kJobRing; ++b) {
+      ptx::mbar_init(&jfull_bar[b], 1);
+      ptx::mbar_init(&jempty_bar[b], 8);   // released by the 8 epilogue warps
     }
     ptx::fence_barrier_init();
   }
@@ -217,7 +240,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       bool waited = false;
       if (tr) tr[2] = gtime();
       int pend_c0[STAGES], pend_c1[STAGES];
+      // Before waiting on the predecessor, also pull the weight tiles of the
+      // next kL2Prefetch units (beyond the STAGES staged in smem) into L2, so
+      // the dependency gap is spent streaming HBM instead of idling.
+      JobIter pf_it = it;
+      if (a.stream_k && a.sched)
+        pf_it.set_range(blockIdx.x * a.static_units, (blockIdx.x + 1) * a.static_units);
+      auto l2_prefetch = [&]() {
+        int skipped = 0, issued = 0;
+        Job pj;
+        while (issued < kL2Prefetch && pf_it.next(pj, FEAT_TILE, TOK_TILE)) {
+          const KSeg& ps = a.seg[pj.seg];
+          for (int kb = pj.kb0; kb < pj.kb1 && issued < kL2Prefetch; ++kb) {
+            if (skipped < STAGES) { ++skipped; continue; }   // these go to smem
+            ptx::tma_prefetch_2d(&maps.w[pj.seg], kb * BK, pj.feat0 - ps.feat_begin);
+            ++issued;
+          }
+        }
+      };
       auto flush_pending = [&]() {
+        if (SWAP) l2_prefetch();
         pdl_wait();
         waited = true;
         for (int i = 0; i < u && i < STAGES; ++i) {
@@ -225,9 +267,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::tma_load_2d(dst, &maps.act, &full_bar[i], pend_c0[i], pend_c1[i], pol_a);
         }
       };
-      while (it.next(j, FEAT_TILE, TOK_TILE)) {
-        const KSeg& s = a.seg[j.seg];
-        for (int kb = j.kb0; kb < j.kb1; ++kb, ++u) {
+      int jslot = 0;
+      uint32_t jphase = 0;
+      auto push = [&](const Job& jb) {
+        ptx::mbar_wait(&jempty_bar[jslot], jphase ^ 1);
+        jobs[jslot] = jb;
+        ptx::mbar_arrive(&jfull_bar[jslot]);
+        if (++jslot == kJobRing) { jslot = 0; jphase ^= 1; }
+      };
+      auto emit = [&](const Job& jb) {
+        push(jb);
+        const KSeg& s = a.seg[jb.seg];
+        for (int kb = jb.kb0; kb < jb.kb1; ++kb, ++u) {
           if (u >= STAGES && !waited) flush_pending();
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sp = smem + stage * STAGE_BYTES;
@@ -236,16 +287,31 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int kx = kb * BK;
           uint8_t* sw = SWAP ? sp : sq;
           uint8_t* sa = SWAP ? sq : sp;
-          ptx::tma_load_2d(sw, &maps.w[j.seg], &full_bar[stage], kx, j.feat0 - s.feat_begin, pol_w);
+          ptx::tma_load_2d(sw, &maps.w[jb.seg], &full_bar[stage], kx, jb.feat0 - s.feat_begin, pol_w);
           if (waited) {
-            ptx::tma_load_2d(sa, &maps.act, &full_bar[stage], s.act_koff + kx, j.tok0, pol_a);
+            ptx::tma_load_2d(sa, &maps.act, &full_bar[stage], s.act_koff + kx, jb.tok0, pol_a);
           } else {
             pend_c0[u] = s.act_koff + kx;
-            pend_c1[u] = j.tok0;
+            pend_c1[u] = jb.tok0;
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
+      };
+      if (a.stream_k && a.sched) {
+        it.set_range(blockIdx.x * a.static_units, (blockIdx.x + 1) * a.static_units);
+        while (it.next(j, FEAT_TILE, TOK_TILE)) emit(j);
+        for (;;) {   // dynamic tail: fast SMs take more pieces
+          const long long g = a.dyn_begin + static_cast<long long>(atomicAdd(a.sched, static_cast<unsigned>(a.chunk)));
+          if (g >= a.total_units) break;
+          it.set_range(g, g + a.chunk < a.total_units ? g + a.chunk : a.total_units);
+          while (it.next(j, FEAT_TILE, TOK_TILE)) emit(j);
+        }
+      } else {
+        while (it.next(j, FEAT_TILE, TOK_TILE)) emit(j);
       }
+      Job end;
+      end.seg = -1;
+      push(end);
       if (!waited) flush_pending();
     }
   } else if (warp == 1) {
@@ -255,7 +321,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      while (it.next(j, FEAT_TILE, TOK_TILE)) {
+      int jslot = 0;
+      uint32_t jphase = 0;
+      for (;;) {
+        ptx::mbar_wait(&jfull_bar[jslot], jphase);
+        j = jobs[jslot];
+        if (++jslot == kJobRing) { jslot = 0; jphase ^= 1; }
+        if (j.seg < 0) break;
         ptx::mbar_wait(&acce_bar[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -292,7 +364,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int HALF_COLS = BN / 2;
     int acc = 0;
     uint32_t acc_phase = 0;
-    while (it.next(j, FEAT_TILE, TOK_TILE)) {
+    int jslot = 0;
+    uint32_t jphase = 0;
+    for (;;) {
+      ptx::mbar_wait(&jfull_bar[jslot], jphase);
+      j = jobs[jslot];
+      const int my_slot = jslot;
+      if (++jslot == kJobRing) { jslot = 0; jphase ^= 1; }
+      if (j.seg < 0) break;
       const KSeg& s = a.seg[j.seg];
       ptx::mbar_wait(&accf_bar[acc], acc_phase);
       if (tr && warp == 2 && lane == 0) tr[5] = gtime();   // accumulator of this job ready
@@ -314,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int tok0 = j.tok0 + c0;
           const int ntok = a.T - tok0;
           if (f < s.write_end && ntok > 0) {
-            const long long tstride = a.scatter_p <= 1 ? a.ldo : a.slab;
+            const long long tstride = a.scatter_p <= 0 ? a.ldo : a.slab;
             const long long base = out_index(a, s, tok0, f);
             if (a.mode == OUT_F32_RED) {
               float* p = static_cast<float*>(a.out) + base;
@@ -407,7 +486,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&acce_bar[acc]);
+      if (lane == 0) {
+        ptx::mbar_arrive(&acce_bar[acc]);
+        ptx::mbar_arrive(&jempty_bar[my_slot]);
+      }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
     if (tr && warp == 2 && lane == 0) tr[6] = gtime();   // epilogue done
@@ -417,6 +499,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   if (warp == 1) ptx::tmem_dealloc<TMEM_COLS>(tmem_base);
+  if (a.sched && threadIdx.x == 0) {   // last CTA out resets the work counter for reuse
+    __threadfence();
+    if (atomicAdd(a.sched + 1, 1u) == gridDim.x - 1) {
+      atomicExch(a.sched, 0u);
+      atomicExch(a.sched + 1, 0u);
+      __threadfence();
+    }
+  }
 
 }
 
@@ -706,13 +796,34 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   a.out = p.out.ptr;
   a.ldo = p.out.ld;
   a.mode = p.out.mode;
+  // debug A/B switches (timing experiments only; results are wrong with NORED)
+  static const bool dbg_tile_order = getenv("DL_DEBUG_SK_TILEORDER") != nullptr;
+  static const bool dbg_nored = getenv("DL_DEBUG_NORED") != nullptr;
+  if (stream_k && dbg_tile_order) a.stream_k = 0;
+  if (stream_k && dbg_nored) a.mode = OUT_F32_STORE;
   a.accumulate = p.out.accumulate;
   a.scatter_p = p.out.scatter_p;
   a.slab = p.out.slab;
+  a.trace_slot = g_trace_host_on ? g_trace_next++ : -1;
+  a.sched = nullptr;
+  if (stream_k && p.sched) {
+    static const double frac = getenv("DL_SK_STATIC") ? atof(getenv("DL_SK_STATIC")) : 0.9;
+    static const int chunk = getenv("DL_SK_CHUNK") ? atoi(getenv("DL_SK_CHUNK")) : 8;
+    const int cap = num_sms() * ((SWAP && STAGES <= 4) ? 2 : 1);   // must match the grid below
+    const int g = static_cast<int>(units < cap ? (units > 0 ? units : 1) : cap);
+    a.sched = p.sched;
+    a.static_units = static_cast<long long>(frac * static_cast<double>(units) / g);
+    a.dyn_begin = a.static_units * g;
+    a.chunk = chunk > 0 ? chunk : 1;
+  }
   const int sms = num_sms();
   int grid;
   if (stream_k) {
-    grid = static_cast<int>(units < sms ? (units > 0 ? units : 1) : sms);
+    // shallow configurations (<= 4 stages) fit two CTAs per SM: the next
+    // launch can then start streaming on an SM while one CTA is still draining
+    const int per_sm = (SWAP && STAGES <= 4) ? 2 : 1;
+    const int cap = sms * per_sm;
+    grid = static_cast<int>(units < cap ? (units > 0 ? units : 1) : cap);
   } else if (PAIR) {
     const int clusters = sms / 2;
     grid = 2 * (tiles < clusters ? (tiles > 0 ? tiles : 1) : clusters);
@@ -758,6 +869,8 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
 
 dl_status set_gemm_trace(void* buf) {
   unsigned long long* p = static_cast<unsigned long long*>(buf);
+  g_trace_host_on = p != nullptr;
+  g_trace_next = 0;
   return cuda_status(cudaMemcpyToSymbol(g_trace, &p, sizeof(p)), "set trace");
 }
 

@@ -1,0 +1,76 @@
+"""GPU test of the tensor-parallel code path of dl_decomposed_block_forward on
+a single B200: a 1-rank NCCL communicator (torch ProcessGroupNCCL) and
+DL_FORCE_TP_PATH=1 make the block take the TP branch (bf16 partials laid out
+by head for the reduce-scatter, NCCL ReduceScatter / AllGather / AllReduce,
+un-permute, bf16 finalize kernels).  Results are compared with the fp64 oracle.
+Runs in a subprocess so the env switch and process group stay isolated.
+"""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r'''
+import os, sys, numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, __ROOT__)
+import oracle, paper_2604_17709_b200 as dl
+from synthetic import ModelShape, block_ranks, gen_block_weights, gen_normal
+os.environ.setdefault("MASTER_ADDR", "127.0.0.1"); os.environ.setdefault("MASTER_PORT", __PORT__)
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+comm = dl.Comm.from_process_group()
+s = ModelShape("tp1", h=512, n_heads=4, n_kv_heads=2, head_dim=128, m=1024, n_layers=1, vocab=10)
+rk = block_ranks(s, 0.4)
+w = gen_block_weights(s, rk, 0, 21)
+cfgo = oracle.BlockCfg(s.h, s.n_heads, s.n_kv_heads, s.head_dim, s.m, rk["q"], rk["k"], rk["v"], rk["o"],
+                       rk["gate"], rk["up"], rk["down"], rope_theta=s.rope_theta, rms_eps=s.rms_eps)
+def rel(a, b):
+    a = np.asarray(a, np.float64); b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+wd = dl.BlockWeights({k: v.cuda() for k, v in w.items()}, world=1, rank=0)
+errs = []
+for T in (40, 300):                       # skinny (stream-K) and wide (whole-tile) paths, prefill
+    x = gen_normal((T, s.h), 1.0, 22, dtype=torch.bfloat16)
+    cfg = dl.make_block_config(s, rk, max_tokens=T, max_seqs=1)
+    ws = torch.zeros(dl.dl_block_workspace(cfg, 1), dtype=torch.uint8, device="cuda")
+    kc = torch.zeros(1, s.n_kv_heads, T, s.head_dim, dtype=torch.bfloat16, device="cuda"); vc = torch.zeros_like(kc)
+    pos = torch.arange(T, dtype=torch.int32, device="cuda"); cu = torch.tensor([0, T], dtype=torch.int32, device="cuda")
+    xd = x.cuda()
+    dl.dl_decomposed_block_forward(cfg, wd, xd, pos, cu, 1, dl.DL_PREFILL, kc, vc,
+                                   torch.zeros(1, dtype=torch.int32, device="cuda"), comm, ws)
+    torch.cuda.synchronize()
+    ref, _, _ = oracle.block_prefill(cfgo, w, x, np.arange(T), [0, T])
+    errs.append(rel(xd.cpu().double() - x.double(), ref - x.double().numpy()))
+S = 8                                     # decode with cache
+lens = [5, 0, 17, 3, 9, 1, 30, 12]
+x = gen_normal((S, s.h), 1.0, 23, dtype=torch.bfloat16)
+kc = gen_normal((S, s.n_kv_heads, 31, s.head_dim), 1.0, 24, dtype=torch.bfloat16)
+vc = gen_normal((S, s.n_kv_heads, 31, s.head_dim), 1.0, 25, dtype=torch.bfloat16)
+ko = kc.permute(0, 2, 1, 3).reshape(S, 31, -1); vo = vc.permute(0, 2, 1, 3).reshape(S, 31, -1)
+cfg = dl.make_block_config(s, rk, max_tokens=S, max_seqs=S)
+ws = torch.zeros(dl.dl_block_workspace(cfg, 1), dtype=torch.uint8, device="cuda")
+cl = torch.tensor(lens, dtype=torch.int32, device="cuda")
+xd = x.cuda()
+dl.dl_decomposed_block_forward(cfg, wd, xd, cl, None, S, dl.DL_DECODE, kc.cuda(), vc.cuda(), cl, comm, ws)
+torch.cuda.synchronize()
+ref, _, _ = oracle.block_decode(cfgo, w, x, ko, vo, lens)
+errs.append(rel(xd.cpu().double() - x.double(), ref - x.double().numpy()))
+print("ERRS", errs)
+dist.destroy_process_group()
+'''
+
+
+def test_block_tp_code_path_one_rank_nccl():
+    from paper_2604_17709_b200 import build
+    build.build()
+    env = dict(os.environ, DL_FORCE_TP_PATH="1")
+    src = SCRIPT.replace("__ROOT__", repr(ROOT)).replace("__PORT__", repr("29533"))
+    r = subprocess.run([sys.executable, "-c", src], capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    line = [ln for ln in r.stdout.splitlines() if ln.startswith("ERRS")][-1]
+    errs = eval(line[5:])
+    assert all(e <= 2e-2 for e in errs), errs
