@@ -494,6 +494,7 @@ struct BlockWs {
   float* apart;                      // split-KV attention partials (decode)
   size_t apart_bytes;
   unsigned int* sched;               // kSchedSlots x 2 stream-K work counters
+  unsigned int* tile_cnt;            // stream-K fixup arrival counters (one per output tile)
   int64_t ldz32, ldzb, ldy32;
 };
 
@@ -518,6 +519,7 @@ BlockWs carve_block(Carver& c, const BlockDims& d, int64_t Tmax) {
   w.apart_bytes = attention_workspace(Ts, static_cast<int>(d.Hq_loc), static_cast<int>(d.d));
   w.apart = c.take<float>(w.apart_bytes / sizeof(float));
   w.sched = c.take<unsigned int>(2 * kSchedSlots);
+  w.tile_cnt = c.take<unsigned int>(static_cast<size_t>((d.nmax + d.kmax) / 128 + 64));
   return w;
 }
 
@@ -605,20 +607,49 @@ GemmProblem stage2(const dl_factor_group& grp, int nseg, const int64_t* rows, co
 
 // One factor group: Z = act . B^T (Z kept as bf16 in the workspace), then
 // Y = Z . A_g^T into `out2` (skinny: stream-K fp32 reduction; wide: bf16).
+// Stream-K last-contributor fixups are opt-in (DL_FIXUP=1).  Measured on B200
+// (tools/decode_timeline.py, 4 x 70B layers): 2.2-2.5 ms with fixups vs
+// 1.8-1.9 ms with separate finalize kernels -- under static stream-K every
+// tile's last contributor finishes at the end of its range, so all finalizes
+// (and their fence / counter round trips) pile onto the kernel's tail, while a
+// PDL-launched finalize kernel overlaps the GEMM drain.
+bool use_fixup() {
+  static const bool on = getenv("DL_FIXUP") && atoi(getenv("DL_FIXUP")) != 0;
+  return on;
+}
+
+// One factor group: Z = act . B^T (bf16 Z in the workspace), then
+// Y = Z . A_g^T into `out2` (skinny: stream-K fp32 reduction; wide: bf16).
+// Skinny path: stage 1 finalizes Z to bf16 in its last-contributor fixup; a
+// stage-2 fixup `fix2` (op != FIX_NONE) finalizes the group output in place
+// of a separate kernel (then `out2` only supplies the output pointer/layout).
 dl_status run_group(const dl_factor_group& grp, int nseg, const int64_t* rows, const __nv_bfloat16* act,
                     int64_t ld_act, int64_t n, int64_t T, bool skinny, const BlockWs& ws, const GemmOut& out2,
-                    cudaStream_t st) {
+                    cudaStream_t st, const GemmFixup* fix2 = nullptr) {
   const ZLayout zl = zlayout(grp, nseg);
   if (skinny) {
-    GemmProblem p1 = stage1(grp, nseg, act, ld_act, T, n, zl, out_plain(ws.zf, ws.ldz32, OUT_F32_RED, 0));
-    p1.sched = next_sched(ws.sched);
-    DL_TRY(tc_gemm(p1, true, st));
-    DL_TRY(launch_f32_to_bf16(ws.zf, ws.ldz32, ws.zb, ws.ldzb, T, zl.width, 1, st));
+    if (use_fixup()) {
+      GemmProblem p1 = stage1(grp, nseg, act, ld_act, T, n, zl, out_plain(ws.zb, ws.ldzb, OUT_BF16, 0));
+      p1.sched = next_sched(ws.sched);
+      p1.fix.op = FIX_BF16;
+      p1.fix.acc32 = ws.zf;
+      p1.fix.acc_ld = ws.ldz32;
+      p1.fix.tile_cnt = ws.tile_cnt;
+      DL_TRY(tc_gemm(p1, true, st));
+    } else {
+      GemmProblem p1 = stage1(grp, nseg, act, ld_act, T, n, zl, out_plain(ws.zf, ws.ldz32, OUT_F32_RED, 0));
+      p1.sched = next_sched(ws.sched);
+      DL_TRY(tc_gemm(p1, true, st));
+      DL_TRY(launch_f32_to_bf16(ws.zf, ws.ldz32, ws.zb, ws.ldzb, T, zl.width, 1, st));
+    }
   } else {
     DL_TRY(tc_gemm(stage1(grp, nseg, act, ld_act, T, n, zl, out_plain(ws.zb, ws.ldzb, OUT_BF16, 0)), false, st));
   }
   GemmProblem p2 = stage2(grp, nseg, rows, ws.zb, ws.ldzb, T, zl, out2);
-  if (skinny) p2.sched = next_sched(ws.sched);
+  if (skinny) {
+    p2.sched = next_sched(ws.sched);
+    if (fix2 && fix2->op != FIX_NONE) p2.fix = *fix2;
+  }
   return tc_gemm(p2, skinny, st);
 }
 
@@ -719,8 +750,21 @@ dl_status dl_decomposed_block_forward(const dl_block_config* cfg, const dl_block
   qkv_out.ptr = skinny ? static_cast<void*>(ws.yf) : static_cast<void*>(ws.yb);
   qkv_out.ld = skinny ? ws.ldy32 : NQKV;
 
-  DL_TRY(launch_rmsnorm(x, static_cast<const __nv_bfloat16*>(w->attn_norm), ws.xn, T, d.h, cfg->rms_eps, st));
-  DL_TRY(run_group(w->qkv, 3, qkv_rows, ws.xn, d.h, d.h, T, skinny, ws, qkv_out, st));
+  // skinny, single rank: every group's finalize (RoPE + cache append, residual,
+  // SiLU*up) runs in the stage-2 GEMM's last-contributor fixup
+  const bool fx = skinny && !tp && use_fixup();
+  auto fixup = [&](int op) {
+    GemmFixup f{};
+    f.op = op;
+    f.acc32 = ws.yf;
+    f.acc_ld = ws.ldy32;
+    f.tile_cnt = ws.tile_cnt;
+    f.resid = x;
+    f.ld_resid = d.h;
+    f.act_out = ws.act;
+    f.ld_act_out = d.m;
+    return f;
+  };
 
   RopeCacheArgs rc{};
   rc.q_out = ws.q;
@@ -737,7 +781,19 @@ dl_status dl_decomposed_block_forward(const dl_block_config* cfg, const dl_block
   rc.Hk = static_cast<int>(d.Hk_loc);
   rc.d = static_cast<int>(d.d);
   rc.theta = cfg->rope_theta;
-  if (!tp) {
+
+  DL_TRY(launch_rmsnorm(x, static_cast<const __nv_bfloat16*>(w->attn_norm), ws.xn, T, d.h, cfg->rms_eps, st));
+  if (fx) {
+    GemmFixup f = fixup(FIX_ROPE_CACHE);
+    f.rope = rc;
+    DL_TRY(run_group(w->qkv, 3, qkv_rows, ws.xn, d.h, d.h, T, skinny, ws, qkv_out, st, &f));
+  } else {
+    DL_TRY(run_group(w->qkv, 3, qkv_rows, ws.xn, d.h, d.h, T, skinny, ws, qkv_out, st));
+  }
+
+  if (fx) {
+    // RoPE + cache append done by the q|k|v stage-2 fixup
+  } else if (!tp) {
     if (skinny) {
       rc.acc = ws.yf;
       rc.ld_src = ws.ldy32;
@@ -752,7 +808,7 @@ dl_status dl_decomposed_block_forward(const dl_block_config* cfg, const dl_block
     rc.src = ws.rs;
     rc.ld_src = d.W;
   }
-  DL_TRY(launch_rope_cache(rc, st));
+  if (!fx) DL_TRY(launch_rope_cache(rc, st));
 
   AttnArgs aa{};
   aa.q = ws.q;
@@ -795,22 +851,26 @@ dl_status dl_decomposed_block_forward(const dl_block_config* cfg, const dl_block
   };
 
   // ---- o projection + residual ----------------------------------------------
-  DL_TRY(run_group(w->o, 1, h_rows, att_in, d.h, d.h, T, skinny, ws, resid_out(), st));
-  DL_TRY(finish_residual(d.h));
+  const GemmFixup fres = fixup(fx ? FIX_RESIDUAL : FIX_NONE);
+  DL_TRY(run_group(w->o, 1, h_rows, att_in, d.h, d.h, T, skinny, ws, resid_out(), st, &fres));
+  if (!fx) DL_TRY(finish_residual(d.h));
 
   // ---- MLP: gate|up group, SiLU(gate)*up, down + residual ----------------------
   DL_TRY(launch_rmsnorm(x, static_cast<const __nv_bfloat16*>(w->mlp_norm), ws.xn, T, d.h, cfg->rms_eps, st));
   GemmOut gu_out = skinny ? out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0) : out_plain(ws.yb, 2 * d.m, OUT_BF16, 0);
-  DL_TRY(run_group(w->gu, 2, gu_rows, ws.xn, d.h, d.h, T, skinny, ws, gu_out, st));
-  if (!tp && skinny) {
+  const GemmFixup fsilu = fixup(fx ? FIX_SILU : FIX_NONE);
+  DL_TRY(run_group(w->gu, 2, gu_rows, ws.xn, d.h, d.h, T, skinny, ws, gu_out, st, &fsilu));
+  if (fx) {
+    // SiLU(gate)*up done by the gate|up stage-2 fixup
+  } else if (!tp && skinny) {
     DL_TRY(launch_silu_mul_f32(ws.yf, ws.ldy32, ws.act, d.m, T, d.m, 1, st));
   } else {
     if (skinny) DL_TRY(launch_f32_to_bf16(ws.yf, ws.ldy32, ws.yb, 2 * d.m, T, 2 * d.m, 1, st));
     if (tp) DL_TRY(all_reduce(comm, ws.yb, static_cast<size_t>(T) * 2 * d.m, kNcclBfloat16, st));
     DL_TRY(launch_silu_mul_bf16(ws.yb, 2 * d.m, ws.act, d.m, T, d.m, st));
   }
-  DL_TRY(run_group(w->down, 1, h_rows, ws.act, d.m, d.m, T, skinny, ws, resid_out(), st));
-  DL_TRY(finish_residual(d.h));
+  DL_TRY(run_group(w->down, 1, h_rows, ws.act, d.m, d.m, T, skinny, ws, resid_out(), st, &fres));
+  if (!fx) DL_TRY(finish_residual(d.h));
   return DL_OK;
 }
 // ---------------------------------------------------------------------------

@@ -52,6 +52,32 @@ dl_status launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
 // act is bf16 row-major [T x Kact] (ld in elements); each segment's weight is
 // bf16 row-major [rows x klen] (K-major).  Tiles never straddle segments.
 // ---------------------------------------------------------------------------
+// q|k|v local rows [T x (Hq + 2 Hk) * d] (fp32 acc or bf16): RoPE on q, k;
+// q written (bf16) to q_out [T x Hq*d]; k, v appended to the cache at
+// position cache_lens[seq(t)] + (t - cu[seq]) (decode: seq = t).
+struct RopeCacheArgs {
+  const float* acc; const __nv_bfloat16* src; int64_t ld_src; int clear;
+  __nv_bfloat16* q_out;
+  __nv_bfloat16* k_cache; __nv_bfloat16* v_cache; int64_t max_seq;
+  const int32_t* positions; const int32_t* cu_seqlens; const int32_t* cache_lens;
+  int32_t num_seqs; int decode;
+  int64_t T; int Hq, Hk, d; float theta;
+};
+
+// Last-contributor finalize of a stream-K GEMM (FixupOp); buffers zeroed on entry,
+// left zeroed on exit.
+struct GemmFixup {
+  int op;                       // FixupOp
+  float* acc32;                 // fp32 reduction scratch, output layout (plain rows: acc_ld)
+  int64_t acc_ld;
+  unsigned int* tile_cnt;       // >= number of output tiles, zeroed
+  __nv_bfloat16* resid;         // FIX_RESIDUAL: x += y
+  int64_t ld_resid;
+  __nv_bfloat16* act_out;       // FIX_SILU: act = silu(seg0) * seg1
+  int64_t ld_act_out;
+  RopeCacheArgs rope;           // FIX_ROPE_CACHE
+};
+
 struct GemmSeg {
   const void* w;      // [rows x klen] bf16 (may be null iff klen == 0)
   int64_t ldw;        // elements
@@ -62,6 +88,8 @@ struct GemmSeg {
 };
 
 enum OutMode { OUT_BF16 = 0, OUT_F32_RED = 1, OUT_F32_STORE = 2 };
+// Finalize applied by the last stream-K contributor of each output tile.
+enum FixupOp { FIX_NONE = 0, FIX_BF16 = 1, FIX_RESIDUAL = 2, FIX_SILU = 3, FIX_ROPE_CACHE = 4 };
 
 struct GemmOut {
   void* ptr;
@@ -92,6 +120,8 @@ struct GemmProblem {
   // memory enabling the hybrid static + dynamic split; null -> static split.
   // Launches that may overlap (PDL) must use different counter pairs.
   unsigned int* sched;
+  // stream-K + swap only: last-arriver finalize (requires sched)
+  GemmFixup fix;
 };
 
 // Picks the tile configuration (swap-AB for T <= 256, stream-K when the
@@ -134,17 +164,7 @@ dl_status launch_silu_mul_f32(float* acc, int64_t ld_acc, __nv_bfloat16* act,
 dl_status launch_silu_mul_bf16(const __nv_bfloat16* src, int64_t ld_src,
                                __nv_bfloat16* act, int64_t ld_act, int64_t T,
                                int64_t m, cudaStream_t st);
-// q|k|v local rows [T x (Hq + 2 Hk) * d] (fp32 acc or bf16): RoPE on q, k;
-// q written (bf16) to q_out [T x Hq*d]; k, v appended to the cache at
-// position cache_lens[seq(t)] + (t - cu[seq]).
-struct RopeCacheArgs {
-  const float* acc; const __nv_bfloat16* src; int64_t ld_src; int clear;
-  __nv_bfloat16* q_out;
-  __nv_bfloat16* k_cache; __nv_bfloat16* v_cache; int64_t max_seq;
-  const int32_t* positions; const int32_t* cu_seqlens; const int32_t* cache_lens;
-  int32_t num_seqs; int decode;
-  int64_t T; int Hq, Hk, d; float theta;
-};
+// RoPE + cache append as a standalone kernel (see RopeCacheArgs)
 dl_status launch_rope_cache(const RopeCacheArgs& a, cudaStream_t st);
 dl_status launch_embedding(const __nv_bfloat16* table, int64_t vocab, int64_t h,
                            const int32_t* ids, int64_t T, __nv_bfloat16* out,

@@ -44,7 +44,7 @@ constexpr int BK = 64;   // K elements per stage = one 128-byte swizzle row
 constexpr int BM = 128;  // MMA M = TMEM lanes
 constexpr int kThreads = 320;   // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
 constexpr int kJobRing = 8;     // producer -> MMA / epilogue job queue depth
-constexpr int kL2Prefetch = 24; // decode: weight tiles pulled into L2 while waiting (PDL)
+constexpr int kL2Prefetch = 0;  // weight tiles pulled into L2 before griddepcontrol.wait (DL_L2PF); measured: 24 costs ~1 ms per 70B decode step
 
 struct KSeg {
   int feat_begin, feat_end;  // global output features [begin, end)
@@ -80,7 +80,221 @@ struct KArgs {
   unsigned int* sched;
   long long static_units, dyn_begin;
   int chunk;
+  int l2pf;                  // weight tiles prefetched into L2 before griddepcontrol.wait
+  // Stream-K fixup (swap-AB stream-K only): contributors red.add fp32 partials
+  // into acc32 (same layout as the output, plain rows use acc_ld), bump
+  // tile_cnt[tile]; the last contributor applies `fixup` to the reduced tile,
+  // writes the final output and zeroes acc32 / the counter.
+  int fixup;                 // FixupOp
+  float* acc32;
+  long long acc_ld;
+  unsigned int* tile_cnt;
+  __nv_bfloat16* resid;      // FIX_RESIDUAL target x [T x ld_resid]
+  long long ld_resid;
+  __nv_bfloat16* act_out;    // FIX_SILU output [T x ld_act_out] (gate = seg 0, up = seg 1)
+  long long ld_act_out;
+  RopeCacheArgs rope;        // FIX_ROPE_CACHE (q|k|v segments, one 128-feature head per tile)
 };
+
+__device__ __forceinline__ long long acc_index(const KArgs& a, const KSeg& s, int tok, int f) {
+  if (a.scatter_p <= 0) return static_cast<long long>(tok) * a.acc_ld + s.col_off + (f - s.feat_begin);
+  long long loc = f - s.feat_begin;
+  long long owner = loc / s.rpr;
+  return owner * static_cast<long long>(a.T) * a.slab + static_cast<long long>(tok) * a.slab + s.slab_off +
+         loc % s.rpr;
+}
+
+// Number of stream-K pieces (jobs) covering the unit interval [lo, hi) under
+// the hybrid partition: static range starts c*S (1 <= c <= grid) and dynamic
+// chunk starts dyn_begin + i*chunk (i >= 1) that fall strictly inside.
+__device__ __forceinline__ int pieces_in(const KArgs& a, long long lo, long long hi, int grid) {
+  int n = 1;
+  const long long S = a.static_units;
+  if (S > 0) {
+    long long c0 = lo / S + 1;                       // first c with c*S > lo
+    long long c1 = (hi - 1) / S;                     // last c with c*S < hi
+    if (c1 > grid) c1 = grid;
+    if (c1 >= c0) n += static_cast<int>(c1 - c0 + 1);
+  }
+  const long long D = a.dyn_begin, C = a.chunk;
+  long long i0 = lo < D ? 1 : (lo - D) / C + 1;      // first i >= 1 with D + i*C > lo
+  long long i1 = hi - 1 < D ? 0 : (hi - 1 - D) / C;  // last i with D + i*C < hi
+  if (i1 >= i0) n += static_cast<int>(i1 - i0 + 1);
+  return n;
+}
+
+struct Job {
+  int seg, feat0, tok0, kb0, kb1;
+};
+
+__device__ __forceinline__ long long out_index(const KArgs& a, const KSeg& s, int tok, int f) {
+  if (a.scatter_p <= 0) return static_cast<long long>(tok) * a.ldo + s.col_off + (f - s.feat_begin);
+  long long loc = f - s.feat_begin;
+  long long owner = loc / s.rpr;
+  long long col = s.slab_off + loc % s.rpr;
+  return owner * static_cast<long long>(a.T) * a.slab + static_cast<long long>(tok) * a.slab + col;
+}
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }   // 8 epilogue warps
+
+__device__ __forceinline__ float silu_f(float g) { return g / (1.f + __expf(-g)); }
+
+__device__ __forceinline__ float4 ldcg4(const float* p) { return __ldcg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ void st4zero(float* p) { *reinterpret_cast<float4*>(p) = make_float4(0.f, 0.f, 0.f, 0.f); }
+__device__ __forceinline__ void st_bf16x4(__nv_bfloat16* p, float a, float b, float c, float d) {
+  uint2 o;
+  reinterpret_cast<__nv_bfloat162*>(&o)[0] = __floats2bfloat162_rn(a, b);
+  reinterpret_cast<__nv_bfloat162*>(&o)[1] = __floats2bfloat162_rn(c, d);
+  *reinterpret_cast<uint2*>(p) = o;
+}
+
+// Stream-K fixup for one finished job of the swap-AB kernel (feature tile of
+// 128 rows, all tokens).  Runs on the 256 epilogue threads (etid 0..255).
+// Release: the CTA's red.add partials are ordered before the counter update by
+// bar.sync + one thread's gpu-scope fence (cumulative, as in split-K
+// semaphores).  The last contributor of the tile (or of the gate/up tile pair
+// for FIX_SILU) then reads the reduced fp32 tile from L2 (float4, 8 loads in
+// flight per thread), applies the finalize op, writes the final output and
+// zeroes the scratch and the counter.
+__device__ __noinline__ void fixup_tile(const KArgs& a, const struct Job& j, int etid, int& last_flag) {
+  epi_bar();
+  const KSeg& s = a.seg[j.seg];
+  const int tl = (j.feat0 - s.feat_begin) / 128;   // tile index inside its segment
+  const int ci = a.fixup == FIX_SILU ? tl : s.tile_first + tl;
+  if (etid == 0) {
+    int expected;
+    if (a.fixup == FIX_SILU) {
+      const KSeg& g0 = a.seg[0];
+      const KSeg& g1 = a.seg[1];
+      expected = pieces_in(a, g0.unit_first + static_cast<long long>(tl) * g0.nkb,
+                           g0.unit_first + static_cast<long long>(tl + 1) * g0.nkb, gridDim.x) +
+                 pieces_in(a, g1.unit_first + static_cast<long long>(tl) * g1.nkb,
+                           g1.unit_first + static_cast<long long>(tl + 1) * g1.nkb, gridDim.x);
+    } else {
+      expected = pieces_in(a, s.unit_first + static_cast<long long>(tl) * s.nkb,
+                           s.unit_first + static_cast<long long>(tl + 1) * s.nkb, gridDim.x);
+    }
+    unsigned old;
+    asm volatile("fence.acq_rel.gpu;\n\tatom.add.acq_rel.gpu.global.u32 %0, [%1], 1;"
+                 : "=r"(old) : "l"(a.tile_cnt + ci) : "memory");
+    last_flag = (static_cast<int>(old) == expected - 1) ? 1 : 0;
+  }
+  epi_bar();
+  if (!last_flag) return;
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");   // acquire: all contributors' partials visible
+  const int T = a.T;
+  constexpr int V = 8;                               // float4 loads in flight per thread
+  const int nq = 32 * T;                             // float4 quads in a 128-feature x T tile
+  if (a.fixup == FIX_BF16 || a.fixup == FIX_RESIDUAL) {
+    const int nf = min(128, s.write_end - j.feat0);
+    for (int base = etid; base < nq; base += 256 * V) {
+      float4 v[V];
+      float* pa[V];
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const int q = base + k * 256, fl = (q & 31) * 4, t = q >> 5;
+        pa[k] = (q < nq && fl < nf) ? a.acc32 + acc_index(a, s, t, j.feat0 + fl) : nullptr;
+        v[k] = pa[k] ? ldcg4(pa[k]) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        if (!pa[k]) continue;
+        st4zero(pa[k]);
+        const int q = base + k * 256, fl = (q & 31) * 4, t = q >> 5;
+        const int f = j.feat0 + fl;
+        if (a.fixup == FIX_BF16) {
+          st_bf16x4(static_cast<__nv_bfloat16*>(a.out) + out_index(a, s, t, f), v[k].x, v[k].y, v[k].z, v[k].w);
+        } else {
+          __nv_bfloat16* px = a.resid + static_cast<long long>(t) * a.ld_resid + f;
+          const uint2 xo = *reinterpret_cast<const uint2*>(px);
+          const float2 x0 = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(&xo)[0]);
+          const float2 x1 = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(&xo)[1]);
+          st_bf16x4(px, x0.x + v[k].x, x0.y + v[k].y, x1.x + v[k].z, x1.y + v[k].w);
+        }
+      }
+    }
+  } else if (a.fixup == FIX_SILU) {
+    const KSeg& g0 = a.seg[0];
+    const KSeg& g1 = a.seg[1];
+    const int fg0 = g0.feat_begin + tl * 128, fu0 = g1.feat_begin + tl * 128;
+    const int nf = min(128, g0.feat_end - fg0);
+    for (int base = etid; base < nq; base += 256 * (V / 2)) {
+      float4 gv[V / 2], uv[V / 2];
+      float *pg[V / 2], *pu[V / 2];
+#pragma unroll
+      for (int k = 0; k < V / 2; ++k) {
+        const int q = base + k * 256, fl = (q & 31) * 4, t = q >> 5;
+        const bool ok = q < nq && fl < nf;
+        pg[k] = ok ? a.acc32 + acc_index(a, g0, t, fg0 + fl) : nullptr;
+        pu[k] = ok ? a.acc32 + acc_index(a, g1, t, fu0 + fl) : nullptr;
+        gv[k] = ok ? ldcg4(pg[k]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        uv[k] = ok ? ldcg4(pu[k]) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int k = 0; k < V / 2; ++k) {
+        if (!pg[k]) continue;
+        st4zero(pg[k]);
+        st4zero(pu[k]);
+        const int q = base + k * 256, fl = (q & 31) * 4, t = q >> 5;
+        st_bf16x4(a.act_out + static_cast<long long>(t) * a.ld_act_out + tl * 128 + fl, silu_f(gv[k].x) * uv[k].x,
+                  silu_f(gv[k].y) * uv[k].y, silu_f(gv[k].z) * uv[k].z, silu_f(gv[k].w) * uv[k].w);
+      }
+    }
+  } else if (a.fixup == FIX_ROPE_CACHE) {
+    const RopeCacheArgs& r = a.rope;
+    const int hh = tl;                         // head index inside the q / k / v segment
+    const float l2t = log2f(r.theta);
+    for (int base = etid; base < nq; base += 256 * V) {
+      float4 v[V];
+      float* pa[V];
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const int q = base + k * 256, e = (q & 31) * 4, t = q >> 5;
+        pa[k] = q < nq ? a.acc32 + acc_index(a, s, t, j.feat0 + e) : nullptr;
+        v[k] = pa[k] ? ldcg4(pa[k]) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        if (!pa[k]) continue;
+        st4zero(pa[k]);
+        const int q = base + k * 256, e = (q & 31) * 4, t = q >> 5;
+        float4 o = v[k];
+        if (j.seg < 2) {   // rotate pairs (e, e+1), (e+2, e+3) by pos * theta^(-e/d)
+          const float pos = static_cast<float>(r.positions[t]);
+          float s0, c0, s1, c1;
+          sincosf(pos * exp2f(-l2t * static_cast<float>(e) / r.d), &s0, &c0);
+          sincosf(pos * exp2f(-l2t * static_cast<float>(e + 2) / r.d), &s1, &c1);
+          o = make_float4(v[k].x * c0 - v[k].y * s0, v[k].x * s0 + v[k].y * c0, v[k].z * c1 - v[k].w * s1,
+                          v[k].z * s1 + v[k].w * c1);
+        }
+        if (j.seg == 0) {
+          st_bf16x4(r.q_out + static_cast<long long>(t) * r.Hq * r.d + static_cast<long long>(hh) * r.d + e, o.x, o.y,
+                    o.z, o.w);
+        } else {
+          int sq;
+          long long cpos;
+          if (r.decode) {
+            sq = t;
+            cpos = r.cache_lens[t];
+          } else {
+            int lo = 0, hi = r.num_seqs - 1;
+            while (lo < hi) {
+              const int mid = (lo + hi + 1) >> 1;
+              if (r.cu_seqlens[mid] <= t) lo = mid; else hi = mid - 1;
+            }
+            sq = lo;
+            cpos = r.cache_lens[sq] + (t - r.cu_seqlens[sq]);
+          }
+          st_bf16x4((j.seg == 1 ? r.k_cache : r.v_cache) +
+                        ((static_cast<long long>(sq) * r.Hk + hh) * r.max_seq + cpos) * r.d + e,
+                    o.x, o.y, o.z, o.w);
+        }
+      }
+    }
+  }
+  epi_bar();
+  if (etid == 0) atomicExch(a.tile_cnt + ci, 0u);
+}
 
 struct __align__(64) KMaps {
   CUtensorMap act;
@@ -101,9 +315,6 @@ __device__ __forceinline__ unsigned smid() {
   return s;
 }
 
-struct Job {
-  int seg, feat0, tok0, kb0, kb1;
-};
 
 // Job enumeration shared by the three roles (pure function of blockIdx).
 struct JobIter {
@@ -161,13 +372,6 @@ struct JobIter {
   }
 };
 
-__device__ __forceinline__ long long out_index(const KArgs& a, const KSeg& s, int tok, int f) {
-  if (a.scatter_p <= 0) return static_cast<long long>(tok) * a.ldo + s.col_off + (f - s.feat_begin);
-  long long loc = f - s.feat_begin;
-  long long owner = loc / s.rpr;
-  long long col = s.slab_off + loc % s.rpr;
-  return owner * static_cast<long long>(a.T) * a.slab + static_cast<long long>(tok) * a.slab + col;
-}
 
 template <int BN, bool SWAP, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -191,6 +395,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t jfull_bar[kJobRing];
   __shared__ __align__(8) uint64_t jempty_bar[kJobRing];
   __shared__ Job jobs[kJobRing];
+  __shared__ int fix_last;
   __shared__ uint32_t tmem_slot;
 
   const int warp = threadIdx.x / 32;
@@ -249,9 +454,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto l2_prefetch = [&]() {
         int skipped = 0, issued = 0;
         Job pj;
-        while (issued < kL2Prefetch && pf_it.next(pj, FEAT_TILE, TOK_TILE)) {
+        while (issued < a.l2pf && pf_it.next(pj, FEAT_TILE, TOK_TILE)) {
           const KSeg& ps = a.seg[pj.seg];
-          for (int kb = pj.kb0; kb < pj.kb1 && issued < kL2Prefetch; ++kb) {
+          for (int kb = pj.kb0; kb < pj.kb1 && issued < a.l2pf; ++kb) {
             if (skipped < STAGES) { ++skipped; continue; }   // these go to smem
             ptx::tma_prefetch_2d(&maps.w[pj.seg], kb * BK, pj.feat0 - ps.feat_begin);
             ++issued;
@@ -393,10 +598,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int tok0 = j.tok0 + c0;
           const int ntok = a.T - tok0;
           if (f < s.write_end && ntok > 0) {
-            const long long tstride = a.scatter_p <= 0 ? a.ldo : a.slab;
-            const long long base = out_index(a, s, tok0, f);
-            if (a.mode == OUT_F32_RED) {
-              float* p = static_cast<float*>(a.out) + base;
+            const bool fx = a.fixup != FIX_NONE;
+            const long long tstride = a.scatter_p <= 0 ? (fx ? a.acc_ld : a.ldo) : a.slab;
+            const long long base = fx ? acc_index(a, s, tok0, f) : out_index(a, s, tok0, f);
+            if (fx || a.mode == OUT_F32_RED) {
+              float* p = (fx ? a.acc32 : static_cast<float*>(a.out)) + base;
 #pragma unroll
               for (int i = 0; i < 32; ++i, p += tstride)
                 if (i < ntok) ptx::red_add_f32(p, __uint_as_float(r[i]));
@@ -491,6 +697,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_arrive(&jempty_bar[my_slot]);
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (SWAP && a.fixup != FIX_NONE) fixup_tile(a, j, threadIdx.x - 64, fix_last);
     }
     if (tr && warp == 2 && lane == 0) tr[6] = gtime();   // epilogue done
   }
@@ -805,6 +1012,30 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   a.scatter_p = p.out.scatter_p;
   a.slab = p.out.slab;
   a.trace_slot = g_trace_host_on ? g_trace_next++ : -1;
+  a.fixup = FIX_NONE;
+  static const int l2pf = getenv("DL_L2PF") ? atoi(getenv("DL_L2PF")) : kL2Prefetch;
+  a.l2pf = l2pf;
+  if (p.fix.op != FIX_NONE) {
+    bool ok = SWAP && stream_k && p.sched && p.fix.acc32 && p.fix.tile_cnt;
+    for (int g = 0; g < p.nseg; ++g) ok = ok && (p.seg[g].rows == 0 || p.seg[g].klen > 0);
+    if (p.fix.op == FIX_SILU) ok = ok && p.nseg == 2 && p.seg[0].rows == p.seg[1].rows && p.fix.act_out;
+    if (p.fix.op == FIX_RESIDUAL) ok = ok && p.nseg == 1 && p.fix.resid;
+    if (p.fix.op == FIX_ROPE_CACHE) ok = ok && p.nseg == 3 && p.out.scatter_p == 0;
+    if (!ok) {
+      set_error("tc_gemm: fixup %d needs swap-AB stream-K with scheduler, scratch and non-empty segments",
+                p.fix.op);
+      return DL_ERR_INVALID_ARG;
+    }
+    a.fixup = p.fix.op;
+    a.acc32 = p.fix.acc32;
+    a.acc_ld = p.fix.acc_ld;
+    a.tile_cnt = p.fix.tile_cnt;
+    a.resid = p.fix.resid;
+    a.ld_resid = p.fix.ld_resid;
+    a.act_out = p.fix.act_out;
+    a.ld_act_out = p.fix.ld_act_out;
+    a.rope = p.fix.rope;
+  }
   a.sched = nullptr;
   if (stream_k && p.sched) {
     static const double frac = getenv("DL_SK_STATIC") ? atof(getenv("DL_SK_STATIC")) : 0.9;
@@ -880,7 +1111,7 @@ dl_status tc_gemm(const GemmProblem& p, bool stream_k, cudaStream_t st) {
     set_error("cuTensorMapEncodeTiled unavailable (driver too old or no GPU)");
     return DL_ERR_CUDA;
   }
-  if (stream_k && p.out.mode != OUT_F32_RED) {
+  if (stream_k && p.out.mode != OUT_F32_RED && p.fix.op == FIX_NONE) {
     set_error("stream-K requires an fp32 reduction output");
     return DL_ERR_INVALID_ARG;
   }
