@@ -483,6 +483,8 @@ dl_status block_dims(const dl_block_config* c, int world, BlockDims* d) {
 // Stream-K launches rotate over kSchedSlots counter pairs: a launch can only
 // overlap (PDL) with its immediate neighbours, so 4 slots never collide.
 constexpr int kSchedSlots = 4;
+// prefill tail scratch: up to 56 tiles of 256 x 256 fp32 (>= 75% of 74 clusters)
+constexpr size_t kTailBytes = static_cast<size_t>(56) * 256 * 256 * 4;
 unsigned int* next_sched(unsigned int* base) {
   static std::atomic<unsigned> slot{0};
   return base + 2 * (slot.fetch_add(1) % kSchedSlots);
@@ -495,6 +497,8 @@ struct BlockWs {
   size_t apart_bytes;
   unsigned int* sched;               // kSchedSlots x 2 stream-K work counters
   unsigned int* tile_cnt;            // stream-K fixup arrival counters (one per output tile)
+  float* tail;                       // prefill DP + stream-K tail scratch (zero-maintained)
+  size_t tail_bytes;
   int64_t ldz32, ldzb, ldy32;
 };
 
@@ -520,6 +524,8 @@ BlockWs carve_block(Carver& c, const BlockDims& d, int64_t Tmax) {
   w.apart = c.take<float>(w.apart_bytes / sizeof(float));
   w.sched = c.take<unsigned int>(2 * kSchedSlots);
   w.tile_cnt = c.take<unsigned int>(static_cast<size_t>((d.nmax + d.kmax) / 128 + 64));
+  w.tail_bytes = Tmax > 256 ? kTailBytes : 0;
+  w.tail = w.tail_bytes ? c.take<float>(w.tail_bytes / sizeof(float)) : nullptr;
   return w;
 }
 
@@ -643,12 +649,18 @@ dl_status run_group(const dl_factor_group& grp, int nseg, const int64_t* rows, c
       DL_TRY(launch_f32_to_bf16(ws.zf, ws.ldz32, ws.zb, ws.ldzb, T, zl.width, 1, st));
     }
   } else {
-    DL_TRY(tc_gemm(stage1(grp, nseg, act, ld_act, T, n, zl, out_plain(ws.zb, ws.ldzb, OUT_BF16, 0)), false, st));
+    GemmProblem p1 = stage1(grp, nseg, act, ld_act, T, n, zl, out_plain(ws.zb, ws.ldzb, OUT_BF16, 0));
+    p1.tail_acc = ws.tail;
+    p1.tail_bytes = ws.tail_bytes;
+    DL_TRY(tc_gemm(p1, false, st));
   }
   GemmProblem p2 = stage2(grp, nseg, rows, ws.zb, ws.ldzb, T, zl, out2);
   if (skinny) {
     p2.sched = next_sched(ws.sched);
     if (fix2 && fix2->op != FIX_NONE) p2.fix = *fix2;
+  } else {
+    p2.tail_acc = ws.tail;
+    p2.tail_bytes = ws.tail_bytes;
   }
   return tc_gemm(p2, skinny, st);
 }

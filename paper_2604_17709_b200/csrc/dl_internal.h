@@ -122,6 +122,10 @@ struct GemmProblem {
   unsigned int* sched;
   // stream-K + swap only: last-arriver finalize (requires sched)
   GemmFixup fix;
+  // prefill (CTA-pair) only: zeroed fp32 scratch for the DP + stream-K tail
+  // (<= 44 tiles x 256 x 256 x 4 B); left zeroed.  null -> whole tiles only.
+  float* tail_acc;
+  size_t tail_bytes;
 };
 
 // Picks the tile configuration (swap-AB for T <= 256, stream-K when the

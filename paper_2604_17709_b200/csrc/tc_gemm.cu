@@ -81,6 +81,11 @@ struct KArgs {
   long long static_units, dyn_begin;
   int chunk;
   int l2pf;                  // weight tiles prefetched into L2 before griddepcontrol.wait
+  // DP + stream-K tail (whole-tile kernels): tiles [0, dp_tiles) whole, each of
+  // the remaining tiles split in tail_split K-pieces accumulated in fp32 into
+  // tail_acc [tail tile][256][256], finalized by tc_tail_finalize_kernel.
+  int dp_tiles, tail_split;
+  float* tail_acc;
   // Stream-K fixup (swap-AB stream-K only): contributors red.add fp32 partials
   // into acc32 (same layout as the output, plain rows use acc_ld), bump
   // tile_cnt[tile]; the last contributor applies `fixup` to the reduced tile,
@@ -125,6 +130,7 @@ __device__ __forceinline__ int pieces_in(const KArgs& a, long long lo, long long
 
 struct Job {
   int seg, feat0, tok0, kb0, kb1;
+  int part;   // >= 0: K-split piece of tail tile `part` (fp32 partial into tail_acc)
 };
 
 __device__ __forceinline__ long long out_index(const KArgs& a, const KSeg& s, int tok, int f) {
@@ -321,6 +327,7 @@ struct JobIter {
   const KArgs& a;
   int cta, grid;
   int next_tile;            // whole-tile mode
+  bool tail_taken = false;  // DP + stream-K tail piece already issued
   long long u, u_end;       // stream-K mode
   __device__ JobIter(const KArgs& args, int c, int g) : a(args), cta(c), grid(g) {
     next_tile = c;
@@ -337,17 +344,34 @@ struct JobIter {
   }
   __device__ bool next(Job& j, int FEAT_TILE, int TOK_TILE) {
     if (!a.stream_k) {
-      if (next_tile >= a.total_tiles) return false;
-      int t = next_tile;
-      next_tile += grid;
+      // data-parallel whole tiles, then (DP + stream-K tail) one K-split piece
+      // of the last partial wave's tiles per CTA / cluster
+      int t, part = -1;
+      if (next_tile < a.dp_tiles) {
+        t = next_tile;
+        next_tile += grid;
+      } else if (a.tail_split > 0 && !tail_taken && cta < (a.total_tiles - a.dp_tiles) * a.tail_split) {
+        tail_taken = true;
+        part = cta / a.tail_split;
+        t = a.dp_tiles + part;
+      } else {
+        return false;
+      }
       int g = 0;
       while (g + 1 < a.nseg && t >= a.seg[g + 1].tile_first) ++g;
       int local = t - a.seg[g].tile_first;
       j.seg = g;
       j.feat0 = a.seg[g].feat_begin + (local / a.tiles_tok) * FEAT_TILE;
       j.tok0 = (local % a.tiles_tok) * TOK_TILE;
-      j.kb0 = 0;
-      j.kb1 = a.seg[g].nkb;
+      j.part = part;
+      if (part < 0) {
+        j.kb0 = 0;
+        j.kb1 = a.seg[g].nkb;
+      } else {
+        const int piece = cta % a.tail_split, nkb = a.seg[g].nkb;
+        j.kb0 = piece * nkb / a.tail_split;
+        j.kb1 = (piece + 1) * nkb / a.tail_split;
+      }
       return true;
     }
     while (u < u_end) {
@@ -365,6 +389,7 @@ struct JobIter {
       j.tok0 = (tile % a.tiles_tok) * TOK_TILE;
       j.kb0 = kb0;
       j.kb1 = kb1;
+      j.part = -1;
       u += kb1 - kb0;
       return true;
     }
@@ -864,7 +889,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int i = 0; i < 32; ++i) r[i] = 0u;
         }
         const int f0 = j.feat0 + c0;
-        if (tok < a.T && f0 < s.write_end) {
+        if (j.part >= 0) {
+          // K-split tail piece: fp32 partial of tile row (rank*128 + row), columns c0..c0+31
+          if (has_k) {
+            float* pt = a.tail_acc + (static_cast<long long>(j.part) * TILE + rank * HALF + row) * TILE + c0;
+#pragma unroll
+            for (int q = 0; q < 32; q += 4)
+              ptx::red_add_v4_f32(pt + q, __uint_as_float(r[q]), __uint_as_float(r[q + 1]), __uint_as_float(r[q + 2]),
+                                  __uint_as_float(r[q + 3]));
+          }
+        } else if (tok < a.T && f0 < s.write_end) {
           __nv_bfloat16* o = static_cast<__nv_bfloat16*>(a.out) + out_index(a, s, tok, f0);
           if (f0 + 32 <= s.write_end && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
 #pragma unroll
@@ -911,6 +945,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   ptx::cluster_sync();
   ptx::tc_fence_after();
   if (warp == 1) ptx::tmem_dealloc_pair<TMEM_COLS>(tmem_base);
+}
+
+// DP + stream-K tail finalize: grid (tail tiles, 8 row blocks of 32 token rows),
+// 256 threads = 64 float4 column groups x 4 row lanes; each thread issues its
+// 8 float4 loads before using them.  out = bf16(sum of K-pieces (+ out));
+// scratch cleared.  ~100 CTAs: one resident wave, so the next GEMM launches early.
+__global__ void __launch_bounds__(256) tc_tail_finalize_kernel(KArgs a) {
+  pdl_trigger();
+  pdl_wait();
+  const int tt = blockIdx.x, rb = blockIdx.y;
+  const int t = a.dp_tiles + tt;
+  int g = 0;
+  while (g + 1 < a.nseg && t >= a.seg[g + 1].tile_first) ++g;
+  const KSeg& s = a.seg[g];
+  const int local = t - s.tile_first;
+  const int feat0 = s.feat_begin + (local / a.tiles_tok) * 256;
+  const int tok0 = (local % a.tiles_tok) * 256 + rb * 32;
+  const int c4 = (threadIdx.x & 63) * 4, lane_r = threadIdx.x >> 6;
+  const int f = feat0 + c4;
+  float4 v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = rb * 32 + lane_r + 4 * i;
+    v[i] = __ldcg(reinterpret_cast<const float4*>(a.tail_acc + (static_cast<long long>(tt) * 256 + r) * 256 + c4));
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = rb * 32 + lane_r + 4 * i;
+    *reinterpret_cast<float4*>(a.tail_acc + (static_cast<long long>(tt) * 256 + r) * 256 + c4) =
+        make_float4(0.f, 0.f, 0.f, 0.f);
+    const int tok = tok0 + lane_r + 4 * i;
+    if (tok >= a.T) continue;
+    const float vv[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (f + e >= s.write_end) break;
+      __nv_bfloat16* o = static_cast<__nv_bfloat16*>(a.out) + out_index(a, s, tok, f + e);
+      *o = __float2bfloat16_rn(a.accumulate ? vv[e] + __bfloat162float(*o) : vv[e]);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1012,6 +1086,9 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   a.scatter_p = p.out.scatter_p;
   a.slab = p.out.slab;
   a.trace_slot = g_trace_host_on ? g_trace_next++ : -1;
+  a.dp_tiles = tiles;
+  a.tail_split = 0;
+  a.tail_acc = nullptr;
   a.fixup = FIX_NONE;
   static const int l2pf = getenv("DL_L2PF") ? atoi(getenv("DL_L2PF")) : kL2Prefetch;
   a.l2pf = l2pf;
@@ -1058,6 +1135,17 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   } else if (PAIR) {
     const int clusters = sms / 2;
     grid = 2 * (tiles < clusters ? (tiles > 0 ? tiles : 1) : clusters);
+    // DP + stream-K tail: a last wave filled to <= 75% is split along K
+    static const bool dpsk = !getenv("DL_PREFILL_DPSK") || atoi(getenv("DL_PREFILL_DPSK")) != 0;
+    const int full = tiles / clusters, tail = tiles % clusters;
+    if (dpsk && p.tail_acc && full >= 1 && tail > 0 && tail * 4 <= clusters * 3) {
+      const int split = clusters / tail;
+      if (split >= 2 && static_cast<size_t>(tail) * 256 * 256 * 4 <= p.tail_bytes) {
+        a.dp_tiles = tiles - tail;
+        a.tail_split = split;
+        a.tail_acc = p.tail_acc;
+      }
+    }
   } else {
     grid = tiles < sms ? (tiles > 0 ? tiles : 1) : sms;
   }
@@ -1085,6 +1173,13 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   prof_end(prof, st, bytes, flops, SWAP ? 1 : 0);
   launched("tc_gemm");
   if (e == cudaSuccess) e = cudaGetLastError();
+  if (e == cudaSuccess && a.tail_split > 0) {
+    const int pf = prof_begin(st);
+    const dl_status fs = launch_pdl(tc_tail_finalize_kernel, dim3(a.total_tiles - a.dp_tiles, 8), dim3(256), 0,
+                                    st, "tc_gemm tail finalize", a);
+    prof_end(pf, st, 0.0, 0.0, 2);
+    if (fs != DL_OK) return fs;
+  }
   if (e != cudaSuccess) {
     set_error("tc_gemm<BN=%d,swap=%d> (T=%lld k_act=%lld nseg=%d klen=%lld/%lld/%lld koff=%lld/%lld/%lld "
               "grid=%d stream_k=%d): %s", BN, (int)SWAP, (long long)p.T, (long long)p.k_act, p.nseg,
