@@ -345,6 +345,9 @@ typedef struct {
   int64_t h, n_heads, n_kv_heads, head_dim, m;
   int64_t r_q, r_k, r_v, r_o, r_gate, r_up, r_down;
   double rope_theta, rms_eps;
+  /* Table 2 variants: mlp_glu 1 = SiLU(gate)*up (LLaMA), 0 = ReLU(up)
+     (OPT family, "NonGLU uses ReLU"); use_rope 0 = no rotary embedding */
+  int64_t mlp_glu, use_rope;
 } oracle_block_cfg;
 
 typedef struct {
@@ -376,9 +379,13 @@ static int block_tail(const oracle_block_cfg *c, const oracle_block_w *w,
   int rc = lr(att, w->A_o, w->B_o, o, T, h, h, c->r_o, world, align);
   for (int64_t i = 0; i < T * h; ++i) x_out[i] = x_in[i] + o[i];
   oracle_rmsnorm(x_out, w->g_mlp, c->rms_eps, xn, T, h);
-  rc |= lr(xn, w->A_gate, w->B_gate, gt, T, m, h, c->r_gate, world, align);
   rc |= lr(xn, w->A_up, w->B_up, up, T, m, h, c->r_up, world, align);
-  for (int64_t i = 0; i < T * m; ++i) gt[i] = silu(gt[i]) * up[i];
+  if (c->mlp_glu) {
+    rc |= lr(xn, w->A_gate, w->B_gate, gt, T, m, h, c->r_gate, world, align);
+    for (int64_t i = 0; i < T * m; ++i) gt[i] = silu(gt[i]) * up[i];
+  } else {
+    for (int64_t i = 0; i < T * m; ++i) gt[i] = up[i] > 0.0 ? up[i] : 0.0;   /* ReLU */
+  }
   rc |= lr(gt, w->A_down, w->B_down, dn, T, h, m, c->r_down, world, align);
   for (int64_t i = 0; i < T * h; ++i) x_out[i] += dn[i];
   free(o); free(xn); free(gt); free(up); free(dn);
@@ -412,7 +419,7 @@ int oracle_block_prefill(const oracle_block_cfg *c, const oracle_block_w *w,
   oracle_rmsnorm(x, w->g_attn, c->rms_eps, a, T, h);
   rc |= lr(a, w->A_k, w->B_k, kk, T, hkv, h, c->r_k, world, align);
   rc |= lr(a, w->A_v, w->B_v, vv, T, hkv, h, c->r_v, world, align);
-  oracle_rope(kk, pos, T, Hkv, d, c->rope_theta);
+  if (c->use_rope) oracle_rope(kk, pos, T, Hkv, d, c->rope_theta);
   for (int64_t r = 0; r < n_rows; ++r) {
     int64_t t = rows ? rows[r] : r;
     memcpy(xr + r * h, x + t * h, sizeof(double) * (size_t)h);
@@ -420,7 +427,7 @@ int oracle_block_prefill(const oracle_block_cfg *c, const oracle_block_w *w,
     pr[r] = pos[t];
   }
   rc |= lr(ar, w->A_q, w->B_q, qr, n_rows, h, h, c->r_q, world, align);
-  oracle_rope(qr, pr, n_rows, H, d, c->rope_theta);
+  if (c->use_rope) oracle_rope(qr, pr, n_rows, H, d, c->rope_theta);
   /* causal attention of each requested row over its own sequence prefix */
   for (int64_t r = 0; r < n_rows; ++r) {
     int64_t t = rows ? rows[r] : r;
@@ -466,8 +473,10 @@ int oracle_block_decode(const oracle_block_cfg *c, const oracle_block_w *w,
   rc |= lr(a, w->A_q, w->B_q, q, Bn, h, h, c->r_q, world, align);
   rc |= lr(a, w->A_k, w->B_k, kk, Bn, hkv, h, c->r_k, world, align);
   rc |= lr(a, w->A_v, w->B_v, vv, Bn, hkv, h, c->r_v, world, align);
-  oracle_rope(q, cache_len, Bn, H, d, c->rope_theta);
-  oracle_rope(kk, cache_len, Bn, Hkv, d, c->rope_theta);
+  if (c->use_rope) {
+    oracle_rope(q, cache_len, Bn, H, d, c->rope_theta);
+    oracle_rope(kk, cache_len, Bn, Hkv, d, c->rope_theta);
+  }
 #pragma omp parallel for schedule(dynamic)
   for (int64_t b = 0; b < Bn; ++b) {
     int64_t nk = cache_len[b] + 1;
@@ -495,7 +504,7 @@ int64_t oracle_block_params(const oracle_block_cfg *c) {
   int64_t h = c->h, hkv = c->n_kv_heads * c->head_dim, m = c->m;
   return oracle_factor_params(h, h, c->r_q) + oracle_factor_params(hkv, h, c->r_k) +
          oracle_factor_params(hkv, h, c->r_v) + oracle_factor_params(h, h, c->r_o) +
-         oracle_factor_params(m, h, c->r_gate) + oracle_factor_params(m, h, c->r_up) +
+         (c->mlp_glu ? oracle_factor_params(m, h, c->r_gate) : 0) + oracle_factor_params(m, h, c->r_up) +
          oracle_factor_params(h, m, c->r_down);
 }
 

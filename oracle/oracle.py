@@ -186,7 +186,8 @@ class _CCfg(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in
                 ("h", "n_heads", "n_kv_heads", "head_dim", "m",
                  "r_q", "r_k", "r_v", "r_o", "r_gate", "r_up", "r_down")] + \
-               [("rope_theta", ctypes.c_double), ("rms_eps", ctypes.c_double)]
+               [("rope_theta", ctypes.c_double), ("rms_eps", ctypes.c_double), ("mlp_glu", ctypes.c_int64),
+                ("use_rope", ctypes.c_int64)]
 
 
 _WNAMES = ("g_attn", "g_mlp", "A_q", "B_q", "A_k", "B_k", "A_v", "B_v", "A_o", "B_o",
@@ -201,7 +202,7 @@ class BlockCfg:
     """Plain record of block dimensions / ranks (names as in Table 1)."""
 
     def __init__(self, h, n_heads, n_kv_heads, head_dim, m, r_q, r_k, r_v, r_o,
-                 r_gate, r_up, r_down, rope_theta=500000.0, rms_eps=1e-5):
+                 r_gate, r_up, r_down, rope_theta=500000.0, rms_eps=1e-5, mlp_glu=1, use_rope=1):
         self.__dict__.update(locals())
         del self.__dict__["self"]
 
@@ -210,6 +211,9 @@ class BlockCfg:
 
 
 def _pack_w(w: dict):
+    w = dict(w)
+    if "A_gate" not in w:          # non-GLU MLP: no gate factors (never read by the C code)
+        w["A_gate"] = w["B_gate"] = np.zeros((1, 1))
     arrs = {n: _f64(w[n]) for n in _WNAMES}
     cw = _CW(*(arrs[n].ctypes.data for n in _WNAMES))
     return cw, arrs

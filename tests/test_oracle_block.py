@@ -123,8 +123,11 @@ def test_attention_vs_torch_sdpa(orc, H, Hkv):
 SMALL = dict(h=32, n_heads=4, n_kv_heads=2, head_dim=8, m=48)
 
 
-def _dense_block_torch(x, W, g1, g2, pos, cu, H, Hkv, d, theta, eps):
-    """Independent dense LLaMA block in torch float64 (used only in the lossless-rank pin)."""
+def _dense_block_torch(x, W, g1, g2, pos, cu, H, Hkv, d, theta, eps, glu=True, use_rope=True):
+    """Independent dense block in torch float64 (used only in the lossless-rank pins).
+
+    Default = LLaMA (SiLU-GLU MLP, RoPE); glu=False = OPT-style ReLU MLP,
+    use_rope=False = no rotary embedding (Table 2 variants)."""
     x = torch.tensor(x)
     T, h = x.shape
     a = F.rms_norm(x, (h,), torch.tensor(g1), eps=eps)
@@ -135,7 +138,8 @@ def _dense_block_torch(x, W, g1, g2, pos, cu, H, Hkv, d, theta, eps):
     def rope(t, nh):
         c = torch.view_as_complex(t.reshape(T, nh, d // 2, 2).contiguous())
         return torch.view_as_real(c * rot[:, None]).reshape(T, nh * d)
-    q, k = rope(q, H), rope(k, Hkv)
+    if use_rope:
+        q, k = rope(q, H), rope(k, Hkv)
     att = torch.zeros(T, H * d, dtype=torch.float64)
     for s in range(len(cu) - 1):
         lo, hi = cu[s], cu[s + 1]
@@ -145,15 +149,22 @@ def _dense_block_torch(x, W, g1, g2, pos, cu, H, Hkv, d, theta, eps):
         att[lo:hi] = F.scaled_dot_product_attention(tq, tk, tv, is_causal=True).transpose(0, 1).reshape(-1, H * d)
     x = x + att @ torch.tensor(W["o"]).T
     b = F.rms_norm(x, (h,), torch.tensor(g2), eps=eps)
-    y = F.silu(b @ torch.tensor(W["gate"]).T) * (b @ torch.tensor(W["up"]).T)
+    if glu:
+        y = F.silu(b @ torch.tensor(W["gate"]).T) * (b @ torch.tensor(W["up"]).T)
+    else:
+        y = F.relu(b @ torch.tensor(W["up"]).T)
     return (x + y @ torch.tensor(W["down"]).T).numpy()
 
 
-def _small_block(orc, lossless, seed=0):
+def _small_block(orc, lossless, seed=0, n_kv_heads=None, glu=True, use_rope=True):
     r = np.random.default_rng(seed)
-    s = SMALL
+    s = dict(SMALL)
+    if n_kv_heads is not None:
+        s["n_kv_heads"] = n_kv_heads
     h, hkv, m = s["h"], s["n_kv_heads"] * s["head_dim"], s["m"]
     dims = {"q": (h, h), "k": (hkv, h), "v": (hkv, h), "o": (h, h), "gate": (m, h), "up": (m, h), "down": (h, m)}
+    if not glu:
+        del dims["gate"]
     ranks = {nm: (min(mn) if lossless else max(1, int(0.6 * min(mn) + 0.5))) for nm, mn in dims.items()}
     W, w = {}, {}
     for nm, (mo, ni) in dims.items():
@@ -165,7 +176,8 @@ def _small_block(orc, lossless, seed=0):
     w["g_attn"] = 1 + 0.1 * r.standard_normal(h)
     w["g_mlp"] = 1 + 0.1 * r.standard_normal(h)
     cfg = orc.BlockCfg(h, s["n_heads"], s["n_kv_heads"], s["head_dim"], m, ranks["q"], ranks["k"], ranks["v"],
-                       ranks["o"], ranks["gate"], ranks["up"], ranks["down"], rope_theta=10000.0, rms_eps=1e-5)
+                       ranks["o"], ranks.get("gate", 0), ranks["up"], ranks["down"], rope_theta=10000.0,
+                       rms_eps=1e-5, mlp_glu=int(glu), use_rope=int(use_rope))
     return cfg, w, W
 
 
@@ -181,6 +193,69 @@ def test_block_lossless_equals_dense(orc):
     ref = _dense_block_torch(x, W, w["g_attn"], w["g_mlp"], pos, cu, cfg.n_heads, cfg.n_kv_heads,
                              cfg.head_dim, cfg.rope_theta, cfg.rms_eps)
     assert rel(out, ref) < 1e-12
+
+
+VARIANTS = [  # (n_kv_heads, glu, use_rope): Table 2 model families
+    (4, True, True),     # MHA (LLaMA-2-7B-like)
+    (1, True, True),     # MQA
+    (4, False, False),   # OPT-like: MHA, ReLU MLP, no RoPE
+    (2, False, True),    # GQA + ReLU
+    (2, True, False),    # GQA without RoPE
+]
+
+
+@pytest.mark.parametrize("hkv,glu,use_rope", VARIANTS)
+def test_block_variant_lossless_equals_dense(orc, hkv, glu, use_rope):
+    """Same lossless pin for the attention / MLP / RoPE variants of the N4 row."""
+    cfg, w, W = _small_block(orc, lossless=True, seed=11, n_kv_heads=hkv, glu=glu, use_rope=use_rope)
+    r = np.random.default_rng(12)
+    cu = [0, 4, 11]
+    T = cu[-1]
+    pos = np.concatenate([np.arange(4), np.arange(7)])
+    x = r.standard_normal((T, cfg.h))
+    out, _, _ = orc.block_prefill(cfg, w, x, pos, cu)
+    ref = _dense_block_torch(x, W, w["g_attn"], w["g_mlp"], pos, cu, cfg.n_heads, cfg.n_kv_heads,
+                             cfg.head_dim, cfg.rope_theta, cfg.rms_eps, glu=glu, use_rope=use_rope)
+    assert rel(out, ref) < 1e-12
+
+
+def test_no_rope_is_position_free(orc):
+    """use_rope=0: a single-sequence prefill does not depend on the position ids."""
+    cfg, w, _ = _small_block(orc, lossless=False, seed=13, use_rope=False)
+    x = np.random.default_rng(14).standard_normal((5, cfg.h))
+    o1, k1, _ = orc.block_prefill(cfg, w, x, np.arange(5), [0, 5])
+    o2, k2, _ = orc.block_prefill(cfg, w, x, np.arange(5) + 100, [0, 5])
+    np.testing.assert_array_equal(o1, o2)
+    np.testing.assert_array_equal(k1, k2)
+
+
+def test_block_params_non_glu(orc):
+    """Non-GLU MLP carries no gate factors: sum of k (m + n) over the six remaining matrices."""
+    cfg, _, _ = _small_block(orc, lossless=False, seed=15, glu=False)
+    h, m, d = cfg.h, cfg.m, cfg.head_dim
+    hkv = cfg.n_kv_heads * d
+    fp = lambda mo, ni, k: k * (mo + ni)
+    expect = (fp(h, h, cfg.r_q) + fp(hkv, h, cfg.r_k) + fp(hkv, h, cfg.r_v) + fp(h, h, cfg.r_o)
+              + fp(m, h, cfg.r_up) + fp(h, m, cfg.r_down))
+    assert orc.block_params(cfg) == expect
+
+
+@pytest.mark.parametrize("hkv,glu,use_rope", VARIANTS)
+def test_variant_decode_equals_recompute(orc, hkv, glu, use_rope):
+    cfg, w, _ = _small_block(orc, lossless=False, seed=16, n_kv_heads=hkv, glu=glu, use_rope=use_rope)
+    r = np.random.default_rng(17)
+    lens = [3, 6]
+    hk = cfg.n_kv_heads * cfg.head_dim
+    ck, cv = np.zeros((2, 8, hk)), np.zeros((2, 8, hk))
+    xs, ref = [], []
+    for b, L in enumerate(lens):
+        x = r.standard_normal((L + 1, cfg.h))
+        out, kk, vv = orc.block_prefill(cfg, w, x, np.arange(L + 1), [0, L + 1])
+        ck[b, :L], cv[b, :L] = kk[:L], vv[:L]
+        xs.append(x[L])
+        ref.append(out[L])
+    o, _, _ = orc.block_decode(cfg, w, np.stack(xs), ck, cv, lens)
+    assert rel(o, np.stack(ref)) < 1e-12
 
 
 @pytest.mark.parametrize("world,align", [(2, 1), (4, 1), (4, 8), (8, 1)])
