@@ -154,6 +154,8 @@ dl_status dl_tp_shard_factors(int n_seg, const void *const *A,
  *     q,k <- RoPE(positions);  append k,v to the cache
  *     x += A_o(B_o causal_gqa_attention(q, K, V))
  *     b = rmsnorm(x, mlp_norm); x += A_down(B_down(silu(A_g(B_g b)) * A_u(B_u b)))
+ * (variants via cfg->mlp_act / cfg->no_rope below; any n_heads : n_kv_heads
+ * ratio -- MHA, GQA, MQA).
  * Rank sharding (comm != NULL, world P): each group's factors are the
  * rank's dl_tp_shard_factors shard; the block issues five collectives per
  * call on `stream`: reduce-scatter of the q|k|v partials by head, all-gather
@@ -167,7 +169,17 @@ typedef struct {
   float rope_theta, rms_eps;
   int64_t max_tokens; /* upper bound on T per call (workspace sizing)       */
   int64_t max_seqs;   /* upper bound on num_seqs per call                   */
+  /* Model-family variants (Table 2 evaluates LLaMA-2/3
+   * and OPT; "NonGLU uses ReLU").  Zero-initialised = LLaMA.   */
+  int32_t mlp_act;    /* DL_MLP_SILU_GLU: x += A_down(B_down(silu(g) * u));
+                         DL_MLP_RELU: x += A_down(B_down(relu(u))), no gate:
+                         rank_gate must be 0 and the gu group holds the up
+                         segment alone in seg[0]                            */
+  int32_t no_rope;    /* 1: q, k are not rotated (positions still place the
+                         cache entries)                                     */
 } dl_block_config;
+
+enum { DL_MLP_SILU_GLU = 0, DL_MLP_RELU = 1 };
 
 typedef struct {
   const void *A;  /* [m_seg x k] bf16, this rank's columns (NULL if k==0) */
@@ -185,7 +197,8 @@ typedef struct {
   const void *attn_norm, *mlp_norm; /* gamma, [h] bf16                     */
   dl_factor_group qkv;  /* segments q (m=h), k (m=h_kv), v (m=h_kv); n = h */
   dl_factor_group o;    /* segment o (m=h); n = h                          */
-  dl_factor_group gu;   /* segments gate (m), up (m); n = h                */
+  dl_factor_group gu;   /* segments gate (m), up (m); n = h (DL_MLP_RELU:
+                           seg[0] = up only)                               */
   dl_factor_group down; /* segment down (m=h); n = m                       */
 } dl_block_weights;
 

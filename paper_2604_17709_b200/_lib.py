@@ -43,7 +43,9 @@ class dl_block_config(ctypes.Structure):
     _fields_ = [(n, I64) for n in ("h", "n_heads", "n_kv_heads", "head_dim", "m", "rank_q", "rank_k", "rank_v",
                                    "rank_o", "rank_gate", "rank_up", "rank_down")] + \
                [("rope_theta", ctypes.c_float), ("rms_eps", ctypes.c_float), ("max_tokens", I64),
-                ("max_seqs", I64)]
+                ("max_seqs", I64), ("mlp_act", I32), ("no_rope", I32)]
+
+DL_MLP_SILU_GLU, DL_MLP_RELU = 0, 1
 
 
 class dl_segment(ctypes.Structure):
@@ -243,7 +245,9 @@ def dl_tp_shard_factors(As, Bs, world: int, rank: int, strict: bool = False, str
 def make_block_config(shape, ranks: dict, max_tokens: int, max_seqs: int) -> dl_block_config:
     return dl_block_config(shape.h, shape.n_heads, shape.n_kv_heads, shape.head_dim, shape.m, ranks["q"],
                            ranks["k"], ranks["v"], ranks["o"], ranks["gate"], ranks["up"], ranks["down"],
-                           float(shape.rope_theta), float(shape.rms_eps), max_tokens, max_seqs)
+                           float(shape.rope_theta), float(shape.rms_eps), max_tokens, max_seqs,
+                           DL_MLP_SILU_GLU if getattr(shape, "glu", True) else DL_MLP_RELU,
+                           0 if getattr(shape, "rope", True) else 1)
 
 
 class BlockWeights:
@@ -259,6 +263,8 @@ class BlockWeights:
         self.c.mlp_norm = self.tensors["mlp_norm"].data_ptr()
         self.seg_lens = {}
         for gname, mats in self.GROUPS:
+            if gname == "gu" and "A_gate" not in w:
+                mats = ("up",)          # non-GLU MLP: the group holds up alone
             A_sh, B_sh, lens = dl_tp_shard_factors([w["A_" + m] for m in mats], [w["B_" + m] for m in mats],
                                                    world, rank, stream=stream)
             self.tensors["B_" + gname] = B_sh

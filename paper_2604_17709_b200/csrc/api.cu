@@ -428,6 +428,7 @@ struct BlockDims {
   int64_t Hq_loc, Hk_loc, W;       // local heads, RS slab width
   int64_t k_qkv, k_o, k_gu, k_down, kmax;
   int64_t nmax;                    // widest stage-2 output (features)
+  bool glu;                        // SiLU-GLU MLP (else ReLU on up alone)
 };
 
 dl_status block_dims(const dl_block_config* c, int world, BlockDims* d) {
@@ -452,11 +453,20 @@ dl_status block_dims(const dl_block_config* c, int world, BlockDims* d) {
               (long long)c->n_kv_heads, world);
     return DL_ERR_PARTITION;
   }
+  if (c->mlp_act != DL_MLP_SILU_GLU && c->mlp_act != DL_MLP_RELU) {
+    set_error("mlp_act %d unknown", c->mlp_act);
+    return DL_ERR_INVALID_ARG;
+  }
+  const bool glu = c->mlp_act == DL_MLP_SILU_GLU;
+  if (!glu && c->rank_gate != 0) {
+    set_error("DL_MLP_RELU has no gate: rank_gate must be 0");
+    return DL_ERR_RANK;
+  }
   const int64_t hkv = c->n_kv_heads * c->head_dim;
   const int64_t ranks[7] = {c->rank_q, c->rank_k, c->rank_v, c->rank_o, c->rank_gate, c->rank_up, c->rank_down};
   const int64_t mins[7] = {c->h, hkv, hkv, c->h, std::min(c->h, c->m), std::min(c->h, c->m), std::min(c->h, c->m)};
   for (int i = 0; i < 7; ++i)
-    if (ranks[i] < 1 || ranks[i] > mins[i]) {
+    if (!(i == 4 && !glu) && (ranks[i] < 1 || ranks[i] > mins[i])) {
       set_error("rank %d = %lld outside [1, %lld]", i, (long long)ranks[i], (long long)mins[i]);
       return DL_ERR_RANK;
     }
@@ -476,7 +486,8 @@ dl_status block_dims(const dl_block_config* c, int world, BlockDims* d) {
   d->k_down = cdiv(c->rank_down, world);
   // Z columns: every segment starts on a 64-column (one K block) boundary
   d->kmax = std::max(std::max(d->k_qkv, d->k_o), std::max(d->k_gu, d->k_down)) + 3 * 64;
-  d->nmax = std::max(c->h + 2 * hkv, 2 * c->m);
+  d->nmax = std::max(c->h + 2 * hkv, (glu ? 2 : 1) * c->m);
+  d->glu = glu;
   return DL_OK;
 }
 
@@ -718,7 +729,8 @@ dl_status dl_decomposed_block_forward(const dl_block_config* cfg, const dl_block
   int64_t kq, ko, kg, kd;
   DL_TRY(check_group(w->qkv, 3, d.h, "qkv", &kq));
   DL_TRY(check_group(w->o, 1, d.h, "o", &ko));
-  DL_TRY(check_group(w->gu, 2, d.h, "gate|up", &kg));
+  const int n_gu = d.glu ? 2 : 1;
+  DL_TRY(check_group(w->gu, n_gu, d.h, d.glu ? "gate|up" : "up", &kg));
   DL_TRY(check_group(w->down, 1, d.m, "down", &kd));
   if (kq > d.k_qkv || ko > d.k_o || kg > d.k_gu || kd > d.k_down) {
     set_error("group shard larger than the balanced split allows");
@@ -793,6 +805,7 @@ dl_status dl_decomposed_block_forward(const dl_block_config* cfg, const dl_block
   rc.Hk = static_cast<int>(d.Hk_loc);
   rc.d = static_cast<int>(d.d);
   rc.theta = cfg->rope_theta;
+  rc.rope = cfg->no_rope ? 0 : 1;
 
   DL_TRY(launch_rmsnorm(x, static_cast<const __nv_bfloat16*>(w->attn_norm), ws.xn, T, d.h, cfg->rms_eps, st));
   if (fx) {
@@ -867,19 +880,23 @@ dl_status dl_decomposed_block_forward(const dl_block_config* cfg, const dl_block
   DL_TRY(run_group(w->o, 1, h_rows, att_in, d.h, d.h, T, skinny, ws, resid_out(), st, &fres));
   if (!fx) DL_TRY(finish_residual(d.h));
 
-  // ---- MLP: gate|up group, SiLU(gate)*up, down + residual ----------------------
+  // ---- MLP: gate|up group, SiLU(gate)*up (or ReLU(up)), down + residual ---------
   DL_TRY(launch_rmsnorm(x, static_cast<const __nv_bfloat16*>(w->mlp_norm), ws.xn, T, d.h, cfg->rms_eps, st));
-  GemmOut gu_out = skinny ? out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0) : out_plain(ws.yb, 2 * d.m, OUT_BF16, 0);
-  const GemmFixup fsilu = fixup(fx ? FIX_SILU : FIX_NONE);
-  DL_TRY(run_group(w->gu, 2, gu_rows, ws.xn, d.h, d.h, T, skinny, ws, gu_out, st, &fsilu));
-  if (fx) {
+  const int64_t ngu = n_gu * d.m;
+  GemmOut gu_out = skinny ? out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0) : out_plain(ws.yb, ngu, OUT_BF16, 0);
+  const bool fx_gu = fx && d.glu;
+  const GemmFixup fsilu = fixup(fx_gu ? FIX_SILU : FIX_NONE);
+  DL_TRY(run_group(w->gu, n_gu, gu_rows, ws.xn, d.h, d.h, T, skinny, ws, gu_out, st, &fsilu));
+  if (fx_gu) {
     // SiLU(gate)*up done by the gate|up stage-2 fixup
   } else if (!tp && skinny) {
-    DL_TRY(launch_silu_mul_f32(ws.yf, ws.ldy32, ws.act, d.m, T, d.m, 1, st));
+    if (d.glu) DL_TRY(launch_silu_mul_f32(ws.yf, ws.ldy32, ws.act, d.m, T, d.m, 1, st));
+    else DL_TRY(launch_relu_f32(ws.yf, ws.ldy32, ws.act, d.m, T, d.m, 1, st));
   } else {
-    if (skinny) DL_TRY(launch_f32_to_bf16(ws.yf, ws.ldy32, ws.yb, 2 * d.m, T, 2 * d.m, 1, st));
-    if (tp) DL_TRY(all_reduce(comm, ws.yb, static_cast<size_t>(T) * 2 * d.m, kNcclBfloat16, st));
-    DL_TRY(launch_silu_mul_bf16(ws.yb, 2 * d.m, ws.act, d.m, T, d.m, st));
+    if (skinny) DL_TRY(launch_f32_to_bf16(ws.yf, ws.ldy32, ws.yb, ngu, T, ngu, 1, st));
+    if (tp) DL_TRY(all_reduce(comm, ws.yb, static_cast<size_t>(T) * ngu, kNcclBfloat16, st));
+    if (d.glu) DL_TRY(launch_silu_mul_bf16(ws.yb, ngu, ws.act, d.m, T, d.m, st));
+    else DL_TRY(launch_relu_bf16(ws.yb, ngu, ws.act, d.m, T, d.m, st));
   }
   DL_TRY(run_group(w->down, 1, h_rows, ws.act, d.m, d.m, T, skinny, ws, resid_out(), st, &fres));
   if (!fx) DL_TRY(finish_residual(d.h));

@@ -12,9 +12,10 @@
 // prefill: FlashAttention-2 layout.  CTA = 64 queries x 1 head; warp w owns
 //   query rows [16w, 16w+16); K/V tiles of 64 keys double-buffered; only the
 //   key tiles at or below the diagonal are visited.
-// decode:  one CTA per (sequence, kv head, key split).  The G = Hq/Hk query
-//   heads sharing the kv head are the MMA rows (G <= 16), so every K/V byte
-//   is read from HBM once for the whole group; the 4 warps split each 64-key
+// decode:  one CTA per (sequence, kv head x head chunk, key split).  The
+//   G = Hq/Hk query heads sharing the kv head are the MMA rows, 16 per chunk
+//   (MHA: G = 1; LLaMA-3 GQA: G = 8; MQA with G > 16 takes ceil(G/16)
+//   chunks), so every K/V byte is read from HBM once per 16 query heads; the 4 warps split each 64-key
 //   tile 4 ways and are merged (log-sum-exp) through shared memory; key
 //   splits (for small batch x heads) are merged by a second tiny kernel.
 #include <math.h>
@@ -250,17 +251,21 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, int splits
   extern __shared__ __align__(1024) uint8_t sm[];
   pdl_trigger();   // successor may launch now; it waits for us before reading
   pdl_wait();
-  const int s = blockIdx.z, kvh = blockIdx.y, sp = blockIdx.x;
+  const int s = blockIdx.z, sp = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t4 = lane & 3;
-  const int G = a.Hq / a.Hk;
+  const int Gall = a.Hq / a.Hk;
+  const int nch = (Gall + 15) >> 4;                  // 16-head chunks per kv head
+  const int kvh = blockIdx.y / nch, ch = blockIdx.y - kvh * nch;
+  const int h0 = kvh * Gall + ch * 16;               // first query head of this CTA
+  const int G = min(16, Gall - ch * 16);
   const int64_t n_keys = static_cast<int64_t>(a.cache_lens[s]) + 1;
   int64_t chunk_keys = (n_keys + splits - 1) / splits;
   chunk_keys = (chunk_keys + KT - 1) / KT * KT;
   const int64_t k_begin = sp * chunk_keys;
   const int64_t k_end = min64(n_keys, k_begin + chunk_keys);
   const int64_t ldq = static_cast<int64_t>(a.Hq) * D;
-  const __nv_bfloat16* Qg = a.q + static_cast<int64_t>(s) * ldq + static_cast<int64_t>(kvh) * G * D;
+  const __nv_bfloat16* Qg = a.q + static_cast<int64_t>(s) * ldq + static_cast<int64_t>(h0) * D;
   const int64_t kvoff = (static_cast<int64_t>(s) * a.Hk + kvh) * a.max_seq * D;
   const __nv_bfloat16* Kg = a.k_cache + kvoff;
   const __nv_bfloat16* Vg = a.v_cache + kvoff;
@@ -407,7 +412,7 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, int splits
       L += redm[64 + w * 16 + r] * exp2f(redm[w * 16 + r] - Br);
       o += red[(w * 16 + r) * D + tid];
     }
-    const int h = kvh * G + r;
+    const int h = h0 + r;
     if (splits == 1) {
       a.out[static_cast<int64_t>(s) * ldq + static_cast<int64_t>(h) * D + tid] = __float2bfloat16_rn(o / L);
     } else {
@@ -449,8 +454,8 @@ size_t attention_workspace(int64_t max_tokens, int Hq, int d) {
 
 dl_status launch_attention(const AttnArgs& a, cudaStream_t st) {
   if (a.T <= 0) return DL_OK;
-  if (a.d != D || a.Hq % a.Hk != 0 || a.Hq / a.Hk > 16) {
-    set_error("attention: head_dim %d / group %d unsupported (d = 128, Hq/Hk <= 16)", a.d, a.Hq / a.Hk);
+  if (a.d != D || a.Hk < 1 || a.Hq % a.Hk != 0) {
+    set_error("attention: head_dim %d / heads %d:%d unsupported (d = 128, Hq %% Hk == 0)", a.d, a.Hq, a.Hk);
     return DL_ERR_UNSUPPORTED;
   }
   if (!a.decode) {
@@ -473,11 +478,12 @@ dl_status launch_attention(const AttnArgs& a, cudaStream_t st) {
     attr = true;
   }
   // enough CTAs to cover the SMs twice; each split keeps >= 2 key tiles
-  const int64_t base = static_cast<int64_t>(a.num_seqs) * a.Hk;
+  const int nch = (a.Hq / a.Hk + 15) / 16;
+  const int64_t base = static_cast<int64_t>(a.num_seqs) * a.Hk * nch;
   int splits = 1;
   while (splits < kMaxSplits && base * splits < 2 * num_sms()) splits *= 2;
   if (a.partial == nullptr || a.partial_bytes < attention_workspace(a.T, a.Hq, a.d)) splits = 1;
-  dim3 grid(splits, a.Hk, a.num_seqs);
+  dim3 grid(splits, a.Hk * nch, a.num_seqs);
   dl_status s = launch_pdl(attn_decode_kernel, grid, dim3(128), SMEM, st, "attention decode", a, splits);
   if (s != DL_OK || splits == 1) return s;
   return launch_pdl(attn_combine_kernel, dim3(a.Hq, a.num_seqs), dim3(128), 0, st, "attention combine", a, splits);

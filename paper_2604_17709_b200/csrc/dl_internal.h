@@ -62,6 +62,7 @@ struct RopeCacheArgs {
   const int32_t* positions; const int32_t* cu_seqlens; const int32_t* cache_lens;
   int32_t num_seqs; int decode;
   int64_t T; int Hq, Hk, d; float theta;
+  int rope;            // 0: no rotary embedding (q, k pass through)
 };
 
 // Last-contributor finalize of a stream-K GEMM (FixupOp); buffers zeroed on entry,
@@ -168,6 +169,11 @@ dl_status launch_silu_mul_f32(float* acc, int64_t ld_acc, __nv_bfloat16* act,
 dl_status launch_silu_mul_bf16(const __nv_bfloat16* src, int64_t ld_src,
                                __nv_bfloat16* act, int64_t ld_act, int64_t T,
                                int64_t m, cudaStream_t st);
+// act[t][i] = bf16(relu(u)), u = src[t][i] (non-GLU MLP)
+dl_status launch_relu_f32(float* acc, int64_t ld_acc, __nv_bfloat16* act, int64_t ld_act, int64_t T,
+                          int64_t m, int clear, cudaStream_t st);
+dl_status launch_relu_bf16(const __nv_bfloat16* src, int64_t ld_src, __nv_bfloat16* act, int64_t ld_act,
+                           int64_t T, int64_t m, cudaStream_t st);
 // RoPE + cache append as a standalone kernel (see RopeCacheArgs)
 dl_status launch_rope_cache(const RopeCacheArgs& a, cudaStream_t st);
 dl_status launch_embedding(const __nv_bfloat16* table, int64_t vocab, int64_t h,

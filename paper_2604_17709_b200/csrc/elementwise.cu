@@ -143,6 +143,22 @@ struct SiluMulBf16 {
   }
 };
 
+// Non-GLU MLP activation (OPT family): act = bf16(relu(up)).
+struct ReluF32 {
+  float* acc; int64_t lda; __nv_bfloat16* out; int64_t ldo; int clear;
+  __device__ void operator()(int64_t t, int c) const {
+    float4 u = take4(acc + t * lda + c, clear);
+    store4(out + t * ldo + c, fmaxf(u.x, 0.f), fmaxf(u.y, 0.f), fmaxf(u.z, 0.f), fmaxf(u.w, 0.f));
+  }
+};
+struct ReluBf16 {
+  const __nv_bfloat16* src; int64_t lds; __nv_bfloat16* out; int64_t ldo;
+  __device__ void operator()(int64_t t, int c) const {
+    float4 u = load4(src + t * lds + c);
+    store4(out + t * ldo + c, fmaxf(u.x, 0.f), fmaxf(u.y, 0.f), fmaxf(u.z, 0.f), fmaxf(u.w, 0.f));
+  }
+};
+
 // RoPE + cache append.  grid (ceil(heads*d/4 / 128), T); one thread per 4 dims
 // = two rotation pairs (2i, 2i+1) by pos * theta^(-2i/d).
 __global__ void __launch_bounds__(128) rope_cache_kernel(RopeCacheArgs a) {
@@ -162,7 +178,7 @@ __global__ void __launch_bounds__(128) rope_cache_kernel(RopeCacheArgs a) {
   } else {
     v = load4(a.src + t * a.ld_src + col);
   }
-  if (hd < a.Hq + a.Hk) {
+  if (a.rope && hd < a.Hq + a.Hk) {
     // angle = pos * theta^(-2i/d) in fp32 (relative error ~1e-7, i.e. <= 3e-4 rad at
     // position 2048, far below bf16 resolution); full-range-reduction sincosf
     const float pos = static_cast<float>(a.positions[t]);
@@ -247,6 +263,14 @@ dl_status launch_silu_mul_f32(float* acc, int64_t lda, __nv_bfloat16* act, int64
 dl_status launch_silu_mul_bf16(const __nv_bfloat16* src, int64_t lds, __nv_bfloat16* act, int64_t ldo, int64_t T,
                                int64_t m, cudaStream_t st) {
   return launch_ew4(T, m, SiluMulBf16{src, lds, act, ldo, m}, st, "silu_mul_bf16");
+}
+dl_status launch_relu_f32(float* acc, int64_t lda, __nv_bfloat16* act, int64_t ldo, int64_t T, int64_t m,
+                          int clear, cudaStream_t st) {
+  return launch_ew4(T, m, ReluF32{acc, lda, act, ldo, clear}, st, "relu_f32");
+}
+dl_status launch_relu_bf16(const __nv_bfloat16* src, int64_t lds, __nv_bfloat16* act, int64_t ldo, int64_t T,
+                           int64_t m, cudaStream_t st) {
+  return launch_ew4(T, m, ReluBf16{src, lds, act, ldo}, st, "relu_bf16");
 }
 dl_status launch_rope_cache(const RopeCacheArgs& a, cudaStream_t st) {
   if (a.T <= 0) return DL_OK;

@@ -265,7 +265,7 @@ __device__ __noinline__ void fixup_tile(const KArgs& a, const struct Job& j, int
         st4zero(pa[k]);
         const int q = base + k * 256, e = (q & 31) * 4, t = q >> 5;
         float4 o = v[k];
-        if (j.seg < 2) {   // rotate pairs (e, e+1), (e+2, e+3) by pos * theta^(-e/d)
+        if (r.rope && j.seg < 2) {   // rotate pairs (e, e+1), (e+2, e+3) by pos * theta^(-e/d)
           const float pos = static_cast<float>(r.positions[t]);
           float s0, c0, s1, c1;
           sincosf(pos * exp2f(-l2t * static_cast<float>(e) / r.d), &s0, &c0);

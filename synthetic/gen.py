@@ -19,7 +19,7 @@ import zlib
 
 import torch
 
-__all__ = ["ModelShape", "LLAMA3_8B", "LLAMA3_70B", "rank_for", "block_ranks",
+__all__ = ["ModelShape", "LLAMA3_8B", "LLAMA3_70B", "LLAMA2_7B", "OPT_6_7B", "rank_for", "block_ranks",
            "seed_for", "gen_factor_pair", "gen_block_weights", "gen_normal",
            "MATRICES", "matrix_dims"]
 
@@ -38,14 +38,24 @@ class ModelShape:
     vocab: int
     rope_theta: float = 500000.0
     rms_eps: float = 1e-5
+    glu: bool = True       # SiLU-GLU MLP (LLaMA); False = ReLU on up alone (OPT)
+    rope: bool = True      # rotary position embedding on q, k
 
     @property
     def h_kv(self) -> int:
         return self.n_kv_heads * self.head_dim
 
+    @property
+    def matrices(self):
+        return MATRICES if self.glu else tuple(nm for nm in MATRICES if nm != "gate")
+
 
 LLAMA3_8B = ModelShape("llama3-8b", 4096, 32, 8, 128, 14336, 32, 128256)
 LLAMA3_70B = ModelShape("llama3-70b", 8192, 64, 8, 128, 28672, 80, 128256)
+# Table 2 families at their published layer shapes; OPT modelled as
+# its MLP (non-GLU ReLU) and position handling (no RoPE) -- reading c16.
+LLAMA2_7B = ModelShape("llama2-7b", 4096, 32, 32, 128, 11008, 32, 32000, rope_theta=10000.0)
+OPT_6_7B = ModelShape("opt-6.7b", 4096, 32, 32, 128, 16384, 32, 50272, glu=False, rope=False)
 
 MATRICES = ("q", "k", "v", "o", "gate", "up", "down")
 
@@ -67,7 +77,10 @@ def rank_for(ratio: float, m: int, n: int) -> int:
 
 
 def block_ranks(s: ModelShape, ratio: float) -> dict:
-    return {nm: rank_for(ratio, *matrix_dims(s, nm)) for nm in MATRICES}
+    """Retained rank per matrix; a non-GLU shape has no gate (rank 0)."""
+    r = {nm: rank_for(ratio, *matrix_dims(s, nm)) for nm in s.matrices}
+    r.setdefault("gate", 0)
+    return r
 
 
 def seed_for(config_id: int, layer: int, name: str) -> int:
@@ -94,7 +107,7 @@ def gen_block_weights(s: ModelShape, ranks: dict, config_id: int, layer: int,
                       device="cpu", dtype=torch.bfloat16) -> dict:
     """Per-matrix factors A_<name>, B_<name> plus the two RMSNorm gains."""
     w = {}
-    for nm in MATRICES:
+    for nm in s.matrices:
         mo, ni = matrix_dims(s, nm)
         A, B = gen_factor_pair(mo, ni, ranks[nm], seed_for(config_id, layer, nm), device, dtype)
         w["A_" + nm] = A

@@ -121,3 +121,29 @@ def test_block_workspace_and_validation(lib):
     with pytest.raises(lib.DLError) as e:
         lib.dl_block_workspace(bad, 1)
     assert e.value.name == "DL_ERR_RANK"
+
+
+def test_block_variant_validation(lib):
+    """mlp_act / no_rope fields (appended to dl_block_config): ReLU MLP must carry no gate."""
+    import dataclasses
+    from synthetic import OPT_6_7B, LLAMA2_7B, block_ranks
+    rk = block_ranks(OPT_6_7B, 0.4)
+    assert rk["gate"] == 0
+    cfg = lib.make_block_config(OPT_6_7B, rk, max_tokens=64, max_seqs=64)
+    assert cfg.mlp_act == lib.DL_MLP_RELU and cfg.no_rope == 1
+    assert lib.dl_block_workspace(cfg, 1) > 0
+    with pytest.raises(lib.DLError) as e:
+        lib.dl_block_workspace(lib.make_block_config(OPT_6_7B, dict(rk, gate=100), 64, 64), 1)
+    assert e.value.name == "DL_ERR_RANK"
+    cfg.mlp_act = 7
+    with pytest.raises(lib.DLError) as e:
+        lib.dl_block_workspace(cfg, 1)
+    assert e.value.name == "DL_ERR_INVALID_ARG"
+    mha = lib.make_block_config(LLAMA2_7B, block_ranks(LLAMA2_7B, 0.2), 64, 64)
+    assert mha.mlp_act == lib.DL_MLP_SILU_GLU and mha.no_rope == 0
+    for world in (1, 2, 4, 8, 32):
+        assert lib.dl_block_workspace(mha, world) > 0
+    glu_as_relu = lib.make_block_config(dataclasses.replace(LLAMA2_7B, glu=False), block_ranks(LLAMA2_7B, 0.2),
+                                        64, 64)
+    with pytest.raises(lib.DLError):
+        lib.dl_block_workspace(glu_as_relu, 1)      # LLaMA ranks include a gate

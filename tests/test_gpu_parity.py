@@ -109,7 +109,8 @@ SMALL = ModelShape("small", h=512, n_heads=4, n_kv_heads=2, head_dim=128, m=1024
 
 def _oracle_cfg(orc, s, rk):
     return orc.BlockCfg(s.h, s.n_heads, s.n_kv_heads, s.head_dim, s.m, rk["q"], rk["k"], rk["v"], rk["o"],
-                        rk["gate"], rk["up"], rk["down"], rope_theta=s.rope_theta, rms_eps=s.rms_eps)
+                        rk["gate"], rk["up"], rk["down"], rope_theta=s.rope_theta, rms_eps=s.rms_eps,
+                        mlp_glu=int(s.glu), use_rope=int(s.rope))
 
 
 def _cache_to_oracle(c, S, L):
@@ -234,3 +235,52 @@ def test_block_8b_decode_b64_sampled(dl, orc):
                                  _cache_to_oracle(vc[pick], 4, L + 1), [L] * 4)
     got = xd.cpu()[pick].double() - x[pick].double()
     assert rel(got, ref - x[pick].double().numpy()) <= TOL_BF16
+
+
+# ---- model-family variants (N4: Table 2) -------------------------------------
+VARIANT_SHAPES = {
+    "mha": ModelShape("mha", h=512, n_heads=4, n_kv_heads=4, head_dim=128, m=1024, n_layers=1, vocab=1000,
+                      rope_theta=10000.0),
+    "mqa32": ModelShape("mqa32", h=4096, n_heads=32, n_kv_heads=1, head_dim=128, m=1024, n_layers=1,
+                        vocab=1000),
+    "opt": ModelShape("opt", h=512, n_heads=4, n_kv_heads=4, head_dim=128, m=2048, n_layers=1, vocab=1000,
+                      glu=False, rope=False),
+    "gqa_relu": ModelShape("gqa_relu", h=1024, n_heads=8, n_kv_heads=2, head_dim=128, m=1024, n_layers=1,
+                           vocab=1000, glu=False),
+}
+
+
+@pytest.mark.parametrize("name", sorted(VARIANT_SHAPES))
+@pytest.mark.parametrize("lens", [[70], [300, 45]])
+def test_variant_block_prefill(dl, orc, name, lens):
+    s = VARIANT_SHAPES[name]
+    w, rk, x, xo, pos, cu, kc, vc = _run_prefill(dl, orc, s, 0.4, lens, seed=31 + len(lens))
+    ref, rk_, _ = orc.block_prefill(_oracle_cfg(orc, s, rk), w, x, pos, cu)
+    assert rel(xo.double() - x.double(), ref - x.double().numpy()) <= TOL_BF16
+    kg = kc[0, :, :lens[0]].permute(1, 0, 2).reshape(lens[0], -1).cpu()
+    assert rel(kg, rk_[:lens[0]]) <= TOL_BF16
+
+
+@pytest.mark.parametrize("name", sorted(VARIANT_SHAPES))
+@pytest.mark.parametrize("S", [5, 40])
+def test_variant_block_decode(dl, orc, name, S):
+    s = VARIANT_SHAPES[name]
+    rk = block_ranks(s, 0.4)
+    w = gen_block_weights(s, rk, 0, 41)
+    cache_lens = [(17 * i + 3) % 150 for i in range(S)]
+    max_seq = max(cache_lens) + 1
+    x = gen_normal((S, s.h), 1.0, 42, dtype=torch.bfloat16)
+    kc = gen_normal((S, s.n_kv_heads, max_seq, s.head_dim), 1.0, 43, dtype=torch.bfloat16)
+    vc = gen_normal((S, s.n_kv_heads, max_seq, s.head_dim), 1.0, 44, dtype=torch.bfloat16)
+    cl = torch.tensor(cache_lens, dtype=torch.int32)
+    cfg = dl.make_block_config(s, rk, max_tokens=S, max_seqs=S)
+    wdev = dl.BlockWeights({k: v.cuda() for k, v in w.items()})
+    ws = torch.zeros(dl.dl_block_workspace(cfg), dtype=torch.uint8, device="cuda")
+    xd, kcd, vcd = x.cuda(), kc.cuda(), vc.cuda()
+    dl.dl_decomposed_block_forward(cfg, wdev, xd, cl.cuda(), None, S, dl.DL_DECODE, kcd, vcd, cl.cuda(), None, ws)
+    torch.cuda.synchronize()
+    ref, kn, _ = orc.block_decode(_oracle_cfg(orc, s, rk), w, x, _cache_to_oracle(kc, S, max_seq),
+                                  _cache_to_oracle(vc, S, max_seq), cache_lens)
+    assert rel(xd.cpu().double() - x.double(), ref - x.double().numpy()) <= TOL_BF16
+    kg = torch.stack([kcd[b, :, cache_lens[b]].reshape(-1) for b in range(S)]).cpu()
+    assert rel(kg, kn) <= TOL_BF16
