@@ -348,6 +348,12 @@ typedef struct {
   /* Table 2 variants: mlp_glu 1 = SiLU(gate)*up (LLaMA), 0 = ReLU(up)
      (OPT family, "NonGLU uses ReLU"); use_rope 0 = no rotary embedding */
   int64_t mlp_glu, use_rope;
+  /* layout of the rank sharding when world > 1:
+     0 = rank-parallel (north star: every factor pair split along k, one
+         reduce-sum per pair, Fig. 2(b));
+     1 = DeInfer low-rank communication (Fig. 3): see
+         deinfer_first / deinfer_second below.  Both equal world == 1.     */
+  int64_t layout;
 } oracle_block_cfg;
 
 typedef struct {
@@ -365,6 +371,121 @@ static int lr(const double *X, const double *A, const double *B, double *Y,
 
 static double silu(double g) { return g / (1.0 + exp(-g)); }
 
+/* DeInfer first sub-layer, P:176 (Fig. 3): "all downward projection matrices
+ * x_v in the first sub-layer are in column-wise parallel (in a split manner,
+ * where all matrices are first concatenated and then evenly split), followed
+ * by an all-gather operation in the low-rank latent space ... The upward
+ * projection matrices x_u are also in column-parallel (but in a shard way,
+ * where each process has a shard of the same matrices) ... a batched matrix
+ * multiplication for the low-rank results with different upward matrix
+ * shards".  Segment s: A[s] [m[s] x l[s]], B[s] [l[s] x n]; Y[s] [T x m[s]].
+ *   1. B_cat = [B[0]; B[1]; ...]  (L = sum l rows), rank r holds the rows of
+ *      its balanced share of [0, L) (reading c3);
+ *   2. rank r: Z_r = X B_cat[rows_r]^T                     [T x len_r];
+ *   3. all-gather: Z = [Z_0 | Z_1 | ...]                    [T x L];
+ *   4. rank r, segment s: output rows rows_r(m[s]) (its balanced share of
+ *      A[s]'s rows): Y[s][t][i] = sum_j A[s][i][j] Z[t][off_s + j].        */
+static int deinfer_first(const double *X, int64_t T, int64_t n, int nseg,
+                         const double *const *A, const double *const *B,
+                         const int64_t *m, const int64_t *l, int world,
+                         double *const *Y) {
+  int64_t L = 0, off[3];
+  for (int s = 0; s < nseg; ++s) { off[s] = L; L += l[s]; }
+  double *Bc = (double *)malloc(sizeof(double) * (size_t)(L * n + 1));
+  double *Z = (double *)malloc(sizeof(double) * (size_t)(T * L + 1));
+  if (!Bc || !Z) { free(Bc); free(Z); return ORC_ENOMEM; }
+  for (int s = 0; s < nseg; ++s)                                   /* step 1 */
+    memcpy(Bc + off[s] * n, B[s], sizeof(double) * (size_t)(l[s] * n));
+  for (int r = 0; r < world; ++r) {
+    int64_t b0, len, lp;
+    int rc = oracle_shard_range(L, world, r, 1, &b0, &len, &lp);
+    if (rc) { free(Bc); free(Z); return rc; }
+    double *Zr = (double *)malloc(sizeof(double) * (size_t)(T * len + 1));
+    if (!Zr) { free(Bc); free(Z); return ORC_ENOMEM; }
+    for (int64_t t = 0; t < T; ++t)                                /* step 2 */
+      for (int64_t j = 0; j < len; ++j) {
+        double acc = 0.0;
+        for (int64_t c = 0; c < n; ++c) acc += Bc[(b0 + j) * n + c] * X[t * n + c];
+        Zr[t * len + j] = acc;
+      }
+    for (int64_t t = 0; t < T; ++t)                                /* step 3 */
+      for (int64_t j = 0; j < len; ++j) Z[t * L + b0 + j] = Zr[t * len + j];
+    free(Zr);
+  }
+  for (int r = 0; r < world; ++r)                                  /* step 4 */
+    for (int s = 0; s < nseg; ++s) {
+      int64_t i0, ni, np_;
+      int rc = oracle_shard_range(m[s], world, r, 1, &i0, &ni, &np_);
+      if (rc) { free(Bc); free(Z); return rc; }
+      for (int64_t t = 0; t < T; ++t)
+        for (int64_t i = i0; i < i0 + ni; ++i) {
+          double acc = 0.0;
+          for (int64_t j = 0; j < l[s]; ++j) acc += A[s][i * l[s] + j] * Z[t * L + off[s] + j];
+          Y[s][t * m[s] + i] = acc;
+        }
+    }
+  free(Bc); free(Z);
+  return ORC_OK;
+}
+
+/* DeInfer second sub-layer: "the downward projection matrix is in
+ * row-wise parallel, and upward projection matrix is identical in each
+ * process.  Therefore, after multiplying the downward matrix, each process
+ * needs to have a reduce-sum ... Since every process has identical low-rank
+ * data and identical upward matrix, the output would also be identical."
+ * A [m x l], B [l x n]; rank r holds the columns cols_r (balanced share of
+ * [0, n)) of B and sees only those features of X (its local heads / MLP
+ * slice):  Z = sum_r X[:, cols_r] B[:, cols_r]^T  (reduce-sum, [T x l]);
+ * Y = Z A^T on every rank.                                                 */
+static int deinfer_second(const double *X, int64_t T, int64_t n,
+                          const double *A, const double *B, int64_t m,
+                          int64_t l, int world, double *Y) {
+  double *Z = (double *)calloc((size_t)(T * l + 1), sizeof(double));
+  if (!Z) return ORC_ENOMEM;
+  for (int r = 0; r < world; ++r) {
+    int64_t c0, nc, np_;
+    int rc = oracle_shard_range(n, world, r, 1, &c0, &nc, &np_);
+    if (rc) { free(Z); return rc; }
+    for (int64_t t = 0; t < T; ++t)
+      for (int64_t j = 0; j < l; ++j) {
+        double acc = 0.0;                                  /* rank r's partial */
+        for (int64_t c = c0; c < c0 + nc; ++c) acc += B[j * n + c] * X[t * n + c];
+        Z[t * l + j] += acc;                               /* reduce-sum */
+      }
+  }
+  for (int64_t t = 0; t < T; ++t)
+    for (int64_t i = 0; i < m; ++i) {
+      double acc = 0.0;
+      for (int64_t j = 0; j < l; ++j) acc += A[i * l + j] * Z[t * l + j];
+      Y[t * m + i] = acc;
+    }
+  free(Z);
+  return ORC_OK;
+}
+
+static int use_deinfer(const oracle_block_cfg *c, int world) { return world > 1 && c->layout == 1; }
+
+/* q, k, v projections of the normed rows a [T x h] (q may be NULL). */
+static int project_qkv(const oracle_block_cfg *c, const oracle_block_w *w,
+                       const double *a, int64_t T, double *q, double *kk,
+                       double *vv, int world, int64_t align) {
+  int64_t h = c->h, hkv = c->n_kv_heads * c->head_dim;
+  if (use_deinfer(c, world)) {
+    const double *A[3] = {w->A_q, w->A_k, w->A_v}, *B[3] = {w->B_q, w->B_k, w->B_v};
+    int64_t m[3] = {h, hkv, hkv}, l[3] = {c->r_q, c->r_k, c->r_v};
+    double *qq = q ? q : (double *)malloc(sizeof(double) * (size_t)(T * h + 1));
+    double *Y[3] = {qq, kk, vv};
+    int rc = deinfer_first(a, T, h, 3, A, B, m, l, world, Y);
+    if (!q) free(qq);
+    return rc;
+  }
+  int rc = 0;
+  if (q) rc |= lr(a, w->A_q, w->B_q, q, T, h, h, c->r_q, world, align);
+  rc |= lr(a, w->A_k, w->B_k, kk, T, hkv, h, c->r_k, world, align);
+  rc |= lr(a, w->A_v, w->B_v, vv, T, hkv, h, c->r_v, world, align);
+  return rc;
+}
+
 /* MLP half + O projection are per-token; shared by prefill and decode. */
 static int block_tail(const oracle_block_cfg *c, const oracle_block_w *w,
                       const double *x_in, const double *att, double *x_out,
@@ -376,17 +497,28 @@ static int block_tail(const oracle_block_cfg *c, const oracle_block_w *w,
   double *up = (double *)malloc(sizeof(double) * (size_t)(T * m));
   double *dn = (double *)malloc(sizeof(double) * (size_t)(T * h));
   if (!o || !xn || !gt || !up || !dn) { free(o); free(xn); free(gt); free(up); free(dn); return ORC_ENOMEM; }
-  int rc = lr(att, w->A_o, w->B_o, o, T, h, h, c->r_o, world, align);
+  const int di = use_deinfer(c, world);
+  int rc = di ? deinfer_second(att, T, h, w->A_o, w->B_o, h, c->r_o, world, o)
+              : lr(att, w->A_o, w->B_o, o, T, h, h, c->r_o, world, align);
   for (int64_t i = 0; i < T * h; ++i) x_out[i] = x_in[i] + o[i];
   oracle_rmsnorm(x_out, w->g_mlp, c->rms_eps, xn, T, h);
-  rc |= lr(xn, w->A_up, w->B_up, up, T, m, h, c->r_up, world, align);
+  if (di) {   /* gate | up concatenated and split (first sub-layer) */
+    const double *A2[2] = {w->A_gate, w->A_up}, *B2[2] = {w->B_gate, w->B_up};
+    int64_t m2[2] = {m, m}, l2[2] = {c->r_gate, c->r_up};
+    double *Y2[2] = {gt, up};
+    int g0 = c->mlp_glu ? 0 : 1;
+    rc |= deinfer_first(xn, T, h, 2 - g0, A2 + g0, B2 + g0, m2 + g0, l2 + g0, world, Y2 + g0);
+  } else {
+    rc |= lr(xn, w->A_up, w->B_up, up, T, m, h, c->r_up, world, align);
+    if (c->mlp_glu) rc |= lr(xn, w->A_gate, w->B_gate, gt, T, m, h, c->r_gate, world, align);
+  }
   if (c->mlp_glu) {
-    rc |= lr(xn, w->A_gate, w->B_gate, gt, T, m, h, c->r_gate, world, align);
     for (int64_t i = 0; i < T * m; ++i) gt[i] = silu(gt[i]) * up[i];
   } else {
     for (int64_t i = 0; i < T * m; ++i) gt[i] = up[i] > 0.0 ? up[i] : 0.0;   /* ReLU */
   }
-  rc |= lr(gt, w->A_down, w->B_down, dn, T, h, m, c->r_down, world, align);
+  rc |= di ? deinfer_second(gt, T, m, w->A_down, w->B_down, h, c->r_down, world, dn)
+           : lr(gt, w->A_down, w->B_down, dn, T, h, m, c->r_down, world, align);
   for (int64_t i = 0; i < T * h; ++i) x_out[i] += dn[i];
   free(o); free(xn); free(gt); free(up); free(dn);
   return rc;
@@ -417,8 +549,7 @@ int oracle_block_prefill(const oracle_block_cfg *c, const oracle_block_w *w,
   if (!a || !kk || !vv || !xr || !ar || !qr || !att || !pr) return ORC_ENOMEM;
   int rc = 0;
   oracle_rmsnorm(x, w->g_attn, c->rms_eps, a, T, h);
-  rc |= lr(a, w->A_k, w->B_k, kk, T, hkv, h, c->r_k, world, align);
-  rc |= lr(a, w->A_v, w->B_v, vv, T, hkv, h, c->r_v, world, align);
+  rc |= project_qkv(c, w, a, T, NULL, kk, vv, world, align);
   if (c->use_rope) oracle_rope(kk, pos, T, Hkv, d, c->rope_theta);
   for (int64_t r = 0; r < n_rows; ++r) {
     int64_t t = rows ? rows[r] : r;
@@ -426,7 +557,14 @@ int oracle_block_prefill(const oracle_block_cfg *c, const oracle_block_w *w,
     memcpy(ar + r * h, a + t * h, sizeof(double) * (size_t)h);
     pr[r] = pos[t];
   }
-  rc |= lr(ar, w->A_q, w->B_q, qr, n_rows, h, h, c->r_q, world, align);
+  if (use_deinfer(c, world)) {   /* q rows from the same first sub-layer pass */
+    double *kq = (double *)malloc(sizeof(double) * (size_t)(n_rows * hkv + 1));
+    double *vq = (double *)malloc(sizeof(double) * (size_t)(n_rows * hkv + 1));
+    rc |= project_qkv(c, w, ar, n_rows, qr, kq, vq, world, align);
+    free(kq); free(vq);
+  } else {
+    rc |= lr(ar, w->A_q, w->B_q, qr, n_rows, h, h, c->r_q, world, align);
+  }
   if (c->use_rope) oracle_rope(qr, pr, n_rows, H, d, c->rope_theta);
   /* causal attention of each requested row over its own sequence prefix */
   for (int64_t r = 0; r < n_rows; ++r) {
@@ -470,9 +608,7 @@ int oracle_block_decode(const oracle_block_cfg *c, const oracle_block_w *w,
   if (!a || !q || !kk || !vv || !att) return ORC_ENOMEM;
   int rc = 0;
   oracle_rmsnorm(x, w->g_attn, c->rms_eps, a, Bn, h);
-  rc |= lr(a, w->A_q, w->B_q, q, Bn, h, h, c->r_q, world, align);
-  rc |= lr(a, w->A_k, w->B_k, kk, Bn, hkv, h, c->r_k, world, align);
-  rc |= lr(a, w->A_v, w->B_v, vv, Bn, hkv, h, c->r_v, world, align);
+  rc |= project_qkv(c, w, a, Bn, q, kk, vv, world, align);
   if (c->use_rope) {
     oracle_rope(q, cache_len, Bn, H, d, c->rope_theta);
     oracle_rope(kk, cache_len, Bn, Hkv, d, c->rope_theta);

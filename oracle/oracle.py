@@ -23,7 +23,7 @@ __all__ = [
     "build", "load", "matmul", "lowrank_linear", "shard_range",
     "lowrank_linear_sharded", "truncated_svd", "factor_params", "rmsnorm",
     "rope", "attention", "BlockCfg", "block_prefill", "block_decode",
-    "block_params", "census", "num_threads",
+    "block_params", "census", "num_threads", "LAYOUT_RANK_PARALLEL", "LAYOUT_DEINFER",
 ]
 
 
@@ -187,7 +187,9 @@ class _CCfg(ctypes.Structure):
                 ("h", "n_heads", "n_kv_heads", "head_dim", "m",
                  "r_q", "r_k", "r_v", "r_o", "r_gate", "r_up", "r_down")] + \
                [("rope_theta", ctypes.c_double), ("rms_eps", ctypes.c_double), ("mlp_glu", ctypes.c_int64),
-                ("use_rope", ctypes.c_int64)]
+                ("use_rope", ctypes.c_int64), ("layout", ctypes.c_int64)]
+
+LAYOUT_RANK_PARALLEL, LAYOUT_DEINFER = 0, 1
 
 
 _WNAMES = ("g_attn", "g_mlp", "A_q", "B_q", "A_k", "B_k", "A_v", "B_v", "A_o", "B_o",
@@ -202,7 +204,7 @@ class BlockCfg:
     """Plain record of block dimensions / ranks (names as in Table 1)."""
 
     def __init__(self, h, n_heads, n_kv_heads, head_dim, m, r_q, r_k, r_v, r_o,
-                 r_gate, r_up, r_down, rope_theta=500000.0, rms_eps=1e-5, mlp_glu=1, use_rope=1):
+                 r_gate, r_up, r_down, rope_theta=500000.0, rms_eps=1e-5, mlp_glu=1, use_rope=1, layout=0):
         self.__dict__.update(locals())
         del self.__dict__["self"]
 

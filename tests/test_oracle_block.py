@@ -156,7 +156,7 @@ def _dense_block_torch(x, W, g1, g2, pos, cu, H, Hkv, d, theta, eps, glu=True, u
     return (x + y @ torch.tensor(W["down"]).T).numpy()
 
 
-def _small_block(orc, lossless, seed=0, n_kv_heads=None, glu=True, use_rope=True):
+def _small_block(orc, lossless, seed=0, n_kv_heads=None, glu=True, use_rope=True, layout=0):
     r = np.random.default_rng(seed)
     s = dict(SMALL)
     if n_kv_heads is not None:
@@ -177,7 +177,7 @@ def _small_block(orc, lossless, seed=0, n_kv_heads=None, glu=True, use_rope=True
     w["g_mlp"] = 1 + 0.1 * r.standard_normal(h)
     cfg = orc.BlockCfg(h, s["n_heads"], s["n_kv_heads"], s["head_dim"], m, ranks["q"], ranks["k"], ranks["v"],
                        ranks["o"], ranks.get("gate", 0), ranks["up"], ranks["down"], rope_theta=10000.0,
-                       rms_eps=1e-5, mlp_glu=int(glu), use_rope=int(use_rope))
+                       rms_eps=1e-5, mlp_glu=int(glu), use_rope=int(use_rope), layout=layout)
     return cfg, w, W
 
 
@@ -256,6 +256,47 @@ def test_variant_decode_equals_recompute(orc, hkv, glu, use_rope):
         ref.append(out[L])
     o, _, _ = orc.block_decode(cfg, w, np.stack(xs), ck, cv, lens)
     assert rel(o, np.stack(ref)) < 1e-12
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+@pytest.mark.parametrize("glu", [True, False])
+def test_block_deinfer_layout_p_invariance(orc, world, glu):
+    """N1 (Fig. 3): the DeInfer rearrangement -- concat-split B with a
+    latent all-gather, row-sharded A, input-sharded B + latent reduce-sum with a
+    replicated A -- equals the unsharded block at every world size (uneven
+    splits included: ranks 0.6*min(m,n) are odd, m=48 / h=32 split 3 ways)."""
+    cfg, w, _ = _small_block(orc, lossless=False, seed=21, glu=glu, layout=orc.LAYOUT_DEINFER)
+    r = np.random.default_rng(22)
+    x = r.standard_normal((7, cfg.h))
+    cu = [0, 3, 7]
+    pos = np.array([0, 1, 2, 0, 1, 2, 3])
+    o1, k1, v1 = orc.block_prefill(cfg, w, x, pos, cu)
+    op, kp, vp = orc.block_prefill(cfg, w, x, pos, cu, world=world)
+    assert rel(op, o1) < 1e-12 and rel(kp, k1) < 1e-12 and rel(vp, v1) < 1e-12
+    part, _, _ = orc.block_prefill(cfg, w, x, pos, cu, rows=[6, 2], world=world)
+    assert rel(part, o1[[6, 2]]) < 1e-12
+
+
+def test_block_deinfer_lossless_equals_dense(orc):
+    cfg, w, W = _small_block(orc, lossless=True, seed=23, layout=orc.LAYOUT_DEINFER)
+    r = np.random.default_rng(24)
+    x = r.standard_normal((6, cfg.h))
+    pos = np.arange(6)
+    out, _, _ = orc.block_prefill(cfg, w, x, pos, [0, 6], world=4)
+    ref = _dense_block_torch(x, W, w["g_attn"], w["g_mlp"], pos, [0, 6], cfg.n_heads, cfg.n_kv_heads,
+                             cfg.head_dim, cfg.rope_theta, cfg.rms_eps)
+    assert rel(out, ref) < 1e-12
+
+
+def test_deinfer_decode_p_invariance(orc):
+    cfg, w, _ = _small_block(orc, lossless=False, seed=25, layout=orc.LAYOUT_DEINFER)
+    r = np.random.default_rng(26)
+    hk = cfg.n_kv_heads * cfg.head_dim
+    ck, cv = r.standard_normal((3, 6, hk)), r.standard_normal((3, 6, hk))
+    x = r.standard_normal((3, cfg.h))
+    o1, k1, _ = orc.block_decode(cfg, w, x, ck, cv, [0, 2, 5])
+    o2, k2, _ = orc.block_decode(cfg, w, x, ck, cv, [0, 2, 5], world=2)
+    assert rel(o2, o1) < 1e-12 and rel(k2, k1) < 1e-12
 
 
 @pytest.mark.parametrize("world,align", [(2, 1), (4, 1), (4, 8), (8, 1)])
