@@ -177,9 +177,48 @@ typedef struct {
                          segment alone in seg[0]                            */
   int32_t no_rope;    /* 1: q, k are not rotated (positions still place the
                          cache entries)                                     */
+  int32_t layout;     /* rank-sharding layout when comm != NULL (below)     */
 } dl_block_config;
 
 enum { DL_MLP_SILU_GLU = 0, DL_MLP_RELU = 1 };
+
+/* Sharding layouts (both compute the same block; they differ in what each
+ * rank stores and which collectives run, Table 1):
+ * DL_LAYOUT_RANK_PARALLEL (north star, Fig. 2(b)): every factor pair split
+ *   along k (dl_tp_shard_factors), partials reduced in the full space:
+ *   RS(q|k|v by head), AG(attention), AR(o), AR(gate|up), AR(down).
+ * DL_LAYOUT_DEINFER (Fig. 3, low-rank communication):
+ *   q|k|v and gate|up ("first sub-layer"): concatenated B split by rows as
+ *   above, then an all-gather of the LATENT Z [T x (l_q+l_k+l_v)], then the
+ *   rank's row shard of each A (its local heads / its m/P MLP features,
+ *   all l columns); o and down ("second sub-layer"): B split by input
+ *   columns (the rank's local features), a reduce-sum of the LATENT
+ *   partial [T x l], and the full A replicated on every rank.  Shards come
+ *   from dl_deinfer_shard_factors; the weights struct then holds
+ *   qkv/gu: B = concat-split rows, seg[s] = {A row shard, lda, k = l_s};
+ *   o/down: B = column shard [l x n/P] (ldb), seg[0] = {full A, lda, l}.
+ *   Requires m % (64 P) == 0 and h % (64 P) == 0.  Collectives per block:
+ *   AG(l_q+l_k+l_v), AR(l_o), AG(l_gate+l_up), AR(l_down).                 */
+enum { DL_LAYOUT_RANK_PARALLEL = 0, DL_LAYOUT_DEINFER = 1 };
+
+/* dl_deinfer_shard_factors: copy rank `rank`'s DeInfer shard of one factor
+ * group on `stream` (device memory, caller-allocated outputs).
+ * sublayer 1 (q|k|v or gate|up, n_seg <= 3): B_shard [k_loc x n] is the
+ *   rank's balanced share of the concatenated B rows (identical to
+ *   dl_tp_shard_factors' B_shard, k_loc from dl_tp_plan); A_shard[g]
+ *   [m[g]/world x r[g]] = rows [rank m[g]/world, (rank+1) m[g]/world) of
+ *   A[g].  m[g] % world != 0 -> DL_ERR_PARTITION.
+ * sublayer 2 (o or down, n_seg == 1): B_shard [r[0] x n/world] = columns
+ *   [rank n/world, (rank+1) n/world) of B[0]; A_shard[0] [m[0] x r[0]] =
+ *   a full copy of A[0].  n % world != 0 -> DL_ERR_PARTITION.
+ * Leading dimensions must be multiples of 8 (bf16) / 4 (fp32).            */
+dl_status dl_deinfer_shard_factors(int sublayer, int n_seg, const void *const *A,
+                                   const int64_t *lda, const void *const *B,
+                                   const int64_t *ldb, const int64_t *m,
+                                   const int64_t *r, int64_t n, dl_dtype dtype,
+                                   int world, int rank, void *B_shard,
+                                   int64_t ldb_shard, void *const *A_shard,
+                                   const int64_t *lda_shard, void *stream);
 
 typedef struct {
   const void *A;  /* [m_seg x k] bf16, this rank's columns (NULL if k==0) */

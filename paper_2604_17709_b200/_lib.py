@@ -23,7 +23,7 @@ EXPORTS = ("dl_last_error", "dl_version", "dl_device_ok", "dl_comm_create", "dl_
            "dl_lowrank_linear_workspace", "dl_lowrank_linear", "dl_tp_plan", "dl_tp_shard_factors",
            "dl_block_workspace", "dl_decomposed_block_forward", "dl_embedding", "dl_rmsnorm",
            "dl_dense_workspace", "dl_dense", "dl_launch_count", "dl_profile_begin", "dl_profile_end",
-           "dl_profile_count", "dl_profile_get", "dl_debug_gemm_trace")
+           "dl_profile_count", "dl_profile_get", "dl_debug_gemm_trace", "dl_deinfer_shard_factors")
 
 
 class DLError(RuntimeError):
@@ -43,9 +43,10 @@ class dl_block_config(ctypes.Structure):
     _fields_ = [(n, I64) for n in ("h", "n_heads", "n_kv_heads", "head_dim", "m", "rank_q", "rank_k", "rank_v",
                                    "rank_o", "rank_gate", "rank_up", "rank_down")] + \
                [("rope_theta", ctypes.c_float), ("rms_eps", ctypes.c_float), ("max_tokens", I64),
-                ("max_seqs", I64), ("mlp_act", I32), ("no_rope", I32)]
+                ("max_seqs", I64), ("mlp_act", I32), ("no_rope", I32), ("layout", I32)]
 
 DL_MLP_SILU_GLU, DL_MLP_RELU = 0, 1
+DL_LAYOUT_RANK_PARALLEL, DL_LAYOUT_DEINFER = 0, 1
 
 
 class dl_segment(ctypes.Structure):
@@ -95,6 +96,7 @@ def load():
             lib.dl_profile_begin.argtypes = [I]
             lib.dl_profile_get.argtypes = [I, P, P, P, P]
             lib.dl_debug_gemm_trace.argtypes = [P]
+            lib.dl_deinfer_shard_factors.argtypes = [I, I, P, P, P, P, P, P, I64, I, I, I, P, I64, P, P, P]
             for name in EXPORTS[3:]:
                 getattr(lib, name).restype = I
             lib.dl_launch_count.restype = ctypes.c_longlong
@@ -241,13 +243,46 @@ def dl_tp_shard_factors(As, Bs, world: int, rank: int, strict: bool = False, str
     return A_shards, B_shard, list(out_len)
 
 
+def dl_deinfer_shard_factors(sublayer: int, As, Bs, world: int, rank: int, stream=None):
+    """DeInfer shard of a factor group (Fig. 3).  sublayer 1 (q|k|v, gate|up):
+    B = the rank's concat-split rows, A_g = its output-row shard (all latent
+    columns); sublayer 2 (o, down): B = its input-column shard, A = full copy.
+    Returns (A_shards, B_shard)."""
+    ng = len(As)
+    dt = _dtype(As[0])
+    n = Bs[0].shape[1]
+    ranks = [a.shape[1] for a in As]
+    dev = As[0].device
+    if sublayer == 1:
+        _, _, kloc = dl_tp_plan(ranks, world, rank)
+        B_shard = torch.zeros((kloc, _pad8(n)), dtype=As[0].dtype, device=dev)[:, :n]
+        A_shards = [torch.zeros((a.shape[0] // world, _pad8(a.shape[1])), dtype=a.dtype, device=dev)[:, :a.shape[1]]
+                    for a in As]
+    else:
+        nl = n // world
+        B_shard = torch.zeros((ranks[0], _pad8(nl)), dtype=As[0].dtype, device=dev)[:, :nl]
+        A_shards = [torch.zeros((As[0].shape[0], _pad8(ranks[0])), dtype=As[0].dtype, device=dev)[:, :ranks[0]]]
+    arr = lambda vals, ty=I64: (ty * ng)(*vals)  # noqa: E731
+    a_p = (P * ng)(*[a.data_ptr() for a in As])
+    b_p = (P * ng)(*[b.data_ptr() for b in Bs])
+    as_p = (P * ng)(*[a.data_ptr() for a in A_shards])
+    _check(load().dl_deinfer_shard_factors(sublayer, ng, ctypes.cast(a_p, P), ctypes.cast(arr([_ld(a) for a in As]), P),
+                                           ctypes.cast(b_p, P), ctypes.cast(arr([_ld(b) for b in Bs]), P),
+                                           ctypes.cast(arr([a.shape[0] for a in As]), P), ctypes.cast(arr(ranks), P),
+                                           n, dt, world, rank, _ptr(B_shard), B_shard.stride(0),
+                                           ctypes.cast(as_p, P), ctypes.cast(arr([a.stride(0) for a in A_shards]), P),
+                                           _stream(stream)))
+    return A_shards, B_shard
+
+
 # ---------------------------------------------------------------------------
-def make_block_config(shape, ranks: dict, max_tokens: int, max_seqs: int) -> dl_block_config:
+def make_block_config(shape, ranks: dict, max_tokens: int, max_seqs: int,
+                      layout: int = DL_LAYOUT_RANK_PARALLEL) -> dl_block_config:
     return dl_block_config(shape.h, shape.n_heads, shape.n_kv_heads, shape.head_dim, shape.m, ranks["q"],
                            ranks["k"], ranks["v"], ranks["o"], ranks["gate"], ranks["up"], ranks["down"],
                            float(shape.rope_theta), float(shape.rms_eps), max_tokens, max_seqs,
                            DL_MLP_SILU_GLU if getattr(shape, "glu", True) else DL_MLP_RELU,
-                           0 if getattr(shape, "rope", True) else 1)
+                           0 if getattr(shape, "rope", True) else 1, layout)
 
 
 class BlockWeights:
@@ -256,7 +291,9 @@ class BlockWeights:
 
     GROUPS = (("qkv", ("q", "k", "v")), ("o", ("o",)), ("gu", ("gate", "up")), ("down", ("down",)))
 
-    def __init__(self, w: dict, world: int = 1, rank: int = 0, stream=None):
+    SUBLAYER = {"qkv": 1, "o": 2, "gu": 1, "down": 2}   # DeInfer roles
+
+    def __init__(self, w: dict, world: int = 1, rank: int = 0, stream=None, layout: int = DL_LAYOUT_RANK_PARALLEL):
         self.tensors = {"attn_norm": w["g_attn"].contiguous(), "mlp_norm": w["g_mlp"].contiguous()}
         self.c = dl_block_weights()
         self.c.attn_norm = self.tensors["attn_norm"].data_ptr()
@@ -265,8 +302,12 @@ class BlockWeights:
         for gname, mats in self.GROUPS:
             if gname == "gu" and "A_gate" not in w:
                 mats = ("up",)          # non-GLU MLP: the group holds up alone
-            A_sh, B_sh, lens = dl_tp_shard_factors([w["A_" + m] for m in mats], [w["B_" + m] for m in mats],
-                                                   world, rank, stream=stream)
+            As, Bs = [w["A_" + m] for m in mats], [w["B_" + m] for m in mats]
+            if layout == DL_LAYOUT_DEINFER:
+                A_sh, B_sh = dl_deinfer_shard_factors(self.SUBLAYER[gname], As, Bs, world, rank, stream=stream)
+                lens = [a.shape[1] for a in As]          # every latent column stays on the rank
+            else:
+                A_sh, B_sh, lens = dl_tp_shard_factors(As, Bs, world, rank, stream=stream)
             self.tensors["B_" + gname] = B_sh
             grp = getattr(self.c, gname)
             grp.B = B_sh.data_ptr()

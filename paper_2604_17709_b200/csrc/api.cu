@@ -418,6 +418,61 @@ dl_status dl_tp_shard_factors(int n_seg, const void* const* A, const int64_t* ld
   return DL_OK;
 }
 
+dl_status dl_deinfer_shard_factors(int sublayer, int n_seg, const void* const* A, const int64_t* lda,
+                                   const void* const* B, const int64_t* ldb, const int64_t* m, const int64_t* r,
+                                   int64_t n, dl_dtype dtype, int world, int rank, void* B_shard, int64_t ldb_shard,
+                                   void* const* A_shard, const int64_t* lda_shard, void* stream) {
+  if (!A || !lda || !B || !ldb || !m || !r || !A_shard || !lda_shard || !B_shard) {
+    set_error("dl_deinfer_shard_factors: null argument");
+    return DL_ERR_INVALID_ARG;
+  }
+  if ((sublayer != 1 && sublayer != 2) || n_seg < 1 || n_seg > 3 || (sublayer == 2 && n_seg != 1)) {
+    set_error("dl_deinfer_shard_factors: sublayer %d / n_seg %d invalid", sublayer, n_seg);
+    return DL_ERR_INVALID_ARG;
+  }
+  if (world < 1 || rank < 0 || rank >= world) {
+    set_error("dl_deinfer_shard_factors: rank %d / world %d invalid", rank, world);
+    return DL_ERR_PARTITION;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t es = esize(dtype);
+  if (sublayer == 1) {
+    // B: the rank's balanced share of the concatenated rows (as dl_tp_shard_factors)
+    int64_t beg[3], len[3], kloc = 0;
+    DL_TRY(dl_tp_plan(r, n_seg, world, rank, 0, beg, len, &kloc));
+    DL_TRY(check_ld(ldb_shard, n, dtype, "ldb_shard"));
+    int64_t row = 0;
+    for (int g = 0; g < n_seg; ++g) {
+      if (m[g] % world != 0) {
+        set_error("dl_deinfer_shard_factors: m[%d] = %lld not divisible by world %d", g, (long long)m[g], world);
+        return DL_ERR_PARTITION;
+      }
+      if (len[g] > 0) {
+        const uint8_t* bsrc = static_cast<const uint8_t*>(B[g]) + beg[g] * ldb[g] * es;
+        uint8_t* bdst = static_cast<uint8_t*>(B_shard) + row * ldb_shard * es;
+        DL_TRY(launch_copy2d(bsrc, ldb[g] * es, bdst, ldb_shard * es, len[g], n * es, st));
+        row += len[g];
+      }
+      // A: rows of the rank's output features, every latent column
+      const int64_t ml = m[g] / world;
+      DL_TRY(check_ld(lda_shard[g], r[g], dtype, "lda_shard"));
+      const uint8_t* asrc = static_cast<const uint8_t*>(A[g]) + rank * ml * lda[g] * es;
+      DL_TRY(launch_copy2d(asrc, lda[g] * es, A_shard[g], lda_shard[g] * es, ml, r[g] * es, st));
+    }
+    return DL_OK;
+  }
+  if (n % world != 0) {
+    set_error("dl_deinfer_shard_factors: n = %lld not divisible by world %d", (long long)n, world);
+    return DL_ERR_PARTITION;
+  }
+  const int64_t nl = n / world;
+  DL_TRY(check_ld(ldb_shard, nl, dtype, "ldb_shard"));
+  DL_TRY(check_ld(lda_shard[0], r[0], dtype, "lda_shard"));
+  const uint8_t* bsrc = static_cast<const uint8_t*>(B[0]) + rank * nl * es;
+  DL_TRY(launch_copy2d(bsrc, ldb[0] * es, B_shard, ldb_shard * es, r[0], nl * es, st));
+  return launch_copy2d(A[0], lda[0] * es, A_shard[0], lda_shard[0] * es, m[0], r[0] * es, st);
+}
+
 // ---------------------------------------------------------------------------
 // decomposed block
 // ---------------------------------------------------------------------------
@@ -429,6 +484,8 @@ struct BlockDims {
   int64_t k_qkv, k_o, k_gu, k_down, kmax;
   int64_t nmax;                    // widest stage-2 output (features)
   bool glu;                        // SiLU-GLU MLP (else ReLU on up alone)
+  int layout;                      // DL_LAYOUT_*
+  int64_t lat_slot;                // DeInfer: per-rank latent slice width in the all-gather
 };
 
 dl_status block_dims(const dl_block_config* c, int world, BlockDims* d) {
@@ -488,6 +545,30 @@ dl_status block_dims(const dl_block_config* c, int world, BlockDims* d) {
   d->kmax = std::max(std::max(d->k_qkv, d->k_o), std::max(d->k_gu, d->k_down)) + 3 * 64;
   d->nmax = std::max(c->h + 2 * hkv, (glu ? 2 : 1) * c->m);
   d->glu = glu;
+  d->layout = c->layout;
+  d->lat_slot = 0;
+  if (c->layout != DL_LAYOUT_RANK_PARALLEL && c->layout != DL_LAYOUT_DEINFER) {
+    set_error("layout %d unknown", c->layout);
+    return DL_ERR_INVALID_ARG;
+  }
+  if (c->layout == DL_LAYOUT_DEINFER) {
+    if (c->m % (64 * world) || c->h % (64 * world)) {
+      set_error("DeInfer layout needs h and m divisible by 64 * world");
+      return DL_ERR_PARTITION;
+    }
+    // stage 2 of q|k|v and gate|up reads the FULL latent (all-gathered);
+    // o / down stage 2 reads the full reduced latent
+    auto zw = [](std::initializer_list<int64_t> ks) {
+      int64_t w = 0;
+      for (int64_t k : ks) w += rup(k, 64);
+      return w;
+    };
+    const int64_t Lqkv = c->rank_q + c->rank_k + c->rank_v;
+    const int64_t Lgu = c->rank_gate + c->rank_up;
+    d->lat_slot = rup(cdiv(std::max(Lqkv, Lgu), world), 64);
+    d->kmax = std::max({zw({c->rank_q, c->rank_k, c->rank_v}), zw({c->rank_gate, c->rank_up}),
+                        rup(c->rank_o, 64), rup(c->rank_down, 64), d->lat_slot}) + 64;
+  }
   return DL_OK;
 }
 
@@ -510,6 +591,7 @@ struct BlockWs {
   unsigned int* tile_cnt;            // stream-K fixup arrival counters (one per output tile)
   float* tail;                       // prefill DP + stream-K tail scratch (zero-maintained)
   size_t tail_bytes;
+  __nv_bfloat16 *lat_send, *lat_recv;   // DeInfer latent all-gather [T x slot] / [P][T][slot]
   int64_t ldz32, ldzb, ldy32;
 };
 
@@ -537,6 +619,10 @@ BlockWs carve_block(Carver& c, const BlockDims& d, int64_t Tmax) {
   w.tile_cnt = c.take<unsigned int>(static_cast<size_t>((d.nmax + d.kmax) / 128 + 64));
   w.tail_bytes = Tmax > 256 ? kTailBytes : 0;
   w.tail = w.tail_bytes ? c.take<float>(w.tail_bytes / sizeof(float)) : nullptr;
+  if (d.layout == DL_LAYOUT_DEINFER) {
+    w.lat_send = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.lat_slot);
+    w.lat_recv = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.P * d.lat_slot);
+  }
   return w;
 }
 
@@ -676,6 +762,86 @@ dl_status run_group(const dl_factor_group& grp, int nseg, const int64_t* rows, c
   return tc_gemm(p2, skinny, st);
 }
 
+// DeInfer first sub-layer (Fig. 3) of a q|k|v or gate|up group:
+// stage 1 on the rank's concat-split B rows -> latent slice [T x k_loc];
+// all-gather of the slices (the low-rank communication); un-permute into the
+// group's Z layout; stage 2 with the rank's row shards of A (all l columns).
+// out2 receives the rank's local features [T x sum rows_loc].
+dl_status deinfer_first(const dl_factor_group& grp, int nseg, const int64_t* rows_loc, const __nv_bfloat16* act,
+                        int64_t ld_act, int64_t n, int64_t T, bool skinny, const BlockWs& ws, const BlockDims& d,
+                        dl_comm comm, const GemmOut& out2, cudaStream_t st) {
+  int64_t lens[3], beg[3], len[3], kloc = 0;
+  for (int s = 0; s < nseg; ++s) lens[s] = grp.seg[s].k;
+  DL_TRY(dl_tp_plan(lens, nseg, comm->world, comm->rank, 0, beg, len, &kloc));
+  if (skinny) {
+    GemmProblem p1 = one_seg(act, ld_act, T, n, grp.B, grp.ldb, kloc, n, out_plain(ws.zf, ws.ldz32, OUT_F32_RED, 0));
+    p1.sched = next_sched(ws.sched);
+    DL_TRY(tc_gemm(p1, true, st));
+    DL_TRY(launch_f32_to_bf16(ws.zf, ws.ldz32, ws.lat_send, d.lat_slot, T, rup(kloc, 4), 1, st));
+  } else {
+    GemmProblem p1 = one_seg(act, ld_act, T, n, grp.B, grp.ldb, kloc, n, out_plain(ws.lat_send, d.lat_slot, OUT_BF16, 0));
+    p1.tail_acc = ws.tail;
+    p1.tail_bytes = ws.tail_bytes;
+    DL_TRY(tc_gemm(p1, false, st));
+  }
+  DL_TRY(all_gather(comm, ws.lat_send, ws.lat_recv, static_cast<size_t>(T) * d.lat_slot, kNcclBfloat16, st));
+  const ZLayout zl = zlayout(grp, nseg);
+  LatentMap mp{};
+  mp.nseg = nseg;
+  mp.P = comm->world;
+  mp.T = T;
+  mp.slot = d.lat_slot;
+  int64_t L = 0;
+  for (int s = 0; s < nseg; ++s) {
+    mp.seg_beg[s] = L;
+    mp.seg_len[s] = lens[s];
+    mp.zoff[s] = zl.off[s];
+    L += lens[s];
+  }
+  mp.base = L / comm->world;
+  mp.extra = L % comm->world;
+  mp.width = zl.width;
+  DL_TRY(launch_latent_unpermute(ws.lat_recv, ws.zb, ws.ldzb, mp, st));
+  GemmProblem p2 = stage2(grp, nseg, rows_loc, ws.zb, ws.ldzb, T, zl, out2);
+  if (skinny) {
+    p2.sched = next_sched(ws.sched);
+  } else {
+    p2.tail_acc = ws.tail;
+    p2.tail_bytes = ws.tail_bytes;
+  }
+  return tc_gemm(p2, skinny, st);
+}
+
+// DeInfer second sub-layer (o or down): stage 1 with the rank's input-column
+// shard of B on its local activations -> partial latent [T x l]; reduce-sum
+// of the latent (fp32 on the decode path, bf16 on the prefill path); stage 2
+// with the replicated A, residual added into x.
+dl_status deinfer_second(const dl_factor_group& grp, const __nv_bfloat16* act, int64_t n_loc, int64_t m_out,
+                         int64_t T, bool skinny, const BlockWs& ws, dl_comm comm, __nv_bfloat16* x, cudaStream_t st) {
+  const int64_t l = grp.seg[0].k;
+  if (skinny) {
+    GemmProblem p1 = one_seg(act, n_loc, T, n_loc, grp.B, grp.ldb, l, n_loc, out_plain(ws.zf, ws.ldz32, OUT_F32_RED, 0));
+    p1.sched = next_sched(ws.sched);
+    DL_TRY(tc_gemm(p1, true, st));
+    DL_TRY(all_reduce(comm, ws.zf, static_cast<size_t>(T) * ws.ldz32, kNcclFloat32, st));
+    DL_TRY(launch_f32_to_bf16(ws.zf, ws.ldz32, ws.zb, ws.ldzb, T, rup(l, 4), 1, st));
+    GemmProblem p2 = one_seg(ws.zb, ws.ldzb, T, l, grp.seg[0].A, grp.seg[0].lda, m_out, l,
+                             out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0));
+    p2.sched = next_sched(ws.sched);
+    DL_TRY(tc_gemm(p2, true, st));
+    return launch_residual_add_f32(ws.yf, ws.ldy32, x, m_out, T, m_out, 1, st);
+  }
+  GemmProblem p1 = one_seg(act, n_loc, T, n_loc, grp.B, grp.ldb, l, n_loc, out_plain(ws.zb, ws.ldzb, OUT_BF16, 0));
+  p1.tail_acc = ws.tail;
+  p1.tail_bytes = ws.tail_bytes;
+  DL_TRY(tc_gemm(p1, false, st));
+  DL_TRY(all_reduce(comm, ws.zb, static_cast<size_t>(T) * ws.ldzb, kNcclBfloat16, st));
+  GemmProblem p2 = one_seg(ws.zb, ws.ldzb, T, l, grp.seg[0].A, grp.seg[0].lda, m_out, l, out_plain(x, m_out, OUT_BF16, 1));
+  p2.tail_acc = ws.tail;
+  p2.tail_bytes = ws.tail_bytes;
+  return tc_gemm(p2, false, st);
+}
+
 }  // namespace
 
 dl_status dl_block_workspace(const dl_block_config* cfg, int world, size_t* bytes) {
@@ -727,12 +893,26 @@ dl_status dl_decomposed_block_forward(const dl_block_config* cfg, const dl_block
   DL_TRY(check_ptr(w->attn_norm, "attn_norm"));
   DL_TRY(check_ptr(w->mlp_norm, "mlp_norm"));
   int64_t kq, ko, kg, kd;
-  DL_TRY(check_group(w->qkv, 3, d.h, "qkv", &kq));
-  DL_TRY(check_group(w->o, 1, d.h, "o", &ko));
   const int n_gu = d.glu ? 2 : 1;
+  const bool deinfer = comm && d.layout == DL_LAYOUT_DEINFER;
+  // DeInfer o / down hold the rank's input-column shard of B: [l x n/P]
+  DL_TRY(check_group(w->qkv, 3, d.h, "qkv", &kq));
+  DL_TRY(check_group(w->o, 1, deinfer ? d.h / P : d.h, "o", &ko));
   DL_TRY(check_group(w->gu, n_gu, d.h, d.glu ? "gate|up" : "up", &kg));
-  DL_TRY(check_group(w->down, 1, d.m, "down", &kd));
-  if (kq > d.k_qkv || ko > d.k_o || kg > d.k_gu || kd > d.k_down) {
+  DL_TRY(check_group(w->down, 1, deinfer ? d.m / P : d.m, "down", &kd));
+  if (deinfer) {
+    // segments carry the full ranks (the A shards keep every latent column)
+    const int64_t want[7] = {cfg->rank_q, cfg->rank_k, cfg->rank_v, cfg->rank_o, cfg->rank_gate, cfg->rank_up,
+                             cfg->rank_down};
+    const int64_t have[7] = {w->qkv.seg[0].k, w->qkv.seg[1].k, w->qkv.seg[2].k, w->o.seg[0].k,
+                             d.glu ? w->gu.seg[0].k : 0, w->gu.seg[d.glu ? 1 : 0].k, w->down.seg[0].k};
+    for (int i = 0; i < 7; ++i)
+      if (want[i] != have[i]) {
+        set_error("DeInfer layout: segment %d rank %lld != config rank %lld", i, (long long)have[i],
+                  (long long)want[i]);
+        return DL_ERR_RANK;
+      }
+  } else if (kq > d.k_qkv || ko > d.k_o || kg > d.k_gu || kd > d.k_down) {
     set_error("group shard larger than the balanced split allows");
     return DL_ERR_PARTITION;
   }
@@ -807,6 +987,55 @@ dl_status dl_decomposed_block_forward(const dl_block_config* cfg, const dl_block
   rc.theta = cfg->rope_theta;
   rc.rope = cfg->no_rope ? 0 : 1;
 
+  AttnArgs aa{};
+  aa.q = ws.q;
+  aa.out = ws.att;
+  aa.k_cache = rc.k_cache;
+  aa.v_cache = rc.v_cache;
+  aa.max_seq = max_seq;
+  aa.cu_seqlens = cu_seqlens;
+  aa.cache_lens = cache_lens;
+  aa.num_seqs = num_seqs;
+  aa.T = T;
+  aa.Hq = static_cast<int>(d.Hq_loc);
+  aa.Hk = static_cast<int>(d.Hk_loc);
+  aa.d = static_cast<int>(d.d);
+  aa.decode = phase == DL_DECODE;
+  aa.partial = ws.apart;
+  aa.partial_bytes = ws.apart_bytes;
+
+  if (tp && d.layout == DL_LAYOUT_DEINFER) {
+    // ---- DeInfer low-rank communication (Fig. 3) ----------
+    const int64_t qkv_loc[3] = {d.h / P, d.hkv / P, d.hkv / P};
+    const int64_t m_loc = d.m / P, ngu_loc = n_gu * m_loc;
+    const int64_t gu_loc[2] = {m_loc, m_loc};
+    DL_TRY(launch_rmsnorm(x, static_cast<const __nv_bfloat16*>(w->attn_norm), ws.xn, T, d.h, cfg->rms_eps, st));
+    const GemmOut qo = skinny ? out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0) : out_plain(ws.yb, d.W, OUT_BF16, 0);
+    DL_TRY(deinfer_first(w->qkv, 3, qkv_loc, ws.xn, d.h, d.h, T, skinny, ws, d, comm, qo, st));
+    if (skinny) {
+      rc.acc = ws.yf;
+      rc.ld_src = ws.ldy32;
+      rc.clear = 1;
+    } else {
+      rc.src = ws.yb;
+      rc.ld_src = d.W;
+    }
+    DL_TRY(launch_rope_cache(rc, st));
+    DL_TRY(launch_attention(aa, st));
+    DL_TRY(deinfer_second(w->o, ws.att, d.h / P, d.h, T, skinny, ws, comm, x, st));
+    DL_TRY(launch_rmsnorm(x, static_cast<const __nv_bfloat16*>(w->mlp_norm), ws.xn, T, d.h, cfg->rms_eps, st));
+    const GemmOut go = skinny ? out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0) : out_plain(ws.yb, ngu_loc, OUT_BF16, 0);
+    DL_TRY(deinfer_first(w->gu, n_gu, gu_loc, ws.xn, d.h, d.h, T, skinny, ws, d, comm, go, st));
+    if (skinny) {
+      if (d.glu) DL_TRY(launch_silu_mul_f32(ws.yf, ws.ldy32, ws.act, m_loc, T, m_loc, 1, st));
+      else DL_TRY(launch_relu_f32(ws.yf, ws.ldy32, ws.act, m_loc, T, m_loc, 1, st));
+    } else {
+      if (d.glu) DL_TRY(launch_silu_mul_bf16(ws.yb, ngu_loc, ws.act, m_loc, T, m_loc, st));
+      else DL_TRY(launch_relu_bf16(ws.yb, ngu_loc, ws.act, m_loc, T, m_loc, st));
+    }
+    return deinfer_second(w->down, ws.act, m_loc, d.h, T, skinny, ws, comm, x, st);
+  }
+
   DL_TRY(launch_rmsnorm(x, static_cast<const __nv_bfloat16*>(w->attn_norm), ws.xn, T, d.h, cfg->rms_eps, st));
   if (fx) {
     GemmFixup f = fixup(FIX_ROPE_CACHE);
@@ -835,22 +1064,6 @@ dl_status dl_decomposed_block_forward(const dl_block_config* cfg, const dl_block
   }
   if (!fx) DL_TRY(launch_rope_cache(rc, st));
 
-  AttnArgs aa{};
-  aa.q = ws.q;
-  aa.out = ws.att;
-  aa.k_cache = rc.k_cache;
-  aa.v_cache = rc.v_cache;
-  aa.max_seq = max_seq;
-  aa.cu_seqlens = cu_seqlens;
-  aa.cache_lens = cache_lens;
-  aa.num_seqs = num_seqs;
-  aa.T = T;
-  aa.Hq = static_cast<int>(d.Hq_loc);
-  aa.Hk = static_cast<int>(d.Hk_loc);
-  aa.d = static_cast<int>(d.d);
-  aa.decode = phase == DL_DECODE;
-  aa.partial = ws.apart;
-  aa.partial_bytes = ws.apart_bytes;
   DL_TRY(launch_attention(aa, st));
 
   const __nv_bfloat16* att_in = ws.att;

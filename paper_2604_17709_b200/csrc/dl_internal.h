@@ -182,6 +182,15 @@ dl_status launch_embedding(const __nv_bfloat16* table, int64_t vocab, int64_t h,
 // [P][T][w] -> [T][P*w]
 dl_status launch_unpermute(const __nv_bfloat16* src, __nv_bfloat16* dst,
                            int P, int64_t T, int64_t w, cudaStream_t st);
+// DeInfer latent all-gather result [P][T][slot] -> group Z layout (see elementwise.cu)
+struct LatentMap {
+  int nseg, P; int64_t T, slot;
+  int64_t base, extra;                     // balanced split of the group rank L over P
+  int64_t seg_beg[3], seg_len[3], zoff[3]; // latent start / length / Z column offset per segment
+  int64_t width;                           // Z layout width
+};
+dl_status launch_latent_unpermute(const __nv_bfloat16* recv, __nv_bfloat16* zb, int64_t ldzb,
+                                  const LatentMap& mp, cudaStream_t st);
 dl_status launch_copy2d(const void* src, int64_t lds, void* dst, int64_t ldd,
                         int64_t rows, int64_t cols_bytes, cudaStream_t st);
 

@@ -236,7 +236,41 @@ __global__ void __launch_bounds__(128) unpermute_kernel(const __nv_bfloat16* __r
   reinterpret_cast<uint4*>(dst)[(t * P + p) * w8 + c] = reinterpret_cast<const uint4*>(src)[(p * T + t) * w8 + c];
 }
 
+// DeInfer latent un-permute: the all-gathered slices recv [P][T][slot] (rank
+// p holds latent columns [begin_p, begin_p + len_p) of the concatenated group
+// rank, balanced split) -> the group's Z layout zb [T x width] (segment s at
+// columns [zoff_s, zoff_s + rup(len_s, 64)), zero padded).
+// grid (ceil(width / 256), T), one column per thread.
+__global__ void __launch_bounds__(256) latent_unpermute_kernel(const __nv_bfloat16* __restrict__ recv,
+                                                               __nv_bfloat16* __restrict__ zb, int64_t ldzb,
+                                                               LatentMap mp) {
+  pdl_trigger();   // successor may launch now; it waits for us before reading
+  pdl_wait();
+  const int64_t col = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (col >= mp.width) return;
+  const int64_t t = blockIdx.y;
+  int s = 0;
+  while (s + 1 < mp.nseg && col >= mp.zoff[s + 1]) ++s;
+  const int64_t c = col - mp.zoff[s];
+  __nv_bfloat16 v = __float2bfloat16_rn(0.f);
+  if (c < mp.seg_len[s]) {
+    const int64_t j = mp.seg_beg[s] + c;
+    const int64_t big = mp.extra * (mp.base + 1);
+    const int64_t p = j < big ? j / (mp.base + 1) : mp.extra + (j - big) / mp.base;
+    const int64_t b = p * mp.base + (p < mp.extra ? p : mp.extra);
+    v = recv[(p * mp.T + t) * mp.slot + (j - b)];
+  }
+  zb[t * ldzb + col] = v;
+}
+
 }  // namespace
+
+dl_status launch_latent_unpermute(const __nv_bfloat16* recv, __nv_bfloat16* zb, int64_t ldzb, const LatentMap& mp,
+                                  cudaStream_t st) {
+  if (mp.T <= 0 || mp.width <= 0) return DL_OK;
+  dim3 grid(static_cast<unsigned>((mp.width + 255) / 256), static_cast<unsigned>(mp.T));
+  return launch_pdl(latent_unpermute_kernel, grid, dim3(256), 0, st, "latent_unpermute", recv, zb, ldzb, mp);
+}
 
 dl_status launch_rmsnorm(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bfloat16* y, int64_t T, int64_t h,
                          float eps, cudaStream_t st) {

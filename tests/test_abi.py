@@ -147,3 +147,25 @@ def test_block_variant_validation(lib):
                                         64, 64)
     with pytest.raises(lib.DLError):
         lib.dl_block_workspace(glu_as_relu, 1)      # LLaMA ranks include a gate
+
+
+def test_block_layout_validation(lib):
+    """DL_LAYOUT_DEINFER workspace sizing and its divisibility / enum checks."""
+    from synthetic import LLAMA3_70B, block_ranks
+    rk = block_ranks(LLAMA3_70B, 0.4)
+    rp = lib.make_block_config(LLAMA3_70B, rk, 64, 64)
+    di = lib.make_block_config(LLAMA3_70B, rk, 64, 64, layout=lib.DL_LAYOUT_DEINFER)
+    for world in (1, 2, 4, 8):
+        assert lib.dl_block_workspace(di, world) > 0
+    # latent all-gather buffers: the DeInfer workspace holds [T x slot] + [P x T x slot]
+    assert lib.dl_block_workspace(di, 8) > lib.dl_block_workspace(rp, 8)
+    di.layout = 9
+    with pytest.raises(lib.DLError) as e:
+        lib.dl_block_workspace(di, 1)
+    assert e.value.name == "DL_ERR_INVALID_ARG"
+    import dataclasses
+    odd = dataclasses.replace(LLAMA3_70B, m=64 * 7)      # m not divisible by 64 * 2
+    bad = lib.make_block_config(odd, block_ranks(odd, 0.4), 64, 64, layout=lib.DL_LAYOUT_DEINFER)
+    with pytest.raises(lib.DLError) as e:
+        lib.dl_block_workspace(bad, 2)
+    assert e.value.name == "DL_ERR_PARTITION"

@@ -284,3 +284,26 @@ def test_variant_block_decode(dl, orc, name, S):
     assert rel(xd.cpu().double() - x.double(), ref - x.double().numpy()) <= TOL_BF16
     kg = torch.stack([kcd[b, :, cache_lens[b]].reshape(-1) for b in range(S)]).cpu()
     assert rel(kg, kn) <= TOL_BF16
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_deinfer_shard_factors_match_slices(dl, world):
+    """dl_deinfer_shard_factors: sublayer 1 = concat-split B rows + A row
+    shards; sublayer 2 = B input-column shard + full A.  Byte-exact copies."""
+    As = [gen_normal((m, k), 1.0, 50 + i, dtype=torch.bfloat16).cuda() for i, (m, k) in
+          enumerate([(512, 307), (256, 77), (256, 77)])]
+    Bs = [gen_normal((a.shape[1], 512), 1.0, 60 + i, dtype=torch.bfloat16).cuda() for i, a in enumerate(As)]
+    Bcat = torch.cat(Bs, 0)
+    start = 0
+    for r in range(world):
+        A_sh, B_sh = dl.dl_deinfer_shard_factors(1, As, Bs, world, r)
+        kloc = B_sh.shape[0]
+        assert torch.equal(B_sh, Bcat[start:start + kloc])
+        start += kloc
+        for a, s in zip(As, A_sh):
+            ml = a.shape[0] // world
+            assert torch.equal(s, a[r * ml:(r + 1) * ml])
+        A2, B2 = dl.dl_deinfer_shard_factors(2, As[:1], Bs[:1], world, r)
+        nl = 512 // world
+        assert torch.equal(B2, Bs[0][:, r * nl:(r + 1) * nl]) and torch.equal(A2[0], As[0])
+    assert start == Bcat.shape[0]

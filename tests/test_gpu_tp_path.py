@@ -23,19 +23,21 @@ os.environ.setdefault("MASTER_ADDR", "127.0.0.1"); os.environ.setdefault("MASTER
 torch.cuda.set_device(0)
 dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
 comm = dl.Comm.from_process_group()
-s = ModelShape("tp1", h=512, n_heads=4, n_kv_heads=2, head_dim=128, m=1024, n_layers=1, vocab=10)
+LAYOUT = __LAYOUT__
+s = ModelShape("tp1", h=512, n_heads=4, n_kv_heads=2, head_dim=128, m=1024, n_layers=1, vocab=10, glu=__GLU__)
 rk = block_ranks(s, 0.4)
 w = gen_block_weights(s, rk, 0, 21)
 cfgo = oracle.BlockCfg(s.h, s.n_heads, s.n_kv_heads, s.head_dim, s.m, rk["q"], rk["k"], rk["v"], rk["o"],
-                       rk["gate"], rk["up"], rk["down"], rope_theta=s.rope_theta, rms_eps=s.rms_eps)
+                       rk["gate"], rk["up"], rk["down"], rope_theta=s.rope_theta, rms_eps=s.rms_eps,
+                       mlp_glu=int(s.glu), layout=LAYOUT)
 def rel(a, b):
     a = np.asarray(a, np.float64); b = np.asarray(b, np.float64)
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
-wd = dl.BlockWeights({k: v.cuda() for k, v in w.items()}, world=1, rank=0)
+wd = dl.BlockWeights({k: v.cuda() for k, v in w.items()}, world=1, rank=0, layout=LAYOUT)
 errs = []
 for T in (40, 300):                       # skinny (stream-K) and wide (whole-tile) paths, prefill
     x = gen_normal((T, s.h), 1.0, 22, dtype=torch.bfloat16)
-    cfg = dl.make_block_config(s, rk, max_tokens=T, max_seqs=1)
+    cfg = dl.make_block_config(s, rk, max_tokens=T, max_seqs=1, layout=LAYOUT)
     ws = torch.zeros(dl.dl_block_workspace(cfg, 1), dtype=torch.uint8, device="cuda")
     kc = torch.zeros(1, s.n_kv_heads, T, s.head_dim, dtype=torch.bfloat16, device="cuda"); vc = torch.zeros_like(kc)
     pos = torch.arange(T, dtype=torch.int32, device="cuda"); cu = torch.tensor([0, T], dtype=torch.int32, device="cuda")
@@ -51,7 +53,7 @@ x = gen_normal((S, s.h), 1.0, 23, dtype=torch.bfloat16)
 kc = gen_normal((S, s.n_kv_heads, 31, s.head_dim), 1.0, 24, dtype=torch.bfloat16)
 vc = gen_normal((S, s.n_kv_heads, 31, s.head_dim), 1.0, 25, dtype=torch.bfloat16)
 ko = kc.permute(0, 2, 1, 3).reshape(S, 31, -1); vo = vc.permute(0, 2, 1, 3).reshape(S, 31, -1)
-cfg = dl.make_block_config(s, rk, max_tokens=S, max_seqs=S)
+cfg = dl.make_block_config(s, rk, max_tokens=S, max_seqs=S, layout=LAYOUT)
 ws = torch.zeros(dl.dl_block_workspace(cfg, 1), dtype=torch.uint8, device="cuda")
 cl = torch.tensor(lens, dtype=torch.int32, device="cuda")
 xd = x.cuda()
@@ -64,11 +66,16 @@ dist.destroy_process_group()
 '''
 
 
-def test_block_tp_code_path_one_rank_nccl():
+@pytest.mark.parametrize("layout,glu", [(0, True), (1, True), (1, False)])
+def test_block_tp_code_path_one_rank_nccl(layout, glu):
+    """layout 0 = rank-parallel (RS/AG/AR in the full space); layout 1 = DeInfer
+    (latent all-gather + un-permute, row-sharded A, latent all-reduce with a
+    replicated A)."""
     from paper_2604_17709_b200 import build
     build.build()
     env = dict(os.environ, DL_FORCE_TP_PATH="1")
-    src = SCRIPT.replace("__ROOT__", repr(ROOT)).replace("__PORT__", repr("29533"))
+    src = (SCRIPT.replace("__ROOT__", repr(ROOT)).replace("__PORT__", repr(str(29533 + 2 * layout + int(glu))))
+           .replace("__LAYOUT__", str(layout)).replace("__GLU__", str(glu)))
     r = subprocess.run([sys.executable, "-c", src], capture_output=True, text=True, env=env, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     line = [ln for ln in r.stdout.splitlines() if ln.startswith("ERRS")][-1]

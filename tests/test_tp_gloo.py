@@ -115,3 +115,74 @@ def test_tp_world2_gloo():
         assert err_ar < 1e-10 and err_rs < 1e-10 and err_ag == 0.0 and ok_heads
         klocs += kloc
     assert klocs == 37 + 11 + 13
+
+
+def _deinfer_worker(rank, world, port, q):
+    """DeInfer layout (Fig. 3) host logic: concat-split B rows per
+    dl_tp_plan, latent all-gather + un-permute, row-sharded A; input-sharded
+    B + latent all-reduce with the full A."""
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import oracle
+        import paper_2604_17709_b200 as dl
+        rng = np.random.default_rng(1)
+        T, h, hkv = 4, 64, 32
+        ranks = [37, 11, 13]
+        mats = [(h, ranks[0]), (hkv, ranks[1]), (hkv, ranks[2])]
+        A = [rng.standard_normal((m, k)) for m, k in mats]
+        B = [rng.standard_normal((k, h)) for _, k in mats]
+        X = rng.standard_normal((T, h))
+        full = [oracle.lowrank_linear(X, a, b) for a, b in zip(A, B)]
+        # first sub-layer: the rank's rows of the concatenated B
+        beg, lens, kloc = dl.dl_tp_plan(ranks, world, rank)
+        Bcat = np.concatenate(B, 0)
+        L = Bcat.shape[0]
+        start = sum(dl.dl_tp_plan(ranks, world, r)[2] for r in range(rank))
+        mine = oracle.matmul(X, Bcat[start:start + kloc].T)             # latent slice [T x kloc]
+        slot = -(-L // world)
+        send = torch.zeros(T, slot, dtype=torch.float64)
+        send[:, :kloc] = torch.tensor(mine)
+        recv = [torch.zeros_like(send) for _ in range(world)]
+        dist.all_gather(recv, send)
+        kl = [dl.dl_tp_plan(ranks, world, r)[2] for r in range(world)]
+        Z = np.concatenate([recv[r][:, :kl[r]].numpy() for r in range(world)], 1)   # un-permute
+        off = np.concatenate([[0], np.cumsum(ranks)])
+        err1 = 0.0
+        for g, (m, k) in enumerate(mats):
+            rows = slice(rank * m // world, (rank + 1) * m // world)
+            yl = oracle.matmul(Z[:, off[g]:off[g + 1]], A[g][rows].T)
+            err1 = max(err1, float(np.abs(yl - full[g][:, rows]).max()))
+        # second sub-layer (o): input-column shard of B, latent reduce-sum, full A
+        Ao, Bo = rng.standard_normal((h, 29)), rng.standard_normal((29, h))
+        cols = slice(rank * h // world, (rank + 1) * h // world)
+        part = torch.tensor(oracle.matmul(X[:, cols], Bo[:, cols].T))
+        dist.all_reduce(part)
+        yo = oracle.matmul(part.numpy(), Ao.T)
+        err2 = float(np.abs(yo - oracle.lowrank_linear(X, Ao, Bo)).max())
+        q.put((rank, err1, err2, kloc))
+        dist.destroy_process_group()
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, "error", repr(e)))
+
+
+@pytest.mark.timeout(300)
+def test_deinfer_layout_world2_gloo():
+    from paper_2604_17709_b200 import build
+    build.build()
+    import oracle
+    oracle.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_deinfer_worker, args=(r, WORLD, port, q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(WORLD)]
+    for p in procs:
+        p.join(timeout=60)
+    assert sum(r[3] for r in res if r[1] != "error") == 37 + 11 + 13, res
+    for r in res:
+        assert r[1] != "error", r
+        assert r[1] < 1e-10 and r[2] < 1e-10, r
