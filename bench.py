@@ -44,6 +44,8 @@ def parse():
     p.add_argument("--prefill-tokens", type=int, default=2048)
     p.add_argument("--prefill-steps", type=int, default=3)
     p.add_argument("--layers", type=int, default=0, help="debug only: fewer layers (invalid for reporting)")
+    p.add_argument("--layout", default="rp", choices=["rp", "deinfer"],
+                   help="TP sharding layout: rank-parallel (north star) or DeInfer low-rank communication")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-seqs", type=int, default=64)
     return p.parse_args()
@@ -221,7 +223,8 @@ def main():
     del lm_full_rows
     final_norm = torch.ones(shape.h, dtype=torch.bfloat16, device=dev)
     model = DecomposedLlama(shape, ranks, layer_iter(), embed, final_norm, lm_head, batch=args.batch,
-                            max_seq=args.ctx + 1, prefill_tokens=args.prefill_tokens, comm=comm, device=dev)
+                            max_seq=args.ctx + 1, prefill_tokens=args.prefill_tokens, comm=comm, device=dev,
+                            layout=dl.DL_LAYOUT_DEINFER if args.layout == "deinfer" else dl.DL_LAYOUT_RANK_PARALLEL)
     # context: ctx tokens already cached per sequence (random K/V), fixed for every step
     model.cache.normal_()
     model.cache_lens.fill_(args.ctx)
@@ -321,6 +324,8 @@ def main():
           + (shape.h + shape.m) * (ranks["gate"] + ranks["up"] + ranks["down"]))
     step_bytes = (2 * (n_layers * pl + shape.vocab * shape.h) + args.batch * args.ctx * n_layers * 2 * shape.h_kv * 2) \
         / world
+    if args.layout == "deinfer" and world > 1:   # A_o and A_down are replicated on every rank
+        step_bytes += 2 * n_layers * shape.h * (ranks["o"] + ranks["down"]) * (1 - 1 / world)
     step_gbs = step_bytes / (step_ms * 1e-3) / 1e9
 
     # ---- e2e: H2D ids from pinned host, graph, D2H logits into pinned host -----
@@ -378,6 +383,7 @@ def main():
                 "config": {"workload": f"llama3-{args.model} @{int(round(args.ratio * 100))}% decode "
                                        f"B={args.batch} ctx={args.ctx} (+ prefill {args.prefill_tokens})",
                            "global_batch": args.batch, "seq_len": args.ctx, "parallelism": f"tp{world}",
+                           "tp_layout": "deinfer" if args.layout == "deinfer" else "rank-parallel",
                            "layers": n_layers, "ranks": ranks,
                            "l2": "inputs larger than L2 (weights+KV stream from HBM every step)",
                            "cuda_graph": True},

@@ -20,15 +20,15 @@ class DecomposedLlama:
 
     def __init__(self, shape, ranks: dict, layer_weights, embed: torch.Tensor, final_norm: torch.Tensor,
                  lm_head_local: torch.Tensor, batch: int, max_seq: int, prefill_tokens: int = 0,
-                 comm: L.Comm | None = None, device="cuda"):
-        self.shape, self.ranks, self.comm = shape, ranks, comm
+                 comm: L.Comm | None = None, device="cuda", layout: int = L.DL_LAYOUT_RANK_PARALLEL):
+        self.shape, self.ranks, self.comm, self.layout = shape, ranks, comm, layout
         self.world = comm.world if comm else 1
         self.rank = comm.rank if comm else 0
         self.device = torch.device(device)
         self.batch, self.max_seq = batch, max_seq
         self.layers = []
         for w in layer_weights:
-            self.layers.append(L.BlockWeights(w, self.world, self.rank))
+            self.layers.append(L.BlockWeights(w, self.world, self.rank, layout=layout))
             del w
         self.embed, self.final_norm, self.lm_head = embed, final_norm, lm_head_local
         s = shape
@@ -36,7 +36,7 @@ class DecomposedLlama:
         nl = len(self.layers)
         bf = torch.bfloat16
         self.cache = torch.zeros((nl, 2, batch, hk_loc, max_seq, s.head_dim), dtype=bf, device=self.device)
-        self.dec_cfg = L.make_block_config(s, ranks, max_tokens=batch, max_seqs=batch)
+        self.dec_cfg = L.make_block_config(s, ranks, max_tokens=batch, max_seqs=batch, layout=layout)
         self.dec_ws = torch.zeros(L.dl_block_workspace(self.dec_cfg, self.world), dtype=torch.uint8,
                                   device=self.device)
         # decode-step static buffers
@@ -49,7 +49,7 @@ class DecomposedLlama:
         self.logits = torch.zeros(self.world, batch, vloc, dtype=bf, device=self.device)
         self.prefill_tokens = prefill_tokens
         if prefill_tokens:
-            self.pre_cfg = L.make_block_config(s, ranks, max_tokens=prefill_tokens, max_seqs=1)
+            self.pre_cfg = L.make_block_config(s, ranks, max_tokens=prefill_tokens, max_seqs=1, layout=layout)
             self.pre_ws = torch.zeros(L.dl_block_workspace(self.pre_cfg, self.world), dtype=torch.uint8,
                                       device=self.device)
             self.pre_cache = torch.zeros((nl, 2, 1, hk_loc, prefill_tokens, s.head_dim), dtype=bf,
