@@ -292,6 +292,26 @@ def main():
             dist.barrier()
         return ms, clk.summary()
 
+    def eager_ms(fn, steps):
+        """Same step launched eagerly (no CUDA Graph): the graph on/off study of
+        P:441-470 (Table 6), N2.  Device time between events on the stream."""
+        with torch.cuda.stream(stream):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(steps):
+                fn()
+            e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
     def gemm_roofline(kind, bound):
         recs = [r for r in dl.dl_profile_records() if r[3] == kind]
         if not recs:
@@ -316,6 +336,8 @@ def main():
     dms, dclk = timed(dgraph, args.steps, args.warmup)
     step_ms = dms / args.steps
     dec_tps = args.batch / (step_ms * 1e-3)
+    eager = eager_ms(model.decode_step, min(args.steps, 5))
+    graph_study = {"graph_ms_per_step": step_ms, "eager_ms_per_step": eager, "graph_speedup": eager / step_ms}
     ig = kernel_timing(model.decode_step, n_cap)
     roof = gemm_roofline(1, "hbm")
     del ig
@@ -392,6 +414,7 @@ def main():
                         "h2d_bytes_per_step": ids_h.numel() * ids_h.element_size(),
                         "d2h_bytes_per_step": out_h.numel() * out_h.element_size()},
                 "gpu_launches": dlaunch * args.steps, "clocks": dclk, "prefill": prefill,
+                "graph_study": graph_study,
                 "step_algorithmic_gb_per_gpu": step_bytes / 1e9, "init_s": init_s}
         if args.layers:
             line["invalid"] = f"debug run with {n_layers} layers"

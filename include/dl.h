@@ -260,6 +260,10 @@ typedef enum { DL_PREFILL = 0, DL_DECODE = 1 } dl_phase;
  *            zero-filled (cudaMemset) before its first use; every call
  *            leaves its fp32 reduction scratch zero-filled again (the
  *            epilogues consume-and-clear), so no per-call memset is needed.
+ *            The workspace layout depends on the config (ranks, dims,
+ *            max_tokens, layout) and world: a workspace may be shared only
+ *            by calls with the same config (e.g. all layers of a model with
+ *            uniform ranks); layers with different ranks need their own.
  *            Errors: SHAPE (T > max_tokens, num_seqs), PARTITION (heads %
  *            world, shard wider than the balanced split), RANK, ALIGN,
  *            UNSUPPORTED (head_dim != 128), WORKSPACE, CUDA, NCCL.       */

@@ -15,6 +15,9 @@ class DecomposedLlama:
 
     layer_weights: iterable of per-layer dicts {A_<m>, B_<m>, g_attn, g_mlp}
     (full, unsharded factors on this device; sharded here and then dropped).
+    ranks: one dict for every layer, or a list of per-layer dicts (variadic
+    per-layer ranks); each layer then gets its own block config and
+    the workspaces are sized for the largest.
     embed [V x h], final_norm [h], lm_head_local [V/P x h] (this rank's vocab rows).
     """
 
@@ -36,9 +39,20 @@ class DecomposedLlama:
         nl = len(self.layers)
         bf = torch.bfloat16
         self.cache = torch.zeros((nl, 2, batch, hk_loc, max_seq, s.head_dim), dtype=bf, device=self.device)
-        self.dec_cfg = L.make_block_config(s, ranks, max_tokens=batch, max_seqs=batch, layout=layout)
-        self.dec_ws = torch.zeros(L.dl_block_workspace(self.dec_cfg, self.world), dtype=torch.uint8,
-                                  device=self.device)
+        per_layer = ranks if isinstance(ranks, (list, tuple)) else [ranks] * nl
+        if len(per_layer) != nl:
+            raise ValueError(f"{len(per_layer)} rank dicts for {nl} layers")
+        # a workspace's layout is tied to its config (include/dl.h): one per distinct rank set
+        keys = [tuple(sorted(r.items())) for r in per_layer]
+        self.dec_cfgs = [L.make_block_config(s, r, max_tokens=batch, max_seqs=batch, layout=layout)
+                         for r in per_layer]
+        self.dec_cfg = self.dec_cfgs[0]
+        dws = {}
+        for k, c in zip(keys, self.dec_cfgs):
+            if k not in dws:
+                dws[k] = torch.zeros(L.dl_block_workspace(c, self.world), dtype=torch.uint8, device=self.device)
+        self.dec_wss = [dws[k] for k in keys]
+        self.dec_ws = self.dec_wss[0]
         # decode-step static buffers
         self.ids = torch.zeros(batch, dtype=torch.int32, device=self.device)
         self.cache_lens = torch.zeros(batch, dtype=torch.int32, device=self.device)
@@ -49,9 +63,16 @@ class DecomposedLlama:
         self.logits = torch.zeros(self.world, batch, vloc, dtype=bf, device=self.device)
         self.prefill_tokens = prefill_tokens
         if prefill_tokens:
-            self.pre_cfg = L.make_block_config(s, ranks, max_tokens=prefill_tokens, max_seqs=1, layout=layout)
-            self.pre_ws = torch.zeros(L.dl_block_workspace(self.pre_cfg, self.world), dtype=torch.uint8,
-                                      device=self.device)
+            self.pre_cfgs = [L.make_block_config(s, r, max_tokens=prefill_tokens, max_seqs=1, layout=layout)
+                             for r in per_layer]
+            self.pre_cfg = self.pre_cfgs[0]
+            pws = {}
+            for k, c in zip(keys, self.pre_cfgs):
+                if k not in pws:
+                    pws[k] = torch.zeros(L.dl_block_workspace(c, self.world), dtype=torch.uint8,
+                                         device=self.device)
+            self.pre_wss = [pws[k] for k in keys]
+            self.pre_ws = self.pre_wss[0]
             self.pre_cache = torch.zeros((nl, 2, 1, hk_loc, prefill_tokens, s.head_dim), dtype=bf,
                                          device=self.device)
             self.pre_ids = torch.zeros(prefill_tokens, dtype=torch.int32, device=self.device)
@@ -69,9 +90,9 @@ class DecomposedLlama:
         s = self.shape
         L.dl_embedding(self.embed, self.ids, self.x)
         for i, lw in enumerate(self.layers):
-            L.dl_decomposed_block_forward(self.dec_cfg, lw, self.x, self.cache_lens, None, self.batch, L.DL_DECODE,
+            L.dl_decomposed_block_forward(self.dec_cfgs[i], lw, self.x, self.cache_lens, None, self.batch, L.DL_DECODE,
                                           self.cache[i, 0], self.cache[i, 1], self.cache_lens, self.comm,
-                                          self.dec_ws)
+                                          self.dec_wss[i])
         L.dl_rmsnorm(self.x, self.final_norm, self.xn, s.rms_eps)
         L.dl_dense(self.xn, self.lm_head, self.logits_local)
         if self.world > 1:
@@ -85,9 +106,9 @@ class DecomposedLlama:
         T = self.prefill_tokens
         L.dl_embedding(self.embed, self.pre_ids, self.pre_x)
         for i, lw in enumerate(self.layers):
-            L.dl_decomposed_block_forward(self.pre_cfg, lw, self.pre_x, self.pre_pos, self.pre_cu, 1, L.DL_PREFILL,
+            L.dl_decomposed_block_forward(self.pre_cfgs[i], lw, self.pre_x, self.pre_pos, self.pre_cu, 1, L.DL_PREFILL,
                                           self.pre_cache[i, 0], self.pre_cache[i, 1], self.pre_lens, self.comm,
-                                          self.pre_ws)
+                                          self.pre_wss[i])
         L.dl_embedding(self.pre_x, self.pre_last, self.pre_xl)        # row gather of the last token
         L.dl_rmsnorm(self.pre_xl, self.final_norm, self.pre_xn, s.rms_eps)
         L.dl_dense(self.pre_xn, self.lm_head, self.pre_logits)

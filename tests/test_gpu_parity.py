@@ -307,3 +307,33 @@ def test_deinfer_shard_factors_match_slices(dl, world):
         nl = 512 // world
         assert torch.equal(B2, Bs[0][:, r * nl:(r + 1) * nl]) and torch.equal(A2[0], As[0])
     assert start == Bcat.shape[0]
+
+
+def test_model_decode_variadic_layer_ranks(dl, orc):
+    """N4 variadic per-layer ranks through the whole-model decode step: two
+    layers compressed at 40% and 20%; hidden state after the blocks vs the
+    oracle applied layer by layer (the embedding row is the first input)."""
+    from paper_2604_17709_b200.model import DecomposedLlama
+    s = SMALL
+    rks = [block_ranks(s, 0.4), block_ranks(s, 0.2)]
+    ws_ = [gen_block_weights(s, rk, 5, li) for li, rk in enumerate(rks)]
+    S, L = 6, 9
+    embed = gen_normal((s.vocab, s.h), 1.0, 70, dtype=torch.bfloat16).cuda()
+    lm = gen_normal((s.vocab, s.h), s.h ** -0.5, 71, dtype=torch.bfloat16).cuda()
+    model = DecomposedLlama(s, rks, [{k: v.cuda() for k, v in w.items()} for w in ws_], embed,
+                            torch.ones(s.h, dtype=torch.bfloat16, device="cuda"), lm, batch=S, max_seq=L + 1)
+    model.cache.copy_(gen_normal(tuple(model.cache.shape), 1.0, 72, dtype=torch.bfloat16))
+    model.cache_lens.fill_(L)
+    ids = torch.arange(S, dtype=torch.int32) * 37 % s.vocab
+    model.ids.copy_(ids)
+    cache0 = model.cache.cpu()
+    model.decode_step()
+    torch.cuda.synchronize()
+    x = embed.cpu()[ids.long()].double()
+    for li, (rk, w) in enumerate(zip(rks, ws_)):
+        ko = _cache_to_oracle(cache0[li, 0], S, L + 1)
+        vo = _cache_to_oracle(cache0[li, 1], S, L + 1)
+        x, _, _ = orc.block_decode(_oracle_cfg(orc, s, rk), w, x, ko, vo, [L] * S)
+        x = torch.tensor(x)
+    x0 = embed.cpu()[ids.long()].double()
+    assert rel(model.x.cpu().double() - x0, (x - x0).numpy()) <= TOL_BF16
