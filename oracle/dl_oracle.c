@@ -53,6 +53,19 @@ int oracle_matmul(const double *A, const double *B, double *C, int64_t M,
   return ORC_OK;
 }
 
+/* Z[T x k] = X[T x n] B[k x n]^T: the downward projection alone (stage 1, */
+/* x_v of P:168), used where the paper stores the low-rank result itself.  */
+static int oracle_matmul_bt(const double *X, const double *B, double *Z,
+                            int64_t T, int64_t n, int64_t k) {
+  for (int64_t t = 0; t < T; ++t)
+    for (int64_t j = 0; j < k; ++j) {
+      double s = 0.0;
+      for (int64_t l = 0; l < n; ++l) s += B[j * n + l] * X[t * n + l];
+      Z[t * k + j] = s;
+    }
+  return ORC_OK;
+}
+
 /* ------------------------------------------------------------------------ */
 /* Low-rank linear, P:103-109 (Section 2.1, Eq. 1): y = A (B x).             */
 /*   Z[t][j] = sum_l B[j][l] X[t][l]        (downward projection x_v) */
@@ -632,6 +645,94 @@ int oracle_block_decode(const oracle_block_cfg *c, const oracle_block_w *w,
   if (v_new) memcpy(v_new, vv, sizeof(double) * (size_t)(Bn * hkv));
   free(a); free(q); free(kk); free(vv); free(att);
   return rc;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Low-rank KV cache (N3).  P:111: "the KV cache can be compressed as a       */
+/* by-product of compressing K and V matrices in the attention layers, where  */
+/* the low-rank intermediate results between the two matrix multiplications   */
+/* now act as KV caches."  P:226-230 (two-stage reconstruction): the cached   */
+/* low-rank rows are copied to a buffer, "the compact KV cache multiplies     */
+/* upward matrices to finish the reconstruction", then "in-place rotary       */
+/* position embedding" is applied to the reconstruction results.             */
+/* Decode step of one block with such a cache: zk_cache [Bn x max_seq x r_k], */
+/* zv_cache [Bn x max_seq x r_v] hold z_k = B_k a_j, z_v = B_v a_j of the     */
+/* first cache_len[b] positions (a_j the normed input of token j).  History   */
+/* keys K_j = RoPE(A_k z_k,j, j), values V_j = A_v z_v,j; the new token's     */
+/* latents zk_new / zv_new are returned (what the cache appends).  world = 1  */
+/* (the latent is replicated on every rank, SPEC kvcache design decision).   */
+/* ------------------------------------------------------------------------ */
+int oracle_block_decode_lowrank(const oracle_block_cfg *c, const oracle_block_w *w,
+                                const double *x, int64_t Bn, const double *zk_cache,
+                                const double *zv_cache, int64_t max_seq,
+                                const int32_t *cache_len, double *x_out,
+                                double *zk_new, double *zv_new) {
+  int64_t h = c->h, H = c->n_heads, Hkv = c->n_kv_heads, d = c->head_dim;
+  int64_t hkv = Hkv * d, lk = c->r_k, lv = c->r_v;
+  if (H * d != h || H % Hkv != 0 || Bn < 0) return ORC_ESHAPE;
+  for (int64_t b = 0; b < Bn; ++b)
+    if (cache_len[b] < 0 || cache_len[b] >= max_seq) return ORC_ESHAPE;
+  double *a = (double *)malloc(sizeof(double) * (size_t)(Bn * h + 1));
+  double *q = (double *)malloc(sizeof(double) * (size_t)(Bn * h + 1));
+  double *zk = (double *)malloc(sizeof(double) * (size_t)(Bn * lk + 1));
+  double *zv = (double *)malloc(sizeof(double) * (size_t)(Bn * lv + 1));
+  double *att = (double *)malloc(sizeof(double) * (size_t)(Bn * h + 1));
+  if (!a || !q || !zk || !zv || !att) return ORC_ENOMEM;
+  int rc = 0;
+  oracle_rmsnorm(x, w->g_attn, c->rms_eps, a, Bn, h);
+  rc |= oracle_lowrank_linear(a, w->A_q, w->B_q, q, Bn, h, h, c->r_q);
+  rc |= oracle_matmul_bt(a, w->B_k, zk, Bn, h, lk);      /* z_k = B_k a (stage 1 only) */
+  rc |= oracle_matmul_bt(a, w->B_v, zv, Bn, h, lv);
+  if (c->use_rope) oracle_rope(q, cache_len, Bn, H, d, c->rope_theta);
+#pragma omp parallel for schedule(dynamic)
+  for (int64_t b = 0; b < Bn; ++b) {
+    int64_t nk = cache_len[b] + 1;
+    double *K = (double *)malloc(sizeof(double) * (size_t)(nk * hkv));
+    double *V = (double *)malloc(sizeof(double) * (size_t)(nk * hkv));
+    int32_t *pos = (int32_t *)malloc(sizeof(int32_t) * (size_t)nk);
+    const double **kr = (const double **)malloc(sizeof(double *) * (size_t)nk);
+    const double **vr = (const double **)malloc(sizeof(double *) * (size_t)nk);
+    for (int64_t u = 0; u < nk; ++u) {
+      /* compact low-rank row of token u (history from the cache, u == nk-1 the new one) */
+      const double *zku = u < nk - 1 ? zk_cache + (b * max_seq + u) * lk : zk + b * lk;
+      const double *zvu = u < nk - 1 ? zv_cache + (b * max_seq + u) * lv : zv + b * lv;
+      for (int64_t i = 0; i < hkv; ++i) {      /* reconstruction: A_k z_k, A_v z_v */
+        double sk = 0.0, sv = 0.0;
+        for (int64_t j = 0; j < lk; ++j) sk += w->A_k[i * lk + j] * zku[j];
+        for (int64_t j = 0; j < lv; ++j) sv += w->A_v[i * lv + j] * zvu[j];
+        K[u * hkv + i] = sk;
+        V[u * hkv + i] = sv;
+      }
+      pos[u] = (int32_t)u;
+    }
+    if (c->use_rope) oracle_rope(K, pos, nk, Hkv, d, c->rope_theta);   /* in place, after */
+    for (int64_t u = 0; u < nk; ++u) { kr[u] = K + u * hkv; vr[u] = V + u * hkv; }
+    attend_one(q + b * h, kr, vr, nk, H, Hkv, d, att + b * h);
+    free(K); free(V); free(pos); free(kr); free(vr);
+  }
+  rc |= block_tail(c, w, x, att, x_out, Bn, 1, 1);
+  if (zk_new) memcpy(zk_new, zk, sizeof(double) * (size_t)(Bn * lk));
+  if (zv_new) memcpy(zv_new, zv, sizeof(double) * (size_t)(Bn * lv));
+  free(a); free(q); free(zk); free(zv); free(att);
+  return rc;
+}
+
+/* Preparation-stage scan: "performs a scan to find which logical block */
+/* is physically contiguous".  phys[0..n) = a sequence's physical block ids in */
+/* logical order; a new run starts exactly where phys[i] != phys[i-1] + 1.    */
+/* Writes run starts / lengths (in blocks); returns the run count.           */
+int64_t oracle_kv_runs(const int32_t *phys, int64_t n, int32_t *run_start,
+                       int32_t *run_len) {
+  int64_t r = -1;
+  for (int64_t i = 0; i < n; ++i) {
+    if (i == 0 || phys[i] != phys[i - 1] + 1) {
+      ++r;
+      run_start[r] = phys[i];
+      run_len[r] = 0;
+    }
+    run_len[r] += 1;
+  }
+  return r + 1;
 }
 
 /* Parameter count of one decomposed block: sum over the 7 factor pairs of   */

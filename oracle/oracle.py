@@ -23,7 +23,7 @@ __all__ = [
     "build", "load", "matmul", "lowrank_linear", "shard_range",
     "lowrank_linear_sharded", "truncated_svd", "factor_params", "rmsnorm",
     "rope", "attention", "BlockCfg", "block_prefill", "block_decode",
-    "block_params", "census", "num_threads", "LAYOUT_RANK_PARALLEL", "LAYOUT_DEINFER",
+    "block_params", "census", "num_threads", "block_decode_lowrank", "kv_runs", "LAYOUT_RANK_PARALLEL", "LAYOUT_DEINFER",
 ]
 
 
@@ -63,6 +63,9 @@ def load():
             lib.oracle_attention.argtypes = [P, P, P, P, I64, P, ctypes.c_int32, I64, I64, I64]
             lib.oracle_block_prefill.argtypes = [P, P, P, I64, P, P, ctypes.c_int32, P, I64, P, P, P, I, I64]
             lib.oracle_block_decode.argtypes = [P, P, P, I64, P, P, I64, P, P, P, P, I, I64]
+            lib.oracle_block_decode_lowrank.argtypes = [P, P, P, I64, P, P, I64, P, P, P, P]
+            lib.oracle_kv_runs.argtypes = [P, I64, P, P]
+            lib.oracle_kv_runs.restype = I64
             lib.oracle_block_params.argtypes = [P]
             lib.oracle_block_params.restype = I64
             lib.oracle_census.argtypes = [I64] * 10 + [P]
@@ -267,6 +270,35 @@ def block_decode(cfg: BlockCfg, w: dict, x, cache_k, cache_v, cache_len,
     _check(rc, "block_decode")
     del keep
     return xo, kn, vn
+
+
+def block_decode_lowrank(cfg: BlockCfg, w: dict, x, zk_cache, zv_cache, cache_len):
+    """Decode with a low-rank KV cache.  zk_cache [B x max_seq x r_k],
+    zv_cache [B x max_seq x r_v] -> (x_out, zk_new [B x r_k], zv_new [B x r_v])."""
+    x = _f64(x)
+    zk, zv = _f64(zk_cache), _f64(zv_cache)
+    cl = _i32(cache_len)
+    Bn, h = x.shape
+    xo = np.empty((Bn, h))
+    kn = np.empty((Bn, cfg.r_k))
+    vn = np.empty((Bn, cfg.r_v))
+    cc = cfg._c()
+    cw, keep = _pack_w(w)
+    rc = load().oracle_block_decode_lowrank(ctypes.byref(cc), ctypes.byref(cw), _p(x), Bn, _p(zk), _p(zv),
+                                            zk.shape[1], _p(cl), _p(xo), _p(kn), _p(vn))
+    _check(rc, "block_decode_lowrank")
+    del keep
+    return xo, kn, vn
+
+
+def kv_runs(phys):
+    """Contiguous-run scan of a block list -> [(start, length)]."""
+    ph = _i32(phys)
+    n = len(ph)
+    st = np.zeros(max(n, 1), dtype=np.int32)
+    ln = np.zeros(max(n, 1), dtype=np.int32)
+    r = int(load().oracle_kv_runs(_p(ph), n, _p(st), _p(ln)))
+    return [(int(st[i]), int(ln[i])) for i in range(r)]
 
 
 def block_params(cfg: BlockCfg) -> int:

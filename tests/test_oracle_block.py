@@ -348,3 +348,60 @@ def test_census_table1(orc):
     for key, val in g["expected"].items():
         assert c[key] == val, key
     assert round(100 * (1 - c["deinfer_block_printed"] / c["unopt_block"])) == g["printed_saving_percent"]
+
+
+# ---- low-rank KV cache (N3: P:111) ---------------------------------------
+def test_lowrank_kv_decode_equals_prefill(orc):
+    """Decoding token L with the LATENT cache z_k = B_k a_j, z_v = B_v a_j of tokens j < L
+    (reconstructed K = RoPE(A_k z_k), V = A_v z_v) == prefill row L."""
+    for variant in ({}, {"n_kv_heads": 4}, {"use_rope": False}):
+        cfg, w, _ = _small_block(orc, lossless=False, seed=41, **variant)
+        r = np.random.default_rng(42)
+        lens = [3, 0, 6]
+        max_seq = 8
+        zk = np.zeros((3, max_seq, cfg.r_k))
+        zv = np.zeros((3, max_seq, cfg.r_v))
+        xs, ref, ref_zk = [], [], []
+        for b, L in enumerate(lens):
+            x = r.standard_normal((L + 1, cfg.h))
+            out, _, _ = orc.block_prefill(cfg, w, x, np.arange(L + 1), [0, L + 1])
+            a = orc.rmsnorm(x, w["g_attn"], cfg.rms_eps)
+            zk[b, :L] = orc.matmul(a, w["B_k"].T)[:L]
+            zv[b, :L] = orc.matmul(a, w["B_v"].T)[:L]
+            xs.append(x[L])
+            ref.append(out[L])
+            ref_zk.append(orc.matmul(a[L:L + 1], w["B_k"].T)[0])
+        o, zk_new, _ = orc.block_decode_lowrank(cfg, w, np.stack(xs), zk, zv, lens)
+        assert rel(o, np.stack(ref)) < 1e-12, variant
+        assert rel(zk_new, np.stack(ref_zk)) < 1e-13
+
+
+def _brute_min_runs(phys):
+    """Minimal order-preserving partition into ascending-by-one runs (exhaustive)."""
+    n = len(phys)
+    best = None
+    for mask in range(1 << max(n - 1, 0)):
+        cuts = [i + 1 for i in range(n - 1) if mask >> i & 1]
+        parts, lo = [], 0
+        for c in cuts + [n]:
+            parts.append(phys[lo:c])
+            lo = c
+        if all(all(p[i + 1] == p[i] + 1 for i in range(len(p) - 1)) for p in parts):
+            if best is None or len(parts) < len(best):
+                best = parts
+    return [(p[0], len(p)) for p in best] if n else []
+
+
+def test_kv_runs_examples_and_minimality(orc):
+    """P:226 contiguous-run scan: SPEC examples and a brute-force minimal partition."""
+    assert orc.kv_runs([5, 6, 7]) == [(5, 3)]
+    assert orc.kv_runs([5, 7, 6]) == [(5, 1), (7, 1), (6, 1)]
+    assert orc.kv_runs([]) == []
+    r = np.random.default_rng(43)
+    for _ in range(60):
+        n = int(r.integers(1, 9))
+        phys = [int(v) for v in r.permutation(12)[:n]] if r.random() < 0.5 else \
+            [int(v) for v in np.sort(r.choice(12, n, replace=False))]
+        runs = orc.kv_runs(phys)
+        assert runs == _brute_min_runs(phys), phys
+        assert sum(ln for _, ln in runs) == n
