@@ -277,6 +277,74 @@ dl_status dl_decomposed_block_forward(
     void *stream);
 
 /* ------------------------------------------------------------------------
+ * Paged low-rank KV cache ("the low-rank
+ * intermediate results between the two matrix multiplications now act as KV
+ * caches", PAPER.md:219-237 two-stage reconstruction).
+ *
+ * Every cached token stores its latent z_k = B_k a and z_v = B_v a instead of
+ * post-RoPE K / V: (l_k + l_v) / (2 h_kv) of the bytes (0.6 at 40 %).
+ * Pool: num_blocks blocks of block_size slots; slot row (bf16, ld_slot
+ * elements, multiple of 8) = [z_k (l_k) | zero pad to zv_off | z_v (l_v)]
+ * with zv_off = rup(l_k, 64); slot_pos holds each slot's position.
+ * A decode step has the paper's two stages:
+ *  preparation (host, before the replay; any CPU / GPU work allowed):
+ *    dl_kv_prepare scans each sequence's block table for physically
+ *    contiguous runs and derives the remapping index list (the first
+ *    buffer block of each sequence); the caller copies the plan to the
+ *    device arrays below.
+ *  replay (device, fixed buffers and shapes, CUDA-Graph capturable):
+ *    dl_decomposed_block_forward_kvlr appends the new tokens' latents to the
+ *    pool, copies the runs into the squeeze buffer, reconstructs K | V of the
+ *    whole buffer capacity with ONE fixed-size tcgen05 GEMM ("we only need to
+ *    use the GEMM kernel that has a large size"), rotates K in place
+ *    with the stored positions and attends through the remapping list.
+ * Works at TP = 1 and with DL_LAYOUT_DEINFER (the latent is all-gathered, so
+ * every rank holds the full low-rank cache and reconstructs its local kv
+ * heads); the rank-parallel layout at P > 1 has only partial latents:
+ * DL_ERR_UNSUPPORTED.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  void *pool;                  /* [num_blocks * block_size][ld_slot] bf16    */
+  int32_t *slot_pos;           /* [num_blocks * block_size]                  */
+  int64_t num_blocks, block_size, ld_slot;
+  const int32_t *block_tables; /* device [max_seqs][max_blocks_per_seq]      */
+  int64_t max_blocks_per_seq;
+  /* plan (device int32, from dl_kv_prepare)                                 */
+  const int32_t *run_src;      /* [max_runs] first physical block of run r   */
+  const int32_t *run_dst;      /* [max_runs] first buffer block (ascending)  */
+  const int32_t *run_len;      /* [max_runs] length in blocks                */
+  const int32_t *n_runs;       /* [1]                                        */
+  const int32_t *seq_block;    /* [max_seqs] remapping index list            */
+  /* fixed buffers (caller-owned, allocated once)                            */
+  void *squeeze;               /* [cap_blocks * block_size][ld_slot] bf16    */
+  int32_t *squeeze_pos;        /* [cap_blocks * block_size]                  */
+  void *recon;                 /* [cap_blocks * block_size][2 h_kv / P] bf16 */
+  int64_t cap_blocks;
+} dl_kv_lowrank;
+
+/* dl_kv_prepare (host only): block_tables [num_seqs][max_blocks_per_seq]
+ * (host), seq_tokens[s] = tokens of sequence s AFTER this step's append.
+ * Outputs (host, caller-allocated): run_src / run_dst / run_len [max_runs],
+ * *n_runs, seq_block [num_seqs].  Runs never cross sequences; a run starts
+ * where block i+1 is not physically block i + 1.  Errors: SHAPE (bad sizes,
+ * block id < 0), WORKSPACE (more than max_runs runs or cap_blocks blocks). */
+dl_status dl_kv_prepare(const int32_t *block_tables, int64_t max_blocks_per_seq,
+                        const int32_t *seq_tokens, int32_t num_seqs,
+                        int64_t block_size, int64_t max_runs, int64_t cap_blocks,
+                        int32_t *run_src, int32_t *run_dst, int32_t *run_len,
+                        int32_t *n_runs, int32_t *seq_block);
+
+/* Decode step of one block with the low-rank cache (T == num_seqs new
+ * tokens, token s at position positions[s], appended at slot cache_lens[s]
+ * of sequence s; attention covers cache_lens[s] + 1 keys).  Other arguments
+ * as dl_decomposed_block_forward.  Extra errors: INVALID_ARG (kv fields),
+ * UNSUPPORTED (rank-parallel layout at P > 1).                             */
+dl_status dl_decomposed_block_forward_kvlr(
+    const dl_block_config *cfg, const dl_block_weights *w, void *x, int64_t T,
+    const int32_t *positions, const dl_kv_lowrank *kv, const int32_t *cache_lens,
+    dl_comm comm, void *workspace, size_t workspace_bytes, void *stream);
+
+/* ------------------------------------------------------------------------
  * Model-level helpers used by the decode / prefill step (embedding gather,
  * final norm + dense LM head).  Not part of the paper's method; provided so
  * a whole-model step runs in this library's kernels only.

@@ -23,7 +23,8 @@ EXPORTS = ("dl_last_error", "dl_version", "dl_device_ok", "dl_comm_create", "dl_
            "dl_lowrank_linear_workspace", "dl_lowrank_linear", "dl_tp_plan", "dl_tp_shard_factors",
            "dl_block_workspace", "dl_decomposed_block_forward", "dl_embedding", "dl_rmsnorm",
            "dl_dense_workspace", "dl_dense", "dl_launch_count", "dl_profile_begin", "dl_profile_end",
-           "dl_profile_count", "dl_profile_get", "dl_debug_gemm_trace", "dl_deinfer_shard_factors")
+           "dl_profile_count", "dl_profile_get", "dl_debug_gemm_trace", "dl_deinfer_shard_factors",
+           "dl_kv_prepare", "dl_decomposed_block_forward_kvlr")
 
 
 class DLError(RuntimeError):
@@ -62,6 +63,13 @@ class dl_block_weights(ctypes.Structure):
                 ("gu", dl_factor_group), ("down", dl_factor_group)]
 
 
+class dl_kv_lowrank(ctypes.Structure):
+    _fields_ = [("pool", P), ("slot_pos", P), ("num_blocks", I64), ("block_size", I64), ("ld_slot", I64),
+                ("block_tables", P), ("max_blocks_per_seq", I64), ("run_src", P), ("run_dst", P), ("run_len", P),
+                ("n_runs", P), ("seq_block", P), ("squeeze", P), ("squeeze_pos", P), ("recon", P),
+                ("cap_blocks", I64)]
+
+
 _lock = threading.Lock()
 _lib = None
 
@@ -97,6 +105,10 @@ def load():
             lib.dl_profile_get.argtypes = [I, P, P, P, P]
             lib.dl_debug_gemm_trace.argtypes = [P]
             lib.dl_deinfer_shard_factors.argtypes = [I, I, P, P, P, P, P, P, I64, I, I, I, P, I64, P, P, P]
+            lib.dl_kv_prepare.argtypes = [P, I64, P, I32, I64, I64, I64, P, P, P, P, P]
+            lib.dl_decomposed_block_forward_kvlr.argtypes = [ctypes.POINTER(dl_block_config),
+                                                             ctypes.POINTER(dl_block_weights), P, I64, P,
+                                                             ctypes.POINTER(dl_kv_lowrank), P, P, P, ctypes.c_size_t, P]
             for name in EXPORTS[3:]:
                 getattr(lib, name).restype = I
             lib.dl_launch_count.restype = ctypes.c_longlong
@@ -336,6 +348,82 @@ def dl_decomposed_block_forward(cfg: dl_block_config, weights: BlockWeights, x: 
                                               _ptr(positions), _ptr(cu_seqlens), num_seqs, phase, _ptr(k_cache),
                                               _ptr(v_cache), _ptr(cache_lens), k_cache.shape[2], _comm(comm),
                                               _ptr(workspace), workspace.numel(), _stream(stream)))
+    return x
+
+
+def dl_kv_prepare(block_tables, seq_tokens, block_size: int, max_runs: int, cap_blocks: int):
+    """Preparation stage of the low-rank KV cache: contiguous-run scan and
+    remapping index list.  Host int32 arrays in; returns (run_src, run_dst, run_len,
+    n_runs, seq_block) as numpy int32 arrays (length max_runs / num_seqs)."""
+    import numpy as np
+    bt = np.ascontiguousarray(np.asarray(block_tables, dtype=np.int32))
+    st = np.ascontiguousarray(np.asarray(seq_tokens, dtype=np.int32))
+    ns = len(st)
+    rs, rd, rl = (np.zeros(max(max_runs, 1), np.int32) for _ in range(3))
+    nr = np.zeros(1, np.int32)
+    sb = np.zeros(max(ns, 1), np.int32)
+    p = lambda a: a.ctypes.data_as(P)  # noqa: E731
+    _check(load().dl_kv_prepare(p(bt), bt.shape[1] if bt.ndim == 2 else 1, p(st), ns, block_size, max_runs,
+                                cap_blocks, p(rs), p(rd), p(rl), p(nr), p(sb)))
+    return rs, rd, rl, int(nr[0]), sb[:ns]
+
+
+class LowRankKVCache:
+    """Paged low-rank KV cache of ONE layer plus the step's fixed buffers
+    (squeeze / reconstruction buffers may be shared by all layers: pass them in).
+
+    pool slot = [z_k (l_k) | pad to rup(l_k, 64) | z_v (l_v)] bf16; see include/dl.h."""
+
+    def __init__(self, l_k: int, l_v: int, hkv_local: int, num_blocks: int, block_size: int, max_seqs: int,
+                 max_blocks_per_seq: int, cap_blocks: int, max_runs: int | None = None, device="cuda",
+                 shared: "LowRankKVCache | None" = None):
+        dev = torch.device(device)
+        self.l_k, self.l_v, self.block_size = l_k, l_v, block_size
+        self.zv_off = -(-l_k // 64) * 64
+        self.ld_slot = _pad8(self.zv_off + l_v)
+        self.pool = torch.zeros(num_blocks * block_size, self.ld_slot, dtype=torch.bfloat16, device=dev)
+        self.slot_pos = torch.zeros(num_blocks * block_size, dtype=torch.int32, device=dev)
+        self.block_tables = torch.zeros(max_seqs, max_blocks_per_seq, dtype=torch.int32, device=dev)
+        self.max_runs = max_runs or max_seqs * max_blocks_per_seq
+        if shared is None:
+            self.run_src = torch.zeros(self.max_runs, dtype=torch.int32, device=dev)
+            self.run_dst = torch.zeros_like(self.run_src)
+            self.run_len = torch.zeros_like(self.run_src)
+            self.n_runs = torch.zeros(1, dtype=torch.int32, device=dev)
+            self.seq_block = torch.zeros(max_seqs, dtype=torch.int32, device=dev)
+            rows = cap_blocks * block_size
+            self.squeeze = torch.zeros(rows, self.ld_slot, dtype=torch.bfloat16, device=dev)
+            self.squeeze_pos = torch.zeros(rows, dtype=torch.int32, device=dev)
+            self.recon = torch.zeros(rows, 2 * hkv_local, dtype=torch.bfloat16, device=dev)
+        else:
+            for k in ("run_src", "run_dst", "run_len", "n_runs", "seq_block", "squeeze", "squeeze_pos", "recon"):
+                setattr(self, k, getattr(shared, k))
+        self.cap_blocks = cap_blocks
+        self.c = dl_kv_lowrank(self.pool.data_ptr(), self.slot_pos.data_ptr(), num_blocks, block_size, self.ld_slot,
+                               self.block_tables.data_ptr(), max_blocks_per_seq, self.run_src.data_ptr(),
+                               self.run_dst.data_ptr(), self.run_len.data_ptr(), self.n_runs.data_ptr(),
+                               self.seq_block.data_ptr(), self.squeeze.data_ptr(), self.squeeze_pos.data_ptr(),
+                               self.recon.data_ptr(), cap_blocks)
+
+    def prepare(self, block_tables_host, seq_tokens):
+        """Preparation stage: plan on the host, copy into the fixed device plan arrays."""
+        rs, rd, rl, nr, sb = dl_kv_prepare(block_tables_host, seq_tokens, self.block_size, self.max_runs,
+                                           self.cap_blocks)
+        self.run_src.copy_(torch.from_numpy(rs[:self.max_runs]))
+        self.run_dst.copy_(torch.from_numpy(rd[:self.max_runs]))
+        self.run_len.copy_(torch.from_numpy(rl[:self.max_runs]))
+        self.n_runs.fill_(nr)
+        self.seq_block[:len(sb)].copy_(torch.from_numpy(sb))
+        return nr
+
+
+def dl_decomposed_block_forward_kvlr(cfg: dl_block_config, weights: BlockWeights, x: torch.Tensor,
+                                     positions: torch.Tensor, kv: LowRankKVCache, cache_lens: torch.Tensor,
+                                     comm: Comm | None, workspace: torch.Tensor, stream=None) -> torch.Tensor:
+    _check(load().dl_decomposed_block_forward_kvlr(ctypes.byref(cfg), ctypes.byref(weights.c), _ptr(x), x.shape[0],
+                                                   _ptr(positions), ctypes.byref(kv.c), _ptr(cache_lens),
+                                                   _comm(comm), _ptr(workspace), workspace.numel(),
+                                                   _stream(stream)))
     return x
 
 

@@ -767,9 +767,10 @@ dl_status run_group(const dl_factor_group& grp, int nseg, const int64_t* rows, c
 // all-gather of the slices (the low-rank communication); un-permute into the
 // group's Z layout; stage 2 with the rank's row shards of A (all l columns).
 // out2 receives the rank's local features [T x sum rows_loc].
-dl_status deinfer_first(const dl_factor_group& grp, int nseg, const int64_t* rows_loc, const __nv_bfloat16* act,
-                        int64_t ld_act, int64_t n, int64_t T, bool skinny, const BlockWs& ws, const BlockDims& d,
-                        dl_comm comm, const GemmOut& out2, cudaStream_t st) {
+// Stage 1 + latent all-gather + un-permute: the full latent Z of the group in
+// ws.zb (segment-aligned layout zlayout(grp, nseg)).
+dl_status deinfer_latent(const dl_factor_group& grp, int nseg, const __nv_bfloat16* act, int64_t ld_act, int64_t n,
+                         int64_t T, bool skinny, const BlockWs& ws, const BlockDims& d, dl_comm comm, cudaStream_t st) {
   int64_t lens[3], beg[3], len[3], kloc = 0;
   for (int s = 0; s < nseg; ++s) lens[s] = grp.seg[s].k;
   DL_TRY(dl_tp_plan(lens, nseg, comm->world, comm->rank, 0, beg, len, &kloc));
@@ -801,7 +802,14 @@ dl_status deinfer_first(const dl_factor_group& grp, int nseg, const int64_t* row
   mp.base = L / comm->world;
   mp.extra = L % comm->world;
   mp.width = zl.width;
-  DL_TRY(launch_latent_unpermute(ws.lat_recv, ws.zb, ws.ldzb, mp, st));
+  return launch_latent_unpermute(ws.lat_recv, ws.zb, ws.ldzb, mp, st);
+}
+
+dl_status deinfer_first(const dl_factor_group& grp, int nseg, const int64_t* rows_loc, const __nv_bfloat16* act,
+                        int64_t ld_act, int64_t n, int64_t T, bool skinny, const BlockWs& ws, const BlockDims& d,
+                        dl_comm comm, const GemmOut& out2, cudaStream_t st) {
+  DL_TRY(deinfer_latent(grp, nseg, act, ld_act, n, T, skinny, ws, d, comm, st));
+  const ZLayout zl = zlayout(grp, nseg);
   GemmProblem p2 = stage2(grp, nseg, rows_loc, ws.zb, ws.ldzb, T, zl, out2);
   if (skinny) {
     p2.sched = next_sched(ws.sched);
@@ -842,6 +850,70 @@ dl_status deinfer_second(const dl_factor_group& grp, const __nv_bfloat16* act, i
   return tc_gemm(p2, false, st);
 }
 
+// Low-rank KV cache decode attention (N3): latent of
+// the new tokens -> pool; squeeze the runs; ONE fixed-size reconstruction GEMM
+// over the buffer capacity; in-place RoPE; q projection; attention through the
+// remapping index list.  Output: ws.att [T x Hq_loc*d].
+dl_status kvlr_attention(const dl_block_config* cfg, const BlockDims& d, const dl_block_weights* w, const BlockWs& ws,
+                         const dl_kv_lowrank* kv, int64_t T, const int32_t* positions, const int32_t* cache_lens,
+                         bool tp, dl_comm comm, AttnArgs aa, RopeCacheArgs rc, cudaStream_t st) {
+  const dl_factor_group& g = w->qkv;
+  const ZLayout zl = zlayout(g, 3);
+  // 1. latent z = xn . B^T of q|k|v (DeInfer: all-gathered)
+  if (tp) {
+    DL_TRY(deinfer_latent(g, 3, ws.xn, d.h, d.h, T, true, ws, d, comm, st));
+  } else {
+    GemmProblem p1 = stage1(g, 3, ws.xn, d.h, T, d.h, zl, out_plain(ws.zf, ws.ldz32, OUT_F32_RED, 0));
+    p1.sched = next_sched(ws.sched);
+    DL_TRY(tc_gemm(p1, true, st));
+    DL_TRY(launch_f32_to_bf16(ws.zf, ws.ldz32, ws.zb, ws.ldzb, T, zl.width, 1, st));
+  }
+  const int64_t lk = g.seg[1].k, lv = g.seg[2].k, zv_off = zl.off[2] - zl.off[1];
+  // 2. append [z_k | pad | z_v] of each new token to its pool slot
+  DL_TRY(launch_kv_append(ws.zb, ws.ldzb, zl.off[1], zv_off + lv, static_cast<__nv_bfloat16*>(kv->pool), kv->ld_slot,
+                          kv->slot_pos, kv->block_size, kv->block_tables, kv->max_blocks_per_seq, cache_lens,
+                          positions, T, st));
+  // 3. squeeze the contiguous runs into the compact buffer
+  DL_TRY(launch_kv_squeeze(static_cast<const __nv_bfloat16*>(kv->pool), kv->slot_pos,
+                           static_cast<__nv_bfloat16*>(kv->squeeze), kv->squeeze_pos, kv->ld_slot, kv->block_size,
+                           kv->run_src, kv->run_dst, kv->run_len, kv->n_runs, kv->cap_blocks, st));
+  // 4. reconstruction K | V = [z_k | z_v] . [A_k | A_v]^T at the buffer capacity
+  const int64_t hkl = d.hkv / d.P, rows = kv->cap_blocks * kv->block_size;
+  GemmProblem pr{};
+  pr.act = kv->squeeze;
+  pr.ld_act = kv->ld_slot;
+  pr.T = rows;
+  pr.k_act = kv->ld_slot;
+  pr.nseg = 2;
+  pr.seg[0] = GemmSeg{g.seg[1].A, g.seg[1].lda, hkl, lk, 0, 0};
+  pr.seg[1] = GemmSeg{g.seg[2].A, g.seg[2].lda, hkl, lv, hkl, zv_off};
+  pr.n_feat = 2 * hkl;
+  pr.out = out_plain(kv->recon, 2 * hkl, OUT_BF16, 0);
+  DL_TRY(tc_gemm(pr, false, st));
+  // 5. in-place RoPE of the reconstructed keys (stored positions)
+  if (!cfg->no_rope)
+    DL_TRY(launch_rope_rows(static_cast<__nv_bfloat16*>(kv->recon), 2 * hkl, static_cast<int>(d.Hk_loc),
+                            kv->squeeze_pos, rows, cfg->rope_theta, st));
+  // 6. q = z_q . A_q^T (local heads) + RoPE
+  const int64_t q_rows[1] = {d.h / d.P};
+  GemmProblem pq = stage2(g, 1, q_rows, ws.zb, ws.ldzb, T, zl, out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0));
+  pq.sched = next_sched(ws.sched);
+  DL_TRY(tc_gemm(pq, true, st));
+  rc.acc = ws.yf;
+  rc.ld_src = ws.ldy32;
+  rc.clear = 1;
+  rc.Hk = 0;   // q only: keys come from the reconstruction buffer
+  DL_TRY(launch_rope_cache(rc, st));
+  // 7. attention over the buffer through the remapping index list
+  const __nv_bfloat16* recon = static_cast<const __nv_bfloat16*>(kv->recon);
+  aa.k_cache = recon;
+  aa.v_cache = recon + hkl;
+  aa.kv_ld = 2 * hkl;
+  aa.kv_blk0 = kv->seq_block;
+  aa.kv_bs = kv->block_size;
+  return launch_attention(aa, st);
+}
+
 }  // namespace
 
 dl_status dl_block_workspace(const dl_block_config* cfg, int world, size_t* bytes) {
@@ -857,11 +929,11 @@ dl_status dl_block_workspace(const dl_block_config* cfg, int world, size_t* byte
   return DL_OK;
 }
 
-dl_status dl_decomposed_block_forward(const dl_block_config* cfg, const dl_block_weights* w, void* x_, int64_t T,
-                                      const int32_t* positions, const int32_t* cu_seqlens, int32_t num_seqs,
-                                      dl_phase phase, void* k_cache, void* v_cache, const int32_t* cache_lens,
-                                      int64_t max_seq, dl_comm comm, void* workspace, size_t workspace_bytes,
-                                      void* stream) {
+namespace {
+dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights* w, void* x_, int64_t T,
+                             const int32_t* positions, const int32_t* cu_seqlens, int32_t num_seqs, dl_phase phase,
+                             void* k_cache, void* v_cache, const int32_t* cache_lens, int64_t max_seq, dl_comm comm,
+                             void* workspace, size_t workspace_bytes, void* stream, const dl_kv_lowrank* kv) {
   const int P = comm ? comm->world : 1;
   BlockDims d;
   DL_TRY(block_dims(cfg, P, &d));
@@ -888,8 +960,10 @@ dl_status dl_decomposed_block_forward(const dl_block_config* cfg, const dl_block
     return DL_ERR_INVALID_ARG;
   }
   DL_TRY(check_ptr(x_, "x"));
-  DL_TRY(check_ptr(k_cache, "k_cache"));
-  DL_TRY(check_ptr(v_cache, "v_cache"));
+  if (!kv) {
+    DL_TRY(check_ptr(k_cache, "k_cache"));
+    DL_TRY(check_ptr(v_cache, "v_cache"));
+  }
   DL_TRY(check_ptr(w->attn_norm, "attn_norm"));
   DL_TRY(check_ptr(w->mlp_norm, "mlp_norm"));
   int64_t kq, ko, kg, kd;
@@ -934,6 +1008,24 @@ dl_status dl_decomposed_block_forward(const dl_block_config* cfg, const dl_block
   // TP code path is exercised on a single GPU.
   static const bool force_tp = getenv("DL_FORCE_TP_PATH") && atoi(getenv("DL_FORCE_TP_PATH")) != 0;
   const bool tp = comm && (P > 1 || force_tp);
+  if (kv) {
+    if (phase != DL_DECODE || !skinny) {
+      set_error("low-rank KV cache: decode only (T <= 256)");
+      return DL_ERR_INVALID_ARG;
+    }
+    if (tp && d.layout != DL_LAYOUT_DEINFER) {
+      set_error("low-rank KV cache needs the full latent: TP = 1 or DL_LAYOUT_DEINFER");
+      return DL_ERR_UNSUPPORTED;
+    }
+    const int64_t zv_need = rup(w->qkv.seg[1].k, 64) + w->qkv.seg[2].k;
+    if (!kv->pool || !kv->slot_pos || !kv->block_tables || !kv->run_src || !kv->run_dst || !kv->run_len ||
+        !kv->n_runs || !kv->seq_block || !kv->squeeze || !kv->squeeze_pos || !kv->recon || kv->block_size < 1 ||
+        kv->cap_blocks < 1 || kv->max_blocks_per_seq < 1 || kv->ld_slot % 8 || kv->ld_slot < zv_need ||
+        (kv->block_size * kv->ld_slot) % 8) {
+      set_error("dl_kv_lowrank: missing buffer or bad sizes (ld_slot >= rup(l_k, 64) + l_v, multiple of 8)");
+      return DL_ERR_INVALID_ARG;
+    }
+  }
   const int64_t qkv_rows[3] = {d.h, d.hkv, d.hkv};
   const int64_t gu_rows[2] = {d.m, d.m};
   const int64_t h_rows[1] = {d.h};
@@ -1010,18 +1102,22 @@ dl_status dl_decomposed_block_forward(const dl_block_config* cfg, const dl_block
     const int64_t m_loc = d.m / P, ngu_loc = n_gu * m_loc;
     const int64_t gu_loc[2] = {m_loc, m_loc};
     DL_TRY(launch_rmsnorm(x, static_cast<const __nv_bfloat16*>(w->attn_norm), ws.xn, T, d.h, cfg->rms_eps, st));
-    const GemmOut qo = skinny ? out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0) : out_plain(ws.yb, d.W, OUT_BF16, 0);
-    DL_TRY(deinfer_first(w->qkv, 3, qkv_loc, ws.xn, d.h, d.h, T, skinny, ws, d, comm, qo, st));
-    if (skinny) {
-      rc.acc = ws.yf;
-      rc.ld_src = ws.ldy32;
-      rc.clear = 1;
+    if (kv) {
+      DL_TRY(kvlr_attention(cfg, d, w, ws, kv, T, positions, cache_lens, true, comm, aa, rc, st));
     } else {
-      rc.src = ws.yb;
-      rc.ld_src = d.W;
+      const GemmOut qo = skinny ? out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0) : out_plain(ws.yb, d.W, OUT_BF16, 0);
+      DL_TRY(deinfer_first(w->qkv, 3, qkv_loc, ws.xn, d.h, d.h, T, skinny, ws, d, comm, qo, st));
+      if (skinny) {
+        rc.acc = ws.yf;
+        rc.ld_src = ws.ldy32;
+        rc.clear = 1;
+      } else {
+        rc.src = ws.yb;
+        rc.ld_src = d.W;
+      }
+      DL_TRY(launch_rope_cache(rc, st));
+      DL_TRY(launch_attention(aa, st));
     }
-    DL_TRY(launch_rope_cache(rc, st));
-    DL_TRY(launch_attention(aa, st));
     DL_TRY(deinfer_second(w->o, ws.att, d.h / P, d.h, T, skinny, ws, comm, x, st));
     DL_TRY(launch_rmsnorm(x, static_cast<const __nv_bfloat16*>(w->mlp_norm), ws.xn, T, d.h, cfg->rms_eps, st));
     const GemmOut go = skinny ? out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0) : out_plain(ws.yb, ngu_loc, OUT_BF16, 0);
@@ -1037,7 +1133,9 @@ dl_status dl_decomposed_block_forward(const dl_block_config* cfg, const dl_block
   }
 
   DL_TRY(launch_rmsnorm(x, static_cast<const __nv_bfloat16*>(w->attn_norm), ws.xn, T, d.h, cfg->rms_eps, st));
-  if (fx) {
+  if (kv) {
+    DL_TRY(kvlr_attention(cfg, d, w, ws, kv, T, positions, cache_lens, false, comm, aa, rc, st));
+  } else if (fx) {
     GemmFixup f = fixup(FIX_ROPE_CACHE);
     f.rope = rc;
     DL_TRY(run_group(w->qkv, 3, qkv_rows, ws.xn, d.h, d.h, T, skinny, ws, qkv_out, st, &f));
@@ -1045,8 +1143,8 @@ dl_status dl_decomposed_block_forward(const dl_block_config* cfg, const dl_block
     DL_TRY(run_group(w->qkv, 3, qkv_rows, ws.xn, d.h, d.h, T, skinny, ws, qkv_out, st));
   }
 
-  if (fx) {
-    // RoPE + cache append done by the q|k|v stage-2 fixup
+  if (fx || kv) {
+    // RoPE + cache append done by the q|k|v stage-2 fixup / low-rank KV path
   } else if (!tp) {
     if (skinny) {
       rc.acc = ws.yf;
@@ -1062,9 +1160,9 @@ dl_status dl_decomposed_block_forward(const dl_block_config* cfg, const dl_block
     rc.src = ws.rs;
     rc.ld_src = d.W;
   }
-  if (!fx) DL_TRY(launch_rope_cache(rc, st));
+  if (!fx && !kv) DL_TRY(launch_rope_cache(rc, st));
 
-  DL_TRY(launch_attention(aa, st));
+  if (!kv) DL_TRY(launch_attention(aa, st));
 
   const __nv_bfloat16* att_in = ws.att;
   if (tp) {
@@ -1113,6 +1211,73 @@ dl_status dl_decomposed_block_forward(const dl_block_config* cfg, const dl_block
   }
   DL_TRY(run_group(w->down, 1, h_rows, ws.act, d.m, d.m, T, skinny, ws, resid_out(), st, &fres));
   if (!fx) DL_TRY(finish_residual(d.h));
+  return DL_OK;
+}
+}  // namespace
+
+dl_status dl_decomposed_block_forward(const dl_block_config* cfg, const dl_block_weights* w, void* x_, int64_t T,
+                                      const int32_t* positions, const int32_t* cu_seqlens, int32_t num_seqs,
+                                      dl_phase phase, void* k_cache, void* v_cache, const int32_t* cache_lens,
+                                      int64_t max_seq, dl_comm comm, void* workspace, size_t workspace_bytes,
+                                      void* stream) {
+  return block_forward_impl(cfg, w, x_, T, positions, cu_seqlens, num_seqs, phase, k_cache, v_cache, cache_lens,
+                            max_seq, comm, workspace, workspace_bytes, stream, nullptr);
+}
+
+dl_status dl_decomposed_block_forward_kvlr(const dl_block_config* cfg, const dl_block_weights* w, void* x, int64_t T,
+                                           const int32_t* positions, const dl_kv_lowrank* kv,
+                                           const int32_t* cache_lens, dl_comm comm, void* workspace,
+                                           size_t workspace_bytes, void* stream) {
+  if (!kv) {
+    set_error("kv is NULL");
+    return DL_ERR_INVALID_ARG;
+  }
+  return block_forward_impl(cfg, w, x, T, positions, nullptr, static_cast<int32_t>(T), DL_DECODE, nullptr, nullptr,
+                            cache_lens, 1, comm, workspace, workspace_bytes, stream, kv);
+}
+
+dl_status dl_kv_prepare(const int32_t* block_tables, int64_t max_blocks_per_seq, const int32_t* seq_tokens,
+                        int32_t num_seqs, int64_t block_size, int64_t max_runs, int64_t cap_blocks, int32_t* run_src,
+                        int32_t* run_dst, int32_t* run_len, int32_t* n_runs, int32_t* seq_block) {
+  if (!block_tables || !seq_tokens || !run_src || !run_dst || !run_len || !n_runs || !seq_block || num_seqs < 0 ||
+      block_size < 1 || max_blocks_per_seq < 1) {
+    set_error("dl_kv_prepare: bad arguments");
+    return DL_ERR_SHAPE;
+  }
+  int64_t nr = 0, dst = 0;
+  for (int32_t s = 0; s < num_seqs; ++s) {
+    const int64_t nblk = (static_cast<int64_t>(seq_tokens[s]) + block_size - 1) / block_size;
+    if (seq_tokens[s] < 0 || nblk > max_blocks_per_seq) {
+      set_error("dl_kv_prepare: sequence %d has %d tokens (max %lld blocks)", s, seq_tokens[s],
+                (long long)max_blocks_per_seq);
+      return DL_ERR_SHAPE;
+    }
+    seq_block[s] = static_cast<int32_t>(dst);     // remapping index list: consecutive buffer blocks
+    const int32_t* row = block_tables + static_cast<int64_t>(s) * max_blocks_per_seq;
+    for (int64_t i = 0; i < nblk; ++i) {
+      if (row[i] < 0) {
+        set_error("dl_kv_prepare: negative block id");
+        return DL_ERR_SHAPE;
+      }
+      if (i == 0 || row[i] != row[i - 1] + 1) {    // a new physically contiguous run
+        if (nr == max_runs) {
+          set_error("dl_kv_prepare: more than max_runs = %lld runs", (long long)max_runs);
+          return DL_ERR_WORKSPACE;
+        }
+        run_src[nr] = row[i];
+        run_dst[nr] = static_cast<int32_t>(dst + i);
+        run_len[nr] = 0;
+        ++nr;
+      }
+      run_len[nr - 1] += 1;
+    }
+    dst += nblk;
+  }
+  if (dst > cap_blocks) {
+    set_error("dl_kv_prepare: %lld blocks exceed the buffer capacity %lld", (long long)dst, (long long)cap_blocks);
+    return DL_ERR_WORKSPACE;
+  }
+  *n_runs = static_cast<int32_t>(nr);
   return DL_OK;
 }
 // ---------------------------------------------------------------------------

@@ -266,7 +266,12 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, int splits
   const int64_t k_end = min64(n_keys, k_begin + chunk_keys);
   const int64_t ldq = static_cast<int64_t>(a.Hq) * D;
   const __nv_bfloat16* Qg = a.q + static_cast<int64_t>(s) * ldq + static_cast<int64_t>(h0) * D;
-  const int64_t kvoff = (static_cast<int64_t>(s) * a.Hk + kvh) * a.max_seq * D;
+  // key row stride: head-major cache rows are D apart; the low-rank-KV
+  // reconstruction buffer is token-major [row][K | V] (kv_ld), sequence s
+  // starting at buffer row kv_blk0[s] * kv_bs (the remapping index list)
+  const int64_t ldkv = a.kv_ld ? a.kv_ld : D;
+  const int64_t kvoff = a.kv_ld ? static_cast<int64_t>(a.kv_blk0[s]) * a.kv_bs * a.kv_ld + static_cast<int64_t>(kvh) * D
+                                : (static_cast<int64_t>(s) * a.Hk + kvh) * a.max_seq * D;
   const __nv_bfloat16* Kg = a.k_cache + kvoff;
   const __nv_bfloat16* Vg = a.v_cache + kvoff;
 
@@ -280,8 +285,8 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, int splits
   load_tile(sQ, Qg, D, 16, G, tid, 128);   // head r of the group at Qg + r*D
   if (n_kt > 0) {
     const int nv = static_cast<int>(min64(KT, k_end - k_begin));
-    load_tile(sK0, Kg + k_begin * D, D, KT, nv, tid, 128);
-    load_tile(sV0, Vg + k_begin * D, D, KT, nv, tid, 128);
+    load_tile(sK0, Kg + k_begin * ldkv, ldkv, KT, nv, tid, 128);
+    load_tile(sV0, Vg + k_begin * ldkv, ldkv, KT, nv, tid, 128);
   }
   cp_commit();
 
@@ -297,8 +302,8 @@ __global__ void __launch_bounds__(128) attn_decode_kernel(AttnArgs a, int splits
     if (kt + 1 < n_kt) {
       const int64_t k1 = k_begin + static_cast<int64_t>(kt + 1) * KT;
       const int nv = static_cast<int>(min64(KT, k_end - k1));
-      load_tile(sK0 + (buf ^ 1) * TILE_BYTES, Kg + k1 * D, D, KT, nv, tid, 128);
-      load_tile(sV0 + (buf ^ 1) * TILE_BYTES, Vg + k1 * D, D, KT, nv, tid, 128);
+      load_tile(sK0 + (buf ^ 1) * TILE_BYTES, Kg + k1 * ldkv, ldkv, KT, nv, tid, 128);
+      load_tile(sV0 + (buf ^ 1) * TILE_BYTES, Vg + k1 * ldkv, ldkv, KT, nv, tid, 128);
     }
     cp_commit();
     cp_wait<1>();
@@ -454,6 +459,10 @@ size_t attention_workspace(int64_t max_tokens, int Hq, int d) {
 
 dl_status launch_attention(const AttnArgs& a, cudaStream_t st) {
   if (a.T <= 0) return DL_OK;
+  if (a.kv_ld && (!a.decode || !a.kv_blk0 || a.kv_bs < 1 || a.kv_ld % 8)) {
+    set_error("attention: token-major K/V (kv_ld) is a decode-only layout with a block map");
+    return DL_ERR_INVALID_ARG;
+  }
   if (a.d != D || a.Hk < 1 || a.Hq % a.Hk != 0) {
     set_error("attention: head_dim %d / heads %d:%d unsupported (d = 128, Hq %% Hk == 0)", a.d, a.Hq, a.Hk);
     return DL_ERR_UNSUPPORTED;

@@ -191,6 +191,22 @@ struct LatentMap {
 };
 dl_status launch_latent_unpermute(const __nv_bfloat16* recv, __nv_bfloat16* zb, int64_t ldzb,
                                   const LatentMap& mp, cudaStream_t st);
+// Low-rank KV cache (N3).  append: latent row zb[t][zoff .. zoff + ncopy) of
+// decode token t -> pool slot of (seq t, position cache_lens[t]) through the
+// block table; slot_pos[slot] = positions[t].
+dl_status launch_kv_append(const __nv_bfloat16* zb, int64_t ldzb, int64_t zoff, int64_t ncopy,
+                           __nv_bfloat16* pool, int64_t ld_slot, int32_t* slot_pos, int64_t block_size,
+                           const int32_t* block_tables, int64_t max_blocks_per_seq, const int32_t* cache_lens,
+                           const int32_t* positions, int64_t T, cudaStream_t st);
+// squeeze: copy the contiguous runs (device plan) of the pool into the
+// compact buffer, whole blocks (rows of ld_slot bf16 + positions)
+dl_status launch_kv_squeeze(const __nv_bfloat16* pool, const int32_t* slot_pos, __nv_bfloat16* squeeze,
+                            int32_t* squeeze_pos, int64_t ld_slot, int64_t block_size, const int32_t* run_src,
+                            const int32_t* run_dst, const int32_t* run_len, const int32_t* n_runs,
+                            int64_t cap_blocks, cudaStream_t st);
+// in-place RoPE of the first `heads` 128-wide heads of each row (positions pos[row])
+dl_status launch_rope_rows(__nv_bfloat16* buf, int64_t ld, int heads, const int32_t* pos, int64_t rows, float theta,
+                           cudaStream_t st);
 dl_status launch_copy2d(const void* src, int64_t lds, void* dst, int64_t ldd,
                         int64_t rows, int64_t cols_bytes, cudaStream_t st);
 
@@ -204,6 +220,9 @@ struct AttnArgs {
   const int32_t* cu_seqlens; const int32_t* cache_lens; int32_t num_seqs;
   int64_t T; int Hq, Hk, d; int decode;
   float* partial; size_t partial_bytes;   // split-KV scratch (decode)
+  // decode only: kv_ld != 0 -> K/V rows are token-major with stride kv_ld
+  // (elements); sequence s starts at row kv_blk0[s] * kv_bs; kv head g at +g*d
+  int64_t kv_ld; const int32_t* kv_blk0; int64_t kv_bs;
 };
 dl_status launch_attention(const AttnArgs& a, cudaStream_t st);
 size_t attention_workspace(int64_t max_tokens, int Hq, int d);

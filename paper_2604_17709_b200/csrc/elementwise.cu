@@ -10,6 +10,8 @@
 // All kernels are PDL-aware (see dl_internal.h).
 #include <math.h>
 
+#include <algorithm>
+
 #include "dl_internal.h"
 
 namespace dl {
@@ -263,7 +265,106 @@ __global__ void __launch_bounds__(256) latent_unpermute_kernel(const __nv_bfloat
   zb[t * ldzb + col] = v;
 }
 
+// ---- low-rank KV cache (N3) ------------------------------------------------
+// grid T, 128 threads: one decode token per CTA, 16-byte copies.
+__global__ void __launch_bounds__(128) kv_append_kernel(const __nv_bfloat16* __restrict__ zb, int64_t ldzb,
+                                                        int64_t zoff, int n8, __nv_bfloat16* __restrict__ pool,
+                                                        int64_t ld_slot, int32_t* __restrict__ slot_pos, int64_t bs,
+                                                        const int32_t* __restrict__ tables, int64_t mbps,
+                                                        const int32_t* __restrict__ cache_lens,
+                                                        const int32_t* __restrict__ positions) {
+  pdl_trigger();   // successor may launch now; it waits for us before reading
+  pdl_wait();
+  const int64_t t = blockIdx.x;
+  const int64_t p = cache_lens[t];
+  const int64_t slot = static_cast<int64_t>(tables[t * mbps + p / bs]) * bs + p % bs;
+  const uint4* src = reinterpret_cast<const uint4*>(zb + t * ldzb + zoff);
+  uint4* dst = reinterpret_cast<uint4*>(pool + slot * ld_slot);
+  for (int i = threadIdx.x; i < n8; i += blockDim.x) dst[i] = src[i];
+  if (threadIdx.x == 0) slot_pos[slot] = positions[t];
+}
+
+// Squeeze ("the physically contiguous KV caches are sequentially copied
+// to the buffer"): buffer block b belongs to the run r with run_dst[r] <= b <
+// run_dst[r] + run_len[r] (run_dst ascending); CTAs stride over buffer blocks.
+__global__ void __launch_bounds__(256) kv_squeeze_kernel(const __nv_bfloat16* __restrict__ pool,
+                                                         const int32_t* __restrict__ slot_pos,
+                                                         __nv_bfloat16* __restrict__ squeeze,
+                                                         int32_t* __restrict__ squeeze_pos, int64_t ld_slot, int64_t bs,
+                                                         const int32_t* __restrict__ run_src,
+                                                         const int32_t* __restrict__ run_dst,
+                                                         const int32_t* __restrict__ run_len,
+                                                         const int32_t* __restrict__ n_runs_p, int64_t cap_blocks) {
+  pdl_trigger();   // successor may launch now; it waits for us before reading
+  pdl_wait();
+  const int n_runs = *n_runs_p;
+  if (n_runs <= 0) return;
+  const int64_t total = static_cast<int64_t>(run_dst[n_runs - 1]) + run_len[n_runs - 1];
+  const int64_t blk8 = bs * ld_slot / 8;     // uint4 per block
+  for (int64_t b = blockIdx.x; b < total && b < cap_blocks; b += gridDim.x) {
+    int lo = 0, hi = n_runs - 1;              // last run with run_dst <= b
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (run_dst[mid] <= b) lo = mid; else hi = mid - 1;
+    }
+    const int64_t src_blk = run_src[lo] + (b - run_dst[lo]);
+    const uint4* s4 = reinterpret_cast<const uint4*>(pool + src_blk * bs * ld_slot);
+    uint4* d4 = reinterpret_cast<uint4*>(squeeze + b * bs * ld_slot);
+    for (int64_t i = threadIdx.x; i < blk8; i += blockDim.x) d4[i] = s4[i];
+    for (int64_t i = threadIdx.x; i < bs; i += blockDim.x) squeeze_pos[b * bs + i] = slot_pos[src_blk * bs + i];
+  }
+}
+
+// in-place RoPE on reconstructed key rows ("in-place rotary position embedding
+// kernel ... to the reconstruction results").  grid (ceil(heads*32/128), rows)
+__global__ void __launch_bounds__(128) rope_rows_kernel(__nv_bfloat16* __restrict__ buf, int64_t ld, int heads,
+                                                        const int32_t* __restrict__ pos, int64_t rows, float theta) {
+  pdl_trigger();   // successor may launch now; it waits for us before reading
+  pdl_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= heads * 32) return;
+  const int e = (i & 31) * 4;
+  const float l2t = log2f(theta);
+  const float f0 = exp2f(-l2t * static_cast<float>(e) / 128.f), f1 = exp2f(-l2t * static_cast<float>(e + 2) / 128.f);
+  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    __nv_bfloat16* p = buf + r * ld + static_cast<int64_t>(i >> 5) * 128 + e;
+    const float4 v = load4(p);
+    const float fp = static_cast<float>(pos[r]);
+    float sn0, cs0, sn1, cs1;
+    sincosf(fp * f0, &sn0, &cs0);
+    sincosf(fp * f1, &sn1, &cs1);
+    store4(p, v.x * cs0 - v.y * sn0, v.x * sn0 + v.y * cs0, v.z * cs1 - v.w * sn1, v.z * sn1 + v.w * cs1);
+  }
+}
+
 }  // namespace
+
+dl_status launch_kv_append(const __nv_bfloat16* zb, int64_t ldzb, int64_t zoff, int64_t ncopy, __nv_bfloat16* pool,
+                           int64_t ld_slot, int32_t* slot_pos, int64_t block_size, const int32_t* block_tables,
+                           int64_t max_blocks_per_seq, const int32_t* cache_lens, const int32_t* positions, int64_t T,
+                           cudaStream_t st) {
+  if (T <= 0) return DL_OK;
+  const int n8 = static_cast<int>((ncopy + 7) / 8);
+  return launch_pdl(kv_append_kernel, dim3(static_cast<unsigned>(T)), dim3(128), 0, st, "kv_append", zb, ldzb, zoff,
+                    n8, pool, ld_slot, slot_pos, block_size, block_tables, max_blocks_per_seq, cache_lens, positions);
+}
+
+dl_status launch_kv_squeeze(const __nv_bfloat16* pool, const int32_t* slot_pos, __nv_bfloat16* squeeze,
+                            int32_t* squeeze_pos, int64_t ld_slot, int64_t block_size, const int32_t* run_src,
+                            const int32_t* run_dst, const int32_t* run_len, const int32_t* n_runs, int64_t cap_blocks,
+                            cudaStream_t st) {
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(cap_blocks, 8LL * num_sms()));
+  if (grid == 0) return DL_OK;
+  return launch_pdl(kv_squeeze_kernel, dim3(grid), dim3(256), 0, st, "kv_squeeze", pool, slot_pos, squeeze,
+                    squeeze_pos, ld_slot, block_size, run_src, run_dst, run_len, n_runs, cap_blocks);
+}
+
+dl_status launch_rope_rows(__nv_bfloat16* buf, int64_t ld, int heads, const int32_t* pos, int64_t rows, float theta,
+                           cudaStream_t st) {
+  if (rows <= 0 || heads <= 0) return DL_OK;
+  dim3 grid((heads * 32 + 127) / 128, static_cast<unsigned>(std::min<int64_t>(rows, 16384)));
+  return launch_pdl(rope_rows_kernel, grid, dim3(128), 0, st, "rope_rows", buf, ld, heads, pos, rows, theta);
+}
 
 dl_status launch_latent_unpermute(const __nv_bfloat16* recv, __nv_bfloat16* zb, int64_t ldzb, const LatentMap& mp,
                                   cudaStream_t st) {

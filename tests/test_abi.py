@@ -8,6 +8,7 @@ import ctypes
 import os
 import re
 
+import numpy as np
 import pytest
 import torch
 
@@ -169,3 +170,43 @@ def test_block_layout_validation(lib):
     with pytest.raises(lib.DLError) as e:
         lib.dl_block_workspace(bad, 2)
     assert e.value.name == "DL_ERR_PARTITION"
+
+
+def test_kv_prepare_matches_oracle_scan(lib, orc):
+    """Preparation stage of the low-rank KV cache: the library's host planner
+    yields, per sequence, the oracle's contiguous runs, placed at consecutive buffer
+    blocks (remapping index list = prefix sums of block counts)."""
+    r = np.random.default_rng(7)
+    bs, mbps, ns = 16, 6, 5
+    for _ in range(20):
+        perm = r.permutation(64).astype(np.int32)
+        tables = np.full((ns, mbps), -1, np.int32)
+        toks = r.integers(0, mbps * bs + 1, ns).astype(np.int32)
+        k = 0
+        for s in range(ns):
+            nb = -(-int(toks[s]) // bs)
+            if r.random() < 0.5:                      # some sequences physically contiguous
+                start = int(r.integers(100, 200))
+                tables[s, :nb] = np.arange(start, start + nb)
+            else:
+                tables[s, :nb] = perm[k:k + nb]
+                k += nb
+        rs, rd, rl, nr, sb = lib.dl_kv_prepare(tables, toks, bs, 64, 64)
+        got = list(zip(rs[:nr].tolist(), rl[:nr].tolist()))
+        exp, dst, exp_dst = [], 0, []
+        for s in range(ns):
+            nb = -(-int(toks[s]) // bs)
+            assert sb[s] == dst
+            runs = orc.kv_runs(tables[s, :nb])
+            for (st, ln) in runs:
+                exp_dst.append(dst)
+                dst += ln
+            exp += runs
+        assert got == exp
+        assert rd[:nr].tolist() == exp_dst
+    with pytest.raises(lib.DLError) as e:                 # over the buffer capacity
+        lib.dl_kv_prepare(np.arange(12, dtype=np.int32).reshape(2, 6), [96, 96], 16, 8, 11)
+    assert e.value.name == "DL_ERR_WORKSPACE"
+    with pytest.raises(lib.DLError) as e:                 # over max_runs
+        lib.dl_kv_prepare(np.array([[0, 2, 4, 6]], np.int32), [64], 16, 3, 8)
+    assert e.value.name == "DL_ERR_WORKSPACE"

@@ -337,3 +337,64 @@ def test_model_decode_variadic_layer_ranks(dl, orc):
         x = torch.tensor(x)
     x0 = embed.cpu()[ids.long()].double()
     assert rel(model.x.cpu().double() - x0, (x - x0).numpy()) <= TOL_BF16
+
+
+# ---- low-rank KV cache (N3: P:111) -------------------------------------------
+def _kvlr_case(dl, orc, s, cache_lens, seed, block_size=16):
+    rk = block_ranks(s, 0.4)
+    w = gen_block_weights(s, rk, 0, seed)
+    S = len(cache_lens)
+    max_seq = max(cache_lens) + 1
+    lk, lv = rk["k"], rk["v"]
+    zk = gen_normal((S, max_seq, lk), 1.0, seed + 1, dtype=torch.bfloat16)
+    zv = gen_normal((S, max_seq, lv), 1.0, seed + 2, dtype=torch.bfloat16)
+    x = gen_normal((S, s.h), 1.0, seed + 3, dtype=torch.bfloat16)
+    mbps = -(-max_seq // block_size)
+    nblk = [-(-(L + 1) // block_size) for L in cache_lens]
+    num_blocks = sum(nblk) + 7
+    perm = np.random.default_rng(seed).permutation(num_blocks).astype(np.int32)
+    tables = np.zeros((S, mbps), np.int32)
+    k = 0
+    for b, nb in enumerate(nblk):
+        if b % 3 == 0:                                   # a physically contiguous sequence
+            tables[b, :nb] = np.sort(perm[k:k + nb])
+        else:
+            tables[b, :nb] = perm[k:k + nb]
+        k += nb
+    cap = sum(nblk) + 2
+    kv = dl.LowRankKVCache(lk, lv, s.n_kv_heads * s.head_dim, num_blocks, block_size, S, mbps, cap)
+    kv.block_tables.copy_(torch.from_numpy(tables))
+    pool = kv.pool.view(num_blocks, block_size, kv.ld_slot)
+    pos = kv.slot_pos.view(num_blocks, block_size)
+    for b, L in enumerate(cache_lens):                   # history latents into their slots
+        for p in range(L):
+            blk, off = tables[b, p // block_size], p % block_size
+            pool[blk, off, :lk] = zk[b, p].cuda()
+            pool[blk, off, kv.zv_off:kv.zv_off + lv] = zv[b, p].cuda()
+            pos[blk, off] = p
+    nr = kv.prepare(tables, [L + 1 for L in cache_lens])
+    cfg = dl.make_block_config(s, rk, max_tokens=S, max_seqs=S)
+    wdev = dl.BlockWeights({kk: v.cuda() for kk, v in w.items()})
+    ws = torch.zeros(dl.dl_block_workspace(cfg), dtype=torch.uint8, device="cuda")
+    cl = torch.tensor(cache_lens, dtype=torch.int32, device="cuda")
+    xd = x.cuda()
+    dl.dl_decomposed_block_forward_kvlr(cfg, wdev, xd, cl, kv, cl, None, ws)
+    torch.cuda.synchronize()
+    ref, zk_new, _ = orc.block_decode_lowrank(_oracle_cfg(orc, s, rk), w, x, zk, zv, cache_lens)
+    got_new = torch.stack([pool[tables[b, L // block_size], L % block_size, :lk] for b, L in
+                           enumerate(cache_lens)]).cpu()
+    return rel(xd.cpu().double() - x.double(), ref - x.double().numpy()), rel(got_new, zk_new), nr
+
+
+@pytest.mark.parametrize("name", ["small", "mha", "opt"])
+def test_lowrank_kv_decode_vs_oracle(dl, orc, name):
+    s = SMALL if name == "small" else VARIANT_SHAPES[name]
+    err, err_new, nr = _kvlr_case(dl, orc, s, [0, 5, 17, 40, 1, 63, 16, 100], seed=81)
+    assert nr > 8                                        # scrambled blocks -> several runs
+    assert err <= TOL_BF16 and err_new <= TOL_BF16, (err, err_new)
+
+
+def test_lowrank_kv_decode_batch64(dl, orc):
+    """Decode batch 64 (the bench's shape family) with ragged contexts."""
+    err, err_new, _ = _kvlr_case(dl, orc, SMALL, [(37 * i) % 130 for i in range(64)], seed=91)
+    assert err <= TOL_BF16 and err_new <= TOL_BF16, (err, err_new)
