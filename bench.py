@@ -46,6 +46,9 @@ def parse():
     p.add_argument("--layers", type=int, default=0, help="debug only: fewer layers (invalid for reporting)")
     p.add_argument("--layout", default="rp", choices=["rp", "deinfer"],
                    help="TP sharding layout: rank-parallel (north star) or DeInfer low-rank communication")
+    p.add_argument("--kv", default="full", choices=["full", "lowrank"],
+                   help="decode KV cache: post-RoPE K/V, or the paged low-rank (latent) cache with the "
+                        "two-stage reconstruction (P:111, P:219-237)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-seqs", type=int, default=64)
     return p.parse_args()
@@ -224,10 +227,18 @@ def main():
     final_norm = torch.ones(shape.h, dtype=torch.bfloat16, device=dev)
     model = DecomposedLlama(shape, ranks, layer_iter(), embed, final_norm, lm_head, batch=args.batch,
                             max_seq=args.ctx + 1, prefill_tokens=args.prefill_tokens, comm=comm, device=dev,
-                            layout=dl.DL_LAYOUT_DEINFER if args.layout == "deinfer" else dl.DL_LAYOUT_RANK_PARALLEL)
+                            layout=dl.DL_LAYOUT_DEINFER if args.layout == "deinfer" else dl.DL_LAYOUT_RANK_PARALLEL,
+                            kv=args.kv)
     # context: ctx tokens already cached per sequence (random K/V), fixed for every step
-    model.cache.normal_()
     model.cache_lens.fill_(args.ctx)
+    if args.kv == "lowrank":
+        for kvl in model.kv_layers:            # latent history N(0, 1), positions 0..ctx-1
+            kvl.pool.normal_()
+            kvl.slot_pos.copy_(torch.arange(kvl.slot_pos.numel(), device=dev, dtype=torch.int32)
+                               % (model.kv_layers[0].block_tables.shape[1] * kvl.block_size))
+        model.kv_prepare([args.ctx] * args.batch)      # preparation stage (host), before capture
+    else:
+        model.cache.normal_()
     g = torch.Generator(device=dev)
     g.manual_seed(7003)
     model.ids.copy_(torch.randint(0, shape.vocab, (args.batch,), generator=g, device=dev, dtype=torch.int32))
@@ -346,7 +357,8 @@ def main():
     # algorithmic bytes per decode step per GPU: factors + LM head + KV reads
     pl = (2 * shape.h * ranks["q"] + (shape.h + shape.h_kv) * (ranks["k"] + ranks["v"]) + 2 * shape.h * ranks["o"]
           + (shape.h + shape.m) * (ranks["gate"] + ranks["up"] + ranks["down"]))
-    step_bytes = (2 * (n_layers * pl + shape.vocab * shape.h) + args.batch * args.ctx * n_layers * 2 * shape.h_kv * 2) \
+    kv_row = 2 * shape.h_kv if args.kv == "full" else ranks["k"] + ranks["v"]   # cached elements per token
+    step_bytes = (2 * (n_layers * pl + shape.vocab * shape.h) + args.batch * args.ctx * n_layers * kv_row * 2) \
         / world
     if args.layout == "deinfer" and world > 1:   # A_o and A_down are replicated on every rank
         step_bytes += 2 * n_layers * shape.h * (ranks["o"] + ranks["down"]) * (1 - 1 / world)
@@ -408,6 +420,8 @@ def main():
                                        f"B={args.batch} ctx={args.ctx} (+ prefill {args.prefill_tokens})",
                            "global_batch": args.batch, "seq_len": args.ctx, "parallelism": f"tp{world}",
                            "tp_layout": "deinfer" if args.layout == "deinfer" else "rank-parallel",
+                           "kv_cache": "post-RoPE K/V" if args.kv == "full" else
+                           "paged low-rank latent, block 16, two-stage reconstruction",
                            "layers": n_layers, "ranks": ranks,
                            "l2": "inputs larger than L2 (weights+KV stream from HBM every step)",
                            "cuda_graph": True},

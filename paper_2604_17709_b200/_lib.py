@@ -383,9 +383,9 @@ class LowRankKVCache:
         self.ld_slot = _pad8(self.zv_off + l_v)
         self.pool = torch.zeros(num_blocks * block_size, self.ld_slot, dtype=torch.bfloat16, device=dev)
         self.slot_pos = torch.zeros(num_blocks * block_size, dtype=torch.int32, device=dev)
-        self.block_tables = torch.zeros(max_seqs, max_blocks_per_seq, dtype=torch.int32, device=dev)
-        self.max_runs = max_runs or max_seqs * max_blocks_per_seq
         if shared is None:
+            self.block_tables = torch.zeros(max_seqs, max_blocks_per_seq, dtype=torch.int32, device=dev)
+            self.max_runs = max_runs or max_seqs * max_blocks_per_seq
             self.run_src = torch.zeros(self.max_runs, dtype=torch.int32, device=dev)
             self.run_dst = torch.zeros_like(self.run_src)
             self.run_len = torch.zeros_like(self.run_src)
@@ -396,7 +396,10 @@ class LowRankKVCache:
             self.squeeze_pos = torch.zeros(rows, dtype=torch.int32, device=dev)
             self.recon = torch.zeros(rows, 2 * hkv_local, dtype=torch.bfloat16, device=dev)
         else:
-            for k in ("run_src", "run_dst", "run_len", "n_runs", "seq_block", "squeeze", "squeeze_pos", "recon"):
+            # one block table and one plan serve every layer (same allocation pattern);
+            # the squeeze / reconstruction buffers are per-step scratch
+            for k in ("run_src", "run_dst", "run_len", "n_runs", "seq_block", "squeeze", "squeeze_pos", "recon",
+                      "block_tables", "max_runs"):
                 setattr(self, k, getattr(shared, k))
         self.cap_blocks = cap_blocks
         self.c = dl_kv_lowrank(self.pool.data_ptr(), self.slot_pos.data_ptr(), num_blocks, block_size, self.ld_slot,

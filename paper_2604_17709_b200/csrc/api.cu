@@ -889,9 +889,18 @@ dl_status kvlr_attention(const dl_block_config* cfg, const BlockDims& d, const d
   pr.seg[1] = GemmSeg{g.seg[2].A, g.seg[2].lda, hkl, lv, hkl, zv_off};
   pr.n_feat = 2 * hkl;
   pr.out = out_plain(kv->recon, 2 * hkl, OUT_BF16, 0);
+  // 5. RoPE of the reconstructed keys with the stored positions ("in-place rotary
+  //    position embedding ... to the reconstruction results"), applied in
+  //    the reconstruction GEMM's epilogue; the separate in-place kernel is kept
+  //    for key widths the vectorised epilogue does not cover
+  const bool epi_rope = !cfg->no_rope && hkl % 128 == 0;
+  if (epi_rope) {
+    pr.out.rope_pos = kv->squeeze_pos;
+    pr.out.rope_end = hkl;
+    pr.out.rope_theta = cfg->rope_theta;
+  }
   DL_TRY(tc_gemm(pr, false, st));
-  // 5. in-place RoPE of the reconstructed keys (stored positions)
-  if (!cfg->no_rope)
+  if (!cfg->no_rope && !epi_rope)
     DL_TRY(launch_rope_rows(static_cast<__nv_bfloat16*>(kv->recon), 2 * hkl, static_cast<int>(d.Hk_loc),
                             kv->squeeze_pos, rows, cfg->rope_theta, st));
   // 6. q = z_q . A_q^T (local heads) + RoPE

@@ -110,6 +110,12 @@ struct GemmOut {
   int remap_cols;
   int64_t seg_col_off[3];
   int64_t seg_write_rows[3];
+  // whole-tile bf16 outputs only: rope_pos != null -> features [0, rope_end)
+  // are 128-wide heads rotated in the epilogue by rope_pos[token] (RoPE of
+  // reconstructed keys)
+  const int32_t* rope_pos;
+  int64_t rope_end;
+  float rope_theta;
 };
 
 struct GemmProblem {

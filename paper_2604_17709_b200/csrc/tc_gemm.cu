@@ -99,7 +99,28 @@ struct KArgs {
   __nv_bfloat16* act_out;    // FIX_SILU output [T x ld_act_out] (gate = seg 0, up = seg 1)
   long long ld_act_out;
   RopeCacheArgs rope;        // FIX_ROPE_CACHE (q|k|v segments, one 128-feature head per tile)
+  // epilogue RoPE of whole-tile bf16 outputs (GemmOut::rope_pos)
+  const int32_t* rope_pos;
+  int rope_end;
+  float rope_l2t;
 };
+
+// RoPE of 8 consecutive output features f..f+7 (4 pairs (2i, 2i+1) of a
+// 128-wide head) of token `tok`: angle = pos * theta^(-dim/128), the same
+// expression as rope_cache_kernel.
+__device__ __forceinline__ void rope8(const KArgs& a, int tok, int f, float* v) {
+  if (a.rope_pos == nullptr || f >= a.rope_end) return;
+  const float pos = static_cast<float>(a.rope_pos[tok]);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int dim = (f + 2 * e) & 127;
+    float sn, cs;
+    sincosf(pos * exp2f(-a.rope_l2t * static_cast<float>(dim) / 128.f), &sn, &cs);
+    const float x = v[2 * e], y = v[2 * e + 1];
+    v[2 * e] = x * cs - y * sn;
+    v[2 * e + 1] = x * sn + y * cs;
+  }
+}
 
 __device__ __forceinline__ long long acc_index(const KArgs& a, const KSeg& s, int tok, int f) {
   if (a.scatter_p <= 0) return static_cast<long long>(tok) * a.acc_ld + s.col_off + (f - s.feat_begin);
@@ -667,6 +688,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   float v[8];
 #pragma unroll
                   for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r[q * 8 + e]);
+                  rope8(a, tok, f0 + q * 8, v);
                   if (a.accumulate) {
                     uint4 old = *reinterpret_cast<const uint4*>(o + q * 8);
                     const __nv_bfloat162* ob = reinterpret_cast<const __nv_bfloat162*>(&old);
@@ -906,6 +928,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               float v[8];
 #pragma unroll
               for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r[q * 8 + e]);
+              rope8(a, tok, f0 + q * 8, v);
               if (a.accumulate) {
                 uint4 old = *reinterpret_cast<const uint4*>(o + q * 8);
                 const __nv_bfloat162* ob = reinterpret_cast<const __nv_bfloat162*>(&old);
@@ -1083,6 +1106,20 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   if (stream_k && dbg_tile_order) a.stream_k = 0;
   if (stream_k && dbg_nored) a.mode = OUT_F32_STORE;
   a.accumulate = p.out.accumulate;
+  a.rope_pos = p.out.rope_pos;
+  a.rope_end = static_cast<int>(p.out.rope_end);
+  a.rope_l2t = p.out.rope_pos ? log2f(p.out.rope_theta) : 0.f;
+  if (p.out.rope_pos) {
+    // the vectorised whole-tile epilogue applies it: bf16 plain output, 32-aligned
+    // feature range inside segment 0, no K-split tail, no stream-K
+    const bool ok = !stream_k && !SWAP && p.out.mode == OUT_BF16 && !p.out.accumulate && p.out.scatter_p == 0 &&
+                    p.tail_acc == nullptr && p.out.rope_end % 32 == 0 && p.seg[0].feat_begin == 0 &&
+                    p.out.rope_end <= p.seg[0].rows && p.out.ld % 8 == 0;
+    if (!ok) {
+      set_error("tc_gemm: epilogue RoPE needs a whole-tile bf16 output without tail split");
+      return DL_ERR_INVALID_ARG;
+    }
+  }
   a.scatter_p = p.out.scatter_p;
   a.slab = p.out.slab;
   a.trace_slot = g_trace_host_on ? g_trace_next++ : -1;

@@ -23,8 +23,11 @@ class DecomposedLlama:
 
     def __init__(self, shape, ranks: dict, layer_weights, embed: torch.Tensor, final_norm: torch.Tensor,
                  lm_head_local: torch.Tensor, batch: int, max_seq: int, prefill_tokens: int = 0,
-                 comm: L.Comm | None = None, device="cuda", layout: int = L.DL_LAYOUT_RANK_PARALLEL):
-        self.shape, self.ranks, self.comm, self.layout = shape, ranks, comm, layout
+                 comm: L.Comm | None = None, device="cuda", layout: int = L.DL_LAYOUT_RANK_PARALLEL,
+                 kv: str = "full", kv_block_size: int = 16):
+        """kv = "full": head-major post-RoPE K/V cache; "lowrank": paged latent cache
+         with the two-stage reconstruction (decode only; uniform ranks)."""
+        self.shape, self.ranks, self.comm, self.layout, self.kv_mode = shape, ranks, comm, layout, kv
         self.world = comm.world if comm else 1
         self.rank = comm.rank if comm else 0
         self.device = torch.device(device)
@@ -38,8 +41,24 @@ class DecomposedLlama:
         hk_loc = s.n_kv_heads // self.world
         nl = len(self.layers)
         bf = torch.bfloat16
-        self.cache = torch.zeros((nl, 2, batch, hk_loc, max_seq, s.head_dim), dtype=bf, device=self.device)
         per_layer = ranks if isinstance(ranks, (list, tuple)) else [ranks] * nl
+        if kv == "lowrank":
+            self.cache = None
+            bs = kv_block_size
+            mbps = -(-max_seq // bs)
+            nblocks = batch * mbps
+            self.kv_layers = []
+            for r in per_layer:
+                self.kv_layers.append(L.LowRankKVCache(r["k"], r["v"], hk_loc * s.head_dim, nblocks, bs, batch, mbps,
+                                                       cap_blocks=nblocks, device=self.device,
+                                                       shared=self.kv_layers[0] if self.kv_layers else None))
+            # default allocation: each sequence owns a contiguous range of blocks
+            self.kv_tables_host = torch.arange(nblocks, dtype=torch.int32).view(batch, mbps).numpy()
+            self.kv_layers[0].block_tables.copy_(torch.from_numpy(self.kv_tables_host))
+        elif kv == "full":
+            self.cache = torch.zeros((nl, 2, batch, hk_loc, max_seq, s.head_dim), dtype=bf, device=self.device)
+        else:
+            raise ValueError(f"kv mode {kv!r}")
         if len(per_layer) != nl:
             raise ValueError(f"{len(per_layer)} rank dicts for {nl} layers")
         # a workspace's layout is tied to its config (include/dl.h): one per distinct rank set
@@ -85,11 +104,23 @@ class DecomposedLlama:
             self.pre_xn = torch.zeros(1, s.h, dtype=bf, device=self.device)
             self.pre_logits = torch.zeros(1, vloc, dtype=bf, device=self.device)
 
+    def kv_prepare(self, cache_lens_host, tables_host=None):
+        """Preparation stage of the low-rank KV cache (host; outside the graph replay):
+        plan the squeeze of every sequence's blocks for a step appending at cache_lens."""
+        if tables_host is not None:
+            self.kv_tables_host = tables_host
+            self.kv_layers[0].block_tables.copy_(torch.as_tensor(tables_host, dtype=torch.int32))
+        return self.kv_layers[0].prepare(self.kv_tables_host, [int(c) + 1 for c in cache_lens_host])
+
     # one decode token for each of the `batch` sequences, at position cache_lens[b]
     def decode_step(self):
         s = self.shape
         L.dl_embedding(self.embed, self.ids, self.x)
-        for i, lw in enumerate(self.layers):
+        if self.kv_mode == "lowrank":
+            for i, lw in enumerate(self.layers):
+                L.dl_decomposed_block_forward_kvlr(self.dec_cfgs[i], lw, self.x, self.cache_lens, self.kv_layers[i],
+                                                   self.cache_lens, self.comm, self.dec_wss[i])
+        for i, lw in enumerate(self.layers if self.kv_mode == "full" else ()):
             L.dl_decomposed_block_forward(self.dec_cfgs[i], lw, self.x, self.cache_lens, None, self.batch, L.DL_DECODE,
                                           self.cache[i, 0], self.cache[i, 1], self.cache_lens, self.comm,
                                           self.dec_wss[i])
