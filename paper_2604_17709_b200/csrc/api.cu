@@ -1198,10 +1198,17 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   // ---- o projection + residual ----------------------------------------------
   const GemmFixup fres = fixup(fx ? FIX_RESIDUAL : FIX_NONE);
   DL_TRY(run_group(w->o, 1, h_rows, att_in, d.h, d.h, T, skinny, ws, resid_out(), st, &fres));
-  if (!fx) DL_TRY(finish_residual(d.h));
+  const __nv_bfloat16* mlp_norm = static_cast<const __nv_bfloat16*>(w->mlp_norm);
+  static const bool no_fuse = getenv("DL_NO_FUSE_RESNORM") != nullptr;   // A/B timing switch
+  if (!fx && !tp && skinny && !no_fuse) {
+    // residual add of the o projection fused with the MLP pre-norm
+    DL_TRY(launch_residual_rmsnorm(ws.yf, ws.ldy32, x, mlp_norm, ws.xn, T, d.h, cfg->rms_eps, st));
+  } else {
+    if (!fx) DL_TRY(finish_residual(d.h));
+    DL_TRY(launch_rmsnorm(x, mlp_norm, ws.xn, T, d.h, cfg->rms_eps, st));
+  }
 
   // ---- MLP: gate|up group, SiLU(gate)*up (or ReLU(up)), down + residual ---------
-  DL_TRY(launch_rmsnorm(x, static_cast<const __nv_bfloat16*>(w->mlp_norm), ws.xn, T, d.h, cfg->rms_eps, st));
   const int64_t ngu = n_gu * d.m;
   GemmOut gu_out = skinny ? out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0) : out_plain(ws.yb, ngu, OUT_BF16, 0);
   const bool fx_gu = fx && d.glu;

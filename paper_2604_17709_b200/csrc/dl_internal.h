@@ -165,6 +165,9 @@ dl_status launch_f32_to_bf16(float* acc, int64_t ld_acc, __nv_bfloat16* out,
 dl_status launch_residual_add_f32(float* acc, int64_t ld_acc, __nv_bfloat16* x,
                                   int64_t ldx, int64_t T, int64_t n,
                                   int clear, cudaStream_t st);
+// x[t][c] = bf16(x + acc) (acc cleared), then y = rmsnorm(x) * g   (h % 8 == 0)
+dl_status launch_residual_rmsnorm(float* acc, int64_t lda, __nv_bfloat16* x, const __nv_bfloat16* g,
+                                  __nv_bfloat16* y, int64_t T, int64_t h, float eps, cudaStream_t st);
 // x[t][c] = bf16(x + y)
 dl_status launch_residual_add_bf16(const __nv_bfloat16* y, int64_t ldy, __nv_bfloat16* x,
                                    int64_t ldx, int64_t T, int64_t n, cudaStream_t st);

@@ -69,6 +69,63 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const __nv_bfloat16* __res
   }
 }
 
+// x = bf16(x + acc) (acc consumed and cleared), then y = rmsnorm(x) * g: the
+// o-projection residual and the MLP pre-norm in one pass (one CTA per row).
+// The norm reads the bf16-rounded x, exactly as the two separate kernels did.
+__global__ void __launch_bounds__(512) residual_rmsnorm_kernel(float* __restrict__ acc, int64_t lda,
+                                                               __nv_bfloat16* __restrict__ x,
+                                                               const __nv_bfloat16* __restrict__ g,
+                                                               __nv_bfloat16* __restrict__ y, int h, float eps) {
+  pdl_trigger();   // successor may launch now; it waits for us before reading
+  pdl_wait();
+  __shared__ float red[16];
+  const int64_t t = blockIdx.x;
+  float* ar = acc + t * lda;
+  uint4* xr = reinterpret_cast<uint4*>(x + t * h);
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < h / 8; i += blockDim.x) {
+    float4 a0 = *reinterpret_cast<float4*>(ar + 8 * i), a1 = *reinterpret_cast<float4*>(ar + 8 * i + 4);
+    *reinterpret_cast<float4*>(ar + 8 * i) = make_float4(0.f, 0.f, 0.f, 0.f);
+    *reinterpret_cast<float4*>(ar + 8 * i + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint4 v = xr[i];
+    __nv_bfloat162* b = reinterpret_cast<__nv_bfloat162*>(&v);
+    const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float2 f = __bfloat1622float2(b[e]);
+      b[e] = __floats2bfloat162_rn(f.x + av[2 * e], f.y + av[2 * e + 1]);
+      f = __bfloat1622float2(b[e]);
+      ss += f.x * f.x + f.y * f.y;
+    }
+    xr[i] = v;
+  }
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float inv = rsqrtf(red[0] / static_cast<float>(h) + eps);
+  const uint4* gr = reinterpret_cast<const uint4*>(g);
+  uint4* yr = reinterpret_cast<uint4*>(y + t * h);
+  for (int i = threadIdx.x; i < h / 8; i += blockDim.x) {   // same indices: own writes
+    uint4 v = xr[i], gv = gr[i], o;
+    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v);
+    const __nv_bfloat162* gb = reinterpret_cast<const __nv_bfloat162*>(&gv);
+    __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float2 f = __bfloat1622float2(b[e]);
+      float2 w = __bfloat1622float2(gb[e]);
+      ob[e] = __floats2bfloat162_rn(f.x * inv * w.x, f.y * inv * w.y);
+    }
+    yr[i] = o;
+  }
+}
+
 // 2-D elementwise over [T x n] in groups of 4 columns: grid (ceil(n/4/256), T).
 template <typename F>
 __global__ void __launch_bounds__(256) ew4_kernel(int n4, F f) {
@@ -378,6 +435,12 @@ dl_status launch_rmsnorm(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bf
   if (T <= 0) return DL_OK;
   return launch_pdl(rmsnorm_kernel, dim3(static_cast<unsigned>(T)), dim3(256), 0, st, "rmsnorm", x, g, y,
                     static_cast<int>(h), eps);
+}
+dl_status launch_residual_rmsnorm(float* acc, int64_t lda, __nv_bfloat16* x, const __nv_bfloat16* g,
+                                  __nv_bfloat16* y, int64_t T, int64_t h, float eps, cudaStream_t st) {
+  if (T <= 0) return DL_OK;
+  return launch_pdl(residual_rmsnorm_kernel, dim3(static_cast<unsigned>(T)), dim3(512), 0, st, "residual_rmsnorm",
+                    acc, lda, x, g, y, static_cast<int>(h), eps);
 }
 dl_status launch_f32_to_bf16(float* acc, int64_t lda, __nv_bfloat16* out, int64_t ldo, int64_t T, int64_t n,
                              int clear, cudaStream_t st) {
