@@ -81,6 +81,13 @@ int dl_device_ok(void);
  * from the process (the NCCL that owns nccl_comm); DL_ERR_NCCL if absent.
  * ---------------------------------------------------------------------- */
 dl_status dl_comm_create(void *nccl_comm, int rank, int world, dl_comm *out);
+/* Measurement only: a communicator of `world` ranks on ONE GPU whose
+ * collectives are replaced by local copies of the same shapes (all-gather:
+ * this rank's slice into its slot; reduce-scatter: its slot; all-reduce:
+ * no-op).  Results are NOT the sharded result; the per-rank kernel work of a
+ * TP = world step is exact, so its compute time can be measured without
+ * world GPUs (tools/tp_emulate.py).                                        */
+dl_status dl_comm_create_loopback(int rank, int world, dl_comm *out);
 dl_status dl_comm_destroy(dl_comm comm);
 
 /* ------------------------------------------------------------------------

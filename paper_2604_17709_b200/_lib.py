@@ -24,7 +24,7 @@ EXPORTS = ("dl_last_error", "dl_version", "dl_device_ok", "dl_comm_create", "dl_
            "dl_block_workspace", "dl_decomposed_block_forward", "dl_embedding", "dl_rmsnorm",
            "dl_dense_workspace", "dl_dense", "dl_launch_count", "dl_profile_begin", "dl_profile_end",
            "dl_profile_count", "dl_profile_get", "dl_debug_gemm_trace", "dl_deinfer_shard_factors",
-           "dl_kv_prepare", "dl_decomposed_block_forward_kvlr")
+           "dl_kv_prepare", "dl_decomposed_block_forward_kvlr", "dl_comm_create_loopback")
 
 
 class DLError(RuntimeError):
@@ -105,6 +105,7 @@ def load():
             lib.dl_profile_get.argtypes = [I, P, P, P, P]
             lib.dl_debug_gemm_trace.argtypes = [P]
             lib.dl_deinfer_shard_factors.argtypes = [I, I, P, P, P, P, P, P, I64, I, I, I, P, I64, P, P, P]
+            lib.dl_comm_create_loopback.argtypes = [I, I, ctypes.POINTER(P)]
             lib.dl_kv_prepare.argtypes = [P, I64, P, I32, I64, I64, I64, P, P, P, P, P]
             lib.dl_decomposed_block_forward_kvlr.argtypes = [ctypes.POINTER(dl_block_config),
                                                              ctypes.POINTER(dl_block_weights), P, I64, P,
@@ -162,6 +163,7 @@ class Comm:
         _check(load().dl_comm_create(ctypes.c_void_p(nccl_comm_ptr), rank, world, ctypes.byref(h)))
         self.handle = h
         self.rank, self.world = rank, world
+        self.is_loopback = False
 
     @classmethod
     def from_process_group(cls, pg=None):
@@ -169,6 +171,17 @@ class Comm:
         pg = pg or dist.group.WORLD
         backend = pg._get_backend(torch.device("cuda"))
         return cls(backend._comm_ptr(), dist.get_rank(pg), dist.get_world_size(pg))
+
+    @classmethod
+    def loopback(cls, rank: int, world: int):
+        """Measurement-only communicator: TP=`world` shapes on one GPU, collectives
+        replaced by local copies (include/dl.h: dl_comm_create_loopback)."""
+        self = cls.__new__(cls)
+        h = P()
+        _check(load().dl_comm_create_loopback(rank, world, ctypes.byref(h)))
+        self.handle, self.rank, self.world = h, rank, world
+        self.is_loopback = True
+        return self
 
     def close(self):
         if self.handle:

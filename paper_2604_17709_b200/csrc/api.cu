@@ -67,6 +67,7 @@ typedef const char* (*nccl_errstr_fn)(int);
 struct dl_comm_s {
   void* nccl;
   int rank, world;
+  int loopback;   // measurement-only emulation: collectives become local copies
   nccl_allreduce_fn allreduce;
   nccl_reducescatter_fn reducescatter;
   nccl_allgather_fn allgather;
@@ -89,13 +90,26 @@ dl_status nccl_check(const dl_comm_s* c, int r, const char* what) {
   return DL_ERR_NCCL;
 }
 
+size_t nccl_esize(int dtype) { return dtype == kNcclFloat32 ? 4 : 2; }
+
 dl_status all_reduce(dl_comm c, void* buf, size_t count, int dtype, cudaStream_t st) {
+  if (c->loopback) return DL_OK;
   return nccl_check(c, c->allreduce(buf, buf, count, dtype, kNcclSum, c->nccl, st), "ncclAllReduce");
 }
 dl_status reduce_scatter(dl_comm c, const void* src, void* dst, size_t recv_count, int dtype, cudaStream_t st) {
+  if (c->loopback) {
+    const size_t b = recv_count * nccl_esize(dtype);
+    return cuda_status(cudaMemcpyAsync(dst, static_cast<const uint8_t*>(src) + c->rank * b, b,
+                                       cudaMemcpyDeviceToDevice, st), "loopback reduce-scatter");
+  }
   return nccl_check(c, c->reducescatter(src, dst, recv_count, dtype, kNcclSum, c->nccl, st), "ncclReduceScatter");
 }
 dl_status all_gather(dl_comm c, const void* src, void* dst, size_t send_count, int dtype, cudaStream_t st) {
+  if (c->loopback) {
+    const size_t b = send_count * nccl_esize(dtype);
+    return cuda_status(cudaMemcpyAsync(static_cast<uint8_t*>(dst) + c->rank * b, src, b, cudaMemcpyDeviceToDevice,
+                                       st), "loopback all-gather");
+  }
   return nccl_check(c, c->allgather(src, dst, send_count, dtype, c->nccl, st), "ncclAllGather");
 }
 
@@ -235,6 +249,19 @@ dl_status dl_comm_create(void* nccl_comm, int rank, int world, dl_comm* out) {
     set_error("dl_comm_create: NCCL symbols not found in the process");
     return DL_ERR_NCCL;
   }
+  *out = new dl_comm_s(c);
+  return DL_OK;
+}
+
+dl_status dl_comm_create_loopback(int rank, int world, dl_comm* out) {
+  if (!out || world < 1 || rank < 0 || rank >= world) {
+    set_error("dl_comm_create_loopback: bad arguments");
+    return DL_ERR_INVALID_ARG;
+  }
+  dl_comm_s c{};
+  c.rank = rank;
+  c.world = world;
+  c.loopback = 1;
   *out = new dl_comm_s(c);
   return DL_OK;
 }

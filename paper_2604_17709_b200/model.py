@@ -126,7 +126,9 @@ class DecomposedLlama:
                                           self.dec_wss[i])
         L.dl_rmsnorm(self.x, self.final_norm, self.xn, s.rms_eps)
         L.dl_dense(self.xn, self.lm_head, self.logits_local)
-        if self.world > 1:
+        if self.world > 1 and getattr(self.comm, "is_loopback", False):
+            self.logits[self.rank].copy_(self.logits_local)      # measurement-only emulation
+        elif self.world > 1:
             import torch.distributed as dist
             dist.all_gather_into_tensor(self.logits, self.logits_local)
         return self.logits_local if self.world == 1 else self.logits

@@ -24,6 +24,7 @@ m = DecomposedLlama(s, rk, (gen_block_weights(s, rk, 3, i, device=dev) for i in 
                     max_seq=513)
 m.cache.normal_()
 m.cache_lens.fill_(512)
+torch.cuda.synchronize()
 st = torch.cuda.Stream()
 with torch.cuda.stream(st):
     m.decode_step()
