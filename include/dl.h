@@ -392,6 +392,12 @@ dl_status dl_profile_get(int i, float *ms, double *bytes, double *flops,
  * done, first TMA issued, first stage landed, last MMA issued, epilogue
  * done, exit; slot 7 = SM id. */
 dl_status dl_debug_gemm_trace(void *device_buf);
+/* Debug timeline of the fused decode kernels (device_buf: >= 48 u64 per CTA
+ * per launch of the next launches, or NULL to disable).  Per launch slot and
+ * CTA: [2p] / [2p+1] globaltimer ns at which the CTA's epilogue warps started /
+ * finished phase p, [28+p] time the TMA producer issued phase p's activation
+ * loads, [46] entry, [47] SM id.  Slots are assigned in launch order. */
+dl_status dl_debug_fused_trace(void *device_buf);
 
 #ifdef __cplusplus
 }

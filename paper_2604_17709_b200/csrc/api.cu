@@ -616,6 +616,7 @@ struct BlockWs {
   size_t apart_bytes;
   unsigned int* sched;               // kSchedSlots x 2 stream-K work counters
   unsigned int* tile_cnt;            // stream-K fixup arrival counters (one per output tile)
+  unsigned int* fbar;                // fused decode: 2 x 16 phase-barrier counters (pre / post attention)
   float* tail;                       // prefill DP + stream-K tail scratch (zero-maintained)
   size_t tail_bytes;
   __nv_bfloat16 *lat_send, *lat_recv;   // DeInfer latent all-gather [T x slot] / [P][T][slot]
@@ -644,6 +645,7 @@ BlockWs carve_block(Carver& c, const BlockDims& d, int64_t Tmax) {
   w.apart = c.take<float>(w.apart_bytes / sizeof(float));
   w.sched = c.take<unsigned int>(2 * kSchedSlots);
   w.tile_cnt = c.take<unsigned int>(static_cast<size_t>((d.nmax + d.kmax) / 128 + 64));
+  w.fbar = c.take<unsigned int>(32);
   w.tail_bytes = Tmax > 256 ? kTailBytes : 0;
   w.tail = w.tail_bytes ? c.take<float>(w.tail_bytes / sizeof(float)) : nullptr;
   if (d.layout == DL_LAYOUT_DEINFER) {
@@ -952,6 +954,83 @@ dl_status kvlr_attention(const dl_block_config* cfg, const BlockDims& d, const d
 
 }  // namespace
 
+// Fused decode of one block at TP = 1 (decode_fused.cu): the pre-attention
+// half (RMSNorm, q|k|v chain, RoPE + cache append) and the post-attention half
+// (o chain + residual + MLP norm, gate|up chain, SiLU*up, down chain +
+// residual) each run as one persistent phase-program kernel; attention in
+// between.  Same arithmetic and rounding points as the per-kernel path.
+dl_status fused_block(const dl_block_config* cfg, const BlockDims& d, const dl_block_weights* w, __nv_bfloat16* x,
+                      int64_t T, const BlockWs& ws, RopeCacheArgs rc, const AttnArgs& aa, cudaStream_t st) {
+  const int64_t qkv_rows[3] = {d.h, d.hkv, d.hkv};
+  const int64_t gu_rows[2] = {d.m, d.m};
+  const int64_t h_rows[1] = {d.h};
+  const int n_gu = d.glu ? 2 : 1;
+  const float eps = cfg->rms_eps;
+  auto gemm = [](const GemmProblem& p) {
+    FusedStep s{};
+    s.kind = FK_GEMM;
+    s.gemm = p;
+    return s;
+  };
+  auto el = [](int kind, float* acc, int64_t lda, __nv_bfloat16* xx, const void* g, __nv_bfloat16* y, int64_t ldy,
+               int64_t n, float e) {
+    FusedStep s{};
+    s.kind = kind;
+    s.acc = acc;
+    s.lda = lda;
+    s.x = xx;
+    s.ldx = n;
+    s.g = static_cast<const __nv_bfloat16*>(g);
+    s.y = y;
+    s.ldy = ldy;
+    s.n = n;
+    s.eps = e;
+    return s;
+  };
+  const GemmOut zout = out_plain(ws.zf, ws.ldz32, OUT_F32_RED, 0);
+  const GemmOut yout = out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0);
+
+  FusedProgram a{};
+  a.T = T;
+  a.bar = ws.fbar;
+  rc.acc = ws.yf;
+  rc.ld_src = ws.ldy32;
+  rc.clear = 1;
+  a.rope = rc;
+  const ZLayout zq = zlayout(w->qkv, 3);
+  a.step[a.n++] = el(FK_RMSNORM, nullptr, 0, x, w->attn_norm, ws.xn, d.h, d.h, eps);
+  a.step[a.n++] = gemm(stage1(w->qkv, 3, ws.xn, d.h, T, d.h, zq, zout));
+  a.step[a.n++] = el(FK_CVT, ws.zf, ws.ldz32, nullptr, nullptr, ws.zb, ws.ldzb, zq.width, 0.f);
+  a.step[a.n++] = gemm(stage2(w->qkv, 3, qkv_rows, ws.zb, ws.ldzb, T, zq, yout));
+  a.step[a.n++] = el(FK_ROPE_CACHE, ws.yf, ws.ldy32, nullptr, nullptr, nullptr, 0, 0, 0.f);
+  DL_TRY(fused_decode(a, st));
+
+  DL_TRY(launch_attention(aa, st));
+
+  FusedProgram b{};
+  b.T = T;
+  b.bar = ws.fbar + 16;
+  const ZLayout zo = zlayout(w->o, 1), zg = zlayout(w->gu, n_gu), zd = zlayout(w->down, 1);
+  b.step[b.n++] = gemm(stage1(w->o, 1, ws.att, d.h, T, d.h, zo, zout));
+  b.step[b.n++] = el(FK_CVT, ws.zf, ws.ldz32, nullptr, nullptr, ws.zb, ws.ldzb, zo.width, 0.f);
+  b.step[b.n++] = gemm(stage2(w->o, 1, h_rows, ws.zb, ws.ldzb, T, zo, yout));
+  b.step[b.n++] = el(FK_RESID_RMSNORM, ws.yf, ws.ldy32, x, w->mlp_norm, ws.xn, d.h, d.h, eps);
+  b.step[b.n++] = gemm(stage1(w->gu, n_gu, ws.xn, d.h, T, d.h, zg, zout));
+  b.step[b.n++] = el(FK_CVT, ws.zf, ws.ldz32, nullptr, nullptr, ws.zb, ws.ldzb, zg.width, 0.f);
+  b.step[b.n++] = gemm(stage2(w->gu, n_gu, gu_rows, ws.zb, ws.ldzb, T, zg, yout));
+  b.step[b.n++] = el(d.glu ? FK_SILU : FK_RELU, ws.yf, ws.ldy32, nullptr, nullptr, ws.act, d.m, d.m, 0.f);
+  b.step[b.n++] = gemm(stage1(w->down, 1, ws.act, d.m, T, d.m, zd, zout));
+  b.step[b.n++] = el(FK_CVT, ws.zf, ws.ldz32, nullptr, nullptr, ws.zb, ws.ldzb, zd.width, 0.f);
+  b.step[b.n++] = gemm(stage2(w->down, 1, h_rows, ws.zb, ws.ldzb, T, zd, yout));
+  b.step[b.n++] = el(FK_RESID, ws.yf, ws.ldy32, x, nullptr, nullptr, 0, d.h, 0.f);
+  return fused_decode(b, st);
+}
+
+bool use_fused() {
+  static const bool on = getenv("DL_FUSED") && atoi(getenv("DL_FUSED")) != 0;   // opt-in while in development
+  return on;
+}
+
 dl_status dl_block_workspace(const dl_block_config* cfg, int world, size_t* bytes) {
   if (!bytes) {
     set_error("bytes is NULL");
@@ -1167,6 +1246,8 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
     }
     return deinfer_second(w->down, ws.act, m_loc, d.h, T, skinny, ws, comm, x, st);
   }
+
+  if (skinny && !tp && !kv && !fx && T <= 128 && d.h <= 8192 && d.m % 64 == 0 && use_fused()) return fused_block(cfg, d, w, x, T, ws, rc, aa, st);
 
   DL_TRY(launch_rmsnorm(x, static_cast<const __nv_bfloat16*>(w->attn_norm), ws.xn, T, d.h, cfg->rms_eps, st));
   if (kv) {

@@ -1,6 +1,7 @@
 // Internal interfaces between the C-ABI layer (api.cu) and the kernels.
 // Product code only: nothing here is shared with oracle/.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
@@ -142,6 +143,48 @@ dl_status tc_gemm(const GemmProblem& p, bool stream_k, cudaStream_t st);
 // (globaltimer ns at entry, setup done, first TMA, first stage landed, last
 // MMA issued, epilogue done, exit; and its SM id)
 dl_status set_gemm_trace(void* buf);
+
+// 2-D bf16 TMA map over a row-major [rows x cols] matrix (ld elements), box
+// {64 cols, box_rows}, 128B swizzle, out-of-bounds elements read as zero.
+bool encode_map_bf16(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows);
+
+// ---------------------------------------------------------------------------
+// Fused decode (decode_fused.cu): a list of phases run by one persistent
+// kernel with grid barriers between them (T <= 128).  GEMM phases are
+// GemmProblems with a plain OUT_F32_RED output (stream-K red.add into a
+// zero-maintained buffer); elementwise phases consume-and-clear fp32 buffers.
+// ---------------------------------------------------------------------------
+constexpr int kFusedMaxPhases = 14;
+constexpr int kFusedMaxGemm = 6;
+enum FusedKind {
+  FK_GEMM = 0,
+  FK_RMSNORM = 1,         // y = rmsnorm(x) * g                               [T x n]
+  FK_RESID_RMSNORM = 2,   // x = bf16(x + acc), acc cleared; y = rmsnorm(x) * g
+  FK_CVT = 3,             // y = bf16(acc), acc cleared                       [T x n]
+  FK_ROPE_CACHE = 4,      // FusedProgram::rope from acc (cleared)
+  FK_SILU = 5,            // y = silu(acc[:, :n]) * acc[:, n:2n], acc cleared
+  FK_RELU = 6,            // y = relu(acc[:, :n]), acc cleared
+  FK_RESID = 7,           // x = bf16(x + acc), acc cleared
+};
+struct FusedStep {
+  int kind;
+  GemmProblem gemm;
+  float* acc; int64_t lda;
+  __nv_bfloat16* x; int64_t ldx;
+  const __nv_bfloat16* g;
+  __nv_bfloat16* y; int64_t ldy;
+  int64_t n; float eps;
+};
+struct FusedProgram {
+  int64_t T;
+  int n;
+  FusedStep step[kFusedMaxPhases];
+  RopeCacheArgs rope;
+  unsigned int* bar;   // kFusedMaxPhases + 1 zeroed u32 counters (workspace), left zeroed
+};
+dl_status fused_decode(const FusedProgram& p, cudaStream_t st);
+// debug timeline of the fused kernels (see decode_fused.cu); buf == NULL: off
+dl_status set_fused_trace(void* buf);
 
 // ---------------------------------------------------------------------------
 // SIMT skinny chain (simt_chain.cu): Y[T x m] (+)= (X B^T) A^T, T <= 16.

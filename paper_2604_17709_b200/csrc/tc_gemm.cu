@@ -1230,6 +1230,10 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
 
 }  // namespace
 
+bool encode_map_bf16(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  return get_encode() && make_map(m, ptr, rows, cols, ld, box_rows);
+}
+
 dl_status set_gemm_trace(void* buf) {
   unsigned long long* p = static_cast<unsigned long long*>(buf);
   g_trace_host_on = p != nullptr;
