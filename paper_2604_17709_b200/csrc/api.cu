@@ -614,6 +614,8 @@ struct BlockWs {
   __nv_bfloat16 *xn, *zb, *yb, *rs, *q, *att, *att_full, *ag, *act;
   float* apart;                      // split-KV attention partials (decode)
   size_t apart_bytes;
+  void* ask;                         // stream-K decode attention: counters + partial slots
+  int64_t ask_items;
   unsigned int* sched;               // kSchedSlots x 2 stream-K work counters
   unsigned int* tile_cnt;            // stream-K fixup arrival counters (one per output tile)
   unsigned int* fbar;                // fused decode: 2 x 16 phase-barrier counters (pre / post attention)
@@ -643,6 +645,8 @@ BlockWs carve_block(Carver& c, const BlockDims& d, int64_t Tmax) {
   w.act = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.m);
   w.apart_bytes = attention_workspace(Ts, static_cast<int>(d.Hq_loc), static_cast<int>(d.d));
   w.apart = c.take<float>(w.apart_bytes / sizeof(float));
+  w.ask_items = Tmax * d.Hq_loc;
+  w.ask = c.take<float>(attention_sk_workspace(Tmax, static_cast<int>(d.Hq_loc)) / sizeof(float));
   w.sched = c.take<unsigned int>(2 * kSchedSlots);
   w.tile_cnt = c.take<unsigned int>(static_cast<size_t>((d.nmax + d.kmax) / 128 + 64));
   w.fbar = c.take<unsigned int>(32);
@@ -949,6 +953,7 @@ dl_status kvlr_attention(const dl_block_config* cfg, const BlockDims& d, const d
   aa.kv_ld = 2 * hkl;
   aa.kv_blk0 = kv->seq_block;
   aa.kv_bs = kv->block_size;
+  aa.kv_rows = rows;
   return launch_attention(aa, st);
 }
 
@@ -1210,6 +1215,8 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   aa.decode = phase == DL_DECODE;
   aa.partial = ws.apart;
   aa.partial_bytes = ws.apart_bytes;
+  aa.sk_ws = ws.ask;
+  aa.sk_items_cap = ws.ask_items;
 
   if (tp && d.layout == DL_LAYOUT_DEINFER) {
     // ---- DeInfer low-rank communication (Fig. 3) ----------

@@ -21,6 +21,7 @@
 #include <math.h>
 
 #include "dl_internal.h"
+#include "sm100_ptx.cuh"
 
 namespace dl {
 namespace {
@@ -450,7 +451,478 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(AttnArgs a, int split
   a.out[s * a.Hq * D + static_cast<int64_t>(h) * D + d] = __float2bfloat16_rn(o / L);
 }
 
+
+// ============================ decode, stream-K =============================
+// Flash-decoding with a balanced, persistent split (row a6 at decode).  The
+// work is the list of (sequence, kv head, 16-head chunk) items, each a run of
+// ceil(n_keys / 64) key tiles; the global tile list is cut into gridDim.x
+// equal contiguous ranges, one per CTA (2 CTAs per SM), so every SM streams
+// the same number of K/V bytes whatever the mix of context lengths.
+//   warp 4      TMA producer: 64-key K and V tiles (2 x 64-column boxes each,
+//               128B swizzle) into an NS-stage ring.  Tiles
+//               holding only keys older than this step (head-major cache) are
+//               requested before griddepcontrol.wait: they do not depend on
+//               the predecessor (the RoPE + cache-append kernel writes
+//               position cache_lens[s] only).
+//   warps 0-3   per tile, warp w scores keys [16w, 16w+16) (mma.sync, the
+//               <= 16 query heads of the group are the row block); the tile
+//               row max is shared so the four P slices have one scale; the P
+//               fragments are exchanged and warp w accumulates output dims
+//               [32w, 32w+32) over all 64 keys.  Row sums are added once per
+//               item.  An item cut by a range boundary leaves a partial
+//               {m, l, o[32]} per contributing CTA and warp (slot 0: the CTA's
+//               first item, slot 1: its last); the warp that completes the
+//               item's (item, warp) counter last merges them and resets it.
+namespace sk {
+constexpr int NS = 3;                       // K|V ring stages (x 2 CTAs per SM)
+constexpr int STAGE = 4 * 8192;             // K box0, K box1, V box0, V box1
+constexpr int kThreads = 160;              // 4 compute warps (dim slices / key slices) + 1 producer
+constexpr int SHR = 128 + 4 * 32 * 4;       // floats: tile row max [64], row sums [64]; P fragments [4][32] x 16 B
+constexpr int kMaxSeqs = 1024;
+constexpr int kPerSM = 2;                   // CTAs per SM (grid = kPerSM x SMs)
+constexpr int kPartRow = 2 + 32;            // partial row of one warp: m, l, o[32 dims]
+constexpr int kMaxGrid = 2 * 192;           // partial slots are sized for this
+constexpr size_t smem_bytes(int nseq) {
+  return NS * STAGE + SHR * 4 + 2 * NS * 8 +
+         static_cast<size_t>(nseq + 1) * 4;
+}
+}  // namespace sk
+
+struct SkMaps {
+  CUtensorMap k, v;
+};
+struct SkArgs {
+  const __nv_bfloat16* q;
+  __nv_bfloat16* out;
+  const int32_t* cache_lens;
+  int num_seqs, Hq, Hk, nch, Gall;
+  int64_t max_seq;                // head-major cache rows per (seq, kv head)
+  int token_major;                // 1: rows kv_blk0[s] * kv_bs + key, kv head at column kvh * 128
+  const int32_t* kv_blk0;
+  int64_t kv_bs;
+  float* part;                    // [kMaxGrid][2][16][2 + D]
+  unsigned* cnt;                  // [items], zero-maintained
+};
+
+struct SkItem {
+  int s, j;                       // sequence, item within the sequence (kvh * nch + ch)
+  int64_t start, end;             // global tile range of the item
+  int64_t g0, g1;                 // this CTA's part of it
+  int n_keys;
+};
+
+__device__ __forceinline__ int64_t sk_bound(int c, int64_t N, int G) { return (static_cast<int64_t>(c) * N) / G; }
+__device__ __forceinline__ int sk_owner(int64_t g, int64_t N, int G) {
+  int c = static_cast<int>((g * G) / N);
+  while (c + 1 < G && sk_bound(c + 1, N, G) <= g) ++c;
+  while (c > 0 && sk_bound(c, N, G) > g) --c;
+  return c;
+}
+// item containing global tile g (g < P[num_seqs]); `s` is a search hint
+__device__ __forceinline__ void sk_item_at(const int32_t* P, int num_seqs, int per_seq, int64_t g, SkItem& it,
+                                           const int32_t* cache_lens) {
+  int lo = 0, hi = num_seqs - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (P[mid] <= g) lo = mid; else hi = mid - 1;
+  }
+  const int s = lo;
+  const int nt = (P[s + 1] - P[s]) / per_seq;
+  const int j = static_cast<int>((g - P[s]) / nt);
+  it.s = s;
+  it.j = j;
+  it.start = P[s] + static_cast<int64_t>(j) * nt;
+  it.end = it.start + nt;
+  it.n_keys = cache_lens[s] + 1;
+}
+
+__device__ __forceinline__ float ex2(float x) {   // 2^x, MUFU.EX2 (ex2(-inf) = 0)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t sk_swz(uint32_t base, int key, int chunk) {   // 128B-swizzled TMA box pair
+  return base + ((chunk >> 3) << 13) + key * 128 + ((((chunk & 7) ^ (key & 7))) << 4);
+}
+
+__global__ void __launch_bounds__(sk::kThreads, sk::kPerSM)
+    attn_decode_sk_kernel(const __grid_constant__ SkMaps maps, const __grid_constant__ SkArgs a) {
+  using namespace sk;
+  extern __shared__ __align__(1024) uint8_t sm[];   // no static shared memory: the base is 1024-aligned
+  uint8_t* stages = sm;
+  float* tmax = reinterpret_cast<float*>(stages + NS * STAGE);   // [4 warps][16] tile row max, then row sums
+  float* pbuf = tmax + 128;                 // [4 k-slices][32 lanes] x uint4 P fragments
+  uint64_t* full = reinterpret_cast<uint64_t*>(pbuf + 4 * 32 * 4);
+  uint64_t* empty = full + NS;
+  int32_t* P = reinterpret_cast<int32_t*>(empty + NS);
+
+  pdl_trigger();
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int per_seq = a.Hk * a.nch;
+  // ---- prefix of tiles per sequence (cache_lens is not written inside the step) ----
+  if (warp == 0) {
+    const int n = a.num_seqs, per = (n + 31) / 32, b = lane * per;
+    int sum = 0;
+    for (int i = b; i < b + per && i < n; ++i) sum += per_seq * ((a.cache_lens[i] + 1 + KT - 1) / KT);
+    int inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += v;
+    }
+    int run = inc - sum;
+    for (int i = b; i < b + per && i < n; ++i) {
+      P[i] = run;
+      run += per_seq * ((a.cache_lens[i] + 1 + KT - 1) / KT);
+    }
+    if (lane == 31) P[n] = inc;
+  }
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], 4);   // released by the 4 compute warps
+    }
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+  const int G = gridDim.x, c = blockIdx.x;
+  const int64_t N = P[a.num_seqs];
+  const int64_t b0 = sk_bound(c, N, G), b1 = sk_bound(c + 1, N, G);
+  const int64_t ldq = static_cast<int64_t>(a.Hq) * D;
+
+  if (warp == 4) {
+    // ============================ producer ============================
+    if (lane != 0) return;
+    ptx::prefetch_tmap(&maps.k);
+    ptx::prefetch_tmap(&maps.v);
+    const uint64_t pol = ptx::policy_evict_first();
+    auto tile_coords = [&](const SkItem& it, int64_t g, int& row, int& col) {
+      const int kvh = it.j / a.nch;
+      const int t = static_cast<int>(g - it.start);
+      if (a.token_major) {
+        row = static_cast<int>(static_cast<int64_t>(a.kv_blk0[it.s]) * a.kv_bs + t * KT);
+        col = kvh * D;
+      } else {
+        row = static_cast<int>((static_cast<int64_t>(it.s) * a.Hk + kvh) * a.max_seq + t * KT);
+        col = 0;
+      }
+    };
+    auto issue = [&](const SkItem& it, int64_t g) {
+      const int64_t l = g - b0;
+      const int st = static_cast<int>(l % NS);
+      ptx::mbar_wait(&empty[st], ((l / NS) & 1) ^ 1);
+      int row, col;
+      tile_coords(it, g, row, col);
+      uint8_t* dst = stages + st * STAGE;
+      ptx::mbar_arrive_expect_tx(&full[st], STAGE);
+      ptx::tma_load_2d(dst, &maps.k, &full[st], col, row, pol);
+      ptx::tma_load_2d(dst + 8192, &maps.k, &full[st], col + 64, row, pol);
+      ptx::tma_load_2d(dst + 16384, &maps.v, &full[st], col, row, pol);
+      ptx::tma_load_2d(dst + 24576, &maps.v, &full[st], col + 64, row, pol);
+    };
+    // 1. before the predecessor completes: leading tiles of old keys only
+    int64_t pre = b0;
+    if (!a.token_major) {
+      SkItem it;
+      while (pre < b1 && pre - b0 < NS) {
+        sk_item_at(P, a.num_seqs, per_seq, pre, it, a.cache_lens);
+        const int t = static_cast<int>(pre - it.start);
+        if ((t + 1) * KT > it.n_keys - 1) break;   // tile holds the key appended by this step
+        issue(it, pre);
+        ++pre;
+      }
+    }
+    pdl_wait();
+    // 2. the remaining tiles
+    for (int64_t g = pre > b0 ? pre : b0; g < b1;) {
+      SkItem it;
+      sk_item_at(P, a.num_seqs, per_seq, g, it, a.cache_lens);
+      const int64_t e = it.end < b1 ? it.end : b1;
+      for (; g < e; ++g) issue(it, g);
+    }
+    return;
+  }
+
+  // ============================== compute ==============================
+  pdl_wait();
+  const int w = warp;
+  const int g8 = lane >> 2, t4 = lane & 3;
+  const float scale = rsqrtf(static_cast<float>(D)) * 1.4426950408889634f;
+  for (int64_t g = b0; g < b1;) {
+    SkItem it;
+    sk_item_at(P, a.num_seqs, per_seq, g, it, a.cache_lens);
+    const int64_t e = it.end < b1 ? it.end : b1;
+    const int kvh = it.j / a.nch, ch = it.j - kvh * a.nch;
+    const int h0 = kvh * a.Gall + ch * 16;
+    const int Gc = min(16, a.Gall - ch * 16);
+    // query fragments (rows g8, g8 + 8) straight from L2 -- written by the
+    // predecessor, so after griddepcontrol.wait; rows >= Gc read as zero
+    uint32_t qf[8][4];
+    {
+      const uint32_t* q0 = reinterpret_cast<const uint32_t*>(a.q + it.s * ldq + static_cast<int64_t>(h0 + g8) * D);
+      const uint32_t* q1 = q0 + 8 * (D / 2);
+      const bool v0 = g8 < Gc, v1 = g8 + 8 < Gc;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        qf[kk][0] = v0 ? q0[kk * 8 + t4] : 0u;
+        qf[kk][1] = v1 ? q1[kk * 8 + t4] : 0u;
+        qf[kk][2] = v0 ? q0[kk * 8 + 4 + t4] : 0u;
+        qf[kk][3] = v1 ? q1[kk * 8 + 4 + t4] : 0u;
+      }
+    }
+    float acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;   // m in log2 units (scaled)
+    for (int64_t gt = g; gt < e; ++gt) {
+      const int64_t l = gt - b0;
+      const int st = static_cast<int>(l % NS);
+      ptx::mbar_wait(&full[st], (l / NS) & 1);
+      const uint32_t sK = ptx::smem_u32(stages + st * STAGE), sV = sK + 16384;
+      const int nv = min(KT, it.n_keys - static_cast<int>(gt - it.start) * KT);   // valid keys of the tile
+      if (nv < KT) {
+        // keys past the end: their P is 0, but 0 * (garbage V) may be NaN;
+        // zero this warp's 4 chunks (dims 32w..32w+31) of the invalid rows
+        for (int i = lane; i < (KT - nv) * 4; i += 32) {
+          const int key = nv + (i >> 2), chk = w * 4 + (i & 3);
+          *reinterpret_cast<uint4*>(stages + st * STAGE + 16384 + sk_swz(0, key, chk)) = make_uint4(0u, 0u, 0u, 0u);
+        }
+        __syncwarp();
+      }
+      // scores of this warp's 16 keys [16w, 16w + 16) of the tile
+      float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      {
+        const int key = w * 16 + (lane & 7) + ((lane >> 4) & 1) * 8;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          uint32_t b0r, b1r, b2r, b3r;
+          ldsm_x4(sk_swz(sK, key, kk * 2 + ((lane >> 3) & 1)), b0r, b1r, b2r, b3r);
+          mma16816(sc[0], qf[kk], b0r, b1r);
+          mma16816(sc[1], qf[kk], b2r, b3r);
+        }
+      }
+      if (w * 16 + 16 > nv) {
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (w * 16 + nt * 8 + 2 * t4 + (q & 1) >= nv) sc[nt][q] = -INFINITY;
+      }
+      float mx0 = fmaxf(fmaxf(sc[0][0], sc[0][1]), fmaxf(sc[1][0], sc[1][1]));
+      float mx1 = fmaxf(fmaxf(sc[0][2], sc[0][3]), fmaxf(sc[1][2], sc[1][3]));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+      // tile row max over the group's 4 warps -> one scale for the whole P tile
+      float* tm = tmax;
+      if (t4 == 0) {
+        tm[w * 16 + g8] = mx0;
+        tm[w * 16 + g8 + 8] = mx1;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+      for (int ww = 0; ww < 4; ++ww) {
+        mx0 = fmaxf(mx0, tm[ww * 16 + g8]);
+        mx1 = fmaxf(mx1, tm[ww * 16 + g8 + 8]);
+      }
+      const float mn0 = fmaxf(m0, mx0 * scale), mn1 = fmaxf(m1, mx1 * scale);   // every tile has a valid key
+      const float c0 = ex2(m0 - mn0), c1 = ex2(m1 - mn1);
+      m0 = mn0;
+      m1 = mn1;
+      l0 *= c0;
+      l1 *= c1;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc[i][0] *= c0; acc[i][1] *= c0;
+        acc[i][2] *= c1; acc[i][3] *= c1;
+      }
+      uint32_t pf[4];
+      {
+        const float p0 = ex2(fmaf(sc[0][0], scale, -mn0)), p1 = ex2(fmaf(sc[0][1], scale, -mn0));
+        const float p2 = ex2(fmaf(sc[0][2], scale, -mn1)), p3 = ex2(fmaf(sc[0][3], scale, -mn1));
+        const float p4 = ex2(fmaf(sc[1][0], scale, -mn0)), p5 = ex2(fmaf(sc[1][1], scale, -mn0));
+        const float p6 = ex2(fmaf(sc[1][2], scale, -mn1)), p7 = ex2(fmaf(sc[1][3], scale, -mn1));
+        l0 += (p0 + p1) + (p4 + p5);
+        l1 += (p2 + p3) + (p6 + p7);
+        pf[0] = pack_bf16(p0, p1);
+        pf[1] = pack_bf16(p2, p3);
+        pf[2] = pack_bf16(p4, p5);
+        pf[3] = pack_bf16(p6, p7);
+      }
+      // share the P fragments (k-slice w of the 16 x 64 P tile) with the group
+      uint4* pb = reinterpret_cast<uint4*>(pbuf);
+      pb[w * 32 + lane] = make_uint4(pf[0], pf[1], pf[2], pf[3]);
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        uint32_t pk[4];
+        if (ks == w) {
+          pk[0] = pf[0]; pk[1] = pf[1]; pk[2] = pf[2]; pk[3] = pf[3];
+        } else {
+          const uint4 v = pb[ks * 32 + lane];
+          pk[0] = v.x; pk[1] = v.y; pk[2] = v.z; pk[3] = v.w;
+        }
+        const int key = ks * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+#pragma unroll
+        for (int dp = 0; dp < 2; ++dp) {
+          uint32_t v0, v1, v2, v3;
+          ldsm_x4_t(sk_swz(sV, key, w * 4 + dp * 2 + (lane >> 4)), v0, v1, v2, v3);
+          mma16816(acc[2 * dp], pk, v0, v1);
+          mma16816(acc[2 * dp + 1], pk, v2, v3);
+        }
+      }
+      if (nv < KT) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic zeros before the next TMA write
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&empty[st]);
+    }
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+    {
+      // each warp summed P over its own key slice: total row sums of the group
+      float* ls = tmax + 64;
+      if (t4 == 0) {
+        ls[w * 16 + g8] = l0;
+        ls[w * 16 + g8 + 8] = l1;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      l0 = ls[g8] + ls[16 + g8] + ls[32 + g8] + ls[48 + g8];
+      l1 = ls[8 + g8] + ls[24 + g8] + ls[40 + g8] + ls[56 + g8];
+      asm volatile("bar.sync 1, 128;" ::: "memory");   // ls reused by the next item
+    }
+    const bool whole = it.start >= b0 && it.end <= b1;
+    __nv_bfloat16* orow = a.out + static_cast<int64_t>(it.s) * ldq + static_cast<int64_t>(h0) * D + w * 32 + 2 * t4;
+    if (!whole) {
+      // publish {m, l, o[32 dims]} of rows g8, g8 + 8; the warp of the last
+      // contributing CTA merges (one counter per item and warp)
+      const int pslot = it.start <= b0 ? 0 : 1;
+      float* pp = a.part + ((static_cast<int64_t>(c) * 2 + pslot) * 4 + w) * 16 * kPartRow;
+      if (t4 == 0) {
+        pp[g8 * kPartRow] = m0;
+        pp[g8 * kPartRow + 1] = l0;
+        pp[(g8 + 8) * kPartRow] = m1;
+        pp[(g8 + 8) * kPartRow + 1] = l1;
+      }
+#pragma unroll
+      for (int dn = 0; dn < 4; ++dn) {
+        *reinterpret_cast<float2*>(pp + g8 * kPartRow + 2 + dn * 8 + 2 * t4) = make_float2(acc[dn][0], acc[dn][1]);
+        *reinterpret_cast<float2*>(pp + (g8 + 8) * kPartRow + 2 + dn * 8 + 2 * t4) = make_float2(acc[dn][2], acc[dn][3]);
+      }
+      __syncwarp();
+      const int cf = sk_owner(it.start, N, G), cl = sk_owner(it.end - 1, N, G);
+      unsigned* cnt = a.cnt + static_cast<int64_t>(it.s * per_seq + it.j) * 4 + w;
+      int last = 0;
+      if (lane == 0) {
+        int nc = 0;   // CTAs with a non-empty range (N < grid leaves some empty)
+        for (int cc = cf; cc <= cl; ++cc) nc += sk_bound(cc + 1, N, G) > sk_bound(cc, N, G);
+        __threadfence();   // release this warp's partial (cumulative over the warp via __syncwarp)
+        last = atomicAdd(cnt, 1u) == static_cast<unsigned>(nc - 1);
+        if (last) {
+          __threadfence();   // acquire the other contributors' partials
+          *cnt = 0u;         // zero-maintained for the next launch
+        }
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (!last) {
+        g = e;
+        continue;
+      }
+      // online merge over the contributors, in CTA order
+      m0 = m1 = -INFINITY;
+      l0 = l1 = 0.f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+      for (int cc = cf; cc <= cl; ++cc) {
+        const int64_t bc = sk_bound(cc, N, G);
+        if (sk_bound(cc + 1, N, G) == bc) continue;
+        const float* pk = a.part + ((static_cast<int64_t>(cc) * 2 + (it.start <= bc ? 0 : 1)) * 4 + w) * 16 * kPartRow;
+        const float km0 = __ldcg(pk + g8 * kPartRow), kl0 = __ldcg(pk + g8 * kPartRow + 1);
+        const float km1 = __ldcg(pk + (g8 + 8) * kPartRow), kl1 = __ldcg(pk + (g8 + 8) * kPartRow + 1);
+        float2 ko[4][2];
+#pragma unroll
+        for (int dn = 0; dn < 4; ++dn) {
+          ko[dn][0] = __ldcg(reinterpret_cast<const float2*>(pk + g8 * kPartRow + 2 + dn * 8 + 2 * t4));
+          ko[dn][1] = __ldcg(reinterpret_cast<const float2*>(pk + (g8 + 8) * kPartRow + 2 + dn * 8 + 2 * t4));
+        }
+        const float n0 = fmaxf(m0, km0), n1 = fmaxf(m1, km1);
+        const float z0 = n0 == -INFINITY ? 0.f : n0, z1 = n1 == -INFINITY ? 0.f : n1;
+        const float so0 = exp2f(m0 - z0), sn0 = exp2f(km0 - z0), so1 = exp2f(m1 - z1), sn1 = exp2f(km1 - z1);
+        m0 = n0;
+        m1 = n1;
+        l0 = l0 * so0 + kl0 * sn0;
+        l1 = l1 * so1 + kl1 * sn1;
+#pragma unroll
+        for (int dn = 0; dn < 4; ++dn) {
+          acc[dn][0] = acc[dn][0] * so0 + ko[dn][0].x * sn0;
+          acc[dn][1] = acc[dn][1] * so0 + ko[dn][0].y * sn0;
+          acc[dn][2] = acc[dn][2] * so1 + ko[dn][1].x * sn1;
+          acc[dn][3] = acc[dn][3] * so1 + ko[dn][1].y * sn1;
+        }
+      }
+    }
+    const float i0 = 1.f / l0, i1 = 1.f / l1;
+#pragma unroll
+    for (int dn = 0; dn < 4; ++dn) {
+      if (g8 < Gc) *reinterpret_cast<uint32_t*>(orow + g8 * D + dn * 8) = pack_bf16(acc[dn][0] * i0, acc[dn][1] * i0);
+      if (g8 + 8 < Gc)
+        *reinterpret_cast<uint32_t*>(orow + (g8 + 8) * D + dn * 8) = pack_bf16(acc[dn][2] * i1, acc[dn][3] * i1);
+    }
+    g = e;
+  }
+}
+
 }  // namespace
+
+size_t attention_sk_workspace(int64_t max_tokens, int Hq) {
+  return static_cast<size_t>((max_tokens * Hq + 63) / 64 * 64) * 4 * 4 +
+         static_cast<size_t>(sk::kMaxGrid) * 2 * 4 * 16 * sk::kPartRow * sizeof(float);
+}
+
+// stream-K decode attention; DL_ERR_UNSUPPORTED -> caller uses the split kernel
+dl_status launch_attention_sk(const AttnArgs& a, cudaStream_t st) {
+  static const bool off = getenv("DL_ATTN_SPLIT") && atoi(getenv("DL_ATTN_SPLIT")) != 0;   // A/B switch
+  const int nch = (a.Hq / a.Hk + 15) / 16;
+  const int64_t items = static_cast<int64_t>(a.num_seqs) * a.Hk * nch;
+  if (off || !a.decode || a.num_seqs > sk::kMaxSeqs || !a.sk_ws || items > a.sk_items_cap) return DL_ERR_UNSUPPORTED;
+  SkMaps maps;
+  SkArgs k{};
+  const int64_t hk_cols = static_cast<int64_t>(a.Hk) * D;
+  bool ok;
+  if (a.kv_ld) {
+    ok = encode_map_bf16(&maps.k, a.k_cache, a.kv_rows, hk_cols, a.kv_ld, KT) &&
+         encode_map_bf16(&maps.v, a.v_cache, a.kv_rows, hk_cols, a.kv_ld, KT);
+  } else {
+    const int64_t rows = static_cast<int64_t>(a.num_seqs) * a.Hk * a.max_seq;
+    ok = encode_map_bf16(&maps.k, a.k_cache, rows, D, D, KT) && encode_map_bf16(&maps.v, a.v_cache, rows, D, D, KT);
+  }
+  if (!ok) return DL_ERR_UNSUPPORTED;
+  k.q = a.q;
+  k.out = a.out;
+  k.cache_lens = a.cache_lens;
+  k.num_seqs = a.num_seqs;
+  k.Hq = a.Hq;
+  k.Hk = a.Hk;
+  k.nch = nch;
+  k.Gall = a.Hq / a.Hk;
+  k.max_seq = a.max_seq;
+  k.token_major = a.kv_ld ? 1 : 0;
+  k.kv_blk0 = a.kv_blk0;
+  k.kv_bs = a.kv_bs;
+  k.cnt = static_cast<unsigned*>(a.sk_ws);
+  k.part = reinterpret_cast<float*>(static_cast<uint8_t*>(a.sk_ws) + (a.sk_items_cap + 63) / 64 * 64 * 4 * 4);
+  const size_t smem = sk::smem_bytes(a.num_seqs);
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(attn_decode_sk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sk::smem_bytes(sk::kMaxSeqs)));
+    attr = sk::smem_bytes(sk::kMaxSeqs);
+  }
+  const int grid = std::min(sk::kPerSM * num_sms(), sk::kMaxGrid);
+  return launch_pdl(attn_decode_sk_kernel, dim3(grid), dim3(sk::kThreads), smem, st, "attention decode (stream-K)",
+                    maps, k);
+}
 
 size_t attention_workspace(int64_t max_tokens, int Hq, int d) {
   (void)d;
@@ -479,6 +951,10 @@ dl_status launch_attention(const AttnArgs& a, cudaStream_t st) {
     const int qtiles = static_cast<int>((a.T + QT - 1) / QT);
     dim3 grid(qtiles, a.Hq, a.num_seqs);
     return launch_pdl(attn_prefill_kernel<KTP>, grid, dim3(128), SMEM, st, "attention prefill", a);
+  }
+  {
+    const dl_status s = launch_attention_sk(a, st);
+    if (s != DL_ERR_UNSUPPORTED) return s;
   }
   constexpr int SMEM = 16 * ROW_BYTES + 4 * TILE_BYTES + (4 * 16 * D + 128) * 4;
   static bool attr = false;

@@ -274,9 +274,13 @@ struct AttnArgs {
   float* partial; size_t partial_bytes;   // split-KV scratch (decode)
   // decode only: kv_ld != 0 -> K/V rows are token-major with stride kv_ld
   // (elements); sequence s starts at row kv_blk0[s] * kv_bs; kv head g at +g*d
-  int64_t kv_ld; const int32_t* kv_blk0; int64_t kv_bs;
+  int64_t kv_ld; const int32_t* kv_blk0; int64_t kv_bs; int64_t kv_rows;
+  // stream-K decode kernel: zero-maintained counters + partial slots
+  // (attention_sk_workspace(sk_items_cap / Hq, Hq) bytes)
+  void* sk_ws; int64_t sk_items_cap;
 };
 dl_status launch_attention(const AttnArgs& a, cudaStream_t st);
 size_t attention_workspace(int64_t max_tokens, int Hq, int d);
+size_t attention_sk_workspace(int64_t max_tokens, int Hq);
 
 }  // namespace dl

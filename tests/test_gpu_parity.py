@@ -178,6 +178,38 @@ def test_block_decode_small(dl, orc, cache_lens):
     assert rel(kg, kn) <= TOL_BF16
 
 
+@pytest.mark.parametrize("cache_lens", [[4000, 3, 700], [63, 64, 127, 128, 0]])
+def test_block_decode_long_ragged_nan_tail(dl, orc, cache_lens):
+    """Stream-K decode attention: one long item spread over many CTAs next to short ones,
+    tile-boundary lengths, and NaN in the unwritten cache slots past each sequence
+    (masked keys must contribute exactly nothing). Two calls: the merge counters reset."""
+    s = SMALL
+    rk = block_ranks(s, 0.4)
+    w = gen_block_weights(s, rk, 0, 21)
+    S = len(cache_lens)
+    max_seq = max(cache_lens) + 70
+    x = gen_normal((S, s.h), 1.0, 22, dtype=torch.bfloat16)
+    kc = gen_normal((S, s.n_kv_heads, max_seq, s.head_dim), 1.0, 23, dtype=torch.bfloat16)
+    vc = gen_normal((S, s.n_kv_heads, max_seq, s.head_dim), 1.0, 24, dtype=torch.bfloat16)
+    ko, vo = _cache_to_oracle(kc, S, max_seq), _cache_to_oracle(vc, S, max_seq)
+    for b, L in enumerate(cache_lens):          # garbage past the appended slot
+        kc[b, :, L + 1:] = float("nan")
+        vc[b, :, L + 1:] = float("nan")
+    cl = torch.tensor(cache_lens, dtype=torch.int32)
+    cfg = dl.make_block_config(s, rk, max_tokens=S, max_seqs=S)
+    wdev = dl.BlockWeights({k: v.cuda() for k, v in w.items()})
+    ws = torch.zeros(dl.dl_block_workspace(cfg), dtype=torch.uint8, device="cuda")
+    ref, _, _ = orc.block_decode(_oracle_cfg(orc, s, rk), w, x, ko, vo, cache_lens)
+    for _ in range(2):
+        xd, kcd, vcd = x.cuda(), kc.cuda(), vc.cuda()
+        dl.dl_decomposed_block_forward(cfg, wdev, xd, cl.cuda(), None, S, dl.DL_DECODE, kcd, vcd, cl.cuda(), None,
+                                       ws)
+        torch.cuda.synchronize()
+        got = xd.cpu().double() - x.double()
+        assert torch.isfinite(got).all()
+        assert rel(got, ref - x.double().numpy()) <= TOL_BF16
+
+
 def test_block_workspace_left_zeroed_and_repeatable(dl, orc):
     """Consume-and-clear: two identical decode calls give identical results."""
     s = SMALL
