@@ -612,6 +612,7 @@ unsigned int* next_sched(unsigned int* base) {
 struct BlockWs {
   float* zf; float* yf;              // fp32 reduction targets (zero-maintained)
   __nv_bfloat16 *xn, *zb, *yb, *rs, *q, *att, *att_full, *ag, *act;
+  __nv_bfloat16* zr;                 // skinny stage-1 Z, bf16 red.add target (zero-maintained)
   float* apart;                      // split-KV attention partials (decode)
   size_t apart_bytes;
   void* ask;                         // stream-K decode attention: counters + partial slots
@@ -635,6 +636,7 @@ BlockWs carve_block(Carver& c, const BlockDims& d, int64_t Tmax) {
   w.yf = c.take<float>(static_cast<size_t>(Ts) * w.ldy32);
   w.xn = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.h);
   w.zb = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * w.ldzb);
+  w.zr = c.take<__nv_bfloat16>(static_cast<size_t>(Ts) * w.ldzb);   // bf16 red.add target (skinny), zero-maintained
   w.yb = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * rup(d.nmax, 8));
   w.rs = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.W);
   w.q = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.Hq_loc * d.d);
@@ -759,10 +761,33 @@ bool use_fixup() {
 // Skinny path: stage 1 finalizes Z to bf16 in its last-contributor fixup; a
 // stage-2 fixup `fix2` (op != FIX_NONE) finalizes the group output in place
 // of a separate kernel (then `out2` only supplies the output pointer/layout).
+bool use_zred() {
+  static const bool on = !getenv("DL_ZRED") || atoi(getenv("DL_ZRED")) != 0;   // A/B switch (default on)
+  return on;
+}
+
+// zero_out != NULL (skinny path): stage 1 red.adds its partials straight into
+// the bf16 Z buffer ws.zr (no fp32 -> bf16 pass); *zero_out is then the clear
+// of that buffer, which the caller hands to the kernel that follows stage 2.
 dl_status run_group(const dl_factor_group& grp, int nseg, const int64_t* rows, const __nv_bfloat16* act,
                     int64_t ld_act, int64_t n, int64_t T, bool skinny, const BlockWs& ws, const GemmOut& out2,
-                    cudaStream_t st, const GemmFixup* fix2 = nullptr) {
+                    cudaStream_t st, const GemmFixup* fix2 = nullptr, SideZero* zero_out = nullptr) {
   const ZLayout zl = zlayout(grp, nseg);
+  if (zero_out) *zero_out = SideZero{};
+  if (skinny && zero_out && use_zred() && !use_fixup()) {
+    GemmProblem p1 = stage1(grp, nseg, act, ld_act, T, n, zl, out_plain(ws.zr, ws.ldzb, OUT_BF16_RED, 0));
+    p1.sched = next_sched(ws.sched);
+    DL_TRY(tc_gemm(p1, true, st));
+    GemmProblem p2 = stage2(grp, nseg, rows, ws.zr, ws.ldzb, T, zl, out2);
+    p2.sched = next_sched(ws.sched);
+    if (fix2 && fix2->op != FIX_NONE) p2.fix = *fix2;
+    DL_TRY(tc_gemm(p2, true, st));
+    zero_out->p = ws.zr;
+    zero_out->ld = ws.ldzb * 2;
+    zero_out->rows = T;
+    zero_out->row_bytes = zl.width * 2;
+    return DL_OK;
+  }
   if (skinny) {
     if (use_fixup()) {
       GemmProblem p1 = stage1(grp, nseg, act, ld_act, T, n, zl, out_plain(ws.zb, ws.ldzb, OUT_BF16, 0));
@@ -1257,6 +1282,7 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   if (skinny && !tp && !kv && !fx && T <= 128 && d.h <= 8192 && d.m % 64 == 0 && use_fused()) return fused_block(cfg, d, w, x, T, ws, rc, aa, st);
 
   DL_TRY(launch_rmsnorm(x, static_cast<const __nv_bfloat16*>(w->attn_norm), ws.xn, T, d.h, cfg->rms_eps, st));
+  SideZero zq;
   if (kv) {
     DL_TRY(kvlr_attention(cfg, d, w, ws, kv, T, positions, cache_lens, false, comm, aa, rc, st));
   } else if (fx) {
@@ -1264,7 +1290,7 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
     f.rope = rc;
     DL_TRY(run_group(w->qkv, 3, qkv_rows, ws.xn, d.h, d.h, T, skinny, ws, qkv_out, st, &f));
   } else {
-    DL_TRY(run_group(w->qkv, 3, qkv_rows, ws.xn, d.h, d.h, T, skinny, ws, qkv_out, st));
+    DL_TRY(run_group(w->qkv, 3, qkv_rows, ws.xn, d.h, d.h, T, skinny, ws, qkv_out, st, nullptr, &zq));
   }
 
   if (fx || kv) {
@@ -1274,12 +1300,13 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
       rc.acc = ws.yf;
       rc.ld_src = ws.ldy32;
       rc.clear = 1;
+      rc.zero = zq;
     } else {
       rc.src = ws.yb;
       rc.ld_src = NQKV;
     }
   } else {
-    if (skinny) DL_TRY(launch_f32_to_bf16(ws.yf, NQKV, ws.yb, NQKV, 1, T * NQKV, 1, st));   // contiguous [P][T][W]
+    if (skinny) DL_TRY(launch_f32_to_bf16(ws.yf, NQKV, ws.yb, NQKV, 1, T * NQKV, 1, st, zq));   // contiguous [P][T][W]
     DL_TRY(reduce_scatter(comm, ws.yb, ws.rs, static_cast<size_t>(T) * d.W, kNcclBfloat16, st));
     rc.src = ws.rs;
     rc.ld_src = d.W;
@@ -1297,9 +1324,9 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   }
 
   // Finish a [T x n] group output: + residual (o, down) with the TP reduction.
-  auto finish_residual = [&](int64_t n) -> dl_status {
-    if (!tp) return skinny ? launch_residual_add_f32(ws.yf, ws.ldy32, x, d.h, T, n, 1, st) : DL_OK;
-    if (skinny) DL_TRY(launch_f32_to_bf16(ws.yf, ws.ldy32, ws.yb, n, T, n, 1, st));
+  auto finish_residual = [&](int64_t n, const SideZero& z) -> dl_status {
+    if (!tp) return skinny ? launch_residual_add_f32(ws.yf, ws.ldy32, x, d.h, T, n, 1, st, z) : DL_OK;
+    if (skinny) DL_TRY(launch_f32_to_bf16(ws.yf, ws.ldy32, ws.yb, n, T, n, 1, st, z));
     DL_TRY(all_reduce(comm, ws.yb, static_cast<size_t>(T) * n, kNcclBfloat16, st));
     return launch_residual_add_bf16(ws.yb, n, x, d.h, T, n, st);
   };
@@ -1312,14 +1339,15 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
 
   // ---- o projection + residual ----------------------------------------------
   const GemmFixup fres = fixup(fx ? FIX_RESIDUAL : FIX_NONE);
-  DL_TRY(run_group(w->o, 1, h_rows, att_in, d.h, d.h, T, skinny, ws, resid_out(), st, &fres));
+  SideZero zo, zg, zd;
+  DL_TRY(run_group(w->o, 1, h_rows, att_in, d.h, d.h, T, skinny, ws, resid_out(), st, &fres, fx ? nullptr : &zo));
   const __nv_bfloat16* mlp_norm = static_cast<const __nv_bfloat16*>(w->mlp_norm);
   static const bool no_fuse = getenv("DL_NO_FUSE_RESNORM") != nullptr;   // A/B timing switch
   if (!fx && !tp && skinny && !no_fuse) {
     // residual add of the o projection fused with the MLP pre-norm
-    DL_TRY(launch_residual_rmsnorm(ws.yf, ws.ldy32, x, mlp_norm, ws.xn, T, d.h, cfg->rms_eps, st));
+    DL_TRY(launch_residual_rmsnorm(ws.yf, ws.ldy32, x, mlp_norm, ws.xn, T, d.h, cfg->rms_eps, st, zo));
   } else {
-    if (!fx) DL_TRY(finish_residual(d.h));
+    if (!fx) DL_TRY(finish_residual(d.h, zo));
     DL_TRY(launch_rmsnorm(x, mlp_norm, ws.xn, T, d.h, cfg->rms_eps, st));
   }
 
@@ -1328,20 +1356,20 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   GemmOut gu_out = skinny ? out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0) : out_plain(ws.yb, ngu, OUT_BF16, 0);
   const bool fx_gu = fx && d.glu;
   const GemmFixup fsilu = fixup(fx_gu ? FIX_SILU : FIX_NONE);
-  DL_TRY(run_group(w->gu, n_gu, gu_rows, ws.xn, d.h, d.h, T, skinny, ws, gu_out, st, &fsilu));
+  DL_TRY(run_group(w->gu, n_gu, gu_rows, ws.xn, d.h, d.h, T, skinny, ws, gu_out, st, &fsilu, fx_gu ? nullptr : &zg));
   if (fx_gu) {
     // SiLU(gate)*up done by the gate|up stage-2 fixup
   } else if (!tp && skinny) {
-    if (d.glu) DL_TRY(launch_silu_mul_f32(ws.yf, ws.ldy32, ws.act, d.m, T, d.m, 1, st));
-    else DL_TRY(launch_relu_f32(ws.yf, ws.ldy32, ws.act, d.m, T, d.m, 1, st));
+    if (d.glu) DL_TRY(launch_silu_mul_f32(ws.yf, ws.ldy32, ws.act, d.m, T, d.m, 1, st, zg));
+    else DL_TRY(launch_relu_f32(ws.yf, ws.ldy32, ws.act, d.m, T, d.m, 1, st, zg));
   } else {
-    if (skinny) DL_TRY(launch_f32_to_bf16(ws.yf, ws.ldy32, ws.yb, ngu, T, ngu, 1, st));
+    if (skinny) DL_TRY(launch_f32_to_bf16(ws.yf, ws.ldy32, ws.yb, ngu, T, ngu, 1, st, zg));
     if (tp) DL_TRY(all_reduce(comm, ws.yb, static_cast<size_t>(T) * ngu, kNcclBfloat16, st));
     if (d.glu) DL_TRY(launch_silu_mul_bf16(ws.yb, ngu, ws.act, d.m, T, d.m, st));
     else DL_TRY(launch_relu_bf16(ws.yb, ngu, ws.act, d.m, T, d.m, st));
   }
-  DL_TRY(run_group(w->down, 1, h_rows, ws.act, d.m, d.m, T, skinny, ws, resid_out(), st, &fres));
-  if (!fx) DL_TRY(finish_residual(d.h));
+  DL_TRY(run_group(w->down, 1, h_rows, ws.act, d.m, d.m, T, skinny, ws, resid_out(), st, &fres, fx ? nullptr : &zd));
+  if (!fx) DL_TRY(finish_residual(d.h, zd));
   return DL_OK;
 }
 }  // namespace

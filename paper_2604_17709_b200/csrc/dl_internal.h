@@ -56,6 +56,13 @@ dl_status launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
 // q|k|v local rows [T x (Hq + 2 Hk) * d] (fp32 acc or bf16): RoPE on q, k;
 // q written (bf16) to q_out [T x Hq*d]; k, v appended to the cache at
 // position cache_lens[seq(t)] + (t - cu[seq]) (decode: seq = t).
+// Side job of a finalize kernel: zero `rows` rows of `row_bytes` (multiple of
+// 16) at p (row stride ld bytes), spread over the kernel's whole grid.
+struct SideZero {
+  void* p = nullptr;
+  int64_t ld = 0, rows = 0, row_bytes = 0;
+};
+
 struct RopeCacheArgs {
   const float* acc; const __nv_bfloat16* src; int64_t ld_src; int clear;
   __nv_bfloat16* q_out;
@@ -64,6 +71,7 @@ struct RopeCacheArgs {
   int32_t num_seqs; int decode;
   int64_t T; int Hq, Hk, d; float theta;
   int rope;            // 0: no rotary embedding (q, k pass through)
+  SideZero zero;       // side job (see SideZero)
 };
 
 // Last-contributor finalize of a stream-K GEMM (FixupOp); buffers zeroed on entry,
@@ -89,7 +97,11 @@ struct GemmSeg {
   int64_t act_koff;   // column offset of this segment's K range inside act
 };
 
-enum OutMode { OUT_BF16 = 0, OUT_F32_RED = 1, OUT_F32_STORE = 2 };
+// OUT_BF16_RED: stream-K partials red.add-ed straight into a zeroed bf16
+// buffer (red.global.add.noftz.bf16) -- the stage-1 latent Z of the skinny
+// path, which needs no fp32 -> bf16 pass; the buffer is zeroed again by the
+// kernel that follows the group's stage 2 (SideZero).
+enum OutMode { OUT_BF16 = 0, OUT_F32_RED = 1, OUT_F32_STORE = 2, OUT_BF16_RED = 3 };
 // Finalize applied by the last stream-K contributor of each output tile.
 enum FixupOp { FIX_NONE = 0, FIX_BF16 = 1, FIX_RESIDUAL = 2, FIX_SILU = 3, FIX_ROPE_CACHE = 4 };
 
@@ -203,27 +215,28 @@ dl_status launch_rmsnorm(const __nv_bfloat16* x, const __nv_bfloat16* g,
 // out_bf16[t][c] = bf16(acc[t][c]) ; acc zeroed afterwards (consume-and-clear)
 dl_status launch_f32_to_bf16(float* acc, int64_t ld_acc, __nv_bfloat16* out,
                              int64_t ld_out, int64_t T, int64_t n, int clear,
-                             cudaStream_t st);
+                             cudaStream_t st, const SideZero& z = SideZero{});
 // x[t][c] = bf16(x + acc) ; acc cleared
 dl_status launch_residual_add_f32(float* acc, int64_t ld_acc, __nv_bfloat16* x,
                                   int64_t ldx, int64_t T, int64_t n,
-                                  int clear, cudaStream_t st);
+                                  int clear, cudaStream_t st, const SideZero& z = SideZero{});
 // x[t][c] = bf16(x + acc) (acc cleared), then y = rmsnorm(x) * g   (h % 8 == 0)
 dl_status launch_residual_rmsnorm(float* acc, int64_t lda, __nv_bfloat16* x, const __nv_bfloat16* g,
-                                  __nv_bfloat16* y, int64_t T, int64_t h, float eps, cudaStream_t st);
+                                  __nv_bfloat16* y, int64_t T, int64_t h, float eps, cudaStream_t st,
+                                  const SideZero& z = SideZero{});
 // x[t][c] = bf16(x + y)
 dl_status launch_residual_add_bf16(const __nv_bfloat16* y, int64_t ldy, __nv_bfloat16* x,
                                    int64_t ldx, int64_t T, int64_t n, cudaStream_t st);
 // act[t][i] = bf16(silu(g) * u) with g = src[t][i], u = src[t][m + i]
 dl_status launch_silu_mul_f32(float* acc, int64_t ld_acc, __nv_bfloat16* act,
                               int64_t ld_act, int64_t T, int64_t m, int clear,
-                              cudaStream_t st);
+                              cudaStream_t st, const SideZero& z = SideZero{});
 dl_status launch_silu_mul_bf16(const __nv_bfloat16* src, int64_t ld_src,
                                __nv_bfloat16* act, int64_t ld_act, int64_t T,
                                int64_t m, cudaStream_t st);
 // act[t][i] = bf16(relu(u)), u = src[t][i] (non-GLU MLP)
 dl_status launch_relu_f32(float* acc, int64_t ld_acc, __nv_bfloat16* act, int64_t ld_act, int64_t T,
-                          int64_t m, int clear, cudaStream_t st);
+                          int64_t m, int clear, cudaStream_t st, const SideZero& z = SideZero{});
 dl_status launch_relu_bf16(const __nv_bfloat16* src, int64_t ld_src, __nv_bfloat16* act, int64_t ld_act,
                            int64_t T, int64_t m, cudaStream_t st);
 // RoPE + cache append as a standalone kernel (see RopeCacheArgs)

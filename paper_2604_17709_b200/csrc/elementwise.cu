@@ -17,6 +17,18 @@
 namespace dl {
 namespace {
 
+// SideZero job: 16-byte zero stores spread over every thread of the grid.
+__device__ __forceinline__ void side_zero(const SideZero& z) {
+  if (!z.p) return;
+  const int64_t per_row = z.row_bytes / 16, total = z.rows * per_row;
+  const int64_t nthr = static_cast<int64_t>(gridDim.x) * gridDim.y * blockDim.x;
+  for (int64_t i = (static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += nthr) {
+    const int64_t r = i / per_row;
+    *reinterpret_cast<uint4*>(static_cast<uint8_t*>(z.p) + r * z.ld + (i - r * per_row) * 16) = make_uint4(0, 0, 0, 0);
+  }
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -75,9 +87,11 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const __nv_bfloat16* __res
 __global__ void __launch_bounds__(512) residual_rmsnorm_kernel(float* __restrict__ acc, int64_t lda,
                                                                __nv_bfloat16* __restrict__ x,
                                                                const __nv_bfloat16* __restrict__ g,
-                                                               __nv_bfloat16* __restrict__ y, int h, float eps) {
+                                                               __nv_bfloat16* __restrict__ y, int h, float eps,
+                                                               SideZero z) {
   pdl_trigger();   // successor may launch now; it waits for us before reading
   pdl_wait();
+  side_zero(z);
   __shared__ float red[16];
   const int64_t t = blockIdx.x;
   float* ar = acc + t * lda;
@@ -128,19 +142,20 @@ __global__ void __launch_bounds__(512) residual_rmsnorm_kernel(float* __restrict
 
 // 2-D elementwise over [T x n] in groups of 4 columns: grid (ceil(n/4/256), T).
 template <typename F>
-__global__ void __launch_bounds__(256) ew4_kernel(int n4, F f) {
+__global__ void __launch_bounds__(256) ew4_kernel(int n4, F f, SideZero z) {
   pdl_trigger();   // successor may launch now; it waits for us before reading
   pdl_wait();
+  side_zero(z);
   const int c4 = blockIdx.x * blockDim.x + threadIdx.x;
   if (c4 < n4) f(static_cast<int64_t>(blockIdx.y), c4 * 4);
 }
 
 template <typename F>
-dl_status launch_ew4(int64_t T, int64_t n, F f, cudaStream_t st, const char* what) {
+dl_status launch_ew4(int64_t T, int64_t n, F f, cudaStream_t st, const char* what, const SideZero& z = SideZero{}) {
   if (T <= 0 || n <= 0) return DL_OK;
   const int n4 = static_cast<int>(n / 4);
   dim3 grid((n4 + 255) / 256, static_cast<unsigned>(T));
-  return launch_pdl(ew4_kernel<F>, grid, dim3(256), 0, st, what, n4, f);
+  return launch_pdl(ew4_kernel<F>, grid, dim3(256), 0, st, what, n4, f, z);
 }
 
 __device__ __forceinline__ float4 take4(float* p, int clear) {
@@ -223,6 +238,7 @@ struct ReluBf16 {
 __global__ void __launch_bounds__(128) rope_cache_kernel(RopeCacheArgs a) {
   pdl_trigger();   // successor may launch now; it waits for us before reading
   pdl_wait();
+  side_zero(a.zero);
   const int heads = a.Hq + 2 * a.Hk;
   const int quads = a.d / 4;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -437,34 +453,35 @@ dl_status launch_rmsnorm(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bf
                     static_cast<int>(h), eps);
 }
 dl_status launch_residual_rmsnorm(float* acc, int64_t lda, __nv_bfloat16* x, const __nv_bfloat16* g,
-                                  __nv_bfloat16* y, int64_t T, int64_t h, float eps, cudaStream_t st) {
+                                  __nv_bfloat16* y, int64_t T, int64_t h, float eps, cudaStream_t st,
+                                  const SideZero& z) {
   if (T <= 0) return DL_OK;
   return launch_pdl(residual_rmsnorm_kernel, dim3(static_cast<unsigned>(T)), dim3(512), 0, st, "residual_rmsnorm",
-                    acc, lda, x, g, y, static_cast<int>(h), eps);
+                    acc, lda, x, g, y, static_cast<int>(h), eps, z);
 }
 dl_status launch_f32_to_bf16(float* acc, int64_t lda, __nv_bfloat16* out, int64_t ldo, int64_t T, int64_t n,
-                             int clear, cudaStream_t st) {
-  return launch_ew4(T, n, F32ToBf16{acc, lda, out, ldo, clear}, st, "f32_to_bf16");
+                             int clear, cudaStream_t st, const SideZero& z) {
+  return launch_ew4(T, n, F32ToBf16{acc, lda, out, ldo, clear}, st, "f32_to_bf16", z);
 }
 dl_status launch_residual_add_f32(float* acc, int64_t lda, __nv_bfloat16* x, int64_t ldx, int64_t T, int64_t n,
-                                  int clear, cudaStream_t st) {
-  return launch_ew4(T, n, ResidualAdd{acc, lda, x, ldx, clear}, st, "residual_add");
+                                  int clear, cudaStream_t st, const SideZero& z) {
+  return launch_ew4(T, n, ResidualAdd{acc, lda, x, ldx, clear}, st, "residual_add", z);
 }
 dl_status launch_residual_add_bf16(const __nv_bfloat16* y, int64_t ldy, __nv_bfloat16* x, int64_t ldx, int64_t T,
                                    int64_t n, cudaStream_t st) {
   return launch_ew4(T, n, ResidualAddBf16{y, ldy, x, ldx}, st, "residual_add_bf16");
 }
 dl_status launch_silu_mul_f32(float* acc, int64_t lda, __nv_bfloat16* act, int64_t ldo, int64_t T, int64_t m,
-                              int clear, cudaStream_t st) {
-  return launch_ew4(T, m, SiluMulF32{acc, lda, act, ldo, m, clear}, st, "silu_mul_f32");
+                              int clear, cudaStream_t st, const SideZero& z) {
+  return launch_ew4(T, m, SiluMulF32{acc, lda, act, ldo, m, clear}, st, "silu_mul_f32", z);
 }
 dl_status launch_silu_mul_bf16(const __nv_bfloat16* src, int64_t lds, __nv_bfloat16* act, int64_t ldo, int64_t T,
                                int64_t m, cudaStream_t st) {
   return launch_ew4(T, m, SiluMulBf16{src, lds, act, ldo, m}, st, "silu_mul_bf16");
 }
 dl_status launch_relu_f32(float* acc, int64_t lda, __nv_bfloat16* act, int64_t ldo, int64_t T, int64_t m,
-                          int clear, cudaStream_t st) {
-  return launch_ew4(T, m, ReluF32{acc, lda, act, ldo, clear}, st, "relu_f32");
+                          int clear, cudaStream_t st, const SideZero& z) {
+  return launch_ew4(T, m, ReluF32{acc, lda, act, ldo, clear}, st, "relu_f32", z);
 }
 dl_status launch_relu_bf16(const __nv_bfloat16* src, int64_t lds, __nv_bfloat16* act, int64_t ldo, int64_t T,
                            int64_t m, cudaStream_t st) {

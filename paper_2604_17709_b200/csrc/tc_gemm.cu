@@ -643,7 +643,30 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int f = j.feat0 + row;
           const int tok0 = j.tok0 + c0;
           const int ntok = a.T - tok0;
-          if (f < s.write_end && ntok > 0) {
+          if (a.mode == OUT_BF16_RED && a.fixup == FIX_NONE && a.scatter_p <= 0) {
+            // bf16x2 reductions: the lane pair (even row, odd row) = two
+            // adjacent output columns swaps token halves, so the even lane
+            // adds (row, row + 1) for tokens 0-15 and the odd lane for 16-31
+            const bool odd = lane & 1;
+            const int fe = j.feat0 + (row & ~1);
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const float mine_lo = __uint_as_float(r[i]), mine_hi = __uint_as_float(r[i + 16]);
+              const float other = __shfl_xor_sync(0xffffffffu, odd ? mine_lo : mine_hi, 1);
+              float lo = odd ? other : mine_lo, hi = odd ? mine_hi : other;   // (column fe, column fe + 1)
+              if (fe + 1 >= s.write_end) hi = 0.f;
+              const __nv_bfloat162 h2 = __floats2bfloat162_rn(lo, hi);
+              pk[i] = *reinterpret_cast<const uint32_t*>(&h2);
+            }
+            const int t0 = odd ? 16 : 0;
+            if (fe < s.write_end && ntok > t0) {
+              __nv_bfloat16* p = static_cast<__nv_bfloat16*>(a.out) + out_index(a, s, tok0 + t0, fe);
+#pragma unroll
+              for (int i = 0; i < 16; ++i, p += a.ldo)
+                if (t0 + i < ntok) ptx::red_add_bf16x2(p, pk[i]);
+            }
+          } else if (f < s.write_end && ntok > 0) {
             const bool fx = a.fixup != FIX_NONE;
             const long long tstride = a.scatter_p <= 0 ? (fx ? a.acc_ld : a.ldo) : a.slab;
             const long long base = fx ? acc_index(a, s, tok0, f) : out_index(a, s, tok0, f);
@@ -1194,7 +1217,8 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
     flops += 2.0 * p.T * rk;
     bytes += 2.0 * rk + 2.0 * p.T * p.seg[g].klen;
   }
-  bytes += static_cast<double>(p.T) * p.n_feat * (p.out.mode == OUT_BF16 ? (p.out.accumulate ? 4 : 2) : 4);
+  bytes += static_cast<double>(p.T) * p.n_feat *
+           (p.out.mode == OUT_BF16 ? (p.out.accumulate ? 4 : 2) : p.out.mode == OUT_BF16_RED ? 2 : 4);
   const int prof = prof_begin(st);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -1247,8 +1271,8 @@ dl_status tc_gemm(const GemmProblem& p, bool stream_k, cudaStream_t st) {
     set_error("cuTensorMapEncodeTiled unavailable (driver too old or no GPU)");
     return DL_ERR_CUDA;
   }
-  if (stream_k && p.out.mode != OUT_F32_RED && p.fix.op == FIX_NONE) {
-    set_error("stream-K requires an fp32 reduction output");
+  if (stream_k && p.out.mode != OUT_F32_RED && p.out.mode != OUT_BF16_RED && p.fix.op == FIX_NONE) {
+    set_error("stream-K requires a reduction output");
     return DL_ERR_INVALID_ARG;
   }
   static const int dec_stages = getenv("DL_DECODE_STAGES") ? atoi(getenv("DL_DECODE_STAGES")) : 9;
