@@ -283,6 +283,20 @@ dl_status dl_decomposed_block_forward(
     int64_t max_seq, dl_comm comm, void *workspace, size_t workspace_bytes,
     void *stream);
 
+/* dl_decomposed_stack_forward -- n_layers consecutive blocks sharing one
+ * config and one workspace: exactly dl_decomposed_block_forward applied to
+ * layers 0 .. n_layers-1 in order (w[l], k_caches[l], v_caches[l] per layer;
+ * host arrays of device pointers), same arguments and errors otherwise.  On
+ * the single-GPU decode path the residual add that ends block l is fused with
+ * block l+1's attention RMSNorm (one kernel instead of two per boundary).
+ * n_layers == 0 is a no-op.                                                 */
+dl_status dl_decomposed_stack_forward(
+    const dl_block_config *cfg, const dl_block_weights *const *w, int32_t n_layers,
+    void *x, int64_t T, const int32_t *positions, const int32_t *cu_seqlens,
+    int32_t num_seqs, dl_phase phase, void *const *k_caches, void *const *v_caches,
+    const int32_t *cache_lens, int64_t max_seq, dl_comm comm, void *workspace,
+    size_t workspace_bytes, void *stream);
+
 /* ------------------------------------------------------------------------
  * Paged low-rank KV cache ("the low-rank
  * intermediate results between the two matrix multiplications now act as KV

@@ -24,7 +24,8 @@ EXPORTS = ("dl_last_error", "dl_version", "dl_device_ok", "dl_comm_create", "dl_
            "dl_block_workspace", "dl_decomposed_block_forward", "dl_embedding", "dl_rmsnorm",
            "dl_dense_workspace", "dl_dense", "dl_launch_count", "dl_profile_begin", "dl_profile_end",
            "dl_profile_count", "dl_profile_get", "dl_debug_gemm_trace", "dl_debug_fused_trace", "dl_deinfer_shard_factors",
-           "dl_kv_prepare", "dl_decomposed_block_forward_kvlr", "dl_comm_create_loopback")
+           "dl_kv_prepare", "dl_decomposed_block_forward_kvlr", "dl_comm_create_loopback",
+           "dl_decomposed_stack_forward")
 
 
 class DLError(RuntimeError):
@@ -97,6 +98,10 @@ def load():
             lib.dl_decomposed_block_forward.argtypes = [ctypes.POINTER(dl_block_config),
                                                         ctypes.POINTER(dl_block_weights), P, I64, P, P, I32, I,
                                                         P, P, P, I64, P, P, ctypes.c_size_t, P]
+            lib.dl_decomposed_stack_forward.argtypes = [ctypes.POINTER(dl_block_config),
+                                                        ctypes.POINTER(ctypes.POINTER(dl_block_weights)), I32, P,
+                                                        I64, P, P, I32, I, ctypes.POINTER(P), ctypes.POINTER(P), P,
+                                                        I64, P, P, ctypes.c_size_t, P]
             lib.dl_embedding.argtypes = [P, I64, I64, P, I64, P, P]
             lib.dl_rmsnorm.argtypes = [P, P, P, I64, I64, ctypes.c_float, P]
             lib.dl_dense_workspace.argtypes = [I64, I64, I64, ctypes.POINTER(ctypes.c_size_t)]
@@ -362,6 +367,32 @@ def dl_decomposed_block_forward(cfg: dl_block_config, weights: BlockWeights, x: 
                                               _ptr(positions), _ptr(cu_seqlens), num_seqs, phase, _ptr(k_cache),
                                               _ptr(v_cache), _ptr(cache_lens), k_cache.shape[2], _comm(comm),
                                               _ptr(workspace), workspace.numel(), _stream(stream)))
+    return x
+
+
+class StackArgs:
+    """Host pointer arrays for dl_decomposed_stack_forward (built once; the
+    weight structs and caches must outlive it)."""
+
+    def __init__(self, weights, k_caches, v_caches):
+        n = len(weights)
+        self.n = n
+        self.w = (ctypes.POINTER(dl_block_weights) * n)(*[ctypes.pointer(bw.c) for bw in weights])
+        self.k = (P * n)(*[_ptr(t) for t in k_caches])
+        self.v = (P * n)(*[_ptr(t) for t in v_caches])
+        self.max_seq = k_caches[0].shape[2] if n else 1
+
+
+def dl_decomposed_stack_forward(cfg: dl_block_config, args: StackArgs, x: torch.Tensor, positions: torch.Tensor,
+                                cu_seqlens: torch.Tensor | None, num_seqs: int, phase: int,
+                                cache_lens: torch.Tensor, comm: Comm | None, workspace: torch.Tensor,
+                                stream=None) -> torch.Tensor:
+    """args.n consecutive blocks sharing cfg and workspace (include/dl.h)."""
+    T = x.shape[0]
+    _check(load().dl_decomposed_stack_forward(ctypes.byref(cfg), args.w, args.n, _ptr(x), T, _ptr(positions),
+                                              _ptr(cu_seqlens), num_seqs, phase, args.k, args.v, _ptr(cache_lens),
+                                              args.max_seq, _comm(comm), _ptr(workspace), workspace.numel(),
+                                              _stream(stream)))
     return x
 
 

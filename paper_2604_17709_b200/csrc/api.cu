@@ -636,7 +636,10 @@ BlockWs carve_block(Carver& c, const BlockDims& d, int64_t Tmax) {
   w.yf = c.take<float>(static_cast<size_t>(Ts) * w.ldy32);
   w.xn = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.h);
   w.zb = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * w.ldzb);
-  w.zr = c.take<__nv_bfloat16>(static_cast<size_t>(Ts) * w.ldzb);   // bf16 red.add target (skinny), zero-maintained
+  // bf16 red.add targets of the skinny stage 1, zero-maintained: two column
+  // slots per row ([t][slot][ldzb]) so the gate|up latent (slot 1) may stay
+  // live until the down group's finalize clears both
+  w.zr = c.take<__nv_bfloat16>(static_cast<size_t>(Ts) * 2 * w.ldzb);
   w.yb = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * rup(d.nmax, 8));
   w.rs = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.W);
   w.q = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.Hq_loc * d.d);
@@ -771,19 +774,22 @@ bool use_zred() {
 // of that buffer, which the caller hands to the kernel that follows stage 2.
 dl_status run_group(const dl_factor_group& grp, int nseg, const int64_t* rows, const __nv_bfloat16* act,
                     int64_t ld_act, int64_t n, int64_t T, bool skinny, const BlockWs& ws, const GemmOut& out2,
-                    cudaStream_t st, const GemmFixup* fix2 = nullptr, SideZero* zero_out = nullptr) {
+                    cudaStream_t st, const GemmFixup* fix2 = nullptr, SideZero* zero_out = nullptr,
+                    int zslot = 0) {
   const ZLayout zl = zlayout(grp, nseg);
   if (zero_out) *zero_out = SideZero{};
   if (skinny && zero_out && use_zred() && !use_fixup()) {
-    GemmProblem p1 = stage1(grp, nseg, act, ld_act, T, n, zl, out_plain(ws.zr, ws.ldzb, OUT_BF16_RED, 0));
+    __nv_bfloat16* z = ws.zr + zslot * ws.ldzb;
+    const int64_t ldz = 2 * ws.ldzb;
+    GemmProblem p1 = stage1(grp, nseg, act, ld_act, T, n, zl, out_plain(z, ldz, OUT_BF16_RED, 0));
     p1.sched = next_sched(ws.sched);
     DL_TRY(tc_gemm(p1, true, st));
-    GemmProblem p2 = stage2(grp, nseg, rows, ws.zr, ws.ldzb, T, zl, out2);
+    GemmProblem p2 = stage2(grp, nseg, rows, z, ldz, T, zl, out2);
     p2.sched = next_sched(ws.sched);
     if (fix2 && fix2->op != FIX_NONE) p2.fix = *fix2;
     DL_TRY(tc_gemm(p2, true, st));
-    zero_out->p = ws.zr;
-    zero_out->ld = ws.ldzb * 2;
+    zero_out->p = z;
+    zero_out->ld = ldz * 2;
     zero_out->rows = T;
     zero_out->row_bytes = zl.width * 2;
     return DL_OK;
@@ -1078,7 +1084,13 @@ namespace {
 dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights* w, void* x_, int64_t T,
                              const int32_t* positions, const int32_t* cu_seqlens, int32_t num_seqs, dl_phase phase,
                              void* k_cache, void* v_cache, const int32_t* cache_lens, int64_t max_seq, dl_comm comm,
-                             void* workspace, size_t workspace_bytes, void* stream, const dl_kv_lowrank* kv) {
+                             void* workspace, size_t workspace_bytes, void* stream, const dl_kv_lowrank* kv,
+                             const void* next_norm = nullptr, bool* next_normed = nullptr, bool prenormed = false) {
+  // Stack chaining (dl_decomposed_stack_forward): with next_norm, a decode
+  // block whose last step is the skinny residual add fuses it with the next
+  // block's attention RMSNorm into ws.xn and sets *next_normed; with
+  // prenormed, ws.xn already holds rmsnorm(x) * attn_norm.
+  if (next_normed) *next_normed = false;
   const int P = comm ? comm->world : 1;
   BlockDims d;
   DL_TRY(block_dims(cfg, P, &d));
@@ -1281,7 +1293,8 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
 
   if (skinny && !tp && !kv && !fx && T <= 128 && d.h <= 8192 && d.m % 64 == 0 && use_fused()) return fused_block(cfg, d, w, x, T, ws, rc, aa, st);
 
-  DL_TRY(launch_rmsnorm(x, static_cast<const __nv_bfloat16*>(w->attn_norm), ws.xn, T, d.h, cfg->rms_eps, st));
+  if (!prenormed)
+    DL_TRY(launch_rmsnorm(x, static_cast<const __nv_bfloat16*>(w->attn_norm), ws.xn, T, d.h, cfg->rms_eps, st));
   SideZero zq;
   if (kv) {
     DL_TRY(kvlr_attention(cfg, d, w, ws, kv, T, positions, cache_lens, false, comm, aa, rc, st));
@@ -1354,9 +1367,13 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   // ---- MLP: gate|up group, SiLU(gate)*up (or ReLU(up)), down + residual ---------
   const int64_t ngu = n_gu * d.m;
   GemmOut gu_out = skinny ? out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0) : out_plain(ws.yb, ngu, OUT_BF16, 0);
-  const bool fx_gu = fx && d.glu;
+  // SiLU(gate)*up by the gate|up stage-2 last-contributor fixup: with all
+  // fixups (DL_FIXUP) or alone (DL_FIXUP_SILU; the latent stays in Z slot 1
+  // until the down group's finalize clears it)
+  static const bool fix_silu = getenv("DL_FIXUP_SILU") && atoi(getenv("DL_FIXUP_SILU")) != 0;
+  const bool fx_gu = (fx || (fix_silu && skinny && !tp)) && d.glu;
   const GemmFixup fsilu = fixup(fx_gu ? FIX_SILU : FIX_NONE);
-  DL_TRY(run_group(w->gu, n_gu, gu_rows, ws.xn, d.h, d.h, T, skinny, ws, gu_out, st, &fsilu, fx_gu ? nullptr : &zg));
+  DL_TRY(run_group(w->gu, n_gu, gu_rows, ws.xn, d.h, d.h, T, skinny, ws, gu_out, st, &fsilu, fx ? nullptr : &zg, 1));
   if (fx_gu) {
     // SiLU(gate)*up done by the gate|up stage-2 fixup
   } else if (!tp && skinny) {
@@ -1369,10 +1386,43 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
     else DL_TRY(launch_relu_bf16(ws.yb, ngu, ws.act, d.m, T, d.m, st));
   }
   DL_TRY(run_group(w->down, 1, h_rows, ws.act, d.m, d.m, T, skinny, ws, resid_out(), st, &fres, fx ? nullptr : &zd));
+  if (fx_gu && zg.p && zd.p) zd.row_bytes = ws.ldzb * 2 + zg.row_bytes;   // slot 0 + the gate|up latent in slot 1
+  if (next_norm && !fx && !tp && skinny && !no_fuse) {
+    // residual add of the down projection fused with the next block's pre-norm
+    DL_TRY(launch_residual_rmsnorm(ws.yf, ws.ldy32, x, static_cast<const __nv_bfloat16*>(next_norm), ws.xn, T, d.h,
+                                   cfg->rms_eps, st, zd));
+    *next_normed = true;
+    return DL_OK;
+  }
   if (!fx) DL_TRY(finish_residual(d.h, zd));
   return DL_OK;
 }
 }  // namespace
+
+dl_status dl_decomposed_stack_forward(const dl_block_config* cfg, const dl_block_weights* const* w, int32_t n_layers,
+                                      void* x, int64_t T, const int32_t* positions, const int32_t* cu_seqlens,
+                                      int32_t num_seqs, dl_phase phase, void* const* k_caches, void* const* v_caches,
+                                      const int32_t* cache_lens, int64_t max_seq, dl_comm comm, void* workspace,
+                                      size_t workspace_bytes, void* stream) {
+  if (!w || n_layers < 0 || (n_layers > 0 && (!k_caches || !v_caches))) {
+    set_error("stack: weights / caches missing");
+    return DL_ERR_INVALID_ARG;
+  }
+  bool normed = false;
+  for (int32_t l = 0; l < n_layers; ++l) {
+    if (!w[l]) {
+      set_error("stack: layer %d weights NULL", l);
+      return DL_ERR_INVALID_ARG;
+    }
+    const void* nn = l + 1 < n_layers ? w[l + 1]->attn_norm : nullptr;
+    bool out_normed = false;
+    DL_TRY(block_forward_impl(cfg, w[l], x, T, positions, cu_seqlens, num_seqs, phase, k_caches[l], v_caches[l],
+                              cache_lens, max_seq, comm, workspace, workspace_bytes, stream, nullptr, nn, &out_normed,
+                              normed));
+    normed = out_normed;
+  }
+  return DL_OK;
+}
 
 dl_status dl_decomposed_block_forward(const dl_block_config* cfg, const dl_block_weights* w, void* x_, int64_t T,
                                       const int32_t* positions, const int32_t* cu_seqlens, int32_t num_seqs,

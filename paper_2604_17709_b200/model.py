@@ -72,6 +72,12 @@ class DecomposedLlama:
                 dws[k] = torch.zeros(L.dl_block_workspace(c, self.world), dtype=torch.uint8, device=self.device)
         self.dec_wss = [dws[k] for k in keys]
         self.dec_ws = self.dec_wss[0]
+        # uniform ranks, full KV: one stack call (cross-block residual + norm fusion)
+        self.stack = None
+        import os
+        if kv == "full" and len(dws) == 1 and nl > 0 and not os.environ.get("DL_NO_STACK"):   # A/B switch
+            self.stack = L.StackArgs(self.layers, [self.cache[i, 0] for i in range(nl)],
+                                     [self.cache[i, 1] for i in range(nl)])
         # decode-step static buffers
         self.ids = torch.zeros(batch, dtype=torch.int32, device=self.device)
         self.cache_lens = torch.zeros(batch, dtype=torch.int32, device=self.device)
@@ -120,7 +126,10 @@ class DecomposedLlama:
             for i, lw in enumerate(self.layers):
                 L.dl_decomposed_block_forward_kvlr(self.dec_cfgs[i], lw, self.x, self.cache_lens, self.kv_layers[i],
                                                    self.cache_lens, self.comm, self.dec_wss[i])
-        for i, lw in enumerate(self.layers if self.kv_mode == "full" else ()):
+        if self.kv_mode == "full" and self.stack is not None:
+            L.dl_decomposed_stack_forward(self.dec_cfg, self.stack, self.x, self.cache_lens, None, self.batch,
+                                          L.DL_DECODE, self.cache_lens, self.comm, self.dec_ws)
+        for i, lw in enumerate(self.layers if self.kv_mode == "full" and self.stack is None else ()):
             L.dl_decomposed_block_forward(self.dec_cfgs[i], lw, self.x, self.cache_lens, None, self.batch, L.DL_DECODE,
                                           self.cache[i, 0], self.cache[i, 1], self.cache_lens, self.comm,
                                           self.dec_wss[i])

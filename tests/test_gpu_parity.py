@@ -371,6 +371,39 @@ def test_model_decode_variadic_layer_ranks(dl, orc):
     assert rel(model.x.cpu().double() - x0, (x - x0).numpy()) <= TOL_BF16
 
 
+def test_model_decode_uniform_stack_three_layers(dl, orc):
+    """Uniform ranks: the model's decode step goes through dl_decomposed_stack_forward
+    (the residual ending block l fused with block l+1's pre-norm). Three layers with
+    distinct norms vs the oracle applied layer by layer."""
+    from paper_2604_17709_b200.model import DecomposedLlama
+    s = SMALL
+    rk = block_ranks(s, 0.4)
+    ws_ = [gen_block_weights(s, rk, 6, li) for li in range(3)]
+    S, L = 5, 70
+    embed = gen_normal((s.vocab, s.h), 1.0, 80, dtype=torch.bfloat16).cuda()
+    lm = gen_normal((s.vocab, s.h), s.h ** -0.5, 81, dtype=torch.bfloat16).cuda()
+    model = DecomposedLlama(s, rk, [{k: v.cuda() for k, v in w.items()} for w in ws_], embed,
+                            torch.ones(s.h, dtype=torch.bfloat16, device="cuda"), lm, batch=S, max_seq=L + 1)
+    assert model.stack is not None
+    model.cache.copy_(gen_normal(tuple(model.cache.shape), 1.0, 82, dtype=torch.bfloat16))
+    model.cache_lens.fill_(L)
+    ids = torch.arange(S, dtype=torch.int32) * 53 % s.vocab
+    model.ids.copy_(ids)
+    cache0 = model.cache.cpu()
+    x0 = embed.cpu()[ids.long()].double()
+    x = x0
+    for li, w in enumerate(ws_):
+        ko = _cache_to_oracle(cache0[li, 0], S, L + 1)
+        vo = _cache_to_oracle(cache0[li, 1], S, L + 1)
+        x, _, _ = orc.block_decode(_oracle_cfg(orc, s, rk), w, x, ko, vo, [L] * S)
+        x = torch.tensor(x)
+    for _ in range(2):                      # twice: the stack leaves its workspace zeroed
+        model.decode_step()
+        torch.cuda.synchronize()
+        assert rel(model.x.cpu().double() - x0, (x - x0).numpy()) <= TOL_BF16
+        model.cache.copy_(cache0.cuda())
+
+
 # ---- low-rank KV cache (N3: P:111, P:219-237) -------------------------------------------
 def _kvlr_case(dl, orc, s, cache_lens, seed, block_size=16):
     rk = block_ranks(s, 0.4)
