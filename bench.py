@@ -63,6 +63,15 @@ def load_peaks():
         return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
 
 
+def load_traffic():
+    """ncu DRAM bytes of the dominant launch (profiles/traffic.json, from one --set full capture)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
 
@@ -338,7 +347,10 @@ def main():
             ach = sum(r[2] for r in recs) / (ms * 1e-3) / 1e12
             peak = bf16_sust
             unit = "TFLOP/s"
-        return {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak, "traffic": None,
+        tr = load_traffic().get("decode" if bound == "hbm" else "prefill", {})
+        return {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
+                "traffic": tr.get("dram_bytes"), "traffic_launch": tr.get("launch"),
+                "traffic_algorithmic_bytes": tr.get("algorithmic_bytes"), "traffic_source": tr.get("source"),
                 "kernel": "tc_gemm (tcgen05 low-rank stage-1/stage-2 GEMMs, all launches of one step)",
                 "launches_per_step": len(recs), "kernel_ms_per_step": ms,
                 "peak_source": f"{peak_src} ({'hbm_gbs' if bound == 'hbm' else 'bf16_tflops_sustained'})"}

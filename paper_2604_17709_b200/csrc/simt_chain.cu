@@ -139,9 +139,15 @@ __global__ void __launch_bounds__(kWarps * 32)
   gemv_warp_rows<E, I, O, TT>(W, ldw, R, C, in, ldi, T, out, ldo, accumulate, row0);
 }
 
-// Fused single-CTA chain: Z in shared memory (k <= 1024, T <= 16).
+// Fused small chain: Z in shared memory (k <= 1024, T <= 16), never written
+// out.  Every CTA (32 warps) computes the whole Z = X B^T (B is small and
+// L2-resident after the first CTA touches it: one pass of 64 rows at k <= 64)
+// and then its own 64-row slice of Y = Z A^T, so the chain costs two dependent
+// memory round trips instead of one per 16 rows (BASELINE config 1: 20 -> ~5 us).
+constexpr int kSmallWarps = 32;
+constexpr int kSmallRowsPerCta = kSmallWarps * kRows;
 template <typename E, int TT>
-__global__ void __launch_bounds__(kWarps * 32)
+__global__ void __launch_bounds__(kSmallWarps * 32)
     chain_small_kernel(const E* __restrict__ X, int64_t ldx, const E* __restrict__ A, int64_t lda,
                        const E* __restrict__ B, int64_t ldb, E* __restrict__ Y, int64_t ldy, int T,
                        int m, int n, int k, int accumulate) {
@@ -150,11 +156,11 @@ __global__ void __launch_bounds__(kWarps * 32)
   pdl_wait();
   const int kp = (k + 3) & ~3;
   const int warp = threadIdx.x >> 5;
-  for (int row0 = warp * kRows; row0 < k; row0 += kWarps * kRows)
+  for (int row0 = warp * kRows; row0 < k; row0 += kSmallWarps * kRows)
     gemv_warp_rows<E, E, float, TT>(B, ldb, k, n, X, ldx, T, zs, kp, 0, row0);
   __syncthreads();
-  for (int row0 = warp * kRows; row0 < m; row0 += kWarps * kRows)
-    gemv_warp_rows<E, float, E, TT>(A, lda, m, k, zs, kp, T, Y, ldy, accumulate, row0);
+  const int row0 = blockIdx.x * kSmallRowsPerCta + warp * kRows;
+  if (row0 < m) gemv_warp_rows<E, float, E, TT>(A, lda, m, k, zs, kp, T, Y, ldy, accumulate, row0);
 }
 
 template <typename E, int TT>
@@ -166,11 +172,12 @@ dl_status run(const void* X, int64_t ldx, const void* A, int64_t lda, const void
   const E* b = static_cast<const E*>(B);
   E* y = static_cast<E*>(Y);
   const int rows_per_cta = kWarps * kRows;
-  if (k <= 1024 && (m + n) * k <= (1 << 16)) {
+  if (k <= 1024 && (m + n) * k <= (1 << 16) && T * ((k + 3) & ~3) * 4 <= 48 * 1024) {
     const int kp = static_cast<int>((k + 3) & ~3);
     size_t smem = sizeof(float) * static_cast<size_t>(T) * kp;
-    return launch_pdl(chain_small_kernel<E, TT>, dim3(1), dim3(kWarps * 32), smem, st, "simt chain_small", x, ldx, a,
-                      lda, b, ldb, y, ldy, (int)T, (int)m, (int)n, (int)k, accumulate);
+    return launch_pdl(chain_small_kernel<E, TT>, dim3(static_cast<int>((m + kSmallRowsPerCta - 1) / kSmallRowsPerCta)),
+                      dim3(kSmallWarps * 32), smem, st, "simt chain_small", x, ldx, a, lda, b, ldb, y, ldy, (int)T,
+                      (int)m, (int)n, (int)k, accumulate);
   }
   float* z = static_cast<float*>(zbuf);
   const int64_t ldz = (k + 3) & ~3;

@@ -1063,6 +1063,13 @@ bool make_map(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64
   return r == CUDA_SUCCESS;
 }
 
+// CTAs per SM of the shallow (<= 4-stage) swap-AB configurations: 2 fills the
+// SM; 1 leaves room for the successor's CTA to become resident early (A/B knob)
+int small_per_sm() {
+  static const int v = getenv("DL_DECODE_PER_SM") ? atoi(getenv("DL_DECODE_PER_SM")) : 2;
+  return v == 1 ? 1 : 2;
+}
+
 template <int BN, bool SWAP, int STAGES, bool PAIR = false>
 dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   // PAIR: cta_group::2 kernel, cluster tile 256 tokens x 256 features, each CTA
@@ -1177,7 +1184,7 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   if (stream_k && p.sched) {
     static const double frac = getenv("DL_SK_STATIC") ? atof(getenv("DL_SK_STATIC")) : 0.9;
     static const int chunk = getenv("DL_SK_CHUNK") ? atoi(getenv("DL_SK_CHUNK")) : 8;
-    const int cap = num_sms() * ((SWAP && STAGES <= 4) ? 2 : 1);   // must match the grid below
+    const int cap = num_sms() * ((SWAP && STAGES <= 4) ? small_per_sm() : 1);   // must match the grid below
     const int g = static_cast<int>(units < cap ? (units > 0 ? units : 1) : cap);
     a.sched = p.sched;
     a.static_units = static_cast<long long>(frac * static_cast<double>(units) / g);
@@ -1189,7 +1196,7 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   if (stream_k) {
     // shallow configurations (<= 4 stages) fit two CTAs per SM: the next
     // launch can then start streaming on an SM while one CTA is still draining
-    const int per_sm = (SWAP && STAGES <= 4) ? 2 : 1;
+    const int per_sm = (SWAP && STAGES <= 4) ? small_per_sm() : 1;
     const int cap = sms * per_sm;
     grid = static_cast<int>(units < cap ? (units > 0 ? units : 1) : cap);
   } else if (PAIR) {

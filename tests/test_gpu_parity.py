@@ -48,6 +48,19 @@ def test_linear_config1_fp32(dl, orc):
     assert rel(Y.cpu(), orc.lowrank_linear(X, A, B)) <= TOL_F32
 
 
+@pytest.mark.parametrize("T,m,n,k,dt", [(4, 256, 256, 64, torch.float32), (16, 200, 120, 96, torch.float32),
+                                        (7, 180, 180, 180, torch.float32), (16, 200, 96, 88, torch.bfloat16),
+                                        (1, 64, 512, 64, torch.bfloat16)])
+def test_linear_simt_small_chain(dl, orc, T, m, n, k, dt):
+    """Fused small chain (Z in shared memory; several CTAs each recompute Z and own a
+    64-row slice of Y): ragged m, T up to 16, fp32 and bf16."""
+    X, A, B = _lin_inputs(T, m, n, k, dt, 30 + T + m)
+    Y = torch.empty(T, m, device="cuda", dtype=dt)
+    dl.dl_lowrank_linear(X.cuda(), A.cuda(), B.cuda(), Y)
+    torch.cuda.synchronize()
+    assert rel(Y.cpu(), orc.lowrank_linear(X, A, B)) <= (TOL_F32 if dt == torch.float32 else TOL_BF16)
+
+
 @pytest.mark.parametrize("T", [1, 3, 16])
 def test_linear_fp32_simt_large(dl, orc, T):
     """fp32 SIMT chain at a size that takes the two-kernel path (k > 1024 is not needed: (m+n)k > 64K)."""

@@ -8,29 +8,32 @@ transfers.  Prints per-rank step time and the per-rank collective payload of
 each layout (the bytes a real run moves over NVLink).
 
 python tools/tp_emulate.py [--layers 80] [--ps 1,2,4,8] [--layouts rp,deinfer]
+                          [--model 70b|8b] [--ratios 0.4[,0.1,...]]   (BASELINE configs 3-5)
 """
 import argparse, json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2604_17709_b200 as dl
 from paper_2604_17709_b200.model import DecomposedLlama
-from synthetic import LLAMA3_70B, block_ranks, gen_block_weights, gen_normal
+from synthetic import LLAMA3_70B, LLAMA3_8B, block_ranks, gen_block_weights, gen_normal
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--layers", type=int, default=80)
+ap.add_argument("--layers", type=int, default=0, help="0: all layers of the model")
 ap.add_argument("--ps", default="1,2,4,8")
 ap.add_argument("--layouts", default="rp,deinfer")
 ap.add_argument("--steps", type=int, default=20)
 ap.add_argument("--batch", type=int, default=64)
 ap.add_argument("--ctx", type=int, default=512)
+ap.add_argument("--model", default="70b", choices=["70b", "8b"])
+ap.add_argument("--ratios", default="0.4")
 a = ap.parse_args()
-s = LLAMA3_70B
-rk = block_ranks(s, 0.4)
+s = LLAMA3_70B if a.model == "70b" else LLAMA3_8B
+a.layers = a.layers or s.n_layers
 dev = torch.device("cuda")
 B = a.batch
 
 
-def comm_elems(layout, P):
+def comm_elems(layout, P, rk):
     """Elements per token per layer this rank sends/receives in its collectives (bf16 unless noted)."""
     if P == 1:
         return 0
@@ -40,8 +43,11 @@ def comm_elems(layout, P):
 
 
 res = []
-for layout in a.layouts.split(","):
-    for P in [int(p) for p in a.ps.split(",")]:
+import itertools
+for ratio, layout, P in itertools.product([float(r) for r in a.ratios.split(",")], a.layouts.split(","),
+                                         [int(p) for p in a.ps.split(",")]):
+    rk = block_ranks(s, ratio)
+    if True:
         lay = dl.DL_LAYOUT_DEINFER if layout == "deinfer" else dl.DL_LAYOUT_RANK_PARALLEL
         print(f"[tp_emulate] {layout} P={P}: {torch.cuda.memory_allocated() / 1e9:.1f} GB allocated", file=sys.stderr)
         comm = dl.Comm.loopback(0, P) if P > 1 else None
@@ -73,9 +79,16 @@ for layout in a.layouts.split(","):
             e1.record(st)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / a.steps
-        cb = comm_elems(layout, P) * B * a.layers * 2
+        cb = comm_elems(layout, P, rk) * B * a.layers * 2
         weights_gb = sum(t.numel() * t.element_size() for lw in m.layers for t in lw.tensors.values()) / 1e9
-        r = {"layout": layout, "P": P, "layers": a.layers, "rank_ms_per_step": round(ms, 3),
+        wbytes = sum(t.numel() * t.element_size() for lw in m.layers for t in lw.tensors.values())
+        kvb = m.cache.numel() * m.cache.element_size() * a.ctx / (a.ctx + 1)
+        lmb = m.lm_head.numel() * 2
+        hbm_ms = (wbytes + kvb + lmb) / 6553.6e9 * 1e3      # MEASURED_PEAKS hbm_gbs
+        r = {"model": a.model, "ratio": ratio, "ranks": rk, "layout": layout, "P": P, "layers": a.layers,
+             "batch": B, "ctx": a.ctx, "rank_ms_per_step": round(ms, 3),
+             "rank_tok_s": round(B / ms * 1e3, 1), "hbm_ideal_ms": round(hbm_ms, 3),
+             "frac_of_hbm": round(hbm_ms / ms, 3),
              "rank_weight_gb": round(weights_gb, 2), "collective_mb_per_step_per_rank": round(cb / 1e6, 1)}
         res.append(r)
         print(json.dumps(r), flush=True)
