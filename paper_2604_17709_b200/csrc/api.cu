@@ -613,6 +613,7 @@ struct BlockWs {
   float* zf; float* yf;              // fp32 reduction targets (zero-maintained)
   __nv_bfloat16 *xn, *zb, *yb, *rs, *q, *att, *att_full, *ag, *act;
   __nv_bfloat16* zr;                 // skinny stage-1 Z, bf16 red.add target (zero-maintained)
+  __nv_bfloat16* yr;                 // skinny TP stage-2 partials, bf16 red.add target = collective buffer (zero-maintained)
   float* apart;                      // split-KV attention partials (decode)
   size_t apart_bytes;
   void* ask;                         // stream-K decode attention: counters + partial slots
@@ -640,6 +641,7 @@ BlockWs carve_block(Carver& c, const BlockDims& d, int64_t Tmax) {
   // slots per row ([t][slot][ldzb]) so the gate|up latent (slot 1) may stay
   // live until the down group's finalize clears both
   w.zr = c.take<__nv_bfloat16>(static_cast<size_t>(Ts) * 2 * w.ldzb);
+  w.yr = c.take<__nv_bfloat16>(static_cast<size_t>(Ts) * rup(d.nmax, 8));
   w.yb = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * rup(d.nmax, 8));
   w.rs = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.W);
   w.q = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.Hq_loc * d.d);
@@ -1188,6 +1190,10 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   const int64_t h_rows[1] = {d.h};
   const int64_t NQKV = d.h + 2 * d.hkv;
   const int red_mode = skinny ? OUT_F32_RED : OUT_BF16;
+  // skinny TP: stage-2 partials red.add-ed as bf16x2 straight into the
+  // collective's buffer ws.yr (no fp32 -> bf16 pass before each collective);
+  // the kernel that consumes the collective's result clears it
+  const bool tpr = tp && skinny && use_zred();
 
   // ---- q|k|v: one group; partials laid out rank-major by head for the RS ----
   GemmOut qkv_out{};
@@ -1202,6 +1208,11 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   qkv_out.seg_rpr[2] = d.hkv / P;
   qkv_out.ptr = skinny ? static_cast<void*>(ws.yf) : static_cast<void*>(ws.yb);
   qkv_out.ld = skinny ? ws.ldy32 : NQKV;
+  if (tpr) {
+    qkv_out.mode = OUT_BF16_RED;
+    qkv_out.ptr = ws.yr;
+    qkv_out.ld = NQKV;
+  }
 
   // skinny, single rank: every group's finalize (RoPE + cache append, residual,
   // SiLU*up) runs in the stage-2 GEMM's last-contributor fixup
@@ -1318,6 +1329,14 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
       rc.src = ws.yb;
       rc.ld_src = NQKV;
     }
+  } else if (tpr) {
+    DL_TRY(reduce_scatter(comm, ws.yr, ws.rs, static_cast<size_t>(T) * d.W, kNcclBfloat16, st));
+    rc.src = ws.rs;
+    rc.ld_src = d.W;
+    rc.zero = zq;
+    rc.zero2.p = ws.yr;                         // contiguous [P][T][W] partials
+    rc.zero2.rows = 1;
+    rc.zero2.row_bytes = rc.zero2.ld = static_cast<int64_t>(T) * NQKV * 2;
   } else {
     if (skinny) DL_TRY(launch_f32_to_bf16(ws.yf, NQKV, ws.yb, NQKV, 1, T * NQKV, 1, st, zq));   // contiguous [P][T][W]
     DL_TRY(reduce_scatter(comm, ws.yb, ws.rs, static_cast<size_t>(T) * d.W, kNcclBfloat16, st));
@@ -1339,12 +1358,17 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   // Finish a [T x n] group output: + residual (o, down) with the TP reduction.
   auto finish_residual = [&](int64_t n, const SideZero& z) -> dl_status {
     if (!tp) return skinny ? launch_residual_add_f32(ws.yf, ws.ldy32, x, d.h, T, n, 1, st, z) : DL_OK;
+    if (tpr) {
+      DL_TRY(all_reduce(comm, ws.yr, static_cast<size_t>(T) * n, kNcclBfloat16, st));
+      return launch_residual_add_bf16(ws.yr, n, x, d.h, T, n, st, 1, z);
+    }
     if (skinny) DL_TRY(launch_f32_to_bf16(ws.yf, ws.ldy32, ws.yb, n, T, n, 1, st, z));
     DL_TRY(all_reduce(comm, ws.yb, static_cast<size_t>(T) * n, kNcclBfloat16, st));
     return launch_residual_add_bf16(ws.yb, n, x, d.h, T, n, st);
   };
   // wide & TP=1: the stage-2 epilogue adds straight into x (fused residual)
   auto resid_out = [&]() -> GemmOut {
+    if (tpr) return out_plain(ws.yr, d.h, OUT_BF16_RED, 0);
     if (skinny) return out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0);
     if (!tp) return out_plain(x, d.h, OUT_BF16, 1);
     return out_plain(ws.yb, d.h, OUT_BF16, 0);
@@ -1367,6 +1391,7 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   // ---- MLP: gate|up group, SiLU(gate)*up (or ReLU(up)), down + residual ---------
   const int64_t ngu = n_gu * d.m;
   GemmOut gu_out = skinny ? out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0) : out_plain(ws.yb, ngu, OUT_BF16, 0);
+  if (tpr) gu_out = out_plain(ws.yr, ngu, OUT_BF16_RED, 0);
   // SiLU(gate)*up by the gate|up stage-2 last-contributor fixup: with all
   // fixups (DL_FIXUP) or alone (DL_FIXUP_SILU; the latent stays in Z slot 1
   // until the down group's finalize clears it)
@@ -1379,6 +1404,10 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   } else if (!tp && skinny) {
     if (d.glu) DL_TRY(launch_silu_mul_f32(ws.yf, ws.ldy32, ws.act, d.m, T, d.m, 1, st, zg));
     else DL_TRY(launch_relu_f32(ws.yf, ws.ldy32, ws.act, d.m, T, d.m, 1, st, zg));
+  } else if (tpr) {
+    DL_TRY(all_reduce(comm, ws.yr, static_cast<size_t>(T) * ngu, kNcclBfloat16, st));
+    if (d.glu) DL_TRY(launch_silu_mul_bf16(ws.yr, ngu, ws.act, d.m, T, d.m, st, 1, zg));
+    else DL_TRY(launch_relu_bf16(ws.yr, ngu, ws.act, d.m, T, d.m, st, 1, zg));
   } else {
     if (skinny) DL_TRY(launch_f32_to_bf16(ws.yf, ws.ldy32, ws.yb, ngu, T, ngu, 1, st, zg));
     if (tp) DL_TRY(all_reduce(comm, ws.yb, static_cast<size_t>(T) * ngu, kNcclBfloat16, st));

@@ -71,7 +71,7 @@ struct RopeCacheArgs {
   int32_t num_seqs; int decode;
   int64_t T; int Hq, Hk, d; float theta;
   int rope;            // 0: no rotary embedding (q, k pass through)
-  SideZero zero;       // side job (see SideZero)
+  SideZero zero, zero2;   // side jobs (see SideZero)
 };
 
 // Last-contributor finalize of a stream-K GEMM (FixupOp); buffers zeroed on entry,
@@ -225,20 +225,22 @@ dl_status launch_residual_rmsnorm(float* acc, int64_t lda, __nv_bfloat16* x, con
                                   __nv_bfloat16* y, int64_t T, int64_t h, float eps, cudaStream_t st,
                                   const SideZero& z = SideZero{});
 // x[t][c] = bf16(x + y)
+// clear != 0: y is zeroed as it is read (a bf16 reduction target)
 dl_status launch_residual_add_bf16(const __nv_bfloat16* y, int64_t ldy, __nv_bfloat16* x,
-                                   int64_t ldx, int64_t T, int64_t n, cudaStream_t st);
+                                   int64_t ldx, int64_t T, int64_t n, cudaStream_t st, int clear = 0,
+                                   const SideZero& z = SideZero{});
 // act[t][i] = bf16(silu(g) * u) with g = src[t][i], u = src[t][m + i]
 dl_status launch_silu_mul_f32(float* acc, int64_t ld_acc, __nv_bfloat16* act,
                               int64_t ld_act, int64_t T, int64_t m, int clear,
                               cudaStream_t st, const SideZero& z = SideZero{});
 dl_status launch_silu_mul_bf16(const __nv_bfloat16* src, int64_t ld_src,
                                __nv_bfloat16* act, int64_t ld_act, int64_t T,
-                               int64_t m, cudaStream_t st);
+                               int64_t m, cudaStream_t st, int clear = 0, const SideZero& z = SideZero{});
 // act[t][i] = bf16(relu(u)), u = src[t][i] (non-GLU MLP)
 dl_status launch_relu_f32(float* acc, int64_t ld_acc, __nv_bfloat16* act, int64_t ld_act, int64_t T,
                           int64_t m, int clear, cudaStream_t st, const SideZero& z = SideZero{});
 dl_status launch_relu_bf16(const __nv_bfloat16* src, int64_t ld_src, __nv_bfloat16* act, int64_t ld_act,
-                           int64_t T, int64_t m, cudaStream_t st);
+                           int64_t T, int64_t m, cudaStream_t st, int clear = 0, const SideZero& z = SideZero{});
 // RoPE + cache append as a standalone kernel (see RopeCacheArgs)
 dl_status launch_rope_cache(const RopeCacheArgs& a, cudaStream_t st);
 dl_status launch_embedding(const __nv_bfloat16* table, int64_t vocab, int64_t h,

@@ -192,10 +192,15 @@ struct ResidualAdd {
     store4(x + t * ldx + c, r.x + v.x, r.y + v.y, r.z + v.z, r.w + v.w);
   }
 };
+__device__ __forceinline__ float4 take4(__nv_bfloat16* p, int clear) {
+  const float4 v = load4(p);
+  if (clear) *reinterpret_cast<uint2*>(p) = make_uint2(0u, 0u);
+  return v;
+}
 struct ResidualAddBf16 {
-  const __nv_bfloat16* y; int64_t ldy; __nv_bfloat16* x; int64_t ldx;
+  __nv_bfloat16* y; int64_t ldy; __nv_bfloat16* x; int64_t ldx; int clear;
   __device__ void operator()(int64_t t, int c) const {
-    float4 v = load4(y + t * ldy + c);
+    float4 v = take4(y + t * ldy + c, clear);
     float4 r = load4(x + t * ldx + c);
     store4(x + t * ldx + c, r.x + v.x, r.y + v.y, r.z + v.z, r.w + v.w);
   }
@@ -209,10 +214,10 @@ struct SiluMulF32 {
   }
 };
 struct SiluMulBf16 {
-  const __nv_bfloat16* src; int64_t lds; __nv_bfloat16* out; int64_t ldo; int64_t m;
+  __nv_bfloat16* src; int64_t lds; __nv_bfloat16* out; int64_t ldo; int64_t m; int clear;
   __device__ void operator()(int64_t t, int c) const {
-    float4 g = load4(src + t * lds + c);
-    float4 u = load4(src + t * lds + m + c);
+    float4 g = take4(src + t * lds + c, clear);
+    float4 u = take4(src + t * lds + m + c, clear);
     store4(out + t * ldo + c, silu(g.x) * u.x, silu(g.y) * u.y, silu(g.z) * u.z, silu(g.w) * u.w);
   }
 };
@@ -226,9 +231,9 @@ struct ReluF32 {
   }
 };
 struct ReluBf16 {
-  const __nv_bfloat16* src; int64_t lds; __nv_bfloat16* out; int64_t ldo;
+  __nv_bfloat16* src; int64_t lds; __nv_bfloat16* out; int64_t ldo; int clear;
   __device__ void operator()(int64_t t, int c) const {
-    float4 u = load4(src + t * lds + c);
+    float4 u = take4(src + t * lds + c, clear);
     store4(out + t * ldo + c, fmaxf(u.x, 0.f), fmaxf(u.y, 0.f), fmaxf(u.z, 0.f), fmaxf(u.w, 0.f));
   }
 };
@@ -239,6 +244,7 @@ __global__ void __launch_bounds__(128) rope_cache_kernel(RopeCacheArgs a) {
   pdl_trigger();   // successor may launch now; it waits for us before reading
   pdl_wait();
   side_zero(a.zero);
+  side_zero(a.zero2);
   const int heads = a.Hq + 2 * a.Hk;
   const int quads = a.d / 4;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -468,24 +474,26 @@ dl_status launch_residual_add_f32(float* acc, int64_t lda, __nv_bfloat16* x, int
   return launch_ew4(T, n, ResidualAdd{acc, lda, x, ldx, clear}, st, "residual_add", z);
 }
 dl_status launch_residual_add_bf16(const __nv_bfloat16* y, int64_t ldy, __nv_bfloat16* x, int64_t ldx, int64_t T,
-                                   int64_t n, cudaStream_t st) {
-  return launch_ew4(T, n, ResidualAddBf16{y, ldy, x, ldx}, st, "residual_add_bf16");
+                                   int64_t n, cudaStream_t st, int clear, const SideZero& z) {
+  return launch_ew4(T, n, ResidualAddBf16{const_cast<__nv_bfloat16*>(y), ldy, x, ldx, clear}, st, "residual_add_bf16",
+                    z);
 }
 dl_status launch_silu_mul_f32(float* acc, int64_t lda, __nv_bfloat16* act, int64_t ldo, int64_t T, int64_t m,
                               int clear, cudaStream_t st, const SideZero& z) {
   return launch_ew4(T, m, SiluMulF32{acc, lda, act, ldo, m, clear}, st, "silu_mul_f32", z);
 }
 dl_status launch_silu_mul_bf16(const __nv_bfloat16* src, int64_t lds, __nv_bfloat16* act, int64_t ldo, int64_t T,
-                               int64_t m, cudaStream_t st) {
-  return launch_ew4(T, m, SiluMulBf16{src, lds, act, ldo, m}, st, "silu_mul_bf16");
+                               int64_t m, cudaStream_t st, int clear, const SideZero& z) {
+  return launch_ew4(T, m, SiluMulBf16{const_cast<__nv_bfloat16*>(src), lds, act, ldo, m, clear}, st, "silu_mul_bf16",
+                    z);
 }
 dl_status launch_relu_f32(float* acc, int64_t lda, __nv_bfloat16* act, int64_t ldo, int64_t T, int64_t m,
                           int clear, cudaStream_t st, const SideZero& z) {
   return launch_ew4(T, m, ReluF32{acc, lda, act, ldo, clear}, st, "relu_f32", z);
 }
 dl_status launch_relu_bf16(const __nv_bfloat16* src, int64_t lds, __nv_bfloat16* act, int64_t ldo, int64_t T,
-                           int64_t m, cudaStream_t st) {
-  return launch_ew4(T, m, ReluBf16{src, lds, act, ldo}, st, "relu_bf16");
+                           int64_t m, cudaStream_t st, int clear, const SideZero& z) {
+  return launch_ew4(T, m, ReluBf16{const_cast<__nv_bfloat16*>(src), lds, act, ldo, clear}, st, "relu_bf16", z);
 }
 dl_status launch_rope_cache(const RopeCacheArgs& a, cudaStream_t st) {
   if (a.T <= 0) return DL_OK;

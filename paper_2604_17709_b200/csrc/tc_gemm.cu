@@ -419,8 +419,11 @@ struct JobIter {
 };
 
 
+// Shallow (<= 4-stage) swap-AB configurations are register-capped for two
+// CTAs per SM, so a successor GEMM's CTA can become resident (and prefetch
+// its weights) while this one still runs.
 template <int BN, bool SWAP, int STAGES>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, (SWAP && STAGES <= 4) ? 2 : 1)
     tc_gemm_kernel(const __grid_constant__ KMaps maps, const __grid_constant__ KArgs a) {
   constexpr int P_ROWS = BM;                 // MMA A operand rows
   constexpr int Q_ROWS = BN;                 // MMA B operand rows
@@ -643,7 +646,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int f = j.feat0 + row;
           const int tok0 = j.tok0 + c0;
           const int ntok = a.T - tok0;
-          if (a.mode == OUT_BF16_RED && a.fixup == FIX_NONE && a.scatter_p <= 0) {
+          if (a.mode == OUT_BF16_RED && a.fixup == FIX_NONE) {
             // bf16x2 reductions: the lane pair (even row, odd row) = two
             // adjacent output columns swaps token halves, so the even lane
             // adds (row, row + 1) for tokens 0-15 and the odd lane for 16-31
@@ -661,9 +664,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             const int t0 = odd ? 16 : 0;
             if (fe < s.write_end && ntok > t0) {
+              // plain rows: stride ldo; reduce-scatter slabs [P][T][slab]: stride slab (rows per
+              // rank and slab offsets are even, so columns fe, fe + 1 stay adjacent)
+              const long long tstr = a.scatter_p <= 0 ? a.ldo : a.slab;
               __nv_bfloat16* p = static_cast<__nv_bfloat16*>(a.out) + out_index(a, s, tok0 + t0, fe);
 #pragma unroll
-              for (int i = 0; i < 16; ++i, p += a.ldo)
+              for (int i = 0; i < 16; ++i, p += tstr)
                 if (t0 + i < ntok) ptx::red_add_bf16x2(p, pk[i]);
             }
           } else if (f < s.write_end && ntok > 0) {

@@ -13,6 +13,7 @@ from synthetic import LLAMA3_70B, block_ranks, gen_block_weights, gen_normal
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--layers", type=int, default=4)
+ap.add_argument("--tp", type=int, default=1, help="P > 1: one rank of TP = P through the loopback communicator")
 a = ap.parse_args()
 s = LLAMA3_70B
 rk = block_ranks(s, 0.4)
@@ -20,8 +21,8 @@ dev = torch.device("cuda")
 m = DecomposedLlama(s, rk, (gen_block_weights(s, rk, 3, i, device=dev) for i in range(a.layers)),
                     gen_normal((s.vocab, s.h), 1.0, 1, device=dev, dtype=torch.bfloat16),
                     torch.ones(s.h, dtype=torch.bfloat16, device=dev),
-                    gen_normal((s.vocab, s.h), s.h ** -0.5, 2, device=dev, dtype=torch.bfloat16), batch=64,
-                    max_seq=513)
+                    gen_normal((s.vocab // a.tp, s.h), s.h ** -0.5, 2, device=dev, dtype=torch.bfloat16), batch=64,
+                    max_seq=513, comm=dl.Comm.loopback(0, a.tp) if a.tp > 1 else None)
 m.cache.normal_()
 m.cache_lens.fill_(512)
 torch.cuda.synchronize()
