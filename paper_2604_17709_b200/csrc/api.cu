@@ -1383,6 +1383,10 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   if (!fx && !tp && skinny && !no_fuse) {
     // residual add of the o projection fused with the MLP pre-norm
     DL_TRY(launch_residual_rmsnorm(ws.yf, ws.ldy32, x, mlp_norm, ws.xn, T, d.h, cfg->rms_eps, st, zo));
+  } else if (tpr && !no_fuse) {
+    // TP: all-reduce of the bf16 partials, then residual + MLP pre-norm in one pass
+    DL_TRY(all_reduce(comm, ws.yr, static_cast<size_t>(T) * d.h, kNcclBfloat16, st));
+    DL_TRY(launch_residual_rmsnorm_bf16(ws.yr, d.h, x, mlp_norm, ws.xn, T, d.h, cfg->rms_eps, st, zo));
   } else {
     if (!fx) DL_TRY(finish_residual(d.h, zo));
     DL_TRY(launch_rmsnorm(x, mlp_norm, ws.xn, T, d.h, cfg->rms_eps, st));
@@ -1420,6 +1424,13 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
     // residual add of the down projection fused with the next block's pre-norm
     DL_TRY(launch_residual_rmsnorm(ws.yf, ws.ldy32, x, static_cast<const __nv_bfloat16*>(next_norm), ws.xn, T, d.h,
                                    cfg->rms_eps, st, zd));
+    *next_normed = true;
+    return DL_OK;
+  }
+  if (next_norm && tpr && !no_fuse && d.layout != DL_LAYOUT_DEINFER) {
+    DL_TRY(all_reduce(comm, ws.yr, static_cast<size_t>(T) * d.h, kNcclBfloat16, st));
+    DL_TRY(launch_residual_rmsnorm_bf16(ws.yr, d.h, x, static_cast<const __nv_bfloat16*>(next_norm), ws.xn, T, d.h,
+                                        cfg->rms_eps, st, zd));
     *next_normed = true;
     return DL_OK;
   }

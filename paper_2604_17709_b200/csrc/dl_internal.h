@@ -224,6 +224,10 @@ dl_status launch_residual_add_f32(float* acc, int64_t ld_acc, __nv_bfloat16* x,
 dl_status launch_residual_rmsnorm(float* acc, int64_t lda, __nv_bfloat16* x, const __nv_bfloat16* g,
                                   __nv_bfloat16* y, int64_t T, int64_t h, float eps, cudaStream_t st,
                                   const SideZero& z = SideZero{});
+// the same with a bf16 accumulator (a TP collective's result, consumed and cleared)
+dl_status launch_residual_rmsnorm_bf16(__nv_bfloat16* acc, int64_t lda, __nv_bfloat16* x, const __nv_bfloat16* g,
+                                       __nv_bfloat16* y, int64_t T, int64_t h, float eps, cudaStream_t st,
+                                       const SideZero& z = SideZero{});
 // x[t][c] = bf16(x + y)
 // clear != 0: y is zeroed as it is read (a bf16 reduction target)
 dl_status launch_residual_add_bf16(const __nv_bfloat16* y, int64_t ldy, __nv_bfloat16* x,

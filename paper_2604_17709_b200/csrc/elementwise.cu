@@ -84,7 +84,26 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const __nv_bfloat16* __res
 // x = bf16(x + acc) (acc consumed and cleared), then y = rmsnorm(x) * g: the
 // o-projection residual and the MLP pre-norm in one pass (one CTA per row).
 // The norm reads the bf16-rounded x, exactly as the two separate kernels did.
-__global__ void __launch_bounds__(512) residual_rmsnorm_kernel(float* __restrict__ acc, int64_t lda,
+// 8 consecutive accumulator values, zeroed as they are read (fp32 or bf16 accumulator)
+__device__ __forceinline__ void take8(float* p, float* o) {
+  const float4 a0 = *reinterpret_cast<float4*>(p), a1 = *reinterpret_cast<float4*>(p + 4);
+  *reinterpret_cast<float4*>(p) = make_float4(0.f, 0.f, 0.f, 0.f);
+  *reinterpret_cast<float4*>(p + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+  o[0] = a0.x; o[1] = a0.y; o[2] = a0.z; o[3] = a0.w; o[4] = a1.x; o[5] = a1.y; o[6] = a1.z; o[7] = a1.w;
+}
+__device__ __forceinline__ void take8(__nv_bfloat16* p, float* o) {
+  const uint4 v = *reinterpret_cast<uint4*>(p);
+  *reinterpret_cast<uint4*>(p) = make_uint4(0u, 0u, 0u, 0u);
+  const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 f = __bfloat1622float2(b[e]);
+    o[2 * e] = f.x;
+    o[2 * e + 1] = f.y;
+  }
+}
+template <typename Acc>
+__global__ void __launch_bounds__(512) residual_rmsnorm_kernel(Acc* __restrict__ acc, int64_t lda,
                                                                __nv_bfloat16* __restrict__ x,
                                                                const __nv_bfloat16* __restrict__ g,
                                                                __nv_bfloat16* __restrict__ y, int h, float eps,
@@ -94,16 +113,14 @@ __global__ void __launch_bounds__(512) residual_rmsnorm_kernel(float* __restrict
   side_zero(z);
   __shared__ float red[16];
   const int64_t t = blockIdx.x;
-  float* ar = acc + t * lda;
+  Acc* ar = acc + t * lda;
   uint4* xr = reinterpret_cast<uint4*>(x + t * h);
   float ss = 0.f;
   for (int i = threadIdx.x; i < h / 8; i += blockDim.x) {
-    float4 a0 = *reinterpret_cast<float4*>(ar + 8 * i), a1 = *reinterpret_cast<float4*>(ar + 8 * i + 4);
-    *reinterpret_cast<float4*>(ar + 8 * i) = make_float4(0.f, 0.f, 0.f, 0.f);
-    *reinterpret_cast<float4*>(ar + 8 * i + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+    float av[8];
+    take8(ar + 8 * i, av);
     uint4 v = xr[i];
     __nv_bfloat162* b = reinterpret_cast<__nv_bfloat162*>(&v);
-    const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       float2 f = __bfloat1622float2(b[e]);
@@ -462,8 +479,15 @@ dl_status launch_residual_rmsnorm(float* acc, int64_t lda, __nv_bfloat16* x, con
                                   __nv_bfloat16* y, int64_t T, int64_t h, float eps, cudaStream_t st,
                                   const SideZero& z) {
   if (T <= 0) return DL_OK;
-  return launch_pdl(residual_rmsnorm_kernel, dim3(static_cast<unsigned>(T)), dim3(512), 0, st, "residual_rmsnorm",
-                    acc, lda, x, g, y, static_cast<int>(h), eps, z);
+  return launch_pdl(residual_rmsnorm_kernel<float>, dim3(static_cast<unsigned>(T)), dim3(512), 0, st,
+                    "residual_rmsnorm", acc, lda, x, g, y, static_cast<int>(h), eps, z);
+}
+dl_status launch_residual_rmsnorm_bf16(__nv_bfloat16* acc, int64_t lda, __nv_bfloat16* x, const __nv_bfloat16* g,
+                                       __nv_bfloat16* y, int64_t T, int64_t h, float eps, cudaStream_t st,
+                                       const SideZero& z) {
+  if (T <= 0) return DL_OK;
+  return launch_pdl(residual_rmsnorm_kernel<__nv_bfloat16>, dim3(static_cast<unsigned>(T)), dim3(512), 0, st,
+                    "residual_rmsnorm_bf16", acc, lda, x, g, y, static_cast<int>(h), eps, z);
 }
 dl_status launch_f32_to_bf16(float* acc, int64_t lda, __nv_bfloat16* out, int64_t ldo, int64_t T, int64_t n,
                              int clear, cudaStream_t st, const SideZero& z) {

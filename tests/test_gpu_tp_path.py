@@ -62,6 +62,16 @@ for rep in range(2):                      # twice: the bf16 reduction / collecti
     dl.dl_decomposed_block_forward(cfg, wd, xd, cl, None, S, dl.DL_DECODE, kc.cuda(), vc.cuda(), cl, comm, ws)
     torch.cuda.synchronize()
     errs.append(rel(xd.cpu().double() - x.double(), ref - x.double().numpy()))
+if LAYOUT == 0:                           # two-layer stack (residual fused with the next norm)
+    cl2 = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    k2 = [kc.cuda(), kc.cuda()]; v2 = [vc.cuda(), vc.cuda()]
+    st_args = dl.StackArgs([wd, wd], k2, v2)
+    xd = x.cuda()
+    dl.dl_decomposed_stack_forward(cfg, st_args, xd, cl2, None, S, dl.DL_DECODE, cl2, comm, ws)
+    torch.cuda.synchronize()
+    x1 = torch.tensor(ref)
+    ref2, _, _ = oracle.block_decode(cfgo, w, x1, ko, vo, lens)
+    errs.append(rel(xd.cpu().double() - x.double(), ref2 - x.double().numpy()))
 print("ERRS", errs)
 dist.destroy_process_group()
 '''
