@@ -412,6 +412,12 @@ dl_status dl_debug_gemm_trace(void *device_buf);
  * finished phase p, [28+p] time the TMA producer issued phase p's activation
  * loads, [46] entry, [47] SM id.  Slots are assigned in launch order. */
 dl_status dl_debug_fused_trace(void *device_buf);
+/* Debug timeline of the non-GEMM decode kernels (SiLU*up, residual +
+ * RMSNorm, RoPE + cache append, stream-K attention): device_buf >= 4 u64 per
+ * launch of the next launches (kind 1-4, then globaltimer ns of the first CTA
+ * entry, the first return from griddepcontrol.wait, the last CTA end; fill
+ * entries 1-2 with ~0 and 3 with 0 before the run), or NULL to disable.     */
+dl_status dl_debug_ew_trace(void *device_buf);
 
 #ifdef __cplusplus
 }

@@ -25,7 +25,7 @@ EXPORTS = ("dl_last_error", "dl_version", "dl_device_ok", "dl_comm_create", "dl_
            "dl_dense_workspace", "dl_dense", "dl_launch_count", "dl_profile_begin", "dl_profile_end",
            "dl_profile_count", "dl_profile_get", "dl_debug_gemm_trace", "dl_debug_fused_trace", "dl_deinfer_shard_factors",
            "dl_kv_prepare", "dl_decomposed_block_forward_kvlr", "dl_comm_create_loopback",
-           "dl_decomposed_stack_forward")
+           "dl_decomposed_stack_forward", "dl_debug_ew_trace")
 
 
 class DLError(RuntimeError):
@@ -110,6 +110,7 @@ def load():
             lib.dl_profile_get.argtypes = [I, P, P, P, P]
             lib.dl_debug_gemm_trace.argtypes = [P]
             lib.dl_debug_fused_trace.argtypes = [P]
+            lib.dl_debug_ew_trace.argtypes = [P]
             lib.dl_deinfer_shard_factors.argtypes = [I, I, P, P, P, P, P, P, I64, I, I, I, P, I64, P, P, P]
             lib.dl_comm_create_loopback.argtypes = [I, I, ctypes.POINTER(P)]
             lib.dl_kv_prepare.argtypes = [P, I64, P, I32, I64, I64, I64, P, P, P, P, P]
@@ -516,6 +517,11 @@ def dl_profile_records():
         _check(L.dl_profile_get(i, ctypes.byref(ms), ctypes.byref(b), ctypes.byref(f), ctypes.byref(k)))
         out.append((ms.value, b.value, f.value, k.value))
     return out
+
+
+def dl_debug_ew_trace(buf: torch.Tensor | None):
+    """Timeline of the non-GEMM decode kernels (see include/dl.h); None disables."""
+    _check(load().dl_debug_ew_trace(_ptr(buf)))
 
 
 def dl_debug_fused_trace(buf: torch.Tensor | None):

@@ -1394,17 +1394,24 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
 
   // ---- MLP: gate|up group, SiLU(gate)*up (or ReLU(up)), down + residual ---------
   const int64_t ngu = n_gu * d.m;
-  GemmOut gu_out = skinny ? out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0) : out_plain(ws.yb, ngu, OUT_BF16, 0);
-  if (tpr) gu_out = out_plain(ws.yr, ngu, OUT_BF16_RED, 0);
   // SiLU(gate)*up by the gate|up stage-2 last-contributor fixup: with all
   // fixups (DL_FIXUP) or alone (DL_FIXUP_SILU; the latent stays in Z slot 1
   // until the down group's finalize clears it)
   static const bool fix_silu = getenv("DL_FIXUP_SILU") && atoi(getenv("DL_FIXUP_SILU")) != 0;
   const bool fx_gu = (fx || (fix_silu && skinny && !tp)) && d.glu;
+  GemmOut gu_out = skinny ? out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0) : out_plain(ws.yb, ngu, OUT_BF16, 0);
+  // skinny TP = 1: gate|up partials as bf16x2 reductions too (the SiLU input is
+  // bf16-rounded anyway); halves the reduction and finalize traffic (DL_GU_F32 A/B)
+  static const bool gu_f32 = getenv("DL_GU_F32") != nullptr;
+  const bool gur = skinny && !tp && use_zred() && !fx_gu && !gu_f32;
+  if (tpr || gur) gu_out = out_plain(ws.yr, ngu, OUT_BF16_RED, 0);
   const GemmFixup fsilu = fixup(fx_gu ? FIX_SILU : FIX_NONE);
   DL_TRY(run_group(w->gu, n_gu, gu_rows, ws.xn, d.h, d.h, T, skinny, ws, gu_out, st, &fsilu, fx ? nullptr : &zg, 1));
   if (fx_gu) {
     // SiLU(gate)*up done by the gate|up stage-2 fixup
+  } else if (!tp && gur) {
+    if (d.glu) DL_TRY(launch_silu_mul_bf16(ws.yr, ngu, ws.act, d.m, T, d.m, st, 1, zg));
+    else DL_TRY(launch_relu_bf16(ws.yr, ngu, ws.act, d.m, T, d.m, st, 1, zg));
   } else if (!tp && skinny) {
     if (d.glu) DL_TRY(launch_silu_mul_f32(ws.yf, ws.ldy32, ws.act, d.m, T, d.m, 1, st, zg));
     else DL_TRY(launch_relu_f32(ws.yf, ws.ldy32, ws.act, d.m, T, d.m, 1, st, zg));

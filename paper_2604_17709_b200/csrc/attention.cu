@@ -502,6 +502,7 @@ struct SkArgs {
   int64_t kv_bs;
   float* part;                    // [kMaxGrid][2][16][2 + D]
   unsigned* cnt;                  // [items], zero-maintained
+  EwTrace tr;                     // debug timeline (dl_debug_ew_trace)
 };
 
 struct SkItem {
@@ -556,6 +557,7 @@ __global__ void __launch_bounds__(sk::kThreads, sk::kPerSM)
   uint64_t* empty = full + NS;
   int32_t* P = reinterpret_cast<int32_t*>(empty + NS);
 
+  ew_mark(a.tr, 1);
   pdl_trigger();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int per_seq = a.Hk * a.nch;
@@ -645,6 +647,7 @@ __global__ void __launch_bounds__(sk::kThreads, sk::kPerSM)
 
   // ============================== compute ==============================
   pdl_wait();
+  ew_mark(a.tr, 2);
   const int w = warp;
   const int g8 = lane >> 2, t4 = lane & 3;
   const float scale = rsqrtf(static_cast<float>(D)) * 1.4426950408889634f;
@@ -871,6 +874,7 @@ __global__ void __launch_bounds__(sk::kThreads, sk::kPerSM)
     }
     g = e;
   }
+  ew_mark(a.tr, 3);
 }
 
 }  // namespace
@@ -911,6 +915,7 @@ dl_status launch_attention_sk(const AttnArgs& a, cudaStream_t st) {
   k.kv_blk0 = a.kv_blk0;
   k.kv_bs = a.kv_bs;
   k.cnt = static_cast<unsigned*>(a.sk_ws);
+  k.tr = ew_trace(4);
   k.part = reinterpret_cast<float*>(static_cast<uint8_t*>(a.sk_ws) + (a.sk_items_cap + 63) / 64 * 64 * 4 * 4);
   const size_t smem = sk::smem_bytes(a.num_seqs);
   static size_t attr = 0;

@@ -155,6 +155,27 @@ dl_status tc_gemm(const GemmProblem& p, bool stream_k, cudaStream_t st);
 // (globaltimer ns at entry, setup done, first TMA, first stage landed, last
 // MMA issued, epilogue done, exit; and its SM id)
 dl_status set_gemm_trace(void* buf);
+// Debug timeline of selected non-GEMM kernels (dl_debug_ew_trace): per launch
+// slot 4 u64 = {kind, min entry, min start after griddepcontrol.wait, max end}.
+dl_status set_ew_trace(void* buf);
+int ew_trace_slot();   // next slot (host), -1 when tracing is off
+struct EwTrace {
+  unsigned long long* buf;   // null: off
+  int slot, kind;
+};
+EwTrace ew_trace(int kind);
+__device__ __forceinline__ unsigned long long ew_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void ew_mark(const EwTrace& tr, int field) {   // field 1 entry, 2 start, 3 end
+  if (!tr.buf || threadIdx.x != 0) return;
+  unsigned long long* r = tr.buf + static_cast<long long>(tr.slot) * 4;
+  if (field == 1) r[0] = static_cast<unsigned long long>(tr.kind);
+  if (field == 3) atomicMax(r + 3, ew_now());
+  else atomicMin(r + field, ew_now());
+}
 
 // 2-D bf16 TMA map over a row-major [rows x cols] matrix (ld elements), box
 // {64 cols, box_rows}, 128B swizzle, out-of-bounds elements read as zero.

@@ -11,10 +11,30 @@
 #include <math.h>
 
 #include <algorithm>
+#include <stdlib.h>
 
 #include "dl_internal.h"
 
 namespace dl {
+namespace {
+unsigned long long* g_ew_buf = nullptr;   // host copy of the trace buffer pointer
+int g_ew_next = 0;
+}  // namespace
+
+dl_status set_ew_trace(void* buf) {
+  g_ew_buf = static_cast<unsigned long long*>(buf);
+  g_ew_next = 0;
+  return DL_OK;
+}
+EwTrace ew_trace(int kind) {
+  EwTrace t{nullptr, -1, kind};
+  if (g_ew_buf) {
+    t.buf = g_ew_buf;
+    t.slot = g_ew_next++;
+  }
+  return t;
+}
+
 namespace {
 
 // SideZero job: 16-byte zero stores spread over every thread of the grid.
@@ -102,59 +122,169 @@ __device__ __forceinline__ void take8(__nv_bfloat16* p, float* o) {
     o[2 * e + 1] = f.y;
   }
 }
+// One CTA (1,024 threads) per row, h <= 16,384 (h % 8 == 0): every thread
+// issues all its loads (accumulator, x, gamma) before any math, so the row
+// costs one memory round trip plus the block reduction; x and the norm
+// input stay in registers.
+constexpr int kRnThreads = 1024;
+constexpr int kRnChunks = 2;   // 8-element chunks per thread
 template <typename Acc>
-__global__ void __launch_bounds__(512) residual_rmsnorm_kernel(Acc* __restrict__ acc, int64_t lda,
-                                                               __nv_bfloat16* __restrict__ x,
-                                                               const __nv_bfloat16* __restrict__ g,
-                                                               __nv_bfloat16* __restrict__ y, int h, float eps,
-                                                               SideZero z) {
+__global__ void __launch_bounds__(kRnThreads) residual_rmsnorm_kernel(Acc* __restrict__ acc, int64_t lda,
+                                                                      __nv_bfloat16* __restrict__ x,
+                                                                      const __nv_bfloat16* __restrict__ g,
+                                                                      __nv_bfloat16* __restrict__ y, int h, float eps,
+                                                                      SideZero z, EwTrace tr) {
+  ew_mark(tr, 1);
   pdl_trigger();   // successor may launch now; it waits for us before reading
   pdl_wait();
+  ew_mark(tr, 2);
   side_zero(z);
-  __shared__ float red[16];
+  __shared__ float red[32];
   const int64_t t = blockIdx.x;
   Acc* ar = acc + t * lda;
   uint4* xr = reinterpret_cast<uint4*>(x + t * h);
+  const uint4* gr = reinterpret_cast<const uint4*>(g);
+  const int n8 = h / 8;
+  float av[kRnChunks][8];
+  uint4 v[kRnChunks], gv[kRnChunks];
+#pragma unroll
+  for (int k = 0; k < kRnChunks; ++k) {
+    const int i = threadIdx.x + k * kRnThreads;
+    if (i < n8) {
+      take8(ar + 8 * i, av[k]);
+      v[k] = xr[i];
+      gv[k] = gr[i];
+    }
+  }
   float ss = 0.f;
-  for (int i = threadIdx.x; i < h / 8; i += blockDim.x) {
-    float av[8];
-    take8(ar + 8 * i, av);
-    uint4 v = xr[i];
-    __nv_bfloat162* b = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+  for (int k = 0; k < kRnChunks; ++k) {
+    const int i = threadIdx.x + k * kRnThreads;
+    if (i >= n8) continue;
+    __nv_bfloat162* b = reinterpret_cast<__nv_bfloat162*>(&v[k]);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       float2 f = __bfloat1622float2(b[e]);
-      b[e] = __floats2bfloat162_rn(f.x + av[2 * e], f.y + av[2 * e + 1]);
-      f = __bfloat1622float2(b[e]);
+      b[e] = __floats2bfloat162_rn(f.x + av[k][2 * e], f.y + av[k][2 * e + 1]);
+      f = __bfloat1622float2(b[e]);   // the norm reads the bf16-rounded x
       ss += f.x * f.x + f.y * f.y;
     }
-    xr[i] = v;
+    xr[i] = v[k];
   }
   ss = warp_sum(ss);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
   if (threadIdx.x < 32) {
-    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
-    v = warp_sum(v);
-    if (threadIdx.x == 0) red[0] = v;
+    float s2 = red[threadIdx.x];
+    s2 = warp_sum(s2);
+    if (threadIdx.x == 0) red[0] = s2;
   }
   __syncthreads();
   const float inv = rsqrtf(red[0] / static_cast<float>(h) + eps);
-  const uint4* gr = reinterpret_cast<const uint4*>(g);
   uint4* yr = reinterpret_cast<uint4*>(y + t * h);
-  for (int i = threadIdx.x; i < h / 8; i += blockDim.x) {   // same indices: own writes
-    uint4 v = xr[i], gv = gr[i], o;
-    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v);
-    const __nv_bfloat162* gb = reinterpret_cast<const __nv_bfloat162*>(&gv);
+#pragma unroll
+  for (int k = 0; k < kRnChunks; ++k) {
+    const int i = threadIdx.x + k * kRnThreads;
+    if (i >= n8) continue;
+    uint4 o;
+    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v[k]);
+    const __nv_bfloat162* gb = reinterpret_cast<const __nv_bfloat162*>(&gv[k]);
     __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&o);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      float2 f = __bfloat1622float2(b[e]);
-      float2 w = __bfloat1622float2(gb[e]);
+      const float2 f = __bfloat1622float2(b[e]);
+      const float2 w = __bfloat1622float2(gb[e]);
       ob[e] = __floats2bfloat162_rn(f.x * inv * w.x, f.y * inv * w.y);
     }
     yr[i] = o;
   }
+  __syncthreads();
+  ew_mark(tr, 3);
+}
+
+// act[t][c..c+7] = bf16(silu(gate) * up) from the fp32 stage-2 accumulator
+// (gate at column c, up at m + c; both consumed and cleared).  Flat item
+// space (t, 8-column group), grid-stride, kSiluU items per thread with every
+// load issued before any store.
+constexpr int kSiluU = 4;
+// 8 accumulator values at p (fp32 or bf16), then zero them
+__device__ __forceinline__ void ld8(const float* p, float* o) {
+  const float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+  o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w; o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
+}
+__device__ __forceinline__ void ld8(const __nv_bfloat16* p, float* o) {
+  const uint4 v = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 f = __bfloat1622float2(b[e]);
+    o[2 * e] = f.x;
+    o[2 * e + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void zero8(float* p) {
+  *reinterpret_cast<float4*>(p) = make_float4(0.f, 0.f, 0.f, 0.f);
+  *reinterpret_cast<float4*>(p + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+__device__ __forceinline__ void zero8(__nv_bfloat16* p) { *reinterpret_cast<uint4*>(p) = make_uint4(0u, 0u, 0u, 0u); }
+
+template <typename Acc>
+__global__ void __launch_bounds__(256) silu_mul_kernel(Acc* __restrict__ acc, int64_t lda, __nv_bfloat16* __restrict__ out,
+                                                       int64_t ldo, int m, int T, int relu, SideZero z, EwTrace tr) {
+  ew_mark(tr, 1);
+  pdl_trigger();   // successor may launch now; it waits for us before reading
+  pdl_wait();
+  ew_mark(tr, 2);
+  side_zero(z);
+  const unsigned per_row = static_cast<unsigned>(m) / 8, total = per_row * static_cast<unsigned>(T);
+  const unsigned stride = gridDim.x * blockDim.x;
+  const int uoff = relu ? 0 : m;
+  for (unsigned base = blockIdx.x * blockDim.x + threadIdx.x; base < total; base += stride * kSiluU) {
+    float gv[kSiluU][8], uv[kSiluU][8];
+    Acc* pr[kSiluU];
+#pragma unroll
+    for (int u = 0; u < kSiluU; ++u) {
+      const unsigned i = base + u * stride;
+      pr[u] = nullptr;
+      if (i < total) {
+        const unsigned t = i / per_row, c = (i - t * per_row) * 8;
+        pr[u] = acc + static_cast<int64_t>(t) * lda + c;
+        ld8(pr[u] + uoff, uv[u]);
+        if (!relu) ld8(pr[u], gv[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kSiluU; ++u) {
+      if (!pr[u]) continue;
+      const unsigned i = base + u * stride;
+      const unsigned t = i / per_row, c = (i - t * per_row) * 8;
+      zero8(pr[u] + uoff);
+      float o[8];
+      if (relu) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = fmaxf(uv[u][e], 0.f);
+      } else {
+        zero8(pr[u]);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = gv[u][e] / (1.f + __expf(-gv[u][e])) * uv[u][e];
+      }
+      uint4 pk;
+      __nv_bfloat162* pb = reinterpret_cast<__nv_bfloat162*>(&pk);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) pb[e] = __floats2bfloat162_rn(o[2 * e], o[2 * e + 1]);
+      *reinterpret_cast<uint4*>(out + static_cast<int64_t>(t) * ldo + c) = pk;
+    }
+  }
+  __syncthreads();
+  ew_mark(tr, 3);
+}
+template <typename Acc>
+dl_status launch_silu_flat(Acc* acc, int64_t lda, __nv_bfloat16* act, int64_t ldo, int64_t T, int64_t m, int relu,
+                           cudaStream_t st, const SideZero& z) {
+  const int64_t items = T * (m / 8);
+  const int grid = static_cast<int>(std::min<int64_t>((items + 256 * kSiluU - 1) / (256 * kSiluU), 8 * num_sms()));
+  return launch_pdl(silu_mul_kernel<Acc>, dim3(grid > 0 ? grid : 1), dim3(256), 0, st, "silu_mul", acc, lda, act, ldo,
+                    static_cast<int>(m), static_cast<int>(T), relu, z, ew_trace(1));
 }
 
 // 2-D elementwise over [T x n] in groups of 4 columns: grid (ceil(n/4/256), T).
@@ -257,58 +387,66 @@ struct ReluBf16 {
 
 // RoPE + cache append.  grid (ceil(heads*d/4 / 128), T); one thread per 4 dims
 // = two rotation pairs (2i, 2i+1) by pos * theta^(-2i/d).
-__global__ void __launch_bounds__(128) rope_cache_kernel(RopeCacheArgs a) {
+__global__ void __launch_bounds__(128) rope_cache_kernel(RopeCacheArgs a, EwTrace tr) {
+  ew_mark(tr, 1);
   pdl_trigger();   // successor may launch now; it waits for us before reading
-  pdl_wait();
-  side_zero(a.zero);
-  side_zero(a.zero2);
+  // Everything that depends only on the call's inputs (positions, cache
+  // lengths, cu_seqlens -- never written inside the block) is done before
+  // griddepcontrol.wait: the angles and the cache slot, overlapping the
+  // predecessor's tail.  After the wait: one load, rotate, one store.
   const int heads = a.Hq + 2 * a.Hk;
   const int quads = a.d / 4;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= heads * quads) return;
+  const bool active = i < heads * quads;
   const int64_t t = blockIdx.y;
-  const int hd = i / quads;
+  const int hd = active ? i / quads : 0;
   const int e = (i - hd * quads) * 4;
   const int64_t col = static_cast<int64_t>(hd) * a.d + e;
+  float sn0 = 0.f, cs0 = 1.f, sn1 = 0.f, cs1 = 1.f;
+  const bool rot = active && a.rope && hd < a.Hq + a.Hk;
+  if (rot) {
+    // angle = pos * theta^(-2i/d) in fp32 (relative error ~1e-7, i.e. <= 3e-4 rad at
+    // position 2048, far below bf16 resolution); full-range-reduction sincosf
+    const float pos = static_cast<float>(a.positions[t]);
+    const float l2t = log2f(a.theta);
+    sincosf(pos * exp2f(-l2t * static_cast<float>(e) / a.d), &sn0, &cs0);
+    sincosf(pos * exp2f(-l2t * static_cast<float>(e + 2) / a.d), &sn1, &cs1);
+  }
+  __nv_bfloat16* dst = nullptr;
+  if (active && hd >= a.Hq) {
+    int s;
+    int64_t cpos;
+    if (a.decode) {
+      s = static_cast<int>(t);
+      cpos = a.cache_lens[s];
+    } else {
+      int lo = 0, hi = a.num_seqs - 1;   // last s with cu[s] <= t
+      while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (a.cu_seqlens[mid] <= t) lo = mid; else hi = mid - 1;
+      }
+      s = lo;
+      cpos = a.cache_lens[s] + (t - a.cu_seqlens[s]);
+    }
+    const bool is_k = hd < a.Hq + a.Hk;
+    const int kvh = is_k ? hd - a.Hq : hd - a.Hq - a.Hk;
+    dst = (is_k ? a.k_cache : a.v_cache) + ((static_cast<int64_t>(s) * a.Hk + kvh) * a.max_seq + cpos) * a.d + e;
+  }
+  pdl_wait();
+  ew_mark(tr, 2);
+  side_zero(a.zero);
+  side_zero(a.zero2);
+  if (!active) return;
   float4 v;
   if (a.acc) {
     v = take4(const_cast<float*>(a.acc) + t * a.ld_src + col, a.clear);
   } else {
     v = load4(a.src + t * a.ld_src + col);
   }
-  if (a.rope && hd < a.Hq + a.Hk) {
-    // angle = pos * theta^(-2i/d) in fp32 (relative error ~1e-7, i.e. <= 3e-4 rad at
-    // position 2048, far below bf16 resolution); full-range-reduction sincosf
-    const float pos = static_cast<float>(a.positions[t]);
-    const float l2t = log2f(a.theta);
-    float sn0, cs0, sn1, cs1;
-    sincosf(pos * exp2f(-l2t * static_cast<float>(e) / a.d), &sn0, &cs0);
-    sincosf(pos * exp2f(-l2t * static_cast<float>(e + 2) / a.d), &sn1, &cs1);
-    v = make_float4(v.x * cs0 - v.y * sn0, v.x * sn0 + v.y * cs0, v.z * cs1 - v.w * sn1, v.z * sn1 + v.w * cs1);
-  }
-  if (hd < a.Hq) {
-    store4(a.q_out + t * static_cast<int64_t>(a.Hq) * a.d + col, v.x, v.y, v.z, v.w);
-    return;
-  }
-  int s;
-  int64_t cpos;
-  if (a.decode) {
-    s = static_cast<int>(t);
-    cpos = a.cache_lens[s];
-  } else {
-    int lo = 0, hi = a.num_seqs - 1;   // last s with cu[s] <= t
-    while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (a.cu_seqlens[mid] <= t) lo = mid; else hi = mid - 1;
-    }
-    s = lo;
-    cpos = a.cache_lens[s] + (t - a.cu_seqlens[s]);
-  }
-  const bool is_k = hd < a.Hq + a.Hk;
-  const int kvh = is_k ? hd - a.Hq : hd - a.Hq - a.Hk;
-  __nv_bfloat16* dst = (is_k ? a.k_cache : a.v_cache) +
-                       ((static_cast<int64_t>(s) * a.Hk + kvh) * a.max_seq + cpos) * a.d + e;
-  store4(dst, v.x, v.y, v.z, v.w);
+  if (rot) v = make_float4(v.x * cs0 - v.y * sn0, v.x * sn0 + v.y * cs0, v.z * cs1 - v.w * sn1, v.z * sn1 + v.w * cs1);
+  if (hd < a.Hq) store4(a.q_out + t * static_cast<int64_t>(a.Hq) * a.d + col, v.x, v.y, v.z, v.w);
+  else store4(dst, v.x, v.y, v.z, v.w);
+  ew_mark(tr, 3);
 }
 
 __global__ void __launch_bounds__(256) embedding_kernel(const __nv_bfloat16* __restrict__ table, int64_t h,
@@ -479,15 +617,23 @@ dl_status launch_residual_rmsnorm(float* acc, int64_t lda, __nv_bfloat16* x, con
                                   __nv_bfloat16* y, int64_t T, int64_t h, float eps, cudaStream_t st,
                                   const SideZero& z) {
   if (T <= 0) return DL_OK;
-  return launch_pdl(residual_rmsnorm_kernel<float>, dim3(static_cast<unsigned>(T)), dim3(512), 0, st,
-                    "residual_rmsnorm", acc, lda, x, g, y, static_cast<int>(h), eps, z);
+  if (h % 8 || h / 8 > kRnThreads * kRnChunks) {
+    set_error("residual_rmsnorm: h=%lld unsupported (multiple of 8, <= %d)", (long long)h, 8 * kRnThreads * kRnChunks);
+    return DL_ERR_UNSUPPORTED;
+  }
+  return launch_pdl(residual_rmsnorm_kernel<float>, dim3(static_cast<unsigned>(T)), dim3(kRnThreads), 0, st,
+                    "residual_rmsnorm", acc, lda, x, g, y, static_cast<int>(h), eps, z, ew_trace(2));
 }
 dl_status launch_residual_rmsnorm_bf16(__nv_bfloat16* acc, int64_t lda, __nv_bfloat16* x, const __nv_bfloat16* g,
                                        __nv_bfloat16* y, int64_t T, int64_t h, float eps, cudaStream_t st,
                                        const SideZero& z) {
   if (T <= 0) return DL_OK;
-  return launch_pdl(residual_rmsnorm_kernel<__nv_bfloat16>, dim3(static_cast<unsigned>(T)), dim3(512), 0, st,
-                    "residual_rmsnorm_bf16", acc, lda, x, g, y, static_cast<int>(h), eps, z);
+  if (h % 8 || h / 8 > kRnThreads * kRnChunks) {
+    set_error("residual_rmsnorm: h=%lld unsupported (multiple of 8, <= %d)", (long long)h, 8 * kRnThreads * kRnChunks);
+    return DL_ERR_UNSUPPORTED;
+  }
+  return launch_pdl(residual_rmsnorm_kernel<__nv_bfloat16>, dim3(static_cast<unsigned>(T)), dim3(kRnThreads), 0, st,
+                    "residual_rmsnorm_bf16", acc, lda, x, g, y, static_cast<int>(h), eps, z, ew_trace(2));
 }
 dl_status launch_f32_to_bf16(float* acc, int64_t lda, __nv_bfloat16* out, int64_t ldo, int64_t T, int64_t n,
                              int clear, cudaStream_t st, const SideZero& z) {
@@ -504,10 +650,16 @@ dl_status launch_residual_add_bf16(const __nv_bfloat16* y, int64_t ldy, __nv_bfl
 }
 dl_status launch_silu_mul_f32(float* acc, int64_t lda, __nv_bfloat16* act, int64_t ldo, int64_t T, int64_t m,
                               int clear, cudaStream_t st, const SideZero& z) {
+  static const bool ew4 = getenv("DL_SILU_EW4") != nullptr;   // A/B switch
+  if (!ew4 && clear && m % 8 == 0 && lda % 4 == 0 && ldo % 8 == 0 && T > 0) {
+    return launch_silu_flat(acc, lda, act, ldo, T, m, 0, st, z);
+  }
   return launch_ew4(T, m, SiluMulF32{acc, lda, act, ldo, m, clear}, st, "silu_mul_f32", z);
 }
 dl_status launch_silu_mul_bf16(const __nv_bfloat16* src, int64_t lds, __nv_bfloat16* act, int64_t ldo, int64_t T,
                                int64_t m, cudaStream_t st, int clear, const SideZero& z) {
+  if (clear && m % 8 == 0 && lds % 8 == 0 && ldo % 8 == 0 && T > 0)
+    return launch_silu_flat(const_cast<__nv_bfloat16*>(src), lds, act, ldo, T, m, 0, st, z);
   return launch_ew4(T, m, SiluMulBf16{const_cast<__nv_bfloat16*>(src), lds, act, ldo, m, clear}, st, "silu_mul_bf16",
                     z);
 }
@@ -517,13 +669,15 @@ dl_status launch_relu_f32(float* acc, int64_t lda, __nv_bfloat16* act, int64_t l
 }
 dl_status launch_relu_bf16(const __nv_bfloat16* src, int64_t lds, __nv_bfloat16* act, int64_t ldo, int64_t T,
                            int64_t m, cudaStream_t st, int clear, const SideZero& z) {
+  if (clear && m % 8 == 0 && lds % 8 == 0 && ldo % 8 == 0 && T > 0)
+    return launch_silu_flat(const_cast<__nv_bfloat16*>(src), lds, act, ldo, T, m, 1, st, z);
   return launch_ew4(T, m, ReluBf16{const_cast<__nv_bfloat16*>(src), lds, act, ldo, clear}, st, "relu_bf16", z);
 }
 dl_status launch_rope_cache(const RopeCacheArgs& a, cudaStream_t st) {
   if (a.T <= 0) return DL_OK;
   const int per_tok = (a.Hq + 2 * a.Hk) * (a.d / 4);
   dim3 grid((per_tok + 127) / 128, static_cast<unsigned>(a.T));
-  return launch_pdl(rope_cache_kernel, grid, dim3(128), 0, st, "rope_cache", a);
+  return launch_pdl(rope_cache_kernel, grid, dim3(128), 0, st, "rope_cache", a, ew_trace(3));
 }
 dl_status launch_embedding(const __nv_bfloat16* table, int64_t vocab, int64_t h, const int32_t* ids, int64_t T,
                            __nv_bfloat16* out, cudaStream_t st) {

@@ -33,6 +33,8 @@ torch.cuda.synchronize()
 slots = 16 * a.layers + 8
 buf = torch.zeros(slots * 148 * 8, dtype=torch.int64, device=dev)
 _lib.dl_debug_gemm_trace(buf)
+ew = torch.zeros(256 * a.layers * 4, dtype=torch.int64, device=dev)
+_lib.dl_debug_ew_trace(ew)                       # slots are assigned at capture
 g = torch.cuda.CUDAGraph()
 with torch.cuda.graph(g, stream=st):
     m.decode_step()
@@ -40,11 +42,14 @@ with torch.cuda.stream(st):
     g.replay()
 torch.cuda.synchronize()
 buf.zero_()
+ew.zero_()
+ew.view(-1, 4)[:, 1:3] = -1                      # 0xffff... for the atomicMin fields
 e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
 with torch.cuda.stream(st):
     e0.record(st); g.replay(); e1.record(st)
 torch.cuda.synchronize()
 _lib.dl_debug_gemm_trace(None)
+_lib.dl_debug_ew_trace(None)
 step_us = e0.elapsed_time(e1) * 1e3
 t = buf.view(slots, 148, 8).cpu().double()
 rows = []
@@ -69,3 +74,11 @@ for i, st_, land, end, first_end, n in rows:
           f"{(first_end - t0) / 1e3:11.1f} {gap:6.1f} {n:5d}")
     prev_end = end
 print(f"sum of GEMM spans {tot_gemm:.1f} us; last end {(rows[-1][3] - t0) / 1e3:.1f} us")
+names = {1: "silu", 2: "res+norm", 3: "rope", 4: "attention"}
+ev = ew.view(-1, 4).cpu()
+print("non-GEMM kernels (us from the first GEMM start): entry / after-wait / end")
+for r in ev:
+    if int(r[0]) == 0:
+        continue
+    f = lambda v: (v.item() - t0) / 1e3 if v.item() > 0 else float("nan")  # noqa: E731
+    print(f"  {names.get(int(r[0]), r[0])}: {f(r[1]):8.1f} {f(r[2]):8.1f} {f(r[3]):8.1f}  run {f(r[3]) - f(r[2]):6.1f}")

@@ -12,6 +12,12 @@ __global__ void red4(float* p, int n, int reps) {
     for (int i = (blockIdx.x * blockDim.x + threadIdx.x) * 4; i < n; i += gridDim.x * blockDim.x * 4)
       asm volatile("red.global.add.v4.f32 [%0], {%1,%1,%1,%1};" ::"l"(p + i), "f"(1.f) : "memory");
 }
+__global__ void red2bf(float* p, int n, int reps) {   // packed bf16x2 adds over the same bytes
+  unsigned* q = reinterpret_cast<unsigned*>(p);
+  for (int r = 0; r < reps; ++r)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+      asm volatile("red.global.add.noftz.bf16x2 [%0], %1;" ::"l"(q + i), "r"(0x3f803f80u) : "memory");
+}
 __global__ void st4(float* p, int n, int reps) {
   for (int r = 0; r < reps; ++r)
     for (int i = (blockIdx.x * blockDim.x + threadIdx.x) * 4; i < n; i += gridDim.x * blockDim.x * 4)
@@ -41,6 +47,7 @@ int main() {
   };
   run("red.f32", [&] { red1<<<148 * 8, 256>>>(p, n, reps); });
   run("red.v4", [&] { red4<<<148 * 8, 256>>>(p, n, reps); });
+  run("red.bf16x2", [&] { red2bf<<<148 * 8, 256>>>(p, n, reps); });
   run("st.v4", [&] { st4<<<148 * 8, 256>>>(p, n, reps); });
   run("ld.cg.v4", [&] { ld4<<<148 * 8, 256>>>(p, n, reps, o); });
   return 0;
