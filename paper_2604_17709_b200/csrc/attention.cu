@@ -19,6 +19,7 @@
 //   tile 4 ways and are merged (log-sum-exp) through shared memory; key
 //   splits (for small batch x heads) are merged by a second tiny kernel.
 #include <math.h>
+#include <stdlib.h>
 
 #include "dl_internal.h"
 #include "sm100_ptx.cuh"
@@ -503,6 +504,7 @@ struct SkArgs {
   float* part;                    // [kMaxGrid][2][16][2 + D]
   unsigned* cnt;                  // [items], zero-maintained
   EwTrace tr;                     // debug timeline (dl_debug_ew_trace)
+  int l2pf;                       // old-key tiles prefetched into L2 before griddepcontrol.wait
 };
 
 struct SkItem {
@@ -632,6 +634,20 @@ __global__ void __launch_bounds__(sk::kThreads, sk::kPerSM)
         if ((t + 1) * KT > it.n_keys - 1) break;   // tile holds the key appended by this step
         issue(it, pre);
         ++pre;
+      }
+      // ... and the next l2pf old-key tiles into L2 (HBM is otherwise idle
+      // while the predecessor finishes)
+      int64_t g = pre;
+      for (int n = 0; n < a.l2pf && g < b1; ++n, ++g) {
+        sk_item_at(P, a.num_seqs, per_seq, g, it, a.cache_lens);
+        const int t = static_cast<int>(g - it.start);
+        if ((t + 1) * KT > it.n_keys - 1) continue;
+        int row, col;
+        tile_coords(it, g, row, col);
+        ptx::tma_prefetch_2d(&maps.k, col, row);
+        ptx::tma_prefetch_2d(&maps.k, col + 64, row);
+        ptx::tma_prefetch_2d(&maps.v, col, row);
+        ptx::tma_prefetch_2d(&maps.v, col + 64, row);
       }
     }
     pdl_wait();
@@ -916,6 +932,8 @@ dl_status launch_attention_sk(const AttnArgs& a, cudaStream_t st) {
   k.kv_bs = a.kv_bs;
   k.cnt = static_cast<unsigned*>(a.sk_ws);
   k.tr = ew_trace(4);
+  static const int l2pf = getenv("DL_ATTN_L2PF") ? atoi(getenv("DL_ATTN_L2PF")) : 0;
+  k.l2pf = l2pf;
   k.part = reinterpret_cast<float*>(static_cast<uint8_t*>(a.sk_ws) + (a.sk_items_cap + 63) / 64 * 64 * 4 * 4);
   const size_t smem = sk::smem_bytes(a.num_seqs);
   static size_t attr = 0;

@@ -230,7 +230,8 @@ __device__ __forceinline__ void zero8(__nv_bfloat16* p) { *reinterpret_cast<uint
 
 template <typename Acc>
 __global__ void __launch_bounds__(256) silu_mul_kernel(Acc* __restrict__ acc, int64_t lda, __nv_bfloat16* __restrict__ out,
-                                                       int64_t ldo, int m, int T, int relu, SideZero z, EwTrace tr) {
+                                                       int64_t ldo, int m, int T, int relu, int clear, SideZero z,
+                                                       EwTrace tr) {
   ew_mark(tr, 1);
   pdl_trigger();   // successor may launch now; it waits for us before reading
   pdl_wait();
@@ -258,13 +259,13 @@ __global__ void __launch_bounds__(256) silu_mul_kernel(Acc* __restrict__ acc, in
       if (!pr[u]) continue;
       const unsigned i = base + u * stride;
       const unsigned t = i / per_row, c = (i - t * per_row) * 8;
-      zero8(pr[u] + uoff);
+      if (clear) zero8(pr[u] + uoff);
       float o[8];
       if (relu) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) o[e] = fmaxf(uv[u][e], 0.f);
       } else {
-        zero8(pr[u]);
+        if (clear) zero8(pr[u]);
 #pragma unroll
         for (int e = 0; e < 8; ++e) o[e] = gv[u][e] / (1.f + __expf(-gv[u][e])) * uv[u][e];
       }
@@ -280,11 +281,11 @@ __global__ void __launch_bounds__(256) silu_mul_kernel(Acc* __restrict__ acc, in
 }
 template <typename Acc>
 dl_status launch_silu_flat(Acc* acc, int64_t lda, __nv_bfloat16* act, int64_t ldo, int64_t T, int64_t m, int relu,
-                           cudaStream_t st, const SideZero& z) {
+                           cudaStream_t st, const SideZero& z, int clear = 1) {
   const int64_t items = T * (m / 8);
   const int grid = static_cast<int>(std::min<int64_t>((items + 256 * kSiluU - 1) / (256 * kSiluU), 8 * num_sms()));
   return launch_pdl(silu_mul_kernel<Acc>, dim3(grid > 0 ? grid : 1), dim3(256), 0, st, "silu_mul", acc, lda, act, ldo,
-                    static_cast<int>(m), static_cast<int>(T), relu, z, ew_trace(1));
+                    static_cast<int>(m), static_cast<int>(T), relu, clear, z, ew_trace(1));
 }
 
 // 2-D elementwise over [T x n] in groups of 4 columns: grid (ceil(n/4/256), T).
@@ -658,8 +659,8 @@ dl_status launch_silu_mul_f32(float* acc, int64_t lda, __nv_bfloat16* act, int64
 }
 dl_status launch_silu_mul_bf16(const __nv_bfloat16* src, int64_t lds, __nv_bfloat16* act, int64_t ldo, int64_t T,
                                int64_t m, cudaStream_t st, int clear, const SideZero& z) {
-  if (clear && m % 8 == 0 && lds % 8 == 0 && ldo % 8 == 0 && T > 0)
-    return launch_silu_flat(const_cast<__nv_bfloat16*>(src), lds, act, ldo, T, m, 0, st, z);
+  if (m % 8 == 0 && lds % 8 == 0 && ldo % 8 == 0 && T > 0)
+    return launch_silu_flat(const_cast<__nv_bfloat16*>(src), lds, act, ldo, T, m, 0, st, z, clear);
   return launch_ew4(T, m, SiluMulBf16{const_cast<__nv_bfloat16*>(src), lds, act, ldo, m, clear}, st, "silu_mul_bf16",
                     z);
 }
@@ -669,8 +670,8 @@ dl_status launch_relu_f32(float* acc, int64_t lda, __nv_bfloat16* act, int64_t l
 }
 dl_status launch_relu_bf16(const __nv_bfloat16* src, int64_t lds, __nv_bfloat16* act, int64_t ldo, int64_t T,
                            int64_t m, cudaStream_t st, int clear, const SideZero& z) {
-  if (clear && m % 8 == 0 && lds % 8 == 0 && ldo % 8 == 0 && T > 0)
-    return launch_silu_flat(const_cast<__nv_bfloat16*>(src), lds, act, ldo, T, m, 1, st, z);
+  if (m % 8 == 0 && lds % 8 == 0 && ldo % 8 == 0 && T > 0)
+    return launch_silu_flat(const_cast<__nv_bfloat16*>(src), lds, act, ldo, T, m, 1, st, z, clear);
   return launch_ew4(T, m, ReluBf16{const_cast<__nv_bfloat16*>(src), lds, act, ldo, clear}, st, "relu_bf16", z);
 }
 dl_status launch_rope_cache(const RopeCacheArgs& a, cudaStream_t st) {
