@@ -1213,6 +1213,23 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
     qkv_out.ptr = ws.yr;
     qkv_out.ld = NQKV;
   }
+  // Opt-in (DL_ROPE_FUSE=1): TP = 1 decode with the q|k|v partials as bf16x2
+  // in ws.yr and RoPE + cache append done by the stream-K attention kernel
+  // itself; the o group's residual + MLP-norm kernel clears ws.yr's q|k|v rows.
+  // Measured 0.2-0.3 ms/step slower: without the small RoPE kernel between
+  // them, the attention CTAs only become resident once the q|k|v stage-2
+  // GEMM's CTAs (216 KB of shared memory each) exit, so the old-key tiles are
+  // no longer streamed while the predecessor drains.
+  static const bool no_rope_fuse = !(getenv("DL_ROPE_FUSE") && atoi(getenv("DL_ROPE_FUSE")) != 0);
+  static const bool no_fuse_rn = getenv("DL_NO_FUSE_RESNORM") != nullptr;
+  const bool rope_attn = skinny && !tp && !kv && use_zred() && !use_fixup() && !no_rope_fuse && !no_fuse_rn &&
+                         phase == DL_DECODE && num_seqs <= 1024 && d.d == 128 &&
+                         !(skinny && !tp && !kv && T <= 128 && use_fused());
+  if (rope_attn) {
+    qkv_out.mode = OUT_BF16_RED;
+    qkv_out.ptr = ws.yr;
+    qkv_out.ld = NQKV;
+  }
 
   // skinny, single rank: every group's finalize (RoPE + cache append, residual,
   // SiLU*up) runs in the stage-2 GEMM's last-contributor fixup
@@ -1343,9 +1360,18 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
     rc.src = ws.rs;
     rc.ld_src = d.W;
   }
-  if (!fx && !kv) DL_TRY(launch_rope_cache(rc, st));
-
-  if (!kv) DL_TRY(launch_attention(aa, st));
+  if (rope_attn) {
+    aa.qkv = ws.yr;
+    aa.ld_qkv = NQKV;
+    aa.positions = positions;
+    aa.theta = cfg->rope_theta;
+    aa.rope = cfg->no_rope ? 0 : 1;
+    aa.zero = zq;
+    DL_TRY(launch_attention(aa, st));
+  } else {
+    if (!fx && !kv) DL_TRY(launch_rope_cache(rc, st));
+    if (!kv) DL_TRY(launch_attention(aa, st));
+  }
 
   const __nv_bfloat16* att_in = ws.att;
   if (tp) {
@@ -1382,7 +1408,13 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   static const bool no_fuse = getenv("DL_NO_FUSE_RESNORM") != nullptr;   // A/B timing switch
   if (!fx && !tp && skinny && !no_fuse) {
     // residual add of the o projection fused with the MLP pre-norm
-    DL_TRY(launch_residual_rmsnorm(ws.yf, ws.ldy32, x, mlp_norm, ws.xn, T, d.h, cfg->rms_eps, st, zo));
+    SideZero zqkv;
+    if (rope_attn) {
+      zqkv.p = ws.yr;
+      zqkv.rows = 1;
+      zqkv.row_bytes = zqkv.ld = static_cast<int64_t>(T) * NQKV * 2;
+    }
+    DL_TRY(launch_residual_rmsnorm(ws.yf, ws.ldy32, x, mlp_norm, ws.xn, T, d.h, cfg->rms_eps, st, zo, zqkv));
   } else if (tpr && !no_fuse) {
     // TP: all-reduce of the bf16 partials, then residual + MLP pre-norm in one pass
     DL_TRY(all_reduce(comm, ws.yr, static_cast<size_t>(T) * d.h, kNcclBfloat16, st));

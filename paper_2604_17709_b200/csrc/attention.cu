@@ -505,7 +505,26 @@ struct SkArgs {
   unsigned* cnt;                  // [items], zero-maintained
   EwTrace tr;                     // debug timeline (dl_debug_ew_trace)
   int l2pf;                       // old-key tiles prefetched into L2 before griddepcontrol.wait
+  // fused RoPE + cache append (AttnArgs::qkv)
+  const __nv_bfloat16* qkv;
+  int64_t ld_qkv;
+  const int32_t* positions;
+  float l2t;                      // log2(theta)
+  int rope;
+  __nv_bfloat16* kc;              // head-major caches (written: the appended key / value)
+  __nv_bfloat16* vc;
+  SideZero zero;
 };
+
+// RoPE of the interleaved pair (dim, dim + 1) at position pos (fp32 angle
+// pos * theta^(-dim/128), full-range sincosf -- the rope_cache_kernel expression)
+__device__ __forceinline__ uint32_t rope_pair(uint32_t v, float pos, int dim, float l2t) {
+  __nv_bfloat162 b = *reinterpret_cast<__nv_bfloat162*>(&v);
+  const float2 f = __bfloat1622float2(b);
+  float sn, cs;
+  sincosf(pos * exp2f(-l2t * static_cast<float>(dim) / D), &sn, &cs);
+  return pack_bf16(f.x * cs - f.y * sn, f.x * sn + f.y * cs);
+}
 
 struct SkItem {
   int s, j;                       // sequence, item within the sequence (kvh * nch + ch)
@@ -664,6 +683,14 @@ __global__ void __launch_bounds__(sk::kThreads, sk::kPerSM)
   // ============================== compute ==============================
   pdl_wait();
   ew_mark(a.tr, 2);
+  if (a.zero.p) {   // side clear (the q|k|v group's latent buffer), spread over every compute thread
+    const int64_t per_row = a.zero.row_bytes / 16, total = a.zero.rows * per_row;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * 128 + tid; i < total; i += static_cast<int64_t>(gridDim.x) * 128) {
+      const int64_t r = i / per_row;
+      *reinterpret_cast<uint4*>(static_cast<uint8_t*>(a.zero.p) + r * a.zero.ld + (i - r * per_row) * 16) =
+          make_uint4(0u, 0u, 0u, 0u);
+    }
+  }
   const int w = warp;
   const int g8 = lane >> 2, t4 = lane & 3;
   const float scale = rsqrtf(static_cast<float>(D)) * 1.4426950408889634f;
@@ -678,7 +705,10 @@ __global__ void __launch_bounds__(sk::kThreads, sk::kPerSM)
     // predecessor, so after griddepcontrol.wait; rows >= Gc read as zero
     uint32_t qf[8][4];
     {
-      const uint32_t* q0 = reinterpret_cast<const uint32_t*>(a.q + it.s * ldq + static_cast<int64_t>(h0 + g8) * D);
+      // fused mode: raw q|k|v rows, q rotated here (pair (2i, 2i+1) = one u32)
+      const uint32_t* q0 = a.qkv ? reinterpret_cast<const uint32_t*>(a.qkv + it.s * a.ld_qkv +
+                                                                     static_cast<int64_t>(h0 + g8) * D)
+                                 : reinterpret_cast<const uint32_t*>(a.q + it.s * ldq + static_cast<int64_t>(h0 + g8) * D);
       const uint32_t* q1 = q0 + 8 * (D / 2);
       const bool v0 = g8 < Gc, v1 = g8 + 8 < Gc;
 #pragma unroll
@@ -687,6 +717,49 @@ __global__ void __launch_bounds__(sk::kThreads, sk::kPerSM)
         qf[kk][1] = v1 ? q1[kk * 8 + t4] : 0u;
         qf[kk][2] = v0 ? q0[kk * 8 + 4 + t4] : 0u;
         qf[kk][3] = v1 ? q1[kk * 8 + 4 + t4] : 0u;
+      }
+      if (a.qkv && a.rope) {
+        const float pos = static_cast<float>(a.positions[it.s]);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          float sn0, cs0, sn1, cs1;
+          sincosf(pos * exp2f(-a.l2t * static_cast<float>(kk * 16 + 2 * t4) / D), &sn0, &cs0);
+          sincosf(pos * exp2f(-a.l2t * static_cast<float>(kk * 16 + 8 + 2 * t4) / D), &sn1, &cs1);
+          auto rot = [](uint32_t v, float sn, float cs) {
+            const float2 f = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&v));
+            return pack_bf16(f.x * cs - f.y * sn, f.x * sn + f.y * cs);
+          };
+          qf[kk][0] = rot(qf[kk][0], sn0, cs0);
+          qf[kk][1] = rot(qf[kk][1], sn0, cs0);
+          qf[kk][2] = rot(qf[kk][2], sn1, cs1);
+          qf[kk][3] = rot(qf[kk][3], sn1, cs1);
+        }
+      }
+    }
+    // fused append (a.qkv): the CTA owning the item's last tile holds the new
+    // key (rotated) and value rows: lanes 0-15 one 16-byte chunk of k each,
+    // lanes 16-19 this warp's 4 chunks of v.  They patch the shared-memory
+    // tile (the cache slot TMA read may be stale) and are appended to the cache.
+    const bool own_new = a.qkv && e == it.end;
+    const int newrow = (it.n_keys - 1) & (KT - 1);
+    uint4 nkv = make_uint4(0u, 0u, 0u, 0u);
+    if (own_new && lane < 20) {
+      const int64_t rowoff = it.s * a.ld_qkv + static_cast<int64_t>(a.Hq + kvh) * D;
+      const int chunk = lane < 16 ? lane : w * 4 + (lane - 16);
+      const __nv_bfloat16* srcp = a.qkv + rowoff + (lane < 16 ? 0 : static_cast<int64_t>(a.Hk) * D) + chunk * 8;
+      nkv = *reinterpret_cast<const uint4*>(srcp);
+      if (lane < 16 && a.rope) {
+        const float pos = static_cast<float>(a.positions[it.s]);
+        nkv.x = rope_pair(nkv.x, pos, chunk * 8, a.l2t);
+        nkv.y = rope_pair(nkv.y, pos, chunk * 8 + 2, a.l2t);
+        nkv.z = rope_pair(nkv.z, pos, chunk * 8 + 4, a.l2t);
+        nkv.w = rope_pair(nkv.w, pos, chunk * 8 + 6, a.l2t);
+      }
+      const int64_t dst = ((static_cast<int64_t>(it.s) * a.Hk + kvh) * a.max_seq + (it.n_keys - 1)) * D + chunk * 8;
+      if (lane < 16) {
+        if (w == newrow / 16) *reinterpret_cast<uint4*>(a.kc + dst) = nkv;
+      } else {
+        *reinterpret_cast<uint4*>(a.vc + dst) = nkv;
       }
     }
     float acc[4][4];
@@ -706,8 +779,16 @@ __global__ void __launch_bounds__(sk::kThreads, sk::kPerSM)
           const int key = nv + (i >> 2), chk = w * 4 + (i & 3);
           *reinterpret_cast<uint4*>(stages + st * STAGE + 16384 + sk_swz(0, key, chk)) = make_uint4(0u, 0u, 0u, 0u);
         }
-        __syncwarp();
       }
+      const bool patch = own_new && gt == it.end - 1;
+      if (patch && lane < 20) {
+        if (lane < 16) {
+          if (w == newrow / 16) *reinterpret_cast<uint4*>(stages + st * STAGE + sk_swz(0, newrow, lane)) = nkv;
+        } else {
+          *reinterpret_cast<uint4*>(stages + st * STAGE + 16384 + sk_swz(0, newrow, w * 4 + (lane - 16))) = nkv;
+        }
+      }
+      if (nv < KT || patch) __syncwarp();
       // scores of this warp's 16 keys [16w, 16w + 16) of the tile
       float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
       {
@@ -791,7 +872,7 @@ __global__ void __launch_bounds__(sk::kThreads, sk::kPerSM)
           mma16816(acc[2 * dp + 1], pk, v2, v3);
         }
       }
-      if (nv < KT) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic zeros before the next TMA write
+      if (nv < KT || patch) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes before the next TMA write
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&empty[st]);
     }
@@ -906,6 +987,7 @@ dl_status launch_attention_sk(const AttnArgs& a, cudaStream_t st) {
   const int nch = (a.Hq / a.Hk + 15) / 16;
   const int64_t items = static_cast<int64_t>(a.num_seqs) * a.Hk * nch;
   if (off || !a.decode || a.num_seqs > sk::kMaxSeqs || !a.sk_ws || items > a.sk_items_cap) return DL_ERR_UNSUPPORTED;
+  if (a.qkv && (a.kv_ld || !a.positions || a.ld_qkv % 8)) return DL_ERR_UNSUPPORTED;
   SkMaps maps;
   SkArgs k{};
   const int64_t hk_cols = static_cast<int64_t>(a.Hk) * D;
@@ -932,6 +1014,14 @@ dl_status launch_attention_sk(const AttnArgs& a, cudaStream_t st) {
   k.kv_bs = a.kv_bs;
   k.cnt = static_cast<unsigned*>(a.sk_ws);
   k.tr = ew_trace(4);
+  k.qkv = a.qkv;
+  k.ld_qkv = a.ld_qkv;
+  k.positions = a.positions;
+  k.l2t = log2f(a.theta > 0.f ? a.theta : 1.f);
+  k.rope = a.rope;
+  k.kc = const_cast<__nv_bfloat16*>(a.k_cache);
+  k.vc = const_cast<__nv_bfloat16*>(a.v_cache);
+  k.zero = a.zero;
   static const int l2pf = getenv("DL_ATTN_L2PF") ? atoi(getenv("DL_ATTN_L2PF")) : 0;
   k.l2pf = l2pf;
   k.part = reinterpret_cast<float*>(static_cast<uint8_t*>(a.sk_ws) + (a.sk_items_cap + 63) / 64 * 64 * 4 * 4);
@@ -978,6 +1068,10 @@ dl_status launch_attention(const AttnArgs& a, cudaStream_t st) {
   {
     const dl_status s = launch_attention_sk(a, st);
     if (s != DL_ERR_UNSUPPORTED) return s;
+    if (a.qkv) {
+      set_error("attention: fused RoPE + append needs the stream-K decode kernel");
+      return DL_ERR_UNSUPPORTED;
+    }
   }
   constexpr int SMEM = 16 * ROW_BYTES + 4 * TILE_BYTES + (4 * 16 * D + 128) * 4;
   static bool attr = false;

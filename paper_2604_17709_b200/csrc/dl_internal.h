@@ -244,7 +244,7 @@ dl_status launch_residual_add_f32(float* acc, int64_t ld_acc, __nv_bfloat16* x,
 // x[t][c] = bf16(x + acc) (acc cleared), then y = rmsnorm(x) * g   (h % 8 == 0)
 dl_status launch_residual_rmsnorm(float* acc, int64_t lda, __nv_bfloat16* x, const __nv_bfloat16* g,
                                   __nv_bfloat16* y, int64_t T, int64_t h, float eps, cudaStream_t st,
-                                  const SideZero& z = SideZero{});
+                                  const SideZero& z = SideZero{}, const SideZero& z2 = SideZero{});
 // the same with a bf16 accumulator (a TP collective's result, consumed and cleared)
 dl_status launch_residual_rmsnorm_bf16(__nv_bfloat16* acc, int64_t lda, __nv_bfloat16* x, const __nv_bfloat16* g,
                                        __nv_bfloat16* y, int64_t T, int64_t h, float eps, cudaStream_t st,
@@ -318,6 +318,13 @@ struct AttnArgs {
   // stream-K decode kernel: zero-maintained counters + partial slots
   // (attention_sk_workspace(sk_items_cap / Hq, Hq) bytes)
   void* sk_ws; int64_t sk_items_cap;
+  // fused RoPE + cache append (decode, head-major cache, stream-K kernel only):
+  // qkv != null -> q|k|v rows [T x ld_qkv] bf16 straight from the q|k|v group
+  // (the kernel rotates q and the new key with positions[t], appends k and v at
+  // cache_lens[t]); `zero` is a side clear done once the kernel has waited.
+  // The kernel returns DL_ERR_UNSUPPORTED if it cannot take them.
+  const __nv_bfloat16* qkv; int64_t ld_qkv; const int32_t* positions; float theta; int rope;
+  SideZero zero;
 };
 dl_status launch_attention(const AttnArgs& a, cudaStream_t st);
 size_t attention_workspace(int64_t max_tokens, int Hq, int d);

@@ -133,12 +133,13 @@ __global__ void __launch_bounds__(kRnThreads) residual_rmsnorm_kernel(Acc* __res
                                                                       __nv_bfloat16* __restrict__ x,
                                                                       const __nv_bfloat16* __restrict__ g,
                                                                       __nv_bfloat16* __restrict__ y, int h, float eps,
-                                                                      SideZero z, EwTrace tr) {
+                                                                      SideZero z, SideZero z2, EwTrace tr) {
   ew_mark(tr, 1);
   pdl_trigger();   // successor may launch now; it waits for us before reading
   pdl_wait();
   ew_mark(tr, 2);
   side_zero(z);
+  side_zero(z2);
   __shared__ float red[32];
   const int64_t t = blockIdx.x;
   Acc* ar = acc + t * lda;
@@ -616,14 +617,14 @@ dl_status launch_rmsnorm(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bf
 }
 dl_status launch_residual_rmsnorm(float* acc, int64_t lda, __nv_bfloat16* x, const __nv_bfloat16* g,
                                   __nv_bfloat16* y, int64_t T, int64_t h, float eps, cudaStream_t st,
-                                  const SideZero& z) {
+                                  const SideZero& z, const SideZero& z2) {
   if (T <= 0) return DL_OK;
   if (h % 8 || h / 8 > kRnThreads * kRnChunks) {
     set_error("residual_rmsnorm: h=%lld unsupported (multiple of 8, <= %d)", (long long)h, 8 * kRnThreads * kRnChunks);
     return DL_ERR_UNSUPPORTED;
   }
   return launch_pdl(residual_rmsnorm_kernel<float>, dim3(static_cast<unsigned>(T)), dim3(kRnThreads), 0, st,
-                    "residual_rmsnorm", acc, lda, x, g, y, static_cast<int>(h), eps, z, ew_trace(2));
+                    "residual_rmsnorm", acc, lda, x, g, y, static_cast<int>(h), eps, z, z2, ew_trace(2));
 }
 dl_status launch_residual_rmsnorm_bf16(__nv_bfloat16* acc, int64_t lda, __nv_bfloat16* x, const __nv_bfloat16* g,
                                        __nv_bfloat16* y, int64_t T, int64_t h, float eps, cudaStream_t st,
@@ -634,7 +635,8 @@ dl_status launch_residual_rmsnorm_bf16(__nv_bfloat16* acc, int64_t lda, __nv_bfl
     return DL_ERR_UNSUPPORTED;
   }
   return launch_pdl(residual_rmsnorm_kernel<__nv_bfloat16>, dim3(static_cast<unsigned>(T)), dim3(kRnThreads), 0, st,
-                    "residual_rmsnorm_bf16", acc, lda, x, g, y, static_cast<int>(h), eps, z, ew_trace(2));
+                    "residual_rmsnorm_bf16", acc, lda, x, g, y, static_cast<int>(h), eps, z, SideZero{},
+                    ew_trace(2));
 }
 dl_status launch_f32_to_bf16(float* acc, int64_t lda, __nv_bfloat16* out, int64_t ldo, int64_t T, int64_t n,
                              int clear, cudaStream_t st, const SideZero& z) {

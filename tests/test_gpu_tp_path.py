@@ -126,12 +126,15 @@ print("ERRS", errs)
 '''
 
 
-def test_block_decode_stream_k_fixups():
-    """Opt-in last-contributor fixups (DL_FIXUP=1): RoPE+cache, residual and
-    SiLU*up finalized inside the stage-2 GEMMs must match the oracle."""
+@pytest.mark.parametrize("knob", ["DL_FIXUP", "DL_ROPE_FUSE"])
+def test_block_decode_stream_k_fixups(knob):
+    """Opt-in decode variants must match the oracle: DL_FIXUP=1 (RoPE+cache,
+    residual and SiLU*up finalized inside the stage-2 GEMMs' last-contributor
+    fixups) and DL_ROPE_FUSE=1 (RoPE + cache append inside the stream-K
+    attention, q|k|v partials as bf16x2)."""
     from paper_2604_17709_b200 import build
     build.build()
-    env = dict(os.environ, DL_FIXUP="1")
+    env = dict(os.environ, **{knob: "1"})
     src = FIXUP_SCRIPT.replace("__ROOT__", repr(ROOT))
     r = subprocess.run([sys.executable, "-c", src], capture_output=True, text=True, env=env, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
