@@ -624,6 +624,7 @@ struct BlockWs {
   float* tail;                       // prefill DP + stream-K tail scratch (zero-maintained)
   size_t tail_bytes;
   __nv_bfloat16 *lat_send, *lat_recv;   // DeInfer latent all-gather [T x slot] / [P][T][slot]
+  __nv_bfloat16* lat_red;                // DeInfer skinny: stage-1 latent slice, bf16x2 red.add target (zero-maintained)
   int64_t ldz32, ldzb, ldy32;
 };
 
@@ -661,6 +662,7 @@ BlockWs carve_block(Carver& c, const BlockDims& d, int64_t Tmax) {
   w.tail = w.tail_bytes ? c.take<float>(w.tail_bytes / sizeof(float)) : nullptr;
   if (d.layout == DL_LAYOUT_DEINFER) {
     w.lat_send = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.lat_slot);
+    w.lat_red = c.take<__nv_bfloat16>(static_cast<size_t>(Ts) * d.lat_slot);   // skinny bf16x2 target, zero-maintained
     w.lat_recv = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.P * d.lat_slot);
   }
   return w;
@@ -840,7 +842,12 @@ dl_status deinfer_latent(const dl_factor_group& grp, int nseg, const __nv_bfloat
   int64_t lens[3], beg[3], len[3], kloc = 0;
   for (int s = 0; s < nseg; ++s) lens[s] = grp.seg[s].k;
   DL_TRY(dl_tp_plan(lens, nseg, comm->world, comm->rank, 0, beg, len, &kloc));
-  if (skinny) {
+  const bool red16 = skinny && use_zred();   // latent slice reduced as bf16x2 straight into the send buffer
+  if (red16) {
+    GemmProblem p1 = one_seg(act, ld_act, T, n, grp.B, grp.ldb, kloc, n, out_plain(ws.lat_red, d.lat_slot, OUT_BF16_RED, 0));
+    p1.sched = next_sched(ws.sched);
+    DL_TRY(tc_gemm(p1, true, st));
+  } else if (skinny) {
     GemmProblem p1 = one_seg(act, ld_act, T, n, grp.B, grp.ldb, kloc, n, out_plain(ws.zf, ws.ldz32, OUT_F32_RED, 0));
     p1.sched = next_sched(ws.sched);
     DL_TRY(tc_gemm(p1, true, st));
@@ -851,7 +858,8 @@ dl_status deinfer_latent(const dl_factor_group& grp, int nseg, const __nv_bfloat
     p1.tail_bytes = ws.tail_bytes;
     DL_TRY(tc_gemm(p1, false, st));
   }
-  DL_TRY(all_gather(comm, ws.lat_send, ws.lat_recv, static_cast<size_t>(T) * d.lat_slot, kNcclBfloat16, st));
+  DL_TRY(all_gather(comm, red16 ? ws.lat_red : ws.lat_send, ws.lat_recv, static_cast<size_t>(T) * d.lat_slot,
+                    kNcclBfloat16, st));
   const ZLayout zl = zlayout(grp, nseg);
   LatentMap mp{};
   mp.nseg = nseg;
@@ -868,7 +876,13 @@ dl_status deinfer_latent(const dl_factor_group& grp, int nseg, const __nv_bfloat
   mp.base = L / comm->world;
   mp.extra = L % comm->world;
   mp.width = zl.width;
-  return launch_latent_unpermute(ws.lat_recv, ws.zb, ws.ldzb, mp, st);
+  SideZero z;   // the un-permute runs after the all-gather read the send buffer: clear it there
+  if (red16) {
+    z.p = ws.lat_red;
+    z.rows = 1;
+    z.row_bytes = z.ld = static_cast<int64_t>(T) * d.lat_slot * 2;
+  }
+  return launch_latent_unpermute(ws.lat_recv, ws.zb, ws.ldzb, mp, st, z);
 }
 
 dl_status deinfer_first(const dl_factor_group& grp, int nseg, const int64_t* rows_loc, const __nv_bfloat16* act,
@@ -893,6 +907,25 @@ dl_status deinfer_first(const dl_factor_group& grp, int nseg, const int64_t* row
 dl_status deinfer_second(const dl_factor_group& grp, const __nv_bfloat16* act, int64_t n_loc, int64_t m_out,
                          int64_t T, bool skinny, const BlockWs& ws, dl_comm comm, __nv_bfloat16* x, cudaStream_t st) {
   const int64_t l = grp.seg[0].k;
+  if (skinny && use_zred()) {
+    // latent partial as bf16x2 straight into the all-reduce buffer (contiguous
+    // [T x rup(l, 8)] in ws.yr), reduced in place, read by stage 2, cleared by
+    // the residual kernel
+    const int64_t ldl = rup(l, 8);
+    GemmProblem p1 = one_seg(act, n_loc, T, n_loc, grp.B, grp.ldb, l, n_loc, out_plain(ws.yr, ldl, OUT_BF16_RED, 0));
+    p1.sched = next_sched(ws.sched);
+    DL_TRY(tc_gemm(p1, true, st));
+    DL_TRY(all_reduce(comm, ws.yr, static_cast<size_t>(T) * ldl, kNcclBfloat16, st));
+    GemmProblem p2 = one_seg(ws.yr, ldl, T, l, grp.seg[0].A, grp.seg[0].lda, m_out, l,
+                             out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0));
+    p2.sched = next_sched(ws.sched);
+    DL_TRY(tc_gemm(p2, true, st));
+    SideZero z;
+    z.p = ws.yr;
+    z.rows = 1;
+    z.row_bytes = z.ld = T * ldl * 2;
+    return launch_residual_add_f32(ws.yf, ws.ldy32, x, m_out, T, m_out, 1, st, z);
+  }
   if (skinny) {
     GemmProblem p1 = one_seg(act, n_loc, T, n_loc, grp.B, grp.ldb, l, n_loc, out_plain(ws.zf, ws.ldz32, OUT_F32_RED, 0));
     p1.sched = next_sched(ws.sched);

@@ -282,7 +282,7 @@ struct LatentMap {
   int64_t width;                           // Z layout width
 };
 dl_status launch_latent_unpermute(const __nv_bfloat16* recv, __nv_bfloat16* zb, int64_t ldzb,
-                                  const LatentMap& mp, cudaStream_t st);
+                                  const LatentMap& mp, cudaStream_t st, const SideZero& z = SideZero{});
 // Low-rank KV cache (N3).  append: latent row zb[t][zoff .. zoff + ncopy) of
 // decode token t -> pool slot of (seq t, position cache_lens[t]) through the
 // block table; slot_pos[slot] = positions[t].

@@ -481,9 +481,10 @@ __global__ void __launch_bounds__(128) unpermute_kernel(const __nv_bfloat16* __r
 // grid (ceil(width / 256), T), one column per thread.
 __global__ void __launch_bounds__(256) latent_unpermute_kernel(const __nv_bfloat16* __restrict__ recv,
                                                                __nv_bfloat16* __restrict__ zb, int64_t ldzb,
-                                                               LatentMap mp) {
+                                                               LatentMap mp, SideZero z) {
   pdl_trigger();   // successor may launch now; it waits for us before reading
   pdl_wait();
+  side_zero(z);
   const int64_t col = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (col >= mp.width) return;
   const int64_t t = blockIdx.y;
@@ -603,10 +604,10 @@ dl_status launch_rope_rows(__nv_bfloat16* buf, int64_t ld, int heads, const int3
 }
 
 dl_status launch_latent_unpermute(const __nv_bfloat16* recv, __nv_bfloat16* zb, int64_t ldzb, const LatentMap& mp,
-                                  cudaStream_t st) {
+                                  cudaStream_t st, const SideZero& z) {
   if (mp.T <= 0 || mp.width <= 0) return DL_OK;
   dim3 grid(static_cast<unsigned>((mp.width + 255) / 256), static_cast<unsigned>(mp.T));
-  return launch_pdl(latent_unpermute_kernel, grid, dim3(256), 0, st, "latent_unpermute", recv, zb, ldzb, mp);
+  return launch_pdl(latent_unpermute_kernel, grid, dim3(256), 0, st, "latent_unpermute", recv, zb, ldzb, mp, z);
 }
 
 dl_status launch_rmsnorm(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bfloat16* y, int64_t T, int64_t h,
