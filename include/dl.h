@@ -418,6 +418,14 @@ dl_status dl_debug_fused_trace(void *device_buf);
  * entry, the first return from griddepcontrol.wait, the last CTA end; fill
  * entries 1-2 with ~0 and 3 with 0 before the run), or NULL to disable.     */
 dl_status dl_debug_ew_trace(void *device_buf);
+/* Test hook: Y[T x m] = A (B X) with X given rank-major as the attention
+ * all-gather leaves it, Xg [P][T][n/P] (X[t][p*n/P + c] = Xg[p][t][c]); the
+ * stage-1 TMA reads it through a 3-D map exactly as the TP o projection does.
+ * bf16, 1 <= T <= 256, (n/P) % 64 == 0; workspace per dl_lowrank_linear_workspace. */
+dl_status dl_debug_linear_gathered(const void *Xg, int P, const void *A, int64_t lda,
+                                   const void *B, int64_t ldb, void *Y, int64_t ldy,
+                                   int64_t T, int64_t m, int64_t n, int64_t k,
+                                   void *workspace, size_t workspace_bytes, void *stream);
 
 #ifdef __cplusplus
 }

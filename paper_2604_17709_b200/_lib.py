@@ -25,7 +25,7 @@ EXPORTS = ("dl_last_error", "dl_version", "dl_device_ok", "dl_comm_create", "dl_
            "dl_dense_workspace", "dl_dense", "dl_launch_count", "dl_profile_begin", "dl_profile_end",
            "dl_profile_count", "dl_profile_get", "dl_debug_gemm_trace", "dl_debug_fused_trace", "dl_deinfer_shard_factors",
            "dl_kv_prepare", "dl_decomposed_block_forward_kvlr", "dl_comm_create_loopback",
-           "dl_decomposed_stack_forward", "dl_debug_ew_trace")
+           "dl_decomposed_stack_forward", "dl_debug_ew_trace", "dl_debug_linear_gathered")
 
 
 class DLError(RuntimeError):
@@ -111,6 +111,8 @@ def load():
             lib.dl_debug_gemm_trace.argtypes = [P]
             lib.dl_debug_fused_trace.argtypes = [P]
             lib.dl_debug_ew_trace.argtypes = [P]
+            lib.dl_debug_linear_gathered.argtypes = [P, I, P, I64, P, I64, P, I64, I64, I64, I64, I64, P,
+                                                     ctypes.c_size_t, P]
             lib.dl_deinfer_shard_factors.argtypes = [I, I, P, P, P, P, P, P, I64, I, I, I, P, I64, P, P, P]
             lib.dl_comm_create_loopback.argtypes = [I, I, ctypes.POINTER(P)]
             lib.dl_kv_prepare.argtypes = [P, I64, P, I32, I64, I64, I64, P, P, P, P, P]
@@ -517,6 +519,17 @@ def dl_profile_records():
         _check(L.dl_profile_get(i, ctypes.byref(ms), ctypes.byref(b), ctypes.byref(f), ctypes.byref(k)))
         out.append((ms.value, b.value, f.value, k.value))
     return out
+
+
+def dl_debug_linear_gathered(Xg: torch.Tensor, A: torch.Tensor, B: torch.Tensor, Y: torch.Tensor, stream=None):
+    """Test hook (include/dl.h): Y = A(B X) with X rank-major [P][T][n/P]."""
+    P, T, w = Xg.shape
+    m, k = A.shape
+    n = P * w
+    ws = torch.zeros(dl_lowrank_linear_workspace(T, m, n, k), dtype=torch.uint8, device=Xg.device)
+    _check(load().dl_debug_linear_gathered(_ptr(Xg), P, _ptr(A), A.stride(0), _ptr(B), B.stride(0), _ptr(Y),
+                                           Y.stride(0), T, m, n, k, _ptr(ws), ws.numel(), _stream(stream)))
+    return Y
 
 
 def dl_debug_ew_trace(buf: torch.Tensor | None):

@@ -370,6 +370,36 @@ dl_status dl_lowrank_linear(const void* X, int64_t ldx, const void* A, int64_t l
   return launch_f32_to_bf16(ws.yf, ws.ldy32, static_cast<__nv_bfloat16*>(Y), ldy, T, m, 0, st);
 }
 
+// Test hook for the rank-major activation layout the TP o projection reads
+// straight from the attention all-gather (3-D TMA map; include/dl.h).
+dl_status dl_debug_linear_gathered(const void* Xg, int P, const void* A, int64_t lda, const void* B, int64_t ldb,
+                                   void* Y, int64_t ldy, int64_t T, int64_t m, int64_t n, int64_t k, void* workspace,
+                                   size_t workspace_bytes, void* stream) {
+  if (P < 1 || T < 1 || T > 256 || n % P || (n / P) % 64 || m % 4) {
+    set_error("dl_debug_linear_gathered: need 1 <= T <= 256, n / P a multiple of 64, m %% 4 == 0");
+    return DL_ERR_SHAPE;
+  }
+  size_t need = 0;
+  dl_lowrank_linear_workspace(T, m, n, k, DL_BF16, &need);
+  if (!workspace || workspace_bytes < need) {
+    set_error("workspace too small");
+    return DL_ERR_WORKSPACE;
+  }
+  DL_TRY(check_device());
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Carver cv(workspace);
+  LinWs ws = carve_lin(cv, T, m, k, PATH_SKINNY, false);
+  DL_TRY(cuda_status(cudaMemsetAsync(ws.zf, 0, sizeof(float) * T * ws.ldz32, st), "memset"));
+  DL_TRY(cuda_status(cudaMemsetAsync(ws.yf, 0, sizeof(float) * T * ws.ldy32, st), "memset"));
+  GemmProblem p1 = one_seg(Xg, n, T, n, B, ldb, k, n, out_plain(ws.zf, ws.ldz32, OUT_F32_RED, 0));
+  p1.act_p = P;
+  p1.act_w = n / P;
+  DL_TRY(tc_gemm(p1, true, st));
+  DL_TRY(launch_f32_to_bf16(ws.zf, ws.ldz32, ws.zb, ws.ldzb, T, rup(k, 4), 1, st));
+  DL_TRY(tc_gemm(one_seg(ws.zb, ws.ldzb, T, k, A, lda, m, k, out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0)), true, st));
+  return launch_f32_to_bf16(ws.yf, ws.ldy32, static_cast<__nv_bfloat16*>(Y), ldy, T, m, 1, st);
+}
+
 // ---------------------------------------------------------------------------
 // rank-shard planner
 // ---------------------------------------------------------------------------
@@ -779,7 +809,8 @@ bool use_zred() {
 dl_status run_group(const dl_factor_group& grp, int nseg, const int64_t* rows, const __nv_bfloat16* act,
                     int64_t ld_act, int64_t n, int64_t T, bool skinny, const BlockWs& ws, const GemmOut& out2,
                     cudaStream_t st, const GemmFixup* fix2 = nullptr, SideZero* zero_out = nullptr,
-                    int zslot = 0) {
+                    int zslot = 0, int act_p = 0, int64_t act_w = 0) {
+  // act_p > 1 (skinny only): act is a rank-major all-gather output read through a 3-D map
   const ZLayout zl = zlayout(grp, nseg);
   if (zero_out) *zero_out = SideZero{};
   if (skinny && zero_out && use_zred() && !use_fixup()) {
@@ -787,6 +818,8 @@ dl_status run_group(const dl_factor_group& grp, int nseg, const int64_t* rows, c
     const int64_t ldz = 2 * ws.ldzb;
     GemmProblem p1 = stage1(grp, nseg, act, ld_act, T, n, zl, out_plain(z, ldz, OUT_BF16_RED, 0));
     p1.sched = next_sched(ws.sched);
+    p1.act_p = act_p;
+    p1.act_w = act_w;
     DL_TRY(tc_gemm(p1, true, st));
     GemmProblem p2 = stage2(grp, nseg, rows, z, ldz, T, zl, out2);
     p2.sched = next_sched(ws.sched);
@@ -802,6 +835,8 @@ dl_status run_group(const dl_factor_group& grp, int nseg, const int64_t* rows, c
     if (use_fixup()) {
       GemmProblem p1 = stage1(grp, nseg, act, ld_act, T, n, zl, out_plain(ws.zb, ws.ldzb, OUT_BF16, 0));
       p1.sched = next_sched(ws.sched);
+      p1.act_p = act_p;
+      p1.act_w = act_w;
       p1.fix.op = FIX_BF16;
       p1.fix.acc32 = ws.zf;
       p1.fix.acc_ld = ws.ldz32;
@@ -810,6 +845,8 @@ dl_status run_group(const dl_factor_group& grp, int nseg, const int64_t* rows, c
     } else {
       GemmProblem p1 = stage1(grp, nseg, act, ld_act, T, n, zl, out_plain(ws.zf, ws.ldz32, OUT_F32_RED, 0));
       p1.sched = next_sched(ws.sched);
+      p1.act_p = act_p;
+      p1.act_w = act_w;
       DL_TRY(tc_gemm(p1, true, st));
       DL_TRY(launch_f32_to_bf16(ws.zf, ws.ldz32, ws.zb, ws.ldzb, T, zl.width, 1, st));
     }
@@ -1407,11 +1444,21 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   }
 
   const __nv_bfloat16* att_in = ws.att;
+  int o_act_p = 0;
+  int64_t o_act_w = 0;
+  static const bool no_ag3d = getenv("DL_NO_AG3D") != nullptr;   // A/B switch
   if (tp) {
     const int64_t wl = d.Hq_loc * d.d;
     DL_TRY(all_gather(comm, ws.att, ws.ag, static_cast<size_t>(T) * wl, kNcclBfloat16, st));
-    DL_TRY(launch_unpermute(ws.ag, ws.att_full, P, T, wl, st));
-    att_in = ws.att_full;
+    if (skinny && !no_ag3d && wl % 64 == 0) {
+      // o's stage-1 TMA reads the rank-major [P][T][wl] all-gather output directly
+      att_in = ws.ag;
+      o_act_p = P;
+      o_act_w = wl;
+    } else {
+      DL_TRY(launch_unpermute(ws.ag, ws.att_full, P, T, wl, st));
+      att_in = ws.att_full;
+    }
   }
 
   // Finish a [T x n] group output: + residual (o, down) with the TP reduction.
@@ -1436,7 +1483,8 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   // ---- o projection + residual ----------------------------------------------
   const GemmFixup fres = fixup(fx ? FIX_RESIDUAL : FIX_NONE);
   SideZero zo, zg, zd;
-  DL_TRY(run_group(w->o, 1, h_rows, att_in, d.h, d.h, T, skinny, ws, resid_out(), st, &fres, fx ? nullptr : &zo));
+  DL_TRY(run_group(w->o, 1, h_rows, att_in, d.h, d.h, T, skinny, ws, resid_out(), st, &fres, fx ? nullptr : &zo, 0,
+                   o_act_p, o_act_w));
   const __nv_bfloat16* mlp_norm = static_cast<const __nv_bfloat16*>(w->mlp_norm);
   static const bool no_fuse = getenv("DL_NO_FUSE_RESNORM") != nullptr;   // A/B timing switch
   if (!fx && !tp && skinny && !no_fuse) {

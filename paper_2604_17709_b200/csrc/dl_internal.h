@@ -146,6 +146,12 @@ struct GemmProblem {
   // (<= 44 tiles x 256 x 256 x 4 B); left zeroed.  null -> whole tiles only.
   float* tail_acc;
   size_t tail_bytes;
+  // act_p > 1 (swap-AB decode path only): act is the rank-major all-gather
+  // output [act_p][T][act_w] and column c of the logical [T x act_p*act_w]
+  // operand is (c / act_w, c % act_w); act_w % 64 == 0.  The TMA reads it
+  // through a 3-D map, so no un-permute pass is needed.
+  int act_p;
+  int64_t act_w;
 };
 
 // Picks the tile configuration (swap-AB for T <= 256, stream-K when the

@@ -81,6 +81,7 @@ struct KArgs {
   long long static_units, dyn_begin;
   int chunk;
   int l2pf;                  // weight tiles prefetched into L2 before griddepcontrol.wait
+  int act_w;                 // > 0: 3-D activation map, column c -> (c % act_w, token, c / act_w)
   // DP + stream-K tail (whole-tile kernels): tiles [0, dp_tiles) whole, each of
   // the remaining tiles split in tail_split K-pieces accumulated in fp32 into
   // tail_acc [tail tile][256][256], finalized by tc_tail_finalize_kernel.
@@ -512,13 +513,17 @@ __global__ void __launch_bounds__(kThreads, (SWAP && STAGES <= 4) ? 2 : 1)
           }
         }
       };
+      auto act_load = [&](void* dst, uint64_t* bar, int c, int tok) {
+        if (a.act_w > 0) ptx::tma_load_3d(dst, &maps.act, bar, c % a.act_w, tok, c / a.act_w, pol_a);
+        else ptx::tma_load_2d(dst, &maps.act, bar, c, tok, pol_a);
+      };
       auto flush_pending = [&]() {
         if (SWAP) l2_prefetch();
         pdl_wait();
         waited = true;
         for (int i = 0; i < u && i < STAGES; ++i) {
           uint8_t* dst = smem + i * STAGE_BYTES + (SWAP ? P_BYTES : 0);
-          ptx::tma_load_2d(dst, &maps.act, &full_bar[i], pend_c0[i], pend_c1[i], pol_a);
+          act_load(dst, &full_bar[i], pend_c0[i], pend_c1[i]);
         }
       };
       int jslot = 0;
@@ -543,7 +548,7 @@ __global__ void __launch_bounds__(kThreads, (SWAP && STAGES <= 4) ? 2 : 1)
           uint8_t* sa = SWAP ? sq : sp;
           ptx::tma_load_2d(sw, &maps.w[jb.seg], &full_bar[stage], kx, jb.feat0 - s.feat_begin, pol_w);
           if (waited) {
-            ptx::tma_load_2d(sa, &maps.act, &full_bar[stage], s.act_koff + kx, jb.tok0, pol_a);
+            act_load(sa, &full_bar[stage], s.act_koff + kx, jb.tok0);
           } else {
             pend_c0[u] = s.act_koff + kx;
             pend_c1[u] = jb.tok0;
@@ -1126,7 +1131,25 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
       maps.w[g] = maps.w[0];
     }
   }
-  if (!make_map(&maps.act, p.act, p.T, p.k_act, p.ld_act, BOX_A)) {
+  a.act_w = 0;
+  if (p.act_p > 1) {
+    if (!SWAP || PAIR || p.act_w % BK || p.act_w * p.act_p != p.k_act) {
+      set_error("3-D activation layout: swap-AB path with act_w %% 64 == 0 and act_p * act_w == k_act only");
+      return DL_ERR_UNSUPPORTED;
+    }
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(p.act_w), static_cast<cuuint64_t>(p.T),
+                          static_cast<cuuint64_t>(p.act_p)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(p.act_w * 2), static_cast<cuuint64_t>(p.T * p.act_w * 2)};
+    cuuint32_t box[3] = {static_cast<cuuint32_t>(BK), static_cast<cuuint32_t>(BOX_A), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (g_encode(&maps.act, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(p.act), dims, strides, box, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      set_error("cuTensorMapEncodeTiled (3-D activation) failed");
+      return DL_ERR_CUDA;
+    }
+    a.act_w = static_cast<int>(p.act_w);
+  } else if (!make_map(&maps.act, p.act, p.T, p.k_act, p.ld_act, BOX_A)) {
     set_error("cuTensorMapEncodeTiled failed (activation)");
     return DL_ERR_CUDA;
   }

@@ -103,6 +103,22 @@ def test_linear_bf16_large_shapes(dl, orc):
     assert rel(Y.cpu()[rows], ref) <= TOL_BF16
 
 
+@pytest.mark.parametrize("P,T", [(2, 64), (4, 17), (8, 100)])
+def test_linear_reads_rank_major_gather(dl, orc, P, T):
+    """The TP o projection reads the attention all-gather [P][T][h/P] in place
+    through a 3-D TMA map (no un-permute pass): same result as the logical
+    [T x h] operand."""
+    from paper_2604_17709_b200 import _lib
+    w, m, k = 128, 384, 96
+    n = P * w
+    X, A, B = _lin_inputs(T, m, n, k, torch.bfloat16, 40 + P)
+    Xg = X.view(T, P, w).permute(1, 0, 2).contiguous()
+    Y = torch.empty(T, m, dtype=torch.bfloat16, device="cuda")
+    _lib.dl_debug_linear_gathered(Xg.cuda(), A.cuda(), B.cuda(), Y)
+    torch.cuda.synchronize()
+    assert rel(Y.cpu(), orc.lowrank_linear(X, A, B)) <= TOL_BF16
+
+
 def test_dense_lm_head_shape(dl):
     """dl_dense (used for the LM head) vs a float64 torch matmul of the same bf16 values."""
     T, N, K = 64, 1000, 512
