@@ -482,9 +482,10 @@ constexpr int SHR = 128 + 4 * 32 * 4;       // floats: tile row max [64], row su
 constexpr int kMaxSeqs = 1024;
 constexpr int kPerSM = 2;                   // CTAs per SM (grid = kPerSM x SMs)
 constexpr int kPartRow = 2 + 32;            // partial row of one warp: m, l, o[32 dims]
-constexpr int kMaxGrid = 2 * 192;           // partial slots are sized for this
+constexpr int kMaxGrid = 3 * 192;           // partial slots are sized for this
+template <int NSx = NS>
 constexpr size_t smem_bytes(int nseq) {
-  return NS * STAGE + SHR * 4 + 2 * NS * 8 +
+  return NSx * STAGE + SHR * 4 + 2 * NSx * 8 +
          static_cast<size_t>(nseq + 1) * 4;
 }
 }  // namespace sk
@@ -567,7 +568,8 @@ __device__ __forceinline__ uint32_t sk_swz(uint32_t base, int key, int chunk) { 
   return base + ((chunk >> 3) << 13) + key * 128 + ((((chunk & 7) ^ (key & 7))) << 4);
 }
 
-__global__ void __launch_bounds__(sk::kThreads, sk::kPerSM)
+template <int NS, int PERSM>
+__global__ void __launch_bounds__(sk::kThreads, PERSM)
     attn_decode_sk_kernel(const __grid_constant__ SkMaps maps, const __grid_constant__ SkArgs a) {
   using namespace sk;
   extern __shared__ __align__(1024) uint8_t sm[];   // no static shared memory: the base is 1024-aligned
@@ -1025,16 +1027,20 @@ dl_status launch_attention_sk(const AttnArgs& a, cudaStream_t st) {
   static const int l2pf = getenv("DL_ATTN_L2PF") ? atoi(getenv("DL_ATTN_L2PF")) : 0;
   k.l2pf = l2pf;
   k.part = reinterpret_cast<float*>(static_cast<uint8_t*>(a.sk_ws) + (a.sk_items_cap + 63) / 64 * 64 * 4 * 4);
-  const size_t smem = sk::smem_bytes(a.num_seqs);
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaFuncSetAttribute(attn_decode_sk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(sk::smem_bytes(sk::kMaxSeqs)));
-    attr = sk::smem_bytes(sk::kMaxSeqs);
+  // ring depth x CTAs per SM: 3 x 2 (default) or 2 x 3 (DL_ATTN_CFG=23, A/B)
+  static const bool cfg23 = getenv("DL_ATTN_CFG") && atoi(getenv("DL_ATTN_CFG")) == 23;
+  auto kern = cfg23 ? attn_decode_sk_kernel<2, 3> : attn_decode_sk_kernel<3, 2>;
+  const size_t smem = cfg23 ? sk::smem_bytes<2>(a.num_seqs) : sk::smem_bytes<3>(a.num_seqs);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_decode_sk_kernel<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sk::smem_bytes<3>(sk::kMaxSeqs)));
+    cudaFuncSetAttribute(attn_decode_sk_kernel<2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sk::smem_bytes<2>(sk::kMaxSeqs)));
+    attr = true;
   }
-  const int grid = std::min(sk::kPerSM * num_sms(), sk::kMaxGrid);
-  return launch_pdl(attn_decode_sk_kernel, dim3(grid), dim3(sk::kThreads), smem, st, "attention decode (stream-K)",
-                    maps, k);
+  const int grid = std::min((cfg23 ? 3 : 2) * num_sms(), sk::kMaxGrid);
+  return launch_pdl(kern, dim3(grid), dim3(sk::kThreads), smem, st, "attention decode (stream-K)", maps, k);
 }
 
 size_t attention_workspace(int64_t max_tokens, int Hq, int d) {
