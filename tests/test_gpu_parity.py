@@ -207,6 +207,33 @@ def test_block_decode_small(dl, orc, cache_lens):
     assert rel(kg, kn) <= TOL_BF16
 
 
+@pytest.mark.parametrize("S", [100, 200, 256])
+def test_block_decode_wide_batches(dl, orc, S):
+    """Decode batches on the 128- and 256-token swap-AB configurations (the bench runs 64):
+    bf16x2 latent / gate|up reductions, stream-K attention over S sequences, run twice."""
+    s = SMALL
+    rk = block_ranks(s, 0.4)
+    w = gen_block_weights(s, rk, 0, 50 + S)
+    rng = np.random.default_rng(S)
+    cache_lens = [int(v) for v in rng.integers(0, 90, S)]
+    max_seq = max(cache_lens) + 1
+    x = gen_normal((S, s.h), 1.0, 51, dtype=torch.bfloat16)
+    kc = gen_normal((S, s.n_kv_heads, max_seq, s.head_dim), 1.0, 52, dtype=torch.bfloat16)
+    vc = gen_normal((S, s.n_kv_heads, max_seq, s.head_dim), 1.0, 53, dtype=torch.bfloat16)
+    ko, vo = _cache_to_oracle(kc, S, max_seq), _cache_to_oracle(vc, S, max_seq)
+    cl = torch.tensor(cache_lens, dtype=torch.int32)
+    cfg = dl.make_block_config(s, rk, max_tokens=S, max_seqs=S)
+    wdev = dl.BlockWeights({k: v.cuda() for k, v in w.items()})
+    ws = torch.zeros(dl.dl_block_workspace(cfg), dtype=torch.uint8, device="cuda")
+    ref, _, _ = orc.block_decode(_oracle_cfg(orc, s, rk), w, x, ko, vo, cache_lens)
+    for _ in range(2):
+        xd, kcd, vcd = x.cuda(), kc.cuda(), vc.cuda()
+        dl.dl_decomposed_block_forward(cfg, wdev, xd, cl.cuda(), None, S, dl.DL_DECODE, kcd, vcd, cl.cuda(), None,
+                                       ws)
+        torch.cuda.synchronize()
+        assert rel(xd.cpu().double() - x.double(), ref - x.double().numpy()) <= TOL_BF16
+
+
 @pytest.mark.parametrize("cache_lens", [[4000, 3, 700], [63, 64, 127, 128, 0]])
 def test_block_decode_long_ragged_nan_tail(dl, orc, cache_lens):
     """Stream-K decode attention: one long item spread over many CTAs next to short ones,
