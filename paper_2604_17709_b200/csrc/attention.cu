@@ -86,11 +86,13 @@ __device__ __forceinline__ void load_tile(uint32_t sbase, const __nv_bfloat16* s
 
 // =============================== prefill ===================================
 template <int KTP>
-__global__ void __launch_bounds__(128, KTP == 32 ? 3 : 1) attn_prefill_kernel(AttnArgs a) {
+__global__ void __launch_bounds__(128, KTP == 32 ? 3 : 1) attn_prefill_kernel(AttnArgs a, EwTrace tr) {
+  ew_mark(tr, 1);
   constexpr int PT = KTP * ROW_BYTES;   // bytes of one K or V tile
   extern __shared__ __align__(1024) uint8_t sm[];
   pdl_trigger();   // successor may launch now; it waits for us before reading
   pdl_wait();
+  ew_mark(tr, 2);
   const int s = blockIdx.z, h = blockIdx.y;
   const int n_new = a.cu_seqlens[s + 1] - a.cu_seqlens[s];
   const int q0 = blockIdx.x * QT;
@@ -243,6 +245,7 @@ __global__ void __launch_bounds__(128, KTP == 32 ? 3 : 1) attn_prefill_kernel(At
     if (r0 < nq) *reinterpret_cast<uint32_t*>(O + r0 * ldq + col) = pack_bf16(acc[nt][0] * i0, acc[nt][1] * i0);
     if (r1 < nq) *reinterpret_cast<uint32_t*>(O + r1 * ldq + col) = pack_bf16(acc[nt][2] * i1, acc[nt][3] * i1);
   }
+  ew_mark(tr, 3);
 }
 
 // ================================ decode ===================================
@@ -1069,7 +1072,7 @@ dl_status launch_attention(const AttnArgs& a, cudaStream_t st) {
     // grid.x covers the longest sequence: bounded by T
     const int qtiles = static_cast<int>((a.T + QT - 1) / QT);
     dim3 grid(qtiles, a.Hq, a.num_seqs);
-    return launch_pdl(attn_prefill_kernel<KTP>, grid, dim3(128), SMEM, st, "attention prefill", a);
+    return launch_pdl(attn_prefill_kernel<KTP>, grid, dim3(128), SMEM, st, "attention prefill", a, ew_trace(5));
   }
   {
     const dl_status s = launch_attention_sk(a, st);

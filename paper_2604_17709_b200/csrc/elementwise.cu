@@ -229,6 +229,9 @@ __device__ __forceinline__ void zero8(float* p) {
 }
 __device__ __forceinline__ void zero8(__nv_bfloat16* p) { *reinterpret_cast<uint4*>(p) = make_uint4(0u, 0u, 0u, 0u); }
 
+// 2-D grid (column blocks, tokens): row t = blockIdx.y, thread items
+// c = blockIdx.x * 256 + tid + u * gridDim.x * 256 (8 columns each) -- no
+// per-item integer division; fast sigmoid (__expf, __fdividef).
 template <typename Acc>
 __global__ void __launch_bounds__(256) silu_mul_kernel(Acc* __restrict__ acc, int64_t lda, __nv_bfloat16* __restrict__ out,
                                                        int64_t ldo, int m, int T, int relu, int clear, SideZero z,
@@ -238,44 +241,40 @@ __global__ void __launch_bounds__(256) silu_mul_kernel(Acc* __restrict__ acc, in
   pdl_wait();
   ew_mark(tr, 2);
   side_zero(z);
-  const unsigned per_row = static_cast<unsigned>(m) / 8, total = per_row * static_cast<unsigned>(T);
-  const unsigned stride = gridDim.x * blockDim.x;
+  const int per_row = m / 8;
+  const int64_t t = blockIdx.y;
+  Acc* row = acc + t * lda;
+  __nv_bfloat16* orow = out + t * ldo;
   const int uoff = relu ? 0 : m;
-  for (unsigned base = blockIdx.x * blockDim.x + threadIdx.x; base < total; base += stride * kSiluU) {
-    float gv[kSiluU][8], uv[kSiluU][8];
-    Acc* pr[kSiluU];
+  const int stride = gridDim.x * blockDim.x;
+  float gv[kSiluU][8], uv[kSiluU][8];
 #pragma unroll
-    for (int u = 0; u < kSiluU; ++u) {
-      const unsigned i = base + u * stride;
-      pr[u] = nullptr;
-      if (i < total) {
-        const unsigned t = i / per_row, c = (i - t * per_row) * 8;
-        pr[u] = acc + static_cast<int64_t>(t) * lda + c;
-        ld8(pr[u] + uoff, uv[u]);
-        if (!relu) ld8(pr[u], gv[u]);
-      }
+  for (int u = 0; u < kSiluU; ++u) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x + u * stride;
+    if (i < per_row) {
+      ld8(row + uoff + i * 8, uv[u]);
+      if (!relu) ld8(row + i * 8, gv[u]);
     }
+  }
 #pragma unroll
-    for (int u = 0; u < kSiluU; ++u) {
-      if (!pr[u]) continue;
-      const unsigned i = base + u * stride;
-      const unsigned t = i / per_row, c = (i - t * per_row) * 8;
-      if (clear) zero8(pr[u] + uoff);
-      float o[8];
-      if (relu) {
+  for (int u = 0; u < kSiluU; ++u) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x + u * stride;
+    if (i >= per_row) continue;
+    if (clear) zero8(row + uoff + i * 8);
+    float o[8];
+    if (relu) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = fmaxf(uv[u][e], 0.f);
-      } else {
-        if (clear) zero8(pr[u]);
+      for (int e = 0; e < 8; ++e) o[e] = fmaxf(uv[u][e], 0.f);
+    } else {
+      if (clear) zero8(row + i * 8);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = gv[u][e] / (1.f + __expf(-gv[u][e])) * uv[u][e];
-      }
-      uint4 pk;
-      __nv_bfloat162* pb = reinterpret_cast<__nv_bfloat162*>(&pk);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) pb[e] = __floats2bfloat162_rn(o[2 * e], o[2 * e + 1]);
-      *reinterpret_cast<uint4*>(out + static_cast<int64_t>(t) * ldo + c) = pk;
+      for (int e = 0; e < 8; ++e) o[e] = __fdividef(gv[u][e], 1.f + __expf(-gv[u][e])) * uv[u][e];
     }
+    uint4 pk;
+    __nv_bfloat162* pb = reinterpret_cast<__nv_bfloat162*>(&pk);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) pb[e] = __floats2bfloat162_rn(o[2 * e], o[2 * e + 1]);
+    *reinterpret_cast<uint4*>(orow + i * 8) = pk;
   }
   __syncthreads();
   ew_mark(tr, 3);
@@ -283,10 +282,11 @@ __global__ void __launch_bounds__(256) silu_mul_kernel(Acc* __restrict__ acc, in
 template <typename Acc>
 dl_status launch_silu_flat(Acc* acc, int64_t lda, __nv_bfloat16* act, int64_t ldo, int64_t T, int64_t m, int relu,
                            cudaStream_t st, const SideZero& z, int clear = 1) {
-  const int64_t items = T * (m / 8);
-  const int grid = static_cast<int>(std::min<int64_t>((items + 256 * kSiluU - 1) / (256 * kSiluU), 8 * num_sms()));
-  return launch_pdl(silu_mul_kernel<Acc>, dim3(grid > 0 ? grid : 1), dim3(256), 0, st, "silu_mul", acc, lda, act, ldo,
-                    static_cast<int>(m), static_cast<int>(T), relu, clear, z, ew_trace(1));
+  const int per_row = static_cast<int>(m / 8);
+  const int gx = (per_row + 256 * kSiluU - 1) / (256 * kSiluU);
+  return launch_pdl(silu_mul_kernel<Acc>, dim3(gx > 0 ? gx : 1, static_cast<unsigned>(T)), dim3(256), 0, st,
+                    "silu_mul", acc, lda, act, ldo, static_cast<int>(m), static_cast<int>(T), relu, clear, z,
+                    ew_trace(1));
 }
 
 // 2-D elementwise over [T x n] in groups of 4 columns: grid (ceil(n/4/256), T).
@@ -387,9 +387,98 @@ struct ReluBf16 {
   }
 };
 
-// RoPE + cache append.  grid (ceil(heads*d/4 / 128), T); one thread per 4 dims
-// = two rotation pairs (2i, 2i+1) by pos * theta^(-2i/d).
+// RoPE + cache append.  Thread = (token, rotation pair p of the head dim):
+// its angle pos * theta^(-2p/d) is computed once (before griddepcontrol.wait:
+// positions, cache lengths and cu_seqlens are call inputs) and applied to
+// kRopeHeads heads; grid (head groups, tokens), 128 threads = 2 x 64 pairs.
+constexpr int kRopeHeads = 5;
+constexpr int kRopeVec = 2;   // rotation pairs per thread (8-byte bf16 accesses)
 __global__ void __launch_bounds__(128) rope_cache_kernel(RopeCacheArgs a, EwTrace tr) {
+  ew_mark(tr, 1);
+  pdl_trigger();   // successor may launch now; it waits for us before reading
+  constexpr int TPH = 64 / kRopeVec;                    // threads per head (d = 128)
+  const int heads = a.Hq + 2 * a.Hk;
+  const int p0 = (threadIdx.x % TPH) * kRopeVec;        // first rotation pair of this thread
+  const int hg = blockIdx.x * (128 / TPH) + threadIdx.x / TPH;
+  const int h0 = hg * kRopeHeads;
+  const int64_t t = blockIdx.y;
+  const bool active = 2 * p0 < a.d && h0 < heads;
+  float sn[kRopeVec], cs[kRopeVec];
+#pragma unroll
+  for (int q = 0; q < kRopeVec; ++q) {
+    sn[q] = 0.f;
+    cs[q] = 1.f;
+  }
+  if (active && a.rope && h0 < a.Hq + a.Hk) {
+    // angle = pos * theta^(-2p/d) in fp32 (relative error ~1e-7, i.e. <= 3e-4 rad at
+    // position 2048, far below bf16 resolution); full-range-reduction sincosf
+    const float pos = static_cast<float>(a.positions[t]);
+    const float l2t = log2f(a.theta);
+#pragma unroll
+    for (int q = 0; q < kRopeVec; ++q)
+      sincosf(pos * exp2f(-l2t * static_cast<float>(2 * (p0 + q)) / a.d), &sn[q], &cs[q]);
+  }
+  int64_t slot = 0;   // cache row of this token for kv head 0: (s * Hk) * max_seq + cpos
+  if (active && h0 + kRopeHeads > a.Hq) {
+    int s;
+    int64_t cpos;
+    if (a.decode) {
+      s = static_cast<int>(t);
+      cpos = a.cache_lens[s];
+    } else {
+      int lo = 0, hi = a.num_seqs - 1;   // last s with cu[s] <= t
+      while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (a.cu_seqlens[mid] <= t) lo = mid; else hi = mid - 1;
+      }
+      s = lo;
+      cpos = a.cache_lens[s] + (t - a.cu_seqlens[s]);
+    }
+    slot = static_cast<int64_t>(s) * a.Hk * a.max_seq + cpos;
+  }
+  pdl_wait();
+  ew_mark(tr, 2);
+  side_zero(a.zero);
+  side_zero(a.zero2);
+  if (!active) return;
+  float4 v[kRopeHeads];
+#pragma unroll
+  for (int j = 0; j < kRopeHeads; ++j) {
+    const int hd = h0 + j;
+    if (hd >= heads) break;
+    const int64_t col = static_cast<int64_t>(hd) * a.d + 2 * p0;
+    if (a.acc) {
+      float* q = const_cast<float*>(a.acc) + t * a.ld_src + col;
+      v[j] = *reinterpret_cast<const float4*>(q);
+      if (a.clear) *reinterpret_cast<float4*>(q) = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      v[j] = load4(a.src + t * a.ld_src + col);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kRopeHeads; ++j) {
+    const int hd = h0 + j;
+    if (hd >= heads) break;
+    float4 r = v[j];
+    if (a.rope && hd < a.Hq + a.Hk)
+      r = make_float4(r.x * cs[0] - r.y * sn[0], r.x * sn[0] + r.y * cs[0], r.z * cs[1] - r.w * sn[1],
+                      r.z * sn[1] + r.w * cs[1]);
+    if (hd < a.Hq) {
+      store4(a.q_out + t * static_cast<int64_t>(a.Hq) * a.d + static_cast<int64_t>(hd) * a.d + 2 * p0, r.x, r.y, r.z,
+             r.w);
+    } else {
+      const bool is_k = hd < a.Hq + a.Hk;
+      const int kvh = is_k ? hd - a.Hq : hd - a.Hq - a.Hk;
+      store4((is_k ? a.k_cache : a.v_cache) + (slot + static_cast<int64_t>(kvh) * a.max_seq) * a.d + 2 * p0, r.x, r.y,
+             r.z, r.w);
+    }
+  }
+  ew_mark(tr, 3);
+}
+
+// Decode-size variant (T <= 256): one thread per 4 dims of one token, grid
+// (ceil(heads*d/4 / 128), T) -- more threads per token, shorter per-thread chains.
+__global__ void __launch_bounds__(128) rope_cache_tok_kernel(RopeCacheArgs a, EwTrace tr) {
   ew_mark(tr, 1);
   pdl_trigger();   // successor may launch now; it waits for us before reading
   // Everything that depends only on the call's inputs (positions, cache
@@ -679,8 +768,18 @@ dl_status launch_relu_bf16(const __nv_bfloat16* src, int64_t lds, __nv_bfloat16*
 }
 dl_status launch_rope_cache(const RopeCacheArgs& a, cudaStream_t st) {
   if (a.T <= 0) return DL_OK;
-  const int per_tok = (a.Hq + 2 * a.Hk) * (a.d / 4);
-  dim3 grid((per_tok + 127) / 128, static_cast<unsigned>(a.T));
+  if (a.T <= 256 && a.d % 4 == 0) {
+    const int per_tok = (a.Hq + 2 * a.Hk) * (a.d / 4);
+    dim3 grid((per_tok + 127) / 128, static_cast<unsigned>(a.T));
+    return launch_pdl(rope_cache_tok_kernel, grid, dim3(128), 0, st, "rope_cache", a, ew_trace(3));
+  }
+  if (a.d != 128) {
+    set_error("rope_cache: head_dim %d unsupported (128)", a.d);
+    return DL_ERR_UNSUPPORTED;
+  }
+  const int groups = (a.Hq + 2 * a.Hk + kRopeHeads - 1) / kRopeHeads;
+  const int per_cta = 128 / (64 / kRopeVec);
+  dim3 grid((groups + per_cta - 1) / per_cta, static_cast<unsigned>(a.T));
   return launch_pdl(rope_cache_kernel, grid, dim3(128), 0, st, "rope_cache", a, ew_trace(3));
 }
 dl_status launch_embedding(const __nv_bfloat16* table, int64_t vocab, int64_t h, const int32_t* ids, int64_t T,

@@ -829,6 +829,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int lane = threadIdx.x % 32;
   const uint32_t rank = ptx::cluster_ctarank();
   const bool leader = rank == 0;
+  unsigned long long* tr = (g_trace && a.trace_slot >= 0 && blockIdx.x < 148)
+                               ? g_trace + (static_cast<long long>(a.trace_slot) * 148 + blockIdx.x) * 8
+                               : nullptr;   // debug timeline: [0] entry, [6] epilogue done
+  if (tr && threadIdx.x == 0) { tr[0] = gtime(); tr[7] = smid(); }
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&maps.act);
@@ -998,6 +1002,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   }
 
+  if (tr && warp == 2 && lane == 0) tr[6] = gtime();
   ptx::tc_fence_before();
   ptx::cluster_sync();
   ptx::tc_fence_after();
