@@ -93,9 +93,12 @@ __global__ void __launch_bounds__(128, KTP == 32 ? 3 : 1) attn_prefill_kernel(At
   pdl_trigger();   // successor may launch now; it waits for us before reading
   pdl_wait();
   ew_mark(tr, 2);
-  const int s = blockIdx.z, h = blockIdx.y;
+  // 1-D (q tile, head) order, heaviest causal q tiles first: the light ones
+  // fill the tail of the launch (blockIdx.x = (qtiles-1-qt) * Hq + h)
+  const int s = blockIdx.z;
+  const int h = blockIdx.x % a.Hq;
+  const int q0 = (static_cast<int>(gridDim.x) / a.Hq - 1 - static_cast<int>(blockIdx.x) / a.Hq) * QT;
   const int n_new = a.cu_seqlens[s + 1] - a.cu_seqlens[s];
-  const int q0 = blockIdx.x * QT;
   if (q0 >= n_new) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t4 = lane & 3;
@@ -1071,7 +1074,7 @@ dl_status launch_attention(const AttnArgs& a, cudaStream_t st) {
     }
     // grid.x covers the longest sequence: bounded by T
     const int qtiles = static_cast<int>((a.T + QT - 1) / QT);
-    dim3 grid(qtiles, a.Hq, a.num_seqs);
+    dim3 grid(qtiles * a.Hq, 1, a.num_seqs);
     return launch_pdl(attn_prefill_kernel<KTP>, grid, dim3(128), SMEM, st, "attention prefill", a, ew_trace(5));
   }
   {
