@@ -392,9 +392,10 @@ def main():
         step_bytes += 2 * n_layers * shape.h * (ranks["o"] + ranks["down"]) * (1 - 1 / world)
     step_gbs = step_bytes / (step_ms * 1e-3) / 1e9
 
-    # ---- e2e: H2D ids from pinned host, graph, D2H logits into pinned host -----
+    # ---- e2e: H2D ids from pinned host, graph, D2H of the step's result (the greedy next
+    # token of every sequence, argmax over the gathered logits on the device) -----
     ids_h = model.ids.to("cpu").pin_memory()
-    out_dev = model.logits_local if world == 1 else model.logits
+    out_dev = model.next_ids
     out_h = torch.empty(out_dev.shape, dtype=out_dev.dtype, pin_memory=True)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

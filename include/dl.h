@@ -370,6 +370,11 @@ dl_status dl_decomposed_block_forward_kvlr(
  * final norm + dense LM head).  Not part of the paper's method; provided so
  * a whole-model step runs in this library's kernels only.
  * ---------------------------------------------------------------------- */
+/* Greedy next token: ids[t] = argmax_v logits (bf16) over P vocab shards,
+ * element (t, global id p*vloc + v) at logits[p*rank_stride + t*ld + v]
+ * (P = 1: plain [T x ld]); ties go to the smallest id.  ids: device int32 [T]. */
+dl_status dl_argmax(const void *logits, int64_t T, int64_t vloc, int32_t P,
+                    int64_t rank_stride, int64_t ld, int32_t *ids, void *stream);
 /* out[t] = table[ids[t]]   (table [vocab x h] bf16, out [T x h] bf16)     */
 dl_status dl_embedding(const void *table, int64_t vocab, int64_t h,
                        const int32_t *ids, int64_t T, void *out, void *stream);

@@ -4,7 +4,7 @@
 """
 from ._lib import (DL_BF16, DL_DECODE, DL_F32, DL_LAYOUT_DEINFER, DL_LAYOUT_RANK_PARALLEL, DL_MLP_RELU,
                    DL_MLP_SILU_GLU, DL_PREFILL, EXPORTS, dl_deinfer_shard_factors, LowRankKVCache, dl_kv_prepare,
-                   dl_decomposed_block_forward_kvlr, dl_decomposed_stack_forward, StackArgs, BlockWeights, Comm, DLError,  # noqa: F401
+                   dl_decomposed_block_forward_kvlr, dl_decomposed_stack_forward, StackArgs, dl_argmax, BlockWeights, Comm, DLError,  # noqa: F401
                    dl_block_config, dl_block_workspace, dl_comm_create, dl_decomposed_block_forward, dl_dense,
                    dl_device_ok, dl_embedding, dl_lowrank_linear, dl_lowrank_linear_workspace, dl_rmsnorm,
                    dl_tp_plan, dl_tp_shard_factors, dl_version, load, make_block_config,

@@ -25,7 +25,7 @@ EXPORTS = ("dl_last_error", "dl_version", "dl_device_ok", "dl_comm_create", "dl_
            "dl_dense_workspace", "dl_dense", "dl_launch_count", "dl_profile_begin", "dl_profile_end",
            "dl_profile_count", "dl_profile_get", "dl_debug_gemm_trace", "dl_debug_fused_trace", "dl_deinfer_shard_factors",
            "dl_kv_prepare", "dl_decomposed_block_forward_kvlr", "dl_comm_create_loopback",
-           "dl_decomposed_stack_forward", "dl_debug_ew_trace", "dl_debug_linear_gathered")
+           "dl_decomposed_stack_forward", "dl_debug_ew_trace", "dl_debug_linear_gathered", "dl_argmax")
 
 
 class DLError(RuntimeError):
@@ -103,6 +103,7 @@ def load():
                                                         I64, P, P, I32, I, ctypes.POINTER(P), ctypes.POINTER(P), P,
                                                         I64, P, P, ctypes.c_size_t, P]
             lib.dl_embedding.argtypes = [P, I64, I64, P, I64, P, P]
+            lib.dl_argmax.argtypes = [P, I64, I64, I32, I64, I64, P, P]
             lib.dl_rmsnorm.argtypes = [P, P, P, I64, I64, ctypes.c_float, P]
             lib.dl_dense_workspace.argtypes = [I64, I64, I64, ctypes.POINTER(ctypes.c_size_t)]
             lib.dl_dense.argtypes = [P, I64, P, I64, P, I64, I64, I64, I64, P, ctypes.c_size_t, P]
@@ -519,6 +520,14 @@ def dl_profile_records():
         _check(L.dl_profile_get(i, ctypes.byref(ms), ctypes.byref(b), ctypes.byref(f), ctypes.byref(k)))
         out.append((ms.value, b.value, f.value, k.value))
     return out
+
+
+def dl_argmax(logits: torch.Tensor, ids: torch.Tensor, stream=None) -> torch.Tensor:
+    """Greedy next token over vocab shards: logits [P, T, vloc] or [T, vloc] (bf16) -> ids [T] int32."""
+    lg = logits if logits.dim() == 3 else logits.unsqueeze(0)
+    P, T, vloc = lg.shape
+    _check(load().dl_argmax(_ptr(lg), T, vloc, P, lg.stride(0), lg.stride(1), _ptr(ids), _stream(stream)))
+    return ids
 
 
 def dl_debug_linear_gathered(Xg: torch.Tensor, A: torch.Tensor, B: torch.Tensor, Y: torch.Tensor, stream=None):

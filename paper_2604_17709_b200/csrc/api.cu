@@ -1652,6 +1652,19 @@ dl_status dl_kv_prepare(const int32_t* block_tables, int64_t max_blocks_per_seq,
 // ---------------------------------------------------------------------------
 // model-level helpers
 // ---------------------------------------------------------------------------
+dl_status dl_argmax(const void* logits, int64_t T, int64_t vloc, int32_t P, int64_t rank_stride, int64_t ld,
+                    int32_t* ids, void* stream) {
+  if (T == 0) return DL_OK;
+  DL_TRY(check_ptr(logits, "logits"));
+  if (!ids || vloc < 1 || P < 1 || ld < vloc || (P > 1 && rank_stride < T * ld) || P * vloc > 0x7fffffff) {
+    set_error("dl_argmax: bad arguments");
+    return DL_ERR_INVALID_ARG;
+  }
+  DL_TRY(check_device());
+  return launch_argmax(static_cast<const __nv_bfloat16*>(logits), T, vloc, P, rank_stride, ld, ids,
+                       static_cast<cudaStream_t>(stream));
+}
+
 dl_status dl_embedding(const void* table, int64_t vocab, int64_t h, const int32_t* ids, int64_t T, void* out,
                        void* stream) {
   if (T == 0) return DL_OK;

@@ -274,6 +274,8 @@ dl_status launch_relu_bf16(const __nv_bfloat16* src, int64_t ld_src, __nv_bfloat
                            int64_t T, int64_t m, cudaStream_t st, int clear = 0, const SideZero& z = SideZero{});
 // RoPE + cache append as a standalone kernel (see RopeCacheArgs)
 dl_status launch_rope_cache(const RopeCacheArgs& a, cudaStream_t st);
+dl_status launch_argmax(const __nv_bfloat16* logits, int64_t T, int64_t vloc, int P, int64_t rank_stride,
+                        int64_t ld, int32_t* ids, cudaStream_t st);
 dl_status launch_embedding(const __nv_bfloat16* table, int64_t vocab, int64_t h,
                            const int32_t* ids, int64_t T, __nv_bfloat16* out,
                            cudaStream_t st);

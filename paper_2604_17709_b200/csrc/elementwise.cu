@@ -551,6 +551,57 @@ __global__ void __launch_bounds__(256) embedding_kernel(const __nv_bfloat16* __r
   for (int i = threadIdx.x; i < h / 8; i += blockDim.x) dst[i] = src[i];
 }
 
+// Greedy next token: ids[t] = argmax over the P vocab shards of
+// logits[p * rank_stride + t * ld + v] (v < vloc; global id p * vloc + v).
+// One CTA (512 threads) per token; ties -> the smallest id.
+__global__ void __launch_bounds__(512) argmax_kernel(const __nv_bfloat16* __restrict__ logits, int64_t vloc, int P,
+                                                     int64_t rank_stride, int64_t ld, int32_t* __restrict__ ids) {
+  pdl_trigger();   // successor may launch now; it waits for us before reading
+  pdl_wait();
+  __shared__ float sv[16];
+  __shared__ int si[16];
+  const int64_t t = blockIdx.x;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int p = 0; p < P; ++p) {
+    const __nv_bfloat16* row = logits + p * rank_stride + t * ld;
+    for (int64_t v = threadIdx.x * 8; v < vloc; v += 512 * 8) {
+      if (v + 8 <= vloc && ((reinterpret_cast<uintptr_t>(row + v) & 15) == 0)) {
+        const uint4 u = *reinterpret_cast<const uint4*>(row + v);
+        const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float f = __bfloat162float(b[e]);
+          const int id = static_cast<int>(p * vloc + v + e);
+          if (f > best || (f == best && id < bi)) { best = f; bi = id; }
+        }
+      } else {
+        for (int64_t e = v; e < v + 8 && e < vloc; ++e) {
+          const float f = __bfloat162float(row[e]);
+          const int id = static_cast<int>(p * vloc + e);
+          if (f > best || (f == best && id < bi)) { best = f; bi = id; }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sv[threadIdx.x >> 5] = best;
+    si[threadIdx.x >> 5] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 16; ++w)
+      if (sv[w] > best || (sv[w] == best && si[w] < bi)) { best = sv[w]; bi = si[w]; }
+    ids[t] = bi;
+  }
+}
+
 // [P][T][w] -> [T][P*w]; grid (ceil(w/8 / 128), T, P)
 __global__ void __launch_bounds__(128) unpermute_kernel(const __nv_bfloat16* __restrict__ src,
                                                         __nv_bfloat16* __restrict__ dst, int P, int64_t T,
@@ -781,6 +832,12 @@ dl_status launch_rope_cache(const RopeCacheArgs& a, cudaStream_t st) {
   const int per_cta = 128 / (64 / kRopeVec);
   dim3 grid((groups + per_cta - 1) / per_cta, static_cast<unsigned>(a.T));
   return launch_pdl(rope_cache_kernel, grid, dim3(128), 0, st, "rope_cache", a, ew_trace(3));
+}
+dl_status launch_argmax(const __nv_bfloat16* logits, int64_t T, int64_t vloc, int P, int64_t rank_stride,
+                        int64_t ld, int32_t* ids, cudaStream_t st) {
+  if (T <= 0) return DL_OK;
+  return launch_pdl(argmax_kernel, dim3(static_cast<unsigned>(T)), dim3(512), 0, st, "argmax", logits, vloc, P,
+                    rank_stride, ld, ids);
 }
 dl_status launch_embedding(const __nv_bfloat16* table, int64_t vocab, int64_t h, const int32_t* ids, int64_t T,
                            __nv_bfloat16* out, cudaStream_t st) {

@@ -86,6 +86,7 @@ class DecomposedLlama:
         vloc = lm_head_local.shape[0]
         self.logits_local = torch.zeros(batch, vloc, dtype=bf, device=self.device)
         self.logits = torch.zeros(self.world, batch, vloc, dtype=bf, device=self.device)
+        self.next_ids = torch.zeros(batch, dtype=torch.int32, device=self.device)   # greedy tokens of the step
         self.prefill_tokens = prefill_tokens
         if prefill_tokens:
             self.pre_cfgs = [L.make_block_config(s, r, max_tokens=prefill_tokens, max_seqs=1, layout=layout)
@@ -140,6 +141,8 @@ class DecomposedLlama:
         elif self.world > 1:
             import torch.distributed as dist
             dist.all_gather_into_tensor(self.logits, self.logits_local)
+        # greedy next token over the (gathered) vocab shards, on the device
+        L.dl_argmax(self.logits_local if self.world == 1 else self.logits, self.next_ids)
         return self.logits_local if self.world == 1 else self.logits
 
     # one sequence of prefill_tokens tokens; logits of its last token

@@ -397,6 +397,21 @@ def test_deinfer_shard_factors_match_slices(dl, world):
     assert start == Bcat.shape[0]
 
 
+@pytest.mark.parametrize("P,T,vloc", [(1, 64, 1000), (4, 7, 333), (8, 64, 16032)])
+def test_argmax_over_vocab_shards(dl, P, T, vloc):
+    """Greedy next token over P vocab shards (bit-exact index work): equals argmax of
+    the concatenated logits, ties to the smallest id."""
+    g = torch.Generator().manual_seed(P * 100 + T)
+    lg = (torch.randn(P, T, vloc, generator=g) * 3).round().to(torch.bfloat16)   # many ties
+    ids = torch.empty(T, dtype=torch.int32, device="cuda")
+    dl.dl_argmax(lg.cuda() if P > 1 else lg[0].cuda(), ids)
+    torch.cuda.synchronize()
+    full = lg.permute(1, 0, 2).reshape(T, P * vloc).float()
+    mx = full.max(dim=1, keepdim=True).values
+    ref = torch.where(full == mx, torch.arange(P * vloc).float(), float("inf")).min(dim=1).values.long()
+    assert torch.equal(ids.cpu().long(), ref)
+
+
 def test_model_decode_variadic_layer_ranks(dl, orc):
     """N4 variadic per-layer ranks through the whole-model decode step: two
     layers compressed at 40% and 20%; hidden state after the blocks vs the
