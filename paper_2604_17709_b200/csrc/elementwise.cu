@@ -152,7 +152,12 @@ __global__ void __launch_bounds__(kRnThreads) residual_rmsnorm_kernel(Acc* __res
   for (int k = 0; k < kRnChunks; ++k) {
     const int i = threadIdx.x + k * kRnThreads;
     if (i < n8) {
-      take8(ar + 8 * i, av[k]);
+      if (acc) {
+        take8(ar + 8 * i, av[k]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) av[k][e] = 0.f;
+      }
       v[k] = xr[i];
       gv[k] = gr[i];
     }
@@ -170,7 +175,7 @@ __global__ void __launch_bounds__(kRnThreads) residual_rmsnorm_kernel(Acc* __res
       f = __bfloat1622float2(b[e]);   // the norm reads the bf16-rounded x
       ss += f.x * f.x + f.y * f.y;
     }
-    xr[i] = v[k];
+    if (acc) xr[i] = v[k];
   }
   ss = warp_sum(ss);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
@@ -753,6 +758,10 @@ dl_status launch_latent_unpermute(const __nv_bfloat16* recv, __nv_bfloat16* zb, 
 dl_status launch_rmsnorm(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bfloat16* y, int64_t T, int64_t h,
                          float eps, cudaStream_t st) {
   if (T <= 0) return DL_OK;
+  if (h % 8 == 0 && h / 8 <= kRnThreads * kRnChunks)   // register-resident one-pass kernel, no accumulator
+    return launch_pdl(residual_rmsnorm_kernel<float>, dim3(static_cast<unsigned>(T)), dim3(kRnThreads), 0, st,
+                      "rmsnorm", static_cast<float*>(nullptr), int64_t{0}, const_cast<__nv_bfloat16*>(x), g, y,
+                      static_cast<int>(h), eps, SideZero{}, SideZero{}, ew_trace(2));
   return launch_pdl(rmsnorm_kernel, dim3(static_cast<unsigned>(T)), dim3(256), 0, st, "rmsnorm", x, g, y,
                     static_cast<int>(h), eps);
 }
