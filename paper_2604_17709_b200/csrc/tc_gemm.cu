@@ -82,6 +82,7 @@ struct KArgs {
   int chunk;
   int l2pf;                  // weight tiles prefetched into L2 before griddepcontrol.wait
   int act_w;                 // > 0: 3-D activation map, column c -> (c % act_w, token, c / act_w)
+  int wpol;                  // pair kernel weight L2 policy: 0 evict_first, 1 evict_normal, 2 evict_last
   // DP + stream-K tail (whole-tile kernels): tiles [0, dp_tiles) whole, each of
   // the remaining tiles split in tail_split K-pieces accumulated in fp32 into
   // tail_acc [tail tile][256][256], finalized by tc_tail_finalize_kernel.
@@ -860,7 +861,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ===================== TMA producer (both CTAs) =====================
     if (lane == 0) {
-      const uint64_t pol_w = ptx::policy_evict_first();
+      // weights: every feature tile is read by all T/256 token tiles of the
+      // cluster schedule, so they are kept in L2 (evict_first -- right for the
+      // decode stream -- made the prefill gate|up GEMM read 1.69x its bytes)
+      const uint64_t pol_w = a.wpol == 0 ? ptx::policy_evict_first()
+                             : a.wpol == 1 ? ptx::policy_evict_normal() : ptx::policy_evict_last();
       const uint64_t pol_a = ptx::policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
@@ -1187,6 +1192,8 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   a.scatter_p = p.out.scatter_p;
   a.slab = p.out.slab;
   a.trace_slot = g_trace_host_on ? g_trace_next++ : -1;
+  static const int wpol = getenv("DL_PAIR_WPOL") ? atoi(getenv("DL_PAIR_WPOL")) : 2;   // A/B: 0 / 1 / 2 (measured best: 2)
+  a.wpol = wpol;
   a.dp_tiles = tiles;
   a.tail_split = 0;
   a.tail_acc = nullptr;
