@@ -207,10 +207,11 @@ def test_block_decode_small(dl, orc, cache_lens):
     assert rel(kg, kn) <= TOL_BF16
 
 
-@pytest.mark.parametrize("S", [100, 200, 256])
+@pytest.mark.parametrize("S", [100, 200, 256, 300])
 def test_block_decode_wide_batches(dl, orc, S):
-    """Decode batches on the 128- and 256-token swap-AB configurations (the bench runs 64):
-    bf16x2 latent / gate|up reductions, stream-K attention over S sequences, run twice."""
+    """Decode batches on the 128- and 256-token swap-AB configurations (the bench runs 64)
+    and beyond (300: whole-tile GEMMs): bf16x2 latent / gate|up reductions, stream-K
+    attention over S sequences, run twice."""
     s = SMALL
     rk = block_ranks(s, 0.4)
     w = gen_block_weights(s, rk, 0, 50 + S)
