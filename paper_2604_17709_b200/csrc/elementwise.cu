@@ -208,6 +208,77 @@ __global__ void __launch_bounds__(kRnThreads) residual_rmsnorm_kernel(Acc* __res
   ew_mark(tr, 3);
 }
 
+// Plain RMSNorm for many rows (prefill): 4 rows per CTA, 256 threads per row,
+// each thread holding its 4 chunks of 8 in registers (h <= 8192, h % 2048 == 0
+// not required: chunks past h are skipped); all loads issued before the
+// per-row reduction (named barrier per row group).
+constexpr int kRrRows = 4;
+constexpr int kRrThreads = 256;
+constexpr int kRrChunks = 4;
+__global__ void __launch_bounds__(kRrRows * kRrThreads) rmsnorm_rows_kernel(const __nv_bfloat16* __restrict__ x,
+                                                                         const __nv_bfloat16* __restrict__ g,
+                                                                         __nv_bfloat16* __restrict__ y, int64_t T,
+                                                                         int h, float eps, EwTrace tr) {
+  ew_mark(tr, 1);
+  pdl_trigger();   // successor may launch now; it waits for us before reading
+  pdl_wait();
+  ew_mark(tr, 2);
+  __shared__ float red[kRrRows][8];
+  const int rg = threadIdx.x / kRrThreads, lt = threadIdx.x % kRrThreads;
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * kRrRows + rg;
+  const bool row_ok = t < T;
+  const int n8 = h / 8;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + (row_ok ? t : 0) * h);
+  const uint4* gr = reinterpret_cast<const uint4*>(g);
+  uint4 v[kRrChunks], gv[kRrChunks];
+#pragma unroll
+  for (int k = 0; k < kRrChunks; ++k) {
+    const int i = lt + k * kRrThreads;
+    if (row_ok && i < n8) {
+      v[k] = xr[i];
+      gv[k] = gr[i];
+    }
+  }
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < kRrChunks; ++k) {
+    const int i = lt + k * kRrThreads;
+    if (!row_ok || i >= n8) continue;
+    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v[k]);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(b[e]);
+      ss += f.x * f.x + f.y * f.y;
+    }
+  }
+  ss = warp_sum(ss);
+  if ((lt & 31) == 0) red[rg][lt >> 5] = ss;
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + rg), "r"(kRrThreads) : "memory");
+  float tot = 0.f;
+#pragma unroll
+  for (int w = 0; w < kRrThreads / 32; ++w) tot += red[rg][w];
+  if (!row_ok) return;
+  const float inv = rsqrtf(tot / static_cast<float>(h) + eps);
+  uint4* yr = reinterpret_cast<uint4*>(y + t * h);
+#pragma unroll
+  for (int k = 0; k < kRrChunks; ++k) {
+    const int i = lt + k * kRrThreads;
+    if (i >= n8) continue;
+    uint4 o;
+    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v[k]);
+    const __nv_bfloat162* gb = reinterpret_cast<const __nv_bfloat162*>(&gv[k]);
+    __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(b[e]);
+      const float2 w = __bfloat1622float2(gb[e]);
+      ob[e] = __floats2bfloat162_rn(f.x * inv * w.x, f.y * inv * w.y);
+    }
+    yr[i] = o;
+  }
+  ew_mark(tr, 3);
+}
+
 // act[t][c..c+7] = bf16(silu(gate) * up) from the fp32 stage-2 accumulator
 // (gate at column c, up at m + c; both consumed and cleared).  Flat item
 // space (t, 8-column group), grid-stride, kSiluU items per thread with every
@@ -758,6 +829,9 @@ dl_status launch_latent_unpermute(const __nv_bfloat16* recv, __nv_bfloat16* zb, 
 dl_status launch_rmsnorm(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bfloat16* y, int64_t T, int64_t h,
                          float eps, cudaStream_t st) {
   if (T <= 0) return DL_OK;
+  if (T >= 512 && h % 8 == 0 && h / 8 <= kRrThreads * kRrChunks)   // many rows: 4 rows per CTA
+    return launch_pdl(rmsnorm_rows_kernel, dim3(static_cast<unsigned>((T + kRrRows - 1) / kRrRows)),
+                      dim3(kRrRows * kRrThreads), 0, st, "rmsnorm", x, g, y, T, static_cast<int>(h), eps, ew_trace(2));
   if (h % 8 == 0 && h / 8 <= kRnThreads * kRnChunks)   // register-resident one-pass kernel, no accumulator
     return launch_pdl(residual_rmsnorm_kernel<float>, dim3(static_cast<unsigned>(T)), dim3(kRnThreads), 0, st,
                       "rmsnorm", static_cast<float*>(nullptr), int64_t{0}, const_cast<__nv_bfloat16*>(x), g, y,
