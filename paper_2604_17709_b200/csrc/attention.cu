@@ -68,6 +68,11 @@ __device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+__device__ __forceinline__ float ex2(float x) {   // 2^x, MUFU.EX2 (ex2(-inf) = 0)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -168,21 +173,20 @@ __global__ void __launch_bounds__(128, KTP == 32 ? 3 : 1) attn_prefill_kernel(At
         mma16816(sc[2 * np + 1], qf[kk], b2, b3);
       }
     }
-    // ---- scale, causal mask, online softmax ----
+    // ---- causal mask, online softmax (m kept in scaled log2 units; the
+    //      1/sqrt(d) * log2(e) scale is folded into one FFMA per score) ----
     const int64_t kbase = static_cast<int64_t>(kt) * KTP;
     const bool need_mask = kbase + KTP - 1 > base_pos + q0 + warp * 16 || kbase + KTP > n_keys;
     float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
     for (int nt = 0; nt < KTP / 8; ++nt) {
+      if (need_mask) {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        float v = sc[nt][e] * scale;
-        if (need_mask) {
+        for (int e = 0; e < 4; ++e) {
           const int64_t kp = kbase + nt * 8 + 2 * t4 + (e & 1);
           const int64_t qp = (e < 2) ? qpos0 : qpos1;
-          if (kp > qp || kp >= n_keys) v = -INFINITY;
+          if (kp > qp || kp >= n_keys) sc[nt][e] = -INFINITY;
         }
-        sc[nt][e] = v;
       }
       mx0 = fmaxf(mx0, fmaxf(sc[nt][0], sc[nt][1]));
       mx1 = fmaxf(mx1, fmaxf(sc[nt][2], sc[nt][3]));
@@ -191,10 +195,10 @@ __global__ void __launch_bounds__(128, KTP == 32 ? 3 : 1) attn_prefill_kernel(At
     mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
     mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
     mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
-    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+    const float mn0 = fmaxf(m0, mx0 * scale), mn1 = fmaxf(m1, mx1 * scale);
     // rows whose every key so far is masked keep m = -inf: use 0 as the exp base
     const float b0 = mn0 == -INFINITY ? 0.f : mn0, b1 = mn1 == -INFINITY ? 0.f : mn1;
-    const float c0 = exp2f(m0 - b0), c1 = exp2f(m1 - b1);
+    const float c0 = ex2(m0 - b0), c1 = ex2(m1 - b1);
     m0 = mn0;
     m1 = mn1;
     l0 *= c0;
@@ -207,8 +211,8 @@ __global__ void __launch_bounds__(128, KTP == 32 ? 3 : 1) attn_prefill_kernel(At
     uint32_t pf[KTP / 16][4];
 #pragma unroll
     for (int nt = 0; nt < KTP / 8; ++nt) {
-      const float p0 = exp2f(sc[nt][0] - b0), p1 = exp2f(sc[nt][1] - b0);
-      const float p2 = exp2f(sc[nt][2] - b1), p3 = exp2f(sc[nt][3] - b1);
+      const float p0 = ex2(fmaf(sc[nt][0], scale, -b0)), p1 = ex2(fmaf(sc[nt][1], scale, -b0));
+      const float p2 = ex2(fmaf(sc[nt][2], scale, -b1)), p3 = ex2(fmaf(sc[nt][3], scale, -b1));
       l0 += p0 + p1;
       l1 += p2 + p3;
       const int j = nt >> 1;
@@ -565,11 +569,6 @@ __device__ __forceinline__ void sk_item_at(const int32_t* P, int num_seqs, int p
   it.n_keys = cache_lens[s] + 1;
 }
 
-__device__ __forceinline__ float ex2(float x) {   // 2^x, MUFU.EX2 (ex2(-inf) = 0)
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
 __device__ __forceinline__ uint32_t sk_swz(uint32_t base, int key, int chunk) {   // 128B-swizzled TMA box pair
   return base + ((chunk >> 3) << 13) + key * 128 + ((((chunk & 7) ^ (key & 7))) << 4);
 }
