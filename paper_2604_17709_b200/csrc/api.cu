@@ -1394,12 +1394,20 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   if (!prenormed)
     DL_TRY(launch_rmsnorm(x, static_cast<const __nv_bfloat16*>(w->attn_norm), ws.xn, T, d.h, cfg->rms_eps, st));
   SideZero zq;
+  static const bool fix_rope = getenv("DL_FIXUP_ROPE") && atoi(getenv("DL_FIXUP_ROPE")) != 0;   // A/B switch
+  const bool fx_rope = !fx && !kv && !tp && skinny && fix_rope && !rope_attn && phase == DL_DECODE && num_seqs <= 1024;
   if (kv) {
     DL_TRY(kvlr_attention(cfg, d, w, ws, kv, T, positions, cache_lens, false, comm, aa, rc, st));
   } else if (fx) {
     GemmFixup f = fixup(FIX_ROPE_CACHE);
     f.rope = rc;
     DL_TRY(run_group(w->qkv, 3, qkv_rows, ws.xn, d.h, d.h, T, skinny, ws, qkv_out, st, &f));
+  } else if (fx_rope) {
+    // RoPE + cache append by the q|k|v stage-2 last-contributor fixup alone
+    // (DL_FIXUP_ROPE=1); the latent clear moves to the attention kernel
+    GemmFixup f = fixup(FIX_ROPE_CACHE);
+    f.rope = rc;
+    DL_TRY(run_group(w->qkv, 3, qkv_rows, ws.xn, d.h, d.h, T, skinny, ws, qkv_out, st, &f, &zq));
   } else {
     DL_TRY(run_group(w->qkv, 3, qkv_rows, ws.xn, d.h, d.h, T, skinny, ws, qkv_out, st, nullptr, &zq));
   }
@@ -1439,7 +1447,8 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
     aa.zero = zq;
     DL_TRY(launch_attention(aa, st));
   } else {
-    if (!fx && !kv) DL_TRY(launch_rope_cache(rc, st));
+    if (fx_rope) aa.zero = zq;
+    if (!fx && !kv && !fx_rope) DL_TRY(launch_rope_cache(rc, st));
     if (!kv) DL_TRY(launch_attention(aa, st));
   }
 

@@ -126,7 +126,7 @@ print("ERRS", errs)
 '''
 
 
-@pytest.mark.parametrize("knob", ["DL_FIXUP", "DL_ROPE_FUSE"])
+@pytest.mark.parametrize("knob", ["DL_FIXUP", "DL_ROPE_FUSE", "DL_FIXUP_ROPE"])
 def test_block_decode_stream_k_fixups(knob):
     """Opt-in decode variants must match the oracle: DL_FIXUP=1 (RoPE+cache,
     residual and SiLU*up finalized inside the stage-2 GEMMs' last-contributor
