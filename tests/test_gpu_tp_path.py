@@ -126,15 +126,17 @@ print("ERRS", errs)
 '''
 
 
-@pytest.mark.parametrize("knob", ["DL_FIXUP", "DL_ROPE_FUSE", "DL_FIXUP_ROPE"])
+@pytest.mark.parametrize("knob", ["DL_FIXUP", "DL_ROPE_FUSE", "DL_FIXUP_ROPE", "DL_ATTN_SPLIT", "DL_ZRED=0",
+                                  "DL_GU_F32", "DL_SILU_EW4", "DL_NO_FUSE_RESNORM", "DL_ATTN_CFG=23"])
 def test_block_decode_stream_k_fixups(knob):
-    """Opt-in decode variants must match the oracle: DL_FIXUP=1 (RoPE+cache,
-    residual and SiLU*up finalized inside the stage-2 GEMMs' last-contributor
-    fixups) and DL_ROPE_FUSE=1 (RoPE + cache append inside the stream-K
-    attention, q|k|v partials as bf16x2)."""
+    """Every A/B switch's decode variant must match the oracle too:
+    stream-K fixups, RoPE inside the attention, the split-KV attention fallback,
+    fp32 latent / gate|up reductions, the old SiLU and un-fused residual/norm
+    kernels, the 3-CTA attention configuration."""
     from paper_2604_17709_b200 import build
     build.build()
-    env = dict(os.environ, **{knob: "1"})
+    name, _, val = knob.partition("=")
+    env = dict(os.environ, **{name: val or "1"})
     src = FIXUP_SCRIPT.replace("__ROOT__", repr(ROOT))
     r = subprocess.run([sys.executable, "-c", src], capture_output=True, text=True, env=env, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
