@@ -372,6 +372,9 @@ def main():
                 "kernel": "tc_gemm (tcgen05 low-rank stage-1/stage-2 GEMMs, all launches of one step)",
                 "launches_per_step": len(recs), "kernel_ms_per_step": ms,
                 "peak_source": f"{peak_src} ({'hbm_gbs' if bound == 'hbm' else 'bf16_tflops_sustained'})",
+                # secondary denominator: the B200 data-sheet peak (8 TB/s HBM3e,
+                # 2.25 PFLOP/s dense bf16)
+                "frac_of_spec": ach / (8000.0 if bound == "hbm" else 2250.0),
                 "largest_launch": largest_launch(recs, bound, peak)}
 
     def largest_launch(recs, bound, peak):
