@@ -63,6 +63,22 @@ def load_peaks():
         return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
 
 
+def collective_census(shape, ranks, n_layers, world, args):
+    """Collectives one rank issues per decode step and their bf16 payload:
+    rank-parallel RS(q|k|v) + AG(attention) + AR(o) + AR(gate|up) + AR(down) per layer;
+    DeInfer AG(latent q|k|v) + AR(latent o) + AG(latent gate|up) + AR(latent down); plus the
+    logits all-gather."""
+    if world == 1:
+        return {"count_per_step": 0, "payload_mb_per_step": 0.0}
+    if args.layout == "rp":
+        per_tok = (shape.h + 2 * shape.h_kv) + shape.h + shape.h + 2 * shape.m + shape.h
+    else:
+        per_tok = (ranks["q"] + ranks["k"] + ranks["v"]) + ranks["o"] + (ranks["gate"] + ranks["up"]) + ranks["down"]
+    payload = (per_tok * n_layers + shape.vocab) * args.batch * 2
+    return {"count_per_step": 4 * n_layers + (n_layers if args.layout == "rp" else 0) + 1,
+            "payload_mb_per_step": payload / 1e6, "layout": args.layout}
+
+
 def load_traffic():
     """ncu DRAM bytes of the dominant launch (profiles/traffic.json, from one --set full capture)."""
     try:
@@ -489,7 +505,8 @@ def main():
                         "d2h_bytes_per_step": out_h.numel() * out_h.element_size()},
                 "gpu_launches": dlaunch * args.steps, "clocks": dclk, "prefill": prefill,
                 "graph_study": graph_study,
-                "step_algorithmic_gb_per_gpu": step_bytes / 1e9, "init_s": init_s}
+                "step_algorithmic_gb_per_gpu": step_bytes / 1e9, "init_s": init_s,
+                "collectives": collective_census(shape, ranks, n_layers, world, args)}
         if args.layers:
             line["invalid"] = f"debug run with {n_layers} layers"
         print(json.dumps(line), flush=True)
