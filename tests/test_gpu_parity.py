@@ -183,6 +183,53 @@ def test_block_prefill_small(dl, orc, lens):
         assert rel(vg, rv_[a:b]) <= TOL_BF16
 
 
+@pytest.mark.parametrize("first,second", [([70], [60]), ([1, 128, 33], [64, 5, 200]), ([129, 0], [1, 77])])
+def test_block_prefill_continues_cached_prefix(dl, orc, first, second):
+    """Chunked prefill (include/dl.h: PREFILL token i of sequence s sits at position
+    cache_lens[s] + i and attends to the cached prefix too): prefill chunk 1, then
+    chunk 2 with cache_lens = len(chunk 1).  Chunk 2's rows must equal the
+    oracle's one-shot causal prefill of the concatenated sequences (PAPER.md
+    eq. 1-3 attention is causal over all earlier keys), and the cache must hold
+    the keys of both chunks."""
+    s = SMALL
+    rk = block_ranks(s, 0.4)
+    w = gen_block_weights(s, rk, 0, 21)
+    S = len(first)
+    full = [a + b for a, b in zip(first, second)]
+    x_full = gen_normal((sum(full), s.h), 1.0, 22, dtype=torch.bfloat16)
+    cu_full = np.concatenate([[0], np.cumsum(full)]).astype(np.int32)
+    pos_full = np.concatenate([np.arange(L) for L in full]).astype(np.int32)
+    ref, rk_, _ = orc.block_prefill(_oracle_cfg(orc, s, rk), w, x_full, pos_full, cu_full)
+
+    max_seq = max(full) + 8
+    cfg = dl.make_block_config(s, rk, max_tokens=sum(full), max_seqs=S)
+    wdev = dl.BlockWeights({k: v.cuda() for k, v in w.items()})
+    ws = torch.zeros(dl.dl_block_workspace(cfg), dtype=torch.uint8, device="cuda")
+    kc = torch.zeros(S, s.n_kv_heads, max_seq, s.head_dim, dtype=torch.bfloat16, device="cuda")
+    vc = torch.zeros_like(kc)
+    outs = []
+    for chunk, before in ((first, [0] * S), (second, first)):
+        rows = np.concatenate([np.arange(cu_full[i] + before[i], cu_full[i] + before[i] + chunk[i])
+                               for i in range(S)]).astype(np.int64)
+        if len(rows) == 0:
+            continue
+        pos = np.concatenate([np.arange(before[i], before[i] + chunk[i]) for i in range(S)]).astype(np.int32)
+        cu = np.concatenate([[0], np.cumsum(chunk)]).astype(np.int32)
+        xd = x_full[rows].clone().cuda()
+        cl = torch.tensor(before, dtype=torch.int32, device="cuda")
+        dl.dl_decomposed_block_forward(cfg, wdev, xd, torch.from_numpy(pos).cuda(), torch.from_numpy(cu).cuda(),
+                                       S, dl.DL_PREFILL, kc, vc, cl, None, ws)
+        torch.cuda.synchronize()
+        outs.append((rows, xd.cpu()))
+    rows2, xo2 = outs[-1]
+    xin2 = x_full[rows2].double()
+    assert rel(xo2.double() - xin2, ref[rows2] - xin2.numpy()) <= TOL_BF16
+    for i in range(S):
+        a, L = cu_full[i], full[i]
+        kg = kc[i, :, :L].permute(1, 0, 2).reshape(L, -1).cpu()
+        assert rel(kg, rk_[a:a + L]) <= TOL_BF16
+
+
 @pytest.mark.parametrize("cache_lens", [[0, 5, 17, 1, 33, 2, 7, 100], [511] * 4])
 def test_block_decode_small(dl, orc, cache_lens):
     s = SMALL
