@@ -119,6 +119,29 @@ def test_linear_reads_rank_major_gather(dl, orc, P, T):
     assert rel(Y.cpu(), orc.lowrank_linear(X, A, B)) <= TOL_BF16
 
 
+@pytest.mark.parametrize("T", [4, 64, 300])
+def test_linear_degenerate_ranks(dl, T):
+    """Degenerate decompositions with closed forms (Eq. 1, y = A(Bx)):
+    B = I (k = n) reduces to the dense product X Aᵀ, and k = 1 to the outer
+    product (X b) aᵀ -- checked against float64 torch, not the oracle."""
+    n, m = 256, 384
+    X = gen_normal((T, n), 1.0, 60 + T, dtype=torch.bfloat16)
+    A = gen_normal((m, n), n ** -0.5, 61, dtype=torch.bfloat16)
+    Y = torch.empty(T, m, dtype=torch.bfloat16, device="cuda")
+    dl.dl_lowrank_linear(X.cuda(), A.cuda(), torch.eye(n, dtype=torch.bfloat16, device="cuda"), Y)
+    torch.cuda.synchronize()
+    assert rel(Y.cpu(), X.double() @ A.double().T) <= TOL_BF16
+    a = gen_normal((m, 1), 1.0, 62, dtype=torch.bfloat16)
+    b = gen_normal((1, n), n ** -0.5, 63, dtype=torch.bfloat16)
+    Y1 = torch.empty(T, m, dtype=torch.bfloat16, device="cuda")
+    a8 = torch.zeros(m, 8, dtype=torch.bfloat16, device="cuda")   # ld must be a 16-byte multiple
+    a8[:, :1] = a.cuda()
+    dl.dl_lowrank_linear(X.cuda(), a8[:, :1], b.cuda(), Y1)
+    torch.cuda.synchronize()
+    z = (X.double() @ b.double().T).to(torch.bfloat16).double()   # the kernel's Z is bf16 (DESIGN §2)
+    assert rel(Y1.cpu(), z @ a.double().T) <= TOL_BF16
+
+
 def test_dense_lm_head_shape(dl):
     """dl_dense (used for the LM head) vs a float64 torch matmul of the same bf16 values."""
     T, N, K = 64, 1000, 512
