@@ -1029,7 +1029,8 @@ dl_status kvlr_attention(const dl_block_config* cfg, const BlockDims& d, const d
   //    position embedding ... to the reconstruction results"), applied in
   //    the reconstruction GEMM's epilogue; the separate in-place kernel is kept
   //    for key widths the vectorised epilogue does not cover
-  const bool epi_rope = !cfg->no_rope && hkl % 128 == 0;
+  static const bool sep_rope = getenv("DL_RECON_ROPE_SEP") && atoi(getenv("DL_RECON_ROPE_SEP")) != 0;   // A/B: RoPE as its own pass
+  const bool epi_rope = !cfg->no_rope && hkl % 128 == 0 && !sep_rope;
   if (epi_rope) {
     pr.out.rope_pos = kv->squeeze_pos;
     pr.out.rope_end = hkl;

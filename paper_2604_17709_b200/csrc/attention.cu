@@ -528,12 +528,12 @@ struct SkArgs {
 };
 
 // RoPE of the interleaved pair (dim, dim + 1) at position pos (fp32 angle
-// pos * theta^(-dim/128), full-range sincosf -- the rope_cache_kernel expression)
+// pos * theta^(-dim/128), rope_sincos -- the rope_cache_kernel expression)
 __device__ __forceinline__ uint32_t rope_pair(uint32_t v, float pos, int dim, float l2t) {
   __nv_bfloat162 b = *reinterpret_cast<__nv_bfloat162*>(&v);
   const float2 f = __bfloat1622float2(b);
   float sn, cs;
-  sincosf(pos * exp2f(-l2t * static_cast<float>(dim) / D), &sn, &cs);
+  rope_sincos(pos * exp2f(-l2t * static_cast<float>(dim) / D), &sn, &cs);
   return pack_bf16(f.x * cs - f.y * sn, f.x * sn + f.y * cs);
 }
 
@@ -730,8 +730,8 @@ __global__ void __launch_bounds__(sk::kThreads, PERSM)
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           float sn0, cs0, sn1, cs1;
-          sincosf(pos * exp2f(-a.l2t * static_cast<float>(kk * 16 + 2 * t4) / D), &sn0, &cs0);
-          sincosf(pos * exp2f(-a.l2t * static_cast<float>(kk * 16 + 8 + 2 * t4) / D), &sn1, &cs1);
+          rope_sincos(pos * exp2f(-a.l2t * static_cast<float>(kk * 16 + 2 * t4) / D), &sn0, &cs0);
+          rope_sincos(pos * exp2f(-a.l2t * static_cast<float>(kk * 16 + 8 + 2 * t4) / D), &sn1, &cs1);
           auto rot = [](uint32_t v, float sn, float cs) {
             const float2 f = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&v));
             return pack_bf16(f.x * cs - f.y * sn, f.x * sn + f.y * cs);

@@ -376,8 +376,8 @@ __device__ __forceinline__ void el_rope_cache(const RopeCacheArgs& a, const FEle
         if (a.rope && hd < a.Hq + a.Hk) {
           const float pos = static_cast<float>(it.pos);
           float sn0, cs0, sn1, cs1;
-          sincosf(pos * exp2f(-l2t * static_cast<float>(c) / a.d), &sn0, &cs0);
-          sincosf(pos * exp2f(-l2t * static_cast<float>(c + 2) / a.d), &sn1, &cs1);
+          rope_sincos(pos * exp2f(-l2t * static_cast<float>(c) / a.d), &sn0, &cs0);
+          rope_sincos(pos * exp2f(-l2t * static_cast<float>(c + 2) / a.d), &sn1, &cs1);
           v = make_float4(v.x * cs0 - v.y * sn0, v.x * sn0 + v.y * cs0, v.z * cs1 - v.w * sn1,
                           v.z * sn1 + v.w * cs1);
         }

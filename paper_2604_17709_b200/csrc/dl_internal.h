@@ -29,6 +29,21 @@ void prof_end(int idx, cudaStream_t st, double bytes, double flops, int kind);
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// sin / cos of a RoPE angle (pos * theta^(-2i/d), up to ~1e5 rad).  Library
+// sincosf takes a Payne-Hanek slow path with a local-memory stack for
+// |x| > 105615 and a long fast path otherwise (ncu on the low-rank KV
+// reconstruction epilogue: local loads/stores, 30 % tensor utilisation).  Here:
+// Cody-Waite reduction by 2*pi in two fp32 parts (2*pi rounded to fp32 exceeds
+// 2*pi by 1.7484556e-7), then the SFU __sincosf on [-pi, pi] (abs error
+// ~2^-21).  The reduction adds |n| * 2^-24-ish rad, below the fp32 rounding of
+// the angle itself (|x| * 2^-24), far below bf16 resolution.
+__device__ __forceinline__ void rope_sincos(float x, float* s, float* c) {
+  const float n = rintf(x * 0.159154943091895336f);
+  float r = fmaf(n, -6.28318548202514648f, x);
+  r = fmaf(n, 1.7484556e-7f, r);
+  __sincosf(r, s, c);
+}
+
 template <typename... KArgs, typename... Args>
 dl_status launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                      const char* what, Args... args) {

@@ -487,12 +487,12 @@ __global__ void __launch_bounds__(128) rope_cache_kernel(RopeCacheArgs a, EwTrac
   }
   if (active && a.rope && h0 < a.Hq + a.Hk) {
     // angle = pos * theta^(-2p/d) in fp32 (relative error ~1e-7, i.e. <= 3e-4 rad at
-    // position 2048, far below bf16 resolution); full-range-reduction sincosf
+    // position 2048, far below bf16 resolution); rope_sincos (dl_internal.h)
     const float pos = static_cast<float>(a.positions[t]);
     const float l2t = log2f(a.theta);
 #pragma unroll
     for (int q = 0; q < kRopeVec; ++q)
-      sincosf(pos * exp2f(-l2t * static_cast<float>(2 * (p0 + q)) / a.d), &sn[q], &cs[q]);
+      rope_sincos(pos * exp2f(-l2t * static_cast<float>(2 * (p0 + q)) / a.d), &sn[q], &cs[q]);
   }
   int64_t slot = 0;   // cache row of this token for kv head 0: (s * Hk) * max_seq + cpos
   if (active && h0 + kRopeHeads > a.Hq) {
@@ -573,11 +573,11 @@ __global__ void __launch_bounds__(128) rope_cache_tok_kernel(RopeCacheArgs a, Ew
   const bool rot = active && a.rope && hd < a.Hq + a.Hk;
   if (rot) {
     // angle = pos * theta^(-2i/d) in fp32 (relative error ~1e-7, i.e. <= 3e-4 rad at
-    // position 2048, far below bf16 resolution); full-range-reduction sincosf
+    // position 2048, far below bf16 resolution); rope_sincos (dl_internal.h)
     const float pos = static_cast<float>(a.positions[t]);
     const float l2t = log2f(a.theta);
-    sincosf(pos * exp2f(-l2t * static_cast<float>(e) / a.d), &sn0, &cs0);
-    sincosf(pos * exp2f(-l2t * static_cast<float>(e + 2) / a.d), &sn1, &cs1);
+    rope_sincos(pos * exp2f(-l2t * static_cast<float>(e) / a.d), &sn0, &cs0);
+    rope_sincos(pos * exp2f(-l2t * static_cast<float>(e + 2) / a.d), &sn1, &cs1);
   }
   __nv_bfloat16* dst = nullptr;
   if (active && hd >= a.Hq) {
@@ -784,8 +784,8 @@ __global__ void __launch_bounds__(128) rope_rows_kernel(__nv_bfloat16* __restric
     const float4 v = load4(p);
     const float fp = static_cast<float>(pos[r]);
     float sn0, cs0, sn1, cs1;
-    sincosf(fp * f0, &sn0, &cs0);
-    sincosf(fp * f1, &sn1, &cs1);
+    rope_sincos(fp * f0, &sn0, &cs0);
+    rope_sincos(fp * f1, &sn1, &cs1);
     store4(p, v.x * cs0 - v.y * sn0, v.x * sn0 + v.y * cs0, v.z * cs1 - v.w * sn1, v.z * sn1 + v.w * cs1);
   }
 }

@@ -117,7 +117,7 @@ __device__ __forceinline__ void rope8(const KArgs& a, int tok, int f, float* v) 
   for (int e = 0; e < 4; ++e) {
     const int dim = (f + 2 * e) & 127;
     float sn, cs;
-    sincosf(pos * exp2f(-a.rope_l2t * static_cast<float>(dim) / 128.f), &sn, &cs);
+    rope_sincos(pos * exp2f(-a.rope_l2t * static_cast<float>(dim) / 128.f), &sn, &cs);
     const float x = v[2 * e], y = v[2 * e + 1];
     v[2 * e] = x * cs - y * sn;
     v[2 * e + 1] = x * sn + y * cs;
@@ -291,8 +291,8 @@ __device__ __noinline__ void fixup_tile(const KArgs& a, const struct Job& j, int
         if (r.rope && j.seg < 2) {   // rotate pairs (e, e+1), (e+2, e+3) by pos * theta^(-e/d)
           const float pos = static_cast<float>(r.positions[t]);
           float s0, c0, s1, c1;
-          sincosf(pos * exp2f(-l2t * static_cast<float>(e) / r.d), &s0, &c0);
-          sincosf(pos * exp2f(-l2t * static_cast<float>(e + 2) / r.d), &s1, &c1);
+          rope_sincos(pos * exp2f(-l2t * static_cast<float>(e) / r.d), &s0, &c0);
+          rope_sincos(pos * exp2f(-l2t * static_cast<float>(e + 2) / r.d), &s1, &c1);
           o = make_float4(v[k].x * c0 - v[k].y * s0, v[k].x * s0 + v[k].y * c0, v[k].z * c1 - v[k].w * s1,
                           v[k].z * s1 + v[k].w * c1);
         }
