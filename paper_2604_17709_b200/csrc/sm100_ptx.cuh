@@ -182,6 +182,18 @@ __device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// Relaxed arrivals: for barriers that only say "my tcgen05.ld of this TMEM
+// accumulator has completed" (tcgen05.wait::ld + fence::before_thread_sync
+// precede them).  The .release forms make the thread first drain its
+// outstanding global stores / reductions (MEMBAR.ALL.GPU for .cluster: the
+// top stall of the pair kernel's epilogue under ncu); nothing the arrive
+// guards lives in global memory.
+__device__ __forceinline__ void mbar_arrive_relaxed(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
 // Pair TMA: both CTAs load their half into their own smem; completion bytes
 // are counted on the leader (rank 0) CTA's barrier at the same offset.
 __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t c0,

@@ -81,6 +81,7 @@ struct KArgs {
   long long static_units, dyn_begin;
   int chunk;
   int l2pf;                  // weight tiles prefetched into L2 before griddepcontrol.wait
+  int relaxed_acce;          // accumulator-empty arrivals without release semantics (DL_ACCE_RELEASE=1: off)
   int act_w;                 // > 0: 3-D activation map, column c -> (c % act_w, token, c / act_w)
   int wpol;                  // pair kernel weight L2 policy: 0 evict_first, 1 evict_normal, 2 evict_last
   // DP + stream-K tail (whole-tile kernels): tiles [0, dp_tiles) whole, each of
@@ -775,7 +776,8 @@ __global__ void __launch_bounds__(kThreads, (SWAP && STAGES <= 4) ? 2 : 1)
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        ptx::mbar_arrive(&acce_bar[acc]);
+        if (a.relaxed_acce) ptx::mbar_arrive_relaxed(&acce_bar[acc]);
+        else ptx::mbar_arrive(&acce_bar[acc]);
         ptx::mbar_arrive(&jempty_bar[my_slot]);
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
@@ -1002,7 +1004,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_cluster(acce0 + acc * 8);   // leader's acce_bar[acc]
+      if (lane == 0) {   // leader's acce_bar[acc]
+        if (a.relaxed_acce) ptx::mbar_arrive_cluster_relaxed(acce0 + acc * 8);
+        else ptx::mbar_arrive_cluster(acce0 + acc * 8);
+      }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
@@ -1200,6 +1205,8 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   a.fixup = FIX_NONE;
   static const int l2pf = getenv("DL_L2PF") ? atoi(getenv("DL_L2PF")) : kL2Prefetch;
   a.l2pf = l2pf;
+  static const int acce_release = getenv("DL_ACCE_RELEASE") ? atoi(getenv("DL_ACCE_RELEASE")) : 0;   // A/B switch
+  a.relaxed_acce = acce_release ? 0 : 1;
   if (p.fix.op != FIX_NONE) {
     bool ok = SWAP && stream_k && p.sched && p.fix.acc32 && p.fix.tile_cnt;
     for (int g = 0; g < p.nseg; ++g) ok = ok && (p.seg[g].rows == 0 || p.seg[g].klen > 0);
