@@ -111,9 +111,12 @@ struct KArgs {
 // RoPE of 8 consecutive output features f..f+7 (4 pairs (2i, 2i+1) of a
 // 128-wide head) of token `tok`: angle = pos * theta^(-dim/128), the same
 // expression as rope_cache_kernel.
-__device__ __forceinline__ void rope8(const KArgs& a, int tok, int f, float* v) {
+// `pos` = rope_pos[tok] as float, loaded once per tile row (rope_pos_of).
+__device__ __forceinline__ float rope_pos_of(const KArgs& a, int tok) {
+  return (a.rope_pos != nullptr && tok < a.T) ? static_cast<float>(a.rope_pos[tok]) : 0.f;
+}
+__device__ __forceinline__ void rope8(const KArgs& a, float pos, int f, float* v) {
   if (a.rope_pos == nullptr || f >= a.rope_end) return;
-  const float pos = static_cast<float>(a.rope_pos[tok]);
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     const int dim = (f + 2 * e) & 127;
@@ -724,7 +727,7 @@ __global__ void __launch_bounds__(kThreads, (SWAP && STAGES <= 4) ? 2 : 1)
                   float v[8];
 #pragma unroll
                   for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r[q * 8 + e]);
-                  rope8(a, tok, f0 + q * 8, v);
+                  rope8(a, rope_pos_of(a, tok), f0 + q * 8, v);
                   if (a.accumulate) {
                     uint4 old = *reinterpret_cast<const uint4*>(o + q * 8);
                     const __nv_bfloat162* ob = reinterpret_cast<const __nv_bfloat162*>(&old);
@@ -941,10 +944,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     while (it.next(j, TILE, TILE)) {
       const KSeg& s = a.seg[j.seg];
+      const int tok = j.tok0 + static_cast<int>(rank) * HALF + row;
+      const float rpos = rope_pos_of(a, tok);   // issued before the accumulator wait
       ptx::mbar_wait(&accf_bar[acc], acc_phase);
       ptx::tc_fence_after();
       const bool has_k = j.kb1 > j.kb0;
-      const int tok = j.tok0 + static_cast<int>(rank) * HALF + row;
 #pragma unroll 1
       for (int c0 = half * 128; c0 < (half + 1) * 128; c0 += 32) {
         uint32_t r[32];
@@ -973,7 +977,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               float v[8];
 #pragma unroll
               for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r[q * 8 + e]);
-              rope8(a, tok, f0 + q * 8, v);
+              rope8(a, rpos, f0 + q * 8, v);
               if (a.accumulate) {
                 uint4 old = *reinterpret_cast<const uint4*>(o + q * 8);
                 const __nv_bfloat162* ob = reinterpret_cast<const __nv_bfloat162*>(&old);
