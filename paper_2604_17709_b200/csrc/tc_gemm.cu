@@ -44,6 +44,7 @@ constexpr int BK = 64;   // K elements per stage = one 128-byte swizzle row
 constexpr int BM = 128;  // MMA M = TMEM lanes
 constexpr int kThreads = 320;   // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
 constexpr int kJobRing = 8;     // producer -> MMA / epilogue job queue depth
+constexpr int kStageOutWarp = 32 * 64;   // pair epilogue: per-warp staging of 32 rows x 32 bf16 features
 constexpr int kL2Prefetch = 0;  // weight tiles pulled into L2 before griddepcontrol.wait (DL_L2PF); measured: 24 costs ~1 ms per 70B decode step
 
 struct KSeg {
@@ -81,7 +82,8 @@ struct KArgs {
   long long static_units, dyn_begin;
   int chunk;
   int l2pf;                  // weight tiles prefetched into L2 before griddepcontrol.wait
-  int relaxed_acce;          // accumulator-empty arrivals without release semantics (DL_ACCE_RELEASE=1: off)
+  int relaxed_acce;
+  int stage_out;             // pair kernel: bf16 stores through the shared-memory transpose (DL_STAGE_OUT=0: off)          // accumulator-empty arrivals without release semantics (DL_ACCE_RELEASE=1: off)
   int act_w;                 // > 0: 3-D activation map, column c -> (c % act_w, token, c / act_w)
   int wpol;                  // pair kernel weight L2 policy: 0 evict_first, 1 evict_normal, 2 evict_last
   // DP + stream-K tail (whole-tile kernels): tiles [0, dp_tiles) whole, each of
@@ -940,6 +942,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int half = (warp - 2) >> 2;
     const int row = quarter * 32 + lane;          // this CTA's token row within its half
     const uint32_t acce0 = ptx::mapa(ptx::smem_u32(&acce_bar[0]), 0);
+    uint8_t* stg = smem + STAGES * STAGE_BYTES + (warp - 2) * kStageOutWarp;   // this warp's store staging
     int acc = 0;
     uint32_t acc_phase = 0;
     while (it.next(j, TILE, TILE)) {
@@ -969,6 +972,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               ptx::red_add_v4_f32(pt + q, __uint_as_float(r[q]), __uint_as_float(r[q + 1]), __uint_as_float(r[q + 2]),
                                   __uint_as_float(r[q + 3]));
           }
+        } else if (a.stage_out && !a.accumulate && f0 + 32 <= s.write_end &&
+                   __all_sync(0xffffffffu, tok >= a.T || ((reinterpret_cast<uintptr_t>(static_cast<__nv_bfloat16*>(a.out) +
+                                                                                     out_index(a, s, tok, f0)) & 15) == 0))) {
+          // Coalesced store through a per-warp 2 KB shared-memory transpose: the
+          // accumulator gives each lane one token row (32 features = 64 B), so a
+          // direct store writes 32 half-sectors per instruction.  Staged, each
+          // instruction writes 8 rows x 64 B (whole sectors).  16-byte units are
+          // XOR-swizzled by row so both the writes and the reads are conflict-free.
+          uint4* sw = reinterpret_cast<uint4*>(stg);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r[q * 8 + e]);
+            rope8(a, rpos, f0 + q * 8, v);
+            uint4 pk;
+            __nv_bfloat162* pb = reinterpret_cast<__nv_bfloat162*>(&pk);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) pb[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+            sw[lane * 4 + (q ^ ((lane >> 1) & 3))] = pk;
+          }
+          __syncwarp();
+          const int c = lane & 3;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int rr = 8 * q + (lane >> 2);
+            const uint4 val = sw[rr * 4 + (c ^ ((rr >> 1) & 3))];
+            const int t2 = j.tok0 + static_cast<int>(rank) * HALF + quarter * 32 + rr;
+            if (t2 < a.T)
+              *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.out) + out_index(a, s, t2, f0) + c * 8) = val;
+          }
+          __syncwarp();   // the next column block reuses the staging buffer
         } else if (tok < a.T && f0 < s.write_end) {
           __nv_bfloat16* o = static_cast<__nv_bfloat16*>(a.out) + out_index(a, s, tok, f0);
           if (f0 + 32 <= s.write_end && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
@@ -1108,7 +1143,7 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   constexpr int TOK_TILE = PAIR ? 256 : (SWAP ? BN : BM);
   constexpr int BOX_W = PAIR ? 128 : FEAT_TILE;
   constexpr int BOX_A = PAIR ? 128 : TOK_TILE;
-  constexpr int SMEM = PAIR ? STAGES * 2 * 128 * BK * 2 + 1024 : STAGES * (BM + BN) * BK * 2 + 1024;
+  constexpr int SMEM = PAIR ? STAGES * 2 * 128 * BK * 2 + 8 * kStageOutWarp + 1024 : STAGES * (BM + BN) * BK * 2 + 1024;
   static bool attr_set = false;
   void (*kern)(KMaps, KArgs) = PAIR ? tc_gemm_pair_kernel<STAGES> : tc_gemm_kernel<BN, SWAP, STAGES>;
   if (!attr_set) {
@@ -1211,6 +1246,8 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   a.l2pf = l2pf;
   static const int acce_release = getenv("DL_ACCE_RELEASE") ? atoi(getenv("DL_ACCE_RELEASE")) : 0;   // A/B switch
   a.relaxed_acce = acce_release ? 0 : 1;
+  static const int stage_out = getenv("DL_STAGE_OUT") ? atoi(getenv("DL_STAGE_OUT")) : 1;   // A/B switch
+  a.stage_out = stage_out;
   if (p.fix.op != FIX_NONE) {
     bool ok = SWAP && stream_k && p.sched && p.fix.acc32 && p.fix.tile_cnt;
     for (int g = 0; g < p.nseg; ++g) ok = ok && (p.seg[g].rows == 0 || p.seg[g].klen > 0);
