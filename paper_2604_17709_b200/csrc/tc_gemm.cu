@@ -83,7 +83,7 @@ struct KArgs {
   int chunk;
   int l2pf;                  // weight tiles prefetched into L2 before griddepcontrol.wait
   int relaxed_acce;
-  int stage_out;             // pair kernel: bf16 stores through the shared-memory transpose (DL_STAGE_OUT=0: off)          // accumulator-empty arrivals without release semantics (DL_ACCE_RELEASE=1: off)
+  int stage_out;             // pair kernel: bf16 stores through the shared-memory transpose (bit 0 plain, bit 1 Y +=; DL_STAGE_OUT)          // accumulator-empty arrivals without release semantics (DL_ACCE_RELEASE=1: off)
   int act_w;                 // > 0: 3-D activation map, column c -> (c % act_w, token, c / act_w)
   int wpol;                  // pair kernel weight L2 policy: 0 evict_first, 1 evict_normal, 2 evict_last
   // DP + stream-K tail (whole-tile kernels): tiles [0, dp_tiles) whole, each of
@@ -972,7 +972,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               ptx::red_add_v4_f32(pt + q, __uint_as_float(r[q]), __uint_as_float(r[q + 1]), __uint_as_float(r[q + 2]),
                                   __uint_as_float(r[q + 3]));
           }
-        } else if (a.stage_out && !a.accumulate && f0 + 32 <= s.write_end &&
+        } else if ((a.stage_out & 1) && !a.accumulate && f0 + 32 <= s.write_end &&
                    __all_sync(0xffffffffu, tok >= a.T || ((reinterpret_cast<uintptr_t>(static_cast<__nv_bfloat16*>(a.out) +
                                                                                      out_index(a, s, tok, f0)) & 15) == 0))) {
           // Coalesced store through a per-warp 2 KB shared-memory transpose: the
@@ -1004,6 +1004,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.out) + out_index(a, s, t2, f0) + c * 8) = val;
           }
           __syncwarp();   // the next column block reuses the staging buffer
+        } else if ((a.stage_out & 2) && a.accumulate && f0 + 32 <= s.write_end &&
+                   __all_sync(0xffffffffu, tok >= a.T || ((reinterpret_cast<uintptr_t>(static_cast<__nv_bfloat16*>(a.out) +
+                                                                                     out_index(a, s, tok, f0)) & 15) == 0))) {
+          // Same transpose for Y += result (the residual-fused stage 2): fp32
+          // staging in two 16-column halves, so the old value is added before
+          // the one bf16 rounding, exactly as on the direct path.
+          float vv[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) vv[i] = __uint_as_float(r[i]);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) rope8(a, rpos, f0 + q * 8, vv + q * 8);
+          float4* sw = reinterpret_cast<float4*>(stg);
+          const int c = lane & 3;
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              sw[lane * 4 + (q ^ ((lane >> 1) & 3))] =
+                  make_float4(vv[h2 * 16 + q * 4], vv[h2 * 16 + q * 4 + 1], vv[h2 * 16 + q * 4 + 2], vv[h2 * 16 + q * 4 + 3]);
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int rr = 8 * q + (lane >> 2);
+              const float4 val = sw[rr * 4 + (c ^ ((rr >> 1) & 3))];
+              const int t2 = j.tok0 + static_cast<int>(rank) * HALF + quarter * 32 + rr;
+              if (t2 < a.T) {
+                uint2* o2 = reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.out) + out_index(a, s, t2, f0) +
+                                                     h2 * 16 + c * 4);
+                const uint2 old = *o2;
+                const float2 a0 = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(&old)[0]);
+                const float2 a1 = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(&old)[1]);
+                uint2 pk;
+                reinterpret_cast<__nv_bfloat162*>(&pk)[0] = __floats2bfloat162_rn(val.x + a0.x, val.y + a0.y);
+                reinterpret_cast<__nv_bfloat162*>(&pk)[1] = __floats2bfloat162_rn(val.z + a1.x, val.w + a1.y);
+                *o2 = pk;
+              }
+            }
+            __syncwarp();
+          }
         } else if (tok < a.T && f0 < s.write_end) {
           __nv_bfloat16* o = static_cast<__nv_bfloat16*>(a.out) + out_index(a, s, tok, f0);
           if (f0 + 32 <= s.write_end && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
@@ -1246,7 +1285,7 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   a.l2pf = l2pf;
   static const int acce_release = getenv("DL_ACCE_RELEASE") ? atoi(getenv("DL_ACCE_RELEASE")) : 0;   // A/B switch
   a.relaxed_acce = acce_release ? 0 : 1;
-  static const int stage_out = getenv("DL_STAGE_OUT") ? atoi(getenv("DL_STAGE_OUT")) : 1;   // A/B switch
+  static const int stage_out = getenv("DL_STAGE_OUT") ? atoi(getenv("DL_STAGE_OUT")) : 3;   // A/B: bit 0 plain, bit 1 accumulate
   a.stage_out = stage_out;
   if (p.fix.op != FIX_NONE) {
     bool ok = SWAP && stream_k && p.sched && p.fix.acc32 && p.fix.tile_cnt;
