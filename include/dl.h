@@ -75,18 +75,52 @@ int dl_version(void);
 /* 1 if a device with compute capability 10.x is current, else 0. */
 int dl_device_ok(void);
 
+/* Reduction applied to the rank partials of dl_lowrank_linear (PAPER.md:123,
+ * Fig. 2(b): the partial results of the rank shards are reduce-summed).      */
+typedef enum {
+  DL_REDUCE_NONE = 0,      /* no collective: Y (+)= this rank's partial A_r(B_r x) */
+  DL_REDUCE_ALLREDUCE = 1, /* Y (+)= sum over ranks, [T x m] on every rank         */
+  DL_REDUCE_SCATTER = 2    /* Y (+)= rank r's slab of the sum: features
+                              [r m/P, (r+1) m/P), Y is [T x m/P]                 */
+} dl_reduce;
+
 /* ------------------------------------------------------------------------
- * Communicator.  nccl_comm: an initialised ncclComm_t (host handle) of
- * `world` ranks in which this process is `rank`.  NCCL symbols are resolved
- * from the process (the NCCL that owns nccl_comm); DL_ERR_NCCL if absent.
+ * Communicators.  Every collective has NCCL semantics and is issued on the
+ * stream of the call that needs it; all ranks must issue the same sequence.
+ *
+ * dl_comm_create: nccl_comm is an initialised ncclComm_t (host handle) of
+ *   `world` ranks in which this process is `rank` (one process per GPU over
+ *   NVLink / NVSwitch).  NCCL symbols are resolved from the process (the NCCL
+ *   that owns nccl_comm); DL_ERR_NCCL if absent.  The comm is not owned.
+ * dl_comm_create_group: `world` (1..8) ranks inside THIS process on the
+ *   current device; comms[r] (host array of `world`, filled) is rank r's
+ *   communicator.  Each rank must be driven by its own host thread (the
+ *   collectives meet on a host barrier), and all ranks must pass the SAME
+ *   stream: the library's persistent kernels (one CTA per SM, tensor-memory
+ *   allocation, programmatic early launch) are written for one kernel
+ *   sequence per device, and two ranks' sequences running concurrently can
+ *   starve each other; a collective whose ranks posted different streams
+ *   returns DL_ERR_INVALID_ARG on every rank.  The collectives are this
+ *   library's peer-memory kernels: rank r reads every rank's posted buffer
+ *   directly and sums in rank order with fp32 accumulation, so every rank gets
+ *   bit-identical results; the host barrier orders the ranks' enqueues (and
+ *   CUDA events their streams).  sym_bytes (>= 256): per-rank symmetric scratch owned by the
+ *   group (allocated once here; all-reduces larger than it run in rounds).
+ *   Not capturable in a CUDA graph (DL_ERR_UNSUPPORTED during capture).  A
+ *   rank that misses a collective for 120 s aborts the group: every later
+ *   collective returns DL_ERR_NCCL.  Freed when all `world` comms are
+ *   destroyed.  Use: TP = world on one GPU (parity of the sharded path).
+ * dl_comm_create_loopback: measurement only -- `world` ranks' shapes on ONE
+ *   GPU with the collectives replaced by local copies (all-gather: this
+ *   rank's slice into its slot; reduce-scatter: its slot; all-reduce: no-op).
+ *   Results are NOT the sharded result; the per-rank kernel work of a TP =
+ *   world step is exact, so its compute time can be measured without world
+ *   GPUs (tools/tp_emulate.py).
+ * Any NCCL or group communicator, even of world 1, selects the tensor-
+ * parallel code path of the block calls; a loopback of world 1 does not.
  * ---------------------------------------------------------------------- */
 dl_status dl_comm_create(void *nccl_comm, int rank, int world, dl_comm *out);
-/* Measurement only: a communicator of `world` ranks on ONE GPU whose
- * collectives are replaced by local copies of the same shapes (all-gather:
- * this rank's slice into its slot; reduce-scatter: its slot; all-reduce:
- * no-op).  Results are NOT the sharded result; the per-rank kernel work of a
- * TP = world step is exact, so its compute time can be measured without
- * world GPUs (tools/tp_emulate.py).                                        */
+dl_status dl_comm_create_group(int world, size_t sym_bytes, dl_comm *comms);
 dl_status dl_comm_create_loopback(int rank, int world, dl_comm *out);
 dl_status dl_comm_destroy(dl_comm comm);
 
@@ -94,27 +128,36 @@ dl_status dl_comm_destroy(dl_comm comm);
  * dl_lowrank_linear -- one decomposed linear layer
  * (Section 2.1, Eq. 1):  Y[t] (+)= A (B X[t])  for t in [0, T).
  *
- *   X [T x n] (ldx), A [m x k] (lda), B [k x n] (ldb), Y [T x m] (ldy).
- *   comm == NULL : A, B are the full factors.
+ *   X [T x n] (ldx), A [m x k] (lda), B [k x n] (ldb), Y [T x m_out] (ldy),
+ *   m_out = m / world for DL_REDUCE_SCATTER with a communicator, else m.
+ *   comm == NULL : A, B are the full factors (reduce is irrelevant: world 1).
  *   comm != NULL : A, B are this rank's k-shards (k = k_r; the columns of A
- *                  and rows of B given by dl_tp_plan) and the rank partials
- *                  are reduce-summed over the communicator (all-reduce,
- *                  PAPER.md:123) so every rank ends with the full Y.
+ *                  and rows of B given by dl_tp_plan); the rank partials are
+ *                  combined per `reduce`.  SCATTER needs
+ *                  m % (32 * world) == 0 (DL_ERR_PARTITION).
  *   accumulate   : 0 -> Y = result;  1 -> Y = Y + result (residual fusion).
  *   The rank-k intermediate Z = X B^T is fp32-accumulated and rounded to
- *   the input dtype before the second stage; for T <= 16 it never leaves
- *   shared memory / registers of the fused SIMT chain.
- *   workspace: >= dl_lowrank_linear_workspace() bytes, 256 B aligned.
- * Errors: SHAPE, RANK (k < 1, or k > min(m,n) when comm == NULL), ALIGN,
- *   DTYPE (fp32 with T > 16), WORKSPACE, CUDA, NCCL.  T == 0 -> DL_OK no-op.
+ *   the input dtype (bf16 for DL_BF16; fp32 stays fp32) before the second
+ *   stage on every path.  Paths: T <= 16 without a bf16 collective, and all
+ *   fp32 calls, run the SIMT chain (Z in shared memory when k <= 1024 and
+ *   (m + n) k <= 65536, otherwise an L2-resident workspace row); larger T
+ *   (or a bf16 collective) run the tcgen05 tensor-core kernels.
+ *   workspace: >= dl_lowrank_linear_workspace() bytes (same T, m, n, k,
+ *   dtype, comm, reduce), 256 B aligned.
+ * Errors: INVALID_ARG (dtype / reduce enum), SHAPE, RANK (k < 1, or k >
+ *   min(m,n) when comm == NULL), PARTITION, ALIGN, DTYPE (fp32 with T > 16),
+ *   UNSUPPORTED (fp32 accumulate with a collective; m % 4 on the tensor
+ *   path), WORKSPACE, CUDA, NCCL.  All checked before any launch.  T == 0 ->
+ *   DL_OK no-op.
  * ---------------------------------------------------------------------- */
 dl_status dl_lowrank_linear_workspace(int64_t T, int64_t m, int64_t n,
-                                      int64_t k, dl_dtype dtype, size_t *bytes);
+                                      int64_t k, dl_dtype dtype, dl_comm comm,
+                                      dl_reduce reduce, size_t *bytes);
 dl_status dl_lowrank_linear(const void *X, int64_t ldx, const void *A,
                             int64_t lda, const void *B, int64_t ldb, void *Y,
                             int64_t ldy, int64_t T, int64_t m, int64_t n,
                             int64_t k, dl_dtype dtype, int accumulate,
-                            dl_comm comm, void *workspace,
+                            dl_comm comm, dl_reduce reduce, void *workspace,
                             size_t workspace_bytes, void *stream);
 
 /* ------------------------------------------------------------------------
@@ -261,7 +304,10 @@ typedef enum { DL_PREFILL = 0, DL_DECODE = 1 } dl_phase;
  *            PREFILL: the sequence's tokens are written at cache positions
  *            cache_lens[s] + i and attend to the cached prefix too.
  *            DECODE: T == num_seqs, token s is appended at cache_lens[s].
- *            The caller advances cache_lens after the call.
+ *            The caller advances cache_lens after the call.  Precondition:
+ *            cache_lens[s] + (tokens of s) <= max_seq; K/V of a position
+ *            outside [0, max_seq) are dropped (not written), so an overrun
+ *            never corrupts another head's or sequence's rows.
  * max_seq    cache capacity per sequence.
  * workspace  >= dl_block_workspace() bytes, 256 B aligned.  It must be
  *            zero-filled (cudaMemset) before its first use; every call
@@ -411,12 +457,6 @@ dl_status dl_profile_get(int i, float *ms, double *bytes, double *flops,
  * done, first TMA issued, first stage landed, last MMA issued, epilogue
  * done, exit; slot 7 = SM id. */
 dl_status dl_debug_gemm_trace(void *device_buf);
-/* Debug timeline of the fused decode kernels (device_buf: >= 48 u64 per CTA
- * per launch of the next launches, or NULL to disable).  Per launch slot and
- * CTA: [2p] / [2p+1] globaltimer ns at which the CTA's epilogue warps started /
- * finished phase p, [28+p] time the TMA producer issued phase p's activation
- * loads, [46] entry, [47] SM id.  Slots are assigned in launch order. */
-dl_status dl_debug_fused_trace(void *device_buf);
 /* Debug timeline of the non-GEMM decode kernels (SiLU*up, residual +
  * RMSNorm, RoPE + cache append, stream-K attention): device_buf >= 4 u64 per
  * launch of the next launches (kind 1-4, then globaltimer ns of the first CTA

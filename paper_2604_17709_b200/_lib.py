@@ -12,9 +12,12 @@ import threading
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdl.so")
+# DL_LIBRARY=ab loads the instrumented build whose A/B timing switches read the
+# environment (build.py); the default is the release library.
+LIB_PATH = os.path.join(HERE, "libdl_ab.so" if os.environ.get("DL_LIBRARY") == "ab" else "libdl.so")
 
 DL_F32, DL_BF16 = 0, 1
+DL_REDUCE_NONE, DL_REDUCE_ALLREDUCE, DL_REDUCE_SCATTER = 0, 1, 2
 DL_PREFILL, DL_DECODE = 0, 1
 STATUS = {0: "DL_OK", 1: "DL_ERR_INVALID_ARG", 2: "DL_ERR_SHAPE", 3: "DL_ERR_RANK", 4: "DL_ERR_PARTITION",
           5: "DL_ERR_DTYPE", 6: "DL_ERR_ALIGN", 7: "DL_ERR_WORKSPACE", 8: "DL_ERR_CUDA", 9: "DL_ERR_NCCL",
@@ -23,9 +26,10 @@ EXPORTS = ("dl_last_error", "dl_version", "dl_device_ok", "dl_comm_create", "dl_
            "dl_lowrank_linear_workspace", "dl_lowrank_linear", "dl_tp_plan", "dl_tp_shard_factors",
            "dl_block_workspace", "dl_decomposed_block_forward", "dl_embedding", "dl_rmsnorm",
            "dl_dense_workspace", "dl_dense", "dl_launch_count", "dl_profile_begin", "dl_profile_end",
-           "dl_profile_count", "dl_profile_get", "dl_debug_gemm_trace", "dl_debug_fused_trace", "dl_deinfer_shard_factors",
+           "dl_profile_count", "dl_profile_get", "dl_debug_gemm_trace", "dl_deinfer_shard_factors",
            "dl_kv_prepare", "dl_decomposed_block_forward_kvlr", "dl_comm_create_loopback",
-           "dl_decomposed_stack_forward", "dl_debug_ew_trace", "dl_debug_linear_gathered", "dl_argmax")
+           "dl_decomposed_stack_forward", "dl_debug_ew_trace", "dl_debug_linear_gathered", "dl_argmax",
+           "dl_comm_create_group")
 
 
 class DLError(RuntimeError):
@@ -89,9 +93,10 @@ def load():
             lib.dl_device_ok.restype = I
             lib.dl_comm_create.argtypes = [P, I, I, ctypes.POINTER(P)]
             lib.dl_comm_destroy.argtypes = [P]
-            lib.dl_lowrank_linear_workspace.argtypes = [I64, I64, I64, I64, I, ctypes.POINTER(ctypes.c_size_t)]
-            lib.dl_lowrank_linear.argtypes = [P, I64, P, I64, P, I64, P, I64, I64, I64, I64, I64, I, I, P, P,
+            lib.dl_lowrank_linear_workspace.argtypes = [I64, I64, I64, I64, I, P, I, ctypes.POINTER(ctypes.c_size_t)]
+            lib.dl_lowrank_linear.argtypes = [P, I64, P, I64, P, I64, P, I64, I64, I64, I64, I64, I, I, P, I, P,
                                               ctypes.c_size_t, P]
+            lib.dl_comm_create_group.argtypes = [I, ctypes.c_size_t, P]
             lib.dl_tp_plan.argtypes = [P, I, I, I, I, P, P, P]
             lib.dl_tp_shard_factors.argtypes = [I, P, P, P, P, P, P, I64, I, I, I, I, P, I64, P, P, P, P]
             lib.dl_block_workspace.argtypes = [ctypes.POINTER(dl_block_config), I, ctypes.POINTER(ctypes.c_size_t)]
@@ -110,7 +115,6 @@ def load():
             lib.dl_profile_begin.argtypes = [I]
             lib.dl_profile_get.argtypes = [I, P, P, P, P]
             lib.dl_debug_gemm_trace.argtypes = [P]
-            lib.dl_debug_fused_trace.argtypes = [P]
             lib.dl_debug_ew_trace.argtypes = [P]
             lib.dl_debug_linear_gathered.argtypes = [P, I, P, I64, P, I64, P, I64, I64, I64, I64, I64, P,
                                                      ctypes.c_size_t, P]
@@ -193,10 +197,54 @@ class Comm:
         self.is_loopback = True
         return self
 
+    @classmethod
+    def group(cls, world: int, sym_bytes: int = 16 << 20):
+        """`world` in-process ranks on the current GPU (include/dl.h:
+        dl_comm_create_group); returns one Comm per rank.  Drive rank r from
+        its own host thread, all ranks on one shared stream (see run_ranks)."""
+        arr = (P * world)()
+        _check(load().dl_comm_create_group(world, sym_bytes, ctypes.cast(arr, P)))
+        out = []
+        for r in range(world):
+            self = cls.__new__(cls)
+            self.handle, self.rank, self.world = P(arr[r]), r, world
+            self.is_loopback = False
+            out.append(self)
+        return out
+
     def close(self):
         if self.handle:
             load().dl_comm_destroy(self.handle)
             self.handle = None
+
+
+def run_ranks(fn, world: int):
+    """Run fn(rank, stream) for every rank of a group communicator, each in its
+    own host thread; the ranks share ONE CUDA stream (include/dl.h:
+    dl_comm_create_group).  Returns the per-rank results, re-raising the first
+    error."""
+    dev = torch.cuda.current_device()
+    shared = torch.cuda.Stream()
+    out, errs = [None] * world, [None] * world
+
+    def body(r):
+        try:
+            torch.cuda.set_device(dev)
+            with torch.cuda.stream(shared):
+                out[r] = fn(r, shared)
+        except BaseException as e:   # noqa: BLE001 -- re-raised below
+            errs[r] = e
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    shared.synchronize()
+    for e in errs:
+        if e is not None:
+            raise e
+    return out
 
 
 def dl_comm_create(nccl_comm_ptr: int, rank: int, world: int) -> Comm:
@@ -208,26 +256,32 @@ def _comm(c):
 
 
 # ---------------------------------------------------------------------------
-def dl_lowrank_linear_workspace(T: int, m: int, n: int, k: int, dtype=torch.bfloat16) -> int:
+def dl_lowrank_linear_workspace(T: int, m: int, n: int, k: int, dtype=torch.bfloat16, comm: Comm | None = None,
+                                reduce: int = DL_REDUCE_ALLREDUCE) -> int:
     b = ctypes.c_size_t()
     _check(load().dl_lowrank_linear_workspace(T, m, n, k, DL_F32 if dtype == torch.float32 else DL_BF16,
-                                              ctypes.byref(b)))
+                                              _comm(comm), reduce, ctypes.byref(b)))
     return b.value
 
 
 def dl_lowrank_linear(X: torch.Tensor, A: torch.Tensor, B: torch.Tensor, Y: torch.Tensor, accumulate: bool = False,
-                      comm: Comm | None = None, workspace: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-    """Y (+)= A (B x) per token row.  Tensors are device tensors."""
+                      comm: Comm | None = None, reduce: int = DL_REDUCE_ALLREDUCE,
+                      workspace: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Y (+)= A (B x) per token row; with a communicator the
+    rank partials are combined per `reduce` (DL_REDUCE_*; SCATTER: Y is [T x m/P]).
+    Tensors are device tensors."""
     T, n = X.shape
     m, k = A.shape
-    if B.shape[0] != k or B.shape[1] != n or Y.shape[0] != T or Y.shape[1] != m:
+    scat = comm is not None and reduce == DL_REDUCE_SCATTER
+    m_out = m // comm.world if scat else m
+    if B.shape[0] != k or B.shape[1] != n or Y.shape[0] != T or Y.shape[1] != m_out:
         raise ValueError("shape mismatch")
     dt = _dtype(X)
     if workspace is None:
-        workspace = torch.empty(dl_lowrank_linear_workspace(T, m, n, k, X.dtype), dtype=torch.uint8,
+        workspace = torch.empty(dl_lowrank_linear_workspace(T, m, n, k, X.dtype, comm, reduce), dtype=torch.uint8,
                                 device=X.device)
     _check(load().dl_lowrank_linear(_ptr(X), _ld(X), _ptr(A), _ld(A), _ptr(B), _ld(B), _ptr(Y), _ld(Y), T, m, n, k,
-                                    dt, int(accumulate), _comm(comm), _ptr(workspace), workspace.numel(),
+                                    dt, int(accumulate), _comm(comm), reduce, _ptr(workspace), workspace.numel(),
                                     _stream(stream)))
     return Y
 
@@ -535,7 +589,7 @@ def dl_debug_linear_gathered(Xg: torch.Tensor, A: torch.Tensor, B: torch.Tensor,
     P, T, w = Xg.shape
     m, k = A.shape
     n = P * w
-    ws = torch.zeros(dl_lowrank_linear_workspace(T, m, n, k), dtype=torch.uint8, device=Xg.device)
+    ws = torch.zeros(dl_lowrank_linear_workspace(max(T, 17), m, n, k), dtype=torch.uint8, device=Xg.device)
     _check(load().dl_debug_linear_gathered(_ptr(Xg), P, _ptr(A), A.stride(0), _ptr(B), B.stride(0), _ptr(Y),
                                            Y.stride(0), T, m, n, k, _ptr(ws), ws.numel(), _stream(stream)))
     return Y
@@ -544,11 +598,6 @@ def dl_debug_linear_gathered(Xg: torch.Tensor, A: torch.Tensor, B: torch.Tensor,
 def dl_debug_ew_trace(buf: torch.Tensor | None):
     """Timeline of the non-GEMM decode kernels (see include/dl.h); None disables."""
     _check(load().dl_debug_ew_trace(_ptr(buf)))
-
-
-def dl_debug_fused_trace(buf: torch.Tensor | None):
-    """Timeline of the fused decode kernels (see include/dl.h); None disables."""
-    _check(load().dl_debug_fused_trace(_ptr(buf)))
 
 
 def dl_debug_gemm_trace(buf: torch.Tensor | None):

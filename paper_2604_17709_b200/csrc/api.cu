@@ -33,6 +33,20 @@ dl_status cuda_status(cudaError_t e, const char* what) {
   return DL_ERR_CUDA;
 }
 
+dl_status check_device_sm100() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_status(e, "cudaGetDevice");
+  int major = 0;
+  e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (e != cudaSuccess) return cuda_status(e, "cudaDeviceGetAttribute");
+  if (major != 10) {
+    set_error("device compute capability %d.x is not sm_100 (B200)", major);
+    return DL_ERR_CUDA;
+  }
+  return DL_OK;
+}
+
 int num_sms() {
   int dev = 0, n = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return kNumSMsB200;
@@ -45,73 +59,9 @@ int num_sms() {
 
 using namespace dl;
 
-#define DL_TRY(expr)                  \
-  do {                                \
-    dl_status _s = (expr);            \
-    if (_s != DL_OK) return _s;       \
-  } while (0)
-
-// ---------------------------------------------------------------------------
-// NCCL, resolved from the process (the NCCL instance that owns the comm).
-// ---------------------------------------------------------------------------
-namespace {
-constexpr int kNcclSum = 0;
-constexpr int kNcclFloat32 = 7;
-constexpr int kNcclBfloat16 = 9;
-typedef int (*nccl_allreduce_fn)(const void*, void*, size_t, int, int, void*, cudaStream_t);
-typedef int (*nccl_reducescatter_fn)(const void*, void*, size_t, int, int, void*, cudaStream_t);
-typedef int (*nccl_allgather_fn)(const void*, void*, size_t, int, void*, cudaStream_t);
-typedef const char* (*nccl_errstr_fn)(int);
-}  // namespace
-
-struct dl_comm_s {
-  void* nccl;
-  int rank, world;
-  int loopback;   // measurement-only emulation: collectives become local copies
-  nccl_allreduce_fn allreduce;
-  nccl_reducescatter_fn reducescatter;
-  nccl_allgather_fn allgather;
-  nccl_errstr_fn errstr;
-};
+#define DL_TRY(expr) DL_TRY_INTERNAL(expr)
 
 namespace {
-
-void* find_sym(const char* name) {
-  void* p = dlsym(RTLD_DEFAULT, name);
-  if (p) return p;
-  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
-  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-  return h ? dlsym(h, name) : nullptr;
-}
-
-dl_status nccl_check(const dl_comm_s* c, int r, const char* what) {
-  if (r == 0) return DL_OK;
-  set_error("%s failed: %s", what, c->errstr ? c->errstr(r) : "nccl error");
-  return DL_ERR_NCCL;
-}
-
-size_t nccl_esize(int dtype) { return dtype == kNcclFloat32 ? 4 : 2; }
-
-dl_status all_reduce(dl_comm c, void* buf, size_t count, int dtype, cudaStream_t st) {
-  if (c->loopback) return DL_OK;
-  return nccl_check(c, c->allreduce(buf, buf, count, dtype, kNcclSum, c->nccl, st), "ncclAllReduce");
-}
-dl_status reduce_scatter(dl_comm c, const void* src, void* dst, size_t recv_count, int dtype, cudaStream_t st) {
-  if (c->loopback) {
-    const size_t b = recv_count * nccl_esize(dtype);
-    return cuda_status(cudaMemcpyAsync(dst, static_cast<const uint8_t*>(src) + c->rank * b, b,
-                                       cudaMemcpyDeviceToDevice, st), "loopback reduce-scatter");
-  }
-  return nccl_check(c, c->reducescatter(src, dst, recv_count, dtype, kNcclSum, c->nccl, st), "ncclReduceScatter");
-}
-dl_status all_gather(dl_comm c, const void* src, void* dst, size_t send_count, int dtype, cudaStream_t st) {
-  if (c->loopback) {
-    const size_t b = send_count * nccl_esize(dtype);
-    return cuda_status(cudaMemcpyAsync(static_cast<uint8_t*>(dst) + c->rank * b, src, b, cudaMemcpyDeviceToDevice,
-                                       st), "loopback all-gather");
-  }
-  return nccl_check(c, c->allgather(src, dst, send_count, dtype, c->nccl, st), "ncclAllGather");
-}
 
 // ---------------------------------------------------------------------------
 // validation helpers
@@ -143,19 +93,7 @@ dl_status check_ptr(const void* p, const char* name) {
   }
   return DL_OK;
 }
-dl_status check_device() {
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return cuda_status(e, "cudaGetDevice");
-  int major = 0;
-  e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
-  if (e != cudaSuccess) return cuda_status(e, "cudaDeviceGetAttribute");
-  if (major != 10) {
-    set_error("device compute capability %d.x is not sm_100 (B200)", major);
-    return DL_ERR_CUDA;
-  }
-  return DL_OK;
-}
+dl_status check_device() { return check_device_sm100(); }
 
 // path of dl_lowrank_linear
 enum LinPath { PATH_SIMT, PATH_SKINNY, PATH_WIDE };
@@ -179,20 +117,40 @@ struct Carver {
 };
 
 struct LinWs {
-  float* zf;           // [T x ldz32] fp32 (skinny) / SIMT z
-  __nv_bfloat16* zb;   // [T x ldzb]
-  float* yf;           // [T x ldy32] fp32
+  float* zf;           // [T x ldz32] fp32: skinny stage-1 reduction target / SIMT z
+  __nv_bfloat16* zb;   // [T x ldzb] bf16 stage-2 operand (tensor-core paths)
+  float* yf;           // [T x ldy32] fp32 rank partial (skinny, or any collective)
+  float* yr;           // [T x m/P] fp32 reduce-scatter receive buffer (DL_REDUCE_SCATTER)
   int64_t ldz32, ldzb, ldy32;
 };
 
-LinWs carve_lin(Carver& c, int64_t T, int64_t m, int64_t k, LinPath path, bool comm) {
+// Which work a dl_lowrank_linear call does: `coll` = a collective runs
+// (communicator given and reduce != NONE); `tensor` = the bf16 tensor-core
+// kernels run (T > 16, or a bf16 collective: the rank partial then comes from
+// the skinny tensor path, whose fp32 output the collective reduces).
+struct LinPlan {
+  LinPath path;
+  bool coll, tensor;
+  int P;
+};
+LinPlan lin_plan(int64_t T, dl_dtype dt, const dl_comm_s* comm, dl_reduce reduce) {
+  LinPlan p{};
+  p.path = lin_path(T, dt);
+  p.P = comm ? comm->world : 1;
+  p.coll = comm != nullptr && reduce != DL_REDUCE_NONE;
+  p.tensor = p.path != PATH_SIMT || (p.coll && dt == DL_BF16);
+  return p;
+}
+
+LinWs carve_lin(Carver& c, int64_t T, int64_t m, int64_t k, const LinPlan& pl, dl_reduce reduce) {
   LinWs w{};
   w.ldz32 = rup(k, 4);
   w.ldzb = rup(k, 8);
   w.ldy32 = rup(m, 4);
   w.zf = c.take<float>(static_cast<size_t>(T) * w.ldz32);
-  if (path != PATH_SIMT) w.zb = c.take<__nv_bfloat16>(static_cast<size_t>(T) * w.ldzb);
-  if (path == PATH_SKINNY || comm) w.yf = c.take<float>(static_cast<size_t>(T) * w.ldy32);
+  if (pl.tensor) w.zb = c.take<__nv_bfloat16>(static_cast<size_t>(T) * w.ldzb);
+  if (pl.path == PATH_SKINNY || pl.coll) w.yf = c.take<float>(static_cast<size_t>(T) * w.ldy32);
+  if (pl.coll && reduce == DL_REDUCE_SCATTER) w.yr = c.take<float>(static_cast<size_t>(T) * (m / pl.P));
   return w;
 }
 
@@ -228,67 +186,35 @@ const char* dl_last_error(void) { return g_last_error.c_str(); }
 int dl_version(void) { return 100; }
 int dl_device_ok(void) { return check_device() == DL_OK ? 1 : 0; }
 
-dl_status dl_comm_create(void* nccl_comm, int rank, int world, dl_comm* out) {
-  if (!out || !nccl_comm) {
-    set_error("dl_comm_create: null argument");
-    return DL_ERR_INVALID_ARG;
-  }
-  if (world < 1 || rank < 0 || rank >= world) {
-    set_error("dl_comm_create: bad rank %d / world %d", rank, world);
-    return DL_ERR_INVALID_ARG;
-  }
-  dl_comm_s c{};
-  c.nccl = nccl_comm;
-  c.rank = rank;
-  c.world = world;
-  c.allreduce = reinterpret_cast<nccl_allreduce_fn>(find_sym("ncclAllReduce"));
-  c.reducescatter = reinterpret_cast<nccl_reducescatter_fn>(find_sym("ncclReduceScatter"));
-  c.allgather = reinterpret_cast<nccl_allgather_fn>(find_sym("ncclAllGather"));
-  c.errstr = reinterpret_cast<nccl_errstr_fn>(find_sym("ncclGetErrorString"));
-  if (!c.allreduce || !c.reducescatter || !c.allgather) {
-    set_error("dl_comm_create: NCCL symbols not found in the process");
-    return DL_ERR_NCCL;
-  }
-  *out = new dl_comm_s(c);
-  return DL_OK;
-}
-
-dl_status dl_comm_create_loopback(int rank, int world, dl_comm* out) {
-  if (!out || world < 1 || rank < 0 || rank >= world) {
-    set_error("dl_comm_create_loopback: bad arguments");
-    return DL_ERR_INVALID_ARG;
-  }
-  dl_comm_s c{};
-  c.rank = rank;
-  c.world = world;
-  c.loopback = 1;
-  *out = new dl_comm_s(c);
-  return DL_OK;
-}
-
-dl_status dl_comm_destroy(dl_comm comm) {
-  delete comm;
-  return DL_OK;
-}
-
 // ---------------------------------------------------------------------------
-dl_status dl_lowrank_linear_workspace(int64_t T, int64_t m, int64_t n, int64_t k, dl_dtype dtype, size_t* bytes) {
+dl_status dl_lowrank_linear_workspace(int64_t T, int64_t m, int64_t n, int64_t k, dl_dtype dtype, dl_comm comm,
+                                      dl_reduce reduce, size_t* bytes) {
   (void)n;
   if (!bytes) {
     set_error("bytes is NULL");
     return DL_ERR_INVALID_ARG;
   }
+  if (reduce < DL_REDUCE_NONE || reduce > DL_REDUCE_SCATTER) {
+    set_error("unknown reduce mode %d", (int)reduce);
+    return DL_ERR_INVALID_ARG;
+  }
   Carver c(nullptr);
-  carve_lin(c, T > 0 ? T : 1, m, k, lin_path(T, dtype), true);
+  const LinPlan pl = lin_plan(T, dtype, comm, reduce);
+  carve_lin(c, T > 0 ? T : 1, m, k, pl, reduce);
   *bytes = c.off;
   return DL_OK;
 }
 
 dl_status dl_lowrank_linear(const void* X, int64_t ldx, const void* A, int64_t lda, const void* B, int64_t ldb,
                             void* Y, int64_t ldy, int64_t T, int64_t m, int64_t n, int64_t k, dl_dtype dtype,
-                            int accumulate, dl_comm comm, void* workspace, size_t workspace_bytes, void* stream) {
+                            int accumulate, dl_comm comm, dl_reduce reduce, void* workspace, size_t workspace_bytes,
+                            void* stream) {
   if (dtype != DL_F32 && dtype != DL_BF16) {
     set_error("unknown dtype %d", (int)dtype);
+    return DL_ERR_INVALID_ARG;
+  }
+  if (reduce < DL_REDUCE_NONE || reduce > DL_REDUCE_SCATTER) {
+    set_error("unknown reduce mode %d", (int)reduce);
     return DL_ERR_INVALID_ARG;
   }
   if (T < 0 || m <= 0 || n <= 0) {
@@ -299,7 +225,14 @@ dl_status dl_lowrank_linear(const void* X, int64_t ldx, const void* A, int64_t l
     set_error("rank k=%lld outside [1, min(m,n)=%lld]", (long long)k, (long long)std::min(m, n));
     return DL_ERR_RANK;
   }
+  const LinPlan pl = lin_plan(T, dtype, comm, reduce);
+  const bool scatter = pl.coll && reduce == DL_REDUCE_SCATTER;
+  if (scatter && m % (32 * pl.P) != 0) {
+    set_error("DL_REDUCE_SCATTER needs m %% (32 * world) == 0 (m=%lld, world=%d)", (long long)m, pl.P);
+    return DL_ERR_PARTITION;
+  }
   if (T == 0) return DL_OK;
+  const int64_t m_out = scatter ? m / pl.P : m;   // features this rank receives
   DL_TRY(check_ptr(X, "X"));
   DL_TRY(check_ptr(A, "A"));
   DL_TRY(check_ptr(B, "B"));
@@ -307,18 +240,21 @@ dl_status dl_lowrank_linear(const void* X, int64_t ldx, const void* A, int64_t l
   DL_TRY(check_ld(ldx, n, dtype, "ldx"));
   DL_TRY(check_ld(lda, k, dtype, "lda"));
   DL_TRY(check_ld(ldb, n, dtype, "ldb"));
-  DL_TRY(check_ld(ldy, m, dtype, "ldy"));
+  DL_TRY(check_ld(ldy, m_out, dtype, "ldy"));
   if (dtype == DL_F32 && T > 16) {
     set_error("fp32 runs on the exact-FFMA SIMT path, limited to T <= 16 (got %lld)", (long long)T);
     return DL_ERR_DTYPE;
   }
-  const LinPath path = lin_path(T, dtype);
-  if ((path != PATH_SIMT || comm) && m % 4 != 0) {
+  if (dtype == DL_F32 && pl.coll && accumulate) {
+    set_error("fp32 accumulate (Y +=) with a collective is not supported");
+    return DL_ERR_UNSUPPORTED;
+  }
+  if (pl.tensor && m % 4 != 0) {
     set_error("tensor-core path requires m %% 4 == 0 (got m=%lld)", (long long)m);
     return DL_ERR_UNSUPPORTED;
   }
   size_t need = 0;
-  dl_lowrank_linear_workspace(T, m, n, k, dtype, &need);
+  dl_lowrank_linear_workspace(T, m, n, k, dtype, comm, reduce, &need);
   if (!workspace || workspace_bytes < need) {
     set_error("workspace %zu B < required %zu B", workspace_bytes, need);
     return DL_ERR_WORKSPACE;
@@ -326,48 +262,62 @@ dl_status dl_lowrank_linear(const void* X, int64_t ldx, const void* A, int64_t l
   DL_TRY(check_device());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Carver cv(workspace);
-  LinWs ws = carve_lin(cv, T, m, k, path, comm != nullptr);
-  const bool reduce = comm != nullptr && comm->world > 1;
+  const LinWs ws = carve_lin(cv, T, m, k, pl, reduce);
+  __nv_bfloat16* Yb = static_cast<__nv_bfloat16*>(Y);
 
-  if (path == PATH_SIMT) {
-    if (!reduce) return simt_lowrank(X, ldx, A, lda, B, ldb, Y, ldy, T, m, n, k, dtype, accumulate, ws.zf, st);
-    // partial into fp32 Y scratch, all-reduce, then finish into Y
-    DL_TRY(cuda_status(cudaMemsetAsync(ws.yf, 0, sizeof(float) * T * ws.ldy32, st), "memset"));
-    if (dtype == DL_F32) {
-      DL_TRY(simt_lowrank(X, ldx, A, lda, B, ldb, ws.yf, ws.ldy32, T, m, n, k, dtype, 0, ws.zf, st));
-      DL_TRY(all_reduce(comm, ws.yf, static_cast<size_t>(T) * ws.ldy32, kNcclFloat32, st));
-      if (!accumulate)
-        return cuda_status(cudaMemcpy2DAsync(Y, ldy * 4, ws.yf, ws.ldy32 * 4, m * 4, T, cudaMemcpyDeviceToDevice, st),
-                           "copy");
-      set_error("fp32 accumulate with comm is not supported");
-      return DL_ERR_UNSUPPORTED;
-    }
-    // bf16: compute bf16 partial into zb-sized scratch via Y itself is unsafe with accumulate -> use tensor path
+  if (!pl.tensor) {
+    // SIMT chain (T <= 16 bf16 without a collective, or fp32)
+    if (!pl.coll) return simt_lowrank(X, ldx, A, lda, B, ldb, Y, ldy, T, m, n, k, dtype, accumulate, ws.zf, st);
+    // fp32 collective: partial into the fp32 scratch, all-reduce, copy this rank's columns
+    DL_TRY(simt_lowrank(X, ldx, A, lda, B, ldb, ws.yf, ws.ldy32, T, m, n, k, dtype, 0, ws.zf, st));
+    DL_TRY(coll_all_reduce(comm, ws.yf, static_cast<size_t>(T) * ws.ldy32, kCollF32, st));
+    const int64_t c0 = scatter ? comm->rank * m_out : 0;
+    return cuda_status(cudaMemcpy2DAsync(Y, ldy * 4, ws.yf + c0, ws.ldy32 * 4, m_out * 4, T, cudaMemcpyDeviceToDevice,
+                                         st), "copy");
   }
 
   // ---- tensor-core paths (bf16) ----
-  if (path == PATH_SKINNY || (path == PATH_SIMT && reduce)) {
-    // stage 1: Zf += X B^T (stream-K, fp32 reduction), then bf16 Z
+  // rank partial output: plain [T x m] fp32, or rank-major slabs [P][T][m/P]
+  // for the reduce-scatter (feature f goes to rank f / (m/P))
+  auto partial_out = [&](int mode) {
+    GemmOut o = out_plain(ws.yf, ws.ldy32, mode, 0);
+    if (scatter) {
+      o.scatter_p = pl.P;
+      o.slab = m_out;
+      o.seg_rpr[0] = m_out;
+    }
+    return o;
+  };
+  // finish: reduce the fp32 partial, then Y (+)= result
+  auto finish = [&]() -> dl_status {
+    float* res = ws.yf;
+    int64_t ldr = ws.ldy32;
+    if (scatter) {
+      DL_TRY(coll_reduce_scatter(comm, ws.yf, ws.yr, static_cast<size_t>(T) * m_out, kCollF32, st));
+      res = ws.yr;
+      ldr = m_out;
+    } else if (pl.coll) {
+      DL_TRY(coll_all_reduce(comm, ws.yf, static_cast<size_t>(T) * ws.ldy32, kCollF32, st));
+    }
+    const int clear = pl.path == PATH_SKINNY || pl.path == PATH_SIMT ? 1 : 0;   // stream-K targets stay zeroed
+    if (accumulate) return launch_residual_add_f32(res, ldr, Yb, ldy, T, m_out, clear, st);
+    return launch_f32_to_bf16(res, ldr, Yb, ldy, T, m_out, clear, st);
+  };
+  if (pl.path == PATH_SKINNY || pl.path == PATH_SIMT) {
+    // stage 1: Zf += X B^T (stream-K, fp32 reduction), bf16 Z, stage 2 partial (stream-K)
     DL_TRY(cuda_status(cudaMemsetAsync(ws.zf, 0, sizeof(float) * T * ws.ldz32, st), "memset"));
     DL_TRY(cuda_status(cudaMemsetAsync(ws.yf, 0, sizeof(float) * T * ws.ldy32, st), "memset"));
     DL_TRY(tc_gemm(one_seg(X, ldx, T, n, B, ldb, k, n, out_plain(ws.zf, ws.ldz32, OUT_F32_RED, 0)), true, st));
     DL_TRY(launch_f32_to_bf16(ws.zf, ws.ldz32, ws.zb, ws.ldzb, T, rup(k, 4), 1, st));
-    DL_TRY(tc_gemm(one_seg(ws.zb, ws.ldzb, T, k, A, lda, m, k, out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0)), true,
-                   st));
-    if (reduce) DL_TRY(all_reduce(comm, ws.yf, static_cast<size_t>(T) * ws.ldy32, kNcclFloat32, st));
-    if (accumulate)
-      return launch_residual_add_f32(ws.yf, ws.ldy32, static_cast<__nv_bfloat16*>(Y), ldy, T, m, 1, st);
-    return launch_f32_to_bf16(ws.yf, ws.ldy32, static_cast<__nv_bfloat16*>(Y), ldy, T, m, 1, st);
+    DL_TRY(tc_gemm(one_seg(ws.zb, ws.ldzb, T, k, A, lda, m, k, partial_out(OUT_F32_RED)), true, st));
+    return finish();
   }
   // PATH_WIDE: whole-tile, bf16 Z straight from the epilogue
   DL_TRY(tc_gemm(one_seg(X, ldx, T, n, B, ldb, k, n, out_plain(ws.zb, ws.ldzb, OUT_BF16, 0)), false, st));
-  if (!reduce)
+  if (!pl.coll)
     return tc_gemm(one_seg(ws.zb, ws.ldzb, T, k, A, lda, m, k, out_plain(Y, ldy, OUT_BF16, accumulate)), false, st);
-  DL_TRY(tc_gemm(one_seg(ws.zb, ws.ldzb, T, k, A, lda, m, k, out_plain(ws.yf, ws.ldy32, OUT_F32_STORE, 0)), false,
-                 st));
-  DL_TRY(all_reduce(comm, ws.yf, static_cast<size_t>(T) * ws.ldy32, kNcclFloat32, st));
-  if (accumulate) return launch_residual_add_f32(ws.yf, ws.ldy32, static_cast<__nv_bfloat16*>(Y), ldy, T, m, 0, st);
-  return launch_f32_to_bf16(ws.yf, ws.ldy32, static_cast<__nv_bfloat16*>(Y), ldy, T, m, 0, st);
+  DL_TRY(tc_gemm(one_seg(ws.zb, ws.ldzb, T, k, A, lda, m, k, partial_out(OUT_F32_STORE)), false, st));
+  return finish();
 }
 
 // Test hook for the rank-major activation layout the TP o projection reads
@@ -379,16 +329,18 @@ dl_status dl_debug_linear_gathered(const void* Xg, int P, const void* A, int64_t
     set_error("dl_debug_linear_gathered: need 1 <= T <= 256, n / P a multiple of 64, m %% 4 == 0");
     return DL_ERR_SHAPE;
   }
-  size_t need = 0;
-  dl_lowrank_linear_workspace(T, m, n, k, DL_BF16, &need);
-  if (!workspace || workspace_bytes < need) {
-    set_error("workspace too small");
+  // the skinny tensor path at every T (workspace: dl_lowrank_linear_workspace with T >= 17)
+  const LinPlan pl{PATH_SKINNY, false, true, 1};
+  Carver need(nullptr);
+  carve_lin(need, T, m, k, pl, DL_REDUCE_NONE);
+  if (!workspace || workspace_bytes < need.off) {
+    set_error("workspace too small (%zu < %zu)", workspace_bytes, need.off);
     return DL_ERR_WORKSPACE;
   }
   DL_TRY(check_device());
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Carver cv(workspace);
-  LinWs ws = carve_lin(cv, T, m, k, PATH_SKINNY, false);
+  const LinWs ws = carve_lin(cv, T, m, k, pl, DL_REDUCE_NONE);
   DL_TRY(cuda_status(cudaMemsetAsync(ws.zf, 0, sizeof(float) * T * ws.ldz32, st), "memset"));
   DL_TRY(cuda_status(cudaMemsetAsync(ws.yf, 0, sizeof(float) * T * ws.ldy32, st), "memset"));
   GemmProblem p1 = one_seg(Xg, n, T, n, B, ldb, k, n, out_plain(ws.zf, ws.ldz32, OUT_F32_RED, 0));
@@ -634,9 +586,12 @@ dl_status block_dims(const dl_block_config* c, int world, BlockDims* d) {
 constexpr int kSchedSlots = 4;
 // prefill tail scratch: up to 56 tiles of 256 x 256 fp32 (>= 75% of 74 clusters)
 constexpr size_t kTailBytes = static_cast<size_t>(56) * 256 * 256 * 4;
+// The rotation is per host thread: a stream is driven by one thread, so a
+// process-wide counter would let another thread's launches (group ranks, one
+// thread each) hand two consecutive launches of one stream the same slot.
 unsigned int* next_sched(unsigned int* base) {
-  static std::atomic<unsigned> slot{0};
-  return base + 2 * (slot.fetch_add(1) % kSchedSlots);
+  static thread_local unsigned slot = 0;
+  return base + 2 * (slot++ % kSchedSlots);
 }
 
 struct BlockWs {
@@ -650,7 +605,6 @@ struct BlockWs {
   int64_t ask_items;
   unsigned int* sched;               // kSchedSlots x 2 stream-K work counters
   unsigned int* tile_cnt;            // stream-K fixup arrival counters (one per output tile)
-  unsigned int* fbar;                // fused decode: 2 x 16 phase-barrier counters (pre / post attention)
   float* tail;                       // prefill DP + stream-K tail scratch (zero-maintained)
   size_t tail_bytes;
   __nv_bfloat16 *lat_send, *lat_recv;   // DeInfer latent all-gather [T x slot] / [P][T][slot]
@@ -687,7 +641,6 @@ BlockWs carve_block(Carver& c, const BlockDims& d, int64_t Tmax) {
   w.ask = c.take<float>(attention_sk_workspace(Tmax, static_cast<int>(d.Hq_loc)) / sizeof(float));
   w.sched = c.take<unsigned int>(2 * kSchedSlots);
   w.tile_cnt = c.take<unsigned int>(static_cast<size_t>((d.nmax + d.kmax) / 128 + 64));
-  w.fbar = c.take<unsigned int>(32);
   w.tail_bytes = Tmax > 256 ? kTailBytes : 0;
   w.tail = w.tail_bytes ? c.take<float>(w.tail_bytes / sizeof(float)) : nullptr;
   if (d.layout == DL_LAYOUT_DEINFER) {
@@ -789,7 +742,7 @@ GemmProblem stage2(const dl_factor_group& grp, int nseg, const int64_t* rows, co
 // (and their fence / counter round trips) pile onto the kernel's tail, while a
 // PDL-launched finalize kernel overlaps the GEMM drain.
 bool use_fixup() {
-  static const bool on = getenv("DL_FIXUP") && atoi(getenv("DL_FIXUP")) != 0;
+  static const bool on = DL_ENV("DL_FIXUP") && atoi(DL_ENV("DL_FIXUP")) != 0;
   return on;
 }
 
@@ -799,7 +752,7 @@ bool use_fixup() {
 // stage-2 fixup `fix2` (op != FIX_NONE) finalizes the group output in place
 // of a separate kernel (then `out2` only supplies the output pointer/layout).
 bool use_zred() {
-  static const bool on = !getenv("DL_ZRED") || atoi(getenv("DL_ZRED")) != 0;   // A/B switch (default on)
+  static const bool on = !DL_ENV("DL_ZRED") || atoi(DL_ENV("DL_ZRED")) != 0;   // A/B switch (default on)
   return on;
 }
 
@@ -895,8 +848,8 @@ dl_status deinfer_latent(const dl_factor_group& grp, int nseg, const __nv_bfloat
     p1.tail_bytes = ws.tail_bytes;
     DL_TRY(tc_gemm(p1, false, st));
   }
-  DL_TRY(all_gather(comm, red16 ? ws.lat_red : ws.lat_send, ws.lat_recv, static_cast<size_t>(T) * d.lat_slot,
-                    kNcclBfloat16, st));
+  DL_TRY(coll_all_gather(comm, red16 ? ws.lat_red : ws.lat_send, ws.lat_recv, static_cast<size_t>(T) * d.lat_slot,
+                    kCollBF16, st));
   const ZLayout zl = zlayout(grp, nseg);
   LatentMap mp{};
   mp.nseg = nseg;
@@ -939,7 +892,9 @@ dl_status deinfer_first(const dl_factor_group& grp, int nseg, const int64_t* row
 
 // DeInfer second sub-layer (o or down): stage 1 with the rank's input-column
 // shard of B on its local activations -> partial latent [T x l]; reduce-sum
-// of the latent (fp32 on the decode path, bf16 on the prefill path); stage 2
+// of the latent (bf16 payload: decode partials red.add-ed as bf16x2 into the
+// all-reduce buffer, prefill bf16 epilogue stores; fp32 only with the
+// DL_ZRED=0 A/B switch); stage 2
 // with the replicated A, residual added into x.
 dl_status deinfer_second(const dl_factor_group& grp, const __nv_bfloat16* act, int64_t n_loc, int64_t m_out,
                          int64_t T, bool skinny, const BlockWs& ws, dl_comm comm, __nv_bfloat16* x, cudaStream_t st) {
@@ -952,7 +907,7 @@ dl_status deinfer_second(const dl_factor_group& grp, const __nv_bfloat16* act, i
     GemmProblem p1 = one_seg(act, n_loc, T, n_loc, grp.B, grp.ldb, l, n_loc, out_plain(ws.yr, ldl, OUT_BF16_RED, 0));
     p1.sched = next_sched(ws.sched);
     DL_TRY(tc_gemm(p1, true, st));
-    DL_TRY(all_reduce(comm, ws.yr, static_cast<size_t>(T) * ldl, kNcclBfloat16, st));
+    DL_TRY(coll_all_reduce(comm, ws.yr, static_cast<size_t>(T) * ldl, kCollBF16, st));
     GemmProblem p2 = one_seg(ws.yr, ldl, T, l, grp.seg[0].A, grp.seg[0].lda, m_out, l,
                              out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0));
     p2.sched = next_sched(ws.sched);
@@ -967,7 +922,7 @@ dl_status deinfer_second(const dl_factor_group& grp, const __nv_bfloat16* act, i
     GemmProblem p1 = one_seg(act, n_loc, T, n_loc, grp.B, grp.ldb, l, n_loc, out_plain(ws.zf, ws.ldz32, OUT_F32_RED, 0));
     p1.sched = next_sched(ws.sched);
     DL_TRY(tc_gemm(p1, true, st));
-    DL_TRY(all_reduce(comm, ws.zf, static_cast<size_t>(T) * ws.ldz32, kNcclFloat32, st));
+    DL_TRY(coll_all_reduce(comm, ws.zf, static_cast<size_t>(T) * ws.ldz32, kCollF32, st));
     DL_TRY(launch_f32_to_bf16(ws.zf, ws.ldz32, ws.zb, ws.ldzb, T, rup(l, 4), 1, st));
     GemmProblem p2 = one_seg(ws.zb, ws.ldzb, T, l, grp.seg[0].A, grp.seg[0].lda, m_out, l,
                              out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0));
@@ -979,7 +934,7 @@ dl_status deinfer_second(const dl_factor_group& grp, const __nv_bfloat16* act, i
   p1.tail_acc = ws.tail;
   p1.tail_bytes = ws.tail_bytes;
   DL_TRY(tc_gemm(p1, false, st));
-  DL_TRY(all_reduce(comm, ws.zb, static_cast<size_t>(T) * ws.ldzb, kNcclBfloat16, st));
+  DL_TRY(coll_all_reduce(comm, ws.zb, static_cast<size_t>(T) * ws.ldzb, kCollBF16, st));
   GemmProblem p2 = one_seg(ws.zb, ws.ldzb, T, l, grp.seg[0].A, grp.seg[0].lda, m_out, l, out_plain(x, m_out, OUT_BF16, 1));
   p2.tail_acc = ws.tail;
   p2.tail_bytes = ws.tail_bytes;
@@ -1029,7 +984,7 @@ dl_status kvlr_attention(const dl_block_config* cfg, const BlockDims& d, const d
   //    position embedding ... to the reconstruction results"), applied in
   //    the reconstruction GEMM's epilogue; the separate in-place kernel is kept
   //    for key widths the vectorised epilogue does not cover
-  static const bool sep_rope = getenv("DL_RECON_ROPE_SEP") && atoi(getenv("DL_RECON_ROPE_SEP")) != 0;   // A/B: RoPE as its own pass
+  static const bool sep_rope = DL_ENV("DL_RECON_ROPE_SEP") && atoi(DL_ENV("DL_RECON_ROPE_SEP")) != 0;   // A/B: RoPE as its own pass
   const bool epi_rope = !cfg->no_rope && hkl % 128 == 0 && !sep_rope;
   if (epi_rope) {
     pr.out.rope_pos = kv->squeeze_pos;
@@ -1062,83 +1017,6 @@ dl_status kvlr_attention(const dl_block_config* cfg, const BlockDims& d, const d
 }
 
 }  // namespace
-
-// Fused decode of one block at TP = 1 (decode_fused.cu): the pre-attention
-// half (RMSNorm, q|k|v chain, RoPE + cache append) and the post-attention half
-// (o chain + residual + MLP norm, gate|up chain, SiLU*up, down chain +
-// residual) each run as one persistent phase-program kernel; attention in
-// between.  Same arithmetic and rounding points as the per-kernel path.
-dl_status fused_block(const dl_block_config* cfg, const BlockDims& d, const dl_block_weights* w, __nv_bfloat16* x,
-                      int64_t T, const BlockWs& ws, RopeCacheArgs rc, const AttnArgs& aa, cudaStream_t st) {
-  const int64_t qkv_rows[3] = {d.h, d.hkv, d.hkv};
-  const int64_t gu_rows[2] = {d.m, d.m};
-  const int64_t h_rows[1] = {d.h};
-  const int n_gu = d.glu ? 2 : 1;
-  const float eps = cfg->rms_eps;
-  auto gemm = [](const GemmProblem& p) {
-    FusedStep s{};
-    s.kind = FK_GEMM;
-    s.gemm = p;
-    return s;
-  };
-  auto el = [](int kind, float* acc, int64_t lda, __nv_bfloat16* xx, const void* g, __nv_bfloat16* y, int64_t ldy,
-               int64_t n, float e) {
-    FusedStep s{};
-    s.kind = kind;
-    s.acc = acc;
-    s.lda = lda;
-    s.x = xx;
-    s.ldx = n;
-    s.g = static_cast<const __nv_bfloat16*>(g);
-    s.y = y;
-    s.ldy = ldy;
-    s.n = n;
-    s.eps = e;
-    return s;
-  };
-  const GemmOut zout = out_plain(ws.zf, ws.ldz32, OUT_F32_RED, 0);
-  const GemmOut yout = out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0);
-
-  FusedProgram a{};
-  a.T = T;
-  a.bar = ws.fbar;
-  rc.acc = ws.yf;
-  rc.ld_src = ws.ldy32;
-  rc.clear = 1;
-  a.rope = rc;
-  const ZLayout zq = zlayout(w->qkv, 3);
-  a.step[a.n++] = el(FK_RMSNORM, nullptr, 0, x, w->attn_norm, ws.xn, d.h, d.h, eps);
-  a.step[a.n++] = gemm(stage1(w->qkv, 3, ws.xn, d.h, T, d.h, zq, zout));
-  a.step[a.n++] = el(FK_CVT, ws.zf, ws.ldz32, nullptr, nullptr, ws.zb, ws.ldzb, zq.width, 0.f);
-  a.step[a.n++] = gemm(stage2(w->qkv, 3, qkv_rows, ws.zb, ws.ldzb, T, zq, yout));
-  a.step[a.n++] = el(FK_ROPE_CACHE, ws.yf, ws.ldy32, nullptr, nullptr, nullptr, 0, 0, 0.f);
-  DL_TRY(fused_decode(a, st));
-
-  DL_TRY(launch_attention(aa, st));
-
-  FusedProgram b{};
-  b.T = T;
-  b.bar = ws.fbar + 16;
-  const ZLayout zo = zlayout(w->o, 1), zg = zlayout(w->gu, n_gu), zd = zlayout(w->down, 1);
-  b.step[b.n++] = gemm(stage1(w->o, 1, ws.att, d.h, T, d.h, zo, zout));
-  b.step[b.n++] = el(FK_CVT, ws.zf, ws.ldz32, nullptr, nullptr, ws.zb, ws.ldzb, zo.width, 0.f);
-  b.step[b.n++] = gemm(stage2(w->o, 1, h_rows, ws.zb, ws.ldzb, T, zo, yout));
-  b.step[b.n++] = el(FK_RESID_RMSNORM, ws.yf, ws.ldy32, x, w->mlp_norm, ws.xn, d.h, d.h, eps);
-  b.step[b.n++] = gemm(stage1(w->gu, n_gu, ws.xn, d.h, T, d.h, zg, zout));
-  b.step[b.n++] = el(FK_CVT, ws.zf, ws.ldz32, nullptr, nullptr, ws.zb, ws.ldzb, zg.width, 0.f);
-  b.step[b.n++] = gemm(stage2(w->gu, n_gu, gu_rows, ws.zb, ws.ldzb, T, zg, yout));
-  b.step[b.n++] = el(d.glu ? FK_SILU : FK_RELU, ws.yf, ws.ldy32, nullptr, nullptr, ws.act, d.m, d.m, 0.f);
-  b.step[b.n++] = gemm(stage1(w->down, 1, ws.act, d.m, T, d.m, zd, zout));
-  b.step[b.n++] = el(FK_CVT, ws.zf, ws.ldz32, nullptr, nullptr, ws.zb, ws.ldzb, zd.width, 0.f);
-  b.step[b.n++] = gemm(stage2(w->down, 1, h_rows, ws.zb, ws.ldzb, T, zd, yout));
-  b.step[b.n++] = el(FK_RESID, ws.yf, ws.ldy32, x, nullptr, nullptr, 0, d.h, 0.f);
-  return fused_decode(b, st);
-}
-
-bool use_fused() {
-  static const bool on = getenv("DL_FUSED") && atoi(getenv("DL_FUSED")) != 0;   // opt-in while in development
-  return on;
-}
 
 dl_status dl_block_workspace(const dl_block_config* cfg, int world, size_t* bytes) {
   if (!bytes) {
@@ -1233,11 +1111,10 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   Carver cv(workspace);
   const BlockWs ws = carve_block(cv, d, cfg->max_tokens);
   const bool skinny = T <= 256;
-  // DL_FORCE_TP_PATH=1 (tests only): take the tensor-parallel branch (bf16
-  // partials, NCCL RS/AG/AR, un-permute) even with a 1-rank communicator, so the
-  // TP code path is exercised on a single GPU.
-  static const bool force_tp = getenv("DL_FORCE_TP_PATH") && atoi(getenv("DL_FORCE_TP_PATH")) != 0;
-  const bool tp = comm && (P > 1 || force_tp);
+  // Any real communicator (NCCL or group, world >= 1) selects the
+  // tensor-parallel branch (bf16 partials, RS / AG / AR); at world 1 its
+  // collectives are identities.  A loopback communicator of world 1 is TP = 1.
+  const bool tp = comm && (P > 1 || comm->kind != kCommLoopback);
   if (kv) {
     if (phase != DL_DECODE || !skinny) {
       set_error("low-rank KV cache: decode only (T <= 256)");
@@ -1291,11 +1168,10 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   // them, the attention CTAs only become resident once the q|k|v stage-2
   // GEMM's CTAs (216 KB of shared memory each) exit, so the old-key tiles are
   // no longer streamed while the predecessor drains.
-  static const bool no_rope_fuse = !(getenv("DL_ROPE_FUSE") && atoi(getenv("DL_ROPE_FUSE")) != 0);
-  static const bool no_fuse_rn = getenv("DL_NO_FUSE_RESNORM") != nullptr;
+  static const bool no_rope_fuse = !(DL_ENV("DL_ROPE_FUSE") && atoi(DL_ENV("DL_ROPE_FUSE")) != 0);
+  static const bool no_fuse_rn = DL_ENV("DL_NO_FUSE_RESNORM") != nullptr;
   const bool rope_attn = skinny && !tp && !kv && use_zred() && !use_fixup() && !no_rope_fuse && !no_fuse_rn &&
-                         phase == DL_DECODE && num_seqs <= 1024 && d.d == 128 &&
-                         !(skinny && !tp && !kv && T <= 128 && use_fused());
+                         phase == DL_DECODE && num_seqs <= 1024 && d.d == 128;
   if (rope_attn) {
     qkv_out.mode = OUT_BF16_RED;
     qkv_out.ptr = ws.yr;
@@ -1390,12 +1266,10 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
     return deinfer_second(w->down, ws.act, m_loc, d.h, T, skinny, ws, comm, x, st);
   }
 
-  if (skinny && !tp && !kv && !fx && T <= 128 && d.h <= 8192 && d.m % 64 == 0 && use_fused()) return fused_block(cfg, d, w, x, T, ws, rc, aa, st);
-
   if (!prenormed)
     DL_TRY(launch_rmsnorm(x, static_cast<const __nv_bfloat16*>(w->attn_norm), ws.xn, T, d.h, cfg->rms_eps, st));
   SideZero zq;
-  static const bool fix_rope = getenv("DL_FIXUP_ROPE") && atoi(getenv("DL_FIXUP_ROPE")) != 0;   // A/B switch
+  static const bool fix_rope = DL_ENV("DL_FIXUP_ROPE") && atoi(DL_ENV("DL_FIXUP_ROPE")) != 0;   // A/B switch
   const bool fx_rope = !fx && !kv && !tp && skinny && fix_rope && !rope_attn && phase == DL_DECODE && num_seqs <= 1024;
   if (kv) {
     DL_TRY(kvlr_attention(cfg, d, w, ws, kv, T, positions, cache_lens, false, comm, aa, rc, st));
@@ -1426,7 +1300,7 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
       rc.ld_src = NQKV;
     }
   } else if (tpr) {
-    DL_TRY(reduce_scatter(comm, ws.yr, ws.rs, static_cast<size_t>(T) * d.W, kNcclBfloat16, st));
+    DL_TRY(coll_reduce_scatter(comm, ws.yr, ws.rs, static_cast<size_t>(T) * d.W, kCollBF16, st));
     rc.src = ws.rs;
     rc.ld_src = d.W;
     rc.zero = zq;
@@ -1435,7 +1309,7 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
     rc.zero2.row_bytes = rc.zero2.ld = static_cast<int64_t>(T) * NQKV * 2;
   } else {
     if (skinny) DL_TRY(launch_f32_to_bf16(ws.yf, NQKV, ws.yb, NQKV, 1, T * NQKV, 1, st, zq));   // contiguous [P][T][W]
-    DL_TRY(reduce_scatter(comm, ws.yb, ws.rs, static_cast<size_t>(T) * d.W, kNcclBfloat16, st));
+    DL_TRY(coll_reduce_scatter(comm, ws.yb, ws.rs, static_cast<size_t>(T) * d.W, kCollBF16, st));
     rc.src = ws.rs;
     rc.ld_src = d.W;
   }
@@ -1456,10 +1330,10 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   const __nv_bfloat16* att_in = ws.att;
   int o_act_p = 0;
   int64_t o_act_w = 0;
-  static const bool no_ag3d = getenv("DL_NO_AG3D") != nullptr;   // A/B switch
+  static const bool no_ag3d = DL_ENV("DL_NO_AG3D") != nullptr;   // A/B switch
   if (tp) {
     const int64_t wl = d.Hq_loc * d.d;
-    DL_TRY(all_gather(comm, ws.att, ws.ag, static_cast<size_t>(T) * wl, kNcclBfloat16, st));
+    DL_TRY(coll_all_gather(comm, ws.att, ws.ag, static_cast<size_t>(T) * wl, kCollBF16, st));
     if (skinny && !no_ag3d && wl % 64 == 0) {
       // o's stage-1 TMA reads the rank-major [P][T][wl] all-gather output directly
       att_in = ws.ag;
@@ -1475,11 +1349,11 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   auto finish_residual = [&](int64_t n, const SideZero& z) -> dl_status {
     if (!tp) return skinny ? launch_residual_add_f32(ws.yf, ws.ldy32, x, d.h, T, n, 1, st, z) : DL_OK;
     if (tpr) {
-      DL_TRY(all_reduce(comm, ws.yr, static_cast<size_t>(T) * n, kNcclBfloat16, st));
+      DL_TRY(coll_all_reduce(comm, ws.yr, static_cast<size_t>(T) * n, kCollBF16, st));
       return launch_residual_add_bf16(ws.yr, n, x, d.h, T, n, st, 1, z);
     }
     if (skinny) DL_TRY(launch_f32_to_bf16(ws.yf, ws.ldy32, ws.yb, n, T, n, 1, st, z));
-    DL_TRY(all_reduce(comm, ws.yb, static_cast<size_t>(T) * n, kNcclBfloat16, st));
+    DL_TRY(coll_all_reduce(comm, ws.yb, static_cast<size_t>(T) * n, kCollBF16, st));
     return launch_residual_add_bf16(ws.yb, n, x, d.h, T, n, st);
   };
   // wide & TP=1: the stage-2 epilogue adds straight into x (fused residual)
@@ -1496,7 +1370,7 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   DL_TRY(run_group(w->o, 1, h_rows, att_in, d.h, d.h, T, skinny, ws, resid_out(), st, &fres, fx ? nullptr : &zo, 0,
                    o_act_p, o_act_w));
   const __nv_bfloat16* mlp_norm = static_cast<const __nv_bfloat16*>(w->mlp_norm);
-  static const bool no_fuse = getenv("DL_NO_FUSE_RESNORM") != nullptr;   // A/B timing switch
+  static const bool no_fuse = DL_ENV("DL_NO_FUSE_RESNORM") != nullptr;   // A/B timing switch
   if (!fx && !tp && skinny && !no_fuse) {
     // residual add of the o projection fused with the MLP pre-norm
     SideZero zqkv;
@@ -1508,7 +1382,7 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
     DL_TRY(launch_residual_rmsnorm(ws.yf, ws.ldy32, x, mlp_norm, ws.xn, T, d.h, cfg->rms_eps, st, zo, zqkv));
   } else if (tpr && !no_fuse) {
     // TP: all-reduce of the bf16 partials, then residual + MLP pre-norm in one pass
-    DL_TRY(all_reduce(comm, ws.yr, static_cast<size_t>(T) * d.h, kNcclBfloat16, st));
+    DL_TRY(coll_all_reduce(comm, ws.yr, static_cast<size_t>(T) * d.h, kCollBF16, st));
     DL_TRY(launch_residual_rmsnorm_bf16(ws.yr, d.h, x, mlp_norm, ws.xn, T, d.h, cfg->rms_eps, st, zo));
   } else {
     if (!fx) DL_TRY(finish_residual(d.h, zo));
@@ -1520,12 +1394,12 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   // SiLU(gate)*up by the gate|up stage-2 last-contributor fixup: with all
   // fixups (DL_FIXUP) or alone (DL_FIXUP_SILU; the latent stays in Z slot 1
   // until the down group's finalize clears it)
-  static const bool fix_silu = getenv("DL_FIXUP_SILU") && atoi(getenv("DL_FIXUP_SILU")) != 0;
+  static const bool fix_silu = DL_ENV("DL_FIXUP_SILU") && atoi(DL_ENV("DL_FIXUP_SILU")) != 0;
   const bool fx_gu = (fx || (fix_silu && skinny && !tp)) && d.glu;
   GemmOut gu_out = skinny ? out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0) : out_plain(ws.yb, ngu, OUT_BF16, 0);
   // skinny TP = 1: gate|up partials as bf16x2 reductions too (the SiLU input is
   // bf16-rounded anyway); halves the reduction and finalize traffic (DL_GU_F32 A/B)
-  static const bool gu_f32 = getenv("DL_GU_F32") != nullptr;
+  static const bool gu_f32 = DL_ENV("DL_GU_F32") != nullptr;
   const bool gur = skinny && !tp && use_zred() && !fx_gu && !gu_f32;
   if (tpr || gur) gu_out = out_plain(ws.yr, ngu, OUT_BF16_RED, 0);
   const GemmFixup fsilu = fixup(fx_gu ? FIX_SILU : FIX_NONE);
@@ -1539,12 +1413,12 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
     if (d.glu) DL_TRY(launch_silu_mul_f32(ws.yf, ws.ldy32, ws.act, d.m, T, d.m, 1, st, zg));
     else DL_TRY(launch_relu_f32(ws.yf, ws.ldy32, ws.act, d.m, T, d.m, 1, st, zg));
   } else if (tpr) {
-    DL_TRY(all_reduce(comm, ws.yr, static_cast<size_t>(T) * ngu, kNcclBfloat16, st));
+    DL_TRY(coll_all_reduce(comm, ws.yr, static_cast<size_t>(T) * ngu, kCollBF16, st));
     if (d.glu) DL_TRY(launch_silu_mul_bf16(ws.yr, ngu, ws.act, d.m, T, d.m, st, 1, zg));
     else DL_TRY(launch_relu_bf16(ws.yr, ngu, ws.act, d.m, T, d.m, st, 1, zg));
   } else {
     if (skinny) DL_TRY(launch_f32_to_bf16(ws.yf, ws.ldy32, ws.yb, ngu, T, ngu, 1, st, zg));
-    if (tp) DL_TRY(all_reduce(comm, ws.yb, static_cast<size_t>(T) * ngu, kNcclBfloat16, st));
+    if (tp) DL_TRY(coll_all_reduce(comm, ws.yb, static_cast<size_t>(T) * ngu, kCollBF16, st));
     if (d.glu) DL_TRY(launch_silu_mul_bf16(ws.yb, ngu, ws.act, d.m, T, d.m, st));
     else DL_TRY(launch_relu_bf16(ws.yb, ngu, ws.act, d.m, T, d.m, st));
   }
@@ -1558,7 +1432,7 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
     return DL_OK;
   }
   if (next_norm && tpr && !no_fuse && d.layout != DL_LAYOUT_DEINFER) {
-    DL_TRY(all_reduce(comm, ws.yr, static_cast<size_t>(T) * d.h, kNcclBfloat16, st));
+    DL_TRY(coll_all_reduce(comm, ws.yr, static_cast<size_t>(T) * d.h, kCollBF16, st));
     DL_TRY(launch_residual_rmsnorm_bf16(ws.yr, d.h, x, static_cast<const __nv_bfloat16*>(next_norm), ws.xn, T, d.h,
                                         cfg->rms_eps, st, zd));
     *next_normed = true;
@@ -1728,7 +1602,7 @@ dl_status dl_dense(const void* X, int64_t ldx, const void* W, int64_t ldw, void*
   // debug A/B switch (DL_DENSE_SK=1): stream-K with an fp32 reduction into the
   // (zeroed, T*N*4 + 256 bytes) workspace, then conversion -- the decode path's
   // scheme applied to a dense GEMM.
-  static const bool sk = getenv("DL_DENSE_SK") && atoi(getenv("DL_DENSE_SK")) != 0;
+  static const bool sk = DL_ENV("DL_DENSE_SK") && atoi(DL_ENV("DL_DENSE_SK")) != 0;
   if (sk && workspace && workspace_bytes >= static_cast<size_t>(T) * N * 4 + 256 && T <= 256 && N % 4 == 0) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     float* acc = static_cast<float*>(workspace);

@@ -990,7 +990,7 @@ size_t attention_sk_workspace(int64_t max_tokens, int Hq) {
 
 // stream-K decode attention; DL_ERR_UNSUPPORTED -> caller uses the split kernel
 dl_status launch_attention_sk(const AttnArgs& a, cudaStream_t st) {
-  static const bool off = getenv("DL_ATTN_SPLIT") && atoi(getenv("DL_ATTN_SPLIT")) != 0;   // A/B switch
+  static const bool off = DL_ENV("DL_ATTN_SPLIT") && atoi(DL_ENV("DL_ATTN_SPLIT")) != 0;   // A/B switch
   const int nch = (a.Hq / a.Hk + 15) / 16;
   const int64_t items = static_cast<int64_t>(a.num_seqs) * a.Hk * nch;
   if (off || !a.decode || a.num_seqs > sk::kMaxSeqs || !a.sk_ws || items > a.sk_items_cap) return DL_ERR_UNSUPPORTED;
@@ -1029,11 +1029,11 @@ dl_status launch_attention_sk(const AttnArgs& a, cudaStream_t st) {
   k.kc = const_cast<__nv_bfloat16*>(a.k_cache);
   k.vc = const_cast<__nv_bfloat16*>(a.v_cache);
   k.zero = a.zero;
-  static const int l2pf = getenv("DL_ATTN_L2PF") ? atoi(getenv("DL_ATTN_L2PF")) : 0;
+  static const int l2pf = DL_ENV("DL_ATTN_L2PF") ? atoi(DL_ENV("DL_ATTN_L2PF")) : 0;
   k.l2pf = l2pf;
   k.part = reinterpret_cast<float*>(static_cast<uint8_t*>(a.sk_ws) + (a.sk_items_cap + 63) / 64 * 64 * 4 * 4);
   // ring depth x CTAs per SM: 3 x 2 (default) or 2 x 3 (DL_ATTN_CFG=23, A/B)
-  static const bool cfg23 = getenv("DL_ATTN_CFG") && atoi(getenv("DL_ATTN_CFG")) == 23;
+  static const bool cfg23 = DL_ENV("DL_ATTN_CFG") && atoi(DL_ENV("DL_ATTN_CFG")) == 23;
   auto kern = cfg23 ? attn_decode_sk_kernel<2, 3> : attn_decode_sk_kernel<3, 2>;
   const size_t smem = cfg23 ? sk::smem_bytes<2>(a.num_seqs) : sk::smem_bytes<3>(a.num_seqs);
   static bool attr = false;

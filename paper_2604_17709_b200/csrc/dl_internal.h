@@ -8,10 +8,58 @@
 
 #include "../../include/dl.h"
 
+#define DL_TRY_INTERNAL(expr)   \
+  do {                          \
+    dl_status _s = (expr);      \
+    if (_s != DL_OK) return _s; \
+  } while (0)
+
+// A/B timing switches.  Alternatives that were measured and lost stay
+// selectable by environment variable for re-measurement, but only in the
+// instrumented build (libdl_ab.so, compiled with -DDL_AB_SWITCHES); the
+// release library libdl.so ignores the environment entirely and always runs
+// the measured defaults, so its behaviour is fixed by include/dl.h alone.
+#ifdef DL_AB_SWITCHES
+#define DL_ENV(name) getenv(name)
+#else
+#define DL_ENV(name) (static_cast<const char*>(nullptr))
+#endif
+
+namespace dl {
+struct CommGroup;   // comm.cu
+enum CommKind { kCommNccl = 0, kCommLoopback = 1, kCommGroup = 2 };
+// NCCL dtype codes (ncclFloat32 / ncclBfloat16), also used by the other kinds
+constexpr int kCollF32 = 7;
+constexpr int kCollBF16 = 9;
+typedef int (*nccl_allreduce_fn)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+typedef int (*nccl_reducescatter_fn)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+typedef int (*nccl_allgather_fn)(const void*, void*, size_t, int, void*, cudaStream_t);
+typedef const char* (*nccl_errstr_fn)(int);
+}  // namespace dl
+
+struct dl_comm_s {
+  int kind;            // dl::CommKind
+  void* nccl;          // kCommNccl: the caller's ncclComm_t
+  int rank, world;
+  dl::nccl_allreduce_fn allreduce;
+  dl::nccl_reducescatter_fn reducescatter;
+  dl::nccl_allgather_fn allgather;
+  dl::nccl_errstr_fn errstr;
+  dl::CommGroup* group;   // kCommGroup: shared by the group's ranks
+};
+
 namespace dl {
 
 void set_error(const char* fmt, ...);
 dl_status cuda_status(cudaError_t e, const char* what);
+// DL_OK if the current device is sm_100 (B200), else DL_ERR_CUDA
+dl_status check_device_sm100();
+
+// collectives (comm.cu), NCCL semantics for every communicator kind
+dl_status coll_all_reduce(dl_comm c, void* buf, size_t count, int dtype, cudaStream_t st);
+dl_status coll_reduce_scatter(dl_comm c, const void* src, void* dst, size_t recv_count, int dtype,
+                              cudaStream_t st);
+dl_status coll_all_gather(dl_comm c, const void* src, void* dst, size_t send_count, int dtype, cudaStream_t st);
 
 constexpr int kNumSMsB200 = 148;
 int num_sms();
@@ -201,44 +249,6 @@ __device__ __forceinline__ void ew_mark(const EwTrace& tr, int field) {   // fie
 // 2-D bf16 TMA map over a row-major [rows x cols] matrix (ld elements), box
 // {64 cols, box_rows}, 128B swizzle, out-of-bounds elements read as zero.
 bool encode_map_bf16(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows);
-
-// ---------------------------------------------------------------------------
-// Fused decode (decode_fused.cu): a list of phases run by one persistent
-// kernel with grid barriers between them (T <= 128).  GEMM phases are
-// GemmProblems with a plain OUT_F32_RED output (stream-K red.add into a
-// zero-maintained buffer); elementwise phases consume-and-clear fp32 buffers.
-// ---------------------------------------------------------------------------
-constexpr int kFusedMaxPhases = 14;
-constexpr int kFusedMaxGemm = 6;
-enum FusedKind {
-  FK_GEMM = 0,
-  FK_RMSNORM = 1,         // y = rmsnorm(x) * g                               [T x n]
-  FK_RESID_RMSNORM = 2,   // x = bf16(x + acc), acc cleared; y = rmsnorm(x) * g
-  FK_CVT = 3,             // y = bf16(acc), acc cleared                       [T x n]
-  FK_ROPE_CACHE = 4,      // FusedProgram::rope from acc (cleared)
-  FK_SILU = 5,            // y = silu(acc[:, :n]) * acc[:, n:2n], acc cleared
-  FK_RELU = 6,            // y = relu(acc[:, :n]), acc cleared
-  FK_RESID = 7,           // x = bf16(x + acc), acc cleared
-};
-struct FusedStep {
-  int kind;
-  GemmProblem gemm;
-  float* acc; int64_t lda;
-  __nv_bfloat16* x; int64_t ldx;
-  const __nv_bfloat16* g;
-  __nv_bfloat16* y; int64_t ldy;
-  int64_t n; float eps;
-};
-struct FusedProgram {
-  int64_t T;
-  int n;
-  FusedStep step[kFusedMaxPhases];
-  RopeCacheArgs rope;
-  unsigned int* bar;   // kFusedMaxPhases + 1 zeroed u32 counters (workspace), left zeroed
-};
-dl_status fused_decode(const FusedProgram& p, cudaStream_t st);
-// debug timeline of the fused kernels (see decode_fused.cu); buf == NULL: off
-dl_status set_fused_trace(void* buf);
 
 // ---------------------------------------------------------------------------
 // SIMT skinny chain (simt_chain.cu): Y[T x m] (+)= (X B^T) A^T, T <= 16.

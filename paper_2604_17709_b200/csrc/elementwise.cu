@@ -510,7 +510,9 @@ __global__ void __launch_bounds__(128) rope_cache_kernel(RopeCacheArgs a, EwTrac
       s = lo;
       cpos = a.cache_lens[s] + (t - a.cu_seqlens[s]);
     }
-    slot = static_cast<int64_t>(s) * a.Hk * a.max_seq + cpos;
+    // a position past the cache capacity is dropped (never written into the
+    // next head's or sequence's rows; include/dl.h)
+    slot = (cpos >= 0 && cpos < a.max_seq) ? static_cast<int64_t>(s) * a.Hk * a.max_seq + cpos : -1;
   }
   pdl_wait();
   ew_mark(tr, 2);
@@ -542,7 +544,7 @@ __global__ void __launch_bounds__(128) rope_cache_kernel(RopeCacheArgs a, EwTrac
     if (hd < a.Hq) {
       store4(a.q_out + t * static_cast<int64_t>(a.Hq) * a.d + static_cast<int64_t>(hd) * a.d + 2 * p0, r.x, r.y, r.z,
              r.w);
-    } else {
+    } else if (slot >= 0) {
       const bool is_k = hd < a.Hq + a.Hk;
       const int kvh = is_k ? hd - a.Hq : hd - a.Hq - a.Hk;
       store4((is_k ? a.k_cache : a.v_cache) + (slot + static_cast<int64_t>(kvh) * a.max_seq) * a.d + 2 * p0, r.x, r.y,
@@ -597,7 +599,8 @@ __global__ void __launch_bounds__(128) rope_cache_tok_kernel(RopeCacheArgs a, Ew
     }
     const bool is_k = hd < a.Hq + a.Hk;
     const int kvh = is_k ? hd - a.Hq : hd - a.Hq - a.Hk;
-    dst = (is_k ? a.k_cache : a.v_cache) + ((static_cast<int64_t>(s) * a.Hk + kvh) * a.max_seq + cpos) * a.d + e;
+    if (cpos >= 0 && cpos < a.max_seq)   // past the capacity: dropped (include/dl.h)
+      dst = (is_k ? a.k_cache : a.v_cache) + ((static_cast<int64_t>(s) * a.Hk + kvh) * a.max_seq + cpos) * a.d + e;
   }
   pdl_wait();
   ew_mark(tr, 2);
@@ -612,7 +615,7 @@ __global__ void __launch_bounds__(128) rope_cache_tok_kernel(RopeCacheArgs a, Ew
   }
   if (rot) v = make_float4(v.x * cs0 - v.y * sn0, v.x * sn0 + v.y * cs0, v.z * cs1 - v.w * sn1, v.z * sn1 + v.w * cs1);
   if (hd < a.Hq) store4(a.q_out + t * static_cast<int64_t>(a.Hq) * a.d + col, v.x, v.y, v.z, v.w);
-  else store4(dst, v.x, v.y, v.z, v.w);
+  else if (dst) store4(dst, v.x, v.y, v.z, v.w);
   ew_mark(tr, 3);
 }
 
@@ -730,6 +733,7 @@ __global__ void __launch_bounds__(128) kv_append_kernel(const __nv_bfloat16* __r
   pdl_wait();
   const int64_t t = blockIdx.x;
   const int64_t p = cache_lens[t];
+  if (p < 0 || p / bs >= mbps) return;   // past the block table: dropped (include/dl.h)
   const int64_t slot = static_cast<int64_t>(tables[t * mbps + p / bs]) * bs + p % bs;
   const uint4* src = reinterpret_cast<const uint4*>(zb + t * ldzb + zoff);
   uint4* dst = reinterpret_cast<uint4*>(pool + slot * ld_slot);
@@ -877,7 +881,7 @@ dl_status launch_residual_add_bf16(const __nv_bfloat16* y, int64_t ldy, __nv_bfl
 }
 dl_status launch_silu_mul_f32(float* acc, int64_t lda, __nv_bfloat16* act, int64_t ldo, int64_t T, int64_t m,
                               int clear, cudaStream_t st, const SideZero& z) {
-  static const bool ew4 = getenv("DL_SILU_EW4") != nullptr;   // A/B switch
+  static const bool ew4 = DL_ENV("DL_SILU_EW4") != nullptr;   // A/B switch
   if (!ew4 && clear && m % 8 == 0 && lda % 4 == 0 && ldo % 8 == 0 && T > 0) {
     return launch_silu_flat(acc, lda, act, ldo, T, m, 0, st, z);
   }

@@ -67,7 +67,6 @@ long long dl_launch_count(void) { return g_launches.load(); }
 dl_status dl_debug_gemm_trace(void* device_buf) { return set_gemm_trace(device_buf); }
 dl_status dl_debug_ew_trace(void* device_buf) { return set_ew_trace(device_buf); }
 
-dl_status dl_debug_fused_trace(void* device_buf) { return set_fused_trace(device_buf); }
 
 dl_status dl_profile_begin(int capacity) {
   std::lock_guard<std::mutex> l(g_mu);

@@ -4,9 +4,14 @@
 // Each warp owns ROWS weight rows and streams them from HBM with 16-byte
 // coalesced loads (the factors are read exactly once); the T token vectors
 // ride in registers; the per-row dot products are finished with warp
-// shuffles.  Z stays fp32 (workspace, L2-resident) between the two stages.
+// shuffles.  Z is held in fp32 storage (workspace row, L2-resident, or shared
+// memory) but, for bf16 inputs, rounded to bf16 first -- the same single
+// rounding the tensor-core paths apply (reading c10), so a token's output does
+// not depend on which path the batch size selects.
 // When the whole chain is small (k <= 1024) a single fused CTA keeps Z in
 // shared memory and never writes it out.
+#include <type_traits>
+
 #include "dl_internal.h"
 
 namespace dl {
@@ -121,8 +126,13 @@ __device__ void gemv_warp_rows(const E* __restrict__ W, int64_t ldw, int R, int 
     for (int r = 0; r < kRows; ++r) {
       if (row0 + r >= R) continue;
 #pragma unroll
-      for (int t = 0; t < TT; ++t)
-        if (t < T) store_out(out + t * ldo + row0 + r, acc[r][t], accumulate);
+      for (int t = 0; t < TT; ++t) {
+        float v = acc[r][t];
+        // stage 1 of a bf16 chain (fp32 Z storage): round Z to bf16
+        if constexpr (std::is_same<O, float>::value && std::is_same<E, __nv_bfloat16>::value)
+          v = __bfloat162float(__float2bfloat16_rn(v));
+        if (t < T) store_out(out + t * ldo + row0 + r, v, accumulate);
+      }
     }
   }
 }

@@ -533,9 +533,16 @@ __global__ void __launch_bounds__(kThreads, (SWAP && STAGES <= 4) ? 2 : 1)
           act_load(dst, &full_bar[i], pend_c0[i], pend_c1[i]);
         }
       };
-      int jslot = 0;
+      int jslot = 0, njobs = 0;
       uint32_t jphase = 0;
       auto push = [&](const Job& jb) {
+        // The ring slot frees only when the epilogue has finished the job that
+        // held it, which needs that job's deferred activation loads: issue them
+        // before the first push that may wait (more than kJobRing jobs -- e.g.
+        // single-k-block tiles -- within the first STAGES units would otherwise
+        // deadlock the producer against its own deferred loads).
+        if (!waited && njobs >= kJobRing) flush_pending();
+        ++njobs;
         ptx::mbar_wait(&jempty_bar[jslot], jphase ^ 1);
         jobs[jslot] = jb;
         ptx::mbar_arrive(&jfull_bar[jslot]);
@@ -1170,7 +1177,7 @@ bool make_map(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int64
 // CTAs per SM of the shallow (<= 4-stage) swap-AB configurations: 2 fills the
 // SM; 1 leaves room for the successor's CTA to become resident early (A/B knob)
 int small_per_sm() {
-  static const int v = getenv("DL_DECODE_PER_SM") ? atoi(getenv("DL_DECODE_PER_SM")) : 2;
+  static const int v = DL_ENV("DL_DECODE_PER_SM") ? atoi(DL_ENV("DL_DECODE_PER_SM")) : 2;
   return v == 1 ? 1 : 2;
 }
 
@@ -1252,11 +1259,6 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   a.out = p.out.ptr;
   a.ldo = p.out.ld;
   a.mode = p.out.mode;
-  // debug A/B switches (timing experiments only; results are wrong with NORED)
-  static const bool dbg_tile_order = getenv("DL_DEBUG_SK_TILEORDER") != nullptr;
-  static const bool dbg_nored = getenv("DL_DEBUG_NORED") != nullptr;
-  if (stream_k && dbg_tile_order) a.stream_k = 0;
-  if (stream_k && dbg_nored) a.mode = OUT_F32_STORE;
   a.accumulate = p.out.accumulate;
   a.rope_pos = p.out.rope_pos;
   a.rope_end = static_cast<int>(p.out.rope_end);
@@ -1275,17 +1277,17 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   a.scatter_p = p.out.scatter_p;
   a.slab = p.out.slab;
   a.trace_slot = g_trace_host_on ? g_trace_next++ : -1;
-  static const int wpol = getenv("DL_PAIR_WPOL") ? atoi(getenv("DL_PAIR_WPOL")) : 2;   // A/B: 0 / 1 / 2 (measured best: 2)
+  static const int wpol = DL_ENV("DL_PAIR_WPOL") ? atoi(DL_ENV("DL_PAIR_WPOL")) : 2;   // A/B: 0 / 1 / 2 (measured best: 2)
   a.wpol = wpol;
   a.dp_tiles = tiles;
   a.tail_split = 0;
   a.tail_acc = nullptr;
   a.fixup = FIX_NONE;
-  static const int l2pf = getenv("DL_L2PF") ? atoi(getenv("DL_L2PF")) : kL2Prefetch;
+  static const int l2pf = DL_ENV("DL_L2PF") ? atoi(DL_ENV("DL_L2PF")) : kL2Prefetch;
   a.l2pf = l2pf;
-  static const int acce_release = getenv("DL_ACCE_RELEASE") ? atoi(getenv("DL_ACCE_RELEASE")) : 0;   // A/B switch
+  static const int acce_release = DL_ENV("DL_ACCE_RELEASE") ? atoi(DL_ENV("DL_ACCE_RELEASE")) : 0;   // A/B switch
   a.relaxed_acce = acce_release ? 0 : 1;
-  static const int stage_out = getenv("DL_STAGE_OUT") ? atoi(getenv("DL_STAGE_OUT")) : 3;   // A/B: bit 0 plain, bit 1 accumulate
+  static const int stage_out = DL_ENV("DL_STAGE_OUT") ? atoi(DL_ENV("DL_STAGE_OUT")) : 3;   // A/B: bit 0 plain, bit 1 accumulate
   a.stage_out = stage_out;
   if (p.fix.op != FIX_NONE) {
     bool ok = SWAP && stream_k && p.sched && p.fix.acc32 && p.fix.tile_cnt;
@@ -1310,8 +1312,8 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   }
   a.sched = nullptr;
   if (stream_k && p.sched) {
-    static const double frac = getenv("DL_SK_STATIC") ? atof(getenv("DL_SK_STATIC")) : 0.9;
-    static const int chunk = getenv("DL_SK_CHUNK") ? atoi(getenv("DL_SK_CHUNK")) : 8;
+    static const double frac = DL_ENV("DL_SK_STATIC") ? atof(DL_ENV("DL_SK_STATIC")) : 0.9;
+    static const int chunk = DL_ENV("DL_SK_CHUNK") ? atoi(DL_ENV("DL_SK_CHUNK")) : 8;
     const int cap = num_sms() * ((SWAP && STAGES <= 4) ? small_per_sm() : 1);   // must match the grid below
     const int g = static_cast<int>(units < cap ? (units > 0 ? units : 1) : cap);
     a.sched = p.sched;
@@ -1331,7 +1333,7 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
     const int clusters = sms / 2;
     grid = 2 * (tiles < clusters ? (tiles > 0 ? tiles : 1) : clusters);
     // DP + stream-K tail: a last wave filled to <= 75% is split along K
-    static const bool dpsk = !getenv("DL_PREFILL_DPSK") || atoi(getenv("DL_PREFILL_DPSK")) != 0;
+    static const bool dpsk = !DL_ENV("DL_PREFILL_DPSK") || atoi(DL_ENV("DL_PREFILL_DPSK")) != 0;
     const int full = tiles / clusters, tail = tiles % clusters;
     if (dpsk && p.tail_acc && full >= 1 && tail > 0 && tail * 4 <= clusters * 3) {
       const int split = clusters / tail;
@@ -1410,12 +1412,12 @@ dl_status tc_gemm(const GemmProblem& p, bool stream_k, cudaStream_t st) {
     set_error("stream-K requires a reduction output");
     return DL_ERR_INVALID_ARG;
   }
-  static const int dec_stages = getenv("DL_DECODE_STAGES") ? atoi(getenv("DL_DECODE_STAGES")) : 9;
+  static const int dec_stages = DL_ENV("DL_DECODE_STAGES") ? atoi(DL_ENV("DL_DECODE_STAGES")) : 9;
   if (p.T <= 64) return dec_stages == 4 ? launch_cfg<64, true, 4>(p, stream_k, st)
                                         : launch_cfg<64, true, 9>(p, stream_k, st);
   if (p.T <= 128) return launch_cfg<128, true, 6>(p, stream_k, st);
   if (p.T <= 256) return launch_cfg<256, true, 4>(p, stream_k, st);
-  static const bool pair = !getenv("DL_PREFILL_PAIR") || atoi(getenv("DL_PREFILL_PAIR")) != 0;
+  static const bool pair = !DL_ENV("DL_PREFILL_PAIR") || atoi(DL_ENV("DL_PREFILL_PAIR")) != 0;
   if (pair && !stream_k && p.out.mode == OUT_BF16) return launch_cfg<256, false, 6, true>(p, stream_k, st);
   return launch_cfg<256, false, 4>(p, stream_k, st);
 }

@@ -82,10 +82,12 @@ def test_plan_strict_rejects_uneven(lib):
         lib.dl_tp_plan([3], 4, 0)          # fewer ranks than world
 
 
-def _call_linear(lib, T=4, m=256, n=256, k=64, ldx=256, lda=64, ldb=256, ldy=256, dt=0, X=256, ws=1 << 20):
+def _call_linear(lib, T=4, m=256, n=256, k=64, ldx=256, lda=64, ldb=256, ldy=256, dt=0, X=256, ws=1 << 20,
+                 acc=0, comm=None, reduce=0):
     L = lib.load()
     return L.dl_lowrank_linear(ctypes.c_void_p(X), ldx, ctypes.c_void_p(4096), lda, ctypes.c_void_p(8192), ldb,
-                               ctypes.c_void_p(16384), ldy, T, m, n, k, dt, 0, None, ctypes.c_void_p(65536), ws, None)
+                               ctypes.c_void_p(16384), ldy, T, m, n, k, dt, acc, comm, reduce,
+                               ctypes.c_void_p(65536), ws, None)
 
 
 def test_linear_validation_codes(lib):
@@ -98,6 +100,38 @@ def test_linear_validation_codes(lib):
     assert _call_linear(lib, T=32, dt=0) == 5     # fp32 beyond the SIMT path
     assert _call_linear(lib, ws=16) == 7          # DL_ERR_WORKSPACE
     assert _call_linear(lib, T=0) == 0            # empty input is a no-op
+    assert _call_linear(lib, reduce=3) == 1       # DL_ERR_INVALID_ARG: unknown dl_reduce
+
+
+def test_linear_reduce_validation(lib):
+    """dl_reduce modes (include/dl.h): argument errors are reported before any launch,
+    also on a GPU-less host (loopback communicators need no device)."""
+    c = lib.Comm.loopback(0, 2)
+    h = c.handle
+    assert _call_linear(lib, m=96, ldy=48, comm=h, reduce=2) == 4         # SCATTER: m % (32 * world) != 0
+    assert _call_linear(lib, comm=h, reduce=1, acc=1) == 10               # fp32 Y += with a collective
+    assert _call_linear(lib, comm=h, reduce=2, ldy=130) == 6              # ldy checked against m / P (fp32: 16 B)
+    assert _call_linear(lib, comm=h, reduce=2, ldy=100) == 2              # ldy < m / P
+    assert _call_linear(lib, comm=h, reduce=2, ldy=128, ws=16) == 7       # workspace includes the RS buffer
+    sz = {}
+    for red in (0, 1, 2):
+        b = ctypes.c_size_t()
+        assert lib.load().dl_lowrank_linear_workspace(64, 256, 256, 64, 1, h, red, ctypes.byref(b)) == 0
+        sz[red] = b.value
+    assert sz[2] > sz[1] > 0 and sz[1] >= sz[0]
+    # bf16, T <= 16 with a collective takes the tensor path: its workspace holds the bf16 Z
+    b16, b16n = ctypes.c_size_t(), ctypes.c_size_t()
+    lib.load().dl_lowrank_linear_workspace(8, 256, 256, 64, 1, h, 1, ctypes.byref(b16))
+    lib.load().dl_lowrank_linear_workspace(8, 256, 256, 64, 1, None, 0, ctypes.byref(b16n))
+    assert b16.value > b16n.value
+    c.close()
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the GPU-less failure mode")
+def test_group_comm_needs_gpu(lib):
+    arr = (ctypes.c_void_p * 2)()
+    assert lib.load().dl_comm_create_group(2, 1 << 20, ctypes.cast(arr, ctypes.c_void_p)) == 8   # DL_ERR_CUDA
+    assert lib.load().dl_comm_create_group(9, 1 << 20, ctypes.cast(arr, ctypes.c_void_p)) == 1   # world > 8
 
 
 @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the GPU-less failure mode")

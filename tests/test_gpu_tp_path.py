@@ -1,6 +1,6 @@
 """GPU test of the tensor-parallel code path of dl_decomposed_block_forward on
 a single B200: a 1-rank NCCL communicator (torch ProcessGroupNCCL) and
-DL_FORCE_TP_PATH=1 make the block take the TP branch (bf16 partials laid out
+a communicator (any world) makes the block take the TP branch (bf16 partials laid out
 by head for the reduce-scatter, NCCL ReduceScatter / AllGather / AllReduce,
 un-permute, bf16 finalize kernels).  Results are compared with the fp64 oracle.
 Runs in a subprocess so the env switch and process group stay isolated.
@@ -84,7 +84,7 @@ def test_block_tp_code_path_one_rank_nccl(layout, glu):
     replicated A)."""
     from paper_2604_17709_b200 import build
     build.build()
-    env = dict(os.environ, DL_FORCE_TP_PATH="1")
+    env = dict(os.environ)
     src = (SCRIPT.replace("__ROOT__", repr(ROOT)).replace("__PORT__", repr(str(29533 + 2 * layout + int(glu))))
            .replace("__LAYOUT__", str(layout)).replace("__GLU__", str(glu)))
     r = subprocess.run([sys.executable, "-c", src], capture_output=True, text=True, env=env, timeout=600)
@@ -136,7 +136,7 @@ def test_block_decode_stream_k_fixups(knob):
     from paper_2604_17709_b200 import build
     build.build()
     name, _, val = knob.partition("=")
-    env = dict(os.environ, **{name: val or "1"})
+    env = dict(os.environ, DL_LIBRARY="ab", **{name: val or "1"})
     src = FIXUP_SCRIPT.replace("__ROOT__", repr(ROOT))
     r = subprocess.run([sys.executable, "-c", src], capture_output=True, text=True, env=env, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
