@@ -322,6 +322,17 @@ typedef enum { DL_PREFILL = 0, DL_DECODE = 1 } dl_phase;
  *            UNSUPPORTED (head_dim != 128), WORKSPACE, CUDA, NCCL.       */
 dl_status dl_block_workspace(const dl_block_config *cfg, int world,
                              size_t *bytes);
+/* Bytes of a group communicator's symmetric window (dl_comm_create_group
+ * sym_bytes) that the fused collectives of this config need: with a group
+ * communicator, the rank-parallel decode path (T <= 256) red.adds its
+ * stage-2 partials straight into the ranks' windows (all-reduce into every
+ * rank's copy, reduce-scatter into the owner's) and pushes the attention
+ * output into every rank's all-gather slot, so each collective is a barrier
+ * instead of a pass over the data.  With a smaller window (or another
+ * communicator kind) the same calls run the collective kernels instead.
+ * 0 for DL_LAYOUT_DEINFER (always the collective path). */
+dl_status dl_block_window_bytes(const dl_block_config *cfg, int world,
+                                size_t *bytes);
 dl_status dl_decomposed_block_forward(
     const dl_block_config *cfg, const dl_block_weights *w, void *x, int64_t T,
     const int32_t *positions, const int32_t *cu_seqlens, int32_t num_seqs,

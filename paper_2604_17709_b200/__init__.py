@@ -9,4 +9,5 @@ from ._lib import (DL_BF16, DL_DECODE, DL_F32, DL_LAYOUT_DEINFER, DL_LAYOUT_RANK
                    dl_device_ok, dl_embedding, dl_lowrank_linear, dl_lowrank_linear_workspace, dl_rmsnorm,
                    dl_tp_plan, dl_tp_shard_factors, dl_version, load, make_block_config,
                    dl_launch_count, dl_profile_begin, dl_profile_end, dl_profile_records,
-                   DL_REDUCE_NONE, DL_REDUCE_ALLREDUCE, DL_REDUCE_SCATTER, run_ranks)
+                   DL_REDUCE_NONE, DL_REDUCE_ALLREDUCE, DL_REDUCE_SCATTER, run_ranks,
+                   dl_block_window_bytes)

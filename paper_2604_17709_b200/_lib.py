@@ -29,7 +29,7 @@ EXPORTS = ("dl_last_error", "dl_version", "dl_device_ok", "dl_comm_create", "dl_
            "dl_profile_count", "dl_profile_get", "dl_debug_gemm_trace", "dl_deinfer_shard_factors",
            "dl_kv_prepare", "dl_decomposed_block_forward_kvlr", "dl_comm_create_loopback",
            "dl_decomposed_stack_forward", "dl_debug_ew_trace", "dl_debug_linear_gathered", "dl_argmax",
-           "dl_comm_create_group")
+           "dl_comm_create_group", "dl_block_window_bytes")
 
 
 class DLError(RuntimeError):
@@ -100,6 +100,8 @@ def load():
             lib.dl_tp_plan.argtypes = [P, I, I, I, I, P, P, P]
             lib.dl_tp_shard_factors.argtypes = [I, P, P, P, P, P, P, I64, I, I, I, I, P, I64, P, P, P, P]
             lib.dl_block_workspace.argtypes = [ctypes.POINTER(dl_block_config), I, ctypes.POINTER(ctypes.c_size_t)]
+            lib.dl_block_window_bytes.argtypes = [ctypes.POINTER(dl_block_config), I,
+                                                  ctypes.POINTER(ctypes.c_size_t)]
             lib.dl_decomposed_block_forward.argtypes = [ctypes.POINTER(dl_block_config),
                                                         ctypes.POINTER(dl_block_weights), P, I64, P, P, I32, I,
                                                         P, P, P, I64, P, P, ctypes.c_size_t, P]
@@ -407,6 +409,13 @@ class BlockWeights:
                 grp.seg[i].lda = a.stride(0)
                 grp.seg[i].k = ln
             self.seg_lens[gname] = lens
+
+
+def dl_block_window_bytes(cfg: dl_block_config, world: int = 1) -> int:
+    """Group-window bytes the fused collectives of this config need (include/dl.h)."""
+    b = ctypes.c_size_t()
+    _check(load().dl_block_window_bytes(ctypes.byref(cfg), world, ctypes.byref(b)))
+    return b.value
 
 
 def dl_block_workspace(cfg: dl_block_config, world: int = 1) -> int:

@@ -612,6 +612,24 @@ struct BlockWs {
   int64_t ldz32, ldzb, ldy32;
 };
 
+// Fused collectives of the skinny rank-parallel path (group communicator):
+// three zero-maintained bf16 buffers in every rank's symmetric window, at the
+// same offsets on every rank.  X = reduce-scatter target [T x W] and, later in
+// the block, the gate|up all-reduce [T x 2m]; Y = the o and down all-reduces
+// [T x h]; G = the attention all-gather [P][T][h/P].  Consecutive collectives
+// alternate X / Y, so a rank writes a buffer only after a barrier that every
+// rank reached after consuming (and clearing) that buffer's previous use.
+struct FanBufs {
+  bool on = false;
+  __nv_bfloat16 *X = nullptr, *Y = nullptr, *G = nullptr;
+  int64_t delta[8] = {};
+};
+size_t fan_window_bytes(const BlockDims& d, int64_t Tmax) {
+  const size_t Ts = static_cast<size_t>(std::min<int64_t>(Tmax, 256));
+  const size_t nx = static_cast<size_t>(std::max<int64_t>(d.W, (d.glu ? 2 : 1) * d.m));
+  return rup_sz(Ts * nx * 2) + 2 * rup_sz(Ts * static_cast<size_t>(d.h) * 2);
+}
+
 BlockWs carve_block(Carver& c, const BlockDims& d, int64_t Tmax) {
   BlockWs w{};
   const int64_t Ts = std::min<int64_t>(Tmax, 256);   // skinny path bound
@@ -1018,6 +1036,17 @@ dl_status kvlr_attention(const dl_block_config* cfg, const BlockDims& d, const d
 
 }  // namespace
 
+dl_status dl_block_window_bytes(const dl_block_config* cfg, int world, size_t* bytes) {
+  if (!bytes) {
+    set_error("bytes is NULL");
+    return DL_ERR_INVALID_ARG;
+  }
+  BlockDims d;
+  DL_TRY(block_dims(cfg, world, &d));
+  *bytes = d.layout == DL_LAYOUT_RANK_PARALLEL ? fan_window_bytes(d, std::max<int64_t>(cfg->max_tokens, 1)) : 0;
+  return DL_OK;
+}
+
 dl_status dl_block_workspace(const dl_block_config* cfg, int world, size_t* bytes) {
   if (!bytes) {
     set_error("bytes is NULL");
@@ -1142,6 +1171,36 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   // collective's buffer ws.yr (no fp32 -> bf16 pass before each collective);
   // the kernel that consumes the collective's result clears it
   const bool tpr = tp && skinny && use_zred();
+  // Fused collectives: with a group communicator the skinny
+  // rank-parallel path red.adds its stage-2 partials straight into the ranks'
+  // symmetric windows (all-reduce: every rank's copy; reduce-scatter: the
+  // owner's) and pushes the attention output into every rank's all-gather slot,
+  // so each collective is a barrier, not a pass over the data.
+  FanBufs fan;
+  if (tpr && d.layout == DL_LAYOUT_RANK_PARALLEL &&
+      comm_window_bytes(comm) >= fan_window_bytes(d, cfg->max_tokens)) {
+    fan.on = true;
+    Carver fc(comm_window(comm, comm->rank));
+    const int64_t Ts = std::min<int64_t>(cfg->max_tokens, 256);
+    fan.X = fc.take<__nv_bfloat16>(static_cast<size_t>(Ts) * std::max<int64_t>(d.W, n_gu * d.m));
+    fan.Y = fc.take<__nv_bfloat16>(static_cast<size_t>(Ts) * d.h);
+    fan.G = fc.take<__nv_bfloat16>(static_cast<size_t>(Ts) * d.h);
+    for (int j = 0; j < P; ++j) fan.delta[j] = (comm_window(comm, j) - comm_window(comm, comm->rank)) / 2;
+  }
+  auto fan_all = [&](GemmOut o) {   // all-reduce by fan-out red.add into every rank's copy
+    if (fan.on) {
+      o.fan_n = P;
+      for (int j = 0; j < P; ++j) o.fan_delta[j] = fan.delta[j];
+    }
+    return o;
+  };
+  // the bf16 all-reduce target of the skinny TP path: Y / X of the window, else ws.yr
+  __nv_bfloat16* const arY = fan.on ? fan.Y : ws.yr;
+  __nv_bfloat16* const arX = fan.on ? fan.X : ws.yr;
+  auto all_reduce_bf16 = [&](__nv_bfloat16* buf, int64_t n) -> dl_status {
+    if (fan.on) return comm_barrier(comm, st);   // the epilogues already summed into every copy
+    return coll_all_reduce(comm, buf, static_cast<size_t>(T) * n, kCollBF16, st);
+  };
 
   // ---- q|k|v: one group; partials laid out rank-major by head for the RS ----
   GemmOut qkv_out{};
@@ -1160,6 +1219,10 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
     qkv_out.mode = OUT_BF16_RED;
     qkv_out.ptr = ws.yr;
     qkv_out.ld = NQKV;
+    if (fan.on) {   // reduce-scatter by owner: [T][W] in the owner's window
+      qkv_out.ptr = fan.X;
+      qkv_out = fan_all(qkv_out);
+    }
   }
   // Opt-in (DL_ROPE_FUSE=1): TP = 1 decode with the q|k|v partials as bf16x2
   // in ws.yr and RoPE + cache append done by the stream-K attention kernel
@@ -1299,6 +1362,11 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
       rc.src = ws.yb;
       rc.ld_src = NQKV;
     }
+  } else if (fan.on) {
+    DL_TRY(comm_barrier(comm, st));   // every rank's q|k|v partials are in the owners' windows
+    rc.src = fan.X;
+    rc.ld_src = d.W;
+    rc.zero = zq;
   } else if (tpr) {
     DL_TRY(coll_reduce_scatter(comm, ws.yr, ws.rs, static_cast<size_t>(T) * d.W, kCollBF16, st));
     rc.src = ws.rs;
@@ -1333,14 +1401,28 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   static const bool no_ag3d = DL_ENV("DL_NO_AG3D") != nullptr;   // A/B switch
   if (tp) {
     const int64_t wl = d.Hq_loc * d.d;
-    DL_TRY(coll_all_gather(comm, ws.att, ws.ag, static_cast<size_t>(T) * wl, kCollBF16, st));
+    const __nv_bfloat16* ag = ws.ag;
+    if (fan.on) {
+      // all-gather by push into every rank's slot [rank][T][wl]; the reduce-
+      // scatter buffer X (consumed by RoPE) is cleared on the side
+      SideZero zx;
+      zx.p = fan.X;
+      zx.rows = 1;
+      zx.row_bytes = zx.ld = static_cast<int64_t>(T) * d.W * 2;
+      DL_TRY(launch_fan_copy(ws.att, wl, fan.G + static_cast<int64_t>(comm->rank) * T * wl, fan.delta, P, T, wl, st,
+                             zx));
+      DL_TRY(comm_barrier(comm, st));
+      ag = fan.G;
+    } else {
+      DL_TRY(coll_all_gather(comm, ws.att, ws.ag, static_cast<size_t>(T) * wl, kCollBF16, st));
+    }
     if (skinny && !no_ag3d && wl % 64 == 0) {
       // o's stage-1 TMA reads the rank-major [P][T][wl] all-gather output directly
-      att_in = ws.ag;
+      att_in = ag;
       o_act_p = P;
       o_act_w = wl;
     } else {
-      DL_TRY(launch_unpermute(ws.ag, ws.att_full, P, T, wl, st));
+      DL_TRY(launch_unpermute(ag, ws.att_full, P, T, wl, st));
       att_in = ws.att_full;
     }
   }
@@ -1349,8 +1431,8 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   auto finish_residual = [&](int64_t n, const SideZero& z) -> dl_status {
     if (!tp) return skinny ? launch_residual_add_f32(ws.yf, ws.ldy32, x, d.h, T, n, 1, st, z) : DL_OK;
     if (tpr) {
-      DL_TRY(coll_all_reduce(comm, ws.yr, static_cast<size_t>(T) * n, kCollBF16, st));
-      return launch_residual_add_bf16(ws.yr, n, x, d.h, T, n, st, 1, z);
+      DL_TRY(all_reduce_bf16(arY, n));
+      return launch_residual_add_bf16(arY, n, x, d.h, T, n, st, 1, z);
     }
     if (skinny) DL_TRY(launch_f32_to_bf16(ws.yf, ws.ldy32, ws.yb, n, T, n, 1, st, z));
     DL_TRY(coll_all_reduce(comm, ws.yb, static_cast<size_t>(T) * n, kCollBF16, st));
@@ -1358,7 +1440,7 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   };
   // wide & TP=1: the stage-2 epilogue adds straight into x (fused residual)
   auto resid_out = [&]() -> GemmOut {
-    if (tpr) return out_plain(ws.yr, d.h, OUT_BF16_RED, 0);
+    if (tpr) return fan_all(out_plain(arY, d.h, OUT_BF16_RED, 0));
     if (skinny) return out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0);
     if (!tp) return out_plain(x, d.h, OUT_BF16, 1);
     return out_plain(ws.yb, d.h, OUT_BF16, 0);
@@ -1382,8 +1464,8 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
     DL_TRY(launch_residual_rmsnorm(ws.yf, ws.ldy32, x, mlp_norm, ws.xn, T, d.h, cfg->rms_eps, st, zo, zqkv));
   } else if (tpr && !no_fuse) {
     // TP: all-reduce of the bf16 partials, then residual + MLP pre-norm in one pass
-    DL_TRY(coll_all_reduce(comm, ws.yr, static_cast<size_t>(T) * d.h, kCollBF16, st));
-    DL_TRY(launch_residual_rmsnorm_bf16(ws.yr, d.h, x, mlp_norm, ws.xn, T, d.h, cfg->rms_eps, st, zo));
+    DL_TRY(all_reduce_bf16(arY, d.h));
+    DL_TRY(launch_residual_rmsnorm_bf16(arY, d.h, x, mlp_norm, ws.xn, T, d.h, cfg->rms_eps, st, zo));
   } else {
     if (!fx) DL_TRY(finish_residual(d.h, zo));
     DL_TRY(launch_rmsnorm(x, mlp_norm, ws.xn, T, d.h, cfg->rms_eps, st));
@@ -1401,7 +1483,7 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   // bf16-rounded anyway); halves the reduction and finalize traffic (DL_GU_F32 A/B)
   static const bool gu_f32 = DL_ENV("DL_GU_F32") != nullptr;
   const bool gur = skinny && !tp && use_zred() && !fx_gu && !gu_f32;
-  if (tpr || gur) gu_out = out_plain(ws.yr, ngu, OUT_BF16_RED, 0);
+  if (tpr || gur) gu_out = fan_all(out_plain(arX, ngu, OUT_BF16_RED, 0));
   const GemmFixup fsilu = fixup(fx_gu ? FIX_SILU : FIX_NONE);
   DL_TRY(run_group(w->gu, n_gu, gu_rows, ws.xn, d.h, d.h, T, skinny, ws, gu_out, st, &fsilu, fx ? nullptr : &zg, 1));
   if (fx_gu) {
@@ -1413,9 +1495,9 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
     if (d.glu) DL_TRY(launch_silu_mul_f32(ws.yf, ws.ldy32, ws.act, d.m, T, d.m, 1, st, zg));
     else DL_TRY(launch_relu_f32(ws.yf, ws.ldy32, ws.act, d.m, T, d.m, 1, st, zg));
   } else if (tpr) {
-    DL_TRY(coll_all_reduce(comm, ws.yr, static_cast<size_t>(T) * ngu, kCollBF16, st));
-    if (d.glu) DL_TRY(launch_silu_mul_bf16(ws.yr, ngu, ws.act, d.m, T, d.m, st, 1, zg));
-    else DL_TRY(launch_relu_bf16(ws.yr, ngu, ws.act, d.m, T, d.m, st, 1, zg));
+    DL_TRY(all_reduce_bf16(arX, ngu));
+    if (d.glu) DL_TRY(launch_silu_mul_bf16(arX, ngu, ws.act, d.m, T, d.m, st, 1, zg));
+    else DL_TRY(launch_relu_bf16(arX, ngu, ws.act, d.m, T, d.m, st, 1, zg));
   } else {
     if (skinny) DL_TRY(launch_f32_to_bf16(ws.yf, ws.ldy32, ws.yb, ngu, T, ngu, 1, st, zg));
     if (tp) DL_TRY(coll_all_reduce(comm, ws.yb, static_cast<size_t>(T) * ngu, kCollBF16, st));
@@ -1432,8 +1514,8 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
     return DL_OK;
   }
   if (next_norm && tpr && !no_fuse && d.layout != DL_LAYOUT_DEINFER) {
-    DL_TRY(coll_all_reduce(comm, ws.yr, static_cast<size_t>(T) * d.h, kCollBF16, st));
-    DL_TRY(launch_residual_rmsnorm_bf16(ws.yr, d.h, x, static_cast<const __nv_bfloat16*>(next_norm), ws.xn, T, d.h,
+    DL_TRY(all_reduce_bf16(arY, d.h));
+    DL_TRY(launch_residual_rmsnorm_bf16(arY, d.h, x, static_cast<const __nv_bfloat16*>(next_norm), ws.xn, T, d.h,
                                         cfg->rms_eps, st, zd));
     *next_normed = true;
     return DL_OK;

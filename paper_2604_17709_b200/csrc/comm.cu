@@ -24,7 +24,13 @@
 //             the producer of a collective's input, all ranks meet, then each
 //             stream waits on every rank's event before the collective kernel,
 //             and once more before anyone may overwrite a buffer that a peer
-//             still reads.  Every rank sums in the same order, so all ranks
+//             still reads.  All-reduce is in place and two-shot (reduce-
+//             scatter of slabs, then all-gather), so it needs no scratch; the
+//             group's symmetric window (sym_bytes per rank, one allocation)
+//             belongs to the fused epilogue reductions of the decode path:
+//             stage-2 epilogues red.add their partials straight into every
+//             rank's window (all-reduce) or the owner's (reduce-scatter) and
+//             the collective reduces to comm_barrier().  Every rank sums in the same order, so all ranks
 //             receive bit-identical results (the residual stream stays
 //             replicated exactly, as with NCCL).  A host barrier that is not
 //             met within kBarrierTimeoutS marks the group aborted and every
@@ -55,6 +61,7 @@ struct CommGroup {
   bool aborted = false;
   const void* post[kMaxGroup] = {};
   cudaStream_t post_stream[kMaxGroup] = {};
+  unsigned long long seq[kMaxGroup] = {};   // syncs issued by each rank (same sequence on every rank)
   cudaEvent_t ev[kMaxGroup][2] = {};
   std::atomic<int> refs{0};
 };
@@ -136,6 +143,27 @@ __global__ void __launch_bounds__(256) peer_gather_kernel(PeerPtrs src, uint8_t*
   }
 }
 
+// dst[j * chunk .. min((j + 1) * chunk, total)) = src_j[same range] for every
+// j = blockIdx.y != self (the all-gather half of the two-shot all-reduce)
+template <bool VEC>
+__global__ void __launch_bounds__(256) peer_slab_gather_kernel(PeerPtrs src, uint8_t* __restrict__ dst, size_t chunk,
+                                                               size_t total, int self) {
+  const int j = blockIdx.y;
+  if (j == self) return;
+  const size_t lo = static_cast<size_t>(j) * chunk;
+  if (lo >= total) return;
+  const size_t n = (total - lo < chunk ? total - lo : chunk);
+  const uint8_t* s = static_cast<const uint8_t*>(src.p[j]) + lo;
+  uint8_t* d = dst + lo;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  if constexpr (VEC) {
+    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n / 16; i += stride)
+      reinterpret_cast<uint4*>(d)[i] = __ldcg(reinterpret_cast<const uint4*>(s) + i);
+  } else {
+    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) d[i] = s[i];
+  }
+}
+
 bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 int grid_for(size_t work) {
@@ -190,10 +218,14 @@ dl_status group_barrier(CommGroup* g) {
   return DL_OK;
 }
 
-// record this rank's event `slot` on st, meet every rank, then make st wait
-// for every other rank's event of the same slot
-dl_status group_sync(dl_comm c, int slot, cudaStream_t st) {
+// record this rank's event on st, meet every rank, then make st wait for
+// every other rank's event of the same sync.  Events alternate between two
+// slots per rank: a rank re-records a slot two syncs later, i.e. after it
+// passed the next barrier, which every rank reaches only after issuing its
+// waits on the slot's previous record.
+dl_status group_sync(dl_comm c, cudaStream_t st) {
   CommGroup* g = c->group;
+  const int slot = static_cast<int>(g->seq[c->rank]++ & 1);
   g->post_stream[c->rank] = st;
   DL_TRY_INTERNAL(cuda_status(cudaEventRecord(g->ev[c->rank][slot], st), "group: cudaEventRecord"));
   DL_TRY_INTERNAL(group_barrier(g));
@@ -225,26 +257,32 @@ PeerPtrs posted(const CommGroup* g, size_t byte_off) {
   return p;
 }
 
+// In-place two-shot all-reduce, no scratch: rank r sums slab r of every
+// rank's buffer into its own slab r (only rank r touches slab r in this phase),
+// then copies every other rank's finished slab into its buffer.  The group's
+// symmetric window stays free for the fused epilogue reductions.
 dl_status group_all_reduce(dl_comm c, void* buf, size_t count, int dtype, cudaStream_t st) {
   CommGroup* g = c->group;
   DL_TRY_INTERNAL(group_enter(c, st));
-  const size_t es = coll_esize(dtype);
-  const size_t cap = (g->sym_bytes / es) & ~static_cast<size_t>(7);   // elements per round (16-byte multiple)
-  if (cap == 0) {
-    set_error("group communicator: symmetric scratch of %zu bytes is too small", g->sym_bytes);
-    return DL_ERR_WORKSPACE;
-  }
-  void* scratch = g->sym + static_cast<size_t>(c->rank) * g->sym_bytes;
-  for (size_t off = 0; off < count; off += cap) {
-    const size_t n = std::min(cap, count - off);
-    g->post[c->rank] = static_cast<uint8_t*>(buf) + off * es;
-    DL_TRY_INTERNAL(group_sync(c, 0, st));                 // every rank's input is complete
-    DL_TRY_INTERNAL(launch_reduce(posted(g, 0), g->world, scratch, n, dtype, st));
-    DL_TRY_INTERNAL(group_sync(c, 1, st));                 // nobody reads the inputs any more
-    DL_TRY_INTERNAL(cuda_status(cudaMemcpyAsync(static_cast<uint8_t*>(buf) + off * es, scratch, n * es,
-                                                cudaMemcpyDeviceToDevice, st), "group all-reduce copy"));
-  }
-  return DL_OK;
+  const size_t es = coll_esize(dtype), P = static_cast<size_t>(g->world);
+  const size_t chunk = ((count + P - 1) / P + 7) & ~static_cast<size_t>(7);   // 16-byte multiple slabs
+  const size_t r = static_cast<size_t>(c->rank);
+  const size_t lo = std::min(count, r * chunk), hi = std::min(count, lo + chunk);
+  g->post[c->rank] = buf;
+  DL_TRY_INTERNAL(group_sync(c, st));                     // every rank's input is complete
+  DL_TRY_INTERNAL(launch_reduce(posted(g, lo * es), g->world, static_cast<uint8_t*>(buf) + lo * es, hi - lo, dtype,
+                                st));
+  DL_TRY_INTERNAL(group_sync(c, st));                     // every slab is final
+  const size_t bytes = count * es, cb = chunk * es;
+  bool vec = al16(buf) && cb % 16 == 0 && bytes % 16 == 0;
+  for (int j = 0; j < g->world; ++j) vec = vec && al16(g->post[j]);
+  const dim3 grid(grid_for(vec ? cb / 16 : cb) / g->world + 1, g->world);
+  if (vec) peer_slab_gather_kernel<true><<<grid, 256, 0, st>>>(posted(g, 0), static_cast<uint8_t*>(buf), cb, bytes,
+                                                               c->rank);
+  else peer_slab_gather_kernel<false><<<grid, 256, 0, st>>>(posted(g, 0), static_cast<uint8_t*>(buf), cb, bytes,
+                                                            c->rank);
+  DL_TRY_INTERNAL(launched("group all-reduce gather"));
+  return group_sync(c, st);                               // nobody reads this buffer any more
 }
 
 dl_status group_reduce_scatter(dl_comm c, const void* src, void* dst, size_t recv_count, int dtype,
@@ -252,17 +290,17 @@ dl_status group_reduce_scatter(dl_comm c, const void* src, void* dst, size_t rec
   CommGroup* g = c->group;
   DL_TRY_INTERNAL(group_enter(c, st));
   g->post[c->rank] = src;
-  DL_TRY_INTERNAL(group_sync(c, 0, st));
+  DL_TRY_INTERNAL(group_sync(c, st));
   DL_TRY_INTERNAL(launch_reduce(posted(g, static_cast<size_t>(c->rank) * recv_count * coll_esize(dtype)), g->world,
                                 dst, recv_count, dtype, st));
-  return group_sync(c, 1, st);
+  return group_sync(c, st);
 }
 
 dl_status group_all_gather(dl_comm c, const void* src, void* dst, size_t send_count, int dtype, cudaStream_t st) {
   CommGroup* g = c->group;
   DL_TRY_INTERNAL(group_enter(c, st));
   g->post[c->rank] = src;
-  DL_TRY_INTERNAL(group_sync(c, 0, st));
+  DL_TRY_INTERNAL(group_sync(c, st));
   const size_t bytes = send_count * coll_esize(dtype);
   if (bytes) {
     bool vec = al16(dst) && bytes % 16 == 0;
@@ -272,7 +310,7 @@ dl_status group_all_gather(dl_comm c, const void* src, void* dst, size_t send_co
     else peer_gather_kernel<false><<<grid, 256, 0, st>>>(posted(g, 0), static_cast<uint8_t*>(dst), bytes);
     DL_TRY_INTERNAL(launched("group all-gather"));
   }
-  return group_sync(c, 1, st);
+  return group_sync(c, st);
 }
 
 void group_release(CommGroup* g) {
@@ -286,6 +324,24 @@ void group_release(CommGroup* g) {
 }
 
 }  // namespace
+
+// ---------------------------------------------------------------------------
+// symmetric window of a group communicator (fused epilogue reductions)
+// ---------------------------------------------------------------------------
+size_t comm_window_bytes(dl_comm c) {
+  return (c && c->kind == kCommGroup) ? c->group->sym_bytes : 0;
+}
+uint8_t* comm_window(dl_comm c, int rank) {
+  return c->group->sym + static_cast<size_t>(rank) * c->group->sym_bytes;
+}
+dl_status comm_barrier(dl_comm c, cudaStream_t st) {
+  if (c->kind != kCommGroup) {
+    set_error("comm_barrier: only group communicators have a device-visible window");
+    return DL_ERR_UNSUPPORTED;
+  }
+  DL_TRY_INTERNAL(group_enter(c, st));
+  return group_sync(c, st);
+}
 
 // ---------------------------------------------------------------------------
 // collectives used by api.cu
@@ -376,6 +432,8 @@ dl_status dl_comm_create_group(int world, size_t sym_bytes, dl_comm* comms) {
   g->sym_bytes = (sym_bytes + 255) & ~static_cast<size_t>(255);
   cudaError_t e = cudaGetDevice(&g->device);
   if (e == cudaSuccess) e = cudaMalloc(&g->sym, g->sym_bytes * world);
+  if (e == cudaSuccess) e = cudaMemset(g->sym, 0, g->sym_bytes * world);   // window buffers are zero-maintained
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
   for (int j = 0; j < world && e == cudaSuccess; ++j)
     for (int s = 0; s < 2 && e == cudaSuccess; ++s)
       e = cudaEventCreateWithFlags(&g->ev[j][s], cudaEventDisableTiming);

@@ -60,6 +60,12 @@ dl_status coll_all_reduce(dl_comm c, void* buf, size_t count, int dtype, cudaStr
 dl_status coll_reduce_scatter(dl_comm c, const void* src, void* dst, size_t recv_count, int dtype,
                               cudaStream_t st);
 dl_status coll_all_gather(dl_comm c, const void* src, void* dst, size_t send_count, int dtype, cudaStream_t st);
+// group communicator symmetric window (comm.cu): per-rank bytes (0: the
+// communicator has none), rank j's window base, and the barrier that orders
+// every rank's preceding stream work before every rank's following work.
+size_t comm_window_bytes(dl_comm c);
+uint8_t* comm_window(dl_comm c, int rank);
+dl_status comm_barrier(dl_comm c, cudaStream_t st);
 
 constexpr int kNumSMsB200 = 148;
 int num_sms();
@@ -192,6 +198,13 @@ struct GemmOut {
   const int32_t* rope_pos;
   int64_t rope_end;
   float rope_theta;
+  // fused collective (swap-AB OUT_BF16_RED only): fan_n > 0 -> the bf16x2
+  // partials are red.add-ed into other ranks' buffers (group window, same
+  // offset in every window; fan_delta[j] = element offset from ptr to rank j's
+  // copy).  scatter_p > 0 (reduce-scatter): only the owner's buffer, laid out
+  // [T][slab] (element tok * slab + col); else all fan_n copies (all-reduce).
+  int fan_n;
+  int64_t fan_delta[8];
 };
 
 struct GemmProblem {
@@ -304,6 +317,10 @@ dl_status launch_argmax(const __nv_bfloat16* logits, int64_t T, int64_t vloc, in
 dl_status launch_embedding(const __nv_bfloat16* table, int64_t vocab, int64_t h,
                            const int32_t* ids, int64_t T, __nv_bfloat16* out,
                            cudaStream_t st);
+// all-gather by push (fused collective): src [T x w] (ld_src) -> dst + delta[j]
+// + t * w for j < P (dst = this rank's slot of its own window); `z` side clear
+dl_status launch_fan_copy(const __nv_bfloat16* src, int64_t ld_src, __nv_bfloat16* dst, const int64_t* delta,
+                          int P, int64_t T, int64_t w, cudaStream_t st, const SideZero& z = SideZero{});
 // [P][T][w] -> [T][P*w]
 dl_status launch_unpermute(const __nv_bfloat16* src, __nv_bfloat16* dst,
                            int P, int64_t T, int64_t w, cudaStream_t st);

@@ -698,6 +698,26 @@ __global__ void __launch_bounds__(128) unpermute_kernel(const __nv_bfloat16* __r
 // rank, balanced split) -> the group's Z layout zb [T x width] (segment s at
 // columns [zoff_s, zoff_s + rup(len_s, 64)), zero padded).
 // grid (ceil(width / 256), T), one column per thread.
+// All-gather by push into the ranks' symmetric windows (fused collective):
+// row t of src [T x w] goes to dst + delta[j] + t * w (dst already offset to
+// this rank's slot [rank][T][w]) for every rank j < P.  grid (ceil(w/8/128), T).
+struct FanDeltas {
+  long long d[8];
+};
+__global__ void __launch_bounds__(128) fan_copy_kernel(const __nv_bfloat16* __restrict__ src, int64_t ld_src,
+                                                       __nv_bfloat16* dst, FanDeltas dl, int P, int w8,
+                                                       SideZero z) {
+  pdl_trigger();
+  pdl_wait();
+  side_zero(z);
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= w8) return;
+  const int64_t t = blockIdx.y;
+  const uint4 v = *reinterpret_cast<const uint4*>(src + t * ld_src + c * 8);
+  for (int j = 0; j < P; ++j)
+    *reinterpret_cast<uint4*>(dst + dl.d[j] + t * static_cast<int64_t>(w8) * 8 + c * 8) = v;
+}
+
 __global__ void __launch_bounds__(256) latent_unpermute_kernel(const __nv_bfloat16* __restrict__ recv,
                                                                __nv_bfloat16* __restrict__ zb, int64_t ldzb,
                                                                LatentMap mp, SideZero z) {
@@ -939,6 +959,19 @@ dl_status launch_unpermute(const __nv_bfloat16* src, __nv_bfloat16* dst, int P, 
   const int w8 = static_cast<int>(w / 8);
   dim3 grid((w8 + 127) / 128, static_cast<unsigned>(T), static_cast<unsigned>(P));
   return launch_pdl(unpermute_kernel, grid, dim3(128), 0, st, "unpermute", src, dst, P, T, w8);
+}
+dl_status launch_fan_copy(const __nv_bfloat16* src, int64_t ld_src, __nv_bfloat16* dst, const int64_t* delta,
+                          int P, int64_t T, int64_t w, cudaStream_t st, const SideZero& z) {
+  if (T <= 0 || w <= 0) return DL_OK;
+  if (w % 8 || ld_src % 8 || P < 1 || P > 8) {
+    set_error("fan_copy: w and ld must be multiples of 8, 1 <= P <= 8");
+    return DL_ERR_UNSUPPORTED;
+  }
+  FanDeltas dl{};
+  for (int j = 0; j < P; ++j) dl.d[j] = delta[j];
+  const int w8 = static_cast<int>(w / 8);
+  dim3 grid((w8 + 127) / 128, static_cast<unsigned>(T));
+  return launch_pdl(fan_copy_kernel, grid, dim3(128), 0, st, "fan_copy", src, ld_src, dst, dl, P, w8, z);
 }
 dl_status launch_copy2d(const void* src, int64_t lds, void* dst, int64_t ldd, int64_t rows, int64_t cols_bytes,
                         cudaStream_t st) {

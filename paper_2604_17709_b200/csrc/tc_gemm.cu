@@ -108,6 +108,9 @@ struct KArgs {
   const int32_t* rope_pos;
   int rope_end;
   float rope_l2t;
+  // fused collective targets (GemmOut::fan_n / fan_delta)
+  int fan_n;
+  long long fan_delta[8];
 };
 
 // RoPE of 8 consecutive output features f..f+7 (4 pairs (2i, 2i+1) of a
@@ -686,10 +689,25 @@ __global__ void __launch_bounds__(kThreads, (SWAP && STAGES <= 4) ? 2 : 1)
               // plain rows: stride ldo; reduce-scatter slabs [P][T][slab]: stride slab (rows per
               // rank and slab offsets are even, so columns fe, fe + 1 stay adjacent)
               const long long tstr = a.scatter_p <= 0 ? a.ldo : a.slab;
-              __nv_bfloat16* p = static_cast<__nv_bfloat16*>(a.out) + out_index(a, s, tok0 + t0, fe);
+              if (a.fan_n > 0 && a.scatter_p > 0) {
+                // fused reduce-scatter: the owner's [T][slab] buffer in its window
+                const long long loc = fe - s.feat_begin, owner = loc / s.rpr;
+                __nv_bfloat16* p = static_cast<__nv_bfloat16*>(a.out) + a.fan_delta[owner] +
+                                   static_cast<long long>(tok0 + t0) * a.slab + s.slab_off + loc % s.rpr;
 #pragma unroll
-              for (int i = 0; i < 16; ++i, p += tstr)
-                if (t0 + i < ntok) ptx::red_add_bf16x2(p, pk[i]);
+                for (int i = 0; i < 16; ++i, p += tstr)
+                  if (t0 + i < ntok) ptx::red_add_bf16x2(p, pk[i]);
+              } else {
+                __nv_bfloat16* p0 = static_cast<__nv_bfloat16*>(a.out) + out_index(a, s, tok0 + t0, fe);
+                // fused all-reduce: the same element of every rank's copy (fan_n == 0: own buffer)
+                const int nd = a.fan_n > 0 ? a.fan_n : 1;
+                for (int dj = 0; dj < nd; ++dj) {
+                  __nv_bfloat16* p = p0 + (a.fan_n > 0 ? a.fan_delta[dj] : 0);
+#pragma unroll
+                  for (int i = 0; i < 16; ++i, p += tstr)
+                    if (t0 + i < ntok) ptx::red_add_bf16x2(p, pk[i]);
+                }
+              }
             }
           } else if (f < s.write_end && ntok > 0) {
             const bool fx = a.fixup != FIX_NONE;
@@ -1276,6 +1294,15 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   }
   a.scatter_p = p.out.scatter_p;
   a.slab = p.out.slab;
+  a.fan_n = 0;
+  if (p.out.fan_n > 0) {
+    if (!SWAP || PAIR || !stream_k || p.out.mode != OUT_BF16_RED || p.fix.op != FIX_NONE || p.out.fan_n > 8) {
+      set_error("tc_gemm: fused collective outputs need the swap-AB stream-K bf16 reduction path");
+      return DL_ERR_INVALID_ARG;
+    }
+    a.fan_n = p.out.fan_n;
+    for (int j = 0; j < 8; ++j) a.fan_delta[j] = j < p.out.fan_n ? p.out.fan_delta[j] : 0;
+  }
   a.trace_slot = g_trace_host_on ? g_trace_next++ : -1;
   static const int wpol = DL_ENV("DL_PAIR_WPOL") ? atoi(DL_ENV("DL_PAIR_WPOL")) : 2;   // A/B: 0 / 1 / 2 (measured best: 2)
   a.wpol = wpol;

@@ -41,6 +41,17 @@ def group(dl, P, sym=8 << 20):
     return dl.Comm.group(P, sym)
 
 
+def test_window_bytes_query(dl):
+    """dl_block_window_bytes: rank-parallel configs need X + Y + G in the window; 0 for DeInfer."""
+    s = SHAPE
+    rk = block_ranks(s, 0.4)
+    cfg = dl.make_block_config(s, rk, max_tokens=64, max_seqs=64)
+    W = (s.h + 2 * s.h_kv) // 4
+    exp = 64 * max(W, 2 * s.m) * 2 + 2 * 64 * s.h * 2
+    assert dl.dl_block_window_bytes(cfg, 4) == exp
+    assert dl.dl_block_window_bytes(dl.make_block_config(s, rk, 64, 64, layout=1), 4) == 0
+
+
 def same_stream(layout, a, b):
     """Rank-parallel: every rank adds the same all-reduced bytes -> bit-identical
     residual streams.  DeInfer: the replicated second-sub-layer up-projection runs
@@ -176,10 +187,12 @@ def block_case():
     return s, rk, w, w2
 
 
-def _run_block(dl, s, rk, w, layout, P, mode, T=None, lens=None, w2=None):
+def _run_block(dl, s, rk, w, layout, P, mode, T=None, lens=None, w2=None, window=8 << 20):
     """Runs one block (or a 2-block stack) on P group ranks; returns per-rank
-    (x_out, k_cache, v_cache) on the host."""
-    comms = group(dl, P)
+    (x_out, k_cache, v_cache) on the host.  window: the group's symmetric window;
+    a window >= dl_block_window_bytes selects the fused epilogue collectives of
+    the skinny rank-parallel path, a smaller one the collective kernels."""
+    comms = group(dl, P, window)
     hk = s.n_kv_heads // P
 
     def body(r, st):
@@ -225,15 +238,17 @@ def _run_block(dl, s, rk, w, layout, P, mode, T=None, lens=None, w2=None):
     return res
 
 
-@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("layout,fused", [(0, True), (0, False), (1, False)])
 @pytest.mark.parametrize("P", [2, 4, 8])
 @pytest.mark.parametrize("T", [40, 300])
-def test_block_prefill_multirank(dl, orc, block_case, layout, P, T):
+def test_block_prefill_multirank(dl, orc, block_case, layout, fused, P, T):
     """Prefill (skinny stream-K path at T = 40, whole-tile path at T = 300) with P
     ranks: RS slabs of every owner, attention all-gather, AR sums (rank-parallel) /
     latent all-gather + latent all-reduce (DeInfer); K/V of each rank's heads."""
+    if T > 256 and fused:
+        pytest.skip("the wide prefill path always uses the collective kernels")
     s, rk, w, _ = block_case
-    res = _run_block(dl, s, rk, w, layout, P, "prefill", T=T)
+    res = _run_block(dl, s, rk, w, layout, P, "prefill", T=T, window=(8 << 20) if fused else 256)
     x = gen_normal((T, s.h), 1.0, 500 + T, dtype=torch.bfloat16)
     ref, kref, vref = orc.block_prefill(_ocfg(orc, s, rk, layout), w, x, np.arange(T), [0, T], world=P)
     d0 = ref - x.double().numpy()
@@ -248,13 +263,15 @@ def test_block_prefill_multirank(dl, orc, block_case, layout, P, T):
         assert rel(vr, vref[:, r * hk * dd:(r + 1) * hk * dd]) <= TOL_BF16
 
 
-@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("layout,fused", [(0, True), (0, False), (1, False)])
 @pytest.mark.parametrize("P", [2, 4, 8])
-def test_block_decode_multirank(dl, orc, block_case, layout, P):
-    """Decode of 8 sequences with mixed cache lengths (empty included), called twice."""
+def test_block_decode_multirank(dl, orc, block_case, layout, fused, P):
+    """Decode of 8 sequences with mixed cache lengths (empty included), called twice
+    (the window / collective buffers must be left zeroed).  fused: the rank-parallel
+    stage-2 epilogues reduce straight into the ranks' windows."""
     s, rk, w, _ = block_case
     lens = [5, 0, 17, 3, 9, 1, 30, 12]
-    res = _run_block(dl, s, rk, w, layout, P, "decode", lens=lens)
+    res = _run_block(dl, s, rk, w, layout, P, "decode", lens=lens, window=(8 << 20) if fused else 256)
     S, L = len(lens), max(lens) + 1
     x = gen_normal((S, s.h), 1.0, 600, dtype=torch.bfloat16)
     kf = gen_normal((S, s.n_kv_heads, L, s.head_dim), 1.0, 601, dtype=torch.bfloat16)
@@ -275,13 +292,13 @@ def test_block_decode_multirank(dl, orc, block_case, layout, P):
         assert rel(vnew, vn[:, r * hk * dd:(r + 1) * hk * dd]) <= TOL_BF16
 
 
-@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("layout,fused", [(0, True), (0, False), (1, False)])
 @pytest.mark.parametrize("P", [2, 8])
-def test_stack_decode_multirank(dl, orc, block_case, layout, P):
+def test_stack_decode_multirank(dl, orc, block_case, layout, fused, P):
     """Two-block stack (cross-block residual + norm fusion after the last all-reduce)."""
     s, rk, w, w2 = block_case
     lens = [4, 11, 0, 7]
-    res = _run_block(dl, s, rk, w, layout, P, "stack", lens=lens, w2=w2)
+    res = _run_block(dl, s, rk, w, layout, P, "stack", lens=lens, w2=w2, window=(8 << 20) if fused else 256)
     S, L = len(lens), max(lens) + 1
     x = gen_normal((S, s.h), 1.0, 600, dtype=torch.bfloat16)
     kf = gen_normal((S, s.n_kv_heads, L, s.head_dim), 1.0, 601, dtype=torch.bfloat16)
