@@ -72,10 +72,15 @@ def collective_census(shape, ranks, n_layers, world, args):
         return {"count_per_step": 0, "payload_mb_per_step": 0.0}
     if args.layout == "rp":
         per_tok = (shape.h + 2 * shape.h_kv) + shape.h + shape.h + 2 * shape.m + shape.h
+        ar = shape.h + 2 * shape.m + shape.h          # all-reduced elements (cost 2n on a ring)
+        n_coll = 5
     else:
         per_tok = (ranks["q"] + ranks["k"] + ranks["v"]) + ranks["o"] + (ranks["gate"] + ranks["up"]) + ranks["down"]
+        ar = ranks["o"] + ranks["down"]
+        n_coll = 4
     payload = (per_tok * n_layers + shape.vocab) * args.batch * 2
-    return {"count_per_step": 4 * n_layers + (n_layers if args.layout == "rp" else 0) + 1,
+    return {"count_per_step": n_coll * n_layers + 1, "collectives_per_layer": n_coll,
+            "units_per_token_layer_nvls": per_tok, "units_per_token_layer_ring": per_tok + ar,
             "payload_mb_per_step": payload / 1e6, "layout": args.layout}
 
 

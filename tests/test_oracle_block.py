@@ -350,6 +350,23 @@ def test_census_table1(orc):
     assert round(100 * (1 - c["deinfer_block_printed"] / c["unopt_block"])) == g["printed_saving_percent"]
 
 
+def test_census_build_collectives(orc):
+    """This build's collective volume (165,888 ring units, 5 collectives),
+    and bench.py's own census (which reports it without importing oracle/) agrees."""
+    g = golden("build_census.json")
+    c = orc.census(**g["inputs"])
+    for key, val in g["expected"].items():
+        assert c[key] == val, key
+    import argparse
+    import bench
+    from synthetic import LLAMA3_70B, block_ranks
+    args = argparse.Namespace(layout="rp", batch=1)
+    bc = bench.collective_census(LLAMA3_70B, block_ranks(LLAMA3_70B, 0.4), 1, 8, args)
+    assert bc["units_per_token_layer_nvls"] == g["nvls_units_per_token"]
+    assert bc["units_per_token_layer_ring"] == c["build_block"]
+    assert bc["collectives_per_layer"] == c["build_collectives"]
+
+
 # ---- low-rank KV cache (N3: P:111, P:219-237) ---------------------------------------
 def test_lowrank_kv_decode_equals_prefill(orc):
     """Decoding token L with the LATENT cache z_k = B_k a_j, z_v = B_v a_j of tokens j < L
