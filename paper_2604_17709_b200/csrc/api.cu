@@ -1187,7 +1187,22 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
     fan.G = fc.take<__nv_bfloat16>(static_cast<size_t>(Ts) * d.h);
     for (int j = 0; j < P; ++j) fan.delta[j] = (comm_window(comm, j) - comm_window(comm, comm->rank)) / 2;
   }
-  auto fan_all = [&](GemmOut o) {   // all-reduce by fan-out red.add into every rank's copy
+  // Two-shot all-reduce fused into the epilogue: the columns of an all-reduced
+  // output are split into P slabs; the stage-2 epilogue red.adds each partial
+  // into the slab owner's copy only (reduce-scatter, the transfer overlapping
+  // the GEMM), then each owner pushes its finished slab into the others' copies.
+  // Per rank (P-1)/P of the output is sent twice, as in a ring / two-shot
+  // all-reduce (a one-shot fan-out into all P copies would send P-1 times it).
+  auto ar_slab = [&](int64_t n) { return rup((n + P - 1) / P, 8); };
+  auto fan_ar = [&](GemmOut o, int64_t n) {
+    if (fan.on) {
+      o.fan_n = P;
+      o.fan_cols = ar_slab(n);
+      for (int j = 0; j < P; ++j) o.fan_delta[j] = fan.delta[j];
+    }
+    return o;
+  };
+  auto fan_all = [&](GemmOut o) {   // reduce-scatter by owner (scatter layout)
     if (fan.on) {
       o.fan_n = P;
       for (int j = 0; j < P; ++j) o.fan_delta[j] = fan.delta[j];
@@ -1198,8 +1213,11 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   __nv_bfloat16* const arY = fan.on ? fan.Y : ws.yr;
   __nv_bfloat16* const arX = fan.on ? fan.X : ws.yr;
   auto all_reduce_bf16 = [&](__nv_bfloat16* buf, int64_t n) -> dl_status {
-    if (fan.on) return comm_barrier(comm, st);   // the epilogues already summed into every copy
-    return coll_all_reduce(comm, buf, static_cast<size_t>(T) * n, kCollBF16, st);
+    if (!fan.on) return coll_all_reduce(comm, buf, static_cast<size_t>(T) * n, kCollBF16, st);
+    DL_TRY(comm_barrier(comm, st));               // every slab holds the sum of all partials
+    const int64_t sl = ar_slab(n), c0 = std::min<int64_t>(n, comm->rank * sl), c1 = std::min<int64_t>(n, c0 + sl);
+    DL_TRY(launch_fan_push(buf, n, T, c0, c1, fan.delta, P, comm->rank, st));
+    return comm_barrier(comm, st);                // every copy holds every slab
   };
 
   // ---- q|k|v: one group; partials laid out rank-major by head for the RS ----
@@ -1440,7 +1458,7 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   };
   // wide & TP=1: the stage-2 epilogue adds straight into x (fused residual)
   auto resid_out = [&]() -> GemmOut {
-    if (tpr) return fan_all(out_plain(arY, d.h, OUT_BF16_RED, 0));
+    if (tpr) return fan_ar(out_plain(arY, d.h, OUT_BF16_RED, 0), d.h);
     if (skinny) return out_plain(ws.yf, ws.ldy32, OUT_F32_RED, 0);
     if (!tp) return out_plain(x, d.h, OUT_BF16, 1);
     return out_plain(ws.yb, d.h, OUT_BF16, 0);
@@ -1483,7 +1501,7 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   // bf16-rounded anyway); halves the reduction and finalize traffic (DL_GU_F32 A/B)
   static const bool gu_f32 = DL_ENV("DL_GU_F32") != nullptr;
   const bool gur = skinny && !tp && use_zred() && !fx_gu && !gu_f32;
-  if (tpr || gur) gu_out = fan_all(out_plain(arX, ngu, OUT_BF16_RED, 0));
+  if (tpr || gur) gu_out = fan_ar(out_plain(arX, ngu, OUT_BF16_RED, 0), ngu);
   const GemmFixup fsilu = fixup(fx_gu ? FIX_SILU : FIX_NONE);
   DL_TRY(run_group(w->gu, n_gu, gu_rows, ws.xn, d.h, d.h, T, skinny, ws, gu_out, st, &fsilu, fx ? nullptr : &zg, 1));
   if (fx_gu) {

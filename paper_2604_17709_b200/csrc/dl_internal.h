@@ -202,8 +202,11 @@ struct GemmOut {
   // partials are red.add-ed into other ranks' buffers (group window, same
   // offset in every window; fan_delta[j] = element offset from ptr to rank j's
   // copy).  scatter_p > 0 (reduce-scatter): only the owner's buffer, laid out
-  // [T][slab] (element tok * slab + col); else all fan_n copies (all-reduce).
+  // [T][slab] (element tok * slab + col); else fan_cols > 0: plain layout,
+  // column c goes to the copy of owner c / fan_cols only (the reduce-scatter
+  // half of a two-shot all-reduce); else all fan_n copies (one-shot).
   int fan_n;
+  int64_t fan_cols;
   int64_t fan_delta[8];
 };
 
@@ -321,6 +324,11 @@ dl_status launch_embedding(const __nv_bfloat16* table, int64_t vocab, int64_t h,
 // + t * w for j < P (dst = this rank's slot of its own window); `z` side clear
 dl_status launch_fan_copy(const __nv_bfloat16* src, int64_t ld_src, __nv_bfloat16* dst, const int64_t* delta,
                           int P, int64_t T, int64_t w, cudaStream_t st, const SideZero& z = SideZero{});
+// all-gather half of a fused two-shot all-reduce: this rank's finished columns
+// [c0, c1) of buf [T x ld] (its window) copied into the same place of every
+// other rank's window (buf + delta[j]); `z` side clear
+dl_status launch_fan_push(__nv_bfloat16* buf, int64_t ld, int64_t T, int64_t c0, int64_t c1, const int64_t* delta,
+                          int P, int self, cudaStream_t st, const SideZero& z = SideZero{});
 // [P][T][w] -> [T][P*w]
 dl_status launch_unpermute(const __nv_bfloat16* src, __nv_bfloat16* dst,
                            int P, int64_t T, int64_t w, cudaStream_t st);

@@ -718,6 +718,20 @@ __global__ void __launch_bounds__(128) fan_copy_kernel(const __nv_bfloat16* __re
     *reinterpret_cast<uint4*>(dst + dl.d[j] + t * static_cast<int64_t>(w8) * 8 + c * 8) = v;
 }
 
+// grid (ceil(w8 / 128), T, P): rank blockIdx.z != self receives this rank's
+// columns [c0, c0 + 8 * w8) of row t
+__global__ void __launch_bounds__(128) fan_push_kernel(__nv_bfloat16* buf, int64_t ld, int64_t c0, int w8,
+                                                       FanDeltas dl, int self, SideZero z) {
+  pdl_trigger();
+  pdl_wait();
+  side_zero(z);
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.z;
+  if (c >= w8 || j == self) return;
+  const int64_t off = static_cast<int64_t>(blockIdx.y) * ld + c0 + c * 8;
+  *reinterpret_cast<uint4*>(buf + dl.d[j] + off) = __ldcg(reinterpret_cast<const uint4*>(buf + off));
+}
+
 __global__ void __launch_bounds__(256) latent_unpermute_kernel(const __nv_bfloat16* __restrict__ recv,
                                                                __nv_bfloat16* __restrict__ zb, int64_t ldzb,
                                                                LatentMap mp, SideZero z) {
@@ -972,6 +986,20 @@ dl_status launch_fan_copy(const __nv_bfloat16* src, int64_t ld_src, __nv_bfloat1
   const int w8 = static_cast<int>(w / 8);
   dim3 grid((w8 + 127) / 128, static_cast<unsigned>(T));
   return launch_pdl(fan_copy_kernel, grid, dim3(128), 0, st, "fan_copy", src, ld_src, dst, dl, P, w8, z);
+}
+dl_status launch_fan_push(__nv_bfloat16* buf, int64_t ld, int64_t T, int64_t c0, int64_t c1, const int64_t* delta,
+                          int P, int self, cudaStream_t st, const SideZero& z) {
+  if (T <= 0 || P < 1) return DL_OK;
+  if ((c1 - c0) % 8 || c0 % 8 || ld % 8 || P > 8) {
+    set_error("fan_push: column range and ld must be multiples of 8, P <= 8");
+    return DL_ERR_UNSUPPORTED;
+  }
+  FanDeltas dl{};
+  for (int j = 0; j < P; ++j) dl.d[j] = delta[j];
+  const int w8 = static_cast<int>((c1 - c0) / 8);
+  if (w8 <= 0) return DL_OK;
+  dim3 grid((w8 + 127) / 128, static_cast<unsigned>(T), static_cast<unsigned>(P));
+  return launch_pdl(fan_push_kernel, grid, dim3(128), 0, st, "fan_push", buf, ld, c0, w8, dl, self, z);
 }
 dl_status launch_copy2d(const void* src, int64_t lds, void* dst, int64_t ldd, int64_t rows, int64_t cols_bytes,
                         cudaStream_t st) {

@@ -108,8 +108,9 @@ struct KArgs {
   const int32_t* rope_pos;
   int rope_end;
   float rope_l2t;
-  // fused collective targets (GemmOut::fan_n / fan_delta)
+  // fused collective targets (GemmOut::fan_n / fan_cols / fan_delta)
   int fan_n;
+  long long fan_cols;
   long long fan_delta[8];
 };
 
@@ -699,10 +700,16 @@ __global__ void __launch_bounds__(kThreads, (SWAP && STAGES <= 4) ? 2 : 1)
                   if (t0 + i < ntok) ptx::red_add_bf16x2(p, pk[i]);
               } else {
                 __nv_bfloat16* p0 = static_cast<__nv_bfloat16*>(a.out) + out_index(a, s, tok0 + t0, fe);
-                // fused all-reduce: the same element of every rank's copy (fan_n == 0: own buffer)
-                const int nd = a.fan_n > 0 ? a.fan_n : 1;
+                // fused all-reduce: two-shot (fan_cols > 0: the column owner's copy only, its
+                // finished slab is pushed to the others after a barrier) or one-shot (every
+                // rank's copy); fan_n == 0: own buffer
+                const bool owner_only = a.fan_n > 0 && a.fan_cols > 0;
+                const int nd = a.fan_n > 0 && !owner_only ? a.fan_n : 1;
                 for (int dj = 0; dj < nd; ++dj) {
-                  __nv_bfloat16* p = p0 + (a.fan_n > 0 ? a.fan_delta[dj] : 0);
+                  const long long dlt =
+                      a.fan_n == 0 ? 0
+                      : owner_only ? a.fan_delta[(s.col_off + (fe - s.feat_begin)) / a.fan_cols] : a.fan_delta[dj];
+                  __nv_bfloat16* p = p0 + dlt;
 #pragma unroll
                   for (int i = 0; i < 16; ++i, p += tstr)
                     if (t0 + i < ntok) ptx::red_add_bf16x2(p, pk[i]);
@@ -1300,7 +1307,12 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
       set_error("tc_gemm: fused collective outputs need the swap-AB stream-K bf16 reduction path");
       return DL_ERR_INVALID_ARG;
     }
+    if (p.out.scatter_p == 0 && p.out.fan_cols > 0 && p.out.fan_cols % 2) {
+      set_error("tc_gemm: fused all-reduce slabs must have an even column count");
+      return DL_ERR_INVALID_ARG;
+    }
     a.fan_n = p.out.fan_n;
+    a.fan_cols = p.out.fan_cols;
     for (int j = 0; j < 8; ++j) a.fan_delta[j] = j < p.out.fan_n ? p.out.fan_delta[j] : 0;
   }
   a.trace_slot = g_trace_host_on ? g_trace_next++ : -1;
