@@ -97,6 +97,20 @@ dl_status check_device() { return check_device_sm100(); }
 
 // path of dl_lowrank_linear
 enum LinPath { PATH_SIMT, PATH_SKINNY, PATH_WIDE };
+// Skinny stage 1 -> stage 2 as ONE fused chain launch (tc_gemm_chain).
+// dl_lowrank_linear uses it by default (DL_CHAIN=0: two launches).  Inside the
+// PDL-chained block the two-launch form measured faster (70B@40% decode:
+// 25.8 vs 26.5 ms/step at TP = 1, 9.85 vs 10.1-10.2 ms per rank at TP = 8;
+// DESIGN.md §6), so the block path takes the chain only with DL_CHAIN=1.
+bool use_chain() {
+  static const bool on = !DL_ENV("DL_CHAIN") || atoi(DL_ENV("DL_CHAIN")) != 0;
+  return on;
+}
+bool use_chain_block() {
+  static const bool on = DL_ENV("DL_CHAIN") && atoi(DL_ENV("DL_CHAIN")) != 0;
+  return on;
+}
+
 LinPath lin_path(int64_t T, dl_dtype dt) {
   if (dt == DL_F32 || T <= 16) return PATH_SIMT;
   if (T <= 256) return PATH_SKINNY;
@@ -121,6 +135,7 @@ struct LinWs {
   __nv_bfloat16* zb;   // [T x ldzb] bf16 stage-2 operand (tensor-core paths)
   float* yf;           // [T x ldy32] fp32 rank partial (skinny, or any collective)
   float* yr;           // [T x m/P] fp32 reduce-scatter receive buffer (DL_REDUCE_SCATTER)
+  unsigned int* chain; // fused-chain arrival counters (skinny tensor path)
   int64_t ldz32, ldzb, ldy32;
 };
 
@@ -151,6 +166,7 @@ LinWs carve_lin(Carver& c, int64_t T, int64_t m, int64_t k, const LinPlan& pl, d
   if (pl.tensor) w.zb = c.take<__nv_bfloat16>(static_cast<size_t>(T) * w.ldzb);
   if (pl.path == PATH_SKINNY || pl.coll) w.yf = c.take<float>(static_cast<size_t>(T) * w.ldy32);
   if (pl.coll && reduce == DL_REDUCE_SCATTER) w.yr = c.take<float>(static_cast<size_t>(T) * (m / pl.P));
+  if (pl.tensor) w.chain = c.take<unsigned int>(2);
   return w;
 }
 
@@ -304,12 +320,20 @@ dl_status dl_lowrank_linear(const void* X, int64_t ldx, const void* A, int64_t l
     return launch_f32_to_bf16(res, ldr, Yb, ldy, T, m_out, clear, st);
   };
   if (pl.path == PATH_SKINNY || pl.path == PATH_SIMT) {
-    // stage 1: Zf += X B^T (stream-K, fp32 reduction), bf16 Z, stage 2 partial (stream-K)
-    DL_TRY(cuda_status(cudaMemsetAsync(ws.zf, 0, sizeof(float) * T * ws.ldz32, st), "memset"));
-    DL_TRY(cuda_status(cudaMemsetAsync(ws.yf, 0, sizeof(float) * T * ws.ldy32, st), "memset"));
-    DL_TRY(tc_gemm(one_seg(X, ldx, T, n, B, ldb, k, n, out_plain(ws.zf, ws.ldz32, OUT_F32_RED, 0)), true, st));
-    DL_TRY(launch_f32_to_bf16(ws.zf, ws.ldz32, ws.zb, ws.ldzb, T, rup(k, 4), 1, st));
-    DL_TRY(tc_gemm(one_seg(ws.zb, ws.ldzb, T, k, A, lda, m, k, partial_out(OUT_F32_RED)), true, st));
+    // The fused chain (one launch): stage 1 reduces bf16x2 partials of
+    // Z = X B^T into the zeroed L2-resident bf16 Z (stream-K), stage 2 reduces
+    // the fp32 rank partial Z A^T once every CTA's stage-1 share has landed.
+    // Z, the fp32 partial and the chain counters are zeroed by one memset.
+    uint8_t* z0 = reinterpret_cast<uint8_t*>(ws.zb);
+    DL_TRY(cuda_status(cudaMemsetAsync(z0, 0, static_cast<uint8_t*>(workspace) + cv.off - z0, st), "memset"));
+    GemmProblem p1 = one_seg(X, ldx, T, n, B, ldb, k, n, out_plain(ws.zb, ws.ldzb, OUT_BF16_RED, 0));
+    GemmProblem p2 = one_seg(ws.zb, ws.ldzb, T, k, A, lda, m, k, partial_out(OUT_F32_RED));
+    if (use_chain()) {
+      DL_TRY(tc_gemm_chain(p1, p2, ws.chain, st));
+    } else {
+      DL_TRY(tc_gemm(p1, true, st));
+      DL_TRY(tc_gemm(p2, true, st));
+    }
     return finish();
   }
   // PATH_WIDE: whole-tile, bf16 Z straight from the epilogue
@@ -581,9 +605,13 @@ dl_status block_dims(const dl_block_config* c, int world, BlockDims* d) {
   return DL_OK;
 }
 
-// Stream-K launches rotate over kSchedSlots counter pairs: a launch can only
-// overlap (PDL) with its immediate neighbours, so 4 slots never collide.
-constexpr int kSchedSlots = 4;
+// Stream-K launches rotate over kSchedSlots counter pairs.  A kernel touches
+// its pair only after griddepcontrol.wait (transitively: every earlier kernel
+// has completed and its last CTA has reset the pair it used), so reuse is safe
+// at any distance; the rotation is margin.  Small grids let many PDL-launched
+// kernels be resident at once: a dynamic-chunk grab before the wait once stole
+// units of a still-running launch two chain kernels back (fixed in tc_gemm.cu).
+constexpr int kSchedSlots = 8;
 // prefill tail scratch: up to 56 tiles of 256 x 256 fp32 (>= 75% of 74 clusters)
 constexpr size_t kTailBytes = static_cast<size_t>(56) * 256 * 256 * 4;
 // The rotation is per host thread: a stream is driven by one thread, so a
@@ -593,6 +621,11 @@ unsigned int* next_sched(unsigned int* base) {
   static thread_local unsigned slot = 0;
   return base + 2 * (slot++ % kSchedSlots);
 }
+unsigned int* next_chain(unsigned int* base) {
+  static thread_local unsigned slot = 0;
+  return base + 2 * (slot++ % kSchedSlots);
+}
+
 
 struct BlockWs {
   float* zf; float* yf;              // fp32 reduction targets (zero-maintained)
@@ -604,6 +637,7 @@ struct BlockWs {
   void* ask;                         // stream-K decode attention: counters + partial slots
   int64_t ask_items;
   unsigned int* sched;               // kSchedSlots x 2 stream-K work counters
+  unsigned int* chain;               // kSchedSlots x 2 fused-chain arrival counters (tc_gemm_chain)
   unsigned int* tile_cnt;            // stream-K fixup arrival counters (one per output tile)
   float* tail;                       // prefill DP + stream-K tail scratch (zero-maintained)
   size_t tail_bytes;
@@ -658,6 +692,7 @@ BlockWs carve_block(Carver& c, const BlockDims& d, int64_t Tmax) {
   w.ask_items = Tmax * d.Hq_loc;
   w.ask = c.take<float>(attention_sk_workspace(Tmax, static_cast<int>(d.Hq_loc)) / sizeof(float));
   w.sched = c.take<unsigned int>(2 * kSchedSlots);
+  w.chain = c.take<unsigned int>(2 * kSchedSlots);
   w.tile_cnt = c.take<unsigned int>(static_cast<size_t>((d.nmax + d.kmax) / 128 + 64));
   w.tail_bytes = Tmax > 256 ? kTailBytes : 0;
   w.tail = w.tail_bytes ? c.take<float>(w.tail_bytes / sizeof(float)) : nullptr;
@@ -791,11 +826,15 @@ dl_status run_group(const dl_factor_group& grp, int nseg, const int64_t* rows, c
     p1.sched = next_sched(ws.sched);
     p1.act_p = act_p;
     p1.act_w = act_w;
-    DL_TRY(tc_gemm(p1, true, st));
     GemmProblem p2 = stage2(grp, nseg, rows, z, ldz, T, zl, out2);
     p2.sched = next_sched(ws.sched);
     if (fix2 && fix2->op != FIX_NONE) p2.fix = *fix2;
-    DL_TRY(tc_gemm(p2, true, st));
+    if (use_chain_block()) {
+      DL_TRY(tc_gemm_chain(p1, p2, next_chain(ws.chain), st));
+    } else {
+      DL_TRY(tc_gemm(p1, true, st));
+      DL_TRY(tc_gemm(p2, true, st));
+    }
     zero_out->p = z;
     zero_out->ld = ldz * 2;
     zero_out->rows = T;

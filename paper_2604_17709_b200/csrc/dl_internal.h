@@ -236,6 +236,13 @@ struct GemmProblem {
 // Picks the tile configuration (swap-AB for T <= 256, stream-K when the
 // output is fp32-reduced) and launches.  `stream_k` requires OUT_F32_RED.
 dl_status tc_gemm(const GemmProblem& p, bool stream_k, cudaStream_t st);
+// Fused two-stage chain of one factor group in ONE persistent launch (skinny
+// swap-AB stream-K path, T <= 256): p1 = stage 1 (its reduction output is p2's
+// activation), p2 = stage 2.  Stage-2 weight tiles stream while stage 1 is
+// still reducing; stage-2 activation loads wait on the in-kernel arrival
+// counter `chain` (2 zero-initialised uint32, left zeroed; launches that may
+// overlap under PDL must use different pairs).
+dl_status tc_gemm_chain(const GemmProblem& p1, const GemmProblem& p2, unsigned int* chain, cudaStream_t st);
 // debug timeline: when buf != NULL every GEMM CTA writes 8 u64 at buf[cta*8]
 // (globaltimer ns at entry, setup done, first TMA, first stage landed, last
 // MMA issued, epilogue done, exit; and its SM id)

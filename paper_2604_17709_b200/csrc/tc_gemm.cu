@@ -76,12 +76,14 @@ struct KArgs {
   int trace_slot;            // debug timeline slot of this launch (-1: none)
   // hybrid stream-K: CTA c first takes units [c*static_units, (c+1)*static_units),
   // then grabs `chunk`-unit pieces of [dyn_begin, total_units) from sched[0];
-  // sched[1] counts finished CTAs (the last one resets both).  sched == null:
+  // sched[1] counts CTAs done grabbing (the last one resets both).  sched == null:
   // purely static stream-K.
   unsigned int* sched;
   long long static_units, dyn_begin;
   int chunk;
   int l2pf;                  // weight tiles prefetched into L2 before griddepcontrol.wait
+  int chain_pf;              // chain stage 2: units whose weights are staged before the in-kernel wait (DL_CHAIN_PF)
+  int chain_warp;            // chain: stage-1 arrivals per epilogue warp instead of per CTA (DL_CHAIN_WARP)
   int relaxed_acce;
   int stage_out;             // pair kernel: bf16 stores through the shared-memory transpose (bit 0 plain, bit 1 Y +=; DL_STAGE_OUT)          // accumulator-empty arrivals without release semantics (DL_ACCE_RELEASE=1: off)
   int act_w;                 // > 0: 3-D activation map, column c -> (c % act_w, token, c / act_w)
@@ -164,6 +166,7 @@ __device__ __forceinline__ int pieces_in(const KArgs& a, long long lo, long long
 struct Job {
   int seg, feat0, tok0, kb0, kb1;
   int part;   // >= 0: K-split piece of tail tile `part` (fp32 partial into tail_acc)
+  int ph;     // chain kernel: 0 = stage 1, 1 = stage 2
 };
 
 __device__ __forceinline__ long long out_index(const KArgs& a, const KSeg& s, int tok, int f) {
@@ -431,12 +434,206 @@ struct JobIter {
 };
 
 
+// Epilogue of one job (warps 2..9): drain this warp's quarter of TMEM lanes
+// and column half of the accumulator `acc` into the output described by `a`.
+template <int BN, bool SWAP>
+__device__ __forceinline__ void epilogue_job(const KArgs& a, const Job& j, uint32_t tmem_base, int acc, int warp,
+                                             int lane) {
+  const int quarter = warp & 3;              // TMEM lane quarter this warp may access
+  const int half = (warp - 2) >> 2;
+  const int row = quarter * 32 + lane;       // accumulator row (M index)
+  constexpr int HALF_COLS = BN / 2;
+  const KSeg& s = a.seg[j.seg];
+  const bool has_k = j.kb1 > j.kb0;
+#pragma unroll 1
+  for (int c0 = half * HALF_COLS; c0 < (half + 1) * HALF_COLS; c0 += 32) {
+    uint32_t r[32];
+    if (has_k) {
+      ptx::tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + c0, r);
+      ptx::tmem_ld_wait();
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) r[i] = 0u;
+    }
+    if (SWAP) {
+      // row = feature, the 32 columns = consecutive tokens (stride tstride)
+      const int f = j.feat0 + row;
+      const int tok0 = j.tok0 + c0;
+      const int ntok = a.T - tok0;
+      if (a.mode == OUT_BF16_RED && a.fixup == FIX_NONE) {
+        // bf16x2 reductions: the lane pair (even row, odd row) = two
+        // adjacent output columns swaps token halves, so the even lane
+        // adds (row, row + 1) for tokens 0-15 and the odd lane for 16-31
+        const bool odd = lane & 1;
+        const int fe = j.feat0 + (row & ~1);
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float mine_lo = __uint_as_float(r[i]), mine_hi = __uint_as_float(r[i + 16]);
+          const float other = __shfl_xor_sync(0xffffffffu, odd ? mine_lo : mine_hi, 1);
+          float lo = odd ? other : mine_lo, hi = odd ? mine_hi : other;   // (column fe, column fe + 1)
+          if (fe + 1 >= s.write_end) hi = 0.f;
+          const __nv_bfloat162 h2 = __floats2bfloat162_rn(lo, hi);
+          pk[i] = *reinterpret_cast<const uint32_t*>(&h2);
+        }
+        const int t0 = odd ? 16 : 0;
+        if (fe < s.write_end && ntok > t0) {
+          // plain rows: stride ldo; reduce-scatter slabs [P][T][slab]: stride slab (rows per
+          // rank and slab offsets are even, so columns fe, fe + 1 stay adjacent)
+          const long long tstr = a.scatter_p <= 0 ? a.ldo : a.slab;
+          if (a.fan_n > 0 && a.scatter_p > 0) {
+            // fused reduce-scatter: the owner's [T][slab] buffer in its window
+            const long long loc = fe - s.feat_begin, owner = loc / s.rpr;
+            __nv_bfloat16* p = static_cast<__nv_bfloat16*>(a.out) + a.fan_delta[owner] +
+                               static_cast<long long>(tok0 + t0) * a.slab + s.slab_off + loc % s.rpr;
+#pragma unroll
+            for (int i = 0; i < 16; ++i, p += tstr)
+              if (t0 + i < ntok) ptx::red_add_bf16x2(p, pk[i]);
+          } else {
+            __nv_bfloat16* p0 = static_cast<__nv_bfloat16*>(a.out) + out_index(a, s, tok0 + t0, fe);
+            // fused all-reduce: two-shot (fan_cols > 0: the column owner's copy only, its
+            // finished slab is pushed to the others after a barrier) or one-shot (every
+            // rank's copy); fan_n == 0: own buffer
+            const bool owner_only = a.fan_n > 0 && a.fan_cols > 0;
+            const int nd = a.fan_n > 0 && !owner_only ? a.fan_n : 1;
+            for (int dj = 0; dj < nd; ++dj) {
+              const long long dlt =
+                  a.fan_n == 0 ? 0
+                  : owner_only ? a.fan_delta[(s.col_off + (fe - s.feat_begin)) / a.fan_cols] : a.fan_delta[dj];
+              __nv_bfloat16* p = p0 + dlt;
+#pragma unroll
+              for (int i = 0; i < 16; ++i, p += tstr)
+                if (t0 + i < ntok) ptx::red_add_bf16x2(p, pk[i]);
+            }
+          }
+        }
+      } else if (f < s.write_end && ntok > 0) {
+        const bool fx = a.fixup != FIX_NONE;
+        const long long tstride = a.scatter_p <= 0 ? (fx ? a.acc_ld : a.ldo) : a.slab;
+        const long long base = fx ? acc_index(a, s, tok0, f) : out_index(a, s, tok0, f);
+        if (fx || a.mode == OUT_F32_RED) {
+          float* p = (fx ? a.acc32 : static_cast<float*>(a.out)) + base;
+#pragma unroll
+          for (int i = 0; i < 32; ++i, p += tstride)
+            if (i < ntok) ptx::red_add_f32(p, __uint_as_float(r[i]));
+        } else if (a.mode == OUT_F32_STORE) {
+          float* p = static_cast<float*>(a.out) + base;
+#pragma unroll
+          for (int i = 0; i < 32; ++i, p += tstride)
+            if (i < ntok) *p = __uint_as_float(r[i]);
+        } else {
+          __nv_bfloat16* p = static_cast<__nv_bfloat16*>(a.out) + base;
+          const bool accum = a.accumulate != 0;
+#pragma unroll
+          for (int i0 = 0; i0 < 32; i0 += 8) {
+            float old[8];
+            __nv_bfloat16* q = p;
+#pragma unroll
+            for (int i = 0; i < 8; ++i, q += tstride)
+              old[i] = (accum && i0 + i < ntok) ? __bfloat162float(*q) : 0.f;
+#pragma unroll
+            for (int i = 0; i < 8; ++i, p += tstride)
+              if (i0 + i < ntok) *p = __float2bfloat16_rn(__uint_as_float(r[i0 + i]) + old[i]);
+          }
+        }
+      }
+    } else {
+      // row = token, columns = features f0 .. f0+31 (same segment, same owner)
+      const int tok = j.tok0 + row;
+      const int f0 = j.feat0 + c0;
+      if (tok < a.T && f0 < s.write_end) {
+        const long long idx0 = out_index(a, s, tok, f0);
+        const bool full = (f0 + 32 <= s.write_end);
+        if (a.mode == OUT_BF16) {
+          __nv_bfloat16* o = static_cast<__nv_bfloat16*>(a.out) + idx0;
+          if (full && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              float v[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r[q * 8 + e]);
+              rope8(a, rope_pos_of(a, tok), f0 + q * 8, v);
+              if (a.accumulate) {
+                uint4 old = *reinterpret_cast<const uint4*>(o + q * 8);
+                const __nv_bfloat162* ob = reinterpret_cast<const __nv_bfloat162*>(&old);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  float2 f2 = __bfloat1622float2(ob[e]);
+                  v[2 * e] += f2.x;
+                  v[2 * e + 1] += f2.y;
+                }
+              }
+              uint4 pk;
+              __nv_bfloat162* pb = reinterpret_cast<__nv_bfloat162*>(&pk);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) pb[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+              *reinterpret_cast<uint4*>(o + q * 8) = pk;
+            }
+          } else {
+            const int nf = s.write_end - f0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              if (i < nf) {
+                float w = __uint_as_float(r[i]);
+                if (a.accumulate) w += __bfloat162float(o[i]);
+                o[i] = __float2bfloat16_rn(w);
+              }
+            }
+          }
+        } else {
+          float* o = static_cast<float*>(a.out) + idx0;
+          const int nf = s.write_end - f0;
+          if (a.mode == OUT_F32_RED) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4)
+              if (i + 4 <= nf) ptx::red_add_v4_f32(o + i, __uint_as_float(r[i]), __uint_as_float(r[i + 1]),
+                                                   __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+              else
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  if (i + e < nf) ptx::red_add_f32(o + i + e, __uint_as_float(r[i + e]));
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (i < nf) o[i] = __uint_as_float(r[i]);
+          }
+        }
+      }
+    }
+  }
+}
+
+// A {counter, done} pair is reset for the next launch by the last of the
+// grid's CTAs to be finished with c[0]: each calls this once, after its last
+// access to c[0] (release: that access is ordered before the done count).
+// Called by the producer mid-kernel, so no atomic round trip sits on the
+// kernel's exit path (the successor's griddepcontrol.wait waits for it).
+__device__ __forceinline__ void release_pair(unsigned int* c) {
+  unsigned old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(c + 1) : "memory");
+  if (old == gridDim.x - 1) {
+    atomicExch(c, 0u);
+    atomicExch(c + 1, 0u);
+  }
+}
+
 // Shallow (<= 4-stage) swap-AB configurations are register-capped for two
 // CTAs per SM, so a successor GEMM's CTA can become resident (and prefetch
 // its weights) while this one still runs.
-template <int BN, bool SWAP, int STAGES>
+//
+// CHAIN (swap-AB stream-K only): the fused two-stage chain of one factor group
+// in ONE persistent launch (y = A(Bx)).  Phase 0 is stage 1
+// (maps / a: Z = X.B^T, bf16x2 partials reduced into the L2-resident Z
+// buffer), phase 1 is stage 2 (maps2 / a2: Y = Z.A_g^T reading that Z).  The
+// producer streams phase-1 weight tiles into the ring while phase 0 is still
+// being reduced; only their Z halves wait, on a grid-wide arrival counter
+// (chain[0] = CTAs whose phase-0 epilogue has retired, released by each CTA
+// after its last phase-0 red.add) instead of a kernel boundary.  All CTAs are
+// co-resident (one wave), so the in-kernel wait cannot deadlock.
+template <int BN, bool SWAP, int STAGES, bool CHAIN>
 __global__ void __launch_bounds__(kThreads, (SWAP && STAGES <= 4) ? 2 : 1)
-    tc_gemm_kernel(const __grid_constant__ KMaps maps, const __grid_constant__ KArgs a) {
+    tc_gemm_kernel(const __grid_constant__ KMaps maps, const __grid_constant__ KArgs a,
+                   const __grid_constant__ KMaps maps2, const __grid_constant__ KArgs a2, unsigned int* chain) {
   constexpr int P_ROWS = BM;                 // MMA A operand rows
   constexpr int Q_ROWS = BN;                 // MMA B operand rows
   constexpr int P_BYTES = P_ROWS * BK * 2;
@@ -446,6 +643,7 @@ __global__ void __launch_bounds__(kThreads, (SWAP && STAGES <= 4) ? 2 : 1)
   constexpr int TOK_TILE = SWAP ? BN : BM;
   constexpr uint32_t TMEM_COLS = 2 * BN;
   constexpr uint32_t IDESC = ptx::idesc_bf16_f32(BM, BN);
+  constexpr int kPhaseMark = -2;             // job-ring marker: end of phase 0 (CHAIN)
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -461,12 +659,20 @@ __global__ void __launch_bounds__(kThreads, (SWAP && STAGES <= 4) ? 2 : 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  unsigned long long* tr = (g_trace && a.trace_slot >= 0) ? g_trace + (static_cast<long long>(a.trace_slot) * 148 + blockIdx.x) * 8 : nullptr;   // debug timeline
+  // debug timeline (dl_debug_gemm_trace); a chain launch traces its stage 2
+  // in a second slot whose "entry" is the release of the in-kernel wait
+  unsigned long long* tr = (g_trace && a.trace_slot >= 0) ? g_trace + (static_cast<long long>(a.trace_slot) * 148 + blockIdx.x) * 8 : nullptr;
+  unsigned long long* tr2 = (CHAIN && g_trace && a2.trace_slot >= 0) ? g_trace + (static_cast<long long>(a2.trace_slot) * 148 + blockIdx.x) * 8 : nullptr;
   if (tr && threadIdx.x == 0) { tr[0] = gtime(); tr[7] = smid(); }
+  if (tr2 && threadIdx.x == 0) { tr2[1] = gtime(); tr2[7] = smid(); }
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&maps.act);
     for (int g = 0; g < a.nseg; ++g) ptx::prefetch_tmap(&maps.w[g]);
+    if (CHAIN) {
+      ptx::prefetch_tmap(&maps2.act);
+      for (int g = 0; g < a2.nseg; ++g) ptx::prefetch_tmap(&maps2.w[g]);
+    }
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full_bar[s], 1);
       ptx::mbar_init(&empty_bar[s], 1);
@@ -489,7 +695,6 @@ __global__ void __launch_bounds__(kThreads, (SWAP && STAGES <= 4) ? 2 : 1)
   if (tr && threadIdx.x == 0) tr[1] = gtime();
 
   pdl_trigger();   // let the next kernel launch and prefetch its own weights early
-  JobIter it(a, blockIdx.x, gridDim.x);
   Job j;
 
   if (warp == 0) {
@@ -499,97 +704,131 @@ __global__ void __launch_bounds__(kThreads, (SWAP && STAGES <= 4) ? 2 : 1)
       const uint64_t pol_a = ptx::policy_evict_last();    // activations: re-read
       int stage = 0;
       uint32_t phase = 0;
-      // PDL: the static weight tiles of the first STAGES units are requested
-      // before griddepcontrol.wait (they do not depend on the predecessor);
-      // their activation halves follow once the predecessor has completed.
-      int u = 0;
-      bool waited = false;
-      if (tr) tr[2] = gtime();
-      int pend_c0[STAGES], pend_c1[STAGES];
-      // Before waiting on the predecessor, also pull the weight tiles of the
-      // next kL2Prefetch units (beyond the STAGES staged in smem) into L2, so
-      // the dependency gap is spent streaming HBM instead of idling.
-      JobIter pf_it = it;
-      if (a.stream_k && a.sched)
-        pf_it.set_range(blockIdx.x * a.static_units, (blockIdx.x + 1) * a.static_units);
-      auto l2_prefetch = [&]() {
-        int skipped = 0, issued = 0;
-        Job pj;
-        while (issued < a.l2pf && pf_it.next(pj, FEAT_TILE, TOK_TILE)) {
-          const KSeg& ps = a.seg[pj.seg];
-          for (int kb = pj.kb0; kb < pj.kb1 && issued < a.l2pf; ++kb) {
-            if (skipped < STAGES) { ++skipped; continue; }   // these go to smem
-            ptx::tma_prefetch_2d(&maps.w[pj.seg], kb * BK, pj.feat0 - ps.feat_begin);
-            ++issued;
-          }
-        }
-      };
-      auto act_load = [&](void* dst, uint64_t* bar, int c, int tok) {
-        if (a.act_w > 0) ptx::tma_load_3d(dst, &maps.act, bar, c % a.act_w, tok, c / a.act_w, pol_a);
-        else ptx::tma_load_2d(dst, &maps.act, bar, c, tok, pol_a);
-      };
-      auto flush_pending = [&]() {
-        if (SWAP) l2_prefetch();
-        pdl_wait();
-        waited = true;
-        for (int i = 0; i < u && i < STAGES; ++i) {
-          uint8_t* dst = smem + i * STAGE_BYTES + (SWAP ? P_BYTES : 0);
-          act_load(dst, &full_bar[i], pend_c0[i], pend_c1[i]);
-        }
-      };
-      int jslot = 0, njobs = 0;
+      int jslot = 0;
       uint32_t jphase = 0;
-      auto push = [&](const Job& jb) {
-        // The ring slot frees only when the epilogue has finished the job that
-        // held it, which needs that job's deferred activation loads: issue them
-        // before the first push that may wait (more than kJobRing jobs -- e.g.
-        // single-k-block tiles -- within the first STAGES units would otherwise
-        // deadlock the producer against its own deferred loads).
-        if (!waited && njobs >= kJobRing) flush_pending();
-        ++njobs;
-        ptx::mbar_wait(&jempty_bar[jslot], jphase ^ 1);
-        jobs[jslot] = jb;
-        ptx::mbar_arrive(&jfull_bar[jslot]);
-        if (++jslot == kJobRing) { jslot = 0; jphase ^= 1; }
-      };
-      auto emit = [&](const Job& jb) {
-        push(jb);
-        const KSeg& s = a.seg[jb.seg];
-        for (int kb = jb.kb0; kb < jb.kb1; ++kb, ++u) {
-          if (u >= STAGES && !waited) flush_pending();
-          ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-          uint8_t* sp = smem + stage * STAGE_BYTES;
-          uint8_t* sq = sp + P_BYTES;
-          ptx::mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES);
-          const int kx = kb * BK;
-          uint8_t* sw = SWAP ? sp : sq;
-          uint8_t* sa = SWAP ? sq : sp;
-          ptx::tma_load_2d(sw, &maps.w[jb.seg], &full_bar[stage], kx, jb.feat0 - s.feat_begin, pol_w);
-          if (waited) {
-            act_load(sa, &full_bar[stage], s.act_koff + kx, jb.tok0);
-          } else {
-            pend_c0[u] = s.act_koff + kx;
-            pend_c1[u] = jb.tok0;
+      // One phase of work (the whole kernel unless CHAIN).  The static weight
+      // tiles of the phase's first STAGES units are requested before its
+      // dependency wait (phase 0: griddepcontrol.wait on the predecessor kernel;
+      // phase 1: the grid-wide stage-1 arrival counter); their activation
+      // halves follow once the dependency is met.
+      auto run_phase = [&](const KArgs& A, const KMaps& M, int ph) {
+        unsigned long long* tp = ph ? tr2 : tr;
+        if (tp) tp[2] = gtime();
+        JobIter it(A, blockIdx.x, gridDim.x);
+        int u = 0, njobs = 0;
+        bool waited = false;
+        int pend_c0[STAGES], pend_c1[STAGES], pend_st[STAGES];
+        // Before waiting on the predecessor, also pull the weight tiles of the
+        // next kL2Prefetch units (beyond the STAGES staged in smem) into L2, so
+        // the dependency gap is spent streaming HBM instead of idling.
+        JobIter pf_it = it;
+        if (A.stream_k && A.sched)
+          pf_it.set_range(blockIdx.x * A.static_units, (blockIdx.x + 1) * A.static_units);
+        auto l2_prefetch = [&]() {
+          int skipped = 0, issued = 0;
+          Job pj;
+          while (issued < A.l2pf && pf_it.next(pj, FEAT_TILE, TOK_TILE)) {
+            const KSeg& ps = A.seg[pj.seg];
+            for (int kb = pj.kb0; kb < pj.kb1 && issued < A.l2pf; ++kb) {
+              if (skipped < STAGES) { ++skipped; continue; }   // these go to smem
+              ptx::tma_prefetch_2d(&M.w[pj.seg], kb * BK, pj.feat0 - ps.feat_begin);
+              ++issued;
+            }
           }
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        }
-      };
-      if (a.stream_k && a.sched) {
-        it.set_range(blockIdx.x * a.static_units, (blockIdx.x + 1) * a.static_units);
-        while (it.next(j, FEAT_TILE, TOK_TILE)) emit(j);
-        for (;;) {   // dynamic tail: fast SMs take more pieces
-          const long long g = a.dyn_begin + static_cast<long long>(atomicAdd(a.sched, static_cast<unsigned>(a.chunk)));
-          if (g >= a.total_units) break;
-          it.set_range(g, g + a.chunk < a.total_units ? g + a.chunk : a.total_units);
+        };
+        auto act_load = [&](void* dst, uint64_t* bar, int c, int tok) {
+          if (A.act_w > 0) ptx::tma_load_3d(dst, &M.act, bar, c % A.act_w, tok, c / A.act_w, pol_a);
+          else ptx::tma_load_2d(dst, &M.act, bar, c, tok, pol_a);
+        };
+        auto flush_pending = [&]() {
+          if (ph == 0) {
+            if (SWAP) l2_prefetch();
+            pdl_wait();
+          } else {
+            // stage 2 reads Z: every CTA's stage-1 partials must have landed
+            const unsigned need = gridDim.x * (A.chain_warp ? 8u : 1u);
+            for (;;) {
+              unsigned v;
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(chain) : "memory");
+              if (v >= need) break;
+              __nanosleep(32);
+            }
+            // generic-proxy writes (the red.adds) before async-proxy (TMA) reads
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            if (tp) tp[0] = gtime();
+            release_pair(chain);
+          }
+          waited = true;
+          for (int i = 0; i < u && i < STAGES; ++i) {
+            uint8_t* dst = smem + pend_st[i] * STAGE_BYTES + (SWAP ? P_BYTES : 0);
+            act_load(dst, &full_bar[pend_st[i]], pend_c0[i], pend_c1[i]);
+          }
+        };
+        auto push = [&](const Job& jb) {
+          // The ring slot frees only when the epilogue has finished the job that
+          // held it, which needs that job's deferred activation loads: issue them
+          // before the first push that may wait (more than kJobRing jobs -- e.g.
+          // single-k-block tiles -- within the first STAGES units would otherwise
+          // deadlock the producer against its own deferred loads).
+          if (!waited && njobs >= kJobRing) flush_pending();
+          ++njobs;
+          ptx::mbar_wait(&jempty_bar[jslot], jphase ^ 1);
+          jobs[jslot] = jb;
+          ptx::mbar_arrive(&jfull_bar[jslot]);
+          if (++jslot == kJobRing) { jslot = 0; jphase ^= 1; }
+        };
+        auto emit = [&](Job jb) {
+          jb.ph = ph;
+          push(jb);
+          const KSeg& s = A.seg[jb.seg];
+          const int pf_limit = ph && A.chain_pf < STAGES ? A.chain_pf : STAGES;
+          for (int kb = jb.kb0; kb < jb.kb1; ++kb, ++u) {
+            if (u >= pf_limit && !waited) flush_pending();
+            ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+            uint8_t* sp = smem + stage * STAGE_BYTES;
+            uint8_t* sq = sp + P_BYTES;
+            ptx::mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES);
+            const int kx = kb * BK;
+            uint8_t* sw = SWAP ? sp : sq;
+            uint8_t* sa = SWAP ? sq : sp;
+            ptx::tma_load_2d(sw, &M.w[jb.seg], &full_bar[stage], kx, jb.feat0 - s.feat_begin, pol_w);
+            if (waited) {
+              act_load(sa, &full_bar[stage], s.act_koff + kx, jb.tok0);
+            } else {
+              pend_c0[u] = s.act_koff + kx;
+              pend_c1[u] = jb.tok0;
+              pend_st[u] = stage;
+            }
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+        };
+        if (A.stream_k && A.sched) {
+          it.set_range(blockIdx.x * A.static_units, (blockIdx.x + 1) * A.static_units);
+          while (it.next(j, FEAT_TILE, TOK_TILE)) emit(j);
+          for (;;) {   // dynamic tail: fast SMs take more pieces
+            // the counter pairs rotate over launches: touch one only after every
+            // earlier kernel has completed (griddepcontrol.wait is transitive)
+            if (ph == 0 && !waited) flush_pending();
+            const long long g = A.dyn_begin + static_cast<long long>(atomicAdd(A.sched, static_cast<unsigned>(A.chunk)));
+            if (g >= A.total_units) {
+              release_pair(A.sched);
+              break;
+            }
+            it.set_range(g, g + A.chunk < A.total_units ? g + A.chunk : A.total_units);
+            while (it.next(j, FEAT_TILE, TOK_TILE)) emit(j);
+          }
+        } else {
           while (it.next(j, FEAT_TILE, TOK_TILE)) emit(j);
         }
-      } else {
-        while (it.next(j, FEAT_TILE, TOK_TILE)) emit(j);
-      }
-      Job end;
-      end.seg = -1;
-      push(end);
-      if (!waited) flush_pending();
+        Job end;
+        end.seg = (CHAIN && ph == 0) ? kPhaseMark : -1;
+        end.ph = ph;
+        push(end);
+        // phase 1: every CTA passes the chain wait once (it resets the counter)
+        if (!waited && (ph == 0 || u > 0 || CHAIN)) flush_pending();
+      };
+      run_phase(a, maps, 0);
+      if (CHAIN) run_phase(a2, maps2, 1);
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (one thread) =====================
@@ -604,13 +843,18 @@ __global__ void __launch_bounds__(kThreads, (SWAP && STAGES <= 4) ? 2 : 1)
         ptx::mbar_wait(&jfull_bar[jslot], jphase);
         j = jobs[jslot];
         if (++jslot == kJobRing) { jslot = 0; jphase ^= 1; }
+        if (j.seg == kPhaseMark) {
+          if (tr) tr[4] = gtime();
+          continue;
+        }
         if (j.seg < 0) break;
+        unsigned long long* tj = (CHAIN && j.ph) ? tr2 : tr;
         ptx::mbar_wait(&acce_bar[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = j.kb0; kb < j.kb1; ++kb) {
           ptx::mbar_wait(&full_bar[stage], phase);
-          if (tr && tr[3] == 0) tr[3] = gtime();
+          if (tj && tj[3] == 0) tj[3] = gtime();
           ptx::tc_fence_after();
           const uint32_t sp = ptx::smem_u32(smem + stage * STAGE_BYTES);
           const uint32_t sq = sp + P_BYTES;
@@ -627,7 +871,7 @@ __global__ void __launch_bounds__(kThreads, (SWAP && STAGES <= 4) ? 2 : 1)
         ptx::umma_commit(&accf_bar[acc]);        // accumulator ready for the epilogue
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
-      if (tr) tr[4] = gtime();
+      if (CHAIN ? tr2 : tr) (CHAIN ? tr2 : tr)[4] = gtime();
     }
   } else {
     // ===================== epilogue (warps 2..9) =====================
@@ -635,10 +879,6 @@ __global__ void __launch_bounds__(kThreads, (SWAP && STAGES <= 4) ? 2 : 1)
     // one warp hides behind the other; warp e handles TMEM lane quarter
     // (warp & 3) and column half (e / 4) of the accumulator.
     pdl_wait();                                // outputs may alias a predecessor's buffers
-    const int quarter = warp & 3;              // TMEM lane quarter this warp may access
-    const int half = (warp - 2) >> 2;
-    const int row = quarter * 32 + lane;       // accumulator row (M index)
-    constexpr int HALF_COLS = BN / 2;
     int acc = 0;
     uint32_t acc_phase = 0;
     int jslot = 0;
@@ -648,168 +888,31 @@ __global__ void __launch_bounds__(kThreads, (SWAP && STAGES <= 4) ? 2 : 1)
       j = jobs[jslot];
       const int my_slot = jslot;
       if (++jslot == kJobRing) { jslot = 0; jphase ^= 1; }
-      if (j.seg < 0) break;
-      const KSeg& s = a.seg[j.seg];
-      ptx::mbar_wait(&accf_bar[acc], acc_phase);
-      if (tr && warp == 2 && lane == 0) tr[5] = gtime();   // accumulator of this job ready
-      ptx::tc_fence_after();
-      const bool has_k = j.kb1 > j.kb0;
-#pragma unroll 1
-      for (int c0 = half * HALF_COLS; c0 < (half + 1) * HALF_COLS; c0 += 32) {
-        uint32_t r[32];
-        if (has_k) {
-          ptx::tmem_ld32(tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN + c0, r);
-          ptx::tmem_ld_wait();
+      if (j.seg == kPhaseMark) {
+        // every epilogue warp has retired its phase-0 (stage-1) reductions:
+        // publish this CTA's arrival (bar.sync + one thread's release, the
+        // grid-barrier pattern; the fence is cumulative over the CTA's stores)
+        if (a2.chain_warp) {
+          __syncwarp();
+          if (lane == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" :: "l"(chain) : "memory");
         } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) r[i] = 0u;
+          epi_bar();
+          if (threadIdx.x == 64)
+            asm volatile("fence.acq_rel.gpu;\n\tred.release.gpu.global.add.u32 [%0], 1;" :: "l"(chain) : "memory");
         }
-        if (SWAP) {
-          // row = feature, the 32 columns = consecutive tokens (stride tstride)
-          const int f = j.feat0 + row;
-          const int tok0 = j.tok0 + c0;
-          const int ntok = a.T - tok0;
-          if (a.mode == OUT_BF16_RED && a.fixup == FIX_NONE) {
-            // bf16x2 reductions: the lane pair (even row, odd row) = two
-            // adjacent output columns swaps token halves, so the even lane
-            // adds (row, row + 1) for tokens 0-15 and the odd lane for 16-31
-            const bool odd = lane & 1;
-            const int fe = j.feat0 + (row & ~1);
-            uint32_t pk[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const float mine_lo = __uint_as_float(r[i]), mine_hi = __uint_as_float(r[i + 16]);
-              const float other = __shfl_xor_sync(0xffffffffu, odd ? mine_lo : mine_hi, 1);
-              float lo = odd ? other : mine_lo, hi = odd ? mine_hi : other;   // (column fe, column fe + 1)
-              if (fe + 1 >= s.write_end) hi = 0.f;
-              const __nv_bfloat162 h2 = __floats2bfloat162_rn(lo, hi);
-              pk[i] = *reinterpret_cast<const uint32_t*>(&h2);
-            }
-            const int t0 = odd ? 16 : 0;
-            if (fe < s.write_end && ntok > t0) {
-              // plain rows: stride ldo; reduce-scatter slabs [P][T][slab]: stride slab (rows per
-              // rank and slab offsets are even, so columns fe, fe + 1 stay adjacent)
-              const long long tstr = a.scatter_p <= 0 ? a.ldo : a.slab;
-              if (a.fan_n > 0 && a.scatter_p > 0) {
-                // fused reduce-scatter: the owner's [T][slab] buffer in its window
-                const long long loc = fe - s.feat_begin, owner = loc / s.rpr;
-                __nv_bfloat16* p = static_cast<__nv_bfloat16*>(a.out) + a.fan_delta[owner] +
-                                   static_cast<long long>(tok0 + t0) * a.slab + s.slab_off + loc % s.rpr;
-#pragma unroll
-                for (int i = 0; i < 16; ++i, p += tstr)
-                  if (t0 + i < ntok) ptx::red_add_bf16x2(p, pk[i]);
-              } else {
-                __nv_bfloat16* p0 = static_cast<__nv_bfloat16*>(a.out) + out_index(a, s, tok0 + t0, fe);
-                // fused all-reduce: two-shot (fan_cols > 0: the column owner's copy only, its
-                // finished slab is pushed to the others after a barrier) or one-shot (every
-                // rank's copy); fan_n == 0: own buffer
-                const bool owner_only = a.fan_n > 0 && a.fan_cols > 0;
-                const int nd = a.fan_n > 0 && !owner_only ? a.fan_n : 1;
-                for (int dj = 0; dj < nd; ++dj) {
-                  const long long dlt =
-                      a.fan_n == 0 ? 0
-                      : owner_only ? a.fan_delta[(s.col_off + (fe - s.feat_begin)) / a.fan_cols] : a.fan_delta[dj];
-                  __nv_bfloat16* p = p0 + dlt;
-#pragma unroll
-                  for (int i = 0; i < 16; ++i, p += tstr)
-                    if (t0 + i < ntok) ptx::red_add_bf16x2(p, pk[i]);
-                }
-              }
-            }
-          } else if (f < s.write_end && ntok > 0) {
-            const bool fx = a.fixup != FIX_NONE;
-            const long long tstride = a.scatter_p <= 0 ? (fx ? a.acc_ld : a.ldo) : a.slab;
-            const long long base = fx ? acc_index(a, s, tok0, f) : out_index(a, s, tok0, f);
-            if (fx || a.mode == OUT_F32_RED) {
-              float* p = (fx ? a.acc32 : static_cast<float*>(a.out)) + base;
-#pragma unroll
-              for (int i = 0; i < 32; ++i, p += tstride)
-                if (i < ntok) ptx::red_add_f32(p, __uint_as_float(r[i]));
-            } else if (a.mode == OUT_F32_STORE) {
-              float* p = static_cast<float*>(a.out) + base;
-#pragma unroll
-              for (int i = 0; i < 32; ++i, p += tstride)
-                if (i < ntok) *p = __uint_as_float(r[i]);
-            } else {
-              __nv_bfloat16* p = static_cast<__nv_bfloat16*>(a.out) + base;
-              const bool accum = a.accumulate != 0;
-#pragma unroll
-              for (int i0 = 0; i0 < 32; i0 += 8) {
-                float old[8];
-                __nv_bfloat16* q = p;
-#pragma unroll
-                for (int i = 0; i < 8; ++i, q += tstride)
-                  old[i] = (accum && i0 + i < ntok) ? __bfloat162float(*q) : 0.f;
-#pragma unroll
-                for (int i = 0; i < 8; ++i, p += tstride)
-                  if (i0 + i < ntok) *p = __float2bfloat16_rn(__uint_as_float(r[i0 + i]) + old[i]);
-              }
-            }
-          }
-        } else {
-          // row = token, columns = features f0 .. f0+31 (same segment, same owner)
-          const int tok = j.tok0 + row;
-          const int f0 = j.feat0 + c0;
-          if (tok < a.T && f0 < s.write_end) {
-            const long long idx0 = out_index(a, s, tok, f0);
-            const bool full = (f0 + 32 <= s.write_end);
-            if (a.mode == OUT_BF16) {
-              __nv_bfloat16* o = static_cast<__nv_bfloat16*>(a.out) + idx0;
-              if (full && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  float v[8];
-#pragma unroll
-                  for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(r[q * 8 + e]);
-                  rope8(a, rope_pos_of(a, tok), f0 + q * 8, v);
-                  if (a.accumulate) {
-                    uint4 old = *reinterpret_cast<const uint4*>(o + q * 8);
-                    const __nv_bfloat162* ob = reinterpret_cast<const __nv_bfloat162*>(&old);
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                      float2 f2 = __bfloat1622float2(ob[e]);
-                      v[2 * e] += f2.x;
-                      v[2 * e + 1] += f2.y;
-                    }
-                  }
-                  uint4 pk;
-                  __nv_bfloat162* pb = reinterpret_cast<__nv_bfloat162*>(&pk);
-#pragma unroll
-                  for (int e = 0; e < 4; ++e) pb[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
-                  *reinterpret_cast<uint4*>(o + q * 8) = pk;
-                }
-              } else {
-                const int nf = s.write_end - f0;
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                  if (i < nf) {
-                    float w = __uint_as_float(r[i]);
-                    if (a.accumulate) w += __bfloat162float(o[i]);
-                    o[i] = __float2bfloat16_rn(w);
-                  }
-                }
-              }
-            } else {
-              float* o = static_cast<float*>(a.out) + idx0;
-              const int nf = s.write_end - f0;
-              if (a.mode == OUT_F32_RED) {
-#pragma unroll
-                for (int i = 0; i < 32; i += 4)
-                  if (i + 4 <= nf) ptx::red_add_v4_f32(o + i, __uint_as_float(r[i]), __uint_as_float(r[i + 1]),
-                                                       __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
-                  else
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                      if (i + e < nf) ptx::red_add_f32(o + i + e, __uint_as_float(r[i + e]));
-              } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i)
-                  if (i < nf) o[i] = __uint_as_float(r[i]);
-              }
-            }
-          }
-        }
+        if (tr && threadIdx.x == 64) tr[6] = gtime();
+        if (lane == 0) ptx::mbar_arrive(&jempty_bar[my_slot]);
+        continue;
       }
+      if (j.seg < 0) break;
+      ptx::mbar_wait(&accf_bar[acc], acc_phase);
+      if (warp == 2 && lane == 0) {   // accumulator of this job ready
+        unsigned long long* tj = (CHAIN && j.ph) ? tr2 : tr;
+        if (tj) tj[5] = gtime();
+      }
+      ptx::tc_fence_after();
+      if (CHAIN && j.ph) epilogue_job<BN, SWAP>(a2, j, tmem_base, acc, warp, lane);
+      else epilogue_job<BN, SWAP>(a, j, tmem_base, acc, warp, lane);
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -818,24 +921,18 @@ __global__ void __launch_bounds__(kThreads, (SWAP && STAGES <= 4) ? 2 : 1)
         ptx::mbar_arrive(&jempty_bar[my_slot]);
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-      if (SWAP && a.fixup != FIX_NONE) fixup_tile(a, j, threadIdx.x - 64, fix_last);
+      if (SWAP) {
+        if (CHAIN && j.ph) { if (a2.fixup != FIX_NONE) fixup_tile(a2, j, threadIdx.x - 64, fix_last); }
+        else if (a.fixup != FIX_NONE) fixup_tile(a, j, threadIdx.x - 64, fix_last);
+      }
     }
-    if (tr && warp == 2 && lane == 0) tr[6] = gtime();   // epilogue done
+    if (warp == 2 && lane == 0 && (CHAIN ? tr2 : tr)) (CHAIN ? tr2 : tr)[6] = gtime();   // epilogue done
   }
 
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   if (warp == 1) ptx::tmem_dealloc<TMEM_COLS>(tmem_base);
-  if (a.sched && threadIdx.x == 0) {   // last CTA out resets the work counter for reuse
-    __threadfence();
-    if (atomicAdd(a.sched + 1, 1u) == gridDim.x - 1) {
-      atomicExch(a.sched, 0u);
-      atomicExch(a.sched + 1, 0u);
-      __threadfence();
-    }
-  }
-
 }
 
 
@@ -849,7 +946,8 @@ __global__ void __launch_bounds__(kThreads, (SWAP && STAGES <= 4) ? 2 : 1)
 // ---------------------------------------------------------------------------
 template <int STAGES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    tc_gemm_pair_kernel(const __grid_constant__ KMaps maps, const __grid_constant__ KArgs a) {
+    tc_gemm_pair_kernel(const __grid_constant__ KMaps maps, const __grid_constant__ KArgs a,
+                        const __grid_constant__ KMaps, const __grid_constant__ KArgs, unsigned int*) {
   constexpr int HALF = 128;                       // rows per CTA of both operands
   constexpr int TILE = 256;                       // cluster tile (tokens and features)
   constexpr int A_BYTES = HALF * BK * 2;
@@ -1206,28 +1304,40 @@ int small_per_sm() {
   return v == 1 ? 1 : 2;
 }
 
-template <int BN, bool SWAP, int STAGES, bool PAIR = false>
-dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
+template <int BN, bool SWAP, int STAGES, bool PAIR>
+struct Cfg {
   // PAIR: cta_group::2 kernel, cluster tile 256 tokens x 256 features, each CTA
   // loads 128-row boxes of both operands.
-  constexpr int FEAT_TILE = PAIR ? 256 : (SWAP ? BM : BN);
-  constexpr int TOK_TILE = PAIR ? 256 : (SWAP ? BN : BM);
-  constexpr int BOX_W = PAIR ? 128 : FEAT_TILE;
-  constexpr int BOX_A = PAIR ? 128 : TOK_TILE;
-  constexpr int SMEM = PAIR ? STAGES * 2 * 128 * BK * 2 + 8 * kStageOutWarp + 1024 : STAGES * (BM + BN) * BK * 2 + 1024;
-  static bool attr_set = false;
-  void (*kern)(KMaps, KArgs) = PAIR ? tc_gemm_pair_kernel<STAGES> : tc_gemm_kernel<BN, SWAP, STAGES>;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(tc_gemm)");
-    attr_set = true;
-  }
-  KMaps maps;
+  static constexpr int FEAT_TILE = PAIR ? 256 : (SWAP ? BM : BN);
+  static constexpr int TOK_TILE = PAIR ? 256 : (SWAP ? BN : BM);
+  static constexpr int BOX_W = PAIR ? 128 : FEAT_TILE;
+  static constexpr int BOX_A = PAIR ? 128 : TOK_TILE;
+  static constexpr int SMEM =
+      PAIR ? STAGES * 2 * 128 * BK * 2 + 8 * kStageOutWarp + 1024 : STAGES * (BM + BN) * BK * 2 + 1024;
+  // stream-K grid cap: shallow configurations (<= 4 stages) fit two CTAs per
+  // SM, so the next launch can start streaming on an SM while one CTA drains
+  static int cap() { return num_sms() * ((SWAP && STAGES <= 4) ? small_per_sm() : 1); }
+};
+
+using KernFn = void (*)(KMaps, KArgs, KMaps, KArgs, unsigned int*);
+
+dl_status set_smem_attr(KernFn kern, int smem, bool* done) {
+  if (*done) return DL_OK;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(tc_gemm)");
+  *done = true;
+  return DL_OK;
+}
+
+// Kernel arguments of one GEMM problem (everything but the stream-K scheduler,
+// which depends on the grid: set_sched).  bytes / flops: algorithmic work.
+template <int BN, bool SWAP, int STAGES, bool PAIR>
+dl_status prep_args(const GemmProblem& p, bool stream_k, KMaps& maps, KArgs& a, double* bytes, double* flops) {
+  using C = Cfg<BN, SWAP, STAGES, PAIR>;
   memset(&maps, 0, sizeof(maps));
-  KArgs a;
   memset(&a, 0, sizeof(a));
   a.T = static_cast<int>(p.T);
-  a.tiles_tok = static_cast<int>((p.T + TOK_TILE - 1) / TOK_TILE);
+  a.tiles_tok = static_cast<int>((p.T + C::TOK_TILE - 1) / C::TOK_TILE);
   a.nseg = p.nseg;
   int tiles = 0;
   long long units = 0;
@@ -1239,7 +1349,7 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
     k.act_koff = static_cast<int>(s.act_koff);
     k.nkb = static_cast<int>((s.klen + BK - 1) / BK);
     k.tile_first = tiles;
-    k.ntiles = static_cast<int>((s.rows + FEAT_TILE - 1) / FEAT_TILE) * a.tiles_tok;
+    k.ntiles = static_cast<int>((s.rows + C::FEAT_TILE - 1) / C::FEAT_TILE) * a.tiles_tok;
     k.unit_first = units;
     k.slab_off = p.out.seg_slab_off[g];
     k.rpr = p.out.seg_rpr[g] > 0 ? p.out.seg_rpr[g] : 1;
@@ -1248,7 +1358,7 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
     tiles += k.ntiles;
     units += static_cast<long long>(k.ntiles) * k.nkb;
     if (s.klen > 0 && s.rows > 0) {
-      if (!make_map(&maps.w[g], s.w, s.rows, s.klen, s.ldw, BOX_W)) {
+      if (!make_map(&maps.w[g], s.w, s.rows, s.klen, s.ldw, C::BOX_W)) {
         set_error("cuTensorMapEncodeTiled failed (weight segment %d)", g);
         return DL_ERR_CUDA;
       }
@@ -1265,7 +1375,7 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(p.act_w), static_cast<cuuint64_t>(p.T),
                           static_cast<cuuint64_t>(p.act_p)};
     cuuint64_t strides[2] = {static_cast<cuuint64_t>(p.act_w * 2), static_cast<cuuint64_t>(p.T * p.act_w * 2)};
-    cuuint32_t box[3] = {static_cast<cuuint32_t>(BK), static_cast<cuuint32_t>(BOX_A), 1};
+    cuuint32_t box[3] = {static_cast<cuuint32_t>(BK), static_cast<cuuint32_t>(C::BOX_A), 1};
     cuuint32_t estr[3] = {1, 1, 1};
     if (g_encode(&maps.act, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(p.act), dims, strides, box, estr,
                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1274,7 +1384,7 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
       return DL_ERR_CUDA;
     }
     a.act_w = static_cast<int>(p.act_w);
-  } else if (!make_map(&maps.act, p.act, p.T, p.k_act, p.ld_act, BOX_A)) {
+  } else if (!make_map(&maps.act, p.act, p.T, p.k_act, p.ld_act, C::BOX_A)) {
     set_error("cuTensorMapEncodeTiled failed (activation)");
     return DL_ERR_CUDA;
   }
@@ -1324,6 +1434,10 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   a.fixup = FIX_NONE;
   static const int l2pf = DL_ENV("DL_L2PF") ? atoi(DL_ENV("DL_L2PF")) : kL2Prefetch;
   a.l2pf = l2pf;
+  static const int chain_pf = DL_ENV("DL_CHAIN_PF") ? atoi(DL_ENV("DL_CHAIN_PF")) : 64;
+  a.chain_pf = chain_pf;
+  static const int chain_warp = DL_ENV("DL_CHAIN_WARP") ? atoi(DL_ENV("DL_CHAIN_WARP")) : 0;
+  a.chain_warp = chain_warp;
   static const int acce_release = DL_ENV("DL_ACCE_RELEASE") ? atoi(DL_ENV("DL_ACCE_RELEASE")) : 0;   // A/B switch
   a.relaxed_acce = acce_release ? 0 : 1;
   static const int stage_out = DL_ENV("DL_STAGE_OUT") ? atoi(DL_ENV("DL_STAGE_OUT")) : 3;   // A/B: bit 0 plain, bit 1 accumulate
@@ -1350,24 +1464,67 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
     a.rope = p.fix.rope;
   }
   a.sched = nullptr;
-  if (stream_k && p.sched) {
-    static const double frac = DL_ENV("DL_SK_STATIC") ? atof(DL_ENV("DL_SK_STATIC")) : 0.9;
-    static const int chunk = DL_ENV("DL_SK_CHUNK") ? atoi(DL_ENV("DL_SK_CHUNK")) : 8;
-    const int cap = num_sms() * ((SWAP && STAGES <= 4) ? small_per_sm() : 1);   // must match the grid below
-    const int g = static_cast<int>(units < cap ? (units > 0 ? units : 1) : cap);
-    a.sched = p.sched;
-    a.static_units = static_cast<long long>(frac * static_cast<double>(units) / g);
-    a.dyn_begin = a.static_units * g;
-    a.chunk = chunk > 0 ? chunk : 1;
+  // algorithmic work of this launch: every weight element once, the
+  // activation K-range of each segment once, every output element once
+  double fl = 0, by = 0;
+  for (int g = 0; g < p.nseg; ++g) {
+    const double rk = static_cast<double>(p.seg[g].rows) * p.seg[g].klen;
+    fl += 2.0 * p.T * rk;
+    by += 2.0 * rk + 2.0 * p.T * p.seg[g].klen;
   }
+  by += static_cast<double>(p.T) * p.n_feat *
+        (p.out.mode == OUT_BF16 ? (p.out.accumulate ? 4 : 2) : p.out.mode == OUT_BF16_RED ? 2 : 4);
+  *bytes += by;
+  *flops += fl;
+  return DL_OK;
+}
+
+// Hybrid stream-K of a launch with `grid` CTAs: CTA c first takes its static
+// range, then dynamic chunks from the work counter p.sched.
+void set_sched(const GemmProblem& p, KArgs& a, int grid) {
+  static const double frac = DL_ENV("DL_SK_STATIC") ? atof(DL_ENV("DL_SK_STATIC")) : 0.9;
+  static const int chunk = DL_ENV("DL_SK_CHUNK") ? atoi(DL_ENV("DL_SK_CHUNK")) : 8;
+  a.sched = p.sched;
+  a.static_units = static_cast<long long>(frac * static_cast<double>(a.total_units) / grid);
+  a.dyn_begin = a.static_units * grid;
+  a.chunk = chunk > 0 ? chunk : 1;
+}
+
+cudaError_t launch_kern(KernFn kern, int grid, int smem, const KMaps& m1, const KArgs& a1, const KMaps& m2,
+                        const KArgs& a2, unsigned int* chain, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, m1, a1, m2, a2, chain);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return e;
+}
+
+template <int BN, bool SWAP, int STAGES, bool PAIR = false>
+dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
+  using C = Cfg<BN, SWAP, STAGES, PAIR>;
+  static bool attr_set = false;
+  KernFn kern = PAIR ? tc_gemm_pair_kernel<STAGES> : tc_gemm_kernel<BN, SWAP, STAGES, false>;
+  DL_TRY_INTERNAL(set_smem_attr(kern, C::SMEM, &attr_set));
+  KMaps maps;
+  KArgs a;
+  double bytes = 0, flops = 0;
+  DL_TRY_INTERNAL((prep_args<BN, SWAP, STAGES, PAIR>(p, stream_k, maps, a, &bytes, &flops)));
+  const long long units = a.total_units;
+  const int tiles = a.total_tiles;
   const int sms = num_sms();
   int grid;
   if (stream_k) {
-    // shallow configurations (<= 4 stages) fit two CTAs per SM: the next
-    // launch can then start streaming on an SM while one CTA is still draining
-    const int per_sm = (SWAP && STAGES <= 4) ? small_per_sm() : 1;
-    const int cap = sms * per_sm;
+    const int cap = C::cap();
     grid = static_cast<int>(units < cap ? (units > 0 ? units : 1) : cap);
+    if (p.sched) set_sched(p, a, grid);
   } else if (PAIR) {
     const int clusters = sms / 2;
     grid = 2 * (tiles < clusters ? (tiles > 0 ? tiles : 1) : clusters);
@@ -1385,31 +1542,10 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   } else {
     grid = tiles < sms ? (tiles > 0 ? tiles : 1) : sms;
   }
-  // algorithmic work of this launch: every weight element once, the
-  // activation K-range of each segment once, every output element once
-  double flops = 0, bytes = 0;
-  for (int g = 0; g < p.nseg; ++g) {
-    const double rk = static_cast<double>(p.seg[g].rows) * p.seg[g].klen;
-    flops += 2.0 * p.T * rk;
-    bytes += 2.0 * rk + 2.0 * p.T * p.seg[g].klen;
-  }
-  bytes += static_cast<double>(p.T) * p.n_feat *
-           (p.out.mode == OUT_BF16 ? (p.out.accumulate ? 4 : 2) : p.out.mode == OUT_BF16_RED ? 2 : 4);
   const int prof = prof_begin(st);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = SMEM;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, maps, a);
+  cudaError_t e = launch_kern(kern, grid, C::SMEM, maps, a, maps, a, nullptr, st);
   prof_end(prof, st, bytes, flops, SWAP ? 1 : 0);
   launched("tc_gemm");
-  if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess && a.tail_split > 0) {
     const int pf = prof_begin(st);
     const dl_status fs = launch_pdl(tc_tail_finalize_kernel, dim3(a.total_tiles - a.dp_tiles, 8), dim3(256), 0,
@@ -1423,6 +1559,49 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
               (long long)p.seg[0].klen, (long long)p.seg[1].klen, (long long)p.seg[2].klen,
               (long long)p.seg[0].act_koff, (long long)p.seg[1].act_koff, (long long)p.seg[2].act_koff, grid,
               (int)stream_k, cudaGetErrorString(e));
+    return DL_ERR_CUDA;
+  }
+  return DL_OK;
+}
+
+// Fused two-stage chain (swap-AB stream-K, both problems with the same T):
+// one launch, stage 2 waits on the in-kernel stage-1 arrival counter `chain`
+// (2 zero-initialised uint32, reset by the kernel's last CTA).
+template <int BN, int STAGES>
+dl_status launch_chain(const GemmProblem& p1, const GemmProblem& p2, unsigned int* chain, cudaStream_t st) {
+  using C = Cfg<BN, true, STAGES, false>;
+  static bool attr_set = false;
+  KernFn kern = tc_gemm_kernel<BN, true, STAGES, true>;
+  DL_TRY_INTERNAL(set_smem_attr(kern, C::SMEM, &attr_set));
+  KMaps m1, m2;
+  KArgs a1, a2;
+  double bytes = 0, flops = 0;
+  DL_TRY_INTERNAL((prep_args<BN, true, STAGES, false>(p1, true, m1, a1, &bytes, &flops)));
+  DL_TRY_INTERNAL((prep_args<BN, true, STAGES, false>(p2, true, m2, a2, &bytes, &flops)));
+  const long long units = a1.total_units > a2.total_units ? a1.total_units : a2.total_units;
+  // the in-kernel stage-1 -> stage-2 wait needs every CTA co-resident: cap the
+  // grid at what the occupancy calculator says fits (e.g. BN = 256: 197 KB of
+  // smem, one CTA per SM although the register budget would allow two)
+  static int resident = 0;
+  if (resident == 0) {
+    int per_sm = 0;
+    cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, C::SMEM);
+    if (oe != cudaSuccess || per_sm < 1) {
+      set_error("tc_gemm_chain: occupancy query failed (%s, %d CTAs/SM)", cudaGetErrorString(oe), per_sm);
+      return DL_ERR_CUDA;
+    }
+    resident = per_sm * num_sms();
+  }
+  const int cap = C::cap() < resident ? C::cap() : resident;
+  const int grid = static_cast<int>(units < cap ? (units > 0 ? units : 1) : cap);
+  if (p1.sched) set_sched(p1, a1, grid);
+  if (p2.sched) set_sched(p2, a2, grid);
+  const int prof = prof_begin(st);
+  cudaError_t e = launch_kern(kern, grid, C::SMEM, m1, a1, m2, a2, chain, st);
+  prof_end(prof, st, bytes, flops, 1);
+  launched("tc_gemm");
+  if (e != cudaSuccess) {
+    set_error("tc_gemm chain<BN=%d> (T=%lld grid=%d): %s", BN, (long long)p1.T, grid, cudaGetErrorString(e));
     return DL_ERR_CUDA;
   }
   return DL_OK;
@@ -1459,6 +1638,23 @@ dl_status tc_gemm(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   static const bool pair = !DL_ENV("DL_PREFILL_PAIR") || atoi(DL_ENV("DL_PREFILL_PAIR")) != 0;
   if (pair && !stream_k && p.out.mode == OUT_BF16) return launch_cfg<256, false, 6, true>(p, stream_k, st);
   return launch_cfg<256, false, 4>(p, stream_k, st);
+}
+
+dl_status tc_gemm_chain(const GemmProblem& p1, const GemmProblem& p2, unsigned int* chain, cudaStream_t st) {
+  if (p1.T <= 0) return DL_OK;
+  if (!get_encode()) {
+    set_error("cuTensorMapEncodeTiled unavailable (driver too old or no GPU)");
+    return DL_ERR_CUDA;
+  }
+  const bool red_ok = (p1.out.mode == OUT_F32_RED || p1.out.mode == OUT_BF16_RED) && p1.fix.op == FIX_NONE &&
+                      (p2.out.mode == OUT_F32_RED || p2.out.mode == OUT_BF16_RED || p2.fix.op != FIX_NONE);
+  if (p1.T != p2.T || p1.T > 256 || !red_ok || chain == nullptr || p2.act_p > 1) {
+    set_error("tc_gemm_chain: two stream-K reduction problems with the same T <= 256 and a chain counter");
+    return DL_ERR_INVALID_ARG;
+  }
+  if (p1.T <= 64) return launch_chain<64, 9>(p1, p2, chain, st);
+  if (p1.T <= 128) return launch_chain<128, 6>(p1, p2, chain, st);
+  return launch_chain<256, 4>(p1, p2, chain, st);
 }
 
 }  // namespace dl

@@ -1,0 +1,12 @@
+mkdir -p gpurun_out
+python -m paper_2604_17709_b200.build > /dev/null
+run() { echo "== $*"; env DL_LIBRARY=ab "$@" timeout 600 python tools/tp_emulate.py --layers 80 --ps 1,8 --layouts rp --steps 10 2>&1 | grep -o '"P": [0-9]*\|"rank_ms_per_step": [0-9.]*' | paste - - ; }
+{
+run DL_CHAIN=0
+run DL_CHAIN=1
+run DL_CHAIN_PF=2
+run DL_CHAIN_PF=0
+run DL_CHAIN_WARP=1
+run DL_CHAIN_WARP=1 DL_CHAIN_PF=2
+run DL_CHAIN=0
+} > gpurun_out/r02e_ab.log 2>&1
