@@ -525,6 +525,8 @@ struct SkArgs {
   __nv_bfloat16* kc;              // head-major caches (written: the appended key / value)
   __nv_bfloat16* vc;
   SideZero zero;
+  unsigned long long* ctr;        // per-CTA debug timeline (dl_debug_gemm_trace), 8 u64 per CTA
+  int reorder;                    // shared last item first (DL_ATTN_ORDER=1; default plain range order)
 };
 
 // RoPE of the interleaved pair (dim, dim + 1) at position pos (fp32 angle
@@ -589,11 +591,25 @@ __global__ void __launch_bounds__(sk::kThreads, PERSM)
   pdl_trigger();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int per_seq = a.Hk * a.nch;
+  unsigned long long* ctr = a.ctr ? a.ctr + static_cast<long long>(blockIdx.x) * 8 : nullptr;
+  if (ctr && tid == 0) { ctr[0] = ew_now(); unsigned s; asm volatile("mov.u32 %0, %%smid;" : "=r"(s)); ctr[7] = s; }
   // ---- prefix of tiles per sequence (cache_lens is not written inside the step) ----
   if (warp == 0) {
+    // lane l owns sequences [l*per, l*per + per): their tile counts are loaded
+    // once (all loads in flight together), scanned across the warp, written
     const int n = a.num_seqs, per = (n + 31) / 32, b = lane * per;
+    constexpr int R = kMaxSeqs / 32;
+    int cnt[R];
     int sum = 0;
-    for (int i = b; i < b + per && i < n; ++i) sum += per_seq * ((a.cache_lens[i] + 1 + KT - 1) / KT);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      cnt[r] = (r < per && b + r < n) ? __ldg(a.cache_lens + b + r) : -1;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      cnt[r] = cnt[r] < 0 ? 0 : per_seq * ((cnt[r] + 1 + KT - 1) / KT);
+      sum += cnt[r];
+    }
     int inc = sum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -601,9 +617,10 @@ __global__ void __launch_bounds__(sk::kThreads, PERSM)
       if (lane >= o) inc += v;
     }
     int run = inc - sum;
-    for (int i = b; i < b + per && i < n; ++i) {
-      P[i] = run;
-      run += per_seq * ((a.cache_lens[i] + 1 + KT - 1) / KT);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (r < per && b + r < n) P[b + r] = run;
+      run += cnt[r];
     }
     if (lane == 31) P[n] = inc;
   }
@@ -615,10 +632,23 @@ __global__ void __launch_bounds__(sk::kThreads, PERSM)
     ptx::fence_barrier_init();
   }
   __syncthreads();
+  if (ctr && tid == 0) ctr[1] = ew_now();
   const int G = gridDim.x, c = blockIdx.x;
   const int64_t N = P[a.num_seqs];
   const int64_t b0 = sk_bound(c, N, G), b1 = sk_bound(c + 1, N, G);
   const int64_t ldq = static_cast<int64_t>(a.Hq) * D;
+  // Processing order: the range's last item (usually shared with the next
+  // CTA) first, then [b0, split).  The next CTA processes that shared item
+  // first too, so the merges of split items happen early, overlapped with the
+  // other CTAs' streaming, instead of all piling up at the kernel's tail.
+  int64_t split = b0;
+  if (b1 > b0 && a.reorder) {
+    SkItem li;
+    sk_item_at(P, a.num_seqs, per_seq, b1 - 1, li, a.cache_lens);
+    split = li.start > b0 ? li.start : b0;
+  }
+  const int64_t nA = b1 - split;
+  auto tile_at = [&](int64_t q) -> int64_t { return q < nA ? split + q : b0 + (q - nA); };
 
   if (warp == 4) {
     // ============================ producer ============================
@@ -637,8 +667,7 @@ __global__ void __launch_bounds__(sk::kThreads, PERSM)
         col = 0;
       }
     };
-    auto issue = [&](const SkItem& it, int64_t g) {
-      const int64_t l = g - b0;
+    auto issue = [&](const SkItem& it, int64_t g, int64_t l) {   // l: position in the processing order
       const int st = static_cast<int>(l % NS);
       ptx::mbar_wait(&empty[st], ((l / NS) & 1) ^ 1);
       int row, col;
@@ -650,21 +679,23 @@ __global__ void __launch_bounds__(sk::kThreads, PERSM)
       ptx::tma_load_2d(dst + 16384, &maps.v, &full[st], col, row, pol);
       ptx::tma_load_2d(dst + 24576, &maps.v, &full[st], col + 64, row, pol);
     };
+    const int64_t ntl = b1 - b0;
     // 1. before the predecessor completes: leading tiles of old keys only
-    int64_t pre = b0;
+    int64_t pre = 0;
     if (!a.token_major) {
       SkItem it;
-      while (pre < b1 && pre - b0 < NS) {
-        sk_item_at(P, a.num_seqs, per_seq, pre, it, a.cache_lens);
-        const int t = static_cast<int>(pre - it.start);
+      while (pre < ntl && pre < NS) {
+        const int64_t g = tile_at(pre);
+        sk_item_at(P, a.num_seqs, per_seq, g, it, a.cache_lens);
+        const int t = static_cast<int>(g - it.start);
         if ((t + 1) * KT > it.n_keys - 1) break;   // tile holds the key appended by this step
-        issue(it, pre);
+        issue(it, g, pre);
         ++pre;
       }
       // ... and the next l2pf old-key tiles into L2 (HBM is otherwise idle
       // while the predecessor finishes)
-      int64_t g = pre;
-      for (int n = 0; n < a.l2pf && g < b1; ++n, ++g) {
+      for (int64_t n = 0, q = pre; n < a.l2pf && q < ntl; ++n, ++q) {
+        const int64_t g = tile_at(q);
         sk_item_at(P, a.num_seqs, per_seq, g, it, a.cache_lens);
         const int t = static_cast<int>(g - it.start);
         if ((t + 1) * KT > it.n_keys - 1) continue;
@@ -678,11 +709,12 @@ __global__ void __launch_bounds__(sk::kThreads, PERSM)
     }
     pdl_wait();
     // 2. the remaining tiles
-    for (int64_t g = pre > b0 ? pre : b0; g < b1;) {
-      SkItem it;
-      sk_item_at(P, a.num_seqs, per_seq, g, it, a.cache_lens);
-      const int64_t e = it.end < b1 ? it.end : b1;
-      for (; g < e; ++g) issue(it, g);
+    SkItem it{};
+    it.end = -1;
+    for (int64_t q = pre; q < ntl; ++q) {
+      const int64_t g = tile_at(q);
+      if (g < it.start || g >= it.end) sk_item_at(P, a.num_seqs, per_seq, g, it, a.cache_lens);
+      issue(it, g, q);
     }
     return;
   }
@@ -690,6 +722,7 @@ __global__ void __launch_bounds__(sk::kThreads, PERSM)
   // ============================== compute ==============================
   pdl_wait();
   ew_mark(a.tr, 2);
+  if (ctr && tid == 0) ctr[2] = ew_now();
   if (a.zero.p) {   // side clear (the q|k|v group's latent buffer), spread over every compute thread
     const int64_t per_row = a.zero.row_bytes / 16, total = a.zero.rows * per_row;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * 128 + tid; i < total; i += static_cast<int64_t>(gridDim.x) * 128) {
@@ -701,10 +734,16 @@ __global__ void __launch_bounds__(sk::kThreads, PERSM)
   const int w = warp;
   const int g8 = lane >> 2, t4 = lane & 3;
   const float scale = rsqrtf(static_cast<float>(D)) * 1.4426950408889634f;
-  for (int64_t g = b0; g < b1;) {
+  int64_t lpos = 0;   // position in the processing order (ring slot / phase)
+  for (int64_t g = split, send = b1; g < send || send == b1;) {
+    if (g >= send) {   // segment A [split, b1) done: then [b0, split)
+      if (split == b0) break;
+      g = b0;
+      send = split;
+    }
     SkItem it;
     sk_item_at(P, a.num_seqs, per_seq, g, it, a.cache_lens);
-    const int64_t e = it.end < b1 ? it.end : b1;
+    const int64_t e = it.end < send ? it.end : send;
     const int kvh = it.j / a.nch, ch = it.j - kvh * a.nch;
     const int h0 = kvh * a.Gall + ch * 16;
     const int Gc = min(16, a.Gall - ch * 16);
@@ -774,9 +813,10 @@ __global__ void __launch_bounds__(sk::kThreads, PERSM)
     for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
     float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;   // m in log2 units (scaled)
     for (int64_t gt = g; gt < e; ++gt) {
-      const int64_t l = gt - b0;
+      const int64_t l = lpos++;
       const int st = static_cast<int>(l % NS);
       ptx::mbar_wait(&full[st], (l / NS) & 1);
+      if (ctr && tid == 0 && ctr[3] == 0) ctr[3] = ew_now();
       const uint32_t sK = ptx::smem_u32(stages + st * STAGE), sV = sK + 16384;
       const int nv = min(KT, it.n_keys - static_cast<int>(gt - it.start) * KT);   // valid keys of the tile
       if (nv < KT) {
@@ -883,6 +923,7 @@ __global__ void __launch_bounds__(sk::kThreads, PERSM)
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&empty[st]);
     }
+    if (ctr && tid == 0) ctr[4] = ew_now();
     l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
     l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
     l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
@@ -924,12 +965,13 @@ __global__ void __launch_bounds__(sk::kThreads, PERSM)
       if (lane == 0) {
         int nc = 0;   // CTAs with a non-empty range (N < grid leaves some empty)
         for (int cc = cf; cc <= cl; ++cc) nc += sk_bound(cc + 1, N, G) > sk_bound(cc, N, G);
-        __threadfence();   // release this warp's partial (cumulative over the warp via __syncwarp)
-        last = atomicAdd(cnt, 1u) == static_cast<unsigned>(nc - 1);
-        if (last) {
-          __threadfence();   // acquire the other contributors' partials
-          *cnt = 0u;         // zero-maintained for the next launch
-        }
+        // acq_rel: releases this warp's partial (cumulative over the warp via
+        // __syncwarp) and, for the last contributor, acquires the others'.
+        // (fence.sc.gpu + relaxed atomic measured ~2x slower tails at TP = 8)
+        unsigned old;
+        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
+        last = old == static_cast<unsigned>(nc - 1);
+        if (last) *cnt = 0u;   // zero-maintained for the next launch
       }
       last = __shfl_sync(0xffffffffu, last, 0);
       if (!last) {
@@ -979,6 +1021,7 @@ __global__ void __launch_bounds__(sk::kThreads, PERSM)
     g = e;
   }
   ew_mark(a.tr, 3);
+  if (ctr && tid == 0) ctr[6] = ew_now();
 }
 
 }  // namespace
@@ -1029,6 +1072,9 @@ dl_status launch_attention_sk(const AttnArgs& a, cudaStream_t st) {
   k.kc = const_cast<__nv_bfloat16*>(a.k_cache);
   k.vc = const_cast<__nv_bfloat16*>(a.v_cache);
   k.zero = a.zero;
+  k.ctr = nullptr;
+  static const int order = DL_ENV("DL_ATTN_ORDER") ? atoi(DL_ENV("DL_ATTN_ORDER")) : 0;   // measured neutral (A/B)
+  k.reorder = order;
   static const int l2pf = DL_ENV("DL_ATTN_L2PF") ? atoi(DL_ENV("DL_ATTN_L2PF")) : 0;
   k.l2pf = l2pf;
   k.part = reinterpret_cast<float*>(static_cast<uint8_t*>(a.sk_ws) + (a.sk_items_cap + 63) / 64 * 64 * 4 * 4);
@@ -1044,7 +1090,17 @@ dl_status launch_attention_sk(const AttnArgs& a, cudaStream_t st) {
                          static_cast<int>(sk::smem_bytes<2>(sk::kMaxSeqs)));
     attr = true;
   }
-  const int grid = std::min((cfg23 ? 3 : 2) * num_sms(), sk::kMaxGrid);
+  // grid: every CTA keeps >= ~4 key tiles (fewer split items to merge when the
+  // step is small, e.g. one KV head per rank at TP = 8), at most 2 (3) per SM
+  int64_t tiles = 0;
+  {
+    // host-side estimate from the capacity: cache_lens lives on the device
+    tiles = static_cast<int64_t>(a.num_seqs) * a.Hk * nch * ((a.max_seq + KT - 1) / KT);
+  }
+  int grid = std::min((cfg23 ? 3 : 2) * num_sms(), sk::kMaxGrid);
+  if (tiles < static_cast<int64_t>(grid) * 4) grid = std::max(num_sms(), static_cast<int>(tiles / 4));
+  grid = std::min(grid, (cfg23 ? 3 : 2) * num_sms());
+  k.ctr = gemm_trace_cta_slots((grid + 147) / 148);
   return launch_pdl(kern, dim3(grid), dim3(sk::kThreads), smem, st, "attention decode (stream-K)", maps, k);
 }
 

@@ -247,6 +247,9 @@ dl_status tc_gemm_chain(const GemmProblem& p1, const GemmProblem& p2, unsigned i
 // (globaltimer ns at entry, setup done, first TMA, first stage landed, last
 // MMA issued, epilogue done, exit; and its SM id)
 dl_status set_gemm_trace(void* buf);
+// per-CTA debug timeline of a non-GEMM launch in the GEMM trace buffer:
+// nslots consecutive 148-CTA slots (8 u64 per CTA), or null when tracing is off
+unsigned long long* gemm_trace_cta_slots(int nslots);
 // Debug timeline of selected non-GEMM kernels (dl_debug_ew_trace): per launch
 // slot 4 u64 = {kind, min entry, min start after griddepcontrol.wait, max end}.
 dl_status set_ew_trace(void* buf);

@@ -346,6 +346,7 @@ struct __align__(64) KMaps {
 __device__ unsigned long long* g_trace = nullptr;
 bool g_trace_host_on = false;   // host: assign a slot to every launch while tracing
 int g_trace_next = 0;
+unsigned long long* g_trace_host_buf = nullptr;
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -1613,10 +1614,18 @@ bool encode_map_bf16(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols
   return get_encode() && make_map(m, ptr, rows, cols, ld, box_rows);
 }
 
+unsigned long long* gemm_trace_cta_slots(int nslots) {
+  if (!g_trace_host_on) return nullptr;
+  unsigned long long* p = g_trace_host_buf + static_cast<long long>(g_trace_next) * 148 * 8;
+  g_trace_next += nslots;
+  return p;
+}
+
 dl_status set_gemm_trace(void* buf) {
   unsigned long long* p = static_cast<unsigned long long*>(buf);
   g_trace_host_on = p != nullptr;
   g_trace_next = 0;
+  g_trace_host_buf = p;
   return cuda_status(cudaMemcpyToSymbol(g_trace, &p, sizeof(p)), "set trace");
 }
 
