@@ -1120,6 +1120,9 @@ dl_status launch_attention(const AttnArgs& a, cudaStream_t st) {
     return DL_ERR_UNSUPPORTED;
   }
   if (!a.decode) {
+    // tcgen05 kernel (attn_tc.cu); DL_ATTN_PREFILL_MMA=1: the FA2-style mma.sync kernel below (A/B)
+    static const bool mma_sync = DL_ENV("DL_ATTN_PREFILL_MMA") && atoi(DL_ENV("DL_ATTN_PREFILL_MMA")) != 0;
+    if (!mma_sync) return launch_attention_prefill_tc(a, st);
     constexpr int KTP = 64;   // 64-key tiles (32-key tiles at 3 CTAs/SM measured 7% slower)
     constexpr int SMEM = QT * ROW_BYTES + 4 * KTP * ROW_BYTES;
     static bool attr = false;

@@ -395,6 +395,8 @@ struct AttnArgs {
   SideZero zero;
 };
 dl_status launch_attention(const AttnArgs& a, cudaStream_t st);
+// prefill (a.decode == 0) on tcgen05 / TMEM / TMA (attn_tc.cu)
+dl_status launch_attention_prefill_tc(const AttnArgs& a, cudaStream_t st);
 size_t attention_workspace(int64_t max_tokens, int Hq, int d);
 size_t attention_sk_workspace(int64_t max_tokens, int Hq);
 

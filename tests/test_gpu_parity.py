@@ -253,6 +253,45 @@ def test_block_prefill_continues_cached_prefix(dl, orc, first, second):
         assert rel(kg, rk_[a:a + L]) <= TOL_BF16
 
 
+@pytest.mark.parametrize("first,second", [([300, 1], [129, 250]), ([0, 127], [385, 1])])
+def test_block_prefill_cached_prefix_nan_tail(dl, orc, first, second):
+    """The tcgen05 prefill attention reads whole 128-key tiles of the cache: key
+    rows past the visible range (unwritten slots, here NaN) must neither leak
+    through the masked scores nor through 0 x NaN in P.V.  Chunked prefill over
+    NaN-initialised caches, query tiles spanning several key tiles, ragged ends."""
+    s = SMALL
+    rk = block_ranks(s, 0.4)
+    w = gen_block_weights(s, rk, 0, 31)
+    S = len(first)
+    full = [a + b for a, b in zip(first, second)]
+    x_full = gen_normal((sum(full), s.h), 1.0, 32, dtype=torch.bfloat16)
+    cu_full = np.concatenate([[0], np.cumsum(full)]).astype(np.int32)
+    pos_full = np.concatenate([np.arange(L) for L in full]).astype(np.int32)
+    ref, _, _ = orc.block_prefill(_oracle_cfg(orc, s, rk), w, x_full, pos_full, cu_full)
+    max_seq = max(full) + 200
+    cfg = dl.make_block_config(s, rk, max_tokens=sum(full), max_seqs=S)
+    wdev = dl.BlockWeights({k: v.cuda() for k, v in w.items()})
+    ws = torch.zeros(dl.dl_block_workspace(cfg), dtype=torch.uint8, device="cuda")
+    kc = torch.full((S, s.n_kv_heads, max_seq, s.head_dim), float("nan"), dtype=torch.bfloat16, device="cuda")
+    vc = torch.full_like(kc, float("nan"))
+    last = None
+    for chunk, before in ((first, [0] * S), (second, first)):
+        rows = np.concatenate([np.arange(cu_full[i] + before[i], cu_full[i] + before[i] + chunk[i])
+                               for i in range(S)]).astype(np.int64)
+        pos = np.concatenate([np.arange(before[i], before[i] + chunk[i]) for i in range(S)]).astype(np.int32)
+        cu = np.concatenate([[0], np.cumsum(chunk)]).astype(np.int32)
+        xd = x_full[rows].clone().cuda()
+        cl = torch.tensor(before, dtype=torch.int32, device="cuda")
+        dl.dl_decomposed_block_forward(cfg, wdev, xd, torch.from_numpy(pos).cuda(), torch.from_numpy(cu).cuda(),
+                                       S, dl.DL_PREFILL, kc, vc, cl, None, ws)
+        torch.cuda.synchronize()
+        last = (rows, xd.cpu())
+    rows2, xo2 = last
+    assert torch.isfinite(xo2.float()).all()
+    xin2 = x_full[rows2].double()
+    assert rel(xo2.double() - xin2, ref[rows2] - xin2.numpy()) <= TOL_BF16
+
+
 @pytest.mark.parametrize("cache_lens", [[0, 5, 17, 1, 33, 2, 7, 100], [511] * 4])
 def test_block_decode_small(dl, orc, cache_lens):
     s = SMALL
@@ -605,3 +644,22 @@ def test_lowrank_kv_decode_batch64(dl, orc):
     """Decode batch 64 (the bench's shape family) with ragged contexts."""
     err, err_new, _ = _kvlr_case(dl, orc, SMALL, [(37 * i) % 130 for i in range(64)], seed=91)
     assert err <= TOL_BF16 and err_new <= TOL_BF16, (err, err_new)
+
+
+@pytest.mark.parametrize("knob", ["DL_FA_CLUSTER=2", "DL_FA_CLUSTER=8", "DL_ATTN_PREFILL_MMA=1"])
+def test_prefill_attention_variants(knob):
+    """The A/B variants of the prefill attention against the oracle:
+    K/V tiles multicast to 2- and 8-CTA clusters (GQA heads of one KV head), and
+    the previous mma.sync kernel -- every prefill parity test of this file, run
+    against the instrumented library in a subprocess."""
+    import os
+    import subprocess
+    import sys
+    name, _, val = knob.partition("=")
+    env = dict(os.environ, DL_LIBRARY="ab", **{name: val})
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_gpu_parity.py"), "-k",
+                        "prefill and not test_prefill_attention_variants"],
+                       capture_output=True, text=True, env=env, timeout=900, cwd=root)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
