@@ -5,7 +5,7 @@ out=gpurun_out
 mkdir -p $out
 # 1. launch list of the bench command (cold-cache, serialised: compare shares)
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
-  -k regex:"tc_gemm|tc_tail|rmsnorm|ew4|silu|rope|attn|embedding|latent|unpermute|gemv|chain" \
+  -k regex:"tc_gemm|tc_tail|rmsnorm|ew4|silu|rope|attn|embedding|latent|unpermute|gemv|chain|residual|argmax|f32_to" \
   --log-file $out/${tag}_launches_raw.csv python bench.py --steps 2 --warmup 1 --prefill-steps 1 \
   --no-cpu-baseline > $out/${tag}_ncu_bench.log 2>&1
 # 2. full sections of the top kernels (one launch each, 2-layer eager steps)
