@@ -443,8 +443,10 @@ def main():
         step_bytes += 2 * n_layers * shape.h * (ranks["o"] + ranks["down"]) * (1 - 1 / world)
     step_gbs = step_bytes / (step_ms * 1e-3) / 1e9
 
-    # ---- e2e: H2D ids from pinned host, graph, D2H of the step's result (the greedy next
-    # token of every sequence, argmax over the gathered logits on the device) -----
+    # ---- e2e: the autoregressive loop a serving user runs: H2D of the step's token ids
+    # from pinned host memory, the captured step, D2H of its result (the greedy next token
+    # of every sequence, argmax over the gathered logits on the device), and the host
+    # round trip that turns those tokens into the next step's input -----------------
     ids_h = model.ids.to("cpu").pin_memory()
     out_dev = model.next_ids
     out_h = torch.empty(out_dev.shape, dtype=out_dev.dtype, pin_memory=True)
@@ -456,6 +458,8 @@ def main():
             model.ids.copy_(ids_h, non_blocking=True)
             dgraph.replay()
             out_h.copy_(out_dev, non_blocking=True)
+            stream.synchronize()        # the host needs this step's tokens ...
+            ids_h.copy_(out_h)          # ... to feed them back as the next step's input
         e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / args.steps
