@@ -24,9 +24,11 @@ class DecomposedLlama:
     def __init__(self, shape, ranks: dict, layer_weights, embed: torch.Tensor, final_norm: torch.Tensor,
                  lm_head_local: torch.Tensor, batch: int, max_seq: int, prefill_tokens: int = 0,
                  comm: L.Comm | None = None, device="cuda", layout: int = L.DL_LAYOUT_RANK_PARALLEL,
-                 kv: str = "full", kv_block_size: int = 16):
+                 kv: str = "full", kv_block_size: int = 16, prefill_chunks: int = 1):
         """kv = "full": head-major post-RoPE K/V cache; "lowrank": paged latent cache
-         with the two-stage reconstruction (decode only; uniform ranks)."""
+         with the two-stage reconstruction (decode only; uniform ranks).
+        prefill_chunks > 1: the prefill sequence is split into that many chunks that run
+        as a wavefront over (layer, chunk) on one stream per chunk (prefill_step)."""
         self.shape, self.ranks, self.comm, self.layout, self.kv_mode = shape, ranks, comm, layout, kv
         self.world = comm.world if comm else 1
         self.rank = comm.rank if comm else 0
@@ -110,6 +112,28 @@ class DecomposedLlama:
             self.pre_xl = torch.zeros(1, s.h, dtype=bf, device=self.device)
             self.pre_xn = torch.zeros(1, s.h, dtype=bf, device=self.device)
             self.pre_logits = torch.zeros(1, vloc, dtype=bf, device=self.device)
+            # chunked wavefront (prefill_chunks > 1): chunk c = tokens [c*Tc, (c+1)*Tc) of the
+            # sequence, continuing the cached prefix of chunks < c (cache_lens = c*Tc), with its
+            # own workspaces and stream
+            C = max(1, int(prefill_chunks))
+            if prefill_tokens % C:
+                raise ValueError("prefill_chunks must divide prefill_tokens")
+            self.pre_chunks = C
+            if C > 1:
+                Tc = prefill_tokens // C
+                self.chunk_cfgs = [L.make_block_config(s, r, max_tokens=Tc, max_seqs=1, layout=layout)
+                                   for r in per_layer]
+                self.chunk_wss = []
+                for c in range(C):
+                    cws = {}
+                    for k, cf in zip(keys, self.chunk_cfgs):
+                        if k not in cws:
+                            cws[k] = torch.zeros(L.dl_block_workspace(cf, self.world), dtype=torch.uint8,
+                                                 device=self.device)
+                    self.chunk_wss.append([cws[k] for k in keys])
+                self.chunk_cu = torch.tensor([0, Tc], dtype=torch.int32, device=self.device)
+                self.chunk_lens = [torch.tensor([c * Tc], dtype=torch.int32, device=self.device) for c in range(C)]
+                self.chunk_streams = [None] + [torch.cuda.Stream(device=self.device) for _ in range(C - 1)]
 
     def kv_prepare(self, cache_lens_host, tables_host=None):
         """Preparation stage of the low-rank KV cache (host; outside the graph replay):
@@ -150,7 +174,9 @@ class DecomposedLlama:
         s = self.shape
         T = self.prefill_tokens
         L.dl_embedding(self.embed, self.pre_ids, self.pre_x)
-        for i, lw in enumerate(self.layers):
+        if self.pre_chunks > 1:
+            self._prefill_wavefront()
+        for i, lw in enumerate(self.layers if self.pre_chunks == 1 else ()):
             L.dl_decomposed_block_forward(self.pre_cfgs[i], lw, self.pre_x, self.pre_pos, self.pre_cu, 1, L.DL_PREFILL,
                                           self.pre_cache[i, 0], self.pre_cache[i, 1], self.pre_lens, self.comm,
                                           self.pre_wss[i])
@@ -159,3 +185,38 @@ class DecomposedLlama:
         L.dl_dense(self.pre_xn, self.lm_head, self.pre_logits)
         del T
         return self.pre_logits
+
+    def _prefill_wavefront(self):
+        """Block (layer i, chunk c) runs on chunk c's stream after block (i, c - 1) -- its keys
+        and values are the cached prefix chunk c attends to (chunked prefill, include/dl.h) --
+        and after block (i - 1, c) (stream order).  Block (i, c) therefore overlaps block
+        (i + 1, c - 1): one chunk's TP collectives (NCCL on its stream) run while another
+        chunk's GEMMs stream (the communication / computation overlap of PAPER.md:224), and on
+        one GPU the second stream's kernels fill the SMs the first stream's small kernels and
+        GEMM tails leave idle.  Capturable in a CUDA graph (fork / join through events)."""
+        C = self.pre_chunks
+        Tc = self.prefill_tokens // C
+        main = torch.cuda.current_stream(self.device)
+        streams = [main] + self.chunk_streams[1:]
+        fork = torch.cuda.Event()
+        fork.record(main)
+        for st in streams[1:]:
+            st.wait_event(fork)
+        done = [[None] * C for _ in self.layers]
+        for i, lw in enumerate(self.layers):
+            for c in range(C):
+                st = streams[c]
+                if c > 0:
+                    st.wait_event(done[i][c - 1])
+                rows = slice(c * Tc, (c + 1) * Tc)
+                with torch.cuda.stream(st):
+                    L.dl_decomposed_block_forward(self.chunk_cfgs[i], lw, self.pre_x[rows], self.pre_pos[rows],
+                                                  self.chunk_cu, 1, L.DL_PREFILL, self.pre_cache[i, 0],
+                                                  self.pre_cache[i, 1], self.chunk_lens[c], self.comm,
+                                                  self.chunk_wss[c][i], stream=st)
+                ev = torch.cuda.Event()
+                ev.record(st)
+                done[i][c] = ev
+        for c in range(1, C):   # join: the last token's row comes from the last chunk
+            main.wait_event(done[-1][c])
+

@@ -231,3 +231,44 @@ def test_graph_replay_lowrank_kv_decode(dl, orc):
             got = pool[tables[b, L // bs], L % bs, :lk].cpu()
             assert rel(got, zk_new[b]) <= TOL_BF16
         lens = [L + 1 for L in lens]
+
+
+@pytest.mark.parametrize("chunks", [2, 4])
+def test_prefill_chunk_wavefront(dl, orc, chunks):
+    """Chunked prefill wavefront (model.py `_prefill_wavefront`): the sequence split into
+    `chunks` chunks, block (layer i, chunk c) on chunk c's stream after block (i, c - 1),
+    captured in a CUDA graph and replayed.  Every token's final hidden state vs the
+    oracle's one-shot causal prefill of the whole sequence, layer by layer (chunks
+    continue each other's cached prefix: include/dl.h, PREFILL)."""
+    from paper_2604_17709_b200.model import DecomposedLlama
+    s = SMALL
+    rk = block_ranks(s, 0.4)
+    ws_ = [gen_block_weights(s, rk, 11, li) for li in range(3)]
+    T = 384
+    embed = gen_normal((s.vocab, s.h), 1.0, 95, dtype=torch.bfloat16).cuda()
+    lm = gen_normal((s.vocab, s.h), s.h ** -0.5, 96, dtype=torch.bfloat16).cuda()
+    model = DecomposedLlama(s, rk, [{k: v.cuda() for k, v in w.items()} for w in ws_], embed,
+                            torch.ones(s.h, dtype=torch.bfloat16, device="cuda"), lm, batch=1, max_seq=8,
+                            prefill_tokens=T, prefill_chunks=chunks)
+    ids = (torch.arange(T, dtype=torch.int32) * 37 + 5) % s.vocab
+    model.pre_ids.copy_(ids)
+    stream = torch.cuda.Stream()
+    stream.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(stream):
+        model.prefill_step()
+    stream.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        model.prefill_step()
+    model.pre_x.zero_()
+    torch.cuda.synchronize()
+    graph.replay()
+    torch.cuda.synchronize()
+    x0 = embed.cpu()[ids.long()].double()
+    x = x0
+    pos = np.arange(T, dtype=np.int32)
+    cu = np.array([0, T], dtype=np.int32)
+    for w in ws_:
+        x, _, _ = orc.block_prefill(_ocfg(orc, s, rk), w, x, pos, cu)
+        x = torch.tensor(x)
+    assert rel(model.pre_x.cpu().double() - x0, (x - x0).numpy()) <= TOL_BF16
