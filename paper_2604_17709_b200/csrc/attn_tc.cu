@@ -482,6 +482,9 @@ __global__ void __launch_bounds__(fa::kThreads, 1)
           ptx::fence_async_smem();   // zeroed V rows before the MMA reads them
         }
         ptx::tmem_st_wait();       // P (and any O rescale) in TMEM before the P.V
+        // observe every P.V retirement (the previous tile's P.V ran during this softmax,
+        // so this costs nothing; it keeps each p_empty phase waited on)
+        if (g > 0) ptx::mbar_wait(&p_empty[(g - 1) & 1], ((g - 1) >> 1) & 1);
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&p_full[sl]);
