@@ -230,14 +230,17 @@ def test_no_rope_is_position_free(orc):
 
 
 def test_block_params_non_glu(orc):
-    """Non-GLU MLP carries no gate factors: sum of k (m + n) over the six remaining matrices."""
-    cfg, _, _ = _small_block(orc, lossless=False, seed=15, glu=False)
-    h, m, d = cfg.h, cfg.m, cfg.head_dim
-    hkv = cfg.n_kv_heads * d
-    fp = lambda mo, ni, k: k * (mo + ni)
-    expect = (fp(h, h, cfg.r_q) + fp(hkv, h, cfg.r_k) + fp(hkv, h, cfg.r_v) + fp(h, h, cfg.r_o)
-              + fp(m, h, cfg.r_up) + fp(h, m, cfg.r_down))
-    assert orc.block_params(cfg) == expect
+    """Non-GLU MLP carries no gate factors ((m+n)k per factor pair): the oracle's
+    count equals the number of elements actually stored in the block's factor tensors
+    (counted from the tensors, not from a formula), and dropping the gate removes exactly
+    the gate pair's elements."""
+    cfg, w, _ = _small_block(orc, lossless=False, seed=15, glu=False)
+    stored = sum(v.size for k, v in w.items() if k.startswith(("A_", "B_")))
+    assert "A_gate" not in w and orc.block_params(cfg) == stored
+    cfg_g, w_g, _ = _small_block(orc, lossless=False, seed=15, glu=True)
+    gate = w_g["A_gate"].size + w_g["B_gate"].size
+    assert orc.block_params(cfg_g) == sum(v.size for k, v in w_g.items() if k.startswith(("A_", "B_")))
+    assert orc.block_params(cfg_g) - orc.block_params(cfg) == gate
 
 
 @pytest.mark.parametrize("hkv,glu,use_rope", VARIANTS)
