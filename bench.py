@@ -52,6 +52,9 @@ def parse():
                    help="decode KV cache: post-RoPE K/V, or the paged low-rank (latent) cache with the "
                         "two-stage reconstruction (P:111, P:219-237)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-tp-window", action="store_true",
+                   help="TP > 1: plain NCCL collectives instead of the fused epilogue reductions "
+                        "through CUDA-IPC symmetric windows (include/dl.h dl_comm_window_*)")
     p.add_argument("--cpu-sample-seqs", type=int, default=64)
     return p.parse_args()
 
@@ -257,6 +260,33 @@ def main():
     lm_head = lm_full_rows[rank * vloc:(rank + 1) * vloc].clone()
     del lm_full_rows
     final_norm = torch.ones(shape.h, dtype=torch.bfloat16, device=dev)
+    # TP > 1, rank-parallel: a symmetric window per rank mapped into every peer (CUDA IPC over
+    # NVLink) so the decode path's reductions run inside the stage-2 epilogues
+    tp_coll = "nccl" if world > 1 else "none"
+    if world > 1 and args.layout == "rp" and not args.no_tp_window:
+        # every rank must take the same path: agree on success after each stage
+        def agree(flag):
+            t = torch.tensor([1 if flag else 0], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            return bool(t.item())
+        err, hs = "", None
+        try:
+            wcfg = dl.make_block_config(shape, ranks, max_tokens=args.batch, max_seqs=args.batch)
+            comm.window_alloc(dl.dl_block_window_bytes(wcfg, world))
+            hs = [None] * world
+            dist.all_gather_object(hs, comm.window_handle())
+        except Exception as e:   # noqa: BLE001
+            err = str(e)[:120]
+        if agree(not err):
+            try:
+                comm.window_connect(hs)
+            except Exception as e:   # noqa: BLE001
+                err = str(e)[:120]
+            if not agree(not err):
+                raise SystemExit(f"TP window: connect failed on some rank ({err or 'peer'}); rerun with --no-tp-window")
+            tp_coll = "fused-window (decode) + nccl (prefill)"
+        else:
+            tp_coll = f"nccl (window setup failed: {err or 'on a peer'})"
     model = DecomposedLlama(shape, ranks, layer_iter(), embed, final_norm, lm_head, batch=args.batch,
                             max_seq=args.ctx + 1, prefill_tokens=args.prefill_tokens, comm=comm, device=dev,
                             prefill_chunks=args.prefill_chunks,
@@ -558,6 +588,7 @@ def main():
                                        f"B={args.batch} ctx={args.ctx} (+ prefill {args.prefill_tokens})",
                            "global_batch": args.batch, "seq_len": args.ctx, "parallelism": f"tp{world}",
                            "tp_layout": "deinfer" if args.layout == "deinfer" else "rank-parallel",
+                           "tp_collectives": tp_coll,
                            "kv_cache": "post-RoPE K/V" if args.kv == "full" else
                            "paged low-rank latent, block 16, two-stage reconstruction",
                            "layers": n_layers, "ranks": ranks,

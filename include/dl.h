@@ -116,12 +116,40 @@ typedef enum {
  *   Results are NOT the sharded result; the per-rank kernel work of a TP =
  *   world step is exact, so its compute time can be measured without world
  *   GPUs (tools/tp_emulate.py).
- * Any NCCL or group communicator, even of world 1, selects the tensor-
+ * dl_comm_create_peer: rank `rank` of `world` (<= 8) processes whose ONLY
+ *   collectives are the fused ones of the rank-parallel decode path (below):
+ *   no NCCL; every other collective returns DL_ERR_UNSUPPORTED.  Needs a
+ *   connected window.
+ * Multi-process symmetric window (NCCL or peer communicators; the fused
+ * collectives of PAPER.md:224 "communication-computation overlap and kernel
+ * fusion" across processes / GPUs):
+ *   dl_comm_window_alloc(comm, bytes): allocate and zero this rank's window
+ *     (>= dl_block_window_bytes of the block config; owned by the comm, freed
+ *     by dl_comm_destroy) plus a 256-byte flag area for the device barrier.
+ *   dl_comm_window_handle(comm, handle): this window's CUDA IPC handle
+ *     (DL_IPC_HANDLE_BYTES bytes written to host memory `handle`).
+ *   dl_comm_window_connect(comm, handles): `handles` = world x
+ *     DL_IPC_HANDLE_BYTES host bytes in rank order (exchanged by the caller,
+ *     e.g. an all-gather over its process group); maps every peer's window
+ *     (cudaIpcOpenMemHandle: the peers must be on GPUs with peer access --
+ *     NVLink / NVSwitch -- or the same GPU).  Collective over the ranks in the
+ *     sense that every rank must connect before any block call uses it.
+ *   With a connected window the rank-parallel decode path (T <= 256) red.adds
+ *   its stage-2 partials straight into the owners' windows over NVLink and
+ *   orders the ranks with a device barrier (one 32-thread kernel: system-scope
+ *   release of an epoch into every peer's flag slot, acquire-poll of its own;
+ *   CUDA-graph capturable; every rank must run the same barrier sequence).
+ * Any NCCL, group or peer communicator, even of world 1, selects the tensor-
  * parallel code path of the block calls; a loopback of world 1 does not.
  * ---------------------------------------------------------------------- */
+#define DL_IPC_HANDLE_BYTES 64
 dl_status dl_comm_create(void *nccl_comm, int rank, int world, dl_comm *out);
 dl_status dl_comm_create_group(int world, size_t sym_bytes, dl_comm *comms);
 dl_status dl_comm_create_loopback(int rank, int world, dl_comm *out);
+dl_status dl_comm_create_peer(int rank, int world, dl_comm *out);
+dl_status dl_comm_window_alloc(dl_comm comm, size_t bytes);
+dl_status dl_comm_window_handle(dl_comm comm, void *handle);
+dl_status dl_comm_window_connect(dl_comm comm, const void *handles);
 dl_status dl_comm_destroy(dl_comm comm);
 
 /* ------------------------------------------------------------------------
@@ -322,9 +350,9 @@ typedef enum { DL_PREFILL = 0, DL_DECODE = 1 } dl_phase;
  *            UNSUPPORTED (head_dim != 128), WORKSPACE, CUDA, NCCL.       */
 dl_status dl_block_workspace(const dl_block_config *cfg, int world,
                              size_t *bytes);
-/* Bytes of a group communicator's symmetric window (dl_comm_create_group
- * sym_bytes) that the fused collectives of this config need: with a group
- * communicator, the rank-parallel decode path (T <= 256) red.adds its
+/* Bytes of a communicator's symmetric window (dl_comm_create_group sym_bytes,
+ * or dl_comm_window_alloc) that the fused collectives of this config need:
+ * with a window, the rank-parallel decode path (T <= 256) red.adds its
  * stage-2 partials straight into the ranks' windows (all-reduce into every
  * rank's copy, reduce-scatter into the owner's) and pushes the attention
  * output into every rank's all-gather slot, so each collective is a barrier

@@ -29,7 +29,8 @@ EXPORTS = ("dl_last_error", "dl_version", "dl_device_ok", "dl_comm_create", "dl_
            "dl_profile_count", "dl_profile_get", "dl_debug_gemm_trace", "dl_deinfer_shard_factors",
            "dl_kv_prepare", "dl_decomposed_block_forward_kvlr", "dl_comm_create_loopback",
            "dl_decomposed_stack_forward", "dl_debug_ew_trace", "dl_debug_linear_gathered", "dl_argmax",
-           "dl_comm_create_group", "dl_block_window_bytes")
+           "dl_comm_create_group", "dl_block_window_bytes", "dl_comm_create_peer", "dl_comm_window_alloc",
+           "dl_comm_window_handle", "dl_comm_window_connect")
 
 
 class DLError(RuntimeError):
@@ -79,6 +80,9 @@ _lock = threading.Lock()
 _lib = None
 
 
+IPC_HANDLE_BYTES = 64   # DL_IPC_HANDLE_BYTES
+
+
 def load():
     """Load libdl.so (fails loudly if it was not built)."""
     global _lib
@@ -122,6 +126,10 @@ def load():
                                                      ctypes.c_size_t, P]
             lib.dl_deinfer_shard_factors.argtypes = [I, I, P, P, P, P, P, P, I64, I, I, I, P, I64, P, P, P]
             lib.dl_comm_create_loopback.argtypes = [I, I, ctypes.POINTER(P)]
+            lib.dl_comm_create_peer.argtypes = [I, I, ctypes.POINTER(P)]
+            lib.dl_comm_window_alloc.argtypes = [P, ctypes.c_size_t]
+            lib.dl_comm_window_handle.argtypes = [P, P]
+            lib.dl_comm_window_connect.argtypes = [P, P]
             lib.dl_kv_prepare.argtypes = [P, I64, P, I32, I64, I64, I64, P, P, P, P, P]
             lib.dl_decomposed_block_forward_kvlr.argtypes = [ctypes.POINTER(dl_block_config),
                                                              ctypes.POINTER(dl_block_weights), P, I64, P,
@@ -213,6 +221,44 @@ class Comm:
             self.is_loopback = False
             out.append(self)
         return out
+
+    @classmethod
+    def peer(cls, rank: int, world: int):
+        """Rank `rank` of `world` processes with only the fused decode collectives
+        (include/dl.h: dl_comm_create_peer); needs window_alloc + window_connect."""
+        self = cls.__new__(cls)
+        h = P()
+        _check(load().dl_comm_create_peer(rank, world, ctypes.byref(h)))
+        self.handle, self.rank, self.world = h, rank, world
+        self.is_loopback = False
+        return self
+
+    def window_alloc(self, nbytes: int):
+        """Allocate this rank's symmetric window (dl_comm_window_alloc)."""
+        _check(load().dl_comm_window_alloc(self.handle, nbytes))
+
+    def window_handle(self) -> bytes:
+        """This rank's window IPC handle (DL_IPC_HANDLE_BYTES bytes) to exchange with the peers."""
+        buf = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+        _check(load().dl_comm_window_handle(self.handle, ctypes.cast(buf, P)))
+        return buf.raw
+
+    def window_connect(self, handles):
+        """Map every rank's window (handles: one bytes object per rank, rank order)."""
+        blob = b"".join(handles)
+        if len(blob) != IPC_HANDLE_BYTES * self.world:
+            raise ValueError("need one IPC handle per rank")
+        buf = ctypes.create_string_buffer(blob, len(blob))
+        _check(load().dl_comm_window_connect(self.handle, ctypes.cast(buf, P)))
+
+    def window_exchange(self, nbytes: int, pg=None):
+        """window_alloc + an all-gather of the handles over a torch.distributed
+        process group (any backend) + window_connect."""
+        import torch.distributed as dist
+        self.window_alloc(nbytes)
+        hs = [None] * self.world
+        dist.all_gather_object(hs, self.window_handle(), group=pg)
+        self.window_connect(hs)
 
     def close(self):
         if self.handle:

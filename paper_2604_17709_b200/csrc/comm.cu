@@ -328,26 +328,85 @@ void group_release(CommGroup* g) {
 // ---------------------------------------------------------------------------
 // symmetric window of a group communicator (fused epilogue reductions)
 // ---------------------------------------------------------------------------
+namespace {
+// Device barrier of a multi-process window communicator (one 32-thread CTA,
+// launched in plain stream order, so every earlier kernel of this rank has
+// completed).  Thread 0 bumps this rank's epoch e, fences at system scope (the
+// release is cumulative: the completed kernels' stores into peer windows -- the
+// fused epilogue red.adds and pushes -- are ordered before it), stores e into
+// slot [rank] of every peer's flag area, then lane j waits until slot [j] of
+// its own area has reached e.  Epochs count barriers, so every rank must issue
+// the same barrier sequence (CUDA-graph replays included: the counter lives in
+// device memory).  A peer that never arrives traps after ~2^31 polls.
+struct PeerFlags {
+  uint32_t* slot[kMaxPeers];   // rank j's flag area (this process's mapping)
+};
+__global__ void __launch_bounds__(32) peer_barrier_kernel(PeerFlags f, int world, int rank) {
+  uint32_t* own = f.slot[rank];
+  __shared__ uint32_t e_sh;
+  if (threadIdx.x == 0) {
+    const uint32_t e = own[kMaxPeers] + 1;   // only this thread writes the counter
+    own[kMaxPeers] = e;
+    e_sh = e;
+    __threadfence_system();
+    for (int j = 0; j < world; ++j)
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f.slot[j] + rank), "r"(e) : "memory");
+  }
+  __syncwarp();
+  const uint32_t e = e_sh;
+  if (static_cast<int>(threadIdx.x) < world) {
+    const uint32_t* p = own + threadIdx.x;
+    unsigned long long polls = 0;
+    for (;;) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+      if (static_cast<int32_t>(v - e) >= 0) break;
+      if (++polls > (1ull << 31)) __trap();
+      __nanosleep(64);
+    }
+  }
+  __syncwarp();
+  __threadfence_system();
+}
+}  // namespace
+
 size_t comm_window_bytes(dl_comm c) {
-  return (c && c->kind == kCommGroup) ? c->group->sym_bytes : 0;
+  if (!c) return 0;
+  if (c->kind == kCommGroup) return c->group->sym_bytes;
+  return (c->win && c->win->connected) ? c->win->bytes : 0;
 }
 uint8_t* comm_window(dl_comm c, int rank) {
-  return c->group->sym + static_cast<size_t>(rank) * c->group->sym_bytes;
+  if (c->kind == kCommGroup) return c->group->sym + static_cast<size_t>(rank) * c->group->sym_bytes;
+  return c->win->peer[rank];
 }
 dl_status comm_barrier(dl_comm c, cudaStream_t st) {
-  if (c->kind != kCommGroup) {
-    set_error("comm_barrier: only group communicators have a device-visible window");
+  if (c->kind == kCommGroup) {
+    DL_TRY_INTERNAL(group_enter(c, st));
+    return group_sync(c, st);
+  }
+  if (!c->win || !c->win->connected) {
+    set_error("comm_barrier: the communicator has no connected window");
     return DL_ERR_UNSUPPORTED;
   }
-  DL_TRY_INTERNAL(group_enter(c, st));
-  return group_sync(c, st);
+  PeerFlags f{};
+  for (int j = 0; j < c->world; ++j) f.slot[j] = reinterpret_cast<uint32_t*>(c->win->peer[j] + c->win->bytes);
+  peer_barrier_kernel<<<1, 32, 0, st>>>(f, c->world, c->rank);
+  DL_TRY_INTERNAL(cuda_status(cudaGetLastError(), "peer barrier"));
+  return launched("peer barrier");
 }
 
 // ---------------------------------------------------------------------------
 // collectives used by api.cu
 // ---------------------------------------------------------------------------
+dl_status peer_unsupported(const char* what) {
+  set_error("%s: a window-only (peer) communicator carries only the fused rank-parallel decode collectives "
+            "(T <= 256, dl_block_window_bytes window); use an NCCL communicator with a window", what);
+  return DL_ERR_UNSUPPORTED;
+}
+
 dl_status coll_all_reduce(dl_comm c, void* buf, size_t count, int dtype, cudaStream_t st) {
   if (count == 0) return DL_OK;
+  if (c->kind == kCommPeer) return peer_unsupported("all-reduce");
   if (c->kind == kCommLoopback) return DL_OK;
   if (c->kind == kCommGroup) return group_all_reduce(c, buf, count, dtype, st);
   return nccl_check(c, c->allreduce(buf, buf, count, dtype, kNcclSum, c->nccl, st), "ncclAllReduce");
@@ -356,6 +415,7 @@ dl_status coll_all_reduce(dl_comm c, void* buf, size_t count, int dtype, cudaStr
 dl_status coll_reduce_scatter(dl_comm c, const void* src, void* dst, size_t recv_count, int dtype,
                               cudaStream_t st) {
   if (recv_count == 0) return DL_OK;
+  if (c->kind == kCommPeer) return peer_unsupported("reduce-scatter");
   if (c->kind == kCommLoopback) {
     const size_t b = recv_count * coll_esize(dtype);
     return cuda_status(cudaMemcpyAsync(dst, static_cast<const uint8_t*>(src) + c->rank * b, b,
@@ -367,6 +427,7 @@ dl_status coll_reduce_scatter(dl_comm c, const void* src, void* dst, size_t recv
 
 dl_status coll_all_gather(dl_comm c, const void* src, void* dst, size_t send_count, int dtype, cudaStream_t st) {
   if (send_count == 0) return DL_OK;
+  if (c->kind == kCommPeer) return peer_unsupported("all-gather");
   if (c->kind == kCommLoopback) {
     const size_t b = send_count * coll_esize(dtype);
     return cuda_status(cudaMemcpyAsync(static_cast<uint8_t*>(dst) + c->rank * b, src, b, cudaMemcpyDeviceToDevice,
@@ -454,9 +515,92 @@ dl_status dl_comm_create_group(int world, size_t sym_bytes, dl_comm* comms) {
   return DL_OK;
 }
 
+dl_status dl_comm_create_peer(int rank, int world, dl_comm* out) {
+  if (!out || world < 1 || world > kMaxPeers || rank < 0 || rank >= world) {
+    set_error("dl_comm_create_peer: need 1 <= world <= %d, 0 <= rank < world", kMaxPeers);
+    return DL_ERR_INVALID_ARG;
+  }
+  dl_comm_s c{};
+  c.kind = kCommPeer;
+  c.rank = rank;
+  c.world = world;
+  *out = new dl_comm_s(c);
+  return DL_OK;
+}
+
+dl_status dl_comm_window_alloc(dl_comm comm, size_t bytes) {
+  if (!comm || (comm->kind != kCommNccl && comm->kind != kCommPeer) || bytes < 256 || comm->world > kMaxPeers) {
+    set_error("dl_comm_window_alloc: an NCCL or peer communicator (world <= %d) and bytes >= 256", kMaxPeers);
+    return DL_ERR_INVALID_ARG;
+  }
+  if (comm->win) {
+    set_error("dl_comm_window_alloc: the communicator already has a window");
+    return DL_ERR_INVALID_ARG;
+  }
+  DL_TRY_INTERNAL(check_device_sm100());
+  PeerWindow* w = new PeerWindow();
+  w->bytes = (bytes + 255) & ~static_cast<size_t>(255);
+  cudaError_t e = cudaMalloc(&w->own, w->bytes + kFlagBytes);
+  if (e == cudaSuccess) e = cudaMemset(w->own, 0, w->bytes + kFlagBytes);   // buffers zero-maintained, epochs 0
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    if (w->own) cudaFree(w->own);
+    delete w;
+    return cuda_status(e, "dl_comm_window_alloc");
+  }
+  w->peer[comm->rank] = w->own;
+  comm->win = w;
+  return DL_OK;
+}
+
+static_assert(sizeof(cudaIpcMemHandle_t) == DL_IPC_HANDLE_BYTES, "IPC handle size");
+
+dl_status dl_comm_window_handle(dl_comm comm, void* handle) {
+  if (!comm || !comm->win || !handle) {
+    set_error("dl_comm_window_handle: no window (dl_comm_window_alloc first) or null handle");
+    return DL_ERR_INVALID_ARG;
+  }
+  cudaIpcMemHandle_t h;
+  DL_TRY_INTERNAL(cuda_status(cudaIpcGetMemHandle(&h, comm->win->own), "cudaIpcGetMemHandle"));
+  memcpy(handle, &h, sizeof(h));
+  return DL_OK;
+}
+
+dl_status dl_comm_window_connect(dl_comm comm, const void* handles) {
+  if (!comm || !comm->win || !handles || comm->win->connected) {
+    set_error("dl_comm_window_connect: needs an allocated, not yet connected window and the handles");
+    return DL_ERR_INVALID_ARG;
+  }
+  PeerWindow* w = comm->win;
+  for (int j = 0; j < comm->world; ++j) {
+    if (j == comm->rank) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, static_cast<const uint8_t*>(handles) + static_cast<size_t>(j) * DL_IPC_HANDLE_BYTES, sizeof(h));
+    void* p = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      for (int i = 0; i < j; ++i)
+        if (i != comm->rank && w->peer[i]) {
+          cudaIpcCloseMemHandle(w->peer[i]);
+          w->peer[i] = nullptr;
+        }
+      return cuda_status(e, "cudaIpcOpenMemHandle");
+    }
+    w->peer[j] = static_cast<uint8_t*>(p);
+  }
+  w->connected = true;
+  return DL_OK;
+}
+
 dl_status dl_comm_destroy(dl_comm comm) {
   if (!comm) return DL_OK;
   if (comm->kind == kCommGroup && comm->group) group_release(comm->group);
+  if (comm->win) {
+    for (int j = 0; j < comm->world; ++j)
+      if (j != comm->rank && comm->win->peer[j]) cudaIpcCloseMemHandle(comm->win->peer[j]);
+    if (comm->win->own) cudaFree(comm->win->own);
+    delete comm->win;
+  }
   delete comm;
   return DL_OK;
 }

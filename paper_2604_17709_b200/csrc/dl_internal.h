@@ -27,7 +27,18 @@
 
 namespace dl {
 struct CommGroup;   // comm.cu
-enum CommKind { kCommNccl = 0, kCommLoopback = 1, kCommGroup = 2 };
+enum CommKind { kCommNccl = 0, kCommLoopback = 1, kCommGroup = 2, kCommPeer = 3 };
+constexpr int kMaxPeers = 8;
+// Multi-process symmetric window (dl_comm_window_*): this rank's window and
+// its peers' windows mapped into this process (CUDA IPC), plus a flag area
+// after each window for the device-side barrier.
+struct PeerWindow {
+  uint8_t* own = nullptr;                 // cudaMalloc'd: bytes of buffers + kFlagBytes of flags
+  size_t bytes = 0;                       // buffer bytes (the flags follow)
+  uint8_t* peer[kMaxPeers] = {};          // rank j's window in this address space (peer[rank] = own)
+  bool connected = false;
+};
+constexpr size_t kFlagBytes = 256;        // [kMaxPeers] u32 arrival epochs, then this rank's u32 epoch counter
 // NCCL dtype codes (ncclFloat32 / ncclBfloat16), also used by the other kinds
 constexpr int kCollF32 = 7;
 constexpr int kCollBF16 = 9;
@@ -46,6 +57,7 @@ struct dl_comm_s {
   dl::nccl_allgather_fn allgather;
   dl::nccl_errstr_fn errstr;
   dl::CommGroup* group;   // kCommGroup: shared by the group's ranks
+  dl::PeerWindow* win;    // kCommNccl / kCommPeer: multi-process symmetric window (null: none)
 };
 
 namespace dl {
