@@ -812,10 +812,18 @@ bool use_zred() {
 // zero_out != NULL (skinny path): stage 1 red.adds its partials straight into
 // the bf16 Z buffer ws.zr (no fp32 -> bf16 pass); *zero_out is then the clear
 // of that buffer, which the caller hands to the kernel that follows stage 2.
+// In-kernel activation of a stage 1 (GemmProblem::xform): mode, reduced
+// gate|up rows and their layout.
+struct Xform {
+  int mode = XFORM_NONE;
+  const __nv_bfloat16* src = nullptr;
+  int64_t ld = 0, m = 0;
+};
+
 dl_status run_group(const dl_factor_group& grp, int nseg, const int64_t* rows, const __nv_bfloat16* act,
                     int64_t ld_act, int64_t n, int64_t T, bool skinny, const BlockWs& ws, const GemmOut& out2,
                     cudaStream_t st, const GemmFixup* fix2 = nullptr, SideZero* zero_out = nullptr,
-                    int zslot = 0, int act_p = 0, int64_t act_w = 0) {
+                    int zslot = 0, int act_p = 0, int64_t act_w = 0, const Xform& xf = Xform{}) {
   // act_p > 1 (skinny only): act is a rank-major all-gather output read through a 3-D map
   const ZLayout zl = zlayout(grp, nseg);
   if (zero_out) *zero_out = SideZero{};
@@ -826,6 +834,10 @@ dl_status run_group(const dl_factor_group& grp, int nseg, const int64_t* rows, c
     p1.sched = next_sched(ws.sched);
     p1.act_p = act_p;
     p1.act_w = act_w;
+    p1.xform = xf.mode;
+    p1.xsrc = xf.src;
+    p1.xld = xf.ld;
+    p1.xm = xf.m;
     GemmProblem p2 = stage2(grp, nseg, rows, z, ldz, T, zl, out2);
     p2.sched = next_sched(ws.sched);
     if (fix2 && fix2->op != FIX_NONE) p2.fix = *fix2;
@@ -1485,8 +1497,8 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   }
 
   // Finish a [T x n] group output: + residual (o, down) with the TP reduction.
-  auto finish_residual = [&](int64_t n, const SideZero& z) -> dl_status {
-    if (!tp) return skinny ? launch_residual_add_f32(ws.yf, ws.ldy32, x, d.h, T, n, 1, st, z) : DL_OK;
+  auto finish_residual = [&](int64_t n, const SideZero& z, const SideZero& z2 = SideZero{}) -> dl_status {
+    if (!tp) return skinny ? launch_residual_add_f32(ws.yf, ws.ldy32, x, d.h, T, n, 1, st, z, z2) : DL_OK;
     if (tpr) {
       DL_TRY(all_reduce_bf16(arY, n));
       return launch_residual_add_bf16(arY, n, x, d.h, T, n, st, 1, z);
@@ -1540,11 +1552,20 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   // bf16-rounded anyway); halves the reduction and finalize traffic (DL_GU_F32 A/B)
   static const bool gu_f32 = DL_ENV("DL_GU_F32") != nullptr;
   const bool gur = skinny && !tp && use_zred() && !fx_gu && !gu_f32;
+  // the MLP activation inside the down projection's stage 1 instead of the SiLU kernel
+  // (DL_XACT=1, A/B): measured 29.7 vs 26.2 ms/step -- every one of the 39 feature tiles
+  // of the down stage 1 recomputes the activation of its k-range (71.6 M SiLUs per layer
+  // for 1.8 M outputs), DESIGN.md §6
+  static const bool xact_env = DL_ENV("DL_XACT") && atoi(DL_ENV("DL_XACT")) != 0;
+  const bool xact = gur && xact_env && d.m % 8 == 0 && ngu % 8 == 0;
   if (tpr || gur) gu_out = fan_ar(out_plain(arX, ngu, OUT_BF16_RED, 0), ngu);
   const GemmFixup fsilu = fixup(fx_gu ? FIX_SILU : FIX_NONE);
   DL_TRY(run_group(w->gu, n_gu, gu_rows, ws.xn, d.h, d.h, T, skinny, ws, gu_out, st, &fsilu, fx ? nullptr : &zg, 1));
   if (fx_gu) {
     // SiLU(gate)*up done by the gate|up stage-2 fixup
+  } else if (!tp && gur && xact) {
+    // SiLU(gate)*up / ReLU(up) computed by the down projection's stage 1 itself
+    // (in-kernel activation); its gate|up source and latent are cleared below
   } else if (!tp && gur) {
     if (d.glu) DL_TRY(launch_silu_mul_bf16(ws.yr, ngu, ws.act, d.m, T, d.m, st, 1, zg));
     else DL_TRY(launch_relu_bf16(ws.yr, ngu, ws.act, d.m, T, d.m, st, 1, zg));
@@ -1561,12 +1582,24 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
     if (d.glu) DL_TRY(launch_silu_mul_bf16(ws.yb, ngu, ws.act, d.m, T, d.m, st));
     else DL_TRY(launch_relu_bf16(ws.yb, ngu, ws.act, d.m, T, d.m, st));
   }
-  DL_TRY(run_group(w->down, 1, h_rows, ws.act, d.m, d.m, T, skinny, ws, resid_out(), st, &fres, fx ? nullptr : &zd));
-  if (fx_gu && zg.p && zd.p) zd.row_bytes = ws.ldzb * 2 + zg.row_bytes;   // slot 0 + the gate|up latent in slot 1
+  Xform xf;
+  SideZero zyr;   // in-kernel activation: the gate|up rows, cleared once the down stage 1 has read them
+  if (!tp && gur && xact) {
+    xf.mode = d.glu ? XFORM_SILU : XFORM_RELU;
+    xf.src = ws.yr;
+    xf.ld = ngu;
+    xf.m = d.m;
+    zyr.p = ws.yr;
+    zyr.rows = 1;
+    zyr.row_bytes = zyr.ld = static_cast<int64_t>(T) * ngu * 2;
+  }
+  DL_TRY(run_group(w->down, 1, h_rows, ws.act, d.m, d.m, T, skinny, ws, resid_out(), st, &fres, fx ? nullptr : &zd, 0,
+                   0, 0, xf));
+  if ((fx_gu || xf.mode) && zg.p && zd.p) zd.row_bytes = ws.ldzb * 2 + zg.row_bytes;   // slot 0 + the gate|up latent in slot 1
   if (next_norm && !fx && !tp && skinny && !no_fuse) {
     // residual add of the down projection fused with the next block's pre-norm
     DL_TRY(launch_residual_rmsnorm(ws.yf, ws.ldy32, x, static_cast<const __nv_bfloat16*>(next_norm), ws.xn, T, d.h,
-                                   cfg->rms_eps, st, zd));
+                                   cfg->rms_eps, st, zd, zyr));
     *next_normed = true;
     return DL_OK;
   }
@@ -1577,7 +1610,7 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
     *next_normed = true;
     return DL_OK;
   }
-  if (!fx) DL_TRY(finish_residual(d.h, zd));
+  if (!fx) DL_TRY(finish_residual(d.h, zd, zyr));
   return DL_OK;
 }
 }  // namespace

@@ -243,7 +243,17 @@ struct GemmProblem {
   // through a 3-D map, so no un-permute pass is needed.
   int act_p;
   int64_t act_w;
+  // xform != 0 (swap-AB stream-K only): the activation operand is not read by
+  // TMA but computed by the kernel's epilogue warps from xsrc [T x xld] bf16
+  // (the reduced gate|up output of the previous group): XFORM_SILU: act[t][c] =
+  // silu(xsrc[t][c]) * xsrc[t][xm + c]; XFORM_RELU: act[t][c] = relu(xsrc[t][c]);
+  // columns c >= k_act read as zero.  Replaces the SiLU / ReLU kernel between
+  // the MLP's gate|up and down projections (the down group's stage 1).
+  int xform;
+  const __nv_bfloat16* xsrc;
+  int64_t xld, xm;
 };
+enum XformMode { XFORM_NONE = 0, XFORM_SILU = 1, XFORM_RELU = 2 };
 
 // Picks the tile configuration (swap-AB for T <= 256, stream-K when the
 // output is fp32-reduced) and launches.  `stream_k` requires OUT_F32_RED.
@@ -309,7 +319,8 @@ dl_status launch_f32_to_bf16(float* acc, int64_t ld_acc, __nv_bfloat16* out,
 // x[t][c] = bf16(x + acc) ; acc cleared
 dl_status launch_residual_add_f32(float* acc, int64_t ld_acc, __nv_bfloat16* x,
                                   int64_t ldx, int64_t T, int64_t n,
-                                  int clear, cudaStream_t st, const SideZero& z = SideZero{});
+                                  int clear, cudaStream_t st, const SideZero& z = SideZero{},
+                                  const SideZero& z2 = SideZero{});
 // x[t][c] = bf16(x + acc) (acc cleared), then y = rmsnorm(x) * g   (h % 8 == 0)
 dl_status launch_residual_rmsnorm(float* acc, int64_t lda, __nv_bfloat16* x, const __nv_bfloat16* g,
                                   __nv_bfloat16* y, int64_t T, int64_t h, float eps, cudaStream_t st,

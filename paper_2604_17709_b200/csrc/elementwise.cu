@@ -367,20 +367,22 @@ dl_status launch_silu_flat(Acc* acc, int64_t lda, __nv_bfloat16* act, int64_t ld
 
 // 2-D elementwise over [T x n] in groups of 4 columns: grid (ceil(n/4/256), T).
 template <typename F>
-__global__ void __launch_bounds__(256) ew4_kernel(int n4, F f, SideZero z) {
+__global__ void __launch_bounds__(256) ew4_kernel(int n4, F f, SideZero z, SideZero z2) {
   pdl_trigger();   // successor may launch now; it waits for us before reading
   pdl_wait();
   side_zero(z);
+  side_zero(z2);
   const int c4 = blockIdx.x * blockDim.x + threadIdx.x;
   if (c4 < n4) f(static_cast<int64_t>(blockIdx.y), c4 * 4);
 }
 
 template <typename F>
-dl_status launch_ew4(int64_t T, int64_t n, F f, cudaStream_t st, const char* what, const SideZero& z = SideZero{}) {
+dl_status launch_ew4(int64_t T, int64_t n, F f, cudaStream_t st, const char* what, const SideZero& z = SideZero{},
+                     const SideZero& z2 = SideZero{}) {
   if (T <= 0 || n <= 0) return DL_OK;
   const int n4 = static_cast<int>(n / 4);
   dim3 grid((n4 + 255) / 256, static_cast<unsigned>(T));
-  return launch_pdl(ew4_kernel<F>, grid, dim3(256), 0, st, what, n4, f, z);
+  return launch_pdl(ew4_kernel<F>, grid, dim3(256), 0, st, what, n4, f, z, z2);
 }
 
 __device__ __forceinline__ float4 take4(float* p, int clear) {
@@ -905,8 +907,8 @@ dl_status launch_f32_to_bf16(float* acc, int64_t lda, __nv_bfloat16* out, int64_
   return launch_ew4(T, n, F32ToBf16{acc, lda, out, ldo, clear}, st, "f32_to_bf16", z);
 }
 dl_status launch_residual_add_f32(float* acc, int64_t lda, __nv_bfloat16* x, int64_t ldx, int64_t T, int64_t n,
-                                  int clear, cudaStream_t st, const SideZero& z) {
-  return launch_ew4(T, n, ResidualAdd{acc, lda, x, ldx, clear}, st, "residual_add", z);
+                                  int clear, cudaStream_t st, const SideZero& z, const SideZero& z2) {
+  return launch_ew4(T, n, ResidualAdd{acc, lda, x, ldx, clear}, st, "residual_add", z, z2);
 }
 dl_status launch_residual_add_bf16(const __nv_bfloat16* y, int64_t ldy, __nv_bfloat16* x, int64_t ldx, int64_t T,
                                    int64_t n, cudaStream_t st, int clear, const SideZero& z) {

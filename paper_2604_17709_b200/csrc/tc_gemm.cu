@@ -87,6 +87,10 @@ struct KArgs {
   int relaxed_acce;
   int stage_out;             // pair kernel: bf16 stores through the shared-memory transpose (bit 0 plain, bit 1 Y +=; DL_STAGE_OUT)          // accumulator-empty arrivals without release semantics (DL_ACCE_RELEASE=1: off)
   int act_w;                 // > 0: 3-D activation map, column c -> (c % act_w, token, c / act_w)
+  int xform;                 // XformMode: activation computed in-kernel from xsrc (GemmProblem::xform)
+  const __nv_bfloat16* xsrc;
+  long long xld;
+  int xm, xcols;
   int wpol;                  // pair kernel weight L2 policy: 0 evict_first, 1 evict_normal, 2 evict_last
   // DP + stream-K tail (whole-tile kernels): tiles [0, dp_tiles) whole, each of
   // the remaining tiles split in tail_split K-pieces accumulated in fp32 into
@@ -604,6 +608,57 @@ __device__ __forceinline__ void epilogue_job(const KArgs& a, const Job& j, uint3
   }
 }
 
+// One activation tile of the xform mode (GemmProblem::xform) into the act half
+// of a ring slot: BN token rows x 64 k columns, K-major with the 128-byte
+// swizzle TMA would have used (16-byte chunk c of row t at chunk c ^ (t & 7)).
+// One warp; each lane loads 8 chunks' gate / up rows (all in flight), then
+// computes and stores them (the same fp32 expression and bf16 rounding as the
+// SiLU kernel it replaces).
+template <int BN>
+__device__ __forceinline__ void xform_tile(const KArgs& a, uint8_t* dst, int tok0, int k0, int lane) {
+  constexpr int CH = BN * 8;   // 16-byte chunks in the tile
+  constexpr int PER = 8;       // chunks per lane per batch
+#pragma unroll 1
+  for (int base = 0; base < CH; base += 32 * PER) {
+    uint4 g[PER], u[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int i = base + q * 32 + lane, t = i >> 3, c = i & 7;
+      const int tok = tok0 + t, k = k0 + c * 8;
+      g[q] = u[q] = make_uint4(0u, 0u, 0u, 0u);
+      if (i < CH && tok < a.T && k < a.xcols) {
+        const __nv_bfloat16* row = a.xsrc + static_cast<long long>(tok) * a.xld + k;
+        u[q] = __ldcg(reinterpret_cast<const uint4*>(row + a.xm));
+        if (a.xform == XFORM_SILU) g[q] = __ldcg(reinterpret_cast<const uint4*>(row));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int i = base + q * 32 + lane, t = i >> 3, c = i & 7;
+      if (i >= CH) continue;
+      const __nv_bfloat162* gb = reinterpret_cast<const __nv_bfloat162*>(&g[q]);
+      const __nv_bfloat162* ub = reinterpret_cast<const __nv_bfloat162*>(&u[q]);
+      uint4 o;
+      __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 uf = __bfloat1622float2(ub[e]);
+        float2 r;
+        if (a.xform == XFORM_SILU) {
+          const float2 gf = __bfloat1622float2(gb[e]);
+          r.x = __fdividef(gf.x, 1.f + __expf(-gf.x)) * uf.x;
+          r.y = __fdividef(gf.y, 1.f + __expf(-gf.y)) * uf.y;
+        } else {
+          r.x = fmaxf(uf.x, 0.f);
+          r.y = fmaxf(uf.y, 0.f);
+        }
+        ob[e] = __floats2bfloat162_rn(r.x, r.y);
+      }
+      *reinterpret_cast<uint4*>(dst + t * 128 + ((c ^ (t & 7)) << 4)) = o;
+    }
+  }
+}
+
 // A {counter, done} pair is reset for the next launch by the last of the
 // grid's CTAs to be finished with c[0]: each calls this once, after its last
 // access to c[0] (release: that access is ordered before the done count).
@@ -675,7 +730,8 @@ __global__ void __launch_bounds__(kThreads, (SWAP && STAGES <= 4) ? 2 : 1)
       for (int g = 0; g < a2.nseg; ++g) ptx::prefetch_tmap(&maps2.w[g]);
     }
     for (int s = 0; s < STAGES; ++s) {
-      ptx::mbar_init(&full_bar[s], 1);
+      // xform: the producer's weight bytes and one epilogue warp's activation tile
+      ptx::mbar_init(&full_bar[s], (SWAP && a.xform) ? 2 : 1);
       ptx::mbar_init(&empty_bar[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -760,7 +816,7 @@ __global__ void __launch_bounds__(kThreads, (SWAP && STAGES <= 4) ? 2 : 1)
             release_pair(chain);
           }
           waited = true;
-          for (int i = 0; i < u && i < STAGES; ++i) {
+          for (int i = 0; i < u && i < STAGES && !A.xform; ++i) {
             uint8_t* dst = smem + pend_st[i] * STAGE_BYTES + (SWAP ? P_BYTES : 0);
             act_load(dst, &full_bar[pend_st[i]], pend_c0[i], pend_c1[i]);
           }
@@ -788,12 +844,14 @@ __global__ void __launch_bounds__(kThreads, (SWAP && STAGES <= 4) ? 2 : 1)
             ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
             uint8_t* sp = smem + stage * STAGE_BYTES;
             uint8_t* sq = sp + P_BYTES;
-            ptx::mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES);
+            ptx::mbar_arrive_expect_tx(&full_bar[stage], (SWAP && A.xform) ? P_BYTES : STAGE_BYTES);
             const int kx = kb * BK;
             uint8_t* sw = SWAP ? sp : sq;
             uint8_t* sa = SWAP ? sq : sp;
             ptx::tma_load_2d(sw, &M.w[jb.seg], &full_bar[stage], kx, jb.feat0 - s.feat_begin, pol_w);
-            if (waited) {
+            if (SWAP && A.xform) {
+              // the activation half is written by an epilogue warp (xform_tile)
+            } else if (waited) {
               act_load(sa, &full_bar[stage], s.act_koff + kx, jb.tok0);
             } else {
               pend_c0[u] = s.act_koff + kx;
@@ -884,6 +942,56 @@ __global__ void __launch_bounds__(kThreads, (SWAP && STAGES <= 4) ? 2 : 1)
     uint32_t acc_phase = 0;
     int jslot = 0;
     uint32_t jphase = 0;
+    if (SWAP && !CHAIN && a.xform) {
+      // The activation operand is computed here (GemmProblem::xform): for every
+      // unit of a job, epilogue warp (unit % 8) waits for the ring slot, writes
+      // the activation tile act[tok][k] = silu(gate) * up (or relu(up)) from the
+      // reduced gate|up rows into the slot's swizzled act half and arrives on its
+      // full barrier next to the producer's weight bytes.  Each job's accumulator
+      // epilogue runs after the NEXT job's tiles are out, so the MMA never waits
+      // for an epilogue to get its activations.
+      const int ew = warp - 2;
+      int xs = 0, xu = 0;
+      uint32_t xph = 0;
+      Job prev{};
+      int prev_slot = -1;
+      auto epilogue_of = [&](const Job& jb, int slot) {
+        ptx::mbar_wait(&accf_bar[acc], acc_phase);
+        ptx::tc_fence_after();
+        epilogue_job<BN, SWAP>(a, jb, tmem_base, acc, warp, lane);
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (a.relaxed_acce) ptx::mbar_arrive_relaxed(&acce_bar[acc]);
+          else ptx::mbar_arrive(&acce_bar[acc]);
+          ptx::mbar_arrive(&jempty_bar[slot]);
+        }
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      };
+      for (;;) {
+        ptx::mbar_wait(&jfull_bar[jslot], jphase);
+        j = jobs[jslot];
+        const int my_slot = jslot;
+        if (++jslot == kJobRing) { jslot = 0; jphase ^= 1; }
+        if (j.seg < 0) break;
+        const KSeg& s = a.seg[j.seg];
+        for (int kb = j.kb0; kb < j.kb1; ++kb) {
+          if ((xu & 7) == ew) {
+            ptx::mbar_wait(&empty_bar[xs], xph ^ 1);
+            xform_tile<BN>(a, smem + xs * STAGE_BYTES + P_BYTES, j.tok0, s.act_koff + kb * BK, lane);
+            ptx::fence_async_smem();   // generic stores before the MMA's async-proxy reads
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&full_bar[xs]);
+          }
+          ++xu;
+          if (++xs == STAGES) { xs = 0; xph ^= 1; }
+        }
+        if (prev_slot >= 0) epilogue_of(prev, prev_slot);
+        prev = j;
+        prev_slot = my_slot;
+      }
+      if (prev_slot >= 0) epilogue_of(prev, prev_slot);
+    } else
     for (;;) {
       ptx::mbar_wait(&jfull_bar[jslot], jphase);
       j = jobs[jslot];
@@ -1368,7 +1476,20 @@ dl_status prep_args(const GemmProblem& p, bool stream_k, KMaps& maps, KArgs& a, 
     }
   }
   a.act_w = 0;
-  if (p.act_p > 1) {
+  a.xform = XFORM_NONE;
+  if (p.xform != XFORM_NONE) {
+    if (!SWAP || PAIR || !stream_k || p.fix.op != FIX_NONE || !p.xsrc || p.act_p > 1 || p.xld % 8 || p.xm % 8 ||
+        p.k_act % 8) {
+      set_error("tc_gemm: in-kernel activation (xform) needs the swap-AB stream-K path, 16-byte rows, no fixup");
+      return DL_ERR_INVALID_ARG;
+    }
+    a.xform = p.xform;
+    a.xsrc = p.xsrc;
+    a.xld = p.xld;
+    a.xm = static_cast<int>(p.xform == XFORM_SILU ? p.xm : 0);
+    a.xcols = static_cast<int>(p.k_act);
+    maps.act = maps.w[0];   // never read by TMA (a valid map for the descriptor prefetch)
+  } else if (p.act_p > 1) {
     if (!SWAP || PAIR || p.act_w % BK || p.act_w * p.act_p != p.k_act) {
       set_error("3-D activation layout: swap-AB path with act_w %% 64 == 0 and act_p * act_w == k_act only");
       return DL_ERR_UNSUPPORTED;

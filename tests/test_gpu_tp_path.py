@@ -128,7 +128,7 @@ print("ERRS", errs)
 
 @pytest.mark.parametrize("knob", ["DL_FIXUP", "DL_ROPE_FUSE", "DL_FIXUP_ROPE", "DL_ATTN_SPLIT", "DL_ZRED=0",
                                   "DL_GU_F32", "DL_SILU_EW4", "DL_NO_FUSE_RESNORM", "DL_ATTN_CFG=23",
-                                  "DL_CHAIN=1"])
+                                  "DL_CHAIN=1", "DL_XACT=1"])
 def test_block_decode_stream_k_fixups(knob):
     """Every A/B switch's decode variant must match the oracle too:
     stream-K fixups, RoPE inside the attention, the split-KV attention fallback,
