@@ -305,9 +305,20 @@ __device__ __forceinline__ void zero8(float* p) {
 }
 __device__ __forceinline__ void zero8(__nv_bfloat16* p) { *reinterpret_cast<uint4*>(p) = make_uint4(0u, 0u, 0u, 0u); }
 
+// SiLU through one MUFU op: g * sigmoid(g) = r + r * tanh(r), r = g / 2
+// (tanh.approx: relative error ~2^-11, below the bf16 rounding of the result);
+// exp + reciprocal took two MUFU ops per element, which bound the 58.7 M-element
+// prefill SiLU (2,048 x 28,672) as much as its 352 MB of traffic.
+__device__ __forceinline__ float silu_tanh(float g) {
+  const float r = 0.5f * g;
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(r));
+  return fmaf(r, t, r);
+}
+
 // 2-D grid (column blocks, tokens): row t = blockIdx.y, thread items
 // c = blockIdx.x * 256 + tid + u * gridDim.x * 256 (8 columns each) -- no
-// per-item integer division; fast sigmoid (__expf, __fdividef).
+// per-item integer division; fast sigmoid (silu_tanh).
 template <typename Acc>
 __global__ void __launch_bounds__(256) silu_mul_kernel(Acc* __restrict__ acc, int64_t lda, __nv_bfloat16* __restrict__ out,
                                                        int64_t ldo, int m, int T, int relu, int clear, SideZero z,
@@ -344,7 +355,7 @@ __global__ void __launch_bounds__(256) silu_mul_kernel(Acc* __restrict__ acc, in
     } else {
       if (clear) zero8(row + i * 8);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) o[e] = __fdividef(gv[u][e], 1.f + __expf(-gv[u][e])) * uv[u][e];
+      for (int e = 0; e < 8; ++e) o[e] = silu_tanh(gv[u][e]) * uv[u][e];
     }
     uint4 pk;
     __nv_bfloat162* pb = reinterpret_cast<__nv_bfloat162*>(&pk);
@@ -470,7 +481,7 @@ struct ReluBf16 {
 // positions, cache lengths and cu_seqlens are call inputs) and applied to
 // kRopeHeads heads; grid (head groups, tokens), 128 threads = 2 x 64 pairs.
 constexpr int kRopeHeads = 5;
-constexpr int kRopeVec = 2;   // rotation pairs per thread (8-byte bf16 accesses)
+constexpr int kRopeVec = 4;   // rotation pairs per thread (16-byte bf16 accesses; the body assumes 4)
 __global__ void __launch_bounds__(128) rope_cache_kernel(RopeCacheArgs a, EwTrace tr) {
   ew_mark(tr, 1);
   pdl_trigger();   // successor may launch now; it waits for us before reading
@@ -521,7 +532,8 @@ __global__ void __launch_bounds__(128) rope_cache_kernel(RopeCacheArgs a, EwTrac
   side_zero(a.zero);
   side_zero(a.zero2);
   if (!active) return;
-  float4 v[kRopeHeads];
+  constexpr int NV = 2 * kRopeVec;   // values per thread and head
+  float v[kRopeHeads][NV];
 #pragma unroll
   for (int j = 0; j < kRopeHeads; ++j) {
     const int hd = h0 + j;
@@ -529,28 +541,40 @@ __global__ void __launch_bounds__(128) rope_cache_kernel(RopeCacheArgs a, EwTrac
     const int64_t col = static_cast<int64_t>(hd) * a.d + 2 * p0;
     if (a.acc) {
       float* q = const_cast<float*>(a.acc) + t * a.ld_src + col;
-      v[j] = *reinterpret_cast<const float4*>(q);
-      if (a.clear) *reinterpret_cast<float4*>(q) = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int e = 0; e < NV; e += 4) {
+        const float4 f = *reinterpret_cast<const float4*>(q + e);
+        v[j][e] = f.x; v[j][e + 1] = f.y; v[j][e + 2] = f.z; v[j][e + 3] = f.w;
+        if (a.clear) *reinterpret_cast<float4*>(q + e) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
     } else {
-      v[j] = load4(a.src + t * a.ld_src + col);
+      ld8(a.src + t * a.ld_src + col, v[j]);   // NV == 8: one 16-byte load
     }
   }
 #pragma unroll
   for (int j = 0; j < kRopeHeads; ++j) {
     const int hd = h0 + j;
     if (hd >= heads) break;
-    float4 r = v[j];
-    if (a.rope && hd < a.Hq + a.Hk)
-      r = make_float4(r.x * cs[0] - r.y * sn[0], r.x * sn[0] + r.y * cs[0], r.z * cs[1] - r.w * sn[1],
-                      r.z * sn[1] + r.w * cs[1]);
+    float r[NV];
+#pragma unroll
+    for (int q = 0; q < kRopeVec; ++q) {
+      const float x = v[j][2 * q], y = v[j][2 * q + 1];
+      const bool rot = a.rope && hd < a.Hq + a.Hk;
+      r[2 * q] = rot ? x * cs[q] - y * sn[q] : x;
+      r[2 * q + 1] = rot ? x * sn[q] + y * cs[q] : y;
+    }
+    uint4 pk;
+    __nv_bfloat162* pb = reinterpret_cast<__nv_bfloat162*>(&pk);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) pb[e] = __floats2bfloat162_rn(r[2 * e], r[2 * e + 1]);
     if (hd < a.Hq) {
-      store4(a.q_out + t * static_cast<int64_t>(a.Hq) * a.d + static_cast<int64_t>(hd) * a.d + 2 * p0, r.x, r.y, r.z,
-             r.w);
+      *reinterpret_cast<uint4*>(a.q_out + t * static_cast<int64_t>(a.Hq) * a.d + static_cast<int64_t>(hd) * a.d +
+                                2 * p0) = pk;
     } else if (slot >= 0) {
       const bool is_k = hd < a.Hq + a.Hk;
       const int kvh = is_k ? hd - a.Hq : hd - a.Hq - a.Hk;
-      store4((is_k ? a.k_cache : a.v_cache) + (slot + static_cast<int64_t>(kvh) * a.max_seq) * a.d + 2 * p0, r.x, r.y,
-             r.z, r.w);
+      *reinterpret_cast<uint4*>((is_k ? a.k_cache : a.v_cache) +
+                                (slot + static_cast<int64_t>(kvh) * a.max_seq) * a.d + 2 * p0) = pk;
     }
   }
   ew_mark(tr, 3);
