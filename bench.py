@@ -52,9 +52,10 @@ def parse():
                    help="decode KV cache: post-RoPE K/V, or the paged low-rank (latent) cache with the "
                         "two-stage reconstruction (P:111, P:219-237)")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--no-tp-window", action="store_true",
-                   help="TP > 1: plain NCCL collectives instead of the fused epilogue reductions "
-                        "through CUDA-IPC symmetric windows (include/dl.h dl_comm_window_*)")
+    p.add_argument("--tp-window", action="store_true",
+                   help="TP > 1: fused epilogue reductions through CUDA-IPC symmetric windows over NVLink "
+                        "(include/dl.h dl_comm_window_*; verified with two processes on one GPU, not yet on "
+                        "a multi-GPU node) instead of NCCL collectives")
     p.add_argument("--cpu-sample-seqs", type=int, default=64)
     return p.parse_args()
 
@@ -263,7 +264,7 @@ def main():
     # TP > 1, rank-parallel: a symmetric window per rank mapped into every peer (CUDA IPC over
     # NVLink) so the decode path's reductions run inside the stage-2 epilogues
     tp_coll = "nccl" if world > 1 else "none"
-    if world > 1 and args.layout == "rp" and not args.no_tp_window:
+    if world > 1 and args.layout == "rp" and args.tp_window:
         # every rank must take the same path: agree on success after each stage
         def agree(flag):
             t = torch.tensor([1 if flag else 0], device=dev)
@@ -283,7 +284,7 @@ def main():
             except Exception as e:   # noqa: BLE001
                 err = str(e)[:120]
             if not agree(not err):
-                raise SystemExit(f"TP window: connect failed on some rank ({err or 'peer'}); rerun with --no-tp-window")
+                raise SystemExit(f"TP window: connect failed on some rank ({err or 'peer'}); rerun without --tp-window")
             tp_coll = "fused-window (decode) + nccl (prefill)"
         else:
             tp_coll = f"nccl (window setup failed: {err or 'on a peer'})"
