@@ -43,10 +43,8 @@ constexpr int BARS = 32 * 8;           // 22 mbarriers, the TMEM address slot, d
 constexpr int SMEM = 7 * TILE + XCHG + BARS;   // Q, K[3], V[3], exchange, barriers (no static smem)
 constexpr uint32_t TMEM_COLS = 512;    // S/P[0] cols 0-127, S/P[1] 128-255, O 256-383, Q 384-447
 constexpr float kRescale = 8.f;        // log2 units
-#ifndef DL_FA_FMA_EXP
-#define DL_FA_FMA_EXP 0
-#endif
-constexpr int kFmaExp = DL_FA_FMA_EXP;  // exp2 of this many of every 8 scores on the FMA pipe (3 measured slower: the softmax is not MUFU-bound)
+// exp2 of FMAE of every 8 scores on the FMA pipe (template argument; DL_FA_FMA_EXP
+// selects it in the A/B build): 3 measured 10 % slower (the softmax is issue-bound)
 constexpr uint32_t IDESC_S = ptx::idesc_bf16_f32(128, 128);                // A, B K-major
 constexpr uint32_t IDESC_PV = ptx::idesc_bf16_f32(128, 128) | (1u << 16);  // B (V) MN-major
 }  // namespace fa
@@ -135,6 +133,7 @@ __device__ __forceinline__ int fa_snake(int k, int C) {
   return k * G + ((k & 1) ? G - 1 - c : c);
 }
 
+template <int FMAE>
 __global__ void __launch_bounds__(fa::kThreads, 1)
     attn_prefill_tc_kernel(const __grid_constant__ FaMaps maps, const __grid_constant__ FaArgs a) {
   using namespace fa;
@@ -459,7 +458,7 @@ __global__ void __launch_bounds__(fa::kThreads, 1)
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const float xe = fmaf(x[c * 8 + e], a.scale_log2, -m);
-            p[e] = e < kFmaExp ? ex2_fma(xe) : ex2(xe);   // kFmaExp of 8 on the FMA pipe
+            p[e] = e < FMAE ? ex2_fma(xe) : ex2(xe);   // FMAE of 8 on the FMA pipe
             sum8[e] += p[e];
           }
 #pragma unroll
@@ -585,11 +584,16 @@ dl_status launch_attention_prefill_tc(const AttnArgs& a, cudaStream_t st) {
   k.items = k.qtiles * a.num_seqs * a.Hk * k.hgroups;
   k.tr = ew_trace(5);
   k.ctr = gemm_trace_cta_slots(1);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+  static const int fmae = DL_ENV("DL_FA_FMA_EXP") ? atoi(DL_ENV("DL_FA_FMA_EXP")) : 0;
+  void (*kern)(FaMaps, FaArgs) = fmae == 1   ? attn_prefill_tc_kernel<1>
+                                 : fmae == 2 ? attn_prefill_tc_kernel<2>
+                                 : fmae == 3 ? attn_prefill_tc_kernel<3>
+                                             : attn_prefill_tc_kernel<0>;
+  static bool attr[4] = {false, false, false, false};
+  if (!attr[fmae & 3]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(attn_prefill_tc)");
-    attr = true;
+    attr[fmae & 3] = true;
   }
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[2];
@@ -610,7 +614,7 @@ dl_status launch_attention_prefill_tc(const AttnArgs& a, cudaStream_t st) {
   if (max_clusters[C] == 0) {
     cfg.gridDim = dim3(C * num_sms());
     int nc = 0;
-    cudaError_t e = cudaOccupancyMaxActiveClusters(&nc, attn_prefill_tc_kernel, &cfg);
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&nc, kern, &cfg);
     if (e != cudaSuccess || nc < 1) {
       set_error("attention prefill (tcgen05): no co-resident cluster of %d (%s)", C, cudaGetErrorString(e));
       return DL_ERR_CUDA;
@@ -619,7 +623,7 @@ dl_status launch_attention_prefill_tc(const AttnArgs& a, cudaStream_t st) {
   }
   const int clusters = std::max(1, std::min(k.items, max_clusters[C]));
   cfg.gridDim = dim3(clusters * C);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, attn_prefill_tc_kernel, maps, k);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, maps, k);
   if (e != cudaSuccess) return cuda_status(e, "attention prefill (tcgen05)");
   return launched("attention prefill (tcgen05)");
 }
