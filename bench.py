@@ -362,7 +362,7 @@ def main():
         for i in range(slots):
             c = t[i]
             used = c[:, 0] > 0
-            if not used.any() or not (c[:, 5] > 0).any():
+            if not used.any() or not (c[:, 5] > 2 ** 48).any():   # GEMM slots: field 5 is a timestamp
                 continue
             c = c[used]
             spans.append((int(c[:, 0].min()), int(c[:, 6].max())))

@@ -735,6 +735,7 @@ __global__ void __launch_bounds__(sk::kThreads, PERSM)
   const int g8 = lane >> 2, t4 = lane & 3;
   const float scale = rsqrtf(static_cast<float>(D)) * 1.4426950408889634f;
   int64_t lpos = 0;   // position in the processing order (ring slot / phase)
+  int n_items = 0, n_merges = 0;   // debug trace
   for (int64_t g = split, send = b1; g < send || send == b1;) {
     if (g >= send) {   // segment A [split, b1) done: then [b0, split)
       if (split == b0) break;
@@ -940,74 +941,94 @@ __global__ void __launch_bounds__(sk::kThreads, PERSM)
       l1 = ls[8 + g8] + ls[24 + g8] + ls[40 + g8] + ls[56 + g8];
       asm volatile("bar.sync 1, 128;" ::: "memory");   // ls reused by the next item
     }
+    ++n_items;
     const bool whole = it.start >= b0 && it.end <= b1;
     __nv_bfloat16* orow = a.out + static_cast<int64_t>(it.s) * ldq + static_cast<int64_t>(h0) * D + w * 32 + 2 * t4;
     if (!whole) {
-      // publish {m, l, o[32 dims]} of rows g8, g8 + 8; the warp of the last
-      // contributing CTA merges (one counter per item and warp)
-      const int pslot = it.start <= b0 ? 0 : 1;
-      float* pp = a.part + ((static_cast<int64_t>(c) * 2 + pslot) * 4 + w) * 16 * kPartRow;
-      if (t4 == 0) {
-        pp[g8 * kPartRow] = m0;
-        pp[g8 * kPartRow + 1] = l0;
-        pp[(g8 + 8) * kPartRow] = m1;
-        pp[(g8 + 8) * kPartRow + 1] = l1;
-      }
-#pragma unroll
-      for (int dn = 0; dn < 4; ++dn) {
-        *reinterpret_cast<float2*>(pp + g8 * kPartRow + 2 + dn * 8 + 2 * t4) = make_float2(acc[dn][0], acc[dn][1]);
-        *reinterpret_cast<float2*>(pp + (g8 + 8) * kPartRow + 2 + dn * 8 + 2 * t4) = make_float2(acc[dn][2], acc[dn][3]);
-      }
-      __syncwarp();
+      // An item cut by range boundaries: the CTA whose range holds the item's
+      // first tile (cf) processes it LAST (at the end of its range), the others
+      // (cf + 1 .. cl) first -- so cf merges: the others publish {m, l, o[32
+      // dims]} of rows g8, g8 + 8 and bump the (item, warp) counter with release
+      // semantics; cf waits for them (acquire; normally already there) and folds
+      // their partials into its own registers in CTA order (deterministic).  No
+      // store / atomic round trip / re-read of cf's own partial on the kernel's tail.
       const int cf = sk_owner(it.start, N, G), cl = sk_owner(it.end - 1, N, G);
       unsigned* cnt = a.cnt + static_cast<int64_t>(it.s * per_seq + it.j) * 4 + w;
-      int last = 0;
-      if (lane == 0) {
-        int nc = 0;   // CTAs with a non-empty range (N < grid leaves some empty)
-        for (int cc = cf; cc <= cl; ++cc) nc += sk_bound(cc + 1, N, G) > sk_bound(cc, N, G);
-        // acq_rel: releases this warp's partial (cumulative over the warp via
-        // __syncwarp) and, for the last contributor, acquires the others'.
-        // (fence.sc.gpu + relaxed atomic measured ~2x slower tails at TP = 8)
-        unsigned old;
-        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
-        last = old == static_cast<unsigned>(nc - 1);
-        if (last) *cnt = 0u;   // zero-maintained for the next launch
-      }
-      last = __shfl_sync(0xffffffffu, last, 0);
-      if (!last) {
+      if (c != cf) {
+        const int pslot = it.start <= b0 ? 0 : 1;
+        float* pp = a.part + ((static_cast<int64_t>(c) * 2 + pslot) * 4 + w) * 16 * kPartRow;
+        if (t4 == 0) {
+          pp[g8 * kPartRow] = m0;
+          pp[g8 * kPartRow + 1] = l0;
+          pp[(g8 + 8) * kPartRow] = m1;
+          pp[(g8 + 8) * kPartRow + 1] = l1;
+        }
+#pragma unroll
+        for (int dn = 0; dn < 4; ++dn) {
+          *reinterpret_cast<float2*>(pp + g8 * kPartRow + 2 + dn * 8 + 2 * t4) = make_float2(acc[dn][0], acc[dn][1]);
+          *reinterpret_cast<float2*>(pp + (g8 + 8) * kPartRow + 2 + dn * 8 + 2 * t4) = make_float2(acc[dn][2], acc[dn][3]);
+        }
+        __syncwarp();   // release below is cumulative over the warp's stores
+        if (lane == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
         g = e;
         continue;
       }
-      // online merge over the contributors, in CTA order
-      m0 = m1 = -INFINITY;
-      l0 = l1 = 0.f;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
-      for (int cc = cf; cc <= cl; ++cc) {
-        const int64_t bc = sk_bound(cc, N, G);
-        if (sk_bound(cc + 1, N, G) == bc) continue;
-        const float* pk = a.part + ((static_cast<int64_t>(cc) * 2 + (it.start <= bc ? 0 : 1)) * 4 + w) * 16 * kPartRow;
-        const float km0 = __ldcg(pk + g8 * kPartRow), kl0 = __ldcg(pk + g8 * kPartRow + 1);
-        const float km1 = __ldcg(pk + (g8 + 8) * kPartRow), kl1 = __ldcg(pk + (g8 + 8) * kPartRow + 1);
-        float2 ko[4][2];
-#pragma unroll
-        for (int dn = 0; dn < 4; ++dn) {
-          ko[dn][0] = __ldcg(reinterpret_cast<const float2*>(pk + g8 * kPartRow + 2 + dn * 8 + 2 * t4));
-          ko[dn][1] = __ldcg(reinterpret_cast<const float2*>(pk + (g8 + 8) * kPartRow + 2 + dn * 8 + 2 * t4));
+      if (lane == 0) {
+        unsigned nc = 0;   // other contributors with a non-empty range (N < grid leaves some empty)
+        for (int cc = cf + 1; cc <= cl; ++cc) nc += sk_bound(cc + 1, N, G) > sk_bound(cc, N, G);
+        for (;;) {
+          unsigned v;
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+          if (v >= nc) break;
+          __nanosleep(32);
         }
-        const float n0 = fmaxf(m0, km0), n1 = fmaxf(m1, km1);
-        const float z0 = n0 == -INFINITY ? 0.f : n0, z1 = n1 == -INFINITY ? 0.f : n1;
-        const float so0 = exp2f(m0 - z0), sn0 = exp2f(km0 - z0), so1 = exp2f(m1 - z1), sn1 = exp2f(km1 - z1);
-        m0 = n0;
-        m1 = n1;
-        l0 = l0 * so0 + kl0 * sn0;
-        l1 = l1 * so1 + kl1 * sn1;
+        *cnt = 0u;   // zero-maintained for the next launch
+      }
+      __syncwarp();
+      ++n_merges;
+      // contributors' partials are loaded MB at a time (all loads in flight), then
+      // merged in CTA order: one L2 round trip per MB contributors, not per contributor
+      // (MB = 2: a third in flight spills under the 2-CTA/SM register cap)
+      constexpr int MB = 2;
+      for (int cb = cf + 1; cb <= cl; cb += MB) {
+        float km[MB][2], kl[MB][2];
+        float2 ko[MB][4][2];
+        bool ok[MB];
 #pragma unroll
-        for (int dn = 0; dn < 4; ++dn) {
-          acc[dn][0] = acc[dn][0] * so0 + ko[dn][0].x * sn0;
-          acc[dn][1] = acc[dn][1] * so0 + ko[dn][0].y * sn0;
-          acc[dn][2] = acc[dn][2] * so1 + ko[dn][1].x * sn1;
-          acc[dn][3] = acc[dn][3] * so1 + ko[dn][1].y * sn1;
+        for (int q = 0; q < MB; ++q) {
+          const int cc = cb + q;
+          const int64_t bc = sk_bound(cc, N, G);
+          ok[q] = cc <= cl && sk_bound(cc + 1, N, G) > bc;
+          if (!ok[q]) continue;
+          const float* pk = a.part + ((static_cast<int64_t>(cc) * 2 + (it.start <= bc ? 0 : 1)) * 4 + w) * 16 * kPartRow;
+          km[q][0] = __ldcg(pk + g8 * kPartRow);
+          kl[q][0] = __ldcg(pk + g8 * kPartRow + 1);
+          km[q][1] = __ldcg(pk + (g8 + 8) * kPartRow);
+          kl[q][1] = __ldcg(pk + (g8 + 8) * kPartRow + 1);
+#pragma unroll
+          for (int dn = 0; dn < 4; ++dn) {
+            ko[q][dn][0] = __ldcg(reinterpret_cast<const float2*>(pk + g8 * kPartRow + 2 + dn * 8 + 2 * t4));
+            ko[q][dn][1] = __ldcg(reinterpret_cast<const float2*>(pk + (g8 + 8) * kPartRow + 2 + dn * 8 + 2 * t4));
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < MB; ++q) {
+          if (!ok[q]) continue;
+          const float n0 = fmaxf(m0, km[q][0]), n1 = fmaxf(m1, km[q][1]);
+          const float z0 = n0 == -INFINITY ? 0.f : n0, z1 = n1 == -INFINITY ? 0.f : n1;
+          const float so0 = exp2f(m0 - z0), sn0 = exp2f(km[q][0] - z0), so1 = exp2f(m1 - z1),
+                      sn1 = exp2f(km[q][1] - z1);
+          m0 = n0;
+          m1 = n1;
+          l0 = l0 * so0 + kl[q][0] * sn0;
+          l1 = l1 * so1 + kl[q][1] * sn1;
+#pragma unroll
+          for (int dn = 0; dn < 4; ++dn) {
+            acc[dn][0] = acc[dn][0] * so0 + ko[q][dn][0].x * sn0;
+            acc[dn][1] = acc[dn][1] * so0 + ko[q][dn][0].y * sn0;
+            acc[dn][2] = acc[dn][2] * so1 + ko[q][dn][1].x * sn1;
+            acc[dn][3] = acc[dn][3] * so1 + ko[q][dn][1].y * sn1;
+          }
         }
       }
     }
@@ -1021,7 +1042,11 @@ __global__ void __launch_bounds__(sk::kThreads, PERSM)
     g = e;
   }
   ew_mark(a.tr, 3);
-  if (ctr && tid == 0) ctr[6] = ew_now();
+  if (ctr && tid == 0) {
+    ctr[6] = ew_now();
+    ctr[5] = static_cast<unsigned long long>(b1 - b0) | (static_cast<unsigned long long>(n_items) << 16) |
+             (static_cast<unsigned long long>(n_merges) << 32);   // debug: tiles, items, merges of this CTA
+  }
 }
 
 }  // namespace

@@ -55,8 +55,9 @@ while i < slots:
         i += 1
         continue
     # attention launches fill two consecutive slots with 296 CTAs and leave field 5 empty
-    if used.all() and (c[:, 5] == 0).all():
-        two = i + 1 < slots and (t[i + 1][:, 0] > 0).all() and (t[i + 1][:, 5] == 0).all()
+    # attention slots carry tile / item / merge counts in field 5 (< 2^48), GEMM slots a timestamp
+    if used.all() and (c[:, 5] < 2 ** 48).all():
+        two = i + 1 < slots and (t[i + 1][:, 0] > 0).all() and (t[i + 1][:, 5] < 2 ** 48).all()
         c = torch.cat([t[i], t[i + 1]]) if two else t[i]
         t0 = c[:, 0].min()
         print(f"== attention (slot {i}{'-%d' % (i + 1) if two else ''}), {c.shape[0]} CTAs; us from first entry: "
@@ -71,6 +72,15 @@ while i < slots:
                 print(f"   {l:7s} " + " ".join(f"{v[int(q * (n - 1))]:7.1f}" for q in (0, .1, .5, .9, 1)))
         d = ((c[:, 6] - c[:, 2]) / 1e3).sort().values
         print(f"   run (end - wait) per CTA: p10 {d[len(d) // 10]:.1f} p50 {d[len(d) // 2]:.1f} max {d[-1]:.1f}")
+        info = c[:, 5].long()
+        tiles, items, merges = info & 0xFFFF, (info >> 16) & 0xFFFF, (info >> 32) & 0xFFFF
+        run = (c[:, 6] - c[:, 2]) / 1e3
+        order = run.argsort(descending=True)[:8]
+        print("   slowest CTAs: run_us tiles items merges smid")
+        for k in order.tolist():
+            print(f"     {run[k]:6.1f} {int(tiles[k]):5d} {int(items[k]):5d} {int(merges[k]):6d} {int(c[k, 7]):4d}")
+        print(f"   merges: CTAs with >=1 merge {(merges > 0).sum().item()}, mean run {run[merges > 0].mean():.1f} "
+              f"vs {run[merges == 0].mean():.1f} us without")
         i += 2 if two else 1
         continue
     i += 1
