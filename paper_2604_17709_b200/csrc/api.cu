@@ -632,6 +632,7 @@ struct BlockWs {
   __nv_bfloat16 *xn, *zb, *yb, *rs, *q, *att, *att_full, *ag, *act;
   __nv_bfloat16* zr;                 // skinny stage-1 Z, bf16 red.add target (zero-maintained)
   __nv_bfloat16* yr;                 // skinny TP stage-2 partials, bf16 red.add target = collective buffer (zero-maintained)
+  __nv_bfloat16* yr2;                // [Ts x h] the same for the o / down outputs of the skinny TP path
   float* apart;                      // split-KV attention partials (decode)
   size_t apart_bytes;
   void* ask;                         // stream-K decode attention: counters + partial slots
@@ -679,6 +680,7 @@ BlockWs carve_block(Carver& c, const BlockDims& d, int64_t Tmax) {
   // live until the down group's finalize clears both
   w.zr = c.take<__nv_bfloat16>(static_cast<size_t>(Ts) * 2 * w.ldzb);
   w.yr = c.take<__nv_bfloat16>(static_cast<size_t>(Ts) * rup(d.nmax, 8));
+  w.yr2 = c.take<__nv_bfloat16>(static_cast<size_t>(Ts) * d.h);
   w.yb = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * rup(d.nmax, 8));
   w.rs = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.W);
   w.q = c.take<__nv_bfloat16>(static_cast<size_t>(Tmax) * d.Hq_loc * d.d);
@@ -1261,7 +1263,9 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
     return o;
   };
   // the bf16 all-reduce target of the skinny TP path: Y / X of the window, else ws.yr
-  __nv_bfloat16* const arY = fan.on ? fan.Y : ws.yr;
+  // (o / down outputs in their own buffer: the down stage 1 may still read the
+  // gate|up rows in ws.yr while the down stage 2 reduces, DL_XACT_TP)
+  __nv_bfloat16* const arY = fan.on ? fan.Y : ws.yr2;
   __nv_bfloat16* const arX = fan.on ? fan.X : ws.yr;
   auto all_reduce_bf16 = [&](__nv_bfloat16* buf, int64_t n) -> dl_status {
     if (!fan.on) return coll_all_reduce(comm, buf, static_cast<size_t>(T) * n, kCollBF16, st);
@@ -1304,6 +1308,13 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   static const bool no_fuse_rn = DL_ENV("DL_NO_FUSE_RESNORM") != nullptr;
   const bool rope_attn = skinny && !tp && !kv && use_zred() && !use_fixup() && !no_rope_fuse && !no_fuse_rn &&
                          phase == DL_DECODE && num_seqs <= 1024 && d.d == 128;
+  // TP decode (skinny rank-parallel / DeInfer-free path): the attention reads the
+  // reduce-scattered q|k|v rows of the rank's heads and does RoPE + cache
+  // append itself -- one launch (and one dependent boundary) less per layer
+  // (DL_ROPE_FUSE_TP=0: separate RoPE kernel)
+  static const bool rope_fuse_tp = !DL_ENV("DL_ROPE_FUSE_TP") || atoi(DL_ENV("DL_ROPE_FUSE_TP")) != 0;
+  const bool rope_attn_tp = tpr && !kv && rope_fuse_tp && phase == DL_DECODE && num_seqs <= 1024 && d.d == 128 &&
+                            d.layout == DL_LAYOUT_RANK_PARALLEL && d.W % 8 == 0;
   if (rope_attn) {
     qkv_out.mode = OUT_BF16_RED;
     qkv_out.ptr = ws.yr;
@@ -1458,6 +1469,15 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
     aa.rope = cfg->no_rope ? 0 : 1;
     aa.zero = zq;
     DL_TRY(launch_attention(aa, st));
+  } else if (rope_attn_tp) {
+    aa.qkv = rc.src;   // [T x W] rows of the rank's q | k | v heads
+    aa.ld_qkv = rc.ld_src;
+    aa.positions = positions;
+    aa.theta = cfg->rope_theta;
+    aa.rope = cfg->no_rope ? 0 : 1;
+    aa.zero = rc.zero;
+    aa.zero2 = rc.zero2;
+    DL_TRY(launch_attention(aa, st));
   } else {
     if (fx_rope) aa.zero = zq;
     if (!fx && !kv && !fx_rope) DL_TRY(launch_rope_cache(rc, st));
@@ -1501,7 +1521,7 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
     if (!tp) return skinny ? launch_residual_add_f32(ws.yf, ws.ldy32, x, d.h, T, n, 1, st, z, z2) : DL_OK;
     if (tpr) {
       DL_TRY(all_reduce_bf16(arY, n));
-      return launch_residual_add_bf16(arY, n, x, d.h, T, n, st, 1, z);
+      return launch_residual_add_bf16(arY, n, x, d.h, T, n, st, 1, z, z2);
     }
     if (skinny) DL_TRY(launch_f32_to_bf16(ws.yf, ws.ldy32, ws.yb, n, T, n, 1, st, z));
     DL_TRY(coll_all_reduce(comm, ws.yb, static_cast<size_t>(T) * n, kCollBF16, st));
@@ -1558,6 +1578,14 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   // for 1.8 M outputs), DESIGN.md §6
   static const bool xact_env = DL_ENV("DL_XACT") && atoi(DL_ENV("DL_XACT")) != 0;
   const bool xact = gur && xact_env && d.m % 8 == 0 && ngu % 8 == 0;
+  // TP (DL_XACT_TP=1, A/B): the activation in the down stage 1 is recomputed
+  // by only the rank's k-shard feature tiles (5 x at TP = 8 for 70B, 39 x at
+  // TP = 1) and removes the SiLU kernel and its boundary, but each stage-1 unit
+  // then waits on an L2 round trip for its gate|up tile: measured 9.9 vs 8.8 ms
+  // per rank at TP = 8 (down stage 1 29 vs 16 us), DESIGN.md §6
+  static const bool xact_tp_env = DL_ENV("DL_XACT_TP") && atoi(DL_ENV("DL_XACT_TP")) != 0;
+  const bool xact_tp = tpr && !fan.on && xact_tp_env && P > 1 && d.layout == DL_LAYOUT_RANK_PARALLEL &&
+                       d.m % 8 == 0 && ngu % 8 == 0;
   if (tpr || gur) gu_out = fan_ar(out_plain(arX, ngu, OUT_BF16_RED, 0), ngu);
   const GemmFixup fsilu = fixup(fx_gu ? FIX_SILU : FIX_NONE);
   DL_TRY(run_group(w->gu, n_gu, gu_rows, ws.xn, d.h, d.h, T, skinny, ws, gu_out, st, &fsilu, fx ? nullptr : &zg, 1));
@@ -1572,6 +1600,8 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   } else if (!tp && skinny) {
     if (d.glu) DL_TRY(launch_silu_mul_f32(ws.yf, ws.ldy32, ws.act, d.m, T, d.m, 1, st, zg));
     else DL_TRY(launch_relu_f32(ws.yf, ws.ldy32, ws.act, d.m, T, d.m, 1, st, zg));
+  } else if (tpr && xact_tp) {
+    DL_TRY(all_reduce_bf16(arX, ngu));   // the down stage 1 reads (and a later kernel clears) it
   } else if (tpr) {
     DL_TRY(all_reduce_bf16(arX, ngu));
     if (d.glu) DL_TRY(launch_silu_mul_bf16(arX, ngu, ws.act, d.m, T, d.m, st, 1, zg));
@@ -1584,7 +1614,7 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   }
   Xform xf;
   SideZero zyr;   // in-kernel activation: the gate|up rows, cleared once the down stage 1 has read them
-  if (!tp && gur && xact) {
+  if ((!tp && gur && xact) || xact_tp) {
     xf.mode = d.glu ? XFORM_SILU : XFORM_RELU;
     xf.src = ws.yr;
     xf.ld = ngu;
@@ -1606,7 +1636,7 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   if (next_norm && tpr && !no_fuse && d.layout != DL_LAYOUT_DEINFER) {
     DL_TRY(all_reduce_bf16(arY, d.h));
     DL_TRY(launch_residual_rmsnorm_bf16(arY, d.h, x, static_cast<const __nv_bfloat16*>(next_norm), ws.xn, T, d.h,
-                                        cfg->rms_eps, st, zd));
+                                        cfg->rms_eps, st, zd, zyr));
     *next_normed = true;
     return DL_OK;
   }

@@ -524,7 +524,7 @@ struct SkArgs {
   int rope;
   __nv_bfloat16* kc;              // head-major caches (written: the appended key / value)
   __nv_bfloat16* vc;
-  SideZero zero;
+  SideZero zero, zero2;
   unsigned long long* ctr;        // per-CTA debug timeline (dl_debug_gemm_trace), 8 u64 per CTA
   int reorder;                    // shared last item first (DL_ATTN_ORDER=1; default plain range order)
 };
@@ -723,11 +723,14 @@ __global__ void __launch_bounds__(sk::kThreads, PERSM)
   pdl_wait();
   ew_mark(a.tr, 2);
   if (ctr && tid == 0) ctr[2] = ew_now();
-  if (a.zero.p) {   // side clear (the q|k|v group's latent buffer), spread over every compute thread
-    const int64_t per_row = a.zero.row_bytes / 16, total = a.zero.rows * per_row;
+  // side clears (the q|k|v group's latent buffer; at TP the reduce-scatter's
+  // partial buffer), spread over every compute thread
+  for (const SideZero& z : {a.zero, a.zero2}) {
+    if (!z.p) continue;
+    const int64_t per_row = z.row_bytes / 16, total = z.rows * per_row;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * 128 + tid; i < total; i += static_cast<int64_t>(gridDim.x) * 128) {
       const int64_t r = i / per_row;
-      *reinterpret_cast<uint4*>(static_cast<uint8_t*>(a.zero.p) + r * a.zero.ld + (i - r * per_row) * 16) =
+      *reinterpret_cast<uint4*>(static_cast<uint8_t*>(z.p) + r * z.ld + (i - r * per_row) * 16) =
           make_uint4(0u, 0u, 0u, 0u);
     }
   }
@@ -1097,6 +1100,7 @@ dl_status launch_attention_sk(const AttnArgs& a, cudaStream_t st) {
   k.kc = const_cast<__nv_bfloat16*>(a.k_cache);
   k.vc = const_cast<__nv_bfloat16*>(a.v_cache);
   k.zero = a.zero;
+  k.zero2 = a.zero2;
   k.ctr = nullptr;
   static const int order = DL_ENV("DL_ATTN_ORDER") ? atoi(DL_ENV("DL_ATTN_ORDER")) : 0;   // measured neutral (A/B)
   k.reorder = order;

@@ -328,12 +328,12 @@ dl_status launch_residual_rmsnorm(float* acc, int64_t lda, __nv_bfloat16* x, con
 // the same with a bf16 accumulator (a TP collective's result, consumed and cleared)
 dl_status launch_residual_rmsnorm_bf16(__nv_bfloat16* acc, int64_t lda, __nv_bfloat16* x, const __nv_bfloat16* g,
                                        __nv_bfloat16* y, int64_t T, int64_t h, float eps, cudaStream_t st,
-                                       const SideZero& z = SideZero{});
+                                       const SideZero& z = SideZero{}, const SideZero& z2 = SideZero{});
 // x[t][c] = bf16(x + y)
 // clear != 0: y is zeroed as it is read (a bf16 reduction target)
 dl_status launch_residual_add_bf16(const __nv_bfloat16* y, int64_t ldy, __nv_bfloat16* x,
                                    int64_t ldx, int64_t T, int64_t n, cudaStream_t st, int clear = 0,
-                                   const SideZero& z = SideZero{});
+                                   const SideZero& z = SideZero{}, const SideZero& z2 = SideZero{});
 // act[t][i] = bf16(silu(g) * u) with g = src[t][i], u = src[t][m + i]
 dl_status launch_silu_mul_f32(float* acc, int64_t ld_acc, __nv_bfloat16* act,
                               int64_t ld_act, int64_t T, int64_t m, int clear,
@@ -412,10 +412,10 @@ struct AttnArgs {
   // fused RoPE + cache append (decode, head-major cache, stream-K kernel only):
   // qkv != null -> q|k|v rows [T x ld_qkv] bf16 straight from the q|k|v group
   // (the kernel rotates q and the new key with positions[t], appends k and v at
-  // cache_lens[t]); `zero` is a side clear done once the kernel has waited.
+  // cache_lens[t]); `zero`, `zero2` are side clears done once the kernel has waited.
   // The kernel returns DL_ERR_UNSUPPORTED if it cannot take them.
   const __nv_bfloat16* qkv; int64_t ld_qkv; const int32_t* positions; float theta; int rope;
-  SideZero zero;
+  SideZero zero, zero2;
 };
 dl_status launch_attention(const AttnArgs& a, cudaStream_t st);
 // prefill (a.decode == 0) on tcgen05 / TMEM / TMA (attn_tc.cu)

@@ -916,15 +916,14 @@ dl_status launch_residual_rmsnorm(float* acc, int64_t lda, __nv_bfloat16* x, con
 }
 dl_status launch_residual_rmsnorm_bf16(__nv_bfloat16* acc, int64_t lda, __nv_bfloat16* x, const __nv_bfloat16* g,
                                        __nv_bfloat16* y, int64_t T, int64_t h, float eps, cudaStream_t st,
-                                       const SideZero& z) {
+                                       const SideZero& z, const SideZero& z2) {
   if (T <= 0) return DL_OK;
   if (h % 8 || h / 8 > kRnThreads * kRnChunks) {
     set_error("residual_rmsnorm: h=%lld unsupported (multiple of 8, <= %d)", (long long)h, 8 * kRnThreads * kRnChunks);
     return DL_ERR_UNSUPPORTED;
   }
   return launch_pdl(residual_rmsnorm_kernel<__nv_bfloat16>, dim3(static_cast<unsigned>(T)), dim3(kRnThreads), 0, st,
-                    "residual_rmsnorm_bf16", acc, lda, x, g, y, static_cast<int>(h), eps, z, SideZero{},
-                    ew_trace(2));
+                    "residual_rmsnorm_bf16", acc, lda, x, g, y, static_cast<int>(h), eps, z, z2, ew_trace(2));
 }
 dl_status launch_f32_to_bf16(float* acc, int64_t lda, __nv_bfloat16* out, int64_t ldo, int64_t T, int64_t n,
                              int clear, cudaStream_t st, const SideZero& z) {
@@ -935,9 +934,9 @@ dl_status launch_residual_add_f32(float* acc, int64_t lda, __nv_bfloat16* x, int
   return launch_ew4(T, n, ResidualAdd{acc, lda, x, ldx, clear}, st, "residual_add", z, z2);
 }
 dl_status launch_residual_add_bf16(const __nv_bfloat16* y, int64_t ldy, __nv_bfloat16* x, int64_t ldx, int64_t T,
-                                   int64_t n, cudaStream_t st, int clear, const SideZero& z) {
+                                   int64_t n, cudaStream_t st, int clear, const SideZero& z, const SideZero& z2) {
   return launch_ew4(T, n, ResidualAddBf16{const_cast<__nv_bfloat16*>(y), ldy, x, ldx, clear}, st, "residual_add_bf16",
-                    z);
+                    z, z2);
 }
 dl_status launch_silu_mul_f32(float* acc, int64_t lda, __nv_bfloat16* act, int64_t ldo, int64_t T, int64_t m,
                               int clear, cudaStream_t st, const SideZero& z) {

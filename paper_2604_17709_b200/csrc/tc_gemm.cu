@@ -1604,9 +1604,21 @@ dl_status prep_args(const GemmProblem& p, bool stream_k, KMaps& maps, KArgs& a, 
 // Hybrid stream-K of a launch with `grid` CTAs: CTA c first takes its static
 // range, then dynamic chunks from the work counter p.sched.
 void set_sched(const GemmProblem& p, KArgs& a, int grid) {
-  static const double frac = DL_ENV("DL_SK_STATIC") ? atof(DL_ENV("DL_SK_STATIC")) : 0.9;
-  static const int chunk = DL_ENV("DL_SK_CHUNK") ? atoi(DL_ENV("DL_SK_CHUNK")) : 8;
-  a.sched = p.sched;
+  // Hybrid split by problem size (measured, 70B@40% decode): launches with
+  // many units per CTA (TP = 1: 25-120) keep 90 % static and 8-unit dynamic
+  // chunks (finer chunks cost 3-4 ms/step there: each grab is an L2 round trip
+  // before its loads); launches with few (TP = 8: 4-20) balance better with
+  // 85 % static and 4-unit chunks (TP = 4 / 8: 11.0 -> 10.8 / 8.73 -> 8.5 ms
+  // per rank; TP = 2 15.35 -> 15.42, tools/gpu_r02am.sh).
+  static const double frac_l = DL_ENV("DL_SK_STATIC") ? atof(DL_ENV("DL_SK_STATIC")) : 0.9;
+  static const int chunk_l = DL_ENV("DL_SK_CHUNK") ? atoi(DL_ENV("DL_SK_CHUNK")) : 8;
+  static const double frac_s = DL_ENV("DL_SK_STATIC_S") ? atof(DL_ENV("DL_SK_STATIC_S")) : 0.85;
+  static const int chunk_s = DL_ENV("DL_SK_CHUNK_S") ? atoi(DL_ENV("DL_SK_CHUNK_S")) : 4;
+  static const long long small_upc = DL_ENV("DL_SK_SMALL") ? atoll(DL_ENV("DL_SK_SMALL")) : 24;
+  const bool small = a.total_units < small_upc * grid;
+  const double frac = small ? frac_s : frac_l;
+  const int chunk = small ? chunk_s : chunk_l;
+  a.sched = frac >= 1.0 ? nullptr : p.sched;   // static fraction >= 1 (A/B): purely static even split
   a.static_units = static_cast<long long>(frac * static_cast<double>(a.total_units) / grid);
   a.dyn_begin = a.static_units * grid;
   a.chunk = chunk > 0 ? chunk : 1;
