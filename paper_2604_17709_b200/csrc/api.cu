@@ -825,7 +825,7 @@ struct Xform {
 dl_status run_group(const dl_factor_group& grp, int nseg, const int64_t* rows, const __nv_bfloat16* act,
                     int64_t ld_act, int64_t n, int64_t T, bool skinny, const BlockWs& ws, const GemmOut& out2,
                     cudaStream_t st, const GemmFixup* fix2 = nullptr, SideZero* zero_out = nullptr,
-                    int zslot = 0, int act_p = 0, int64_t act_w = 0, const Xform& xf = Xform{}) {
+                    int zslot = 0, int act_p = 0, int64_t act_w = 0, const Xform& xf = Xform{}, int glu = 0) {
   // act_p > 1 (skinny only): act is a rank-major all-gather output read through a 3-D map
   const ZLayout zl = zlayout(grp, nseg);
   if (zero_out) *zero_out = SideZero{};
@@ -887,6 +887,7 @@ dl_status run_group(const dl_factor_group& grp, int nseg, const int64_t* rows, c
   } else {
     p2.tail_acc = ws.tail;
     p2.tail_bytes = ws.tail_bytes;
+    p2.glu = glu;   // out2 is then the [T x m] activation
   }
   return tc_gemm(p2, skinny, st);
 }
@@ -1587,9 +1588,19 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   const bool xact_tp = tpr && !fan.on && xact_tp_env && P > 1 && d.layout == DL_LAYOUT_RANK_PARALLEL &&
                        d.m % 8 == 0 && ngu % 8 == 0;
   if (tpr || gur) gu_out = fan_ar(out_plain(arX, ngu, OUT_BF16_RED, 0), ngu);
+  // prefill (whole-tile pair GEMM), TP = 1: SiLU(gate)*up in the gate|up stage-2
+  // epilogue (GemmProblem::glu): the [T x 2m] gate|up output never reaches HBM
+  // and the SiLU.up kernel is gone (DL_GLU_FUSE=0: separate kernel, A/B)
+  static const bool glu_env = !DL_ENV("DL_GLU_FUSE") || atoi(DL_ENV("DL_GLU_FUSE")) != 0;
+  const bool glu_fuse = glu_env && !skinny && !tp && d.glu && !fx_gu && n_gu == 2 && d.m % 256 == 0 &&
+                        w->gu.seg[0].k == w->gu.seg[1].k && w->gu.seg[0].k > 0;
+  if (glu_fuse) gu_out = out_plain(ws.act, d.m, OUT_BF16, 0);
   const GemmFixup fsilu = fixup(fx_gu ? FIX_SILU : FIX_NONE);
-  DL_TRY(run_group(w->gu, n_gu, gu_rows, ws.xn, d.h, d.h, T, skinny, ws, gu_out, st, &fsilu, fx ? nullptr : &zg, 1));
-  if (fx_gu) {
+  DL_TRY(run_group(w->gu, n_gu, gu_rows, ws.xn, d.h, d.h, T, skinny, ws, gu_out, st, &fsilu, fx ? nullptr : &zg, 1,
+                   0, 0, Xform{}, glu_fuse ? 1 : 0));
+  if (glu_fuse) {
+    // SiLU(gate)*up written by the gate|up stage-2 epilogue
+  } else if (fx_gu) {
     // SiLU(gate)*up done by the gate|up stage-2 fixup
   } else if (!tp && gur && xact) {
     // SiLU(gate)*up / ReLU(up) computed by the down projection's stage 1 itself

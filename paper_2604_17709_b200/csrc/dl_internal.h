@@ -252,6 +252,13 @@ struct GemmProblem {
   int xform;
   const __nv_bfloat16* xsrc;
   int64_t xld, xm;
+  // glu != 0 (prefill CTA-pair path only): segment 0 = gate, segment 1 = up
+  // (equal rows m, m % 256 == 0, equal klen); the epilogue writes only
+  // out[t][f] = bf16(silu(gate[t][f]) * up[t][f]) ([T x m], plain bf16 layout
+  // with out.ld), from the fp32 accumulators -- the SiLU.up pass and the
+  // [T x 2m] gate|up round trip through HBM are gone (the MLP of
+  // the decomposed block).
+  int glu;
 };
 enum XformMode { XFORM_NONE = 0, XFORM_SILU = 1, XFORM_RELU = 2 };
 

@@ -92,6 +92,11 @@ struct KArgs {
   long long xld;
   int xm, xcols;
   int wpol;                  // pair kernel weight L2 policy: 0 evict_first, 1 evict_normal, 2 evict_last
+  // pair kernel GLU mode (GemmProblem::glu): seg 0 = gate, seg 1 = up; the
+  // whole-tile schedule runs over tile PAIRS (total_tiles / dp_tiles count
+  // pairs), each emitted as the gate job (accumulator 0) then the up job of the
+  // same features (accumulator 1); tail pieces go to tail_acc slots 2p, 2p + 1
+  int glu;
   // DP + stream-K tail (whole-tile kernels): tiles [0, dp_tiles) whole, each of
   // the remaining tiles split in tail_split K-pieces accumulated in fp32 into
   // tail_acc [tail tile][256][256], finalized by tc_tail_finalize_kernel.
@@ -127,6 +132,22 @@ struct KArgs {
 __device__ __forceinline__ float rope_pos_of(const KArgs& a, int tok) {
   return (a.rope_pos != nullptr && tok < a.T) ? static_cast<float>(a.rope_pos[tok]) : 0.f;
 }
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ float2 unpack_bf16(uint32_t v) {
+  return make_float2(__uint_as_float(v << 16), __uint_as_float(v & 0xffff0000u));
+}
+// SiLU through one MUFU op (as elementwise.cu's silu_tanh): g sigmoid(g) =
+// r + r tanh(r), r = g / 2 (tanh.approx, relative error ~2^-11)
+__device__ __forceinline__ float silu_tanh_f(float g) {
+  const float r = 0.5f * g;
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(r));
+  return fmaf(r, t, r);
+}
+
 __device__ __forceinline__ void rope8(const KArgs& a, float pos, int f, float* v) {
   if (a.rope_pos == nullptr || f >= a.rope_end) return;
 #pragma unroll
@@ -369,6 +390,7 @@ struct JobIter {
   int cta, grid;
   int next_tile;            // whole-tile mode
   bool tail_taken = false;  // DP + stream-K tail piece already issued
+  bool glu_up = false;      // GLU: the up job of the last gate job is next
   long long u, u_end;       // stream-K mode
   __device__ JobIter(const KArgs& args, int c, int g) : a(args), cta(c), grid(g) {
     next_tile = c;
@@ -384,6 +406,14 @@ struct JobIter {
     u_end = e;
   }
   __device__ bool next(Job& j, int FEAT_TILE, int TOK_TILE) {
+    if (a.glu && glu_up) {
+      // the up tile of the same features / tokens / K range as the gate job in j
+      glu_up = false;
+      j.feat0 += a.seg[1].feat_begin - a.seg[0].feat_begin;
+      j.seg = 1;
+      if (j.part >= 0) ++j.part;
+      return true;
+    }
     if (!a.stream_k) {
       // data-parallel whole tiles, then (DP + stream-K tail) one K-split piece
       // of the last partial wave's tiles per CTA / cluster
@@ -405,6 +435,10 @@ struct JobIter {
       j.feat0 = a.seg[g].feat_begin + (local / a.tiles_tok) * FEAT_TILE;
       j.tok0 = (local % a.tiles_tok) * TOK_TILE;
       j.part = part;
+      if (a.glu) {   // t is a pair: its gate job now, the up job next
+        j.part = part < 0 ? -1 : 2 * part;
+        glu_up = true;
+      }
       if (part < 0) {
         j.kb0 = 0;
         j.kb1 = a.seg[g].nkb;
@@ -1053,7 +1087,7 @@ __global__ void __launch_bounds__(kThreads, (SWAP && STAGES <= 4) ? 2 : 1)
 // relative to the 1-CTA 128x256 tile.  Whole tiles, bf16 (+ fused residual)
 // epilogue; every CTA drains its own TMEM half (its 128 token rows).
 // ---------------------------------------------------------------------------
-template <int STAGES>
+template <int STAGES, bool GLU = false>   // GLU: KArgs::glu launches (gate|up pairs, SiLU.up epilogue)
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_gemm_pair_kernel(const __grid_constant__ KMaps maps, const __grid_constant__ KArgs a,
                         const __grid_constant__ KMaps, const __grid_constant__ KArgs, unsigned int*) {
@@ -1184,6 +1218,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint8_t* stg = smem + STAGES * STAGE_BYTES + (warp - 2) * kStageOutWarp;   // this warp's store staging
     int acc = 0;
     uint32_t acc_phase = 0;
+    uint32_t gpk[64];   // GLU: silu(gate) of this thread's row, 128 columns as bf16 pairs
     while (it.next(j, TILE, TILE)) {
       const KSeg& s = a.seg[j.seg];
       const int tok = j.tok0 + static_cast<int>(rank) * HALF + row;
@@ -1191,6 +1226,52 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       ptx::mbar_wait(&accf_bar[acc], acc_phase);
       ptx::tc_fence_after();
       const bool has_k = j.kb1 > j.kb0;
+      const uint32_t tacc = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * TILE + half * 128;
+      if (GLU && j.part < 0 && j.seg == 0) {
+        // gate job: keep silu(gate) in registers, release the accumulator at once
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t r[32];
+          ptx::tmem_ld32(tacc + c * 32, r);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            gpk[c * 16 + e] = pack_bf16(silu_tanh_f(__uint_as_float(r[2 * e])), silu_tanh_f(__uint_as_float(r[2 * e + 1])));
+        }
+      } else if (GLU && j.part < 0) {
+        // up job: act = silu(gate) * up, staged through the per-warp transpose
+        __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.out);
+        const int fg = j.feat0 - a.seg[1].feat_begin + half * 128;   // gate feature of column 0 of this warp
+        uint4* sw = reinterpret_cast<uint4*>(stg);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t r[32];
+          ptx::tmem_ld32(tacc + c * 32, r);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 pk;
+            uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int i0 = q * 8 + 2 * e;
+              const float2 g2 = unpack_bf16(gpk[c * 16 + q * 4 + e]);
+              pw[e] = pack_bf16(g2.x * __uint_as_float(r[i0]), g2.y * __uint_as_float(r[i0 + 1]));
+            }
+            sw[lane * 4 + (q ^ ((lane >> 1) & 3))] = pk;
+          }
+          __syncwarp();
+          const int cc = lane & 3;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int rr = 8 * q + (lane >> 2);
+            const uint4 val = sw[rr * 4 + (cc ^ ((rr >> 1) & 3))];
+            const int t2 = j.tok0 + static_cast<int>(rank) * HALF + quarter * 32 + rr;
+            if (t2 < a.T) *reinterpret_cast<uint4*>(out + static_cast<long long>(t2) * a.ldo + fg + c * 32 + cc * 8) = val;
+          }
+          __syncwarp();
+        }
+      } else
 #pragma unroll 1
       for (int c0 = half * 128; c0 < (half + 1) * 128; c0 += 32) {
         uint32_t r[32];
@@ -1376,6 +1457,36 @@ __global__ void __launch_bounds__(256) tc_tail_finalize_kernel(KArgs a) {
   }
 }
 
+// GLU mode: tail pair tt has the gate partial sums in tail_acc slot 2 tt and the
+// up ones in slot 2 tt + 1 (gate features seg[0].feat_begin + f, f in the
+// pair's 256-feature tile); out = bf16(silu(gate) * up) [T x m], both slots
+// cleared.  256 threads = 64 float4 column groups x 4 row lanes, 8 rows each.
+__global__ void __launch_bounds__(256) tc_tail_finalize_glu_kernel(KArgs a) {
+  pdl_trigger();
+  pdl_wait();
+  const int tt = blockIdx.x, rb = blockIdx.y;
+  const int local = a.dp_tiles + tt;   // pair index = gate tile index
+  const int f0 = (local / a.tiles_tok) * 256;
+  const int tok0 = (local % a.tiles_tok) * 256 + rb * 32;
+  const int c4 = (threadIdx.x & 63) * 4, lane_r = threadIdx.x >> 6;
+  float* gs = a.tail_acc + static_cast<long long>(2 * tt) * 256 * 256;
+  float* us = gs + 256 * 256;
+#pragma unroll 2
+  for (int i = 0; i < 8; ++i) {
+    const int r = rb * 32 + lane_r + 4 * i;
+    const float4 g = __ldcg(reinterpret_cast<const float4*>(gs + r * 256 + c4));
+    const float4 u = __ldcg(reinterpret_cast<const float4*>(us + r * 256 + c4));
+    *reinterpret_cast<float4*>(gs + r * 256 + c4) = make_float4(0.f, 0.f, 0.f, 0.f);
+    *reinterpret_cast<float4*>(us + r * 256 + c4) = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int tok = tok0 + lane_r + 4 * i;
+    if (tok >= a.T) continue;
+    uint2 pk;
+    pk.x = pack_bf16(silu_tanh_f(g.x) * u.x, silu_tanh_f(g.y) * u.y);
+    pk.y = pack_bf16(silu_tanh_f(g.z) * u.z, silu_tanh_f(g.w) * u.w);
+    *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.out) + static_cast<long long>(tok) * a.ldo + f0 + c4) = pk;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -1474,6 +1585,20 @@ dl_status prep_args(const GemmProblem& p, bool stream_k, KMaps& maps, KArgs& a, 
     } else {
       maps.w[g] = maps.w[0];
     }
+  }
+  a.glu = 0;
+  if (p.glu) {
+    const GemmSeg& g0 = p.seg[0];
+    const GemmSeg& g1 = p.seg[1];
+    if (!PAIR || stream_k || p.nseg != 2 || g0.rows != g1.rows || g0.rows % C::FEAT_TILE != 0 || g0.klen != g1.klen ||
+        g0.klen <= 0 || p.out.mode != OUT_BF16 || p.out.accumulate || p.out.scatter_p || p.out.remap_cols ||
+        p.out.rope_pos || p.out.fan_n || p.out.ld % 8 || (reinterpret_cast<uintptr_t>(p.out.ptr) & 15)) {
+      set_error("tc_gemm: the GLU epilogue needs the prefill pair path, gate|up segments of equal rows (%% 256) "
+                "and rank, a plain 16-byte-aligned bf16 output");
+      return DL_ERR_INVALID_ARG;
+    }
+    a.glu = 1;
+    tiles = a.seg[0].ntiles;   // the whole-tile schedule counts (gate, up) pairs
   }
   a.act_w = 0;
   a.xform = XFORM_NONE;
@@ -1644,9 +1769,11 @@ cudaError_t launch_kern(KernFn kern, int grid, int smem, const KMaps& m1, const 
 template <int BN, bool SWAP, int STAGES, bool PAIR = false>
 dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   using C = Cfg<BN, SWAP, STAGES, PAIR>;
-  static bool attr_set = false;
-  KernFn kern = PAIR ? tc_gemm_pair_kernel<STAGES> : tc_gemm_kernel<BN, SWAP, STAGES, false>;
-  DL_TRY_INTERNAL(set_smem_attr(kern, C::SMEM, &attr_set));
+  static bool attr_set[2] = {false, false};
+  const bool glu = PAIR && p.glu;
+  KernFn kern = PAIR ? (glu ? tc_gemm_pair_kernel<STAGES, true> : tc_gemm_pair_kernel<STAGES, false>)
+                     : tc_gemm_kernel<BN, SWAP, STAGES, false>;
+  DL_TRY_INTERNAL(set_smem_attr(kern, C::SMEM, &attr_set[glu ? 1 : 0]));
   KMaps maps;
   KArgs a;
   double bytes = 0, flops = 0;
@@ -1667,7 +1794,7 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
     const int full = tiles / clusters, tail = tiles % clusters;
     if (dpsk && p.tail_acc && full >= 1 && tail > 0 && tail * 4 <= clusters * 3) {
       const int split = clusters / tail;
-      if (split >= 2 && static_cast<size_t>(tail) * 256 * 256 * 4 <= p.tail_bytes) {
+      if (split >= 2 && static_cast<size_t>(tail) * (a.glu ? 2 : 1) * 256 * 256 * 4 <= p.tail_bytes) {
         a.dp_tiles = tiles - tail;
         a.tail_split = split;
         a.tail_acc = p.tail_acc;
@@ -1682,8 +1809,8 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   launched("tc_gemm");
   if (e == cudaSuccess && a.tail_split > 0) {
     const int pf = prof_begin(st);
-    const dl_status fs = launch_pdl(tc_tail_finalize_kernel, dim3(a.total_tiles - a.dp_tiles, 8), dim3(256), 0,
-                                    st, "tc_gemm tail finalize", a);
+    const dl_status fs = launch_pdl(a.glu ? tc_tail_finalize_glu_kernel : tc_tail_finalize_kernel,
+                                    dim3(a.total_tiles - a.dp_tiles, 8), dim3(256), 0, st, "tc_gemm tail finalize", a);
     prof_end(pf, st, 0.0, 0.0, 2);
     if (fs != DL_OK) return fs;
   }
@@ -1770,6 +1897,10 @@ dl_status tc_gemm(const GemmProblem& p, bool stream_k, cudaStream_t st) {
   }
   if (stream_k && p.out.mode != OUT_F32_RED && p.out.mode != OUT_BF16_RED && p.fix.op == FIX_NONE) {
     set_error("stream-K requires a reduction output");
+    return DL_ERR_INVALID_ARG;
+  }
+  if (p.glu && (stream_k || p.T <= 256)) {
+    set_error("tc_gemm: the GLU epilogue is a prefill (T > 256, whole-tile) configuration");
     return DL_ERR_INVALID_ARG;
   }
   static const int dec_stages = DL_ENV("DL_DECODE_STAGES") ? atoi(DL_ENV("DL_DECODE_STAGES")) : 9;
