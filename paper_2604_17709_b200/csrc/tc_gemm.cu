@@ -97,6 +97,7 @@ struct KArgs {
   // pairs), each emitted as the gate job (accumulator 0) then the up job of the
   // same features (accumulator 1); tail pieces go to tail_acc slots 2p, 2p + 1
   int glu;
+  int glu_spol;              // GLU act stores: 0 plain, 1 L2 evict_last hint (the down stage 1 re-reads them)
   // DP + stream-K tail (whole-tile kernels): tiles [0, dp_tiles) whole, each of
   // the remaining tiles split in tail_split K-pieces accumulated in fp32 into
   // tail_acc [tail tile][256][256], finalized by tc_tail_finalize_kernel.
@@ -1242,6 +1243,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // up job: act = silu(gate) * up, staged through the per-warp transpose
         __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.out);
         const int fg = j.feat0 - a.seg[1].feat_begin + half * 128;   // gate feature of column 0 of this warp
+        const uint64_t spol = ptx::policy_evict_last();
         uint4* sw = reinterpret_cast<uint4*>(stg);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -1267,7 +1269,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const int rr = 8 * q + (lane >> 2);
             const uint4 val = sw[rr * 4 + (cc ^ ((rr >> 1) & 3))];
             const int t2 = j.tok0 + static_cast<int>(rank) * HALF + quarter * 32 + rr;
-            if (t2 < a.T) *reinterpret_cast<uint4*>(out + static_cast<long long>(t2) * a.ldo + fg + c * 32 + cc * 8) = val;
+            if (t2 < a.T) {
+              uint4* dst = reinterpret_cast<uint4*>(out + static_cast<long long>(t2) * a.ldo + fg + c * 32 + cc * 8);
+              if (a.glu_spol)
+                asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(dst), "r"(val.x),
+                             "r"(val.y), "r"(val.z), "r"(val.w), "l"(spol)
+                             : "memory");
+              else
+                *dst = val;
+            }
           }
           __syncwarp();
         }
@@ -1447,7 +1457,20 @@ __global__ void __launch_bounds__(256) tc_tail_finalize_kernel(KArgs a) {
         make_float4(0.f, 0.f, 0.f, 0.f);
     const int tok = tok0 + lane_r + 4 * i;
     if (tok >= a.T) continue;
-    const float vv[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+    float vv[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+    if (a.rope_pos != nullptr && f < a.rope_end) {
+      // the epilogue RoPE of the whole tiles (rope8), on the summed K-pieces
+      const float pos = static_cast<float>(a.rope_pos[tok]);
+#pragma unroll
+      for (int e = 0; e < 4; e += 2) {
+        const int dim = (f + e) & 127;
+        float sn, cs;
+        rope_sincos(pos * exp2f(-a.rope_l2t * static_cast<float>(dim) / 128.f), &sn, &cs);
+        const float x = vv[e], y = vv[e + 1];
+        vv[e] = x * cs - y * sn;
+        vv[e + 1] = x * sn + y * cs;
+      }
+    }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       if (f + e >= s.write_end) break;
@@ -1599,6 +1622,8 @@ dl_status prep_args(const GemmProblem& p, bool stream_k, KMaps& maps, KArgs& a, 
     }
     a.glu = 1;
     tiles = a.seg[0].ntiles;   // the whole-tile schedule counts (gate, up) pairs
+    static const int spol = DL_ENV("DL_GLU_ACT_POL") ? atoi(DL_ENV("DL_GLU_ACT_POL")) : 1;
+    a.glu_spol = spol;
   }
   a.act_w = 0;
   a.xform = XFORM_NONE;
@@ -1648,9 +1673,14 @@ dl_status prep_args(const GemmProblem& p, bool stream_k, KMaps& maps, KArgs& a, 
   if (p.out.rope_pos) {
     // the vectorised whole-tile epilogue applies it: bf16 plain output, 32-aligned
     // feature range inside segment 0, no K-split tail, no stream-K
+    // (features f < rope_end are rotated as head dim f % 128: every segment that
+    // holds some of them starts on a head boundary; the K-split tail finalize
+    // rotates too)
+    bool heads_ok = p.seg[0].feat_begin == 0;
+    for (int g = 0; g < p.nseg; ++g)
+      if (p.seg[g].feat_begin < p.out.rope_end && (p.seg[g].feat_begin % 128 != 0 || p.out.remap_cols)) heads_ok = false;
     const bool ok = !stream_k && !SWAP && p.out.mode == OUT_BF16 && !p.out.accumulate && p.out.scatter_p == 0 &&
-                    p.tail_acc == nullptr && p.out.rope_end % 32 == 0 && p.seg[0].feat_begin == 0 &&
-                    p.out.rope_end <= p.seg[0].rows && p.out.ld % 8 == 0;
+                    !p.glu && p.out.rope_end % 128 == 0 && heads_ok && p.out.rope_end <= p.n_feat && p.out.ld % 8 == 0;
     if (!ok) {
       set_error("tc_gemm: epilogue RoPE needs a whole-tile bf16 output without tail split");
       return DL_ERR_INVALID_ARG;
@@ -1675,6 +1705,9 @@ dl_status prep_args(const GemmProblem& p, bool stream_k, KMaps& maps, KArgs& a, 
   a.trace_slot = g_trace_host_on ? g_trace_next++ : -1;
   static const int wpol = DL_ENV("DL_PAIR_WPOL") ? atoi(DL_ENV("DL_PAIR_WPOL")) : 2;   // A/B: 0 / 1 / 2 (measured best: 2)
   a.wpol = wpol;
+  // GLU launches: weights evict_first (measured 752 vs 764 us per 70B gate|up stage 2 with evict_last, r02bg)
+  static const int glu_wpol = DL_ENV("DL_GLU_WPOL") ? atoi(DL_ENV("DL_GLU_WPOL")) : 0;
+  if (a.glu && glu_wpol >= 0) a.wpol = glu_wpol;
   a.dp_tiles = tiles;
   a.tail_split = 0;
   a.tail_acc = nullptr;
