@@ -1321,6 +1321,17 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
     qkv_out.ptr = ws.yr;
     qkv_out.ld = NQKV;
   }
+  // prefill, TP = 1: RoPE of q and k in the q|k|v stage-2 epilogue (whole tiles
+  // and the K-split tail finalize, one bf16 rounding); the attention reads q in
+  // place from the q|k|v output and a copy-only kernel appends k, v to the
+  // caches (DL_ROPE_EPI=0: the RoPE + cache-append kernel, A/B)
+  static const bool rope_epi_env = !DL_ENV("DL_ROPE_EPI") || atoi(DL_ENV("DL_ROPE_EPI")) != 0;
+  const bool rope_epi = rope_epi_env && !skinny && !tp && !kv && d.d == 128 && NQKV % 8 == 0;
+  if (rope_epi && !cfg->no_rope) {
+    qkv_out.rope_pos = positions;
+    qkv_out.rope_end = (d.Hq_loc + d.Hk_loc) * d.d;
+    qkv_out.rope_theta = cfg->rope_theta;
+  }
 
   // skinny, single rank: every group's finalize (RoPE + cache append, residual,
   // SiLU*up) runs in the stage-2 GEMM's last-contributor fixup
@@ -1442,6 +1453,12 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
     } else {
       rc.src = ws.yb;
       rc.ld_src = NQKV;
+      if (rope_epi) {
+        rc.kv_only = 1;
+        rc.rope = 0;
+        aa.q = ws.yb;
+        aa.ld_q = NQKV;
+      }
     }
   } else if (fan.on) {
     DL_TRY(comm_barrier(comm, st));   // every rank's q|k|v partials are in the owners' windows

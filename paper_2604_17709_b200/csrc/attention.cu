@@ -110,8 +110,9 @@ __global__ void __launch_bounds__(128, KTP == 32 ? 3 : 1) attn_prefill_kernel(At
   const int64_t base_pos = a.cache_lens[s];
   const int kvh = static_cast<int>((static_cast<int64_t>(h) * a.Hk) / a.Hq);
   const int64_t tok0 = a.cu_seqlens[s] + q0;
-  const int64_t ldq = static_cast<int64_t>(a.Hq) * D;
-  const __nv_bfloat16* Qg = a.q + tok0 * ldq + static_cast<int64_t>(h) * D;
+  const int64_t ldq = static_cast<int64_t>(a.Hq) * D;   // output rows
+  const int64_t ldqi = a.ld_q > 0 ? a.ld_q : ldq;         // q rows
+  const __nv_bfloat16* Qg = a.q + tok0 * ldqi + static_cast<int64_t>(h) * D;
   const int64_t kvoff = (static_cast<int64_t>(s) * a.Hk + kvh) * a.max_seq * D;
   const __nv_bfloat16* Kg = a.k_cache + kvoff;
   const __nv_bfloat16* Vg = a.v_cache + kvoff;
@@ -123,7 +124,7 @@ __global__ void __launch_bounds__(128, KTP == 32 ? 3 : 1) attn_prefill_kernel(At
   const uint32_t sK0 = sQ + QT * ROW_BYTES;
   const uint32_t sV0 = sK0 + 2 * PT;
 
-  load_tile(sQ, Qg, ldq, QT, nq, tid, 128);
+  load_tile(sQ, Qg, ldqi, QT, nq, tid, 128);
   load_tile(sK0, Kg, D, KTP, static_cast<int>(min64(KTP, n_keys)), tid, 128);
   load_tile(sV0, Vg, D, KTP, static_cast<int>(min64(KTP, n_keys)), tid, 128);
   cp_commit();

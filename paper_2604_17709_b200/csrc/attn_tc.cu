@@ -562,7 +562,8 @@ dl_status launch_attention_prefill_tc(const AttnArgs& a, cudaStream_t st) {
   while (C > 1 && (G % C != 0 || C > 8)) C >>= 1;
   FaMaps maps;
   const int64_t kv_rows = static_cast<int64_t>(a.num_seqs) * a.Hk * a.max_seq;
-  if (!encode_map_bf16(&maps.q, a.q, a.T, static_cast<int64_t>(a.Hq) * D, static_cast<int64_t>(a.Hq) * D, BQ) ||
+  const int64_t ldq = a.ld_q > 0 ? a.ld_q : static_cast<int64_t>(a.Hq) * D;
+  if (!encode_map_bf16(&maps.q, a.q, a.T, static_cast<int64_t>(a.Hq) * D, ldq, BQ) ||
       !encode_map_bf16(&maps.k, a.k_cache, kv_rows, D, D, BKV / C) ||
       !encode_map_bf16(&maps.v, a.v_cache, kv_rows, D, D, BKV / C)) {
     set_error("attention prefill (tcgen05): cuTensorMapEncodeTiled failed");

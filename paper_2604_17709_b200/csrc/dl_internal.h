@@ -153,6 +153,7 @@ struct RopeCacheArgs {
   int64_t T; int Hq, Hk, d; float theta;
   int rope;            // 0: no rotary embedding (q, k pass through)
   SideZero zero, zero2;   // side jobs (see SideZero)
+  int kv_only;         // prefill: q (and RoPE) handled elsewhere -- only append k and v to the caches
 };
 
 // Last-contributor finalize of a stream-K GEMM (FixupOp); buffers zeroed on entry,
@@ -406,6 +407,7 @@ dl_status launch_copy2d(const void* src, int64_t lds, void* dst, int64_t ldd,
 // ---------------------------------------------------------------------------
 struct AttnArgs {
   const __nv_bfloat16* q; __nv_bfloat16* out;
+  int64_t ld_q;                           // prefill: row stride of q (0: Hq * d)
   const __nv_bfloat16* k_cache; const __nv_bfloat16* v_cache; int64_t max_seq;
   const int32_t* cu_seqlens; const int32_t* cache_lens; int32_t num_seqs;
   int64_t T; int Hq, Hk, d; int decode;

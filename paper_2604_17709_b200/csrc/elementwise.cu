@@ -489,7 +489,7 @@ __global__ void __launch_bounds__(128) rope_cache_kernel(RopeCacheArgs a, EwTrac
   const int heads = a.Hq + 2 * a.Hk;
   const int p0 = (threadIdx.x % TPH) * kRopeVec;        // first rotation pair of this thread
   const int hg = blockIdx.x * (128 / TPH) + threadIdx.x / TPH;
-  const int h0 = hg * kRopeHeads;
+  const int h0 = (a.kv_only ? a.Hq : 0) + hg * kRopeHeads;   // kv_only: k and v heads only
   const int64_t t = blockIdx.y;
   const bool active = 2 * p0 < a.d && h0 < heads;
   float sn[kRopeVec], cs[kRopeVec];
@@ -965,6 +965,10 @@ dl_status launch_relu_bf16(const __nv_bfloat16* src, int64_t lds, __nv_bfloat16*
 }
 dl_status launch_rope_cache(const RopeCacheArgs& a, cudaStream_t st) {
   if (a.T <= 0) return DL_OK;
+  if (a.kv_only && (a.rope || a.T <= 256)) {
+    set_error("rope_cache: kv_only is the prefill append of already rotated keys (rope = 0)");
+    return DL_ERR_INVALID_ARG;
+  }
   if (a.T <= 256 && a.d % 4 == 0) {
     const int per_tok = (a.Hq + 2 * a.Hk) * (a.d / 4);
     dim3 grid((per_tok + 127) / 128, static_cast<unsigned>(a.T));
@@ -974,7 +978,7 @@ dl_status launch_rope_cache(const RopeCacheArgs& a, cudaStream_t st) {
     set_error("rope_cache: head_dim %d unsupported (128)", a.d);
     return DL_ERR_UNSUPPORTED;
   }
-  const int groups = (a.Hq + 2 * a.Hk + kRopeHeads - 1) / kRopeHeads;
+  const int groups = ((a.kv_only ? 0 : a.Hq) + 2 * a.Hk + kRopeHeads - 1) / kRopeHeads;
   const int per_cta = 128 / (64 / kRopeVec);
   dim3 grid((groups + per_cta - 1) / per_cta, static_cast<unsigned>(a.T));
   return launch_pdl(rope_cache_kernel, grid, dim3(128), 0, st, "rope_cache", a, ew_trace(3));

@@ -646,12 +646,14 @@ def test_lowrank_kv_decode_batch64(dl, orc):
     assert err <= TOL_BF16 and err_new <= TOL_BF16, (err, err_new)
 
 
-@pytest.mark.parametrize("knob", ["DL_FA_CLUSTER=2", "DL_FA_CLUSTER=8", "DL_ATTN_PREFILL_MMA=1", "DL_GLU_FUSE=0"])
+@pytest.mark.parametrize("knob", ["DL_FA_CLUSTER=2", "DL_FA_CLUSTER=8", "DL_ATTN_PREFILL_MMA=1", "DL_GLU_FUSE=0",
+                                  "DL_ROPE_EPI=0"])
 def test_prefill_attention_variants(knob):
     """The A/B variants of the prefill path against the oracle:
     K/V tiles multicast to 2- and 8-CTA clusters (GQA heads of one KV head), the
     previous mma.sync attention kernel, and the separate SiLU.up kernel instead of
-    the gate|up GLU epilogue -- every prefill parity test of this file, run
+    the gate|up GLU epilogue, the RoPE + cache-append kernel instead of RoPE in the
+    q|k|v stage-2 epilogue -- every prefill parity test of this file, run
     against the instrumented library in a subprocess."""
     import os
     import subprocess
