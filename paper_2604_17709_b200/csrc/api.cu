@@ -1326,7 +1326,7 @@ dl_status block_forward_impl(const dl_block_config* cfg, const dl_block_weights*
   // place from the q|k|v output and a copy-only kernel appends k, v to the
   // caches (DL_ROPE_EPI=0: the RoPE + cache-append kernel, A/B)
   static const bool rope_epi_env = !DL_ENV("DL_ROPE_EPI") || atoi(DL_ENV("DL_ROPE_EPI")) != 0;
-  const bool rope_epi = rope_epi_env && !skinny && !tp && !kv && d.d == 128 && NQKV % 8 == 0;
+  const bool rope_epi = rope_epi_env && phase == DL_PREFILL && !skinny && !tp && !kv && d.d == 128 && NQKV % 8 == 0;
   if (rope_epi && !cfg->no_rope) {
     qkv_out.rope_pos = positions;
     qkv_out.rope_end = (d.Hq_loc + d.Hk_loc) * d.d;
