@@ -1130,6 +1130,14 @@ dl_status launch_attention_sk(const AttnArgs& a, cudaStream_t st) {
   int grid = std::min((cfg23 ? 3 : 2) * num_sms(), sk::kMaxGrid);
   if (tiles < static_cast<int64_t>(grid) * 4) grid = std::max(num_sms(), static_cast<int>(tiles / 4));
   grid = std::min(grid, (cfg23 ? 3 : 2) * num_sms());
+  // Short items and no more items than CTAs (TP >= 2 at batch 64, context 512):
+  // one CTA per item, no split and no merge.  A split item's merging CTA waits for
+  // its partner's whole share, so 4-5 tiles + a merge cost about as much as the
+  // 9 tiles unsplit, and the merges go away (per-rank decode at TP = 4 / 8:
+  // 10.76 -> 10.29 / 8.59 -> 8.44 ms, r02bl).  Long items keep the stream-K split.
+  // A/B: DL_ATTN_NOSPLIT_TILES=n (items of <= n tiles; default 16, 0 = off)
+  static const int nosplit = DL_ENV("DL_ATTN_NOSPLIT_TILES") ? atoi(DL_ENV("DL_ATTN_NOSPLIT_TILES")) : 16;
+  if ((a.max_seq + KT - 1) / KT <= nosplit && items <= grid) grid = std::max<int64_t>(1, items);
   k.ctr = gemm_trace_cta_slots((grid + 147) / 148);
   return launch_pdl(kern, dim3(grid), dim3(sk::kThreads), smem, st, "attention decode (stream-K)", maps, k);
 }
