@@ -1118,6 +1118,8 @@ dl_status launch_attention_sk(const AttnArgs& a, cudaStream_t st) {
                          static_cast<int>(sk::smem_bytes<3>(sk::kMaxSeqs)));
     cudaFuncSetAttribute(attn_decode_sk_kernel<2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(sk::smem_bytes<2>(sk::kMaxSeqs)));
+    cudaFuncSetAttribute(attn_decode_sk_kernel<6, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sk::smem_bytes<6>(sk::kMaxSeqs)));
     attr = true;
   }
   // grid: every CTA keeps >= ~4 key tiles (fewer split items to merge when the
@@ -1138,7 +1140,14 @@ dl_status launch_attention_sk(const AttnArgs& a, cudaStream_t st) {
   // A/B: DL_ATTN_NOSPLIT_TILES=n (items of <= n tiles; default 16, 0 = off)
   static const int nosplit = DL_ENV("DL_ATTN_NOSPLIT_TILES") ? atoi(DL_ENV("DL_ATTN_NOSPLIT_TILES")) : 16;
   if ((a.max_seq + KT - 1) / KT <= nosplit && items <= grid) grid = std::max<int64_t>(1, items);
+  // at most one CTA per SM: a 6-stage ring per CTA (the whole SM's shared memory),
+  // so a lone item's tiles are in flight together (A/B: DL_ATTN_DEEP=0)
+  static const bool deep = !DL_ENV("DL_ATTN_DEEP") || atoi(DL_ENV("DL_ATTN_DEEP")) != 0;
+  const bool use_deep = deep && !cfg23 && grid <= num_sms();
   k.ctr = gemm_trace_cta_slots((grid + 147) / 148);
+  if (use_deep)
+    return launch_pdl(attn_decode_sk_kernel<6, 1>, dim3(grid), dim3(sk::kThreads), sk::smem_bytes<6>(a.num_seqs), st,
+                      "attention decode (stream-K)", maps, k);
   return launch_pdl(kern, dim3(grid), dim3(sk::kThreads), smem, st, "attention decode (stream-K)", maps, k);
 }
 
