@@ -1139,7 +1139,13 @@ dl_status launch_attention_sk(const AttnArgs& a, cudaStream_t st) {
   // 10.76 -> 10.29 / 8.59 -> 8.44 ms, r02bl).  Long items keep the stream-K split.
   // A/B: DL_ATTN_NOSPLIT_TILES=n (items of <= n tiles; default 16, 0 = off)
   static const int nosplit = DL_ENV("DL_ATTN_NOSPLIT_TILES") ? atoi(DL_ENV("DL_ATTN_NOSPLIT_TILES")) : 16;
-  if ((a.max_seq + KT - 1) / KT <= nosplit && items <= grid) grid = std::max<int64_t>(1, items);
+  // More items than CTA slots (TP = 1): whole items per CTA, ceil(items / slots) each,
+  // so equal-length items are never cut either (A/B: DL_ATTN_NOSPLIT_MULTI=0).
+  static const bool multi = !DL_ENV("DL_ATTN_NOSPLIT_MULTI") || atoi(DL_ENV("DL_ATTN_NOSPLIT_MULTI")) != 0;
+  if ((a.max_seq + KT - 1) / KT <= nosplit && items > 0 && (items <= grid || multi)) {
+    const int64_t per = (items + grid - 1) / grid;
+    grid = static_cast<int>((items + per - 1) / per);
+  }
   // at most one CTA per SM: a 6-stage ring per CTA (the whole SM's shared memory),
   // so a lone item's tiles are in flight together (A/B: DL_ATTN_DEEP=0)
   static const bool deep = !DL_ENV("DL_ATTN_DEEP") || atoi(DL_ENV("DL_ATTN_DEEP")) != 0;
