@@ -1,0 +1,8 @@
+mkdir -p gpurun_out
+python -m paper_2604_17709_b200.build > gpurun_out/r02bu_build.log 2>&1
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -x -q -k "prefill" > gpurun_out/r02bu_t.log 2>&1; echo rc=$? >> gpurun_out/r02bu_t.log
+export DL_LIBRARY=ab
+for i in 1 2; do for E in "DL_X=0" "DL_TAIL_KERNEL=1"; do
+  echo "[$E] $(env $E timeout 300 python tools/prefill_timeline.py 2>&1 | head -1)"
+done; done > gpurun_out/r02bu_ab.log 2>&1
+timeout 300 python tools/prefill_timeline.py > gpurun_out/r02bu_tl.log 2>&1
