@@ -528,6 +528,7 @@ struct SkArgs {
   SideZero zero, zero2;
   unsigned long long* ctr;        // per-CTA debug timeline (dl_debug_gemm_trace), 8 u64 per CTA
   int reorder;                    // shared last item first (DL_ATTN_ORDER=1; default plain range order)
+  int item_per;                   // > 0: CTA c takes whole items [c * item_per, (c + 1) * item_per) (never split)
 };
 
 // RoPE of the interleaved pair (dim, dim + 1) at position pos (fp32 angle
@@ -636,7 +637,15 @@ __global__ void __launch_bounds__(sk::kThreads, PERSM)
   if (ctr && tid == 0) ctr[1] = ew_now();
   const int G = gridDim.x, c = blockIdx.x;
   const int64_t N = P[a.num_seqs];
-  const int64_t b0 = sk_bound(c, N, G), b1 = sk_bound(c + 1, N, G);
+  // whole-item ranges (item_per > 0): the tile index of item i
+  auto item_tile = [&](int64_t i) -> int64_t {
+    const int64_t items = static_cast<int64_t>(a.num_seqs) * per_seq;
+    if (i >= items) return N;
+    const int s = static_cast<int>(i / per_seq), jj = static_cast<int>(i - static_cast<int64_t>(s) * per_seq);
+    return P[s] + static_cast<int64_t>(jj) * ((P[s + 1] - P[s]) / per_seq);
+  };
+  const int64_t b0 = a.item_per > 0 ? item_tile(static_cast<int64_t>(c) * a.item_per) : sk_bound(c, N, G);
+  const int64_t b1 = a.item_per > 0 ? item_tile(static_cast<int64_t>(c + 1) * a.item_per) : sk_bound(c + 1, N, G);
   const int64_t ldq = static_cast<int64_t>(a.Hq) * D;
   // Processing order: the range's last item (usually shared with the next
   // CTA) first, then [b0, split).  The next CTA processes that shared item
@@ -1145,6 +1154,10 @@ dl_status launch_attention_sk(const AttnArgs& a, cudaStream_t st) {
   if ((a.max_seq + KT - 1) / KT <= nosplit && items > 0 && (items <= grid || multi)) {
     const int64_t per = (items + grid - 1) / grid;
     grid = static_cast<int>((items + per - 1) / per);
+    // whole-item ranges: nothing is split, even for ragged contexts (A/B: DL_ATTN_ITEM_RANGES=0 keeps
+    // the equal tile ranges, which cut items whose lengths differ)
+    static const bool item_ranges = !DL_ENV("DL_ATTN_ITEM_RANGES") || atoi(DL_ENV("DL_ATTN_ITEM_RANGES")) != 0;
+    k.item_per = item_ranges ? static_cast<int>(per) : 0;
   }
   // at most one CTA per SM: a 6-stage ring per CTA (the whole SM's shared memory),
   // so a lone item's tiles are in flight together (A/B: DL_ATTN_DEEP=0)
