@@ -92,6 +92,7 @@ struct KArgs {
   long long xld;
   int xm, xcols;
   int wpol;                  // pair kernel weight L2 policy: 0 evict_first, 1 evict_normal, 2 evict_last
+  int tail_vec;              // tail finalize: 8-byte stores, Y += old values loaded up front (DL_TAIL_VEC=0: scalar)
   // pair kernel GLU mode (GemmProblem::glu): seg 0 = gate, seg 1 = up; the
   // whole-tile schedule runs over tile PAIRS (total_tiles / dp_tiles count
   // pairs), each emitted as the gate job (accumulator 0) then the up job of the
@@ -1450,6 +1451,20 @@ __global__ void __launch_bounds__(256) tc_tail_finalize_kernel(KArgs a) {
     const int r = rb * 32 + lane_r + 4 * i;
     v[i] = __ldcg(reinterpret_cast<const float4*>(a.tail_acc + (static_cast<long long>(tt) * 256 + r) * 256 + c4));
   }
+  // 4 features per thread go out as one 8-byte store when they are whole and
+  // aligned; for Y += the old values of all 8 rows are loaded up front (one
+  // round trip instead of 8 dependent ones)
+  const bool vec = a.tail_vec && f + 4 <= s.write_end;
+  uint2 old[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    old[i] = make_uint2(0u, 0u);
+    const int tok = tok0 + lane_r + 4 * i;
+    if (a.accumulate && vec && tok < a.T) {
+      const __nv_bfloat16* o = static_cast<const __nv_bfloat16*>(a.out) + out_index(a, s, tok, f);
+      if ((reinterpret_cast<uintptr_t>(o) & 7) == 0) old[i] = *reinterpret_cast<const uint2*>(o);
+    }
+  }
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int r = rb * 32 + lane_r + 4 * i;
@@ -1470,6 +1485,21 @@ __global__ void __launch_bounds__(256) tc_tail_finalize_kernel(KArgs a) {
         vv[e] = x * cs - y * sn;
         vv[e + 1] = x * sn + y * cs;
       }
+    }
+    __nv_bfloat16* o4 = static_cast<__nv_bfloat16*>(a.out) + out_index(a, s, tok, f);
+    if (vec && (reinterpret_cast<uintptr_t>(o4) & 7) == 0) {
+      if (a.accumulate) {
+        const float2 o01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&old[i].x));
+        const float2 o23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&old[i].y));
+        vv[0] += o01.x;
+        vv[1] += o01.y;
+        vv[2] += o23.x;
+        vv[3] += o23.y;
+      }
+      __nv_bfloat162 p01 = __floats2bfloat162_rn(vv[0], vv[1]), p23 = __floats2bfloat162_rn(vv[2], vv[3]);
+      *reinterpret_cast<uint2*>(o4) =
+          make_uint2(*reinterpret_cast<uint32_t*>(&p01), *reinterpret_cast<uint32_t*>(&p23));
+      continue;
     }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -1705,6 +1735,8 @@ dl_status prep_args(const GemmProblem& p, bool stream_k, KMaps& maps, KArgs& a, 
   a.trace_slot = g_trace_host_on ? g_trace_next++ : -1;
   static const int wpol = DL_ENV("DL_PAIR_WPOL") ? atoi(DL_ENV("DL_PAIR_WPOL")) : 2;   // A/B: 0 / 1 / 2 (measured best: 2)
   a.wpol = wpol;
+  static const bool tail_vec = !DL_ENV("DL_TAIL_VEC") || atoi(DL_ENV("DL_TAIL_VEC")) != 0;
+  a.tail_vec = tail_vec ? 1 : 0;
   // GLU launches: weights evict_first (measured 752 vs 764 us per 70B gate|up stage 2 with evict_last, r02bg)
   static const int glu_wpol = DL_ENV("DL_GLU_WPOL") ? atoi(DL_ENV("DL_GLU_WPOL")) : 0;
   if (a.glu && glu_wpol >= 0) a.wpol = glu_wpol;
