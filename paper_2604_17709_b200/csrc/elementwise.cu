@@ -963,12 +963,72 @@ dl_status launch_relu_bf16(const __nv_bfloat16* src, int64_t lds, __nv_bfloat16*
     return launch_silu_flat(const_cast<__nv_bfloat16*>(src), lds, act, ldo, T, m, 1, st, z, clear);
   return launch_ew4(T, m, ReluBf16{const_cast<__nv_bfloat16*>(src), lds, act, ldo, clear}, st, "relu_bf16", z);
 }
+// Prefill append of already rotated keys and the values (RopeCacheArgs::kv_only):
+// 8 tokens per CTA, one 16-byte chunk per thread (k and v rows of the q|k|v output
+// -> head-major cache rows); the cache slot is found once per token (lanes of
+// warp 0) before griddepcontrol.wait -- positions, cu_seqlens and cache_lens are
+// not written inside the step.
+constexpr int kKvTok = 8;
+__global__ void __launch_bounds__(256) kv_cache_append_kernel(RopeCacheArgs a, EwTrace tr) {
+  ew_mark(tr, 1);
+  pdl_trigger();
+  __shared__ int64_t slot_s[kKvTok];
+  const int chunks = 2 * a.Hk * (a.d / 8);                 // 16-byte chunks per token
+  if (threadIdx.x < kKvTok) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * kKvTok + threadIdx.x;
+    int64_t slot = -1;
+    if (t < a.T) {
+      int lo = 0, hi = a.num_seqs - 1;   // last s with cu[s] <= t
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (a.cu_seqlens[mid] <= t) lo = mid; else hi = mid - 1;
+      }
+      const int64_t cpos = a.cache_lens[lo] + (t - a.cu_seqlens[lo]);
+      if (cpos >= 0 && cpos < a.max_seq) slot = static_cast<int64_t>(lo) * a.Hk * a.max_seq + cpos;   // past capacity: dropped
+    }
+    slot_s[threadIdx.x] = slot;
+  }
+  __syncthreads();
+  pdl_wait();
+  ew_mark(tr, 2);
+  side_zero(a.zero);
+  side_zero(a.zero2);
+  constexpr int PER = 8;   // chunks per thread, all loads before the stores
+  for (int base = threadIdx.x; base < kKvTok * chunks; base += PER * blockDim.x) {
+    uint4 v[PER];
+    __nv_bfloat16* dst[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      dst[q] = nullptr;
+      const int i = base + q * blockDim.x;
+      if (i >= kKvTok * chunks) continue;
+      const int tk = i / chunks, c = i - tk * chunks;
+      const int64_t t = static_cast<int64_t>(blockIdx.x) * kKvTok + tk;
+      const int64_t slot = slot_s[tk];
+      if (t >= a.T || slot < 0) continue;
+      const int hd = c / (a.d / 8), ck = c - hd * (a.d / 8);   // hd < Hk: key head, else value head
+      const bool is_k = hd < a.Hk;
+      const int kvh = is_k ? hd : hd - a.Hk;
+      v[q] = *reinterpret_cast<const uint4*>(a.src + t * a.ld_src + static_cast<int64_t>(a.Hq + hd) * a.d + ck * 8);
+      dst[q] = (is_k ? a.k_cache : a.v_cache) + (slot + static_cast<int64_t>(kvh) * a.max_seq) * a.d + ck * 8;
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q)
+      if (dst[q]) *reinterpret_cast<uint4*>(dst[q]) = v[q];
+  }
+  ew_mark(tr, 3);
+}
+
 dl_status launch_rope_cache(const RopeCacheArgs& a, cudaStream_t st) {
   if (a.T <= 0) return DL_OK;
   if (a.kv_only && (a.rope || a.T <= 256)) {
     set_error("rope_cache: kv_only is the prefill append of already rotated keys (rope = 0)");
     return DL_ERR_INVALID_ARG;
   }
+  static const bool kv_copy = !DL_ENV("DL_KV_APPEND") || atoi(DL_ENV("DL_KV_APPEND")) != 0;   // A/B
+  if (a.kv_only && kv_copy && a.src && !a.acc && a.d % 8 == 0 && a.ld_src % 8 == 0 && !a.decode)
+    return launch_pdl(kv_cache_append_kernel, dim3(static_cast<unsigned>((a.T + kKvTok - 1) / kKvTok)), dim3(256), 0, st,
+                      "kv_cache_append", a, ew_trace(3));
   if (a.T <= 256 && a.d % 4 == 0) {
     const int per_tok = (a.Hq + 2 * a.Hk) * (a.d / 4);
     dim3 grid((per_tok + 127) / 128, static_cast<unsigned>(a.T));
