@@ -1857,7 +1857,8 @@ dl_status launch_cfg(const GemmProblem& p, bool stream_k, cudaStream_t st) {
     // DP + stream-K tail: a last wave filled to <= 75% is split along K
     static const bool dpsk = !DL_ENV("DL_PREFILL_DPSK") || atoi(DL_ENV("DL_PREFILL_DPSK")) != 0;
     const int full = tiles / clusters, tail = tiles % clusters;
-    if (dpsk && p.tail_acc && full >= 1 && tail > 0 && tail * 4 <= clusters * 3) {
+    static const double dpsk_frac = DL_ENV("DL_DPSK_FRAC") ? atof(DL_ENV("DL_DPSK_FRAC")) : 0.75;   // A/B
+    if (dpsk && p.tail_acc && full >= 1 && tail > 0 && tail <= dpsk_frac * clusters) {
       const int split = clusters / tail;
       if (split >= 2 && static_cast<size_t>(tail) * (a.glu ? 2 : 1) * 256 * 256 * 4 <= p.tail_bytes) {
         a.dp_tiles = tiles - tail;
