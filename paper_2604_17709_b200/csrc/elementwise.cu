@@ -49,6 +49,11 @@ __device__ __forceinline__ void side_zero(const SideZero& z) {
   }
 }
 
+// residual + RMSNorm: norm weight loaded before griddepcontrol.wait, side clears after
+// the row loads (A/B: DL_RN_EARLY=0 restores the old order); set once by the host
+__constant__ int g_rn_early = 1;
+__device__ __forceinline__ bool rn_early() { return g_rn_early != 0; }
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -136,10 +141,6 @@ __global__ void __launch_bounds__(kRnThreads) residual_rmsnorm_kernel(Acc* __res
                                                                       SideZero z, SideZero z2, EwTrace tr) {
   ew_mark(tr, 1);
   pdl_trigger();   // successor may launch now; it waits for us before reading
-  pdl_wait();
-  ew_mark(tr, 2);
-  side_zero(z);
-  side_zero(z2);
   __shared__ float red[32];
   const int64_t t = blockIdx.x;
   Acc* ar = acc + t * lda;
@@ -148,6 +149,20 @@ __global__ void __launch_bounds__(kRnThreads) residual_rmsnorm_kernel(Acc* __res
   const int n8 = h / 8;
   float av[kRnChunks][8];
   uint4 v[kRnChunks], gv[kRnChunks];
+  const bool early = rn_early();
+  if (early) {
+#pragma unroll
+    for (int k = 0; k < kRnChunks; ++k) {   // the norm weight is not written inside the step
+      const int i = threadIdx.x + k * kRnThreads;
+      if (i < n8) gv[k] = gr[i];
+    }
+  }
+  pdl_wait();
+  ew_mark(tr, 2);
+  if (!early) {
+    side_zero(z);
+    side_zero(z2);
+  }
 #pragma unroll
   for (int k = 0; k < kRnChunks; ++k) {
     const int i = threadIdx.x + k * kRnThreads;
@@ -159,8 +174,12 @@ __global__ void __launch_bounds__(kRnThreads) residual_rmsnorm_kernel(Acc* __res
         for (int e = 0; e < 8; ++e) av[k][e] = 0.f;
       }
       v[k] = xr[i];
-      gv[k] = gr[i];
+      if (!early) gv[k] = gr[i];
     }
+  }
+  if (early) {   // side clears after this row's loads are in flight (they never alias them)
+    side_zero(z);
+    side_zero(z2);
   }
   float ss = 0.f;
 #pragma unroll
@@ -890,9 +909,21 @@ dl_status launch_latent_unpermute(const __nv_bfloat16* recv, __nv_bfloat16* zb, 
   return launch_pdl(latent_unpermute_kernel, grid, dim3(256), 0, st, "latent_unpermute", recv, zb, ldzb, mp, z);
 }
 
+void rn_early_init() {
+  static const bool done = [] {
+    if (DL_ENV("DL_RN_EARLY") && atoi(DL_ENV("DL_RN_EARLY")) == 0) {
+      const int zero = 0;
+      cudaMemcpyToSymbol(g_rn_early, &zero, sizeof(int));
+    }
+    return true;
+  }();
+  (void)done;
+}
+
 dl_status launch_rmsnorm(const __nv_bfloat16* x, const __nv_bfloat16* g, __nv_bfloat16* y, int64_t T, int64_t h,
                          float eps, cudaStream_t st) {
   if (T <= 0) return DL_OK;
+  rn_early_init();
   if (T >= 512 && h % 8 == 0 && h / 8 <= kRrThreads * kRrChunks)   // many rows: 4 rows per CTA
     return launch_pdl(rmsnorm_rows_kernel, dim3(static_cast<unsigned>((T + kRrRows - 1) / kRrRows)),
                       dim3(kRrRows * kRrThreads), 0, st, "rmsnorm", x, g, y, T, static_cast<int>(h), eps, ew_trace(2));
@@ -907,6 +938,7 @@ dl_status launch_residual_rmsnorm(float* acc, int64_t lda, __nv_bfloat16* x, con
                                   __nv_bfloat16* y, int64_t T, int64_t h, float eps, cudaStream_t st,
                                   const SideZero& z, const SideZero& z2) {
   if (T <= 0) return DL_OK;
+  rn_early_init();
   if (h % 8 || h / 8 > kRnThreads * kRnChunks) {
     set_error("residual_rmsnorm: h=%lld unsupported (multiple of 8, <= %d)", (long long)h, 8 * kRnThreads * kRnChunks);
     return DL_ERR_UNSUPPORTED;
@@ -918,6 +950,7 @@ dl_status launch_residual_rmsnorm_bf16(__nv_bfloat16* acc, int64_t lda, __nv_bfl
                                        __nv_bfloat16* y, int64_t T, int64_t h, float eps, cudaStream_t st,
                                        const SideZero& z, const SideZero& z2) {
   if (T <= 0) return DL_OK;
+  rn_early_init();
   if (h % 8 || h / 8 > kRnThreads * kRnChunks) {
     set_error("residual_rmsnorm: h=%lld unsupported (multiple of 8, <= %d)", (long long)h, 8 * kRnThreads * kRnChunks);
     return DL_ERR_UNSUPPORTED;
