@@ -35,6 +35,8 @@ EwTrace ew_trace(int kind) {
   return t;
 }
 
+void rn_early_init();   // A/B flag of the small kernels' load / side-clear order (below)
+
 namespace {
 
 // SideZero job: 16-byte zero stores spread over every thread of the grid.
@@ -346,7 +348,8 @@ __global__ void __launch_bounds__(256) silu_mul_kernel(Acc* __restrict__ acc, in
   pdl_trigger();   // successor may launch now; it waits for us before reading
   pdl_wait();
   ew_mark(tr, 2);
-  side_zero(z);
+  const bool early = rn_early();   // side clears after the loads are in flight (DL_RN_EARLY)
+  if (!early) side_zero(z);
   const int per_row = m / 8;
   const int64_t t = blockIdx.y;
   Acc* row = acc + t * lda;
@@ -362,6 +365,7 @@ __global__ void __launch_bounds__(256) silu_mul_kernel(Acc* __restrict__ acc, in
       if (!relu) ld8(row + i * 8, gv[u]);
     }
   }
+  if (early) side_zero(z);
 #pragma unroll
   for (int u = 0; u < kSiluU; ++u) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x + u * stride;
@@ -388,6 +392,7 @@ __global__ void __launch_bounds__(256) silu_mul_kernel(Acc* __restrict__ acc, in
 template <typename Acc>
 dl_status launch_silu_flat(Acc* acc, int64_t lda, __nv_bfloat16* act, int64_t ldo, int64_t T, int64_t m, int relu,
                            cudaStream_t st, const SideZero& z, int clear = 1) {
+  rn_early_init();
   const int per_row = static_cast<int>(m / 8);
   const int gx = (per_row + 256 * kSiluU - 1) / (256 * kSiluU);
   return launch_pdl(silu_mul_kernel<Acc>, dim3(gx > 0 ? gx : 1, static_cast<unsigned>(T)), dim3(256), 0, st,
@@ -649,15 +654,24 @@ __global__ void __launch_bounds__(128) rope_cache_tok_kernel(RopeCacheArgs a, Ew
   }
   pdl_wait();
   ew_mark(tr, 2);
-  side_zero(a.zero);
-  side_zero(a.zero2);
-  if (!active) return;
-  float4 v;
-  if (a.acc) {
-    v = take4(const_cast<float*>(a.acc) + t * a.ld_src + col, a.clear);
-  } else {
-    v = load4(a.src + t * a.ld_src + col);
+  const bool early = rn_early();   // side clears after the load is in flight (DL_RN_EARLY)
+  if (!early) {
+    side_zero(a.zero);
+    side_zero(a.zero2);
   }
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (active) {
+    if (a.acc) {
+      v = take4(const_cast<float*>(a.acc) + t * a.ld_src + col, a.clear);
+    } else {
+      v = load4(a.src + t * a.ld_src + col);
+    }
+  }
+  if (early) {
+    side_zero(a.zero);
+    side_zero(a.zero2);
+  }
+  if (!active) return;
   if (rot) v = make_float4(v.x * cs0 - v.y * sn0, v.x * sn0 + v.y * cs0, v.z * cs1 - v.w * sn1, v.z * sn1 + v.w * cs1);
   if (hd < a.Hq) store4(a.q_out + t * static_cast<int64_t>(a.Hq) * a.d + col, v.x, v.y, v.z, v.w);
   else if (dst) store4(dst, v.x, v.y, v.z, v.w);
@@ -1054,6 +1068,7 @@ __global__ void __launch_bounds__(256) kv_cache_append_kernel(RopeCacheArgs a, E
 
 dl_status launch_rope_cache(const RopeCacheArgs& a, cudaStream_t st) {
   if (a.T <= 0) return DL_OK;
+  rn_early_init();
   if (a.kv_only && (a.rope || a.T <= 256)) {
     set_error("rope_cache: kv_only is the prefill append of already rotated keys (rope = 0)");
     return DL_ERR_INVALID_ARG;
